@@ -1,0 +1,127 @@
+/*
+ * he_b200.h -- C ABI of the B200-native MLWE PCMM / Rhombus PCMv path.
+ *
+ * Plain pointers and sizes only (no torch types).  Every pointer argument named *_dev
+ * is DEVICE memory owned by the caller; `stream` is a cudaStream_t passed as void*.
+ * All calls are asynchronous on `stream` unless stated otherwise, validate their
+ * arguments before launching anything, and return an he_status.  he_last_error()
+ * returns a thread-local message for the last non-OK status.
+ *
+ * The reference package (hesim) has no FFI: its "operator API" is the Python export
+ * list (pkg/src/hesim/__init__.py:8-9,26-27).  Each entry point below cites the
+ * reference interface it replaces; the Python mirror lives in
+ * paper_2601_18511_b200/pcmm.py and paper_2601_18511_b200/rhombus.py, and
+ * INTEGRATION.md shows the ctypes binding a hesim maintainer would add.
+ *
+ * Status codes map to the reference's exceptions (matmul.py:139-149, slotsim.py:27-28):
+ *   HE_EINVAL -> ValueError, HE_ETYPE -> TypeError,
+ *   HE_ENEEDS_BOOTSTRAP -> NeedsBootstrapError, HE_ECUDA / HE_ENOMEM -> RuntimeError.
+ *
+ * Data layouts (u32 words, one residue per word):
+ *   RLWE ciphertext batch at level L  : [n_ct][L+1 limbs][2 = (a, b)][N]
+ *   plaintext / activations           : f64 [tokens = d/2][n_cols]  (App. A layout)
+ *   PCMM output (level 0, limb q0)    : b' composed  [n_out/k][N]   (RLWE order)
+ *                                       a' MLWE rows [n_out][k][d]  (row y = block y/k, component y%k)
+ *   weight digit planes               : i8 [d_w][n_out][n_in]        (block-shuffled, balanced digits)
+ */
+#ifndef HE_B200_H
+#define HE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HE_OK = 0,
+  HE_EINVAL = 1,           /* ValueError          */
+  HE_ETYPE = 2,            /* TypeError           */
+  HE_ENEEDS_BOOTSTRAP = 3, /* NeedsBootstrapError */
+  HE_ECUDA = 4,            /* RuntimeError        */
+  HE_ENOMEM = 5            /* RuntimeError        */
+} he_status;
+
+/* Scheme parameters; mirrors hesim.SimParams' role (slotsim.py:86-129). */
+typedef struct {
+  uint32_t mlwe_degree;    /* d  (256)                                  */
+  uint32_t mlwe_rank;      /* k  (256);  N = d * k                      */
+  uint32_t moduli[2];      /* q0 (base), q1 (PCMM scale prime = Delta_w) */
+  uint32_t log_delta;      /* input scale Delta = 2^log_delta           */
+  uint32_t rhombus_degree; /* RLWE degree of the PCMv path (4096)       */
+} he_params;
+
+typedef struct he_context he_context;     /* NTT tables, device constants       */
+typedef struct he_pcmm_plan he_pcmm_plan; /* weight side of the MLWE PCMM       */
+
+/* Operation counters, same field names as hesim.CostLedger (slotsim.py:31-83). */
+typedef struct {
+  int64_t ct_rotations, cc_mults, pc_mults, pt_rotations, pt_mults, rescales, bootstraps;
+} he_ledger;
+
+const char* he_last_error(void);
+int he_version(void);
+
+/* ---------------------------------------------------------------- context */
+/* replaces hesim.SlotContext(SimParams) construction (slotsim.py:171-176) */
+he_status he_context_create(const he_params* params, he_context** out);
+he_status he_context_destroy(he_context* ctx);
+
+/* ---------------------------------------------------------------- keys, encryption (test/bench plumbing) */
+/* ternary secret s (int32 [N]) and its NTT per limb (u32 [2][N]) */
+he_status he_keygen(const he_context* ctx, uint64_t seed, int32_t* s_dev, uint32_t* s_ntt_dev, void* stream);
+/* replaces hesim.encrypt_matrix / pack_sheared (packing.py:81-91): coefficient-encode
+ * acts (f64 [d/2][n_in], App. A layout) and encrypt at level 1 -> ct [n_in/k][2][2][N].
+ * Block r uses RNG streams of global block index r0 + r. */
+he_status he_encrypt_acts(const he_context* ctx, const uint32_t* s_ntt_dev, const double* acts_dev, uint32_t n_in,
+                          uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream);
+/* centred phase of limb `limb` of an RLWE batch: int64 [n_ct][N] */
+he_status he_decrypt_rlwe(const he_context* ctx, const uint32_t* s_ntt_dev, const uint32_t* ct_dev, uint32_t n_ct,
+                          uint32_t limbs, uint32_t limb, int64_t* phase_dev, void* stream);
+/* centred phases of MLWE PCMM output rows [row0, row0+n_rows): int64 [n_rows][d] (level 0, q0) */
+he_status he_decrypt_mlwe(const he_context* ctx, const int32_t* s_dev, const uint32_t* out_b_dev,
+                          const uint32_t* out_a_dev, uint32_t n_out, uint32_t row0, uint32_t n_rows,
+                          int64_t* phase_dev, void* stream);
+
+/* ---------------------------------------------------------------- negacyclic NTT (K2) */
+/* in-place forward (natural -> bit-reversed) / inverse (bit-reversed -> natural, scaled)
+ * over `count` polys of degree n (n = N or rhombus_degree) spaced `stride` words apart,
+ * modulus moduli[limb]. */
+he_status he_ntt_forward(const he_context* ctx, uint32_t* data_dev, uint32_t n, uint32_t limb, uint32_t count,
+                         uint64_t stride, void* stream);
+he_status he_ntt_inverse(const he_context* ctx, uint32_t* data_dev, uint32_t n, uint32_t limb, uint32_t count,
+                         uint64_t stride, void* stream);
+
+/* ---------------------------------------------------------------- MLWE PCMM (K1 + K3) */
+/* replaces hesim.make_pcmm_plan (matmul.py:77-100).  Step 1: encode + block-shuffle
+ * the f64 weights W [n_out][n_in] (row-major, device) into integer W~ = round(q1 * W) in
+ * GEMM order and report max|W~| (synchronous). */
+he_status he_pcmm_weight_maxabs(const he_context* ctx, const double* w_dev, uint32_t n_out, uint32_t n_in,
+                                uint64_t* maxabs_out, void* stream);
+/* Step 2: write the d_w balanced digit planes i8 [d_w][n_out][n_in] (caller-allocated). */
+he_status he_pcmm_encode_weights(const he_context* ctx, const double* w_dev, uint32_t n_out, uint32_t n_in,
+                                 uint32_t d_w, int8_t* digits_dev, void* stream);
+/* Step 3: the immutable plan over caller-owned digit planes (kept alive by the caller). */
+he_status he_pcmm_plan_create(const he_context* ctx, const int8_t* digits_dev, uint32_t n_out, uint32_t n_in,
+                              uint32_t d_w, he_pcmm_plan** out);
+he_status he_pcmm_plan_destroy(he_pcmm_plan* plan);
+/* bytes of scratch he_pcmm_run needs (ciphertext digit planes) */
+he_status he_pcmm_workspace_bytes(const he_pcmm_plan* plan, uint64_t* bytes);
+/* replaces hesim.pcmm_depth1 / pcmm_bsgs (matmul.py:152-176): ct_in at level `level`
+ * (must be 1; 0 -> HE_ENEEDS_BOOTSTRAP) -> level-0 MLWE output.  Increments `ledger`
+ * (may be NULL) like one fused pc_linear per output block: pc_mults += (n_out/k)(n_in/k),
+ * rescales += n_out/k, ct_rotations += 0. */
+he_status he_pcmm_run(const he_pcmm_plan* plan, const uint32_t* ct_in_dev, uint32_t level, uint32_t* out_b_dev,
+                      uint32_t* out_a_dev, void* workspace_dev, uint64_t workspace_bytes, void* stream,
+                      he_ledger* ledger);
+/* the two stages of he_pcmm_run, exposed for profiling */
+he_status he_pcmm_decompose(const he_pcmm_plan* plan, const uint32_t* ct_in_dev, void* workspace_dev,
+                            uint64_t workspace_bytes, void* stream);
+he_status he_pcmm_gemm(const he_pcmm_plan* plan, const void* workspace_dev, uint32_t* out_b_dev,
+                       uint32_t* out_a_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HE_B200_H */

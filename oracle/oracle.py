@@ -1,0 +1,337 @@
+"""ctypes front end of the C oracle (he_oracle.c) plus a pure-Python restatement
+for the toy ring.  Test infrastructure only -- see package docstring."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import time
+from pathlib import Path
+
+import numpy as np
+
+__all__ = [
+    "lib", "build", "keygen", "encode_acts", "decode_acts", "encrypt", "decrypt_rlwe",
+    "encode_weights", "pcmm", "pcmm_limb", "decrypt_mlwe", "decode_mlwe_rows", "rescale",
+    "negacyclic_mul", "negacyclic_mul_schoolbook", "sigma_table", "clear_pcmm", "mlwe_column",
+    "py_mlwe_components", "py_pcmm_rows", "num_threads", "time_pcmm_sample", "rng",
+    "stream_a", "stream_e", "STREAM_SECRET",
+]
+
+_HERE = Path(__file__).resolve().parent
+_SO = _HERE / "_build" / "libhe_oracle.so"
+_lib = None
+
+STREAM_SECRET = 0x5EC0000000000000
+
+
+def stream_a(r: int, limb: int) -> int:
+    return 0xA000000000000000 | (r << 8) | limb
+
+
+def stream_e(r: int) -> int:
+    return 0xE000000000000000 | (r << 8)
+
+
+def build(force: bool = False) -> Path:
+    src = _HERE / "he_oracle.c"
+    if force or not _SO.exists() or _SO.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not _SO.exists():
+            build()
+        L = ctypes.CDLL(str(_SO))
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        f64p = ctypes.POINTER(ctypes.c_double)
+        u32, u64, i64 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int64
+        sig = {
+            "or_rng": (u64, [u64, u64, u64]),
+            "or_keygen": (None, [u64, u32, i32p]),
+            "or_encode_acts": (None, [f64p, u32, u32, u32, ctypes.c_double, i64p]),
+            "or_decode_acts": (None, [i64p, u32, u32, u32, ctypes.c_double, f64p]),
+            "or_encrypt": (ctypes.c_int, [u64, u32, u32, u32p, i32p, i64p, u32, u32, u32p]),
+            "or_decrypt_rlwe": (ctypes.c_int, [u32p, u32p, i32p, u32, u32, i64p]),
+            "or_encode_weights": (None, [f64p, u32, u32, u32, ctypes.c_double, i64p]),
+            "or_pcmm": (ctypes.c_int, [u32, u32, u32p, i64p, u32, u32, u32p, i32p, u32, i32p, u32, u32p]),
+            "or_pcmm_limb": (ctypes.c_int, [u32, u32, u32, u32, u32, i64p, u32, u32, u32p, i32p, u32, i32p, u32, u32p]),
+            "or_decrypt_mlwe": (None, [u32, u32, u32, i32p, u32p, u32, i64p]),
+            "or_rescale": (u32, [u32, u32, u32, u32]),
+            "or_negacyclic_mul": (ctypes.c_int, [u32p, i32p, u32, u32, u32p]),
+            "or_negacyclic_mul_schoolbook": (None, [u32p, i32p, u32, u32, u32p]),
+            "or_sigma": (u32, [u32, u32]),
+            "or_mlwe_column": (None, [u32p, u32, u32, u32, u32, u32, u32, u32, u32p]),
+            "or_num_threads": (ctypes.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def _u32(a):
+    return _p(a, ctypes.c_uint32)
+
+
+def _i32(a):
+    return _p(a, ctypes.c_int32)
+
+
+def _i64(a):
+    return _p(a, ctypes.c_int64)
+
+
+def _f64(a):
+    return _p(a, ctypes.c_double)
+
+
+def _moduli(params) -> np.ndarray:
+    return np.ascontiguousarray(np.array(params.moduli, dtype=np.uint32))
+
+
+def num_threads() -> int:
+    return int(lib().or_num_threads())
+
+
+def rng(seed: int, stream: int, idx: int) -> int:
+    return int(lib().or_rng(seed, stream, idx))
+
+
+def sigma_table(k: int) -> np.ndarray:
+    return np.array([lib().or_sigma(t, k) for t in range(k)], dtype=np.int64)
+
+
+def keygen(params, seed: int) -> np.ndarray:
+    s = np.zeros(params.N, dtype=np.int32)
+    lib().or_keygen(seed, params.N, _i32(s))
+    return s
+
+
+def encode_acts(params, A: np.ndarray) -> np.ndarray:
+    """A: tokens x n_in (tokens = d/2) -> integer plaintext polys [n_in/k, N]."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    tokens, n_in = A.shape
+    if tokens != params.tokens or n_in % params.mlwe_rank:
+        raise ValueError("activation block shape mismatch")
+    pt = np.zeros((n_in // params.mlwe_rank, params.N), dtype=np.int64)
+    lib().or_encode_acts(_f64(A), n_in, params.mlwe_degree, params.mlwe_rank, params.delta, _i64(pt))
+    return pt
+
+
+def decode_acts(params, phase: np.ndarray, n_cols: int) -> np.ndarray:
+    phase = np.ascontiguousarray(phase, dtype=np.int64)
+    A = np.zeros((params.tokens, n_cols), dtype=np.float64)
+    lib().or_decode_acts(_i64(phase), n_cols, params.mlwe_degree, params.mlwe_rank, params.delta, _f64(A))
+    return A
+
+
+def encrypt(params, seed: int, s: np.ndarray, pt: np.ndarray, r0: int = 0) -> np.ndarray:
+    """-> uint32 [n_ct, limbs=2, 2 (a, b), N]"""
+    pt = np.ascontiguousarray(pt, dtype=np.int64)
+    n_ct = pt.shape[0]
+    ct = np.zeros((n_ct, 2, 2, params.N), dtype=np.uint32)
+    rc = lib().or_encrypt(seed, params.N, 2, _u32(_moduli(params)), _i32(np.ascontiguousarray(s)),
+                          _i64(pt), n_ct, r0, _u32(ct))
+    if rc:
+        raise RuntimeError("oracle encrypt failed")
+    return ct
+
+
+def decrypt_rlwe(params, ct: np.ndarray, s: np.ndarray, limb: int = 0) -> np.ndarray:
+    ct = np.ascontiguousarray(ct)
+    out = np.zeros((ct.shape[0], params.N), dtype=np.int64)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    for r in range(ct.shape[0]):
+        a = np.ascontiguousarray(ct[r, limb, 0])
+        b = np.ascontiguousarray(ct[r, limb, 1])
+        row = np.zeros(params.N, dtype=np.int64)
+        lib().or_decrypt_rlwe(_u32(a), _u32(b), _i32(s), params.N, params.moduli[limb], _i64(row))
+        out[r] = row
+    return out
+
+
+def encode_weights(params, W: np.ndarray) -> np.ndarray:
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    n_out, n_in = W.shape
+    Wt = np.zeros((n_out, n_in), dtype=np.int64)
+    lib().or_encode_weights(_f64(W), n_out, n_in, params.mlwe_rank, float(params.delta_w), _i64(Wt))
+    return Wt
+
+
+def _sel(idx):
+    if idx is None:
+        return None, 0
+    a = np.ascontiguousarray(np.asarray(idx, dtype=np.int32))
+    return a, len(a)
+
+
+def pcmm(params, Wt: np.ndarray, ct: np.ndarray, rows=None, cols=None) -> np.ndarray:
+    """Rescaled level-0 output words (limb q0) for selected rows x GEMM columns."""
+    Wt = np.ascontiguousarray(Wt, dtype=np.int64)
+    ct = np.ascontiguousarray(ct, dtype=np.uint32)
+    n_out, n_in = Wt.shape
+    r, nr = _sel(rows)
+    c, nc = _sel(cols)
+    nr = nr if r is not None else n_out
+    nc = nc if c is not None else params.width
+    out = np.zeros((nr, nc), dtype=np.uint32)
+    lib().or_pcmm(params.mlwe_degree, params.mlwe_rank, _u32(_moduli(params)), _i64(Wt), n_out, n_in,
+                  _u32(ct), _i32(r) if r is not None else None, nr, _i32(c) if c is not None else None, nc,
+                  _u32(out))
+    return out
+
+
+def pcmm_limb(params, Wt, ct, limb: int, rows=None, cols=None) -> np.ndarray:
+    Wt = np.ascontiguousarray(Wt, dtype=np.int64)
+    ct = np.ascontiguousarray(ct, dtype=np.uint32)
+    n_out, n_in = Wt.shape
+    r, nr = _sel(rows)
+    c, nc = _sel(cols)
+    nr = nr if r is not None else n_out
+    nc = nc if c is not None else params.width
+    out = np.zeros((nr, nc), dtype=np.uint32)
+    lib().or_pcmm_limb(params.mlwe_degree, params.mlwe_rank, params.moduli[limb], ct.shape[1], limb,
+                       _i64(Wt), n_out, n_in, _u32(ct), _i32(r) if r is not None else None, nr,
+                       _i32(c) if c is not None else None, nc, _u32(out))
+    return out
+
+
+def mlwe_column(params, ct, limb: int, n: int) -> np.ndarray:
+    ct = np.ascontiguousarray(ct, dtype=np.uint32)
+    col = np.zeros(ct.shape[0] * params.mlwe_rank, dtype=np.uint32)
+    lib().or_mlwe_column(_u32(ct), ct.shape[0], ct.shape[1], limb, params.mlwe_degree, params.mlwe_rank,
+                         params.moduli[limb], n, _u32(col))
+    return col
+
+
+def decrypt_mlwe(params, s: np.ndarray, rows_out: np.ndarray) -> np.ndarray:
+    """rows_out: n_rows x width (b' first).  -> centred phases n_rows x d."""
+    rows_out = np.ascontiguousarray(rows_out, dtype=np.uint32)
+    ph = np.zeros((rows_out.shape[0], params.mlwe_degree), dtype=np.int64)
+    lib().or_decrypt_mlwe(params.mlwe_degree, params.mlwe_rank, params.moduli[0],
+                          _i32(np.ascontiguousarray(s, dtype=np.int32)), _u32(rows_out), rows_out.shape[0],
+                          _i64(ph))
+    return ph
+
+
+def decode_mlwe_rows(params, phase: np.ndarray, rows) -> dict:
+    """Map MLWE output rows y (component t' of block r') to (token, out_col) values:
+    phase_y[m] = Delta * Out[bitReverse(m)][k r' + sigma(t')] (App. A layout)."""
+    d, k = params.mlwe_degree, params.mlwe_rank
+    half = d // 2
+    sig = sigma_table(k)
+    lh = half.bit_length() - 1
+    br = np.array([int(format(m, f"0{lh}b")[::-1], 2) if lh else 0 for m in range(half)])
+    vals = {}
+    for i, y in enumerate(rows):
+        col = (y // k) * k + int(sig[y % k])
+        vals[col] = (br, phase[i, :half] / params.delta)
+    return vals
+
+
+def rescale(params, x0: int, x1: int) -> int:
+    return int(lib().or_rescale(x0, x1, params.moduli[0], params.moduli[1]))
+
+
+def negacyclic_mul(a: np.ndarray, s: np.ndarray, q: int) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    out = np.zeros(len(a), dtype=np.uint32)
+    if lib().or_negacyclic_mul(_u32(a), _i32(s), len(a), q, _u32(out)):
+        raise ValueError("q is not NTT-friendly for this N")
+    return out
+
+
+def negacyclic_mul_schoolbook(a, s, q) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    out = np.zeros(len(a), dtype=np.uint32)
+    lib().or_negacyclic_mul_schoolbook(_u32(a), _i32(s), len(a), q, _u32(out))
+    return out
+
+
+def clear_pcmm(W: np.ndarray, A: np.ndarray) -> np.ndarray:
+    """Float oracle in the activation orientation: A (tokens x n_in) -> A @ W^T
+    (tokens x n_out), i.e. (W @ M)^T with M = A^T -- hesim.clear_pcmm(W, M, 0)^T
+    (matmul.py:179-181 with shear power 0)."""
+    return np.asarray(A, float) @ np.asarray(W, float).T
+
+
+# ---------------------------------------------------------------- pure-Python restatement (toy)
+
+def py_mlwe_components(params, a: list[int], q: int):
+    """Explicit RLWE->MLWE a-part from SURVEY.md App. B.2, written in the branchy
+    form (j <= t: a_{t-j};  j > t: Y * a_{t-j+k}) -- independent of the C oracle's
+    unified negacyclic index.  Returns at[t][j] = list of d coefficients."""
+    d, k = params.mlwe_degree, params.mlwe_rank
+    comp = [[a[t + k * m] for m in range(d)] for t in range(k)]  # a_t(Y)
+    at = []
+    for t in range(k):
+        row = []
+        for j in range(k):
+            if j <= t:
+                row.append(list(comp[t - j]))
+            else:
+                p = comp[t - j + k]
+                row.append([(-p[d - 1]) % q] + p[: d - 1])  # Y * p in Z_q[Y]/(Y^d+1)
+        at.append(row)
+    return at
+
+
+def py_pcmm_rows(params, Wt, ct, rows):
+    """Pure-Python MLWE PCMM for a few rows (toy sizes): returns rows x width words."""
+    d, k, N = params.mlwe_degree, params.mlwe_rank, params.N
+    q0, q1 = params.moduli
+    n_ct = ct.shape[0]
+    per_limb = []
+    for limb, q in enumerate((q0, q1)):
+        cols = []  # MLWE ciphertexts x = (r, t): [b (d) | a (k*d)]
+        for r in range(n_ct):
+            a = [int(v) for v in ct[r, limb, 0]]
+            b = [int(v) for v in ct[r, limb, 1]]
+            at = py_mlwe_components(params, a, q)
+            for t in range(k):
+                vec = [b[t + k * m] for m in range(d)]
+                for j in range(k):
+                    vec.extend(at[t][j])
+                cols.append(vec)
+        res = []
+        for y in rows:
+            w = [int(v) for v in Wt[y]]
+            res.append([sum(w[x] * cols[x][n] for x in range(len(cols))) % q for n in range(params.width)])
+        per_limb.append(res)
+    inv = pow(q1, q0 - 2, q0)
+    out = []
+    for i in range(len(rows)):
+        row = []
+        for n in range(params.width):
+            x0, x1 = per_limb[0][i][n], per_limb[1][i][n]
+            x1c = x1 - q1 if x1 > q1 // 2 else x1
+            row.append((x0 - x1c) % q0 * inv % q0)
+        out.append(row)
+    return np.array(out, dtype=np.uint32)
+
+
+# ---------------------------------------------------------------- CPU baseline timing
+
+def time_pcmm_sample(params, Wt, ct, n_rows: int) -> dict:
+    """Time the oracle PCMM on the first n_rows output rows x all columns x full K,
+    both limbs + rescale (the sample the cpu_baseline is extrapolated from)."""
+    rows = list(range(n_rows))
+    t0 = time.perf_counter()
+    pcmm(params, Wt, ct, rows=rows)
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "rows": n_rows, "threads": num_threads()}

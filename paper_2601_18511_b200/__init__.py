@@ -1,0 +1,20 @@
+"""B200-native MLWE-format PCMM / Rhombus PCMv for CKKS-encrypted Llama inference.
+
+Host mirror of the reference's operator API (hesim/__init__.py:3-19 exports) for
+the encrypted-projection path; every computation runs in hand-written sm_100a CUDA
+behind the C ABI of include/he_b200.h.  There is no CPU fallback.
+"""
+
+from .errors import NeedsBootstrapError
+from .params import HeParams
+from .context import CostLedger, CtBlocks, HeContext, MlweBlocks, SecretKey, LEDGER_COUNTERS
+from .layout import bit_reverse, byte_mix, half_reverse, rotate_bits_down, shuffle_matrix, sigma_table
+from .pcmm import MlwePcmmPlan, clear_pcmm, make_mlwe_pcmm_plan, pcmm_mlwe
+
+__all__ = [
+    "NeedsBootstrapError", "HeParams", "CostLedger", "CtBlocks", "HeContext", "MlweBlocks", "SecretKey",
+    "LEDGER_COUNTERS", "bit_reverse", "byte_mix", "half_reverse", "rotate_bits_down", "shuffle_matrix",
+    "sigma_table", "MlwePcmmPlan", "clear_pcmm", "make_mlwe_pcmm_plan", "pcmm_mlwe",
+]
+
+__version__ = "0.1.0"

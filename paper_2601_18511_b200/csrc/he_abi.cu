@@ -1,0 +1,375 @@
+// he_abi.cu -- the extern "C" boundary (include/he_b200.h): argument validation, plan and
+// context objects, TMA descriptor construction, and the launch sequence of each op.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/he_b200.h"
+#include "he_common.cuh"
+#include "he_kernels.h"
+
+using namespace he;
+
+struct he_context {
+  he_params p;
+  RingDims R;
+  NttTable ntt[2];      // degree N, q0 / q1
+  NttTable ntt_rh[2];   // degree rhombus_degree, q0 / q1
+  int sm_count = 148;
+};
+
+struct he_pcmm_plan {
+  const he_context* ctx;
+  uint32_t n_out, n_in, d_w, d0, d1, width;
+  const int8_t* digits;
+  CUtensorMap tmA;
+  GemmEpiConst epi;
+};
+
+static thread_local std::string g_err;
+
+static he_status fail(he_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+static he_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(HE_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+#define HE_CUDA(call, what)                      \
+  do {                                           \
+    cudaError_t _e = (call);                     \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+extern "C" const char* he_last_error(void) { return g_err.c_str(); }
+extern "C" int he_version(void) { return 1; }
+
+// ---------------------------------------------------------------- TMA descriptors
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled_t)p;
+  }
+  return fn;
+}
+// 3-D int8 tensor {inner, rows, planes}, box {128, box_rows, 1}, 128-B swizzle, OOB -> 0
+static he_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t planes,
+                          uint32_t box_rows) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {inner, rows, planes};
+  cuuint64_t strides[2] = {inner, inner * rows};
+  cuuint32_t box[3] = {128, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return HE_OK;
+}
+
+// ---------------------------------------------------------------- context
+static int digits_for(uint32_t q) {
+  // balanced 8-bit digits for a centred residue |c| <= q/2
+  uint64_t bound = q / 2;
+  int n = 1;
+  while (127ull * (((1ull << (8 * n)) - 1) / 255) < bound) ++n;
+  return n;
+}
+
+extern "C" he_status he_context_create(const he_params* p, he_context** out) {
+  if (!p || !out) return fail(HE_EINVAL, "null argument");
+  const uint32_t d = p->mlwe_degree, k = p->mlwe_rank;
+  if (d < 32 || d > 256 || (d & (d - 1))) return fail(HE_EINVAL, "mlwe_degree must be a power of two in [32, 256]");
+  if (k < 16 || k > 256 || (k & (k - 1))) return fail(HE_EINVAL, "mlwe_rank must be a power of two in [16, 256]");
+  const uint32_t N = d * k;
+  for (int i = 0; i < 2; ++i) {
+    uint32_t q = p->moduli[i];
+    if (q < 3 || q >= (1u << 31) || (q - 1) % (2ull * N)) return fail(HE_EINVAL, "modulus %u not NTT-friendly", q);
+  }
+  if (p->moduli[1] / 2 >= p->moduli[0]) return fail(HE_EINVAL, "q1/2 must be below q0");
+  if (p->log_delta < 1 || p->log_delta > 40) return fail(HE_EINVAL, "log_delta out of range");
+  if (p->rhombus_degree < 16 || (p->rhombus_degree & (p->rhombus_degree - 1)) || N % p->rhombus_degree)
+    return fail(HE_EINVAL, "rhombus_degree must be a power of two dividing N");
+  he_context* c = new (std::nothrow) he_context();
+  if (!c) return fail(HE_ENOMEM, "out of host memory");
+  c->p = *p;
+  c->R.d = d;
+  c->R.k = k;
+  c->R.N = N;
+  c->R.logk = (uint32_t)ilog2_h(k);
+  c->R.q[0] = p->moduli[0];
+  c->R.q[1] = p->moduli[1];
+  c->R.log_delta = p->log_delta;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  for (int i = 0; i < 2; ++i) {
+    cudaError_t e = ntt_table_init(c->ntt[i], N, p->moduli[i]);
+    if (e == cudaSuccess) e = ntt_table_init(c->ntt_rh[i], p->rhombus_degree, p->moduli[i]);
+    if (e != cudaSuccess) {
+      he_context_destroy(c);
+      return cuda_fail(e, "NTT table init");
+    }
+  }
+  *out = c;
+  return HE_OK;
+}
+
+extern "C" he_status he_context_destroy(he_context* c) {
+  if (!c) return HE_OK;
+  for (int i = 0; i < 2; ++i) {
+    ntt_table_free(c->ntt[i]);
+    ntt_table_free(c->ntt_rh[i]);
+  }
+  delete c;
+  return HE_OK;
+}
+
+// ---------------------------------------------------------------- keys / encryption
+extern "C" he_status he_keygen(const he_context* c, uint64_t seed, int32_t* s_dev, uint32_t* s_ntt_dev, void* stream) {
+  if (!c || !s_dev || !s_ntt_dev) return fail(HE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  HE_CUDA(launch_keygen(c->R, seed, s_dev, st), "keygen");
+  for (uint32_t L = 0; L < 2; ++L) {
+    uint32_t* dst = s_ntt_dev + (size_t)L * c->R.N;
+    HE_CUDA(launch_reduce_secret(c->R, s_dev, L, dst, st), "reduce secret");
+    HE_CUDA(ntt_forward(c->ntt[L], dst, 1, c->R.N, st), "secret NTT");
+  }
+  return HE_OK;
+}
+
+extern "C" he_status he_encrypt_acts(const he_context* c, const uint32_t* s_ntt_dev, const double* acts_dev,
+                                     uint32_t n_in, uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream) {
+  if (!c || !s_ntt_dev || !acts_dev || !ct_dev) return fail(HE_EINVAL, "null argument");
+  if (n_in == 0 || n_in % c->R.k) return fail(HE_EINVAL, "n_in (%u) must be a positive multiple of k = %u", n_in, c->R.k);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N, n_ct = n_in / c->R.k;
+  HE_CUDA(launch_gen_a(c->R, seed, r0, n_ct, ct_dev, st), "sample a");
+  for (uint32_t L = 0; L < 2; ++L) {
+    uint32_t* bslots = ct_dev + (size_t)L * 2 * N + N;  // stride 4N between cts
+    HE_CUDA(ntt_forward(c->ntt[L], bslots, n_ct, 4ull * N, st), "NTT(a)");
+    HE_CUDA(launch_pointwise_mul(bslots, 4ull * N, s_ntt_dev + (size_t)L * N, N, n_ct, c->R.q[L], bslots, 4ull * N, st),
+            "a^ * s^");
+    HE_CUDA(ntt_inverse(c->ntt[L], bslots, n_ct, 4ull * N, st), "INTT(a s)");
+  }
+  HE_CUDA(launch_finish_encrypt(c->R, acts_dev, n_in, seed, r0, n_ct, ct_dev, st), "finish encrypt");
+  return HE_OK;
+}
+
+extern "C" he_status he_decrypt_rlwe(const he_context* c, const uint32_t* s_ntt_dev, const uint32_t* ct_dev,
+                                     uint32_t n_ct, uint32_t limbs, uint32_t limb, int64_t* phase_dev, void* stream) {
+  if (!c || !s_ntt_dev || !ct_dev || !phase_dev) return fail(HE_EINVAL, "null argument");
+  if (limb >= limbs || limbs > 2 || n_ct == 0) return fail(HE_EINVAL, "bad limb / limbs / n_ct");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N;
+  uint32_t* tmp = nullptr;
+  HE_CUDA(cudaMallocAsync(&tmp, (size_t)n_ct * N * sizeof(uint32_t), st), "alloc");
+  const uint64_t cstride = (uint64_t)limbs * 2 * N;
+  const uint32_t* a = ct_dev + (size_t)limb * 2 * N;
+  cudaError_t e = cudaMemcpy2DAsync(tmp, N * sizeof(uint32_t), a, cstride * sizeof(uint32_t), N * sizeof(uint32_t),
+                                    n_ct, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = ntt_forward(c->ntt[limb], tmp, n_ct, N, st);
+  if (e == cudaSuccess)
+    e = launch_pointwise_mul(tmp, N, s_ntt_dev + (size_t)limb * N, N, n_ct, c->R.q[limb], tmp, N, st);
+  if (e == cudaSuccess) e = ntt_inverse(c->ntt[limb], tmp, n_ct, N, st);
+  if (e == cudaSuccess) e = launch_phase(a + N, cstride, tmp, N, N, n_ct, c->R.q[limb], phase_dev, st);
+  cudaFreeAsync(tmp, st);
+  if (e != cudaSuccess) return cuda_fail(e, "decrypt");
+  return HE_OK;
+}
+
+extern "C" he_status he_decrypt_mlwe(const he_context* c, const int32_t* s_dev, const uint32_t* out_b_dev,
+                                     const uint32_t* out_a_dev, uint32_t n_out, uint32_t row0, uint32_t n_rows,
+                                     int64_t* phase_dev, void* stream) {
+  if (!c || !s_dev || !out_b_dev || !out_a_dev || !phase_dev) return fail(HE_EINVAL, "null argument");
+  if (row0 + n_rows > n_out || n_out % c->R.k) return fail(HE_EINVAL, "row range outside the output");
+  if (n_rows == 0) return HE_OK;
+  HE_CUDA(launch_decrypt_mlwe(c->R, s_dev, out_b_dev, out_a_dev, n_out, row0, n_rows, phase_dev, (cudaStream_t)stream),
+          "decrypt mlwe");
+  return HE_OK;
+}
+
+// ---------------------------------------------------------------- NTT
+static const NttTable* pick(const he_context* c, uint32_t n, uint32_t limb) {
+  if (limb > 1) return nullptr;
+  if (n == c->R.N) return &c->ntt[limb];
+  if (n == c->p.rhombus_degree) return &c->ntt_rh[limb];
+  return nullptr;
+}
+extern "C" he_status he_ntt_forward(const he_context* c, uint32_t* data, uint32_t n, uint32_t limb, uint32_t count,
+                                    uint64_t stride, void* stream) {
+  if (!c || !data) return fail(HE_EINVAL, "null argument");
+  const NttTable* t = pick(c, n, limb);
+  if (!t) return fail(HE_EINVAL, "no NTT table for degree %u limb %u", n, limb);
+  if (stride < n || stride % 4) return fail(HE_EINVAL, "stride must be >= n and a multiple of 4");
+  HE_CUDA(ntt_forward(*t, data, count, stride, (cudaStream_t)stream), "ntt forward");
+  return HE_OK;
+}
+extern "C" he_status he_ntt_inverse(const he_context* c, uint32_t* data, uint32_t n, uint32_t limb, uint32_t count,
+                                    uint64_t stride, void* stream) {
+  if (!c || !data) return fail(HE_EINVAL, "null argument");
+  const NttTable* t = pick(c, n, limb);
+  if (!t) return fail(HE_EINVAL, "no NTT table for degree %u limb %u", n, limb);
+  if (stride < n || stride % 4) return fail(HE_EINVAL, "stride must be >= n and a multiple of 4");
+  HE_CUDA(ntt_inverse(*t, data, count, stride, (cudaStream_t)stream), "ntt inverse");
+  return HE_OK;
+}
+
+// ---------------------------------------------------------------- PCMM
+static he_status check_shape(const he_context* c, uint32_t n_out, uint32_t n_in) {
+  if (n_out == 0 || n_in == 0) return fail(HE_EINVAL, "empty weight matrix");
+  if (n_out % c->R.k || n_in % c->R.k)
+    return fail(HE_EINVAL, "dim mismatch: n_out (%u) and n_in (%u) must be multiples of k = %u", n_out, n_in, c->R.k);
+  if (n_in > 32768) return fail(HE_EINVAL, "n_in (%u) above the int32 accumulator bound 32768", n_in);
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_weight_maxabs(const he_context* c, const double* w_dev, uint32_t n_out, uint32_t n_in,
+                                           uint64_t* maxabs_out, void* stream) {
+  if (!c || !w_dev || !maxabs_out) return fail(HE_EINVAL, "null argument");
+  he_status s = check_shape(c, n_out, n_in);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* dmax = nullptr;
+  HE_CUDA(cudaMallocAsync(&dmax, sizeof(unsigned long long), st), "alloc");
+  cudaError_t e = cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = launch_weight_maxabs(c->R, w_dev, n_out, n_in, dmax, st);
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, dmax, sizeof h, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dmax, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "weight max");
+  *maxabs_out = h;
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_encode_weights(const he_context* c, const double* w_dev, uint32_t n_out, uint32_t n_in,
+                                            uint32_t d_w, int8_t* digits_dev, void* stream) {
+  if (!c || !w_dev || !digits_dev) return fail(HE_EINVAL, "null argument");
+  he_status s = check_shape(c, n_out, n_in);
+  if (s) return s;
+  if (d_w < 1 || d_w > 4) return fail(HE_EINVAL, "d_w must be in [1, 4]");
+  HE_CUDA(launch_encode_weights(c->R, w_dev, n_out, n_in, d_w, digits_dev, (cudaStream_t)stream), "encode weights");
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_plan_create(const he_context* c, const int8_t* digits_dev, uint32_t n_out, uint32_t n_in,
+                                         uint32_t d_w, he_pcmm_plan** out) {
+  if (!c || !digits_dev || !out) return fail(HE_EINVAL, "null argument");
+  he_status s = check_shape(c, n_out, n_in);
+  if (s) return s;
+  if (d_w < 1 || d_w > 4) return fail(HE_EINVAL, "d_w must be in [1, 4]");
+  const int d0 = digits_for(c->R.q[0]), d1 = digits_for(c->R.q[1]);
+  if (gemm_smem_bytes((int)d_w, d0, d1) < 0)
+    return fail(HE_EINVAL, "no GEMM instance for digits (%u, %d, %d)", d_w, d0, d1);
+  he_pcmm_plan* p = new (std::nothrow) he_pcmm_plan();
+  if (!p) return fail(HE_ENOMEM, "out of host memory");
+  p->ctx = c;
+  p->n_out = n_out;
+  p->n_in = n_in;
+  p->d_w = d_w;
+  p->d0 = (uint32_t)d0;
+  p->d1 = (uint32_t)d1;
+  p->width = c->R.d * (1 + c->R.k);
+  p->digits = digits_dev;
+  s = make_map(&p->tmA, digits_dev, n_in, n_out, d_w, 128);
+  if (s) {
+    delete p;
+    return s;
+  }
+  GemmEpiConst& e = p->epi;
+  for (int L = 0; L < 2; ++L) {
+    const uint32_t q = c->R.q[L];
+    e.q[L] = q;
+    e.offs[L] = (uint32_t)((uint64_t)q * (((1ull << 31) + q - 1) / q));
+    for (int sft = 0; sft < 8; ++sft) {
+      uint32_t w = (uint32_t)powmod_h(2, 8ull * sft, q);
+      e.pw[L][sft] = w;
+      e.pwp[L][sft] = shoup_pre(w, q);
+    }
+  }
+  e.q1inv = (uint32_t)powmod_h(c->R.q[1] % c->R.q[0], c->R.q[0] - 2, c->R.q[0]);
+  e.q1invp = shoup_pre(e.q1inv, c->R.q[0]);
+  *out = p;
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_plan_destroy(he_pcmm_plan* p) {
+  delete p;
+  return HE_OK;
+}
+
+static uint64_t ws_bytes(const he_pcmm_plan* p) { return (uint64_t)(p->d0 + p->d1) * p->width * p->n_in; }
+
+extern "C" he_status he_pcmm_workspace_bytes(const he_pcmm_plan* p, uint64_t* bytes) {
+  if (!p || !bytes) return fail(HE_EINVAL, "null argument");
+  *bytes = ws_bytes(p);
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct_in, void* ws, uint64_t ws_size,
+                                       void* stream) {
+  if (!p || !ct_in || !ws) return fail(HE_EINVAL, "null argument");
+  if (ws_size < ws_bytes(p)) return fail(HE_EINVAL, "workspace too small (%llu < %llu)", (unsigned long long)ws_size,
+                                         (unsigned long long)ws_bytes(p));
+  HE_CUDA(launch_decompose(p->ctx->R, ct_in, p->n_in, (int)p->d0, (int)p->d1, (int8_t*)ws,
+                           (uint64_t)p->width * p->n_in, (cudaStream_t)stream),
+          "decompose");
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_t* out_b, uint32_t* out_a,
+                                  void* stream) {
+  if (!p || !ws || !out_b || !out_a) return fail(HE_EINVAL, "null argument");
+  CUtensorMap tmB;
+  he_status s = make_map(&tmB, ws, p->n_in, p->width, p->d0 + p->d1, 32);
+  if (s) return s;
+  GemmArgs a;
+  a.n_out = (int)p->n_out;
+  a.n_in = (int)p->n_in;
+  a.width = (int)p->width;
+  a.d = (int)p->ctx->R.d;
+  a.k = (int)p->ctx->R.k;
+  a.out_b = out_b;
+  a.out_a = out_a;
+  a.c = p->epi;
+  const int tiles = (int)((p->n_out + 127) / 128) * (int)(p->width / 32);
+  const int grid = tiles < p->ctx->sm_count ? tiles : p->ctx->sm_count;
+  HE_CUDA(launch_modgemm((int)p->d_w, (int)p->d0, (int)p->d1, p->tmA, tmB, a, grid, (cudaStream_t)stream),
+          "modgemm");
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_run(const he_pcmm_plan* p, const uint32_t* ct_in, uint32_t level, uint32_t* out_b,
+                                 uint32_t* out_a, void* ws, uint64_t ws_size, void* stream, he_ledger* ledger) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmm needs one level");
+  if (level != 1) return fail(HE_EINVAL, "the MLWE PCMM runs at level 1 (got %u); switch levels first", level);
+  he_status s = he_pcmm_decompose(p, ct_in, ws, ws_size, stream);
+  if (s) return s;
+  s = he_pcmm_gemm(p, ws, out_b, out_a, stream);
+  if (s) return s;
+  if (ledger) {
+    const int64_t bo = p->n_out / p->ctx->R.k, bi = p->n_in / p->ctx->R.k;
+    ledger->pc_mults += bo * bi;
+    ledger->rescales += bo;
+  }
+  return HE_OK;
+}

@@ -1,0 +1,278 @@
+// he_crypto.cu -- K3 (RLWE -> MLWE digit decomposition), weight encoding, and the
+// key/encrypt/decrypt plumbing used to make and check ciphertexts on the device.
+#include "he_common.cuh"
+#include "he_kernels.h"
+
+namespace he {
+
+// ================================================================ K3: decomposition
+// For RLWE ct r and limb i, the per-limb GEMM operand has rows x = r*k + t (MLWE component t)
+// and columns n:
+//   n <  d          : b_r[t + k n]
+//   n = d + d j + m : a~_{t,j}[m] = a_r[t - j + k m], negacyclic (a_r[c < 0] = -a_r[c + N])
+// stored K-major as balanced signed 8-bit digit planes: plane p holds digit e of limb i
+// (p = e for limb 0, D0 + e for limb 1) as planes[p][n][x].  One CTA per (r, m): it stages
+// the 2k-word window of a_r around k*m in shared memory and writes the k+1 rows
+// {n = m} U {n = d + d j + m : j < k}, 4 components per thread, one 32-bit store per digit.
+__global__ void __launch_bounds__(256) decompose_kernel(const uint32_t* __restrict__ ct, uint32_t n_in, uint32_t d,
+                                                        uint32_t k, uint32_t N, uint32_t q0, uint32_t q1, int d0,
+                                                        int d1, int8_t* __restrict__ planes, uint64_t plane_stride) {
+  extern __shared__ uint32_t win[];  // [2 limbs][2k] a-window, then [2 limbs][k] b-row
+  const uint32_t r = blockIdx.x, m = blockIdx.y;
+  const uint32_t qs[2] = {q0, q1};
+  uint32_t* bw = win + 4 * k;
+  for (uint32_t i = threadIdx.x; i < 2 * k; i += blockDim.x) {
+    const int64_t c = (int64_t)k * m - (int64_t)k + i;
+#pragma unroll
+    for (int L = 0; L < 2; ++L) {
+      const uint32_t* a = ct + ((size_t)r * 2 + L) * 2 * N;
+      uint32_t v;
+      if (c >= 0) {
+        v = a[c];
+      } else {
+        uint32_t w = a[c + N];
+        v = w ? qs[L] - w : 0u;
+      }
+      win[L * 2 * k + i] = v;
+    }
+  }
+  for (uint32_t t = threadIdx.x; t < k; t += blockDim.x) {
+#pragma unroll
+    for (int L = 0; L < 2; ++L) bw[L * k + t] = ct[((size_t)r * 2 + L) * 2 * N + N + t + (size_t)k * m];
+  }
+  __syncthreads();
+
+  const uint32_t tpr = k / 4;                 // threads per output row
+  const uint32_t rows_per_pass = blockDim.x / tpr;
+  const uint32_t sub = threadIdx.x % tpr, rsel = threadIdx.x / tpr;
+  const uint32_t t0 = sub * 4;
+  for (uint32_t rho = rsel; rho < k + 1; rho += rows_per_pass) {
+    // rho = 0: b-row n = m; rho = 1 + j: a-row n = d + d j + m
+    const uint32_t n = rho == 0 ? m : d + d * (rho - 1) + m;
+#pragma unroll
+    for (int L = 0; L < 2; ++L) {
+      const uint32_t q = qs[L];
+      uint32_t packed[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t t = t0 + e;
+        const uint32_t v = rho == 0 ? bw[L * k + t] : win[L * 2 * k + (t + k - (rho - 1))];
+        int32_t c = v > (q >> 1) ? (int32_t)(v - q) : (int32_t)v;
+        int8_t dg[4];
+        balanced_digits4(c, dg, 4);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) packed[p] |= ((uint32_t)(uint8_t)dg[p]) << (8 * e);
+      }
+      const int nd = L == 0 ? d0 : d1;
+      const int pbase = L == 0 ? 0 : d0;
+      for (int p = 0; p < nd; ++p) {
+        int8_t* dst = planes + (size_t)(pbase + p) * plane_stride + (size_t)n * n_in + (size_t)r * k + t0;
+        *reinterpret_cast<uint32_t*>(dst) = packed[p];
+      }
+    }
+  }
+}
+
+cudaError_t launch_decompose(const RingDims& R, const uint32_t* ct, uint32_t n_in, int d0, int d1, int8_t* planes,
+                             uint64_t plane_stride, cudaStream_t s) {
+  dim3 grid(n_in / R.k, R.d);
+  size_t smem = (size_t)6 * R.k * sizeof(uint32_t);
+  decompose_kernel<<<grid, 256, smem, s>>>(ct, n_in, R.d, R.k, R.N, R.q[0], R.q[1], d0, d1, planes, plane_stride);
+  return cudaGetLastError();
+}
+
+// ================================================================ weight encoding
+// W~[y][x] = round_half_even(q1 * W[k(y/k) + sigma(y%k)][k(x/k) + sigma(x%k)])
+// (block conjugation by sigma = g o nibble swap, PAPER.md:672 / bitrev.py:57-70).
+__device__ __forceinline__ long long encoded_weight(const double* W, uint32_t n_in, uint32_t k, int logk, double dw,
+                                                    uint32_t y, uint32_t x) {
+  const uint32_t sr = (y / k) * k + sigma_h(y % k, logk);
+  const uint32_t sc = (x / k) * k + sigma_h(x % k, logk);
+  return __double2ll_rn(__dmul_rn(dw, W[(size_t)sr * n_in + sc]));
+}
+
+__global__ void weight_maxabs_kernel(const double* __restrict__ W, uint32_t n_out, uint32_t n_in, uint32_t k, int logk,
+                                     double dw, unsigned long long* maxabs) {
+  unsigned long long m = 0;
+  const size_t total = (size_t)n_out * n_in;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    long long v = encoded_weight(W, n_in, k, logk, dw, (uint32_t)(i / n_in), (uint32_t)(i % n_in));
+    unsigned long long a = (unsigned long long)(v < 0 ? -v : v);
+    m = a > m ? a : m;
+  }
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = t > m ? t : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(maxabs, m);
+}
+
+__global__ void encode_weights_kernel(const double* __restrict__ W, uint32_t n_out, uint32_t n_in, uint32_t k,
+                                      int logk, double dw, uint32_t ndig, int8_t* __restrict__ planes) {
+  const size_t total = (size_t)n_out * n_in;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    long long v = encoded_weight(W, n_in, k, logk, dw, (uint32_t)(i / n_in), (uint32_t)(i % n_in));
+    int8_t dg[4];
+    balanced_digits4((int32_t)v, dg, 4);
+    for (uint32_t p = 0; p < ndig; ++p) planes[(size_t)p * total + i] = dg[p];
+  }
+}
+
+cudaError_t launch_weight_maxabs(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in,
+                                 unsigned long long* maxabs, cudaStream_t s) {
+  weight_maxabs_kernel<<<1184, 256, 0, s>>>(W, n_out, n_in, R.k, (int)R.logk, (double)R.q[1], maxabs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_encode_weights(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in, uint32_t dw,
+                                  int8_t* planes, cudaStream_t s) {
+  encode_weights_kernel<<<1184, 256, 0, s>>>(W, n_out, n_in, R.k, (int)R.logk, (double)R.q[1], dw, planes);
+  return cudaGetLastError();
+}
+
+// ================================================================ keys / encryption / decryption
+__global__ void keygen_kernel(uint64_t seed, uint32_t N, int32_t* s) {
+  const uint64_t key = rng_key(seed, kStreamSecret);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+    s[i] = ternary(rng_draw(key, i));
+}
+cudaError_t launch_keygen(const RingDims& R, uint64_t seed, int32_t* s_dev, cudaStream_t st) {
+  keygen_kernel<<<(R.N + 255) / 256, 256, 0, st>>>(seed, R.N, s_dev);
+  return cudaGetLastError();
+}
+
+__global__ void reduce_secret_kernel(const int32_t* s, uint32_t N, uint32_t q, uint32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    int32_t v = s[i];
+    out[i] = v < 0 ? q + v : (uint32_t)v;
+  }
+}
+cudaError_t launch_reduce_secret(const RingDims& R, const int32_t* s_dev, uint32_t limb, uint32_t* out,
+                                 cudaStream_t st) {
+  reduce_secret_kernel<<<(R.N + 255) / 256, 256, 0, st>>>(s_dev, R.N, R.q[limb], out);
+  return cudaGetLastError();
+}
+
+// a-part of every (ct, limb) and a copy in the b slot (NTT'd in place to form a*s)
+__global__ void gen_a_kernel(uint64_t seed, uint32_t r0, uint32_t N, uint32_t q0, uint32_t q1, uint32_t* ct) {
+  const uint32_t r = blockIdx.y, L = blockIdx.z;
+  const uint32_t q = L ? q1 : q0;
+  const uint64_t key = rng_key(seed, stream_a(r0 + r, L));
+  uint32_t* a = ct + ((size_t)r * 2 + L) * 2 * N;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    uint32_t v = (uint32_t)(rng_draw(key, i) % q);
+    a[i] = v;
+    a[N + i] = v;
+  }
+}
+cudaError_t launch_gen_a(const RingDims& R, uint64_t seed, uint32_t r0, uint32_t n_ct, uint32_t* ct, cudaStream_t st) {
+  dim3 g((R.N + 1023) / 1024, n_ct, 2);
+  gen_a_kernel<<<g, 256, 0, st>>>(seed, r0, R.N, R.q[0], R.q[1], ct);
+  return cudaGetLastError();
+}
+
+__global__ void pointwise_kernel(const uint32_t* x, uint64_t xs, const uint32_t* y, uint32_t n, uint32_t q,
+                                 uint32_t* out, uint64_t os) {
+  const uint32_t p = blockIdx.y;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[p * os + i] = mul_mod(x[p * xs + i], y[i], q);
+}
+cudaError_t launch_pointwise_mul(const uint32_t* x, uint64_t x_stride, const uint32_t* y, uint32_t n,
+                                 uint32_t count, uint32_t q, uint32_t* out, uint64_t out_stride, cudaStream_t st) {
+  dim3 g((n + 1023) / 1024, count);
+  pointwise_kernel<<<g, 256, 0, st>>>(x, x_stride, y, n, q, out, out_stride);
+  return cudaGetLastError();
+}
+
+// b = -(a s) + Ecd_coeff(acts) + e; the b slot holds a*s on entry.
+__global__ void finish_encrypt_kernel(const double* __restrict__ acts, uint32_t n_in, uint32_t d, uint32_t k,
+                                      int logk, uint32_t N, double delta, uint64_t seed, uint32_t r0, uint32_t q0,
+                                      uint32_t q1, uint32_t* ct) {
+  const uint32_t r = blockIdx.y;
+  const uint64_t ekey = rng_key(seed, stream_e(r0 + r));
+  const uint32_t half = d / 2;
+  const int lh = ilog2_h(half);
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+    const uint32_t t = c % k, m = c / k;
+    long long pt = 0;
+    if (m < half) {
+      const double v = acts[(size_t)bitrev_h(m, lh) * n_in + (size_t)k * r + sigma_h(t, logk)];
+      pt = __double2ll_rn(__dmul_rn(delta, v));
+    }
+    const long long e = cbd21_d(rng_draw(ekey, c));
+#pragma unroll
+    for (int L = 0; L < 2; ++L) {
+      const uint32_t q = L ? q1 : q0;
+      uint32_t* b = ct + ((size_t)r * 2 + L) * 2 * N + N;
+      const uint32_t as = b[c];
+      uint64_t v = (uint64_t)from_i64(pt, q) + from_i64(e, q) + (q - as);
+      b[c] = (uint32_t)(v % q);
+    }
+  }
+}
+cudaError_t launch_finish_encrypt(const RingDims& R, const double* acts, uint32_t n_in, uint64_t seed, uint32_t r0,
+                                  uint32_t n_ct, uint32_t* ct, cudaStream_t st) {
+  dim3 g((R.N + 1023) / 1024, n_ct);
+  finish_encrypt_kernel<<<g, 256, 0, st>>>(acts, n_in, R.d, R.k, (int)R.logk, R.N, (double)(1ull << R.log_delta),
+                                           seed, r0, R.q[0], R.q[1], ct);
+  return cudaGetLastError();
+}
+
+__global__ void phase_kernel(const uint32_t* b, uint64_t bs, const uint32_t* as, uint64_t ass, uint32_t n, uint32_t q,
+                             int64_t* phase) {
+  const uint32_t p = blockIdx.y;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t v = add_mod(b[p * bs + i], as[p * ass + i], q);
+    phase[(size_t)p * n + i] = v > q / 2 ? (int64_t)v - q : (int64_t)v;
+  }
+}
+cudaError_t launch_phase(const uint32_t* b, uint64_t b_stride, const uint32_t* as, uint64_t as_stride, uint32_t n,
+                         uint32_t count, uint32_t q, int64_t* phase, cudaStream_t st) {
+  dim3 g((n + 1023) / 1024, count);
+  phase_kernel<<<g, 256, 0, st>>>(b, b_stride, as, as_stride, n, q, phase);
+  return cudaGetLastError();
+}
+
+// MLWE decryption of PCMM output rows (level 0, q0):
+//   phase_y[m] = b'_y[m] + sum_j sum_m' a'_y[j][m'] * s_j[m - m']  (negacyclic in Y^d = -1),
+//   s_j[m] = s[j + k m].   One CTA per row, one thread per m, j streamed through smem.
+__global__ void __launch_bounds__(256) decrypt_mlwe_kernel(const int32_t* __restrict__ s,
+                                                           const uint32_t* __restrict__ out_b,
+                                                           const uint32_t* __restrict__ out_a, uint32_t d, uint32_t k,
+                                                           uint32_t N, uint32_t q0, uint32_t row0, int64_t* phase) {
+  extern __shared__ uint32_t sh[];  // a_j [d], s_j [2d] (s_j[m - m'] with wrap sign folded)
+  int32_t* sj = reinterpret_cast<int32_t*>(sh + d);
+  const uint32_t y = row0 + blockIdx.x;
+  const uint32_t* arow = out_a + (size_t)y * N;
+  int64_t acc = 0;
+  for (uint32_t j = 0; j < k; ++j) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+      sh[i] = arow[(size_t)j * d + i];
+      const int32_t sv = s[j + (size_t)k * i];
+      sj[d + i] = sv;   // index m - m' >= 0
+      sj[i] = -sv;      // index m - m' + d (wrapped, negated)
+    }
+    __syncthreads();
+    for (uint32_t m = threadIdx.x; m < d; m += blockDim.x) {
+      int64_t part = 0;
+      for (uint32_t mp = 0; mp < d; ++mp) part += (int64_t)sh[mp] * sj[d + m - mp];
+      acc += part % (int64_t)q0;  // |part| < d * q0 < 2^40
+    }
+  }
+  for (uint32_t m = threadIdx.x; m < d; m += blockDim.x) {
+    const uint32_t b = out_b[(size_t)(y / k) * N + (y % k) + (size_t)k * m];
+    int64_t v = (acc + b) % (int64_t)q0;
+    if (v < 0) v += q0;
+    phase[(size_t)blockIdx.x * d + m] = v > q0 / 2 ? v - q0 : v;
+  }
+}
+cudaError_t launch_decrypt_mlwe(const RingDims& R, const int32_t* s, const uint32_t* out_b, const uint32_t* out_a,
+                                uint32_t n_out, uint32_t row0, uint32_t n_rows, int64_t* phase, cudaStream_t st) {
+  if (R.d > 256) return cudaErrorInvalidValue;  // one thread per m
+  size_t smem = 3 * (size_t)R.d * sizeof(uint32_t);
+  decrypt_mlwe_kernel<<<n_rows, R.d, smem, st>>>(s, out_b, out_a, R.d, R.k, R.N, R.q[0], row0, phase);
+  return cudaGetLastError();
+}
+
+}  // namespace he

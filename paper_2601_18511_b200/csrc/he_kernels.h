@@ -1,0 +1,66 @@
+// he_kernels.h -- internal launcher declarations shared by the .cu translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace he {
+
+// (weight digits, limb-0 ciphertext digits, limb-1 ciphertext digits) instantiated for K1
+#define HE_GEMM_INSTANCES(X) \
+  X(1, 4, 3) X(2, 4, 3) X(3, 4, 3) X(4, 4, 3) X(1, 4, 4) X(2, 4, 4) X(3, 4, 4) X(4, 4, 4)
+
+struct GemmEpiConst {
+  uint32_t q[2];
+  uint32_t offs[2];     // q * ceil(2^31 / q): maps a negative int32 accumulator into [0, 2^32)
+  uint32_t pw[2][8];    // 2^(8 s) mod q
+  uint32_t pwp[2][8];   // Shoup companions
+  uint32_t q1inv, q1invp;
+};
+
+struct GemmArgs {
+  int n_out, n_in, width, d, k;
+  uint32_t* out_b;
+  uint32_t* out_a;
+  GemmEpiConst c;
+};
+
+int gemm_smem_bytes(int dw, int d0, int d1);
+cudaError_t launch_modgemm(int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                           const GemmArgs& args, int grid, cudaStream_t stream);
+
+// NTT tables for one (modulus, degree)
+struct NttTable {
+  uint32_t n = 0, q = 0;
+  uint32_t *fw = nullptr, *fwp = nullptr, *iv = nullptr, *ivp = nullptr;  // device, n entries each
+  uint32_t ninv = 0, ninvp = 0;
+};
+cudaError_t ntt_table_init(NttTable& t, uint32_t n, uint32_t q);
+void ntt_table_free(NttTable& t);
+cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s);
+cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s);
+
+struct RingDims {
+  uint32_t d, k, N, logk, q[2], log_delta;
+};
+
+cudaError_t launch_decompose(const RingDims& R, const uint32_t* ct, uint32_t n_in, int d0, int d1, int8_t* planes,
+                             uint64_t plane_stride, cudaStream_t s);
+cudaError_t launch_weight_maxabs(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in,
+                                 unsigned long long* maxabs, cudaStream_t s);
+cudaError_t launch_encode_weights(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in, uint32_t dw,
+                                  int8_t* planes, cudaStream_t s);
+cudaError_t launch_keygen(const RingDims& R, uint64_t seed, int32_t* s_dev, cudaStream_t st);
+cudaError_t launch_reduce_secret(const RingDims& R, const int32_t* s_dev, uint32_t limb, uint32_t* out,
+                                 cudaStream_t st);
+cudaError_t launch_gen_a(const RingDims& R, uint64_t seed, uint32_t r0, uint32_t n_ct, uint32_t* ct, cudaStream_t st);
+cudaError_t launch_pointwise_mul(const uint32_t* x, uint64_t x_stride, const uint32_t* y, uint32_t n,
+                                 uint32_t count, uint32_t q, uint32_t* out, uint64_t out_stride, cudaStream_t st);
+cudaError_t launch_finish_encrypt(const RingDims& R, const double* acts, uint32_t n_in, uint64_t seed, uint32_t r0,
+                                  uint32_t n_ct, uint32_t* ct, cudaStream_t st);
+cudaError_t launch_phase(const uint32_t* b, uint64_t b_stride, const uint32_t* as, uint64_t as_stride, uint32_t n,
+                         uint32_t count, uint32_t q, int64_t* phase, cudaStream_t st);
+cudaError_t launch_decrypt_mlwe(const RingDims& R, const int32_t* s, const uint32_t* out_b, const uint32_t* out_a,
+                                uint32_t n_out, uint32_t row0, uint32_t n_rows, int64_t* phase, cudaStream_t st);
+
+}  // namespace he

@@ -1,0 +1,283 @@
+// he_modgemm.cu -- K1: the per-RNS-limb modular GEMM of the MLWE PCMM on tcgen05 int8 tensor cores.
+//
+//   v_i[y][n] = sum_x W~[y][x] * C_i[x][n]  mod q_i      (i = 0, 1;  SURVEY.md App. B.3)
+//   out[y][n] = rescale(v_0, v_1) = ((v_0 - [v_1]_centred) * q_1^-1) mod q_0
+//
+// W~ (integer, |W~| < 2^31) is split into D_W balanced 8-bit digit planes, the centred
+// ciphertext words C_i into D_i planes (he_decompose.cu).  One tile = 128 output rows x
+// 32 GEMM columns x both limbs.  For weight digit a and limb i, ONE tcgen05.mma multiplies
+// the A plane a against the D_i ciphertext planes stacked along N ([C_i,0 | C_i,1 | ...]),
+// writing at TMEM column offset a*32: the product of digit pair (a, b) lands in the
+// accumulator of shift s = a + b.  So each limb needs only D_W + D_i - 1 int32
+// accumulators per output word (not D_W * D_i), and the MMA N is D_i * 32 (128 / 96).
+// The epilogue reduces each shift accumulator mod q_i (Shoup), recombines sum_s 2^(8s),
+// rescales the two limbs into one level-0 word, and stores b' already composed into RLWE
+// order and a' in MLWE row-major order.  Nothing but the level-0
+// result ever reaches HBM.
+//
+// Warp roles (192 threads, 1 CTA per SM, persistent over tiles, m-fastest raster so the
+// 32 M-blocks sharing one ciphertext N-block run together and the B tile is L2-hot):
+//   warp 0  TMA producer (A: weight digits, EVICT_LAST; B: ciphertext digits, EVICT_FIRST)
+//   warp 1  TMEM allocator + single-thread MMA issuer
+//   warps 2-5 epilogue (TMEM lane quarter = warp % 4)
+#include <cuda.h>
+#include "he_common.cuh"
+#include "he_tc.cuh"
+#include "he_kernels.h"
+
+namespace he {
+
+constexpr int kBM = 128;   // output rows per tile (TMEM lanes)
+constexpr int kBN = 32;    // GEMM columns per tile
+constexpr int kBK = 128;   // K bytes per pipeline stage (one 128-B swizzle row)
+constexpr int kThreads = 192;
+
+template <int DW, int D0, int D1>
+struct GemmCfg {
+  static constexpr int S0 = DW + D0 - 1;                 // shift accumulators, limb 0
+  static constexpr int S1 = DW + D1 - 1;                 // shift accumulators, limb 1
+  static constexpr int kTmemCols = (S0 + S1) * kBN;
+  static constexpr int kTmemAlloc = kTmemCols <= 32 ? 32 : kTmemCols <= 64 ? 64 : kTmemCols <= 128 ? 128
+                                  : kTmemCols <= 256 ? 256 : 512;
+  static constexpr int kABytes = DW * kBM * kBK;         // per stage
+  static constexpr int kBBytes = (D0 + D1) * kBN * kBK;  // per stage
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
+  static constexpr int kZeroBytes = 8192;                // zero operand for accumulator clearing
+  static constexpr int kSmemBytes = kStages * kStageBytes + kZeroBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(kTmemCols <= 512, "too many shift accumulators for TMEM");
+  static_assert(kStages >= 2, "not enough shared memory for two stages");
+  static_assert(S0 * kBN <= 256 && S1 * kBN <= 256, "zeroing MMA N out of range");
+};
+
+template <int DW, int D0, int D1>
+__global__ void __launch_bounds__(kThreads, 1)
+    modgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmArgs args) {
+  using C = GemmCfg<DW, D0, D1>;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-B alignment for the 128-B swizzle atoms
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint8_t* sA = smem;                                   // [stage][DW][128 rows][128 B]
+  uint8_t* sB = smem + C::kStages * C::kABytes;         // [stage][D0+D1][32 rows][128 B]
+  uint8_t* sZero = sB + C::kStages * C::kBBytes;        // 8 KB of zeros
+  uint64_t* full = reinterpret_cast<uint64_t*>(sZero + C::kZeroBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tmem_full = empty + C::kStages;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int m_tiles = (args.n_out + kBM - 1) / kBM;
+  const int n_tiles = args.width / kBN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int num_kb = (args.n_in + kBK - 1) / kBK;
+
+  for (int i = threadIdx.x; i < C::kZeroBytes / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 4 * 32);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, C::kTmemAlloc);
+    tmem_relinquish();
+  }
+  fence_proxy_async();  // zero tile visible to the tensor-core (async) proxy
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % m_tiles) * kBM;
+        const int n0 = (tile / m_tiles) * kBN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::kStageBytes);
+          uint8_t* a_dst = sA + stage * C::kABytes;
+          uint8_t* b_dst = sB + stage * C::kBBytes;
+#pragma unroll
+          for (int a = 0; a < DW; ++a)
+            tma_load_3d(a_dst + a * kBM * kBK, &tmA, &full[stage], kb * kBK, m0, a, kEvictLast);
+#pragma unroll
+          for (int p = 0; p < D0 + D1; ++p)
+            tma_load_3d(b_dst + p * kBN * kBK, &tmB, &full[stage], kb * kBK, n0, p, kEvictFirst);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    constexpr uint32_t kIdesc0 = idesc_i8(kBM, D0 * kBN);
+    constexpr uint32_t kIdesc1 = idesc_i8(kBM, D1 * kBN);
+    constexpr uint32_t kIdescZ0 = idesc_i8(kBM, C::S0 * kBN);
+    constexpr uint32_t kIdescZ1 = idesc_i8(kBM, C::S1 * kBN);
+    const uint32_t reg0 = tmem_base;                     // limb-0 shift accumulators
+    const uint32_t reg1 = tmem_base + C::S0 * kBN;       // limb-1 shift accumulators
+    const uint64_t zdesc = desc_noswz(smem_u32(sZero), 128, 256);
+    int stage = 0;
+    uint32_t phase = 0;
+    int iter = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+      if (iter > 0) mbar_wait(tmem_empty, (iter - 1) & 1);  // epilogue drained the accumulators
+      tc_fence_after();
+      if (elect_one()) {
+        // clear all shift accumulators: D = 0 * B
+        mma_i8(reg0, zdesc, zdesc, kIdescZ0, 0);
+        mma_i8(reg1, zdesc, zdesc, kIdescZ1, 0);
+      }
+      __syncwarp();
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
+          const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 32; ++kk) {
+            const uint64_t b0 = desc_sw128(b_base + kk * 32);
+            const uint64_t b1 = desc_sw128(b_base + D0 * kBN * kBK + kk * 32);
+#pragma unroll
+            for (int a = 0; a < DW; ++a) {
+              const uint64_t ad = desc_sw128(a_base + a * kBM * kBK + kk * 32);
+              mma_i8(reg0 + a * kBN, ad, b0, kIdesc0, 1);
+              mma_i8(reg1 + a * kBN, ad, b1, kIdesc1, 1);
+            }
+          }
+          tc_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (elect_one()) tc_commit(tmem_full);
+      __syncwarp();
+    }
+  } else {
+    // ======================= epilogue =======================
+    const uint32_t quarter = warp & 3;                   // TMEM lanes this warp may access
+    const uint32_t row_in_tile = quarter * 32 + lane;
+    const uint32_t lane_addr = (quarter * 32) << 16;
+    const int N = args.d * args.k;
+    const int logk = ilog2_h(args.k);
+    (void)logk;
+    const GemmEpiConst& c = args.c;
+    int iter = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+      const int m0 = (tile % m_tiles) * kBM;
+      const int n0 = (tile / m_tiles) * kBN;
+      mbar_wait(tmem_full, iter & 1);
+      tc_fence_after();
+      const int y = m0 + (int)row_in_tile;
+      const bool row_ok = y < args.n_out;
+#pragma unroll 1
+      for (int c8 = 0; c8 < kBN / 8; ++c8) {
+        uint32_t acc0[C::S0][8], acc1[C::S1][8];
+#pragma unroll
+        for (int s = 0; s < C::S0; ++s) tmem_ld_x8(tmem_base + lane_addr + s * kBN + c8 * 8, acc0[s]);
+#pragma unroll
+        for (int s = 0; s < C::S1; ++s) tmem_ld_x8(tmem_base + lane_addr + (C::S0 + s) * kBN + c8 * 8, acc1[s]);
+        tmem_ld_wait();
+        uint32_t res[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          // limb 0: sum_s 2^(8s) * acc_s  mod q0
+          uint32_t x0 = 0, x1 = 0;
+#pragma unroll
+          for (int s = 0; s < C::S0; ++s) {
+            const uint32_t v = acc0[s][e];
+            const uint32_t u = ((int32_t)v < 0) ? v + c.offs[0] : v;   // == acc (mod q0), < 2^32
+            x0 = add_mod(x0, shoup_mul(u, c.pw[0][s], c.pwp[0][s], c.q[0]), c.q[0]);
+          }
+#pragma unroll
+          for (int s = 0; s < C::S1; ++s) {
+            const uint32_t v = acc1[s][e];
+            const uint32_t u = ((int32_t)v < 0) ? v + c.offs[1] : v;
+            x1 = add_mod(x1, shoup_mul(u, c.pw[1][s], c.pwp[1][s], c.q[1]), c.q[1]);
+          }
+          // rescale: ((x0 - [x1]_centred) * q1^-1) mod q0
+          uint32_t t;
+          if (x1 > (c.q[1] >> 1)) {
+            t = csub(x0 + (c.q[1] - x1), c.q[0]);              // x0 + |x1c|
+          } else {
+            t = sub_mod(x0, x1, c.q[0]);
+          }
+          res[e] = shoup_mul(t, c.q1inv, c.q1invp, c.q[0]);
+        }
+        if (row_ok) {
+          const int n = n0 + c8 * 8;
+          if (n < args.d) {
+            // b' composed into RLWE order: b_rlwe[y / k][(y % k) + k * m]
+            uint32_t* dst = args.out_b + (size_t)(y / args.k) * N + (y % args.k);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dst[(size_t)args.k * (n + e)] = res[e];
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(args.out_a + (size_t)y * (N) + (n - args.d));
+            dst[0] = make_uint4(res[0], res[1], res[2], res[3]);
+            dst[1] = make_uint4(res[4], res[5], res[6], res[7]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tmem_empty);
+    }
+  }
+
+  __syncwarp();  // reconverge each role warp before the CTA barrier
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemAlloc);
+  }
+}
+
+template <int DW, int D0, int D1>
+static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int grid,
+                            cudaStream_t stream) {
+  using C = GemmCfg<DW, D0, D1>;
+  auto kern = modgemm_kernel<DW, D0, D1>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(tmA, tmB, args);
+  return cudaGetLastError();
+}
+
+int gemm_smem_bytes(int dw, int d0, int d1) {
+#define HE_CASE(a, b, c) \
+  if (dw == a && d0 == b && d1 == c) return GemmCfg<a, b, c>::kSmemBytes;
+  HE_GEMM_INSTANCES(HE_CASE)
+#undef HE_CASE
+  return -1;
+}
+
+cudaError_t launch_modgemm(int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                           const GemmArgs& args, int grid, cudaStream_t stream) {
+#define HE_CASE(a, b, c) \
+  if (dw == a && d0 == b && d1 == c) return launch_t<a, b, c>(tmA, tmB, args, grid, stream);
+  HE_GEMM_INSTANCES(HE_CASE)
+#undef HE_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace he

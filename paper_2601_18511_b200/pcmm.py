@@ -1,0 +1,152 @@
+"""MLWE-format PCMM (BCHPS24 Alg. 2 as used at PAPER.md:54-55,134) -- the drop-in entry points.
+
+Mirrors the reference's operator API for a plaintext x ciphertext product
+(pkg/src/hesim/matmul.py:77-181): a weight-side *plan* built once, and a kernel
+call ``(ctx, plan, operand) -> result`` that validates before any compute, raises
+the reference's exceptions, never mutates its inputs, consumes exactly one level
+and records the work in ``ctx.ledger`` like one fused ``pc_linear`` per output
+block (slotsim.py:330-370):
+
+    make_pcmm_plan(ctx, weights, shear_power, split, on_the_fly)   (matmul.py:77-100)
+        -> make_mlwe_pcmm_plan(ctx, weights, d_w=None)
+    pcmm_depth1 / pcmm_bsgs(ctx, plan, B)                         (matmul.py:152-176)
+        -> pcmm_mlwe(ctx, plan, X)
+    clear_pcmm(A, B, shear_power)                                 (matmul.py:179-181)
+        -> clear_pcmm(W, acts)
+
+Work split (all on the device, through the C ABI in include/he_b200.h):
+  plan:  W -> W~ = round(q1 W), k x k blocks conjugated by sigma, balanced int8 digit planes
+  run:   K3 RLWE -> MLWE digit decomposition, then K1 tcgen05 modular GEMM with the digit
+         recombination, reduction mod q_i, rescale and b' compose fused in its epilogue.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import native
+from .context import CtBlocks, HeContext, MlweBlocks, _torch, require_level
+from .params import signed_digits
+
+
+@dataclass
+class MlwePcmmPlan:
+    """Weight side of the MLWE PCMM.  Immutable after creation and
+    safe to share between forked contexts; the digit planes stay on the device."""
+
+    n_out: int
+    n_in: int
+    d_w: int
+    max_abs: int
+    digits: object          # torch int8 [d_w, n_out, n_in]
+    layout: str = "app_a_coeff"
+    _handle: object = field(default=None, repr=False)
+    _workspace: object = field(default=None, repr=False)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self.n_out, self.n_in
+
+    def workspace_bytes(self) -> int:
+        n = ctypes.c_uint64()
+        native.call("he_pcmm_workspace_bytes", self._handle, ctypes.byref(n))
+        return int(n.value)
+
+    def workspace(self, device):
+        torch = _torch()
+        need = self.workspace_bytes()
+        if self._workspace is None or self._workspace.numel() < need:
+            self._workspace = torch.empty(need, dtype=torch.int8, device=device)
+        return self._workspace
+
+    def __del__(self):
+        try:
+            if self._handle:
+                native.lib().he_pcmm_plan_destroy(self._handle)
+        except Exception:
+            pass
+
+
+def make_mlwe_pcmm_plan(ctx: HeContext, weights, d_w: int | None = None) -> MlwePcmmPlan:
+    """Encode the float weights W (n_out x n_in) for the MLWE PCMM.
+
+    W~ = round_half_even(q1 * W) (Delta_w = q1 so the op keeps the input scale),
+    each k x k block conjugated by sigma (PAPER.md:672 / bitrev.py:57-70 in component
+    order), split into ``d_w`` balanced int8 digit planes; ``d_w`` defaults to the
+    fewest digits that hold max|W~|.
+    """
+    torch = _torch()
+    p = ctx.params
+    w = torch.as_tensor(weights, dtype=torch.float64, device=ctx.device)
+    if w.ndim != 2:
+        raise ValueError("weights must be a matrix")
+    n_out, n_in = (int(s) for s in w.shape)
+    k = p.mlwe_rank
+    if n_out % k or n_in % k:
+        raise ValueError(f"dim mismatch: weight dims ({n_out}, {n_in}) must be multiples of k = {k}")
+    if not bool(torch.isfinite(w).all()):
+        raise ValueError("weights must be finite")
+    w = w.contiguous()
+    mx = ctypes.c_uint64()
+    native.call("he_pcmm_weight_maxabs", ctx.handle, w.data_ptr(), n_out, n_in, ctypes.byref(mx), ctx.stream())
+    max_abs = int(mx.value)
+    need = signed_digits(max_abs)
+    if max_abs >= 1 << 31 or need > 4:
+        raise ValueError(f"encoded weights too large (max |W~| = {max_abs} >= 2^31); rescale W")
+    if d_w is None:
+        d_w = need
+    if not need <= d_w <= 4:
+        raise ValueError(f"d_w = {d_w} cannot hold max |W~| = {max_abs} (needs >= {need})")
+    digits = torch.empty((d_w, n_out, n_in), dtype=torch.int8, device=ctx.device)
+    native.call("he_pcmm_encode_weights", ctx.handle, w.data_ptr(), n_out, n_in, d_w, digits.data_ptr(),
+                ctx.stream())
+    h = ctypes.c_void_p()
+    native.call("he_pcmm_plan_create", ctx.handle, digits.data_ptr(), n_out, n_in, d_w, ctypes.byref(h))
+    return MlwePcmmPlan(n_out, n_in, d_w, max_abs, digits, _handle=h)
+
+
+def _check_operand(ctx: HeContext, plan: MlwePcmmPlan, X) -> None:
+    """Error contract of matmul.py:139-149, raised before any compute."""
+    if not isinstance(X, CtBlocks):
+        raise TypeError("pcmm consumes a ciphertext operand")
+    if X.n_cols != plan.n_in:
+        raise ValueError(f"dim mismatch: plan {plan.n_in}, operand {X.n_cols}")
+    if X.layout != plan.layout:
+        raise ValueError(f"layout mismatch: plan expects {plan.layout}, got {X.layout}")
+    require_level(X.level)
+    if X.level != 1:
+        raise ValueError(f"the MLWE PCMM runs at level 1, operand is at level {X.level}; switch levels first")
+    shape = tuple(int(s) for s in X.data.shape)
+    if shape != (plan.n_in // ctx.params.mlwe_rank, 2, 2, ctx.params.N):
+        raise ValueError(f"ciphertext batch has shape {shape}")
+
+
+def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks | None = None) -> MlweBlocks:
+    """Level-1 RLWE block batch (encrypting A, (d/2) x n_in) -> level-0 MLWE blocks
+    encrypting A @ W^T ((d/2) x n_out).  Exactly one level, one rescale per output block,
+    zero ciphertext rotations."""
+    torch = _torch()
+    _check_operand(ctx, plan, X)
+    p = ctx.params
+    if out is None:
+        out_b = torch.empty((plan.n_out // p.mlwe_rank, p.N), dtype=torch.int32, device=ctx.device)
+        out_a = torch.empty((plan.n_out, p.N), dtype=torch.int32, device=ctx.device)
+        out = MlweBlocks(out_b, out_a, level=X.level - 1, n_rows=plan.n_out)
+    ws = plan.workspace(ctx.device)
+    led = native.HeLedgerC()
+    native.call("he_pcmm_run", plan._handle, X.data.data_ptr(), X.level, out.out_b.data_ptr(), out.out_a.data_ptr(),
+                ws.data_ptr(), ws.numel(), ctx.stream(), ctypes.byref(led))
+    ctx.ledger.add_c(led)
+    ctx.ledger.observe_level(X.level - 1)
+    out.level = X.level - 1
+    out.n_rows = plan.n_out
+    return out
+
+
+def clear_pcmm(weights, acts) -> np.ndarray:
+    """Cleartext oracle of what ``pcmm_mlwe`` decrypts to: acts @ W^T, i.e.
+    (W @ M)^T with M = acts^T (hesim.clear_pcmm(W, M, 0), matmul.py:179-181)."""
+    return np.asarray(acts, float) @ np.asarray(weights, float).T
