@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py -- encrypted MLWE PCMM ms/op at 4096x11008x128 (CKKS N = 2^16) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--shape 4096x11008]
+
+One "step" = one MLWE PCMM op on the named Llama shape: the level-1
+RLWE ciphertexts encrypting a 128 x n_in activation block go in, the level-0 MLWE
+blocks encrypting (W @ M)^T come out.  At N > 1 GPUs (torchrun, one rank per GPU, NCCL)
+the weight row-blocks are sharded over ranks: rank 0's input
+ciphertexts are broadcast, every rank runs K3 + K1 on its rows, and the output blocks
+are all-gathered -- all inside the timed region (strong scaling of one op).
+
+``value`` is device time per op (CUDA events, max over ranks) with the inputs resident
+in HBM; ``e2e`` is the same op through the public API with host buffers (pinned H2D of
+the input ciphertexts, D2H of the full output) inside the timed region.  ``--impl
+reference`` times the CPU restatement (oracle/, the port of the path) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np
+
+METRIC = "encrypted PCMM ms/op @4096x11008x128 (N=2^16); modmul-GEMM TOPS vs INT8 peak"
+INT8_PEAK_TOPS = 4500.0   # NVIDIA dense INT8 spec for B200 (no measured int8 figure in MEASURED_PEAKS.json)
+WORKLOADS = {
+    "4096x11008": "Llama-2-7B FFN down-proj PCMM 4096x11008x128, CKKS N=2^16, MLWE (256, 256) (BASELINE config 3, metric shape)",
+    "11008x4096": "Llama-2-7B FFN up/gate-proj PCMM 11008x4096x128 (BASELINE config 3)",
+    "4096x4096": "Llama-2-7B QKV-proj PCMM 4096x4096x128 (BASELINE config 2)",
+    "14336x4096": "Llama-3-8B FFN up-proj PCMM 14336x4096x128 (BASELINE config 4)",
+    "4096x14336": "Llama-3-8B FFN down-proj PCMM 4096x14336x128 (BASELINE config 4)",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--shape", default="4096x11008")
+    ap.add_argument("--params", choices=["llama", "wide"], default="llama")
+    ap.add_argument("--cpu-rows", type=int, default=64, help="oracle sample rows for cpu_baseline (0: skip)")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 0 or a.steps < 1:
+        ap.error("need --steps >= 1")
+    return a
+
+
+def shape_of(s: str):
+    n_out, n_in = (int(v) for v in s.lower().split("x"))
+    return n_out, n_in
+
+
+def params_of(name):
+    from paper_2601_18511_b200 import HeParams
+
+    return HeParams.wide() if name == "wide" else HeParams.llama()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clock and throttle reasons."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.2):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as exc:  # pragma: no cover - depends on the box
+            log("clock sampling unavailable:", exc)
+        self.period = period
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self._t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(a, rank: int, world: int, local: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_18511_b200 import HeContext, make_mlwe_pcmm_plan, pcmm_mlwe
+    from paper_2601_18511_b200.context import MlweBlocks
+    from paper_2601_18511_b200.pcmm import pcmm_ops
+    from paper_2601_18511_b200.sharding import row_shards, shard_slots
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P = params_of(a.params)
+    k, N = P.mlwe_rank, P.N
+    n_out, n_in = shape_of(a.shape)
+    b0, b1 = row_shards(n_out, k, world)[rank]         # balanced output row-blocks of this rank
+    per = shard_slots(n_out, k, world)                 # padded slots per rank for the all-gather
+    rows = (b1 - b0) * k
+    ctx = HeContext(P, device=dev)
+
+    # synthetic data, identical on every rank (seeded device generator)
+    g = torch.Generator(device=dev).manual_seed(20260117)
+    W = (torch.rand((n_out, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1) / math.sqrt(n_in)
+    A = torch.rand((P.tokens, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+    sk = ctx.keygen(7)
+    X = ctx.encrypt_acts(sk, A, seed=11)
+    if rows == 0:
+        raise SystemExit("more ranks than output row blocks")
+    plan = make_mlwe_pcmm_plan(ctx, W[b0 * k:b1 * k])
+    out_b = torch.empty((per, N), dtype=torch.int32, device=dev)
+    out_a = torch.empty((per * k, N), dtype=torch.int32, device=dev)
+    Y = MlweBlocks(out_b[: b1 - b0], out_a[:rows], level=0, n_rows=rows)
+    if world > 1:
+        all_b = torch.empty((per * world, N), dtype=torch.int32, device=dev)
+        all_a = torch.empty((per * world * k, N), dtype=torch.int32, device=dev)
+    del W
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    ev_g0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ev_g1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+
+    def step(i=None):
+        if world > 1:
+            dist.broadcast(X.data, src=0)
+        ev = (ev_g0[i], ev_g1[i]) if i is not None else None
+        pcmm_mlwe(ctx, plan, X, out=Y, gemm_events=ev)
+        if world > 1:
+            dist.all_gather_into_tensor(all_b, out_b)
+            dist.all_gather_into_tensor(all_a, out_a)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for i in range(a.steps):
+            step(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / a.steps
+    gemm_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in zip(ev_g0, ev_g1)]))
+    if world > 1:
+        tt = torch.tensor([ms, gemm_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, gemm_ms = float(tt[0]), float(tt[1])
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a,
+                      all_b if world > 1 else None, all_a if world > 1 else None)
+
+    # ---------------- roofline of the dominant kernel (K1)
+    ops = pcmm_ops(P, rows, n_in, plan.d_w)
+    achieved = ops / (gemm_ms * 1e-3) / 1e12
+    cublas = measure_cublas_int8(dev) if rank == 0 else None
+    traffic = load_traffic(a.shape, plan.d_w)
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": INT8_PEAK_TOPS, "unit": "TOPS",
+            "frac": round(achieved / INT8_PEAK_TOPS, 4), "traffic": traffic,
+            "kernel": "he::modgemm_kernel (K1, tcgen05 kind::i8)", "kernel_ms": round(gemm_ms, 3),
+            "int8_ops_per_launch": ops,
+            "peak_note": "NVIDIA dense INT8 spec (4.5 POPS); MEASURED_PEAKS.json has no int8 entry",
+            "cublas_int8_tops_measured": cublas,
+            "frac_of_2x_measured_bf16": round(achieved / (2 * measured_bf16()), 4) if measured_bf16() else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and a.cpu_rows > 0:
+        cpu = cpu_baseline(P, A, plan, X, n_out, n_in, a.cpu_rows, W_seed_dev=dev, g_seed=20260117)
+
+    if rank == 0:
+        d0, d1 = P.ct_digits(0), P.ct_digits(1)
+        line = {
+            "metric": METRIC, "value": round(ms, 3), "unit": "ms/op", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "mma_dtype": "s8xs8->s32",
+            "data": "synthetic: W ~ U[-1,1)/sqrt(n_in), acts ~ U[-1,1) (seeded), fresh RLWE encryptions on device",
+            "config": {"workload": WORKLOADS.get(a.shape, a.shape), "n_out": n_out, "n_in": n_in,
+                       "tokens": P.tokens, "N": N, "mlwe": [P.mlwe_degree, P.mlwe_rank],
+                       "moduli": list(P.moduli), "log_delta": P.log_delta,
+                       "digits": {"weight": plan.d_w, "ct_q0": d0, "ct_q1": d1},
+                       "parallelism": f"row-shard x{world}" + (" + NCCL bcast/all-gather" if world > 1 else ""),
+                       "l2": "inputs larger than L2: each op writes and reads a "
+                             f"{plan.workspace_bytes() / 1e9:.2f} GB ciphertext-digit workspace"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 2 * a.steps,
+            "clocks": clk.summary(),
+            "kernels_ms": {"modgemm": round(gemm_ms, 3), "decompose_and_rest": round(ms - gemm_ms, 3)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
+    """Same op through pcmm_mlwe with host buffers: pinned H2D of the input ciphertexts
+    (rank 0) and D2H of the whole output (rank 0) inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_18511_b200 import pcmm_mlwe
+
+    steps = a.e2e_steps or max(1, min(a.steps, 5))
+    h_in = torch.empty(X.data.shape, dtype=torch.int32, pin_memory=True)
+    h_in.copy_(X.data)
+    src_b, src_a = (all_b, all_a) if world > 1 else (out_b, out_a)
+    h_b = torch.empty(src_b.shape, dtype=torch.int32, pin_memory=True)
+    h_a = torch.empty(src_a.shape, dtype=torch.int32, pin_memory=True)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if rank == 0:
+            X.data.copy_(h_in, non_blocking=True)
+        if world > 1:
+            dist.broadcast(X.data, src=0)
+        pcmm_mlwe(ctx, plan, X, out=Y)
+        if world > 1:
+            dist.all_gather_into_tensor(all_b, out_b)
+            dist.all_gather_into_tensor(all_a, out_a)
+        if rank == 0:
+            h_b.copy_(src_b, non_blocking=True)
+            h_a.copy_(src_a, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt[0])
+    return {"value": round(ms, 3), "unit": "ms/op", "h2d_bytes_per_step": int(h_in.numel() * 4),
+            "d2h_bytes_per_step": int((h_b.numel() + h_a.numel()) * 4), "steps": steps,
+            "path": "pcmm_mlwe (he_pcmm_run) with pinned host buffers"}
+
+
+def measure_cublas_int8(dev):
+    import torch
+
+    try:
+        n = 8192
+        x = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev)
+        y = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev).t()
+        for _ in range(2):
+            torch._int_mm(x, y)
+        best = 1e9
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(5):
+            e0.record()
+            torch._int_mm(x, y)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return round(2 * n ** 3 / (best * 1e-3) / 1e12, 1)
+    except Exception as exc:  # pragma: no cover
+        log("cublas int8 probe failed:", exc)
+        return None
+
+
+def measured_bf16():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["bf16_tflops"])
+    except Exception:
+        return None
+
+
+def load_traffic(shape: str, d_w: int):
+    """dram bytes per K1 launch from the committed ncu --set full summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        data = json.loads(p.read_text())
+        ent = data.get("modgemm", {}).get(shape)
+        if ent and ent.get("d_w") == d_w:
+            return ent.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+# ----------------------------------------------------------------- CPU baseline / reference arm
+def cpu_baseline(P, A, plan, X, n_out, n_in, n_rows, W_seed_dev=None, g_seed=None):
+    """Time the oracle (C restatement, OpenMP over all host threads) on n_rows output rows x
+    all 65 792 columns x full K, both limbs + rescale; extrapolate to the full op."""
+    import torch
+
+    import oracle as O
+
+    g = torch.Generator(device=W_seed_dev).manual_seed(g_seed)
+    W = ((torch.rand((n_out, n_in), generator=g, device=W_seed_dev, dtype=torch.float64) * 2 - 1)
+         / math.sqrt(n_in))
+    W0 = W[: P.mlwe_rank].cpu().numpy()          # first row block
+    del W
+    Wt = O.encode_weights(P, W0)
+    ct = X.data.cpu().numpy().view(np.uint32)
+    n_rows = min(n_rows, P.mlwe_rank)
+    res = O.time_pcmm_sample(P, Wt, ct, n_rows)
+    per_op = res["seconds"] * n_out / n_rows * 1e3
+    return {"value": round(per_op, 1), "unit": "ms/op", "cores": res["threads"], "kind": "port",
+            "sample": f"oracle/ C restatement: {n_rows} of {n_out} output rows x {P.width} cols x K={n_in}, "
+                      f"both limbs + rescale, {res['seconds']:.2f} s, extrapolated x{n_out / n_rows:.0f}"}
+
+
+def run_reference(a, rank: int, world: int):
+    """--impl reference: the CPU restatement of the path (the reference package has no
+    implementation of it) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import oracle as O
+
+    P = params_of(a.params)
+    n_out, n_in = shape_of(a.shape)
+    k = P.mlwe_rank
+    rng = np.random.default_rng(20260117)
+    W0 = rng.uniform(-1, 1, (k, n_in)) / math.sqrt(n_in)
+    A = rng.uniform(-1, 1, (P.tokens, n_in))
+    s = O.keygen(P, 7)
+    ct = O.encrypt(P, 11, s, O.encode_acts(P, A))
+    Wt = O.encode_weights(P, W0)
+    rows = max(1, min(a.cpu_rows, k) // 4)
+    for _ in range(a.warmup):
+        O.pcmm(P, Wt, ct, rows=list(range(1)), cols=list(range(64)))
+    vals = []
+    for _ in range(a.steps):
+        res = O.time_pcmm_sample(P, Wt, ct, rows)
+        vals.append(res["seconds"] * n_out / rows * 1e3)
+    v = float(np.median(vals))
+    line = {
+        "metric": METRIC, "value": round(v, 1), "unit": "ms/op", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(v, 1), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "impl": "reference",
+        "data": "synthetic: W ~ U[-1,1)/sqrt(n_in), acts ~ U[-1,1) (seeded), fresh RLWE encryptions (CPU)",
+        "config": {"workload": WORKLOADS.get(a.shape, a.shape), "n_out": n_out, "n_in": n_in, "N": P.N,
+                   "mlwe": [P.mlwe_degree, P.mlwe_rank], "moduli": list(P.moduli)},
+        "cpu_baseline": {"value": round(v, 1), "unit": "ms/op", "cores": O.num_threads(), "kind": "port",
+                         "sample": f"per step {rows} of {n_out} output rows x {P.width} cols x K={n_in}, both "
+                                   f"limbs + rescale, extrapolated x{n_out / rows:.0f} (oracle/he_oracle.c, OpenMP)"},
+        "e2e": {"value": round(v, 1), "unit": "ms/op", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "hesim (the reference package) does not implement the MLWE PCMM (SPEC.md:8); the reference "
+                "arm times the CPU restatement of the path",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+    else:
+        run_ours(a, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

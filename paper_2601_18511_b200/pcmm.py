@@ -124,10 +124,12 @@ def _check_operand(ctx: HeContext, plan: MlwePcmmPlan, X) -> None:
         raise ValueError(f"ciphertext batch has shape {shape}")
 
 
-def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks | None = None) -> MlweBlocks:
+def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks | None = None,
+              gemm_events=None) -> MlweBlocks:
     """Level-1 RLWE block batch (encrypting A, (d/2) x n_in) -> level-0 MLWE blocks
     encrypting A @ W^T ((d/2) x n_out).  Exactly one level, one rescale per output block,
-    zero ciphertext rotations."""
+    zero ciphertext rotations.  ``gemm_events`` (two torch.cuda.Event) bracket the K1
+    launch on the current stream, for profiling."""
     torch = _torch()
     _check_operand(ctx, plan, X)
     p = ctx.params
@@ -137,13 +139,34 @@ def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks |
         out = MlweBlocks(out_b, out_a, level=X.level - 1, n_rows=plan.n_out)
     ws = plan.workspace(ctx.device)
     led = native.HeLedgerC()
-    native.call("he_pcmm_run", plan._handle, X.data.data_ptr(), X.level, out.out_b.data_ptr(), out.out_a.data_ptr(),
-                ws.data_ptr(), ws.numel(), ctx.stream(), ctypes.byref(led))
+    st = ctx.stream()
+    if gemm_events is None:
+        native.call("he_pcmm_run", plan._handle, X.data.data_ptr(), X.level, out.out_b.data_ptr(),
+                    out.out_a.data_ptr(), ws.data_ptr(), ws.numel(), st, ctypes.byref(led))
+    else:  # the same two launches as he_pcmm_run, with events around K1
+        native.call("he_pcmm_decompose", plan._handle, X.data.data_ptr(), ws.data_ptr(), ws.numel(), st)
+        gemm_events[0].record()
+        native.call("he_pcmm_gemm", plan._handle, ws.data_ptr(), out.out_b.data_ptr(), out.out_a.data_ptr(), st)
+        gemm_events[1].record()
+        k = ctx.params.mlwe_rank
+        led.pc_mults = (plan.n_out // k) * (plan.n_in // k)
+        led.rescales = plan.n_out // k
     ctx.ledger.add_c(led)
     ctx.ledger.observe_level(X.level - 1)
     out.level = X.level - 1
     out.n_rows = plan.n_out
     return out
+
+
+def pcmm_ops(params, n_out: int, n_in: int, d_w: int) -> int:
+    """Algorithmic int8 tensor-core ops of K1 per launch: 2 * n_out * n_in * width * d_w *
+    (D_0 + D_1) (every weight digit meets every ciphertext digit of both limbs once)."""
+    return 2 * n_out * n_in * params.width * d_w * (params.ct_digits(0) + params.ct_digits(1))
+
+
+def word_ops(params, n_out: int, n_in: int, limbs: int = 2) -> int:
+    """Word-level modular multiply-adds x 2: 2 * n_out * n_in * width * limbs."""
+    return 2 * n_out * n_in * params.width * limbs
 
 
 def clear_pcmm(weights, acts) -> np.ndarray:

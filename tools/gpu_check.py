@@ -97,6 +97,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--bench", action="store_true")
+    ap.add_argument("--time", action="store_true")
     a = ap.parse_args()
     print(torch.cuda.get_device_name(0))
     ok = run(HeParams.toy(), 48, 32)
@@ -110,5 +111,44 @@ def main():
     print("ALL OK" if ok else "FAILURES")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--time" not in sys.argv:
     main()
+
+
+def time_shape(n_out, n_in, iters=5):
+    import ctypes
+    from paper_2601_18511_b200 import native
+    P = HeParams.llama()
+    ctx = HeContext(P)
+    rng = np.random.default_rng(3)
+    A = rng.uniform(-1, 1, (P.tokens, n_in))
+    W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
+    sk = ctx.keygen(1)
+    X = ctx.encrypt_acts(sk, A, seed=2)
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    Y = pcmm_mlwe(ctx, plan, X)
+    torch.cuda.synchronize()
+    ws = plan.workspace(ctx.device)
+    st = ctx.stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tdec, tgemm = [], []
+    for _ in range(iters):
+        ev[0].record()
+        native.call("he_pcmm_decompose", plan._handle, X.data.data_ptr(), ws.data_ptr(), ws.numel(), st)
+        ev[1].record()
+        native.call("he_pcmm_gemm", plan._handle, ws.data_ptr(), Y.out_b.data_ptr(), Y.out_a.data_ptr(), st)
+        ev[2].record()
+        torch.cuda.synchronize()
+        tdec.append(ev[0].elapsed_time(ev[1]))
+        tgemm.append(ev[1].elapsed_time(ev[2]))
+    d0, d1 = P.ct_digits(0), P.ct_digits(1)
+    ops = 2 * n_out * n_in * P.width * plan.d_w * (d0 + d1)
+    g = min(tgemm)
+    print(f"shape {n_out}x{n_in}: d_w={plan.d_w} decompose {min(tdec):.3f} ms, gemm {g:.3f} ms "
+          f"-> {ops / g / 1e9:.1f} TOPS int8 ({ops/g/1e9/4500*100:.1f}% of 4.5 POPS); all {tgemm}")
+    ws_bytes = ws.numel()
+    print(f"  decompose writes {ws_bytes/1e9:.2f} GB -> {ws_bytes/min(tdec)/1e6:.0f} GB/s")
+
+
+if __name__ == "__main__" and "--time" in sys.argv:
+    time_shape(4096, 11008)
