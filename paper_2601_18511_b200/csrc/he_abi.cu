@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -338,8 +339,13 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
 extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_t* out_b, uint32_t* out_a,
                                   void* stream) {
   if (!p || !ws || !out_b || !out_a) return fail(HE_EINVAL, "null argument");
+  static int variant = [] {
+    const char* v = getenv("HE_GEMM_VARIANT");  // profiling switch: 1 = single-CTA kernel
+    return (v && v[0] == '1') ? 1 : 2;
+  }();
   CUtensorMap tmB;
-  he_status s = make_map(&tmB, ws, p->n_in, p->width, p->d0 + p->d1, 32);
+  const int bn2 = gemm2_tile_n((int)p->d_w, (int)p->d0, (int)p->d1);
+  he_status s = make_map(&tmB, ws, p->n_in, p->width, p->d0 + p->d1, variant == 1 ? kGemmBoxRows1 : bn2 / 2);
   if (s) return s;
   GemmArgs a;
   a.n_out = (int)p->n_out;
@@ -350,9 +356,17 @@ extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_
   a.out_b = out_b;
   a.out_a = out_a;
   a.c = p->epi;
-  const int tiles = (int)((p->n_out + 127) / 128) * (int)(p->width / 32);
-  const int grid = tiles < p->ctx->sm_count ? tiles : p->ctx->sm_count;
-  HE_CUDA(launch_modgemm((int)p->d_w, (int)p->d0, (int)p->d1, p->tmA, tmB, a, grid, (cudaStream_t)stream),
+  a.group_m = 8;
+  int grid;
+  if (variant == 1) {
+    const int tiles = (int)((p->n_out + 127) / 128) * (int)(p->width / 32);
+    grid = tiles < p->ctx->sm_count ? tiles : p->ctx->sm_count;
+  } else {
+    const int tiles = (int)((p->n_out + 255) / 256) * (int)((p->width + bn2 - 1) / bn2);
+    const int pairs = p->ctx->sm_count / 2;
+    grid = 2 * (tiles < pairs ? tiles : pairs);
+  }
+  HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, p->tmA, tmB, a, grid, (cudaStream_t)stream),
           "modgemm");
   return HE_OK;
 }

@@ -20,13 +20,17 @@ struct GemmEpiConst {
 
 struct GemmArgs {
   int n_out, n_in, width, d, k;
+  int group_m;          // raster: pair-rows per group (v2)
   uint32_t* out_b;
   uint32_t* out_a;
   GemmEpiConst c;
 };
 
 int gemm_smem_bytes(int dw, int d0, int d1);
-cudaError_t launch_modgemm(int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
+// variant 1: single-CTA 128x32 tiles; variant 2 (default): CTA pair, 256 x gemm2_tile_n tiles
+constexpr int kGemmBoxRows1 = 32;
+int gemm2_tile_n(int dw, int d0, int d1);
+cudaError_t launch_modgemm(int variant, int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmArgs& args, int grid, cudaStream_t stream);
 
 // NTT tables for one (modulus, degree)

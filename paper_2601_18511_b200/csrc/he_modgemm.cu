@@ -252,6 +252,279 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ======================================================================================
+// K1 v2: CTA pair (cta_group::2).  One pair-tile = 256 rows (128 per CTA) x 48 GEMM columns x
+// both limbs.  Each CTA stages its 128 weight rows (A) and HALF of every stacked ciphertext
+// operand (B, split along N between the pair), so the tensor cores of the two SMs share
+// operands and each SM reads ~80 B/clk of shared memory per MMA cycle instead of ~134.
+// The leader CTA issues all MMAs; commits are multicast to both CTAs' barriers.
+// 8 epilogue warps per CTA (two per TMEM lane quarter) halve the drain time of the single
+// accumulator buffer.  Raster: groups of kGroupM pair-rows sweep all N blocks, so the weight
+// planes of a group stay L2-resident while the ciphertext planes stream.
+constexpr int kEpiWarps = 8;
+constexpr int kThreads2 = 64 + 32 * kEpiWarps;
+
+// tile width: 48 GEMM columns when the shift accumulators fit TMEM (d_w <= 2), else 32
+__host__ __device__ constexpr int gemm2_bn(int dw, int d0, int d1) {
+  return ((2 * dw + d0 + d1 - 2) * 48 <= 512 && (dw + d0 - 1) * 48 <= 256 && (dw + d1 - 1) * 48 <= 256) ? 48 : 32;
+}
+
+template <int DW, int D0, int D1>
+struct Gemm2Cfg {
+  static constexpr int kBN2 = gemm2_bn(DW, D0, D1);
+  static constexpr int kChunk = kBN2 / 2;  // TMA box rows for B (half a digit plane)
+  static constexpr int S0 = DW + D0 - 1, S1 = DW + D1 - 1;
+  static constexpr int kTmemCols = (S0 + S1) * kBN2;
+  static constexpr int kTmemAlloc = 512;
+  static constexpr int kABytes = DW * kBM * kBK;                    // per CTA per stage
+  static constexpr int kB0Rows = D0 * kChunk, kB1Rows = D1 * kChunk; // per CTA (half of D_i * 48)
+  static constexpr int kBBytes = (kB0Rows + kB1Rows) * kBK;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (224 * 1024 - 9472) / kStageBytes > 6 ? 6 : (224 * 1024 - 9472) / kStageBytes;
+  static constexpr int kZeroBytes = 8192;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kZeroBytes + 1024 + 256;
+  static_assert(kTmemCols <= 512, "too many shift accumulators for TMEM");
+  static_assert(kStages >= 2, "not enough shared memory");
+  static_assert(S0 * kBN2 <= 256 && S1 * kBN2 <= 256, "zeroing MMA N out of range");
+};
+
+template <int DW, int D0, int D1>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
+    modgemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmArgs args) {
+  using C = Gemm2Cfg<DW, D0, D1>;
+  constexpr int kBN2 = C::kBN2;
+  constexpr int kChunk = C::kChunk;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint8_t* sZero = sB + C::kStages * C::kBBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sZero + C::kZeroBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tmem_full = empty + C::kStages;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int m_tiles = (args.n_out + 2 * kBM - 1) / (2 * kBM);
+  const int n_tiles = (args.width + kBN2 - 1) / kBN2;
+  const int num_tiles = m_tiles * n_tiles;
+  const int num_kb = (args.n_in + kBK - 1) / kBK;
+  const int gm = args.group_m < m_tiles ? args.group_m : m_tiles;
+
+  for (int i = threadIdx.x; i < C::kZeroBytes / 16; i += kThreads2)
+    reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 2);      // leader's expect_tx arrive + the peer's remote arrive
+      mbar_init(&empty[s], 1);     // one multicast commit
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 2 * kEpiWarps);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc_2sm(tmem_slot, C::kTmemAlloc);
+    tmem_relinquish_2sm();
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // tile -> (m block of 256 rows, n block of 48 columns), M-grouped raster
+  auto tile_mn = [&](int tile, int& m0, int& n0) {
+    const int per_group = gm * n_tiles;
+    const int g = tile / per_group, r = tile % per_group;
+    const int rows_in_group = (m_tiles - g * gm) < gm ? (m_tiles - g * gm) : gm;
+    m0 = (g * gm + r % rows_in_group) * (2 * kBM);
+    n0 = (r / rows_in_group) * kBN2;
+  };
+
+  if (warp == 0) {
+    // ======================= TMA producer (both CTAs) =======================
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full0_remote = mapa_rank(&full[0], 0);
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        int m0, n0;
+        tile_mn(tile, m0, n0);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+          else mbar_arrive_cluster(full0_remote + stage * 8);
+          uint8_t* a_dst = sA + stage * C::kABytes;
+          uint8_t* b_dst = sB + stage * C::kBBytes;
+#pragma unroll
+          for (int a = 0; a < DW; ++a)
+            tma_load_3d_2sm(a_dst + a * kBM * kBK, &tmA, &full[stage], kb * kBK, m0 + (int)rank * kBM, a, kEvictLast);
+          // stacked limb-0 operand [C0|C1|..] (D0*48 rows): this CTA holds chunks [rank*D0, rank*D0 + D0)
+#pragma unroll
+          for (int c = 0; c < D0; ++c) {
+            const int g = (int)rank * D0 + c;
+            tma_load_3d_2sm(b_dst + c * kChunk * kBK, &tmB, &full[stage], kb * kBK, n0 + (g & 1) * kChunk, g >> 1,
+                            kEvictFirst);
+          }
+#pragma unroll
+          for (int c = 0; c < D1; ++c) {
+            const int g = (int)rank * D1 + c;
+            tma_load_3d_2sm(b_dst + (C::kB0Rows + c * kChunk) * kBK, &tmB, &full[stage], kb * kBK,
+                            n0 + (g & 1) * kChunk, D0 + (g >> 1), kEvictFirst);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (leader CTA only) =======================
+    if (leader) {
+      constexpr uint32_t kIdesc0 = idesc_i8(2 * kBM, D0 * kBN2);
+      constexpr uint32_t kIdesc1 = idesc_i8(2 * kBM, D1 * kBN2);
+      constexpr uint32_t kIdescZ0 = idesc_i8(2 * kBM, C::S0 * kBN2);
+      constexpr uint32_t kIdescZ1 = idesc_i8(2 * kBM, C::S1 * kBN2);
+      const uint32_t reg0 = tmem_base;
+      const uint32_t reg1 = tmem_base + C::S0 * kBN2;
+      const uint64_t zdesc = desc_noswz(smem_u32(sZero), 128, 256);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++iter) {
+        if (iter > 0) mbar_wait(tmem_empty, (iter - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          mma_i8_2sm(reg0, zdesc, zdesc, kIdescZ0, 0);
+          mma_i8_2sm(reg1, zdesc, zdesc, kIdescZ1, 0);
+        }
+        __syncwarp();
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
+            const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+            for (int kk = 0; kk < kBK / 32; ++kk) {
+              const uint64_t b0 = desc_sw128(b_base + kk * 32);
+              const uint64_t b1 = desc_sw128(b_base + C::kB0Rows * kBK + kk * 32);
+#pragma unroll
+              for (int a = 0; a < DW; ++a) {
+                const uint64_t ad = desc_sw128(a_base + a * kBM * kBK + kk * 32);
+                mma_i8_2sm(reg0 + a * kBN2, ad, b0, kIdesc0, 1);
+                mma_i8_2sm(reg1 + a * kBN2, ad, b1, kIdesc1, 1);
+              }
+            }
+            tc_commit_2sm_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one()) tc_commit_2sm_mc(tmem_full, 0x3);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ======================= epilogue (both CTAs, 8 warps) =======================
+    const uint32_t ew = warp - 2;
+    const uint32_t quarter = warp & 3;
+    const uint32_t half = ew / 4;                      // which 3 of the 6 column chunks
+    const uint32_t lane_addr = (quarter * 32) << 16;
+    const int N = args.d * args.k;
+    const GemmEpiConst& c = args.c;
+    const uint32_t tmem_empty_remote = mapa_rank(tmem_empty, 0);
+    int iter = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs, ++iter) {
+      int m0, n0;
+      tile_mn(tile, m0, n0);
+      mbar_wait(tmem_full, iter & 1);
+      tc_fence_after();
+      const int y = m0 + (int)rank * kBM + (int)(quarter * 32 + lane);
+      const bool row_ok = y < args.n_out;
+#pragma unroll 1
+      for (int cc = 0; cc < kBN2 / 16; ++cc) {
+        const int c8 = (int)half * (kBN2 / 16) + cc;
+        const int n = n0 + c8 * 8;
+        if (n >= args.width) break;  // warp-uniform
+        uint32_t acc0[C::S0][8], acc1[C::S1][8];
+#pragma unroll
+        for (int s = 0; s < C::S0; ++s) tmem_ld_x8(tmem_base + lane_addr + s * kBN2 + c8 * 8, acc0[s]);
+#pragma unroll
+        for (int s = 0; s < C::S1; ++s) tmem_ld_x8(tmem_base + lane_addr + (C::S0 + s) * kBN2 + c8 * 8, acc1[s]);
+        tmem_ld_wait();
+        uint32_t res[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          uint32_t x0 = 0, x1 = 0;
+#pragma unroll
+          for (int s = 0; s < C::S0; ++s) {
+            const uint32_t v = acc0[s][e];
+            const uint32_t u = ((int32_t)v < 0) ? v + c.offs[0] : v;
+            x0 = add_mod(x0, shoup_mul(u, c.pw[0][s], c.pwp[0][s], c.q[0]), c.q[0]);
+          }
+#pragma unroll
+          for (int s = 0; s < C::S1; ++s) {
+            const uint32_t v = acc1[s][e];
+            const uint32_t u = ((int32_t)v < 0) ? v + c.offs[1] : v;
+            x1 = add_mod(x1, shoup_mul(u, c.pw[1][s], c.pwp[1][s], c.q[1]), c.q[1]);
+          }
+          uint32_t t;
+          if (x1 > (c.q[1] >> 1)) t = csub(x0 + (c.q[1] - x1), c.q[0]);
+          else t = sub_mod(x0, x1, c.q[0]);
+          res[e] = shoup_mul(t, c.q1inv, c.q1invp, c.q[0]);
+        }
+        if (row_ok) {
+          if (n < args.d) {
+            uint32_t* dst = args.out_b + (size_t)(y / args.k) * N + (y % args.k);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dst[(size_t)args.k * (n + e)] = res[e];
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(args.out_a + (size_t)y * N + (n - args.d));
+            dst[0] = make_uint4(res[0], res[1], res[2], res[3]);
+            dst[1] = make_uint4(res[4], res[5], res[6], res[7]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tmem_empty_remote);
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, C::kTmemAlloc);
+  }
+}
+
+template <int DW, int D0, int D1>
+static cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int grid,
+                             cudaStream_t stream) {
+  using C = Gemm2Cfg<DW, D0, D1>;
+  auto kern = modgemm2_kernel<DW, D0, D1>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kThreads2, C::kSmemBytes, stream>>>(tmA, tmB, args);
+  return cudaGetLastError();
+}
+
 template <int DW, int D0, int D1>
 static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int grid,
                             cudaStream_t stream) {
@@ -263,6 +536,8 @@ static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
   return cudaGetLastError();
 }
 
+int gemm2_tile_n(int dw, int d0, int d1) { return gemm2_bn(dw, d0, d1); }
+
 int gemm_smem_bytes(int dw, int d0, int d1) {
 #define HE_CASE(a, b, c) \
   if (dw == a && d0 == b && d1 == c) return GemmCfg<a, b, c>::kSmemBytes;
@@ -271,10 +546,12 @@ int gemm_smem_bytes(int dw, int d0, int d1) {
   return -1;
 }
 
-cudaError_t launch_modgemm(int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
+cudaError_t launch_modgemm(int variant, int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmArgs& args, int grid, cudaStream_t stream) {
-#define HE_CASE(a, b, c) \
-  if (dw == a && d0 == b && d1 == c) return launch_t<a, b, c>(tmA, tmB, args, grid, stream);
+#define HE_CASE(a, b, c)                                                                   \
+  if (dw == a && d0 == b && d1 == c)                                                      \
+    return variant == 1 ? launch_t<a, b, c>(tmA, tmB, args, grid, stream)                 \
+                        : launch2_t<a, b, c>(tmA, tmB, args, grid, stream);
   HE_GEMM_INSTANCES(HE_CASE)
 #undef HE_CASE
   return cudaErrorInvalidValue;
