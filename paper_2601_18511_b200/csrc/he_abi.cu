@@ -238,7 +238,6 @@ static he_status check_shape(const he_context* c, uint32_t n_out, uint32_t n_in)
   if (n_out == 0 || n_in == 0) return fail(HE_EINVAL, "empty weight matrix");
   if (n_out % c->R.k || n_in % c->R.k)
     return fail(HE_EINVAL, "dim mismatch: n_out (%u) and n_in (%u) must be multiples of k = %u", n_out, n_in, c->R.k);
-  if (n_in > 32768) return fail(HE_EINVAL, "n_in (%u) above the int32 accumulator bound 32768", n_in);
   return HE_OK;
 }
 
@@ -280,6 +279,25 @@ extern "C" he_status he_pcmm_plan_create(const he_context* c, const int8_t* digi
   const int d0 = digits_for(c->R.q[0]), d1 = digits_for(c->R.q[1]);
   if (gemm_smem_bytes((int)d_w, d0, d1) < 0)
     return fail(HE_EINVAL, "no GEMM instance for digits (%u, %d, %d)", d_w, d0, d1);
+  // exactness bounds of K1 (|digit product| <= 2^14):
+  //   int32 shift accumulator:    n_in * 2^14 * max_s pairs(s) < 2^31
+  //   int64 recombination (S<=5): n_in * 2^14 * sum_s pairs(s) 2^(8s) < 2^62
+  for (int L = 0; L < 2; ++L) {
+    const int dl = L ? d1 : d0, S = (int)d_w + dl - 1;
+    unsigned __int128 sum = 0;
+    int maxp = 0;
+    for (int sft = 0; sft < S; ++sft) {
+      int pairs = 0;
+      for (int a = 0; a < (int)d_w; ++a)
+        if (sft - a >= 0 && sft - a < dl) ++pairs;
+      maxp = pairs > maxp ? pairs : maxp;
+      sum += (unsigned __int128)pairs << (8 * sft);
+    }
+    if ((uint64_t)n_in * 16384ull * (uint64_t)maxp >= (1ull << 31))
+      return fail(HE_EINVAL, "n_in (%u) overflows the int32 digit accumulators at d_w = %u", n_in, d_w);
+    if (S <= 5 && (unsigned __int128)n_in * 16384u * sum >= ((unsigned __int128)1 << 62))
+      return fail(HE_EINVAL, "n_in (%u) overflows the int64 recombination at d_w = %u", n_in, d_w);
+  }
   he_pcmm_plan* p = new (std::nothrow) he_pcmm_plan();
   if (!p) return fail(HE_ENOMEM, "out of host memory");
   p->ctx = c;
@@ -305,6 +323,11 @@ extern "C" he_status he_pcmm_plan_create(const he_context* c, const int8_t* digi
       e.pw[L][sft] = w;
       e.pwp[L][sft] = shoup_pre(w, q);
     }
+  }
+  for (int L = 0; L < 2; ++L) {
+    const uint64_t q = c->R.q[L];
+    e.off64[L] = q * (((1ull << 62) + q - 1) / q);
+    e.mu[L] = (uint64_t)(((unsigned __int128)1 << 64) / q);
   }
   e.q1inv = (uint32_t)powmod_h(c->R.q[1] % c->R.q[0], c->R.q[0] - 2, c->R.q[0]);
   e.q1invp = shoup_pre(e.q1inv, c->R.q[0]);
@@ -344,7 +367,18 @@ extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_
     return (v && v[0] == '1') ? 1 : 2;
   }();
   CUtensorMap tmB;
-  const int bn2 = gemm2_tile_n((int)p->d_w, (int)p->d0, (int)p->d1);
+  // profiling knobs (defaults are the tuned choice): HE_GEMM_BN, HE_GEMM_GROUP_M, HE_GEMM_HINT_A/B
+  static const int env_bn = getenv("HE_GEMM_BN") ? atoi(getenv("HE_GEMM_BN")) : 0;
+  static const int env_gm = getenv("HE_GEMM_GROUP_M") ? atoi(getenv("HE_GEMM_GROUP_M")) : 0;
+  auto hint = [](const char* name, uint64_t dflt) -> uint64_t {
+    const char* v = getenv(name);
+    if (!v) return dflt;
+    if (v[0] == 'f') return 0x12F0000000000000ULL;  // evict_first
+    if (v[0] == 'l') return 0x14F0000000000000ULL;  // evict_last
+    return 0x1000000000000000ULL;                   // evict_normal
+  };
+  int bn2 = gemm2_tile_n((int)p->d_w, (int)p->d0, (int)p->d1);
+  if (env_bn == 32 || (env_bn == 48 && bn2 == 48)) bn2 = env_bn;
   he_status s = make_map(&tmB, ws, p->n_in, p->width, p->d0 + p->d1, variant == 1 ? kGemmBoxRows1 : bn2 / 2);
   if (s) return s;
   GemmArgs a;
@@ -356,7 +390,12 @@ extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_
   a.out_b = out_b;
   a.out_a = out_a;
   a.c = p->epi;
-  a.group_m = 8;
+  a.group_m = env_gm > 0 ? env_gm : 8;
+  a.tile_n = bn2;
+  static const int env_skip = getenv("HE_GEMM_EPI_SKIP") ? 1 : 0;
+  a.epi_skip = env_skip;
+  a.hint_a = hint("HE_GEMM_HINT_A", 0x14F0000000000000ULL);
+  a.hint_b = hint("HE_GEMM_HINT_B", 0x1000000000000000ULL);  // evict_normal: measured 46 vs 64 GB DRAM reads
   int grid;
   if (variant == 1) {
     const int tiles = (int)((p->n_out + 127) / 128) * (int)(p->width / 32);

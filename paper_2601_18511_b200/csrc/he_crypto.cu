@@ -52,17 +52,24 @@ __global__ void __launch_bounds__(256) decompose_kernel(const uint32_t* __restri
 #pragma unroll
     for (int L = 0; L < 2; ++L) {
       const uint32_t q = qs[L];
-      uint32_t packed[4] = {0, 0, 0, 0};
+      // balanced base-256 digits of the centred residue c: the bytes of (c + 0x80808080) ^ 0x80808080
+      // (adding 128 at every byte position turns balanced digits into plain bytes)
+      uint32_t w[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t t = t0 + e;
         const uint32_t v = rho == 0 ? bw[L * k + t] : win[L * 2 * k + (t + k - (rho - 1))];
-        int32_t c = v > (q >> 1) ? (int32_t)(v - q) : (int32_t)v;
-        int8_t dg[4];
-        balanced_digits4(c, dg, 4);
-#pragma unroll
-        for (int p = 0; p < 4; ++p) packed[p] |= ((uint32_t)(uint8_t)dg[p]) << (8 * e);
+        const uint32_t c = v > (q >> 1) ? v - q : v;          // two's complement of the centred value
+        w[e] = (c + 0x80808080u) ^ 0x80808080u;
       }
+      // 4x4 byte transpose: packed[p] byte e = digit p of value e
+      const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140), hi01 = __byte_perm(w[0], w[1], 0x7362);
+      const uint32_t lo23 = __byte_perm(w[2], w[3], 0x5140), hi23 = __byte_perm(w[2], w[3], 0x7362);
+      uint32_t packed[4];
+      packed[0] = __byte_perm(lo01, lo23, 0x5410);
+      packed[1] = __byte_perm(lo01, lo23, 0x7632);
+      packed[2] = __byte_perm(hi01, hi23, 0x5410);
+      packed[3] = __byte_perm(hi01, hi23, 0x7632);
       const int nd = L == 0 ? d0 : d1;
       const int pbase = L == 0 ? 0 : d0;
       for (int p = 0; p < nd; ++p) {

@@ -16,11 +16,16 @@ struct GemmEpiConst {
   uint32_t pw[2][8];    // 2^(8 s) mod q
   uint32_t pwp[2][8];   // Shoup companions
   uint32_t q1inv, q1invp;
+  uint64_t off64[2];    // q * ceil(2^62 / q): maps the signed int64 recombination into [0, 2^64)
+  uint64_t mu[2];       // floor(2^64 / q) (Barrett)
 };
 
 struct GemmArgs {
   int n_out, n_in, width, d, k;
   int group_m;          // raster: pair-rows per group (v2)
+  int tile_n;           // v2 tile width (48 or 32)
+  uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints
+  int epi_skip;         // profiling only: drain TMEM without computing/storing
   uint32_t* out_b;
   uint32_t* out_a;
   GemmEpiConst c;

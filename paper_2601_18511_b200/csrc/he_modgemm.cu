@@ -269,9 +269,33 @@ __host__ __device__ constexpr int gemm2_bn(int dw, int d0, int d1) {
   return ((2 * dw + d0 + d1 - 2) * 48 <= 512 && (dw + d0 - 1) * 48 <= 256 && (dw + d1 - 1) * 48 <= 256) ? 48 : 32;
 }
 
-template <int DW, int D0, int D1>
+// sum_s 2^(8 s) acc_s mod q for one output word.  S <= 5: exact signed int64 sum (plan-time
+// bound K 2^14 sum_s pairs(s) 2^(8s) < 2^62) and one Barrett reduction; else per-shift Shoup.
+template <int S>
+__device__ __forceinline__ uint32_t recombine(const uint32_t (*acc)[8], int e, const GemmEpiConst& c, int L) {
+  const uint32_t q = c.q[L];
+  if constexpr (S <= 5) {
+    int64_t v = (int32_t)acc[0][e];
+#pragma unroll
+    for (int s = 1; s < S; ++s) v += (int64_t)(int32_t)acc[s][e] << (8 * s);
+    const uint64_t u = (uint64_t)v + c.off64[L];
+    const uint64_t qh = __umul64hi(u, c.mu[L]);
+    return csub((uint32_t)(u - qh * q), q);
+  } else {
+    uint32_t x = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const uint32_t v = acc[s][e];
+      const uint32_t u = ((int32_t)v < 0) ? v + c.offs[L] : v;
+      x = add_mod(x, shoup_mul(u, c.pw[L][s], c.pwp[L][s], q), q);
+    }
+    return x;
+  }
+}
+
+template <int DW, int D0, int D1, int BN>
 struct Gemm2Cfg {
-  static constexpr int kBN2 = gemm2_bn(DW, D0, D1);
+  static constexpr int kBN2 = BN;
   static constexpr int kChunk = kBN2 / 2;  // TMA box rows for B (half a digit plane)
   static constexpr int S0 = DW + D0 - 1, S1 = DW + D1 - 1;
   static constexpr int kTmemCols = (S0 + S1) * kBN2;
@@ -288,11 +312,11 @@ struct Gemm2Cfg {
   static_assert(S0 * kBN2 <= 256 && S1 * kBN2 <= 256, "zeroing MMA N out of range");
 };
 
-template <int DW, int D0, int D1>
+template <int DW, int D0, int D1, int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     modgemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmArgs args) {
-  using C = Gemm2Cfg<DW, D0, D1>;
+  using C = Gemm2Cfg<DW, D0, D1, BN>;
   constexpr int kBN2 = C::kBN2;
   constexpr int kChunk = C::kChunk;
   extern __shared__ uint8_t smem_raw[];
@@ -367,19 +391,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           uint8_t* b_dst = sB + stage * C::kBBytes;
 #pragma unroll
           for (int a = 0; a < DW; ++a)
-            tma_load_3d_2sm(a_dst + a * kBM * kBK, &tmA, &full[stage], kb * kBK, m0 + (int)rank * kBM, a, kEvictLast);
+            tma_load_3d_2sm(a_dst + a * kBM * kBK, &tmA, &full[stage], kb * kBK, m0 + (int)rank * kBM, a, args.hint_a);
           // stacked limb-0 operand [C0|C1|..] (D0*48 rows): this CTA holds chunks [rank*D0, rank*D0 + D0)
 #pragma unroll
           for (int c = 0; c < D0; ++c) {
             const int g = (int)rank * D0 + c;
             tma_load_3d_2sm(b_dst + c * kChunk * kBK, &tmB, &full[stage], kb * kBK, n0 + (g & 1) * kChunk, g >> 1,
-                            kEvictFirst);
+                            args.hint_b);
           }
 #pragma unroll
           for (int c = 0; c < D1; ++c) {
             const int g = (int)rank * D1 + c;
             tma_load_3d_2sm(b_dst + (C::kB0Rows + c * kChunk) * kBK, &tmB, &full[stage], kb * kBK,
-                            n0 + (g & 1) * kChunk, D0 + (g >> 1), kEvictFirst);
+                            n0 + (g & 1) * kChunk, D0 + (g >> 1), args.hint_b);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -466,22 +490,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 #pragma unroll
         for (int s = 0; s < C::S1; ++s) tmem_ld_x8(tmem_base + lane_addr + (C::S0 + s) * kBN2 + c8 * 8, acc1[s]);
         tmem_ld_wait();
+        if (args.epi_skip) continue;
         uint32_t res[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          uint32_t x0 = 0, x1 = 0;
-#pragma unroll
-          for (int s = 0; s < C::S0; ++s) {
-            const uint32_t v = acc0[s][e];
-            const uint32_t u = ((int32_t)v < 0) ? v + c.offs[0] : v;
-            x0 = add_mod(x0, shoup_mul(u, c.pw[0][s], c.pwp[0][s], c.q[0]), c.q[0]);
-          }
-#pragma unroll
-          for (int s = 0; s < C::S1; ++s) {
-            const uint32_t v = acc1[s][e];
-            const uint32_t u = ((int32_t)v < 0) ? v + c.offs[1] : v;
-            x1 = add_mod(x1, shoup_mul(u, c.pw[1][s], c.pwp[1][s], c.q[1]), c.q[1]);
-          }
+          const uint32_t x0 = recombine<C::S0>(acc0, e, c, 0);
+          const uint32_t x1 = recombine<C::S1>(acc1, e, c, 1);
           uint32_t t;
           if (x1 > (c.q[1] >> 1)) t = csub(x0 + (c.q[1] - x1), c.q[0]);
           else t = sub_mod(x0, x1, c.q[0]);
@@ -514,11 +528,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   }
 }
 
-template <int DW, int D0, int D1>
+template <int DW, int D0, int D1, int BN>
 static cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int grid,
                              cudaStream_t stream) {
-  using C = Gemm2Cfg<DW, D0, D1>;
-  auto kern = modgemm2_kernel<DW, D0, D1>;
+  using C = Gemm2Cfg<DW, D0, D1, BN>;
+  auto kern = modgemm2_kernel<DW, D0, D1, BN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads2, C::kSmemBytes, stream>>>(tmA, tmB, args);
@@ -549,9 +563,13 @@ int gemm_smem_bytes(int dw, int d0, int d1) {
 cudaError_t launch_modgemm(int variant, int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmArgs& args, int grid, cudaStream_t stream) {
 #define HE_CASE(a, b, c)                                                                   \
-  if (dw == a && d0 == b && d1 == c)                                                      \
-    return variant == 1 ? launch_t<a, b, c>(tmA, tmB, args, grid, stream)                 \
-                        : launch2_t<a, b, c>(tmA, tmB, args, grid, stream);
+  if (dw == a && d0 == b && d1 == c) {                                                    \
+    if (variant == 1) return launch_t<a, b, c>(tmA, tmB, args, grid, stream);            \
+    if constexpr (gemm2_bn(a, b, c) == 48)                                                \
+      if (args.tile_n == 48) return launch2_t<a, b, c, 48>(tmA, tmB, args, grid, stream); \
+    if (args.tile_n == 32) return launch2_t<a, b, c, 32>(tmA, tmB, args, grid, stream);   \
+    return cudaErrorInvalidValue;                                                         \
+  }
   HE_GEMM_INSTANCES(HE_CASE)
 #undef HE_CASE
   return cudaErrorInvalidValue;
