@@ -102,7 +102,8 @@ extern "C" he_status he_context_create(const he_params* p, he_context** out) {
   const uint32_t N = d * k;
   for (int i = 0; i < 2; ++i) {
     uint32_t q = p->moduli[i];
-    if (q < 3 || q >= (1u << 31) || (q - 1) % (2ull * N)) return fail(HE_EINVAL, "modulus %u not NTT-friendly", q);
+    if (q < 3 || q >= (1u << 30) || (q - 1) % (2ull * N))
+      return fail(HE_EINVAL, "modulus %u must be an NTT-friendly prime below 2^30", q);
   }
   if (p->moduli[1] / 2 >= p->moduli[0]) return fail(HE_EINVAL, "q1/2 must be below q0");
   if (p->log_delta < 1 || p->log_delta > 40) return fail(HE_EINVAL, "log_delta out of range");

@@ -10,7 +10,8 @@ limbs q_0..q_l; the PCMM input sits at level 1 (two limbs) and t
 op consumes exactly one level by rescaling away q_1.
 
 Prime choice (the paper does not pin it; SURVEY.md §7 "Choosing Delta_w"):
-  q_0  the base prime, < 2^31 so a centred residue fits int32 (4 signed 8-bit digits);
+  q_0  the base prime, < 2^30: a centred residue takes 4 signed 8-bit digits, and the NTT can run
+       Harvey-lazy butterflies (values in [0, 4q) fit a u32);
   q_1  the PCMM *scale prime*, Delta_w = q_1 exactly, so the output scale equals the
        input scale Delta after the rescale.  The default q_1 ~ 2^20 gives ~15-16
        bits of weight precision for Llama-scale weights (|W| < 2^-6), above the
@@ -81,7 +82,7 @@ class HeParams:
 
     mlwe_degree: int = 256
     mlwe_rank: int = 256
-    moduli: tuple[int, ...] = (2147352577, 1179649)
+    moduli: tuple[int, ...] = (1073479681, 1179649)
     log_delta: int = 26
     rhombus_degree: int = 4096
     seed: int | None = None
@@ -100,8 +101,8 @@ class HeParams:
                 raise ValueError(f"modulus {q} is not prime")
             if (q - 1) % (2 * self.N):
                 raise ValueError(f"modulus {q} is not 1 mod 2N = {2 * self.N}")
-            if q >= 1 << 31:
-                raise ValueError(f"modulus {q} must be below 2^31")
+            if q >= 1 << 30:
+                raise ValueError(f"modulus {q} must be below 2^30 (lazy NTT butterflies)")
         if len(set(self.moduli)) != len(self.moduli):
             raise ValueError("moduli must be distinct")
         if not 1 <= self.log_delta <= 40:
@@ -167,13 +168,13 @@ class HeParams:
     # -- presets ----------------------------------------------------------
     @classmethod
     def llama(cls, **kw) -> "HeParams":
-        """N = 2^16, MLWE (256, 256); q0 < 2^31, q1 ~ 2^20 (the bench / metric preset)."""
+        """N = 2^16, MLWE (256, 256); q0 < 2^30, q1 ~ 2^20 (the bench / metric preset)."""
         return cls(**kw)
 
     @classmethod
     def wide(cls, **kw) -> "HeParams":
-        """N = 2^16 with two ~31-bit primes (4 + 4 ciphertext digits, 4 weight digits)."""
-        kw.setdefault("moduli", tuple(ntt_primes(2 * 65536, 1 << 31, 2)))
+        """N = 2^16 with two ~30-bit primes (4 + 4 ciphertext digits, 4 weight digits)."""
+        kw.setdefault("moduli", tuple(ntt_primes(2 * 65536, 1 << 30, 2)))
         kw.setdefault("name", "wide")
         return cls(**kw)
 
@@ -183,7 +184,7 @@ class HeParams:
         (SURVEY.md §8c), 16-column ciphertext batch like hesim's d=16 PCMM."""
         kw.setdefault("mlwe_degree", 32)
         kw.setdefault("mlwe_rank", 16)
-        kw.setdefault("moduli", (ntt_primes(1024, 1 << 31, 1)[0], ntt_primes(1024, 1 << 21, 1)[0]))
+        kw.setdefault("moduli", (ntt_primes(1024, 1 << 30, 1)[0], ntt_primes(1024, 1 << 21, 1)[0]))
         kw.setdefault("rhombus_degree", 128)
         kw.setdefault("name", "toy")
         return cls(**kw)

@@ -130,9 +130,11 @@ def test_params_validation_and_json_roundtrip(tmp_path):
     with pytest.raises(ValueError, match="unknown"):
         HeParams.from_dict({"slot_count": 4})
     with pytest.raises(ValueError):
-        HeParams(moduli=(2147352577, 2147352577))
+        HeParams(moduli=(1073479681, 1073479681))
     with pytest.raises(ValueError):
-        HeParams(moduli=(2147352577, 1000003))  # not 1 mod 2N
+        HeParams(moduli=(1073479681, 1000003))  # not 1 mod 2N
+    with pytest.raises(ValueError):
+        HeParams(moduli=(2147352577, 1179649))  # >= 2^30
     assert HeParams.wide().ct_digits(1) == 4
     assert signed_digits(127) == 1 and signed_digits(128) == 2 and signed_digits(18432) == 2
 

@@ -96,7 +96,7 @@ def test_toy_wide_weights_use_more_digits():
 
 
 def test_wide_params_four_digit_limbs():
-    P = HeParams.wide(mlwe_degree=32, mlwe_rank=16, moduli=(2147473409, 2147415041), rhombus_degree=128)
+    P = HeParams.wide(mlwe_degree=32, mlwe_rank=16, moduli=(1073738753, 1073732609), rhombus_degree=128)
     ctx, sk, A, W, X = setup(P, 32, 48)
     plan = make_mlwe_pcmm_plan(ctx, W)
     assert P.ct_digits(1) == 4
