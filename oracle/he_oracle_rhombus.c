@@ -1,0 +1,379 @@
+/*
+ * he_oracle_rhombus.c -- CPU restatement of the Rhombus PCMv path (TEST INFRASTRUCTURE ONLY).
+ *
+ * PARITY UNPINNED: hesim does not implement the PCMv; the paper gives only the step
+ * list and the weight shuffle h (bitrev.py:48-54).  This file
+ * restates, in plain exact modular arithmetic, the algorithm the CUDA path implements:
+ *
+ *  (D) decompose: one hybrid key switch (dnum = 2 RNS digits, special prime P) of the degree-N
+ *      ciphertext from s to the sparse key s'(X^rho), rho = N/N', after which the X^rho index
+ *      split is a free map to rho RLWE-N' ciphertexts under s';
+ *  (M) MVM: coefficient-encoded inner products -- for output row r and input piece p the
+ *      plaintext w_{r,p}(Z) = c_pack * sum_k W~[r][N' p + h(k)] Z^{-k} puts <row r, piece p> in the
+ *      constant coefficient of w_{r,p} * piece_p; products are summed over pieces;
+ *  (P) output packing: PackLWEs (Chen-Dai-Kim-Song 2021) over the N' row ciphertexts of an output
+ *      piece -- log2 N' levels of  E + X^{N'/2^l} O + sigma_{2^l+1}(E - X^{N'/2^l} O), each
+ *      automorphism followed by a Galois key switch; c_pack = N'^-1 cancels the 2^l growth;
+ *  (R) rescale by q1 (one level), (C) compose: the free X^rho interleave.
+ *
+ * Vector layout (App. A with h): element e of the input / output vector sits in piece p = e / N',
+ * piece coefficient k with h(k) = e mod N', i.e. degree-N coefficient p + rho k.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+uint64_t or_rng_key(uint64_t seed, uint64_t stream);
+void or_sample_uniform(uint64_t seed, uint64_t stream, uint32_t q, uint32_t* out, int64_t n);
+void or_sample_cbd(uint64_t seed, uint64_t stream, int32_t* out, int64_t n);
+void or_sample_ternary(uint64_t seed, uint64_t stream, int32_t* out, int64_t n);
+int or_negacyclic_mul(const uint32_t* a, const int32_t* s, uint32_t N, uint32_t q, uint32_t* out);
+
+#define STREAM_SECRET_RH 0x5EC1000000000000ULL
+#define STREAM_KSK_A(id, i, j) (0xC000000000000000ULL | ((uint64_t)(id) << 16) | ((uint64_t)(i) << 8) | (uint64_t)(j))
+#define STREAM_KSK_E(id, i) (0xCE00000000000000ULL | ((uint64_t)(id) << 16) | ((uint64_t)(i) << 8))
+
+static inline uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)((u128)a * b % q); }
+static uint64_t powmod(uint64_t a, uint64_t e, uint64_t q) {
+  uint64_t r = 1 % q;
+  a %= q;
+  while (e) {
+    if (e & 1) r = mulmod(r, a, q);
+    a = mulmod(a, a, q);
+    e >>= 1;
+  }
+  return r;
+}
+static inline uint32_t modq_i64(int64_t v, uint32_t q) {
+  int64_t r = v % (int64_t)q;
+  return (uint32_t)(r < 0 ? r + q : r);
+}
+static int ilog2u(uint32_t x) {
+  int l = 0;
+  while ((1u << l) < x) ++l;
+  return l;
+}
+static uint32_t brev(uint32_t x, int bits) {
+  uint32_t r = 0;
+  for (int t = 0; t < bits; ++t) r |= ((x >> t) & 1u) << (bits - 1 - t);
+  return r;
+}
+/* h of PAPER.md:676-680 generalised to degree n: fix the top bit, reverse the others */
+uint32_t or_half_reverse(uint32_t x, uint32_t n) {
+  int l = ilog2u(n) - 1;
+  return (x & (n >> 1)) | brev(x & ((n >> 1) - 1), l);
+}
+
+/* product of a residue poly with a residue poly (both in [0,q)) via the signed NTT helper */
+static void polymul(const uint32_t* a, const uint32_t* b, uint32_t n, uint32_t q, uint32_t* out) {
+  int32_t* bs = (int32_t*)malloc(sizeof(int32_t) * n);
+  /* or_negacyclic_mul takes a signed second operand; centre b (|b| < q/2 < 2^29 fits int32) */
+  for (uint32_t i = 0; i < n; ++i) bs[i] = b[i] > q / 2 ? (int32_t)((int64_t)b[i] - q) : (int32_t)b[i];
+  or_negacyclic_mul(a, bs, n, q, out);
+  free(bs);
+}
+
+/* sigma_k(p)(X) = p(X^k) in Z_q[X]/(X^n+1), k odd */
+void or_automorphism(const uint32_t* p, uint32_t n, uint32_t k, uint32_t q, uint32_t* out) {
+  for (uint32_t i = 0; i < n; ++i) {
+    uint64_t j = ((uint64_t)i * k) % (2ull * n);
+    if (j < n) out[j] = p[i];
+    else out[j - n] = p[i] ? q - p[i] : 0;
+  }
+}
+/* X^e * p (0 <= e < 2n) */
+static void monomial_mul(const uint32_t* p, uint32_t n, uint32_t e, uint32_t q, uint32_t* out) {
+  for (uint32_t i = 0; i < n; ++i) {
+    uint64_t j = (uint64_t)i + e;
+    int neg = 0;
+    while (j >= n) {
+      j -= n;
+      neg ^= 1;
+    }
+    out[j] = (neg && p[i]) ? q - p[i] : p[i];
+  }
+}
+
+/*
+ * Hybrid key-switching key from s_old to s_new (degree n; moduli m[0..2] = q0, q1, P):
+ *   ksk[i][0][j] = alpha_{i,j} (uniform),  ksk[i][1][j] = -alpha s_new + g_{i,j} s_old + e_i  (mod m_j)
+ *   g_{i,j} = P * Qhat_i (mod m_j): nonzero only for j == i (Qhat_0 = q1, Qhat_1 = q0).
+ * Layout: ksk[((i * 2 + part) * 3 + j) * n + c].
+ */
+void or_ksk_gen(uint64_t seed, uint32_t id, const int32_t* s_old, const int32_t* s_new, uint32_t n, const uint32_t* m,
+                uint32_t* ksk) {
+  int32_t* e = (int32_t*)malloc(sizeof(int32_t) * n);
+  uint32_t* as = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  for (uint32_t i = 0; i < 2; ++i) {
+    or_sample_cbd(seed, STREAM_KSK_E(id, i), e, n);
+    for (uint32_t j = 0; j < 3; ++j) {
+      const uint32_t q = m[j];
+      uint32_t* alpha = ksk + ((size_t)(i * 2 + 0) * 3 + j) * n;
+      uint32_t* beta = ksk + ((size_t)(i * 2 + 1) * 3 + j) * n;
+      or_sample_uniform(seed, STREAM_KSK_A(id, i, j), q, alpha, n);
+      or_negacyclic_mul(alpha, s_new, n, q, as);
+      uint64_t g = 0;
+      if (j == i) g = mulmod(m[2] % q, m[1 - i] % q, q);
+      for (uint32_t c = 0; c < n; ++c) {
+        uint64_t v = (uint64_t)(q - as[c]) + modq_i64(e[c], q) + mulmod(g, modq_i64(s_old[c], q), q);
+        beta[c] = (uint32_t)(v % q);
+      }
+    }
+  }
+  free(e);
+  free(as);
+}
+
+/*
+ * Key switch of c (2 limbs, coefficient form, [limb][n]) with ksk -> (u, w) [limb][n] mod q0, q1:
+ *   d_i = c_i * [Qhat_i^-1]_{q_i} mod q_i  (RNS digit, integer in [0, q_i))
+ *   U_j = sum_i d_i * alpha_{i,j},  W_j = sum_i d_i * beta_{i,j}   (mod m_j, j = q0, q1, P)
+ *   ModDown: x_j = (X_j - [X_P]_centred) * P^-1 mod q_j
+ * so that w + u s_new = c s_old + small.
+ */
+void or_keyswitch(const uint32_t* c, const uint32_t* ksk, uint32_t n, const uint32_t* m, uint32_t* u, uint32_t* w) {
+  uint32_t* d[2];
+  uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint32_t* dl = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint32_t* U = (uint32_t*)calloc((size_t)3 * n, sizeof(uint32_t));
+  uint32_t* W = (uint32_t*)calloc((size_t)3 * n, sizeof(uint32_t));
+  for (int i = 0; i < 2; ++i) {
+    d[i] = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    const uint32_t qi = m[i];
+    const uint64_t inv = powmod(m[1 - i] % qi, qi - 2, qi);
+    for (uint32_t k = 0; k < n; ++k) d[i][k] = (uint32_t)mulmod(c[(size_t)i * n + k], inv, qi);
+  }
+  for (int j = 0; j < 3; ++j) {
+    const uint32_t q = m[j];
+    for (int i = 0; i < 2; ++i) {
+      for (uint32_t k = 0; k < n; ++k) dl[k] = d[i][k] % q;
+      polymul(dl, ksk + ((size_t)(i * 2 + 0) * 3 + j) * n, n, q, t);
+      for (uint32_t k = 0; k < n; ++k) U[(size_t)j * n + k] = (uint32_t)(((uint64_t)U[(size_t)j * n + k] + t[k]) % q);
+      polymul(dl, ksk + ((size_t)(i * 2 + 1) * 3 + j) * n, n, q, t);
+      for (uint32_t k = 0; k < n; ++k) W[(size_t)j * n + k] = (uint32_t)(((uint64_t)W[(size_t)j * n + k] + t[k]) % q);
+    }
+  }
+  const uint32_t P = m[2];
+  for (int j = 0; j < 2; ++j) {
+    const uint32_t q = m[j];
+    const uint64_t pinv = powmod(P % q, q - 2, q);
+    for (uint32_t k = 0; k < n; ++k) {
+      int64_t up = U[2 * (size_t)n + k], wp = W[2 * (size_t)n + k];
+      if (up > P / 2) up -= P;
+      if (wp > P / 2) wp -= P;
+      u[(size_t)j * n + k] = (uint32_t)mulmod(modq_i64((int64_t)U[(size_t)j * n + k] - up, q), pinv, q);
+      w[(size_t)j * n + k] = (uint32_t)mulmod(modq_i64((int64_t)W[(size_t)j * n + k] - wp, q), pinv, q);
+    }
+  }
+  free(d[0]);
+  free(d[1]);
+  free(t);
+  free(dl);
+  free(U);
+  free(W);
+}
+
+/* sparse small secret s' (degree n_small) and its embedding s'(X^rho) (degree N) */
+void or_rhombus_secret(uint64_t seed, uint32_t n_small, uint32_t N, int32_t* s_small, int32_t* s_up) {
+  or_sample_ternary(seed, STREAM_SECRET_RH, s_small, n_small);
+  memset(s_up, 0, sizeof(int32_t) * N);
+  const uint32_t rho = N / n_small;
+  for (uint32_t k = 0; k < n_small; ++k) s_up[(size_t)rho * k] = s_small[k];
+}
+
+/* Galois key of sigma_k: from sigma_k(s') to s'  (id = 1 + log2(k - 1)) */
+void or_galois_ksk(uint64_t seed, uint32_t level, const int32_t* s_small, uint32_t n, const uint32_t* m, uint32_t* ksk) {
+  const uint32_t k = (1u << level) + 1;
+  int32_t* ss = (int32_t*)malloc(sizeof(int32_t) * n);
+  for (uint32_t i = 0; i < n; ++i) {
+    uint64_t j = ((uint64_t)i * k) % (2ull * n);
+    if (j < n) ss[j] = s_small[i];
+    else ss[j - n] = -s_small[i];
+  }
+  or_ksk_gen(seed, 1 + level, ss, s_small, n, m, ksk);
+  free(ss);
+}
+
+/* ciphertext helpers: ct = [limb][2 (a, b)][n] */
+static void ct_apply_sigma_ks(const uint32_t* ct, uint32_t n, uint32_t k, const uint32_t* ksk, const uint32_t* m,
+                              uint32_t* out) {
+  uint32_t* sa = (uint32_t*)malloc(sizeof(uint32_t) * 2 * n);
+  uint32_t* sb = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint32_t* u = (uint32_t*)malloc(sizeof(uint32_t) * 2 * n);
+  uint32_t* w = (uint32_t*)malloc(sizeof(uint32_t) * 2 * n);
+  for (int L = 0; L < 2; ++L) or_automorphism(ct + ((size_t)L * 2 + 0) * n, n, k, m[L], sa + (size_t)L * n);
+  or_keyswitch(sa, ksk, n, m, u, w);
+  for (int L = 0; L < 2; ++L) {
+    or_automorphism(ct + ((size_t)L * 2 + 1) * n, n, k, m[L], sb);
+    for (uint32_t i = 0; i < n; ++i) {
+      out[((size_t)L * 2 + 0) * n + i] = u[(size_t)L * n + i];
+      out[((size_t)L * 2 + 1) * n + i] = (uint32_t)(((uint64_t)sb[i] + w[(size_t)L * n + i]) % m[L]);
+    }
+  }
+  free(sa);
+  free(sb);
+  free(u);
+  free(w);
+}
+
+/* PackLWEs, recursive (CDKS21): v = list of 2^l cts (each [2][2][n]) with stride `step` in `base`. */
+static void pack_rec(const uint32_t* const* v, uint32_t count, uint32_t step, uint32_t n, const uint32_t* const* gal,
+                     const uint32_t* m, uint32_t* out) {
+  const size_t cw = (size_t)4 * n;
+  if (count == 1) {
+    memcpy(out, v[0], sizeof(uint32_t) * cw);
+    return;
+  }
+  const uint32_t half = count / 2;
+  const uint32_t** ev = (const uint32_t**)malloc(sizeof(void*) * half);
+  const uint32_t** od = (const uint32_t**)malloc(sizeof(void*) * half);
+  for (uint32_t i = 0; i < half; ++i) {
+    ev[i] = v[2 * i];
+    od[i] = v[2 * i + 1];
+  }
+  uint32_t* E = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  uint32_t* O = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  pack_rec(ev, half, step, n, gal, m, E);
+  pack_rec(od, half, step, n, gal, m, O);
+  const int l = ilog2u(count);
+  const uint32_t e = n >> l;  /* X^{n / 2^l} */
+  uint32_t* MO = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  uint32_t* T = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  uint32_t* ST = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  for (int L = 0; L < 2; ++L)
+    for (int ab = 0; ab < 2; ++ab)
+      monomial_mul(O + ((size_t)L * 2 + ab) * n, n, e, m[L], MO + ((size_t)L * 2 + ab) * n);
+  for (int L = 0; L < 2; ++L)
+    for (size_t i = 0; i < (size_t)2 * n; ++i) {
+      size_t x = (size_t)L * 2 * n + i;
+      T[x] = (uint32_t)(((uint64_t)E[x] + m[L] - MO[x]) % m[L]);
+    }
+  ct_apply_sigma_ks(T, n, (1u << l) + 1, gal[l - 1], m, ST);
+  for (int L = 0; L < 2; ++L)
+    for (size_t i = 0; i < (size_t)2 * n; ++i) {
+      size_t x = (size_t)L * 2 * n + i;
+      out[x] = (uint32_t)(((uint64_t)E[x] + MO[x] + ST[x]) % m[L]);
+    }
+  free(ev);
+  free(od);
+  free(E);
+  free(O);
+  free(MO);
+  free(T);
+  free(ST);
+}
+
+/*
+ * Full Rhombus PCMv.
+ *   ct_in  [2 limbs][2][N]           level-1 input under s
+ *   ksk_dec [2][2][3][N]            key from s to s'(X^rho)
+ *   gal     [log2 n][2][2][3][n]     Galois keys sigma_{2^l+1}, l = 1..log2 n
+ *   Wt      int64 [n_out][n_in]      W~ = round(q1 W) (unshuffled; h is applied here)
+ * outputs: pieces_out [p_out][2][n] level-1 packed pieces before rescale (optional, may be NULL),
+ *          out [N] x 2 (a, b) level 0 under s'(X^rho)  -> out[0..N) = a, out[N..2N) = b.
+ */
+int or_rhombus_pcmv(uint32_t N, uint32_t n, const uint32_t* m, const uint32_t* ct_in, const uint32_t* ksk_dec,
+                    const uint32_t* gal, const int64_t* Wt, uint32_t n_out, uint32_t n_in, uint32_t* pieces_out,
+                    uint32_t* out) {
+  const uint32_t rho = N / n, p_in = (n_in + n - 1) / n, p_out = (n_out + n - 1) / n;
+  const int lg = ilog2u(n);
+  const size_t cw = (size_t)4 * n;
+  /* (D) key switch to s'(X^rho), then split */
+  uint32_t* u = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+  uint32_t* w = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+  uint32_t* a_in = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+  for (int L = 0; L < 2; ++L) memcpy(a_in + (size_t)L * N, ct_in + ((size_t)L * 2 + 0) * N, sizeof(uint32_t) * N);
+  or_keyswitch(a_in, ksk_dec, N, m, u, w);
+  uint32_t* pieces = (uint32_t*)malloc(sizeof(uint32_t) * cw * p_in);
+  for (uint32_t p = 0; p < p_in; ++p)
+    for (int L = 0; L < 2; ++L)
+      for (uint32_t k = 0; k < n; ++k) {
+        const size_t c = p + (size_t)rho * k;
+        pieces[(size_t)p * cw + ((size_t)L * 2 + 0) * n + k] = u[(size_t)L * N + c];
+        pieces[(size_t)p * cw + ((size_t)L * 2 + 1) * n + k] =
+            (uint32_t)(((uint64_t)ct_in[((size_t)L * 2 + 1) * N + c] + w[(size_t)L * N + c]) % m[L]);
+      }
+  free(u);
+  free(w);
+  free(a_in);
+  /* (M) row ciphertexts, in packing leaf order: leaf j of output piece o is row n*o + h(j) */
+  const size_t nrows = (size_t)p_out * n;
+  uint32_t* rows = (uint32_t*)calloc(nrows * cw, sizeof(uint32_t));
+  uint32_t* pt = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  for (size_t leaf = 0; leaf < nrows; ++leaf) {
+    const uint32_t o = (uint32_t)(leaf / n), j = (uint32_t)(leaf % n);
+    const uint32_t r = n * o + or_half_reverse(j, n);
+    if (r >= n_out) continue;
+    for (uint32_t p = 0; p < p_in; ++p)
+      for (int L = 0; L < 2; ++L) {
+        const uint32_t q = m[L];
+        const uint64_t cpack = powmod(n % q, q - 2, q);
+        /* w(Z) = cpack * sum_k W~[r][n p + h(k)] Z^{-k} */
+        for (uint32_t k = 0; k < n; ++k) {
+          const uint32_t col = n * p + or_half_reverse(k, n);
+          const int64_t wv = col < n_in ? Wt[(size_t)r * n_in + col] : 0;
+          uint32_t v = (uint32_t)mulmod(modq_i64(wv, q), cpack, q);
+          if (k == 0) pt[0] = v;
+          else pt[n - k] = v ? q - v : 0;
+        }
+        for (int ab = 0; ab < 2; ++ab) {
+          polymul(pieces + (size_t)p * cw + ((size_t)L * 2 + ab) * n, pt, n, q, t);
+          uint32_t* dst = rows + leaf * cw + ((size_t)L * 2 + ab) * n;
+          for (uint32_t k = 0; k < n; ++k) dst[k] = (uint32_t)(((uint64_t)dst[k] + t[k]) % q);
+        }
+      }
+  }
+  free(pt);
+  free(t);
+  free(pieces);
+  /* (P) pack each output piece */
+  const uint32_t** gk = (const uint32_t**)malloc(sizeof(void*) * lg);
+  for (int l = 0; l < lg; ++l) gk[l] = gal + (size_t)l * 12 * n;
+  const uint32_t** leaves = (const uint32_t**)malloc(sizeof(void*) * n);
+  uint32_t* packed = (uint32_t*)malloc(sizeof(uint32_t) * cw * p_out);
+  for (uint32_t o = 0; o < p_out; ++o) {
+    for (uint32_t j = 0; j < n; ++j) leaves[j] = rows + ((size_t)o * n + j) * cw;
+    pack_rec(leaves, n, 1, n, gk, m, packed + (size_t)o * cw);
+  }
+  if (pieces_out) memcpy(pieces_out, packed, sizeof(uint32_t) * cw * p_out);
+  /* (R) rescale, (C) compose */
+  const uint32_t q0 = m[0], q1 = m[1];
+  const uint64_t q1inv = powmod(q1 % q0, q0 - 2, q0);
+  memset(out, 0, sizeof(uint32_t) * 2 * N);
+  for (uint32_t o = 0; o < p_out; ++o)
+    for (int ab = 0; ab < 2; ++ab)
+      for (uint32_t k = 0; k < n; ++k) {
+        const uint32_t x0 = packed[(size_t)o * cw + (size_t)ab * n + k];
+        const uint32_t x1 = packed[(size_t)o * cw + ((size_t)2 + ab) * n + k];
+        const int64_t x1c = x1 > q1 / 2 ? (int64_t)x1 - q1 : (int64_t)x1;
+        out[(size_t)ab * N + o + (size_t)rho * k] = (uint32_t)mulmod(modq_i64((int64_t)x0 - x1c, q0), q1inv, q0);
+      }
+  free(gk);
+  free(leaves);
+  free(packed);
+  free(rows);
+  return 0;
+}
+
+/* encrypt a vector (n_in values) in the PCMv input layout at level 1 under s (degree N):
+ * element e -> coefficient (e / n) + rho * k with h(k) = e mod n */
+void or_encode_vector(const double* v, uint32_t n_vals, uint32_t N, uint32_t n, double delta, int64_t* pt) {
+  const uint32_t rho = N / n;
+  memset(pt, 0, sizeof(int64_t) * N);
+  for (uint32_t e = 0; e < n_vals; ++e) {
+    const uint32_t p = e / n, k = or_half_reverse(e % n, n);
+    pt[p + (size_t)rho * k] = llrint(delta * v[e]);
+  }
+}
+void or_decode_vector(const int64_t* phase, uint32_t n_vals, uint32_t N, uint32_t n, double delta, double* v) {
+  const uint32_t rho = N / n;
+  for (uint32_t e = 0; e < n_vals; ++e) {
+    const uint32_t p = e / n, k = or_half_reverse(e % n, n);
+    v[e] = (double)phase[p + (size_t)rho * k] / delta;
+  }
+}

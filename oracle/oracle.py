@@ -16,7 +16,8 @@ __all__ = [
     "encode_weights", "pcmm", "pcmm_limb", "decrypt_mlwe", "decode_mlwe_rows", "rescale",
     "negacyclic_mul", "negacyclic_mul_schoolbook", "sigma_table", "clear_pcmm", "mlwe_column",
     "py_mlwe_components", "py_pcmm_rows", "num_threads", "time_pcmm_sample", "rng",
-    "stream_a", "stream_e", "STREAM_SECRET",
+    "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
+    "decode_vector", "rhombus_pcmv", "rhombus_weights", "decrypt_under",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -35,8 +36,8 @@ def stream_e(r: int) -> int:
 
 
 def build(force: bool = False) -> Path:
-    src = _HERE / "he_oracle.c"
-    if force or not _SO.exists() or _SO.stat().st_mtime < src.stat().st_mtime:
+    srcs = [_HERE / "he_oracle.c", _HERE / "he_oracle_rhombus.c"]
+    if force or not _SO.exists() or any(_SO.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
     return _SO
 
@@ -335,3 +336,103 @@ def time_pcmm_sample(params, Wt, ct, n_rows: int) -> dict:
     pcmm(params, Wt, ct, rows=rows)
     dt = time.perf_counter() - t0
     return {"seconds": dt, "rows": n_rows, "threads": num_threads()}
+
+
+# ---------------------------------------------------------------- Rhombus PCMv (he_oracle_rhombus.c)
+def _rh_lib():
+    L = lib()
+    if not getattr(L, "_rh_bound", False):
+        u32p, i32p, i64p, f64p = (ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32),
+                                  ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double))
+        u32, u64 = ctypes.c_uint32, ctypes.c_uint64
+        sig = {
+            "or_half_reverse": (u32, [u32, u32]),
+            "or_automorphism": (None, [u32p, u32, u32, u32, u32p]),
+            "or_ksk_gen": (None, [u64, u32, i32p, i32p, u32, u32p, u32p]),
+            "or_keyswitch": (None, [u32p, u32p, u32, u32p, u32p, u32p]),
+            "or_rhombus_secret": (None, [u64, u32, u32, i32p, i32p]),
+            "or_galois_ksk": (None, [u64, u32, i32p, u32, u32p, u32p]),
+            "or_rhombus_pcmv": (ctypes.c_int, [u32, u32, u32p, u32p, u32p, u32p, i64p, u32, u32, u32p, u32p]),
+            "or_encode_vector": (None, [f64p, u32, u32, u32, ctypes.c_double, i64p]),
+            "or_decode_vector": (None, [i64p, u32, u32, u32, ctypes.c_double, f64p]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        L._rh_bound = True
+    return L
+
+
+def half_reverse(x: int, n: int) -> int:
+    return int(_rh_lib().or_half_reverse(x, n))
+
+
+def rhombus_keys(params, seed: int, s: np.ndarray):
+    """(s_small [n], s_up [N], ksk_dec [2,2,3,N], gal [log n, 2,2,3,n]) -- see he_oracle_rhombus.c."""
+    L = _rh_lib()
+    N, n = params.N, params.rhombus_degree
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    s_small = np.zeros(n, np.int32)
+    s_up = np.zeros(N, np.int32)
+    L.or_rhombus_secret(seed, n, N, _i32(s_small), _i32(s_up))
+    ksk = np.zeros((2, 2, 3, N), np.uint32)
+    L.or_ksk_gen(seed, 0, _i32(np.ascontiguousarray(s, dtype=np.int32)), _i32(s_up), N, _u32(m), _u32(ksk))
+    lg = n.bit_length() - 1
+    gal = np.zeros((lg, 2, 2, 3, n), np.uint32)
+    for lv in range(1, lg + 1):
+        g = np.zeros((2, 2, 3, n), np.uint32)
+        L.or_galois_ksk(seed, lv, _i32(s_small), n, _u32(m), _u32(g))
+        gal[lv - 1] = g
+    return s_small, s_up, ksk, gal
+
+
+def keyswitch(params, c: np.ndarray, ksk: np.ndarray, n: int):
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    c = np.ascontiguousarray(c, dtype=np.uint32)
+    u = np.zeros((2, n), np.uint32)
+    w = np.zeros((2, n), np.uint32)
+    _rh_lib().or_keyswitch(_u32(c), _u32(np.ascontiguousarray(ksk)), n, _u32(m), _u32(u), _u32(w))
+    return u, w
+
+
+def encode_vector(params, v: np.ndarray) -> np.ndarray:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    pt = np.zeros((1, params.N), np.int64)
+    _rh_lib().or_encode_vector(_f64(v), len(v), params.N, params.rhombus_degree, params.delta, _i64(pt))
+    return pt
+
+
+def decode_vector(params, phase: np.ndarray, n_vals: int) -> np.ndarray:
+    v = np.zeros(n_vals)
+    _rh_lib().or_decode_vector(_i64(np.ascontiguousarray(phase, dtype=np.int64)), n_vals, params.N,
+                               params.rhombus_degree, params.delta, _f64(v))
+    return v
+
+
+def rhombus_pcmv(params, ct_in: np.ndarray, ksk: np.ndarray, gal: np.ndarray, Wt: np.ndarray, n_in: int):
+    """ct_in [2 limbs][2][N] level 1 -> (packed level-1 pieces [p_out][2][2][n], out [2][N] level 0)."""
+    N, n = params.N, params.rhombus_degree
+    Wt = np.ascontiguousarray(Wt, dtype=np.int64)
+    n_out = Wt.shape[0]
+    p_out = -(-n_out // n)
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    pieces = np.zeros((p_out, 2, 2, n), np.uint32)
+    out = np.zeros((2, N), np.uint32)
+    _rh_lib().or_rhombus_pcmv(N, n, _u32(m), _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
+                              _u32(np.ascontiguousarray(ksk)), _u32(np.ascontiguousarray(gal)), _i64(Wt), n_out, n_in,
+                              _u32(pieces), _u32(out))
+    return pieces, out
+
+
+def rhombus_weights(params, W: np.ndarray) -> np.ndarray:
+    """W~ = round_half_even(q1 W) (the h shuffle is applied inside the PCMv)."""
+    return np.rint(np.asarray(W, np.float64) * params.delta_w).astype(np.int64)
+
+
+def decrypt_under(params, a: np.ndarray, b: np.ndarray, s: np.ndarray, q: int) -> np.ndarray:
+    """centred b + a s mod q (degree len(a))."""
+    n = len(a)
+    prod = negacyclic_mul(np.ascontiguousarray(a, dtype=np.uint32), np.ascontiguousarray(s, dtype=np.int32), q)
+    v = (prod.astype(np.int64) + b.astype(np.int64)) % q
+    return np.where(v > q // 2, v - q, v)

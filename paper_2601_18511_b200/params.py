@@ -72,7 +72,7 @@ def signed_digits(bound: int) -> int:
     return n
 
 
-_KNOWN = ("name", "mlwe_degree", "mlwe_rank", "moduli", "log_delta", "rhombus_degree", "seed")
+_KNOWN = ("name", "mlwe_degree", "mlwe_rank", "moduli", "log_delta", "rhombus_degree", "special_prime", "seed")
 
 
 @dataclass(frozen=True)
@@ -85,6 +85,7 @@ class HeParams:
     moduli: tuple[int, ...] = (1073479681, 1179649)
     log_delta: int = 26
     rhombus_degree: int = 4096
+    special_prime: int = 1071513601   # P of the hybrid key switches (Rhombus decompose / packing)
     seed: int | None = None
     name: str = "llama"
 
@@ -105,6 +106,10 @@ class HeParams:
                 raise ValueError(f"modulus {q} must be below 2^30 (lazy NTT butterflies)")
         if len(set(self.moduli)) != len(self.moduli):
             raise ValueError("moduli must be distinct")
+        P = int(self.special_prime)
+        object.__setattr__(self, "special_prime", P)
+        if not is_prime(P) or (P - 1) % (2 * self.N) or P >= 1 << 30 or P in self.moduli:
+            raise ValueError("special_prime must be an NTT-friendly prime below 2^30, distinct from the moduli")
         if not 1 <= self.log_delta <= 40:
             raise ValueError("log_delta must be in [1, 40]")
         if self.rhombus_degree & (self.rhombus_degree - 1) or self.N % self.rhombus_degree:
@@ -132,6 +137,16 @@ class HeParams:
     @property
     def delta(self) -> float:
         return float(2 ** self.log_delta)
+
+    @property
+    def ks_moduli(self) -> tuple[int, int, int]:
+        """(q0, q1, P): the moduli of the hybrid key-switching keys."""
+        return (self.moduli[0], self.moduli[1], self.special_prime)
+
+    @property
+    def rho(self) -> int:
+        """Degree-N ciphertext splits into rho = N / rhombus_degree RLWE pieces."""
+        return self.N // self.rhombus_degree
 
     @property
     def delta_w(self) -> int:
@@ -174,7 +189,9 @@ class HeParams:
     @classmethod
     def wide(cls, **kw) -> "HeParams":
         """N = 2^16 with two ~30-bit primes (4 + 4 ciphertext digits, 4 weight digits)."""
-        kw.setdefault("moduli", tuple(ntt_primes(2 * 65536, 1 << 30, 2)))
+        pr = ntt_primes(2 * 65536, 1 << 30, 3)
+        kw.setdefault("moduli", tuple(pr[:2]))
+        kw.setdefault("special_prime", pr[2])
         kw.setdefault("name", "wide")
         return cls(**kw)
 
@@ -184,7 +201,9 @@ class HeParams:
         (SURVEY.md §8c), 16-column ciphertext batch like hesim's d=16 PCMM."""
         kw.setdefault("mlwe_degree", 32)
         kw.setdefault("mlwe_rank", 16)
-        kw.setdefault("moduli", (ntt_primes(1024, 1 << 30, 1)[0], ntt_primes(1024, 1 << 21, 1)[0]))
+        big = ntt_primes(1024, 1 << 30, 2)
+        kw.setdefault("moduli", (big[0], ntt_primes(1024, 1 << 21, 1)[0]))
+        kw.setdefault("special_prime", big[1])
         kw.setdefault("rhombus_degree", 128)
         kw.setdefault("name", "toy")
         return cls(**kw)
