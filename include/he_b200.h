@@ -50,10 +50,12 @@ typedef struct {
   uint32_t moduli[2];      /* q0 (base), q1 (PCMM scale prime = Delta_w) */
   uint32_t log_delta;      /* input scale Delta = 2^log_delta           */
   uint32_t rhombus_degree; /* RLWE degree of the PCMv path (4096)       */
+  uint32_t special_prime;  /* P of the hybrid key switches (PCMv)       */
 } he_params;
 
 typedef struct he_context he_context;     /* NTT tables, device constants       */
 typedef struct he_pcmm_plan he_pcmm_plan; /* weight side of the MLWE PCMM       */
+typedef struct he_rhombus_plan he_rhombus_plan; /* weight side of the Rhombus PCMv */
 
 /* Operation counters, same field names as hesim.CostLedger (slotsim.py:31-83). */
 typedef struct {
@@ -120,6 +122,33 @@ he_status he_pcmm_decompose(const he_pcmm_plan* plan, const uint32_t* ct_in_dev,
                             uint64_t workspace_bytes, void* stream);
 he_status he_pcmm_gemm(const he_pcmm_plan* plan, const void* workspace_dev, uint32_t* out_b_dev,
                        uint32_t* out_a_dev, void* stream);
+
+/* ---------------------------------------------------------------- Rhombus PCMv (K6), degree n = rhombus_degree */
+/* Vector layout (App. A + h): element e sits at degree-N coefficient
+ * (e / n) + rho * h(e mod n), rho = N / n.  No hesim entry point exists for the PCMv
+ * (SPEC.md:8); the calling convention follows pcmm_depth1 (matmul.py:152-162). */
+he_status he_encrypt_vector(const he_context* ctx, const uint32_t* s_ntt_dev, const double* v_dev, uint32_t n_vals,
+                            uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream);
+/* keys: sparse secret s' (int32 [n]), s'(X^rho) (int32 [N]) and its NTT per limb (u32 [2][N]),
+ * the decompose key s -> s'(X^rho) (u32 [2][2][3][N], NTT domain, moduli q0 q1 P) and the
+ * Galois keys sigma_{2^l+1}(s') -> s' (u32 [log2 n][2][2][3][n], NTT domain) */
+he_status he_rhombus_keygen(const he_context* ctx, uint64_t seed, const int32_t* s_dev, int32_t* s_small_dev,
+                            int32_t* s_up_dev, uint32_t* s_up_ntt_dev, uint32_t* ksk_dec_dev, uint32_t* gal_dev,
+                            void* stream);
+/* weights: W~ = round(q1 W) as NTT-domain plaintexts u32 [2][ceil(n_out/n) n][ceil(n_in/n)][n] */
+he_status he_rhombus_weight_bytes(const he_context* ctx, uint32_t n_out, uint32_t n_in, uint64_t* bytes);
+he_status he_rhombus_encode_weights(const he_context* ctx, const double* w_dev, uint32_t n_out, uint32_t n_in,
+                                    uint32_t* wpt_dev, void* stream);
+he_status he_rhombus_plan_create(const he_context* ctx, const uint32_t* wpt_dev, uint32_t n_out, uint32_t n_in,
+                                 he_rhombus_plan** out);
+he_status he_rhombus_plan_destroy(he_rhombus_plan* plan);
+he_status he_rhombus_workspace_bytes(const he_rhombus_plan* plan, uint64_t* bytes);
+/* level-1 degree-N ct [2][2][N] under s -> level-0 degree-N ct [2 (a, b)][N] under s'(X^rho)
+ * holding W v; ledger: pc_mults += n_out * ceil(n_in/n), ct_rotations += (n - 1) * ceil(n_out/n),
+ * rescales += 1 */
+he_status he_rhombus_run(const he_rhombus_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
+                         const uint32_t* ksk_dec_dev, const uint32_t* gal_dev, uint32_t* out_dev, void* workspace_dev,
+                         uint64_t workspace_bytes, void* stream, he_ledger* ledger);
 
 #ifdef __cplusplus
 }

@@ -18,8 +18,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libhe_b200.so"
-SOURCES = ["he_abi.cu", "he_modgemm.cu", "he_ntt.cu", "he_crypto.cu"]
-HEADERS = ["he_common.cuh", "he_tc.cuh", "he_kernels.h"]
+SOURCES = ["he_abi.cu", "he_modgemm.cu", "he_ntt.cu", "he_crypto.cu", "he_rhombus.cu"]
+HEADERS = ["he_common.cuh", "he_tc.cuh", "he_kernels.h", "he_internal.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O3",

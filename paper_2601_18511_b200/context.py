@@ -95,6 +95,7 @@ class _DeviceCtx:
         p.moduli[0], p.moduli[1] = params.moduli
         p.log_delta = params.log_delta
         p.rhombus_degree = params.rhombus_degree
+        p.special_prime = params.special_prime
         h = ctypes.c_void_p()
         with torch.cuda.device(device_index):
             native.call("he_context_create", ctypes.byref(p), ctypes.byref(h))

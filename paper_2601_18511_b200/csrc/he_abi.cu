@@ -15,25 +15,11 @@
 
 using namespace he;
 
-struct he_context {
-  he_params p;
-  RingDims R;
-  NttTable ntt[2];      // degree N, q0 / q1
-  NttTable ntt_rh[2];   // degree rhombus_degree, q0 / q1
-  int sm_count = 148;
-};
-
-struct he_pcmm_plan {
-  const he_context* ctx;
-  uint32_t n_out, n_in, d_w, d0, d1, width;
-  const int8_t* digits;
-  CUtensorMap tmA;
-  GemmEpiConst epi;
-};
+#include "he_internal.h"
 
 static thread_local std::string g_err;
 
-static he_status fail(he_status s, const char* fmt, ...) {
+he_status fail(he_status s, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -42,14 +28,7 @@ static he_status fail(he_status s, const char* fmt, ...) {
   g_err = buf;
   return s;
 }
-static he_status cuda_fail(cudaError_t e, const char* what) {
-  return fail(HE_ECUDA, "%s: %s", what, cudaGetErrorString(e));
-}
-#define HE_CUDA(call, what)                      \
-  do {                                           \
-    cudaError_t _e = (call);                     \
-    if (_e != cudaSuccess) return cuda_fail(_e, what); \
-  } while (0)
+he_status cuda_fail(cudaError_t e, const char* what) { return fail(HE_ECUDA, "%s: %s", what, cudaGetErrorString(e)); }
 
 extern "C" const char* he_last_error(void) { return g_err.c_str(); }
 extern "C" int he_version(void) { return 1; }
@@ -106,6 +85,11 @@ extern "C" he_status he_context_create(const he_params* p, he_context** out) {
       return fail(HE_EINVAL, "modulus %u must be an NTT-friendly prime below 2^30", q);
   }
   if (p->moduli[1] / 2 >= p->moduli[0]) return fail(HE_EINVAL, "q1/2 must be below q0");
+  {
+    const uint32_t P = p->special_prime;
+    if (P < 3 || P >= (1u << 30) || (P - 1) % (2ull * N) || P == p->moduli[0] || P == p->moduli[1])
+      return fail(HE_EINVAL, "special prime %u must be NTT-friendly, below 2^30 and distinct from the moduli", P);
+  }
   if (p->log_delta < 1 || p->log_delta > 40) return fail(HE_EINVAL, "log_delta out of range");
   if (p->rhombus_degree < 16 || (p->rhombus_degree & (p->rhombus_degree - 1)) || N % p->rhombus_degree)
     return fail(HE_EINVAL, "rhombus_degree must be a power of two dividing N");
@@ -122,9 +106,12 @@ extern "C" he_status he_context_create(const he_params* p, he_context** out) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);
-  for (int i = 0; i < 2; ++i) {
-    cudaError_t e = ntt_table_init(c->ntt[i], N, p->moduli[i]);
-    if (e == cudaSuccess) e = ntt_table_init(c->ntt_rh[i], p->rhombus_degree, p->moduli[i]);
+  c->R.n_rh = p->rhombus_degree;
+  c->R.P = p->special_prime;
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t q = i < 2 ? p->moduli[i] : p->special_prime;
+    cudaError_t e = ntt_table_init(c->ntt[i], N, q);
+    if (e == cudaSuccess) e = ntt_table_init(c->ntt_rh[i], p->rhombus_degree, q);
     if (e != cudaSuccess) {
       he_context_destroy(c);
       return cuda_fail(e, "NTT table init");
@@ -136,7 +123,7 @@ extern "C" he_status he_context_create(const he_params* p, he_context** out) {
 
 extern "C" he_status he_context_destroy(he_context* c) {
   if (!c) return HE_OK;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     ntt_table_free(c->ntt[i]);
     ntt_table_free(c->ntt_rh[i]);
   }
@@ -175,6 +162,23 @@ extern "C" he_status he_encrypt_acts(const he_context* c, const uint32_t* s_ntt_
   return HE_OK;
 }
 
+extern "C" he_status he_encrypt_vector(const he_context* c, const uint32_t* s_ntt_dev, const double* v_dev,
+                                       uint32_t n_vals, uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream) {
+  if (!c || !s_ntt_dev || !v_dev || !ct_dev) return fail(HE_EINVAL, "null argument");
+  if (n_vals == 0 || n_vals > c->R.N) return fail(HE_EINVAL, "vector length %u outside [1, N]", n_vals);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N;
+  HE_CUDA(launch_gen_a(c->R, seed, r0, 1, ct_dev, st), "sample a");
+  for (uint32_t L = 0; L < 2; ++L) {
+    uint32_t* bslot = ct_dev + (size_t)L * 2 * N + N;
+    HE_CUDA(ntt_forward(c->ntt[L], bslot, 1, N, st), "NTT(a)");
+    HE_CUDA(launch_pointwise_mul(bslot, N, s_ntt_dev + (size_t)L * N, N, 1, c->R.q[L], bslot, N, st), "a^ * s^");
+    HE_CUDA(ntt_inverse(c->ntt[L], bslot, 1, N, st), "INTT(a s)");
+  }
+  HE_CUDA(launch_finish_encrypt(c->R, v_dev, n_vals, seed, r0, 1, ct_dev, st, 1), "finish encrypt");
+  return HE_OK;
+}
+
 extern "C" he_status he_decrypt_rlwe(const he_context* c, const uint32_t* s_ntt_dev, const uint32_t* ct_dev,
                                      uint32_t n_ct, uint32_t limbs, uint32_t limb, int64_t* phase_dev, void* stream) {
   if (!c || !s_ntt_dev || !ct_dev || !phase_dev) return fail(HE_EINVAL, "null argument");
@@ -210,7 +214,7 @@ extern "C" he_status he_decrypt_mlwe(const he_context* c, const int32_t* s_dev, 
 
 // ---------------------------------------------------------------- NTT
 static const NttTable* pick(const he_context* c, uint32_t n, uint32_t limb) {
-  if (limb > 1) return nullptr;
+  if (limb > 2) return nullptr;  // 2 = the special prime P
   if (n == c->R.N) return &c->ntt[limb];
   if (n == c->p.rhombus_degree) return &c->ntt_rh[limb];
   return nullptr;

@@ -1,0 +1,31 @@
+// he_internal.h -- private definitions shared by the C-ABI translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/he_b200.h"
+#include "he_kernels.h"
+
+struct he_context {
+  he_params p;
+  he::RingDims R;
+  he::NttTable ntt[3];     // degree N: q0, q1, P
+  he::NttTable ntt_rh[3];  // degree rhombus_degree: q0, q1, P
+  int sm_count = 148;
+};
+
+struct he_pcmm_plan {
+  const he_context* ctx;
+  uint32_t n_out, n_in, d_w, d0, d1, width;
+  const int8_t* digits;
+  CUtensorMap tmA;
+  he::GemmEpiConst epi;
+};
+
+he_status fail(he_status s, const char* fmt, ...);
+he_status cuda_fail(cudaError_t e, const char* what);
+#define HE_CUDA(call, what)                              \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, what);   \
+  } while (0)

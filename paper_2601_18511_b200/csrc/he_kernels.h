@@ -51,6 +51,7 @@ cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint6
 
 struct RingDims {
   uint32_t d, k, N, logk, q[2], log_delta;
+  uint32_t n_rh, P;  // Rhombus degree and special prime
 };
 
 cudaError_t launch_decompose(const RingDims& R, const uint32_t* ct, uint32_t n_in, int d0, int d1, int8_t* planes,
@@ -66,7 +67,7 @@ cudaError_t launch_gen_a(const RingDims& R, uint64_t seed, uint32_t r0, uint32_t
 cudaError_t launch_pointwise_mul(const uint32_t* x, uint64_t x_stride, const uint32_t* y, uint32_t n,
                                  uint32_t count, uint32_t q, uint32_t* out, uint64_t out_stride, cudaStream_t st);
 cudaError_t launch_finish_encrypt(const RingDims& R, const double* acts, uint32_t n_in, uint64_t seed, uint32_t r0,
-                                  uint32_t n_ct, uint32_t* ct, cudaStream_t st);
+                                  uint32_t n_ct, uint32_t* ct, cudaStream_t st, int layout = 0);
 cudaError_t launch_phase(const uint32_t* b, uint64_t b_stride, const uint32_t* as, uint64_t as_stride, uint32_t n,
                          uint32_t count, uint32_t q, int64_t* phase, cudaStream_t st);
 cudaError_t launch_decrypt_mlwe(const RingDims& R, const int32_t* s, const uint32_t* out_b, const uint32_t* out_a,

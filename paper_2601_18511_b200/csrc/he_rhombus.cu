@@ -1,0 +1,588 @@
+// he_rhombus.cu -- K6: the Rhombus PCMv at RLWE degree n = rhombus_degree (4096), restated from
+// oracle/he_oracle_rhombus.c (same integer algorithm, so results are bit-exact):
+//   (D) decompose  : hybrid key switch (dnum 2, special prime P) of the degree-N input from s to
+//                    s'(X^rho), then the free X^rho split into rho RLWE-n pieces
+//   (M) MVM        : coefficient-encoded inner products, pt x ct in the NTT domain, summed over pieces
+//   (P) packing    : PackLWEs over the n row ciphertexts of each output piece; the automorphisms act
+//                    in the NTT domain as index permutations, each followed by a Galois key switch
+//   (R)(C)         : rescale by q1 and the free X^rho interleave back to degree N.
+// Every stage is a batched kernel launch (all combines of a packing level at once) around the K2
+// NTT; nothing runs on the host but the launch sequence.
+#include <vector>
+
+#include "he_common.cuh"
+#include "he_internal.h"
+#include "he_kernels.h"
+
+using namespace he;
+
+namespace {
+
+constexpr uint64_t kStreamSecretRh = 0x5EC1000000000000ULL;
+HE_HD uint64_t stream_ksk_a(uint32_t id, uint32_t i, uint32_t j) {
+  return 0xC000000000000000ULL | ((uint64_t)id << 16) | ((uint64_t)i << 8) | (uint64_t)j;
+}
+HE_HD uint64_t stream_ksk_e(uint32_t id, uint32_t i) {
+  return 0xCE00000000000000ULL | ((uint64_t)id << 16) | ((uint64_t)i << 8);
+}
+HE_HD uint32_t half_reverse(uint32_t x, uint32_t n, int logn) {
+  return (x & (n >> 1)) | bitrev_h(x & ((n >> 1) - 1), logn - 1);
+}
+HE_D uint32_t barrett64(uint64_t x, uint64_t mu, uint32_t q) {  // x mod q for any x < 2^64
+  const uint64_t qh = __umul64hi(x, mu);
+  return csub((uint32_t)(x - qh * q), q);
+}
+
+struct Mods {
+  uint32_t m[3];
+  uint64_t mu[3];
+};
+Mods make_mods(const RingDims& R) {
+  Mods M;
+  M.m[0] = R.q[0];
+  M.m[1] = R.q[1];
+  M.m[2] = R.P;
+  for (int j = 0; j < 3; ++j) M.mu[j] = (uint64_t)(((unsigned __int128)1 << 64) / M.m[j]);
+  return M;
+}
+
+// ------------------------------------------------------------------ key generation
+__global__ void k_small_secret(uint64_t seed, uint32_t n, uint32_t N, int32_t* s_small, int32_t* s_up) {
+  const uint64_t key = rng_key(seed, kStreamSecretRh);
+  const uint32_t rho = N / n;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    if (i < n) s_small[i] = ternary(rng_draw(key, i));
+    s_up[i] = (i % rho == 0) ? ternary(rng_draw(key, i / rho)) : 0;
+  }
+}
+// sigma_k(s) on a signed secret
+__global__ void k_secret_auto(const int32_t* s, uint32_t n, uint32_t k, int32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t j = ((uint64_t)i * k) % (2ull * n);
+    if (j < n) out[j] = s[i];
+    else out[j - n] = -s[i];
+  }
+}
+__global__ void k_reduce_signed(const int32_t* s, uint32_t n, uint32_t q, uint32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t v = s[i];
+    out[i] = v < 0 ? q + v : (uint32_t)v;
+  }
+}
+// alpha (uniform) and t = g * s_old + e  (coefficient form, modulus q)
+__global__ void k_ksk_prep(uint64_t seed, uint32_t id, uint32_t i, uint32_t j, uint32_t q, uint32_t g,
+                           const int32_t* s_old, uint32_t n, uint32_t* alpha, uint32_t* t) {
+  const uint64_t ka = rng_key(seed, stream_ksk_a(id, i, j)), ke = rng_key(seed, stream_ksk_e(id, i));
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    alpha[c] = (uint32_t)(rng_draw(ka, c) % q);
+    const int64_t e = cbd21_d(rng_draw(ke, c));
+    const uint64_t gs = (uint64_t)g * from_i64(s_old[c], q) % q;
+    t[c] = (uint32_t)((gs + from_i64(e, q)) % q);
+  }
+}
+// beta = t - alpha * s_new   (NTT domain, in place in t)
+__global__ void k_ksk_beta(const uint32_t* alpha, const uint32_t* s_new, uint32_t n, uint32_t q, uint32_t* t) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    t[c] = sub_mod(t[c], mul_mod(alpha[c], s_new[c], q), q);
+}
+
+// ------------------------------------------------------------------ key switching pieces (batched)
+// digits of c (coefficient form, per limb [2][cnt][n]) lifted to the other moduli:
+//   d_i = c_i * Qhat_i^-1 mod q_i;  D[j][i] = d_i mod m_j for j != i.  D[i][i] comes from the NTT form.
+__global__ void k_modup(const uint32_t* __restrict__ c, const uint32_t* __restrict__ c_ntt, uint64_t cnt_n,
+                        uint32_t q0, uint32_t q1, uint32_t P, uint32_t qhinv0, uint32_t qhinv1, uint32_t* __restrict__ D,
+                        uint32_t q0p, uint32_t q1p) {
+  // D layout: [j (3)][i (2)][cnt * n]
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t d0 = mul_mod(c[x], qhinv0, q0);
+    const uint32_t d1 = mul_mod(c[cnt_n + x], qhinv1, q1);
+    D[(0 * 2 + 1) * cnt_n + x] = d1 % q0;
+    D[(1 * 2 + 0) * cnt_n + x] = d0 % q1;
+    D[(2 * 2 + 0) * cnt_n + x] = d0 % P;
+    D[(2 * 2 + 1) * cnt_n + x] = d1 % P;
+    // own-modulus digits straight from the NTT form (NTT is linear mod q_i)
+    D[(0 * 2 + 0) * cnt_n + x] = mul_mod(c_ntt[x], qhinv0, q0);
+    D[(1 * 2 + 1) * cnt_n + x] = mul_mod(c_ntt[cnt_n + x], qhinv1, q1);
+  }
+  (void)q0p;
+  (void)q1p;
+}
+// U[j] = sum_i D[j][i] * K[i][0][j],  W[j] = sum_i D[j][i] * K[i][1][j]   (NTT domain)
+// K layout [i][part][j][n];  UW layout [j][2][cnt][n]
+__global__ void k_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict__ K, uint32_t n, uint64_t cnt_n,
+                      Mods M, uint32_t* __restrict__ UW) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)(x % n);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const uint64_t dd0 = D[(j * 2 + 0) * cnt_n + x], dd1 = D[(j * 2 + 1) * cnt_n + x];
+      const uint64_t u = dd0 * K[((0 * 2 + 0) * 3 + j) * (size_t)n + c] + dd1 * K[((1 * 2 + 0) * 3 + j) * (size_t)n + c];
+      const uint64_t w = dd0 * K[((0 * 2 + 1) * 3 + j) * (size_t)n + c] + dd1 * K[((1 * 2 + 1) * 3 + j) * (size_t)n + c];
+      UW[(j * 2 + 0) * cnt_n + x] = barrett64(u, M.mu[j], M.m[j]);
+      UW[(j * 2 + 1) * cnt_n + x] = barrett64(w, M.mu[j], M.m[j]);
+    }
+  }
+}
+// ModDown, first half: centred lift of the (coefficient-form) P parts to q0, q1.  LB [j][2][cnt][n]
+__global__ void k_moddown_lift(const uint32_t* __restrict__ UWP, uint64_t cnt_n, uint32_t P, uint32_t q0, uint32_t q1,
+                               uint32_t* __restrict__ LB) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = UWP[x];
+    const int64_t c = v > P / 2 ? (int64_t)v - P : (int64_t)v;
+    LB[x] = from_i64(c, q0);
+    LB[2 * cnt_n + x] = from_i64(c, q1);
+  }
+}
+
+// ------------------------------------------------------------------ decompose (degree N)
+__global__ void k_decomp_modup(const uint32_t* __restrict__ ct, uint32_t N, uint32_t q0, uint32_t q1, uint32_t P,
+                               uint32_t qhinv0, uint32_t qhinv1, uint32_t* __restrict__ D) {
+  // ct [2 limbs][2][N]; D [j][i][N] (coefficient form: all six lifts, NTT'd afterwards)
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
+    const uint32_t d0 = mul_mod(ct[x], qhinv0, q0);
+    const uint32_t d1 = mul_mod(ct[2 * (size_t)N + x], qhinv1, q1);
+    D[0 * (size_t)N + x] = d0;            // j=0,i=0
+    D[1 * (size_t)N + x] = d1 % q0;       // j=0,i=1
+    D[2 * (size_t)N + x] = d0 % q1;       // j=1,i=0
+    D[3 * (size_t)N + x] = d1;            // j=1,i=1
+    D[4 * (size_t)N + x] = d0 % P;
+    D[5 * (size_t)N + x] = d1 % P;
+  }
+}
+// (u, w) mod q_j from UW (coefficient form, [j][2][N]), then the X^rho split:
+//   pieces [L][p][2][n]:  a = u[p + rho k],  b = b_in[p + rho k] + w[p + rho k]
+__global__ void k_decomp_split(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ ct, uint32_t N,
+                               uint32_t n, uint32_t p_in, uint32_t q0, uint32_t q1, uint32_t P, uint32_t pinv0,
+                               uint32_t pinv1, uint32_t* __restrict__ pieces) {
+  const uint32_t rho = N / n;
+  const uint32_t total = p_in * n;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const uint32_t p = x / n, k = x % n;
+    const size_t src = p + (size_t)rho * k;
+#pragma unroll
+    for (int L = 0; L < 2; ++L) {
+      const uint32_t q = L ? q1 : q0, pinv = L ? pinv1 : pinv0;
+      int64_t up = UW[(2 * 2 + 0) * (size_t)N + src], wp = UW[(2 * 2 + 1) * (size_t)N + src];
+      if (up > P / 2) up -= P;
+      if (wp > P / 2) wp -= P;
+      const uint32_t u = mul_mod(from_i64((int64_t)UW[(L * 2 + 0) * (size_t)N + src] - up, q), pinv, q);
+      const uint32_t w = mul_mod(from_i64((int64_t)UW[(L * 2 + 1) * (size_t)N + src] - wp, q), pinv, q);
+      const uint32_t b = ct[(L * 2 + 1) * (size_t)N + src];
+      uint32_t* dst = pieces + (((size_t)L * p_in + p) * 2) * n;
+      dst[k] = u;
+      dst[n + k] = add_mod(b, w, q);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ weights (plan)
+// Wpt [L][leaf][p][n] coefficient form before the NTT:  w(Z) = cpack * sum_k W~[r][n p + h(k)] Z^{-k}
+__global__ void k_rh_weights(const double* __restrict__ W, uint32_t n_out, uint32_t n_in, uint32_t n, int logn,
+                             uint32_t p_in, uint64_t leaves, uint32_t q0, uint32_t q1, uint32_t cp0, uint32_t cp1,
+                             double delta_w, uint32_t* __restrict__ out) {
+  const uint64_t per_l = leaves * p_in * n;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < per_l; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = (uint32_t)(x % n);
+    const uint64_t lp = x / n;
+    const uint32_t p = (uint32_t)(lp % p_in);
+    const uint64_t leaf = lp / p_in;
+    const uint32_t o = (uint32_t)(leaf / n), j = (uint32_t)(leaf % n);
+    const uint32_t r = n * o + half_reverse(j, n, logn);
+    const uint32_t col = n * p + half_reverse(k, n, logn);
+    long long wv = 0;
+    if (r < n_out && col < n_in) wv = __double2ll_rn(__dmul_rn(delta_w, W[(size_t)r * n_in + col]));
+    const uint32_t pos = k == 0 ? 0 : n - k;
+#pragma unroll
+    for (int L = 0; L < 2; ++L) {
+      const uint32_t q = L ? q1 : q0;
+      uint32_t v = mul_mod(from_i64(wv, q), L ? cp1 : cp0, q);
+      if (k != 0 && v) v = q - v;
+      out[(size_t)L * per_l + lp * n + pos] = v;
+    }
+  }
+}
+
+// rows [L][leaf][2][n] = sum_p Wpt[L][leaf][p][.] * pieces[L][p][ab][.]   (NTT domain)
+__global__ void k_rh_mvm(const uint32_t* __restrict__ Wpt, const uint32_t* __restrict__ pieces, uint64_t leaves,
+                         uint32_t p_in, uint32_t n, Mods M, uint32_t* __restrict__ rows) {
+  const uint64_t per_l = leaves * n;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * per_l; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t L = (uint32_t)(x / per_l);
+    const uint64_t y = x % per_l;
+    const uint64_t leaf = y / n;
+    const uint32_t c = (uint32_t)(y % n);
+    const uint32_t* w = Wpt + ((size_t)L * leaves + leaf) * p_in * n + c;
+    const uint32_t* pc = pieces + (size_t)L * p_in * 2 * n + c;
+    uint64_t acc_a = 0, acc_b = 0;
+    for (uint32_t p = 0; p < p_in; ++p) {
+      const uint64_t wv = w[(size_t)p * n];
+      acc_a += wv * pc[(size_t)p * 2 * n];
+      acc_b += wv * pc[(size_t)p * 2 * n + n];
+      if ((p & 7) == 7) {  // keep the sum below 2^64: 8 products < 2^63
+        acc_a = barrett64(acc_a, M.mu[L], M.m[L]);
+        acc_b = barrett64(acc_b, M.mu[L], M.m[L]);
+      }
+    }
+    uint32_t* dst = rows + (((size_t)L * leaves + leaf) * 2) * n + c;
+    dst[0] = barrett64(acc_a, M.mu[L], M.m[L]);
+    dst[n] = barrett64(acc_b, M.mu[L], M.m[L]);
+  }
+}
+
+// ------------------------------------------------------------------ packing level
+// A [L][cnt_in][2][n] -> Ut into An [L][cnt_out][2][n]; T = sigma(E - M O) [L][cnt_out][2][n];
+// C = copy of T's a part [L][cnt_out][n] for the INTT.
+__global__ void k_pack_comb1(const uint32_t* __restrict__ A, uint32_t cnt_in, uint32_t half, uint32_t n,
+                             const uint32_t* __restrict__ mono /* [2][n] */, const uint32_t* __restrict__ perm,
+                             uint32_t q0, uint32_t q1, uint32_t* __restrict__ An, uint32_t* __restrict__ T,
+                             uint32_t* __restrict__ C) {
+  const uint32_t cnt_out = cnt_in / 2;
+  const uint64_t per_l = (uint64_t)cnt_out * n;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * per_l; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t L = (uint32_t)(x / per_l);
+    const uint64_t y = x % per_l;
+    const uint32_t idx = (uint32_t)(y / n), c = (uint32_t)(y % n);
+    const uint32_t o = idx / half, s = idx % half;
+    const uint32_t e_i = o * 2 * half + s, o_i = e_i + half;
+    const uint32_t q = L ? q1 : q0;
+    const uint32_t* Eb = A + (((size_t)L * cnt_in + e_i) * 2) * n;
+    const uint32_t* Ob = A + (((size_t)L * cnt_in + o_i) * 2) * n;
+    const uint32_t* ml = mono + (size_t)L * n;
+    const uint32_t pc = perm[c];
+#pragma unroll
+    for (int ab = 0; ab < 2; ++ab) {
+      const uint32_t mo = mul_mod(Ob[ab * n + c], ml[c], q);
+      An[(((size_t)L * cnt_out + idx) * 2 + ab) * n + c] = add_mod(Eb[ab * n + c], mo, q);
+      const uint32_t t = sub_mod(Eb[ab * n + pc], mul_mod(Ob[ab * n + pc], ml[pc], q), q);
+      T[(((size_t)L * cnt_out + idx) * 2 + ab) * n + c] = t;
+      if (ab == 0) C[((size_t)L * cnt_out + idx) * n + c] = t;
+    }
+  }
+}
+// T's a part (NTT form) re-laid out [L][cnt][n] for the own-modulus digits
+__global__ void k_pack_aview(const uint32_t* __restrict__ T, uint32_t cnt, uint32_t n, uint32_t* __restrict__ Ta) {
+  const uint64_t per_l = (uint64_t)cnt * n;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * per_l; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t L = (uint32_t)(x / per_l);
+    const uint64_t y = x % per_l;
+    Ta[x] = T[(((size_t)L * cnt + y / n) * 2) * n + y % n];
+  }
+}
+// An += (u, T_b + w) with u = (U - LB_u) P^-1, w = (W - LB_w) P^-1   (NTT domain)
+__global__ void k_pack_comb2(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ LB,
+                             const uint32_t* __restrict__ T, uint32_t cnt, uint32_t n, uint32_t q0, uint32_t q1,
+                             uint32_t pinv0, uint32_t pinv1, uint32_t* __restrict__ An) {
+  const uint64_t cnt_n = (uint64_t)cnt * n;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t L = (uint32_t)(x / cnt_n);
+    const uint64_t y = x % cnt_n;
+    const uint32_t idx = (uint32_t)(y / n), c = (uint32_t)(y % n);
+    const uint32_t q = L ? q1 : q0, pinv = L ? pinv1 : pinv0;
+    const uint32_t u = mul_mod(sub_mod(UW[(L * 2 + 0) * cnt_n + y], LB[(L * 2 + 0) * cnt_n + y], q), pinv, q);
+    const uint32_t w = mul_mod(sub_mod(UW[(L * 2 + 1) * cnt_n + y], LB[(L * 2 + 1) * cnt_n + y], q), pinv, q);
+    uint32_t* dst = An + (((size_t)L * cnt + idx) * 2) * n + c;
+    const uint32_t tb = T[(((size_t)L * cnt + idx) * 2 + 1) * n + c];
+    dst[0] = add_mod(dst[0], u, q);
+    dst[n] = add_mod(dst[n], add_mod(tb, w, q), q);
+  }
+}
+// rescale by q1 and compose: out[ab][o + rho k]  (A coefficient form [L][p_out][2][n])
+__global__ void k_rh_rescale_compose(const uint32_t* __restrict__ A, uint32_t p_out, uint32_t n, uint32_t N,
+                                     uint32_t q0, uint32_t q1, uint32_t q1inv, uint32_t q1invp, uint32_t* __restrict__ out) {
+  const uint32_t rho = N / n;
+  const uint64_t per_l = (uint64_t)p_out * 2 * n;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < per_l; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = (uint32_t)(x % n);
+    const uint32_t ab = (uint32_t)((x / n) % 2);
+    const uint32_t o = (uint32_t)(x / (2ull * n));
+    const uint32_t x0 = A[x], x1 = A[per_l + x];
+    uint32_t t;
+    if (x1 > (q1 >> 1)) t = csub(x0 + (q1 - x1), q0);
+    else t = sub_mod(x0, x1, q0);
+    out[(size_t)ab * N + o + (size_t)rho * k] = shoup_mul(t, q1inv, q1invp, q0);
+  }
+}
+
+inline dim3 grid_for(uint64_t work, int threads = 256) {
+  uint64_t b = (work + threads - 1) / threads;
+  if (b > 148ull * 64) b = 148ull * 64;
+  if (b == 0) b = 1;
+  return dim3((unsigned)b);
+}
+
+int ilog2_u(uint32_t x) { return ilog2_h(x); }
+
+}  // namespace
+
+// ======================================================================== plan / C ABI
+struct he_rhombus_plan {
+  const he_context* ctx;
+  uint32_t n_out, n_in, p_in, p_out, n, N, logn;
+  const uint32_t* wpt;       // caller-owned [2][leaves][p_in][n] NTT domain
+  uint32_t* tables;          // owned: perm [logn][n], mono [logn][2][n]
+  Mods M;
+  uint32_t qhinv[2], pinv[2], q1inv, q1invp;
+};
+
+static uint64_t leaves_of(const he_rhombus_plan* p) { return (uint64_t)p->p_out * p->n; }
+
+extern "C" he_status he_rhombus_keygen(const he_context* c, uint64_t seed, const int32_t* s_dev, int32_t* s_small_dev,
+                                       int32_t* s_up_dev, uint32_t* s_up_ntt_dev, uint32_t* ksk_dec_dev,
+                                       uint32_t* gal_dev, void* stream) {
+  if (!c || !s_dev || !s_small_dev || !s_up_dev || !s_up_ntt_dev || !ksk_dec_dev || !gal_dev)
+    return fail(HE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N, n = c->R.n_rh;
+  const int logn = ilog2_u(n);
+  const Mods M = make_mods(c->R);
+  k_small_secret<<<grid_for(N), 256, 0, st>>>(seed, n, N, s_small_dev, s_up_dev);
+  for (int L = 0; L < 2; ++L) {
+    uint32_t* dst = s_up_ntt_dev + (size_t)L * N;
+    k_reduce_signed<<<grid_for(N), 256, 0, st>>>(s_up_dev, N, M.m[L], dst);
+    HE_CUDA(ntt_forward(c->ntt[L], dst, 1, N, st), "NTT(s_up)");
+  }
+  // scratch: s_new NTT per modulus [3][deg] + signed s_old [deg]
+  auto make_ksk = [&](uint32_t id, const int32_t* s_old, const int32_t* s_new, uint32_t deg, const NttTable* tabs,
+                      uint32_t* ksk) -> he_status {
+    uint32_t* snew = nullptr;
+    HE_CUDA(cudaMallocAsync(&snew, 3ull * deg * sizeof(uint32_t), st), "alloc");
+    for (int j = 0; j < 3; ++j) {
+      k_reduce_signed<<<grid_for(deg), 256, 0, st>>>(s_new, deg, M.m[j], snew + (size_t)j * deg);
+      HE_CUDA(ntt_forward(tabs[j], snew + (size_t)j * deg, 1, deg, st), "NTT(s_new)");
+    }
+    for (uint32_t i = 0; i < 2; ++i)
+      for (uint32_t j = 0; j < 3; ++j) {
+        const uint32_t q = M.m[j];
+        // g_{i,j} = P * Qhat_i mod q_j for j == i, else 0  (Qhat_0 = q1, Qhat_1 = q0)
+        const uint32_t g = (j == i) ? (uint32_t)((uint64_t)(M.m[2] % q) * (M.m[1 - i] % q) % q) : 0u;
+        uint32_t* alpha = ksk + ((size_t)(i * 2 + 0) * 3 + j) * deg;
+        uint32_t* beta = ksk + ((size_t)(i * 2 + 1) * 3 + j) * deg;
+        k_ksk_prep<<<grid_for(deg), 256, 0, st>>>(seed, id, i, j, q, g, s_old, deg, alpha, beta);
+        HE_CUDA(ntt_forward(tabs[j], alpha, 1, deg, st), "NTT(alpha)");
+        HE_CUDA(ntt_forward(tabs[j], beta, 1, deg, st), "NTT(t)");
+        k_ksk_beta<<<grid_for(deg), 256, 0, st>>>(alpha, snew + (size_t)j * deg, deg, q, beta);
+      }
+    cudaFreeAsync(snew, st);
+    return HE_OK;
+  };
+  he_status s = make_ksk(0, s_dev, s_up_dev, N, c->ntt, ksk_dec_dev);
+  if (s) return s;
+  int32_t* sk = nullptr;
+  HE_CUDA(cudaMallocAsync(&sk, n * sizeof(int32_t), st), "alloc");
+  for (int lv = 1; lv <= logn; ++lv) {
+    const uint32_t k = (1u << lv) + 1;
+    k_secret_auto<<<grid_for(n), 256, 0, st>>>(s_small_dev, n, k, sk);
+    s = make_ksk(1 + lv, sk, s_small_dev, n, c->ntt_rh, gal_dev + (size_t)(lv - 1) * 12 * n);
+    if (s) break;
+  }
+  cudaFreeAsync(sk, st);
+  if (s) return s;
+  return cudaGetLastError() == cudaSuccess ? HE_OK : fail(HE_ECUDA, "rhombus keygen launch failed");
+}
+
+extern "C" he_status he_rhombus_weight_bytes(const he_context* c, uint32_t n_out, uint32_t n_in, uint64_t* bytes) {
+  if (!c || !bytes) return fail(HE_EINVAL, "null argument");
+  if (!n_out || !n_in) return fail(HE_EINVAL, "empty weight matrix");
+  const uint32_t n = c->R.n_rh, rho = c->R.N / n;
+  const uint32_t p_in = (n_in + n - 1) / n, p_out = (n_out + n - 1) / n;
+  if (p_in > rho || p_out > rho)
+    return fail(HE_EINVAL, "dim mismatch: vector dims (%u, %u) exceed the %u x %u coefficients of one ciphertext",
+                n_out, n_in, rho, n);
+  *bytes = 2ull * p_out * n * p_in * n * sizeof(uint32_t);
+  return HE_OK;
+}
+
+extern "C" he_status he_rhombus_encode_weights(const he_context* c, const double* w_dev, uint32_t n_out, uint32_t n_in,
+                                               uint32_t* wpt_dev, void* stream) {
+  uint64_t bytes;
+  he_status s = he_rhombus_weight_bytes(c, n_out, n_in, &bytes);
+  if (s) return s;
+  if (!w_dev || !wpt_dev) return fail(HE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t n = c->R.n_rh;
+  const uint32_t p_in = (n_in + n - 1) / n, p_out = (n_out + n - 1) / n;
+  const uint64_t leaves = (uint64_t)p_out * n;
+  const Mods M = make_mods(c->R);
+  const uint32_t cp0 = (uint32_t)powmod_h(n, M.m[0] - 2, M.m[0]), cp1 = (uint32_t)powmod_h(n, M.m[1] - 2, M.m[1]);
+  k_rh_weights<<<grid_for(leaves * p_in * n), 256, 0, st>>>(w_dev, n_out, n_in, n, ilog2_u(n), p_in, leaves, M.m[0],
+                                                            M.m[1], cp0, cp1, (double)M.m[1], wpt_dev);
+  for (int L = 0; L < 2; ++L)
+    HE_CUDA(ntt_forward(c->ntt_rh[L], wpt_dev + (size_t)L * leaves * p_in * n, (uint32_t)(leaves * p_in), n, st),
+            "NTT(weights)");
+  return HE_OK;
+}
+
+extern "C" he_status he_rhombus_plan_create(const he_context* c, const uint32_t* wpt_dev, uint32_t n_out, uint32_t n_in,
+                                            he_rhombus_plan** out) {
+  uint64_t bytes;
+  he_status s = he_rhombus_weight_bytes(c, n_out, n_in, &bytes);
+  if (s) return s;
+  if (!wpt_dev || !out) return fail(HE_EINVAL, "null argument");
+  he_rhombus_plan* p = new (std::nothrow) he_rhombus_plan();
+  if (!p) return fail(HE_ENOMEM, "out of host memory");
+  p->ctx = c;
+  p->n = c->R.n_rh;
+  p->N = c->R.N;
+  p->logn = (uint32_t)ilog2_u(p->n);
+  p->n_out = n_out;
+  p->n_in = n_in;
+  p->p_in = (n_in + p->n - 1) / p->n;
+  p->p_out = (n_out + p->n - 1) / p->n;
+  p->wpt = wpt_dev;
+  p->M = make_mods(c->R);
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t qi = p->M.m[i];
+    p->qhinv[i] = (uint32_t)powmod_h(p->M.m[1 - i] % qi, qi - 2, qi);
+    p->pinv[i] = (uint32_t)powmod_h(p->M.m[2] % qi, qi - 2, qi);
+  }
+  p->q1inv = (uint32_t)powmod_h(p->M.m[1] % p->M.m[0], p->M.m[0] - 2, p->M.m[0]);
+  p->q1invp = shoup_pre(p->q1inv, p->M.m[0]);
+  // NTT-domain automorphism permutations and monomials X^{n/2^l}: output c of the forward
+  // transform holds p(psi^{2 brv(c) + 1})
+  const uint32_t n = p->n, logn = p->logn;
+  std::vector<uint32_t> h((size_t)logn * n * 3);
+  uint32_t* perm = h.data();
+  uint32_t* mono = h.data() + (size_t)logn * n;
+  for (uint32_t lv = 1; lv <= logn; ++lv) {
+    const uint64_t k = (1u << lv) + 1;
+    for (uint32_t cc = 0; cc < n; ++cc) {
+      const uint64_t e = 2ull * bitrev_h(cc, (int)logn) + 1;
+      const uint64_t ek = (e * k) % (2ull * n);
+      perm[(size_t)(lv - 1) * n + cc] = bitrev_h((uint32_t)((ek - 1) / 2), (int)logn);
+    }
+    for (int L = 0; L < 2; ++L) {
+      const uint32_t q = p->M.m[L];
+      // psi: the root the NTT tables use (same search as ntt_table_init)
+      uint64_t psi = 0;
+      for (uint64_t g = 2; g < q; ++g) {
+        uint64_t cand = powmod_h(g, (q - 1) / (2ull * n), q);
+        if (powmod_h(cand, n, q) == q - 1) {
+          psi = cand;
+          break;
+        }
+      }
+      const uint64_t ex = n >> lv;
+      for (uint32_t cc = 0; cc < n; ++cc) {
+        const uint64_t e = 2ull * bitrev_h(cc, (int)logn) + 1;
+        mono[((size_t)(lv - 1) * 2 + L) * n + cc] = (uint32_t)powmod_h(psi, (e * ex) % (2ull * n), q);
+      }
+    }
+  }
+  if (cudaMalloc(&p->tables, h.size() * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemcpy(p->tables, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+    delete p;
+    return fail(HE_ECUDA, "rhombus tables");
+  }
+  *out = p;
+  return HE_OK;
+}
+
+extern "C" he_status he_rhombus_plan_destroy(he_rhombus_plan* p) {
+  if (p) {
+    if (p->tables) cudaFree(p->tables);
+    delete p;
+  }
+  return HE_OK;
+}
+
+// workspace carve-up (words)
+struct RhWs {
+  uint32_t *pieces, *A0, *A1, *T, *C, *D, *UW, *LB, *dD, *dUW;
+};
+static uint64_t rh_ws_words(const he_rhombus_plan* p, RhWs* w, uint32_t* base) {
+  const uint64_t n = p->n, N = p->N, leaves = leaves_of(p), c1 = leaves / 2;
+  uint64_t off = 0;
+  auto take = [&](uint32_t*& ptr, uint64_t words) {
+    if (w) ptr = base + off;
+    off += (words + 63) & ~63ull;
+  };
+  RhWs dummy;
+  RhWs& r = w ? *w : dummy;
+  take(r.pieces, 2ull * p->p_in * 2 * n);
+  take(r.A0, 2ull * leaves * 2 * n);
+  take(r.A1, 2ull * c1 * 2 * n);
+  take(r.T, 2ull * c1 * 2 * n);
+  take(r.C, 2ull * c1 * n);
+  take(r.D, 6ull * c1 * n);
+  take(r.UW, 6ull * c1 * n);
+  take(r.LB, 4ull * c1 * n);
+  take(r.dD, 6ull * N);
+  take(r.dUW, 6ull * N);
+  return off;
+}
+
+extern "C" he_status he_rhombus_workspace_bytes(const he_rhombus_plan* p, uint64_t* bytes) {
+  if (!p || !bytes) return fail(HE_EINVAL, "null argument");
+  *bytes = rh_ws_words(p, nullptr, nullptr) * sizeof(uint32_t);
+  return HE_OK;
+}
+
+extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level,
+                                    const uint32_t* ksk_dec, const uint32_t* gal, uint32_t* out, void* ws_dev,
+                                    uint64_t ws_bytes, void* stream, he_ledger* ledger) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmv needs one level");
+  if (level != 1) return fail(HE_EINVAL, "the Rhombus PCMv runs at level 1 (got %u)", level);
+  if (!ct_in || !ksk_dec || !gal || !out || !ws_dev) return fail(HE_EINVAL, "null argument");
+  uint64_t need = rh_ws_words(p, nullptr, nullptr) * sizeof(uint32_t);
+  if (ws_bytes < need) return fail(HE_EINVAL, "workspace too small (%llu < %llu)", (unsigned long long)ws_bytes,
+                                   (unsigned long long)need);
+  cudaStream_t st = (cudaStream_t)stream;
+  const he_context* c = p->ctx;
+  const uint32_t n = p->n, N = p->N, q0 = p->M.m[0], q1 = p->M.m[1], P = p->M.m[2];
+  RhWs w;
+  rh_ws_words(p, &w, (uint32_t*)ws_dev);
+  // (D) decompose: key switch the a part at degree N, then split
+  k_decomp_modup<<<grid_for(N), 256, 0, st>>>(ct_in, N, q0, q1, P, p->qhinv[0], p->qhinv[1], w.dD);
+  for (int j = 0; j < 3; ++j) HE_CUDA(ntt_forward(c->ntt[j], w.dD + (size_t)j * 2 * N, 2, N, st), "NTT(digits)");
+  k_mac<<<grid_for(N), 256, 0, st>>>(w.dD, ksk_dec, N, N, p->M, w.dUW);
+  for (int j = 0; j < 3; ++j) HE_CUDA(ntt_inverse(c->ntt[j], w.dUW + (size_t)j * 2 * N, 2, N, st), "INTT(U,W)");
+  k_decomp_split<<<grid_for((uint64_t)p->p_in * n), 256, 0, st>>>(w.dUW, ct_in, N, n, p->p_in, q0, q1, P, p->pinv[0],
+                                                                   p->pinv[1], w.pieces);
+  for (int L = 0; L < 2; ++L)
+    HE_CUDA(ntt_forward(c->ntt_rh[L], w.pieces + (size_t)L * p->p_in * 2 * n, p->p_in * 2, n, st), "NTT(pieces)");
+  // (M) row ciphertexts
+  const uint64_t leaves = leaves_of(p);
+  k_rh_mvm<<<grid_for(2 * leaves * n), 256, 0, st>>>(p->wpt, w.pieces, leaves, p->p_in, n, p->M, w.A0);
+  // (P) PackLWEs, one batched level at a time
+  uint32_t* A = w.A0;
+  uint32_t* An = w.A1;
+  uint32_t cnt = (uint32_t)leaves;
+  const uint32_t* perm_base = p->tables;
+  const uint32_t* mono_base = p->tables + (size_t)p->logn * n;
+  for (uint32_t lv = 1; lv <= p->logn; ++lv) {
+    const uint32_t cnt_out = cnt / 2, half = n >> lv;
+    const uint64_t cn = (uint64_t)cnt_out * n;
+    k_pack_comb1<<<grid_for(2 * cn), 256, 0, st>>>(A, cnt, half, n, mono_base + (size_t)(lv - 1) * 2 * n,
+                                                   perm_base + (size_t)(lv - 1) * n, q0, q1, An, w.T, w.C);
+    for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt_rh[L], w.C + (size_t)L * cn, cnt_out, n, st), "INTT(T_a)");
+    // own-modulus digits need T_a in NTT form laid out [L][cnt][n]: reuse UW as that view
+    k_pack_aview<<<grid_for(2 * cn), 256, 0, st>>>(w.T, cnt_out, n, w.UW);
+    k_modup<<<grid_for(cn), 256, 0, st>>>(w.C, w.UW, cn, q0, q1, P, p->qhinv[0], p->qhinv[1], w.D, 0, 0);
+    HE_CUDA(ntt_forward(c->ntt_rh[0], w.D + (0 * 2 + 1) * cn, cnt_out, n, st), "NTT(d1 mod q0)");
+    HE_CUDA(ntt_forward(c->ntt_rh[1], w.D + (1 * 2 + 0) * cn, cnt_out, n, st), "NTT(d0 mod q1)");
+    HE_CUDA(ntt_forward(c->ntt_rh[2], w.D + (2 * 2 + 0) * cn, 2 * cnt_out, n, st), "NTT(d mod P)");
+    k_mac<<<grid_for(cn), 256, 0, st>>>(w.D, gal + (size_t)(lv - 1) * 12 * n, n, cn, p->M, w.UW);
+    HE_CUDA(ntt_inverse(c->ntt_rh[2], w.UW + 2 * 2 * cn, 2 * cnt_out, n, st), "INTT(U_P, W_P)");
+    k_moddown_lift<<<grid_for(2 * cn), 256, 0, st>>>(w.UW + 2 * 2 * cn, cn, P, q0, q1, w.LB);
+    HE_CUDA(ntt_forward(c->ntt_rh[0], w.LB, 2 * cnt_out, n, st), "NTT(lift q0)");
+    HE_CUDA(ntt_forward(c->ntt_rh[1], w.LB + 2 * cn, 2 * cnt_out, n, st), "NTT(lift q1)");
+    k_pack_comb2<<<grid_for(2 * cn), 256, 0, st>>>(w.UW, w.LB, w.T, cnt_out, n, q0, q1, p->pinv[0], p->pinv[1], An);
+    uint32_t* tmp = A;
+    A = An;
+    An = (lv == 1) ? w.A0 : tmp;  // level 1 frees A0 for reuse as the next output
+    cnt = cnt_out;
+  }
+  // (R) + (C)
+  for (int L = 0; L < 2; ++L)
+    HE_CUDA(ntt_inverse(c->ntt_rh[L], A + (size_t)L * cnt * 2 * n, cnt * 2, n, st), "INTT(packed)");
+  HE_CUDA(cudaMemsetAsync(out, 0, 2ull * N * sizeof(uint32_t), st), "memset");
+  k_rh_rescale_compose<<<grid_for((uint64_t)cnt * 2 * n), 256, 0, st>>>(A, cnt, n, N, q0, q1, p->q1inv, p->q1invp, out);
+  HE_CUDA(cudaGetLastError(), "rhombus launch");
+  if (ledger) {
+    ledger->pc_mults += (int64_t)p->n_out * p->p_in;
+    ledger->ct_rotations += (int64_t)(n - 1) * p->p_out;
+    ledger->rescales += 1;
+  }
+  return HE_OK;
+}

@@ -25,13 +25,15 @@ EXPORTS = (
     "he_encrypt_acts", "he_decrypt_rlwe", "he_decrypt_mlwe", "he_ntt_forward", "he_ntt_inverse",
     "he_pcmm_weight_maxabs", "he_pcmm_encode_weights", "he_pcmm_plan_create", "he_pcmm_plan_destroy",
     "he_pcmm_workspace_bytes", "he_pcmm_run", "he_pcmm_decompose", "he_pcmm_gemm",
+    "he_encrypt_vector", "he_rhombus_keygen", "he_rhombus_weight_bytes", "he_rhombus_encode_weights",
+    "he_rhombus_plan_create", "he_rhombus_plan_destroy", "he_rhombus_workspace_bytes", "he_rhombus_run",
 )
 
 
 class HeParamsC(ctypes.Structure):
     _fields_ = [("mlwe_degree", ctypes.c_uint32), ("mlwe_rank", ctypes.c_uint32),
                 ("moduli", ctypes.c_uint32 * 2), ("log_delta", ctypes.c_uint32),
-                ("rhombus_degree", ctypes.c_uint32)]
+                ("rhombus_degree", ctypes.c_uint32), ("special_prime", ctypes.c_uint32)]
 
 
 class HeLedgerC(ctypes.Structure):
@@ -77,6 +79,14 @@ def lib():
             "he_pcmm_run": (st, [vp, vp, u32, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_pcmm_decompose": (st, [vp, vp, vp, u64, vp]),
             "he_pcmm_gemm": (st, [vp, vp, vp, vp, vp]),
+            "he_encrypt_vector": (st, [vp, vp, vp, u32, u64, u32, vp, vp]),
+            "he_rhombus_keygen": (st, [vp, u64, vp, vp, vp, vp, vp, vp, vp]),
+            "he_rhombus_weight_bytes": (st, [vp, u32, u32, ctypes.POINTER(u64)]),
+            "he_rhombus_encode_weights": (st, [vp, vp, u32, u32, vp, vp]),
+            "he_rhombus_plan_create": (st, [vp, vp, u32, u32, ctypes.POINTER(vp)]),
+            "he_rhombus_plan_destroy": (st, [vp]),
+            "he_rhombus_workspace_bytes": (st, [vp, ctypes.POINTER(u64)]),
+            "he_rhombus_run": (st, [vp, vp, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

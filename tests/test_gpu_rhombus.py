@@ -1,0 +1,74 @@
+"""Rhombus PCMv on the GPU vs the CPU oracle (he_oracle_rhombus.c): every output word
+bit-exact at toy size; decrypted W v within the stated precision at Llama shapes."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2601_18511_b200 import HeContext, HeParams
+from paper_2601_18511_b200.errors import NeedsBootstrapError
+from paper_2601_18511_b200.rhombus import (CtVector, clear_pcmv, decrypt_vector, encrypt_vector, make_rhombus_plan,
+                                           pcmv_rhombus, rhombus_keygen)
+
+pytestmark = pytest.mark.gpu
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _setup(P, n_out, n_in, seed=0):
+    ctx = HeContext(P)
+    rng = np.random.default_rng(seed)
+    v = rng.uniform(-1, 1, n_in)
+    W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
+    sk = ctx.keygen(7)
+    keys = rhombus_keygen(ctx, sk, 99)
+    x = encrypt_vector(ctx, sk, v, seed=5)
+    return ctx, sk, keys, x, v, W
+
+
+@pytest.mark.parametrize("n_out,n_in", [(200, 300), (512, 512), (64, 100)])
+def test_toy_pcmv_bit_exact(n_out, n_in):
+    P = HeParams.toy()
+    ctx, sk, keys, x, v, W = _setup(P, n_out, n_in)
+    s = O.keygen(P, 7)
+    s_small, s_up, ksk, gal = O.rhombus_keys(P, 99, s)
+    assert np.array_equal(keys.s_small.cpu().numpy(), s_small)
+    assert np.array_equal(keys.s_up.cpu().numpy(), s_up)
+    ct = O.encrypt(P, 5, s, O.encode_vector(P, v))[0]
+    assert np.array_equal(u32(x.data), ct)
+    plan = make_rhombus_plan(ctx, W)
+    before = ctx.ledger.snapshot()
+    y = pcmv_rhombus(ctx, plan, keys, x)
+    diff = ctx.ledger.diff(before)
+    assert diff["rescales"] == 1 and diff["ct_rotations"] == (P.rhombus_degree - 1) * -(-n_out // P.rhombus_degree)
+    _, out = O.rhombus_pcmv(P, ct, ksk, gal, O.rhombus_weights(P, W), n_in)
+    assert np.array_equal(u32(y.data)[0], out)
+    res = decrypt_vector(ctx, keys.s_up_ntt, y)
+    err = np.abs(res - clear_pcmv(W, v)).max()
+    assert err < 2 ** -14, err
+
+
+def test_pcmv_errors():
+    P = HeParams.toy()
+    ctx, sk, keys, x, v, W = _setup(P, 32, 40)
+    plan = make_rhombus_plan(ctx, W)
+    with pytest.raises(TypeError):
+        pcmv_rhombus(ctx, plan, keys, np.zeros(3))
+    with pytest.raises(ValueError, match="dim mismatch"):
+        pcmv_rhombus(ctx, make_rhombus_plan(ctx, np.zeros((32, 41))), keys, x)
+    with pytest.raises(NeedsBootstrapError):
+        pcmv_rhombus(ctx, plan, keys, CtVector(x.data, 0, x.n_vals))
+
+
+@pytest.mark.parametrize("n_out,n_in", [(4096, 11008), (14336, 4096)])
+def test_llama_pcmv_precision(n_out, n_in):
+    """BASELINE config 5 shapes at N' = 4096: decrypted W v vs the float product."""
+    P = HeParams.llama()
+    ctx, sk, keys, x, v, W = _setup(P, n_out, n_in, seed=3)
+    plan = make_rhombus_plan(ctx, W)
+    y = pcmv_rhombus(ctx, plan, keys, x)
+    res = decrypt_vector(ctx, keys.s_up_ntt, y)
+    err = np.abs(res - clear_pcmv(W, v)).max()
+    assert err < 2 ** -12, err

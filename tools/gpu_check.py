@@ -111,7 +111,7 @@ def main():
     print("ALL OK" if ok else "FAILURES")
 
 
-if __name__ == "__main__" and "--time" not in sys.argv:
+if __name__ == "__main__" and "--time" not in sys.argv and "--rhombus" not in sys.argv:
     main()
 
 
@@ -152,3 +152,38 @@ def time_shape(n_out, n_in, iters=5):
 
 if __name__ == "__main__" and "--time" in sys.argv:
     time_shape(4096, 11008)
+
+
+def time_rhombus(shapes=((4096, 11008), (14336, 4096)), iters=3):
+    from paper_2601_18511_b200.rhombus import (clear_pcmv, decrypt_vector, encrypt_vector, make_rhombus_plan,
+                                               pcmv_rhombus, rhombus_keygen)
+    P = HeParams.llama()
+    ctx = HeContext(P)
+    sk = ctx.keygen(7)
+    t0 = time.time()
+    keys = rhombus_keygen(ctx, sk, 99)
+    torch.cuda.synchronize()
+    print(f"rhombus keygen {time.time() - t0:.2f} s")
+    for n_out, n_in in shapes:
+        rng = np.random.default_rng(1)
+        v = rng.uniform(-1, 1, n_in)
+        W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
+        x = encrypt_vector(ctx, sk, v, seed=5)
+        plan = make_rhombus_plan(ctx, W)
+        y = pcmv_rhombus(ctx, plan, keys, x)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            y = pcmv_rhombus(ctx, plan, keys, x)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        res = decrypt_vector(ctx, keys.s_up_ntt, y)
+        err = np.abs(res - clear_pcmv(W, v)).max()
+        print(f"rhombus PCMv {n_out}x{n_in}: {min(ts):.3f} ms (all {['%.2f' % t for t in ts]}), err {err:.2e} = {-np.log2(err):.1f} bits")
+
+
+if __name__ == "__main__" and "--rhombus" in sys.argv:
+    time_rhombus()
