@@ -254,12 +254,14 @@ def run_ours(a, rank: int, world: int, local: int):
 
 
 def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
-    """Same op through pcmm_mlwe with host buffers: pinned H2D of the input ciphertexts
-    (rank 0) and D2H of the whole output (rank 0) inside the timed region."""
+    """Same op through the public API with host buffers: pinned H2D of the input ciphertexts
+    and D2H of the whole output inside the timed region.  N = 1: pcmm_mlwe_to_host (the K1
+    row chunks stream to host memory while the next chunk computes); N > 1: broadcast,
+    sharded pcmm_mlwe, all-gather, then rank 0 copies the gathered output to the host."""
     import torch
     import torch.distributed as dist
 
-    from paper_2601_18511_b200 import pcmm_mlwe
+    from paper_2601_18511_b200 import pcmm_mlwe, pcmm_mlwe_to_host
 
     steps = a.e2e_steps or max(1, min(a.steps, 5))
     h_in = torch.empty(X.data.shape, dtype=torch.int32, pin_memory=True)
@@ -270,14 +272,15 @@ def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
     stream = torch.cuda.current_stream(dev)
 
     def step():
+        if world == 1:
+            pcmm_mlwe_to_host(ctx, plan, X, h_b[: plan.n_out // ctx.params.mlwe_rank], h_a[: plan.n_out], x_host=h_in)
+            return
         if rank == 0:
             X.data.copy_(h_in, non_blocking=True)
-        if world > 1:
-            dist.broadcast(X.data, src=0)
+        dist.broadcast(X.data, src=0)
         pcmm_mlwe(ctx, plan, X, out=Y)
-        if world > 1:
-            dist.all_gather_into_tensor(all_b, out_b)
-            dist.all_gather_into_tensor(all_a, out_a)
+        dist.all_gather_into_tensor(all_b, out_b)
+        dist.all_gather_into_tensor(all_a, out_a)
         if rank == 0:
             h_b.copy_(src_b, non_blocking=True)
             h_a.copy_(src_a, non_blocking=True)
@@ -298,8 +301,10 @@ def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0])
     return {"value": round(ms, 3), "unit": "ms/op", "h2d_bytes_per_step": int(h_in.numel() * 4),
-            "d2h_bytes_per_step": int((h_b.numel() + h_a.numel()) * 4), "steps": steps,
-            "path": "pcmm_mlwe (he_pcmm_run) with pinned host buffers"}
+            "d2h_bytes_per_step": int((plan.n_out // ctx.params.mlwe_rank + plan.n_out) * ctx.params.N * 4)
+            if world == 1 else int((h_b.numel() + h_a.numel()) * 4), "steps": steps,
+            "path": "pcmm_mlwe_to_host (K1 row chunks streamed to pinned host memory)" if world == 1
+            else "broadcast + pcmm_mlwe + all_gather + D2H on rank 0"}
 
 
 def measure_cublas_int8(dev):

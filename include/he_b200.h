@@ -122,6 +122,11 @@ he_status he_pcmm_decompose(const he_pcmm_plan* plan, const uint32_t* ct_in_dev,
                             uint64_t workspace_bytes, void* stream);
 he_status he_pcmm_gemm(const he_pcmm_plan* plan, const void* workspace_dev, uint32_t* out_b_dev,
                        uint32_t* out_a_dev, void* stream);
+/* K1 on output rows [row0, row0 + rows) only (k-aligned), writing the chunk's b' blocks and a'
+ * rows to out_b_dev [rows/k][N] / out_a_dev [rows][k*d]: lets a caller stream the output to
+ * host memory chunk by chunk while the next chunk computes (pcmm_mlwe_to_host). */
+he_status he_pcmm_gemm_rows(const he_pcmm_plan* plan, const void* workspace_dev, uint32_t row0, uint32_t rows,
+                            uint32_t* out_b_dev, uint32_t* out_a_dev, void* stream);
 
 /* ---------------------------------------------------------------- Rhombus PCMv (K6), degree n = rhombus_degree */
 /* Vector layout (App. A + h): element e sits at degree-N coefficient

@@ -50,11 +50,11 @@ static PFN_encodeTiled_t encode_fn() {
 }
 // 3-D int8 tensor {inner, rows, planes}, box {128, box_rows, 1}, 128-B swizzle, OOB -> 0
 static he_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t planes,
-                          uint32_t box_rows) {
+                          uint32_t box_rows, uint64_t plane_stride = 0) {
   PFN_encodeTiled_t fn = encode_fn();
   if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {inner, rows, planes};
-  cuuint64_t strides[2] = {inner, inner * rows};
+  cuuint64_t strides[2] = {inner, plane_stride ? plane_stride : inner * rows};
   cuuint32_t box[3] = {128, box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
@@ -364,9 +364,11 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
   return HE_OK;
 }
 
-extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_t* out_b, uint32_t* out_a,
-                                  void* stream) {
+extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows,
+                                       uint32_t* out_b, uint32_t* out_a, void* stream) {
   if (!p || !ws || !out_b || !out_a) return fail(HE_EINVAL, "null argument");
+  if (rows == 0 || row0 % p->ctx->R.k || rows % p->ctx->R.k || row0 + rows > p->n_out)
+    return fail(HE_EINVAL, "row range [%u, %u) must be k-aligned and inside [0, %u)", row0, row0 + rows, p->n_out);
   static int variant = [] {
     const char* v = getenv("HE_GEMM_VARIANT");  // profiling switch: 1 = single-CTA kernel
     return (v && v[0] == '1') ? 1 : 2;
@@ -386,8 +388,13 @@ extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_
   if (env_bn == 32 || (env_bn == 48 && bn2 == 48)) bn2 = env_bn;
   he_status s = make_map(&tmB, ws, p->n_in, p->width, p->d0 + p->d1, variant == 1 ? kGemmBoxRows1 : bn2 / 2);
   if (s) return s;
+  CUtensorMap tmA = p->tmA;
+  if (row0 != 0 || rows != p->n_out) {
+    s = make_map(&tmA, p->digits + (size_t)row0 * p->n_in, p->n_in, rows, p->d_w, 128, (uint64_t)p->n_out * p->n_in);
+    if (s) return s;
+  }
   GemmArgs a;
-  a.n_out = (int)p->n_out;
+  a.n_out = (int)rows;
   a.n_in = (int)p->n_in;
   a.width = (int)p->width;
   a.d = (int)p->ctx->R.d;
@@ -403,16 +410,22 @@ extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_
   a.hint_b = hint("HE_GEMM_HINT_B", 0x1000000000000000ULL);  // evict_normal: measured 46 vs 64 GB DRAM reads
   int grid;
   if (variant == 1) {
-    const int tiles = (int)((p->n_out + 127) / 128) * (int)(p->width / 32);
+    const int tiles = (int)((rows + 127) / 128) * (int)(p->width / 32);
     grid = tiles < p->ctx->sm_count ? tiles : p->ctx->sm_count;
   } else {
-    const int tiles = (int)((p->n_out + 255) / 256) * (int)((p->width + bn2 - 1) / bn2);
+    const int tiles = (int)((rows + 255) / 256) * (int)((p->width + bn2 - 1) / bn2);
     const int pairs = p->ctx->sm_count / 2;
     grid = 2 * (tiles < pairs ? tiles : pairs);
   }
-  HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, p->tmA, tmB, a, grid, (cudaStream_t)stream),
+  HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, tmA, tmB, a, grid, (cudaStream_t)stream),
           "modgemm");
   return HE_OK;
+}
+
+extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_t* out_b, uint32_t* out_a,
+                                  void* stream) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  return he_pcmm_gemm_rows(p, ws, 0, p->n_out, out_b, out_a, stream);
 }
 
 extern "C" he_status he_pcmm_run(const he_pcmm_plan* p, const uint32_t* ct_in, uint32_t level, uint32_t* out_b,

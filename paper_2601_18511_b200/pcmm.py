@@ -45,6 +45,8 @@ class MlwePcmmPlan:
     layout: str = "app_a_coeff"
     _handle: object = field(default=None, repr=False)
     _workspace: object = field(default=None, repr=False)
+    _stream_bufs: object = field(default=None, repr=False)
+    _copy_stream: object = field(default=None, repr=False)
 
     @property
     def shape(self) -> tuple[int, int]:
@@ -156,6 +158,58 @@ def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks |
     out.level = X.level - 1
     out.n_rows = plan.n_out
     return out
+
+
+def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_host, out_a_host,
+                      x_host=None, chunk_rows: int = 512) -> MlweBlocks:
+    """The same op as ``pcmm_mlwe`` with the level-0 output streamed into (pinned) host
+    buffers ``out_b_host`` [n_out/k, N] and ``out_a_host`` [n_out, N]: K1 runs over row
+    chunks into two alternating device slices while a second stream copies the previous
+    chunk to the host, so the 1 GB device->host transfer overlaps the GEMM.  ``x_host``
+    (pinned, X.data's shape) is first copied into ``X.data`` on the current stream."""
+    torch = _torch()
+    _check_operand(ctx, plan, X)
+    p = ctx.params
+    k, N = p.mlwe_rank, p.N
+    if chunk_rows % 256 or chunk_rows % k or chunk_rows <= 0:
+        raise ValueError("chunk_rows must be a positive multiple of 256 and of k")
+    if tuple(out_a_host.shape) != (plan.n_out, N) or tuple(out_b_host.shape) != (plan.n_out // k, N):
+        raise ValueError("host output buffers have the wrong shape")
+    dev = ctx.device
+    st = torch.cuda.current_stream(dev)
+    if x_host is not None:
+        X.data.copy_(x_host, non_blocking=True)
+    ws = plan.workspace(dev)
+    if getattr(plan, "_stream_bufs", None) is None or plan._stream_bufs[0][1].shape[0] != chunk_rows:
+        plan._stream_bufs = [(torch.empty((chunk_rows // k, N), dtype=torch.int32, device=dev),
+                              torch.empty((chunk_rows, N), dtype=torch.int32, device=dev)) for _ in range(2)]
+        plan._copy_stream = torch.cuda.Stream(dev)
+    cs = plan._copy_stream
+    native.call("he_pcmm_decompose", plan._handle, X.data.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+    copied = [None, None]
+    for c, row0 in enumerate(range(0, plan.n_out, chunk_rows)):
+        rows = min(chunk_rows, plan.n_out - row0)
+        slot = c % 2
+        if copied[slot] is not None:
+            st.wait_event(copied[slot])               # the slot's previous chunk has left the device
+        bb, ba = plan._stream_bufs[slot]
+        native.call("he_pcmm_gemm_rows", plan._handle, ws.data_ptr(), row0, rows, bb.data_ptr(), ba.data_ptr(),
+                    st.cuda_stream)
+        done = torch.cuda.Event()
+        done.record(st)
+        cs.wait_event(done)
+        with torch.cuda.stream(cs):
+            out_a_host[row0:row0 + rows].copy_(ba[:rows], non_blocking=True)
+            out_b_host[row0 // k:(row0 + rows) // k].copy_(bb[:rows // k], non_blocking=True)
+        copied[slot] = torch.cuda.Event()
+        copied[slot].record(cs)
+    for ev in copied:
+        if ev is not None:
+            st.wait_event(ev)
+    ctx.ledger.pc_mults += (plan.n_out // k) * (plan.n_in // k)
+    ctx.ledger.rescales += plan.n_out // k
+    ctx.ledger.observe_level(X.level - 1)
+    return MlweBlocks(out_b_host, out_a_host, level=X.level - 1, n_rows=plan.n_out)
 
 
 def pcmm_ops(params, n_out: int, n_in: int, d_w: int) -> int:

@@ -211,3 +211,23 @@ def test_ntt_roundtrip_and_product():
             native.call("he_ntt_forward", ctx.handle, t.data_ptr(), n, limb, 3, n, ctx.stream())
             native.call("he_ntt_inverse", ctx.handle, t.data_ptr(), n, limb, 3, n, ctx.stream())
             assert np.array_equal(u32(t), a)
+
+
+def test_streamed_to_host_matches_device_output():
+    """pcmm_mlwe_to_host (row chunks of K1 streamed to pinned host memory) == pcmm_mlwe."""
+    import torch
+
+    from paper_2601_18511_b200 import pcmm_mlwe_to_host
+
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, 1280, 512)
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    Y = pcmm_mlwe(ctx, plan, X)
+    hb = torch.empty(tuple(Y.out_b.shape), dtype=torch.int32, pin_memory=True)
+    ha = torch.empty(tuple(Y.out_a.shape), dtype=torch.int32, pin_memory=True)
+    x_host = X.data.cpu().pin_memory()
+    before = ctx.ledger.snapshot()
+    pcmm_mlwe_to_host(ctx, plan, X, hb, ha, x_host=x_host, chunk_rows=512)
+    torch.cuda.synchronize()
+    assert ctx.ledger.diff(before)["rescales"] == 5
+    assert torch.equal(ha, Y.out_a.cpu()) and torch.equal(hb, Y.out_b.cpu())
