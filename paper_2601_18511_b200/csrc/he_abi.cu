@@ -64,6 +64,22 @@ static he_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint
   return HE_OK;
 }
 
+// 4-D int8 tensor with explicit strides (bytes), box {128, box_rows, 1, 1}, 128-B swizzle
+static he_status make_map4(CUtensorMap* m, const void* base, const uint64_t dims_in[4], const uint64_t strides_in[3],
+                           uint32_t box_rows) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {dims_in[0], dims_in[1], dims_in[2], dims_in[3]};
+  cuuint64_t strides[3] = {strides_in[0], strides_in[1], strides_in[2]};
+  cuuint32_t box[4] = {128, box_rows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled (4-D) failed (%d)", (int)r);
+  return HE_OK;
+}
+
 // ---------------------------------------------------------------- context
 static int digits_for(uint32_t q) {
   // balanced 8-bit digits for a centred residue |c| <= q/2
@@ -345,7 +361,33 @@ extern "C" he_status he_pcmm_plan_destroy(he_pcmm_plan* p) {
   return HE_OK;
 }
 
-static uint64_t ws_bytes(const he_pcmm_plan* p) { return (uint64_t)(p->d0 + p->d1) * p->width * p->n_in; }
+// K3 fused into K1 (compact digit planes + 16-byte shifted copies) -- opt-in (HE_GEMM_FUSED=1).
+// Measured (profiles/r01/ncu_full_modgemm_fused.json): DRAM reads 56 -> 2.2 GB per launch, but the
+// 16-B-aligned window rows split every 128-B TMA row over two L2 lines, doubling L2 requests; K1 is
+// L2-request-rate bound at ~6e10 requests/s, so the fused GEMM takes 54 ms vs 25 ms materialised.
+// Valid when the K-blocks of 128 stay inside one RLWE ct and the 32-column tiles inside one key
+// component: k % 128 == 0, d % 32 == 0.
+static int gemm_variant() {
+  static int variant = [] {
+    const char* v = getenv("HE_GEMM_VARIANT");  // profiling switch: 1 = single-CTA kernel
+    return (v && v[0] == '1') ? 1 : 2;
+  }();
+  return variant;
+}
+static bool fused_path(const he_pcmm_plan* p) {
+  static const bool on = getenv("HE_GEMM_FUSED") != nullptr;  // profiling switch
+  const uint32_t k = p->ctx->R.k, d = p->ctx->R.d;
+  return on && gemm_variant() == 2 && k % 128 == 0 && d % 32 == 0;
+}
+static uint64_t fused_stride(const he_pcmm_plan* p) { return (uint64_t)p->ctx->R.N + 2ull * p->ctx->R.k; }
+static uint64_t fused_a_bytes(const he_pcmm_plan* p) {
+  return 16ull * (p->d0 + p->d1) * (p->n_in / p->ctx->R.k) * fused_stride(p);
+}
+static uint64_t ws_bytes(const he_pcmm_plan* p) {
+  if (fused_path(p))
+    return fused_a_bytes(p) + (uint64_t)(p->d0 + p->d1) * (p->n_in / p->ctx->R.k) * p->ctx->R.N;
+  return (uint64_t)(p->d0 + p->d1) * p->width * p->n_in;
+}
 
 extern "C" he_status he_pcmm_workspace_bytes(const he_pcmm_plan* p, uint64_t* bytes) {
   if (!p || !bytes) return fail(HE_EINVAL, "null argument");
@@ -358,6 +400,12 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
   if (!p || !ct_in || !ws) return fail(HE_EINVAL, "null argument");
   if (ws_size < ws_bytes(p)) return fail(HE_EINVAL, "workspace too small (%llu < %llu)", (unsigned long long)ws_size,
                                          (unsigned long long)ws_bytes(p));
+  if (fused_path(p)) {
+    HE_CUDA(launch_digitize(p->ctx->R, ct_in, p->n_in / p->ctx->R.k, (int)p->d0, (int)p->d1, (uint32_t)fused_stride(p),
+                            (int8_t*)ws, (int8_t*)ws + fused_a_bytes(p), (cudaStream_t)stream),
+            "digitize");
+    return HE_OK;
+  }
   HE_CUDA(launch_decompose(p->ctx->R, ct_in, p->n_in, (int)p->d0, (int)p->d1, (int8_t*)ws,
                            (uint64_t)p->width * p->n_in, (cudaStream_t)stream),
           "decompose");
@@ -369,11 +417,8 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
   if (!p || !ws || !out_b || !out_a) return fail(HE_EINVAL, "null argument");
   if (rows == 0 || row0 % p->ctx->R.k || rows % p->ctx->R.k || row0 + rows > p->n_out)
     return fail(HE_EINVAL, "row range [%u, %u) must be k-aligned and inside [0, %u)", row0, row0 + rows, p->n_out);
-  static int variant = [] {
-    const char* v = getenv("HE_GEMM_VARIANT");  // profiling switch: 1 = single-CTA kernel
-    return (v && v[0] == '1') ? 1 : 2;
-  }();
-  CUtensorMap tmB;
+  const int variant = gemm_variant();
+  const bool fused = fused_path(p);
   // profiling knobs (defaults are the tuned choice): HE_GEMM_BN, HE_GEMM_GROUP_M, HE_GEMM_HINT_A/B
   static const int env_bn = getenv("HE_GEMM_BN") ? atoi(getenv("HE_GEMM_BN")) : 0;
   static const int env_gm = getenv("HE_GEMM_GROUP_M") ? atoi(getenv("HE_GEMM_GROUP_M")) : 0;
@@ -386,8 +431,24 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
   };
   int bn2 = gemm2_tile_n((int)p->d_w, (int)p->d0, (int)p->d1);
   if (env_bn == 32 || (env_bn == 48 && bn2 == 48)) bn2 = env_bn;
-  he_status s = make_map(&tmB, ws, p->n_in, p->width, p->d0 + p->d1, variant == 1 ? kGemmBoxRows1 : bn2 / 2);
-  if (s) return s;
+  if (fused) bn2 = 32;  // tiles must not straddle a key component j
+  CUtensorMap tmB, tmBa;
+  he_status s;
+  if (fused) {
+    const uint64_t n_ct = p->n_in / p->ctx->R.k, k = p->ctx->R.k, N = p->ctx->R.N, S = fused_stride(p);
+    const uint64_t planes = p->d0 + p->d1;
+    const uint64_t bd[4] = {k, p->ctx->R.d, n_ct, planes}, bs[3] = {k, N, N * n_ct};
+    s = make_map4(&tmB, (const int8_t*)ws + fused_a_bytes(p), bd, bs, bn2 / 2);
+    if (s) return s;
+    // overlapping rows: extent k + 128 bytes, stride k bytes (every window starts 16-B aligned)
+    const uint64_t ad[4] = {k + 128, N / k + 2, n_ct, 16 * planes}, as[3] = {k, S, S * n_ct};
+    s = make_map4(&tmBa, ws, ad, as, bn2 / 2);
+    if (s) return s;
+  } else {
+    s = make_map(&tmB, ws, p->n_in, p->width, p->d0 + p->d1, variant == 1 ? kGemmBoxRows1 : bn2 / 2);
+    if (s) return s;
+    tmBa = tmB;
+  }
   CUtensorMap tmA = p->tmA;
   if (row0 != 0 || rows != p->n_out) {
     s = make_map(&tmA, p->digits + (size_t)row0 * p->n_in, p->n_in, rows, p->d_w, 128, (uint64_t)p->n_out * p->n_in);
@@ -404,6 +465,7 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
   a.c = p->epi;
   a.group_m = env_gm > 0 ? env_gm : 8;
   a.tile_n = bn2;
+  a.fused = fused ? 1 : 0;
   static const int env_skip = getenv("HE_GEMM_EPI_SKIP") ? 1 : 0;
   a.epi_skip = env_skip;
   a.hint_a = hint("HE_GEMM_HINT_A", 0x14F0000000000000ULL);
@@ -417,7 +479,7 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
     const int pairs = p->ctx->sm_count / 2;
     grid = 2 * (tiles < pairs ? tiles : pairs);
   }
-  HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, tmA, tmB, a, grid, (cudaStream_t)stream),
+  HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, tmA, tmB, tmBa, a, grid, (cudaStream_t)stream),
           "modgemm");
   return HE_OK;
 }

@@ -88,6 +88,83 @@ cudaError_t launch_decompose(const RingDims& R, const uint32_t* ct, uint32_t n_i
   return cudaGetLastError();
 }
 
+// ================================================================ K3 (fused-path form): compact digit planes
+// For K1's on-the-fly producer (he_modgemm.cu, fused): instead of materialising every GEMM column,
+// write per RLWE ct r and digit plane p
+//   b planes  [p][r][N]            digit_p(b_r[i])
+//   a copies  [p][s][r][S]         digit_p(X[i + s]),  X[i'] = a_r[i' - k] read negacyclically,
+//                                  s = 0..15 (16-byte shifted copies: every ã window a_r[t - j + k m]
+//                                  then starts 16-byte aligned in copy s = -j mod 16)
+// ~340 MB at 4096x11008 instead of the 5 GB materialised operand.
+HE_D void digits16(const uint32_t* v, uint32_t q, uint4* out /* [4 planes] */) {
+  uint32_t w[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const uint32_t c = v[e] > (q >> 1) ? v[e] - q : v[e];
+    w[e] = (c + 0x80808080u) ^ 0x80808080u;
+  }
+  uint32_t pk[4][4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const uint32_t lo01 = __byte_perm(w[4 * g], w[4 * g + 1], 0x5140), hi01 = __byte_perm(w[4 * g], w[4 * g + 1], 0x7362);
+    const uint32_t lo23 = __byte_perm(w[4 * g + 2], w[4 * g + 3], 0x5140),
+                   hi23 = __byte_perm(w[4 * g + 2], w[4 * g + 3], 0x7362);
+    pk[0][g] = __byte_perm(lo01, lo23, 0x5410);
+    pk[1][g] = __byte_perm(lo01, lo23, 0x7632);
+    pk[2][g] = __byte_perm(hi01, hi23, 0x5410);
+    pk[3][g] = __byte_perm(hi01, hi23, 0x7632);
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) out[p] = make_uint4(pk[p][0], pk[p][1], pk[p][2], pk[p][3]);
+}
+
+__global__ void __launch_bounds__(256) digitize_kernel(const uint32_t* __restrict__ ct, uint32_t n_ct, uint32_t k,
+                                                       uint32_t N, uint32_t q0, uint32_t q1, int d0, int d1, uint32_t S,
+                                                       int8_t* __restrict__ out_a, int8_t* __restrict__ out_b) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;  // 16-byte group
+  const uint32_t r = blockIdx.y, z = blockIdx.z;              // z < 16: shift copy; z == 16: b planes
+  const uint32_t i0 = 16 * g;
+  if (z == 16 ? i0 >= N : i0 >= S) return;
+  const uint32_t qs[2] = {q0, q1};
+#pragma unroll
+  for (int L = 0; L < 2; ++L) {
+    const uint32_t q = qs[L];
+    const uint32_t* a = ct + ((size_t)r * 2 + L) * 2 * N;
+    uint32_t v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      if (z == 16) {
+        v[e] = a[N + i0 + e];
+      } else {
+        const int64_t xi = (int64_t)i0 + e + z - (int64_t)k;  // index into a_r, negacyclic below 0
+        uint32_t val = 0;
+        if (xi >= 0 && xi < (int64_t)N) val = a[xi];
+        else if (xi < 0) {
+          const uint32_t w = a[xi + N];
+          val = w ? q - w : 0u;
+        }
+        v[e] = val;
+      }
+    }
+    uint4 dg[4];
+    digits16(v, q, dg);
+    const int nd = L == 0 ? d0 : d1, pbase = L == 0 ? 0 : d0;
+    for (int p = 0; p < nd; ++p) {
+      const uint32_t P = pbase + p;
+      int8_t* dst = z == 16 ? out_b + ((size_t)P * n_ct + r) * N + i0
+                            : out_a + (((size_t)P * 16 + z) * n_ct + r) * S + i0;
+      *reinterpret_cast<uint4*>(dst) = dg[p];
+    }
+  }
+}
+
+cudaError_t launch_digitize(const RingDims& R, const uint32_t* ct, uint32_t n_ct, int d0, int d1, uint32_t S,
+                            int8_t* out_a, int8_t* out_b, cudaStream_t s) {
+  dim3 grid((S / 16 + 255) / 256, n_ct, 17);
+  digitize_kernel<<<grid, 256, 0, s>>>(ct, n_ct, R.k, R.N, R.q[0], R.q[1], d0, d1, S, out_a, out_b);
+  return cudaGetLastError();
+}
+
 // ================================================================ weight encoding
 // W~[y][x] = round_half_even(q1 * W[k(y/k) + sigma(y%k)][k(x/k) + sigma(x%k)])
 // (block conjugation by sigma = g o nibble swap, PAPER.md:672 / bitrev.py:57-70).

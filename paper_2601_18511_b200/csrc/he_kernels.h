@@ -26,6 +26,7 @@ struct GemmArgs {
   int tile_n;           // v2 tile width (48 or 32)
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints
   int epi_skip;         // profiling only: drain TMEM without computing/storing
+  int fused;            // 1: B tiles come straight from the compact digit planes (K3 fused into K1)
   uint32_t* out_b;
   uint32_t* out_a;
   GemmEpiConst c;
@@ -36,7 +37,7 @@ int gemm_smem_bytes(int dw, int d0, int d1);
 constexpr int kGemmBoxRows1 = 32;
 int gemm2_tile_n(int dw, int d0, int d1);
 cudaError_t launch_modgemm(int variant, int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                           const GemmArgs& args, int grid, cudaStream_t stream);
+                           const CUtensorMap& tmBa, const GemmArgs& args, int grid, cudaStream_t stream);
 
 // NTT tables for one (modulus, degree)
 struct NttTable {
@@ -56,6 +57,8 @@ struct RingDims {
 
 cudaError_t launch_decompose(const RingDims& R, const uint32_t* ct, uint32_t n_in, int d0, int d1, int8_t* planes,
                              uint64_t plane_stride, cudaStream_t s);
+cudaError_t launch_digitize(const RingDims& R, const uint32_t* ct, uint32_t n_ct, int d0, int d1, uint32_t S,
+                            int8_t* out_a, int8_t* out_b, cudaStream_t s);
 cudaError_t launch_weight_maxabs(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in,
                                  unsigned long long* maxabs, cudaStream_t s);
 cudaError_t launch_encode_weights(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in, uint32_t dw,

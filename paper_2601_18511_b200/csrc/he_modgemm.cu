@@ -315,7 +315,7 @@ struct Gemm2Cfg {
 template <int DW, int D0, int D1, int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     modgemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmArgs args) {
+                    const __grid_constant__ CUtensorMap tmBa, const GemmArgs args) {
   using C = Gemm2Cfg<DW, D0, D1, BN>;
   constexpr int kBN2 = C::kBN2;
   constexpr int kChunk = C::kChunk;
@@ -347,6 +347,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    tma_prefetch(&tmBa);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 2);      // leader's expect_tx arrive + the peer's remote arrive
       mbar_init(&empty[s], 1);     // one multicast commit
@@ -365,13 +366,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // tile -> (m block of 256 rows, n block of 48 columns), M-grouped raster
+  // tile -> (m block of 256 rows, n block of kBN2 columns), M-grouped raster.  Fused path: the
+  // a-part column tiles are visited as (m-range, j mod 16, j / 16) so that consecutive tiles read
+  // the same rows of the same 16-byte-shifted digit copy (L2 reuse across key components j).
   auto tile_mn = [&](int tile, int& m0, int& n0) {
     const int per_group = gm * n_tiles;
     const int g = tile / per_group, r = tile % per_group;
     const int rows_in_group = (m_tiles - g * gm) < gm ? (m_tiles - g * gm) : gm;
     m0 = (g * gm + r % rows_in_group) * (2 * kBM);
-    n0 = (r / rows_in_group) * kBN2;
+    const int v = r / rows_in_group;
+    if (!args.fused) {
+      n0 = v * kBN2;
+    } else {
+      const int nb_b = args.d / kBN2;                  // b-part tiles first
+      if (v < nb_b) {
+        n0 = v * kBN2;
+      } else {
+        const int va = v - nb_b, J = args.k, jh_n = J / 16;
+        const int mb = va / J, rem = va % J;
+        const int j = 16 * (rem % jh_n) + rem / jh_n;
+        n0 = args.d + args.d * j + kBN2 * mb;
+      }
+    }
   };
 
   if (warp == 0) {
@@ -392,18 +408,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 #pragma unroll
           for (int a = 0; a < DW; ++a)
             tma_load_3d_2sm(a_dst + a * kBM * kBK, &tmA, &full[stage], kb * kBK, m0 + (int)rank * kBM, a, args.hint_a);
-          // stacked limb-0 operand [C0|C1|..] (D0*48 rows): this CTA holds chunks [rank*D0, rank*D0 + D0)
+          // stacked limb-i operand [C0|C1|..] (D_i * kBN2 rows): this CTA holds chunks [rank*D_i, (rank+1)*D_i)
+          const int r_ct = (kb * kBK) / args.k, t0 = (kb * kBK) % args.k;
+          auto load_chunk = [&](uint8_t* dst, int plane, int n_c) {
+            if (!args.fused) {
+              tma_load_3d_2sm(dst, &tmB, &full[stage], kb * kBK, n_c, plane, args.hint_b);
+            } else if (n_c < args.d) {             // b part: b_r[t + k m], rows m = n_c ..
+              tma_load_4d_2sm(dst, &tmB, &full[stage], t0, n_c, r_ct, plane, args.hint_b);
+            } else {                               // a part: a_r[t - j + k m] from the shift copy
+              const int j = (n_c - args.d) / args.d, m = (n_c - args.d) % args.d;
+              const int sh = (16 - (j & 15)) & 15;
+              const int I0 = t0 - j + args.k * (m + 1) - sh;
+              tma_load_4d_2sm(dst, &tmBa, &full[stage], I0 % args.k, I0 / args.k, r_ct, plane * 16 + sh, args.hint_b);
+            }
+          };
 #pragma unroll
           for (int c = 0; c < D0; ++c) {
             const int g = (int)rank * D0 + c;
-            tma_load_3d_2sm(b_dst + c * kChunk * kBK, &tmB, &full[stage], kb * kBK, n0 + (g & 1) * kChunk, g >> 1,
-                            args.hint_b);
+            load_chunk(b_dst + c * kChunk * kBK, g >> 1, n0 + (g & 1) * kChunk);
           }
 #pragma unroll
           for (int c = 0; c < D1; ++c) {
             const int g = (int)rank * D1 + c;
-            tma_load_3d_2sm(b_dst + (C::kB0Rows + c * kChunk) * kBK, &tmB, &full[stage], kb * kBK,
-                            n0 + (g & 1) * kChunk, D0 + (g >> 1), args.hint_b);
+            load_chunk(b_dst + (C::kB0Rows + c * kChunk) * kBK, D0 + (g >> 1), n0 + (g & 1) * kChunk);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -529,13 +556,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 }
 
 template <int DW, int D0, int D1, int BN>
-static cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int grid,
-                             cudaStream_t stream) {
+static cudaError_t launch2_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmBa,
+                             const GemmArgs& args, int grid, cudaStream_t stream) {
   using C = Gemm2Cfg<DW, D0, D1, BN>;
   auto kern = modgemm2_kernel<DW, D0, D1, BN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads2, C::kSmemBytes, stream>>>(tmA, tmB, args);
+  kern<<<grid, kThreads2, C::kSmemBytes, stream>>>(tmA, tmB, tmBa, args);
   return cudaGetLastError();
 }
 
@@ -561,13 +588,13 @@ int gemm_smem_bytes(int dw, int d0, int d1) {
 }
 
 cudaError_t launch_modgemm(int variant, int dw, int d0, int d1, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                           const GemmArgs& args, int grid, cudaStream_t stream) {
+                           const CUtensorMap& tmBa, const GemmArgs& args, int grid, cudaStream_t stream) {
 #define HE_CASE(a, b, c)                                                                   \
   if (dw == a && d0 == b && d1 == c) {                                                    \
     if (variant == 1) return launch_t<a, b, c>(tmA, tmB, args, grid, stream);            \
     if constexpr (gemm2_bn(a, b, c) == 48)                                                \
-      if (args.tile_n == 48) return launch2_t<a, b, c, 48>(tmA, tmB, args, grid, stream); \
-    if (args.tile_n == 32) return launch2_t<a, b, c, 32>(tmA, tmB, args, grid, stream);   \
+      if (args.tile_n == 48) return launch2_t<a, b, c, 48>(tmA, tmB, tmBa, args, grid, stream); \
+    if (args.tile_n == 32) return launch2_t<a, b, c, 32>(tmA, tmB, tmBa, args, grid, stream);   \
     return cudaErrorInvalidValue;                                                         \
   }
   HE_GEMM_INSTANCES(HE_CASE)

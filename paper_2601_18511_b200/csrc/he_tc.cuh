@@ -148,6 +148,13 @@ HE_D void tma_load_3d_2sm(void* dst, const void* map, uint64_t* bar, int x, int 
       "l"(map), "r"(smem_u32(bar) & kPeerBitMask), "r"(x), "r"(y), "r"(z), "l"(hint)
       : "memory");
 }
+HE_D void tma_load_4d_2sm(void* dst, const void* map, uint64_t* bar, int x, int y, int z, int w, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & kPeerBitMask), "r"(x), "r"(y), "r"(z), "r"(w), "l"(hint)
+      : "memory");
+}
 HE_D void tmem_alloc_2sm(uint32_t* slot, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
                : "memory");
