@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=64, help="oracle sample rows for cpu_baseline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the Rhombus PCMv / NTT side measurements")
     a = ap.parse_args()
     if a.warmup < 0 or a.steps < 1:
         ap.error("need --steps >= 1")
@@ -222,6 +223,10 @@ def run_ours(a, rank: int, world: int, local: int):
             "cublas_int8_tops_measured": cublas,
             "frac_of_2x_measured_bf16": round(achieved / (2 * measured_bf16()), 4) if measured_bf16() else None}
 
+    extras = {}
+    if rank == 0 and world == 1 and not a.no_extras:
+        extras = side_measurements(P, dev)
+
     cpu = None
     if rank == 0 and world == 1 and a.cpu_rows > 0:
         cpu = cpu_baseline(P, A, plan, X, n_out, n_in, a.cpu_rows, W_seed_dev=dev, g_seed=20260117)
@@ -247,6 +252,7 @@ def run_ours(a, rank: int, world: int, local: int):
             "clocks": clk.summary(),
             "kernels_ms": {"modgemm": round(gemm_ms, 3), "decompose_and_rest": round(ms - gemm_ms, 3)},
         }
+        line.update(extras)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -305,6 +311,73 @@ def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
             if world == 1 else int((h_b.numel() + h_a.numel()) * 4), "steps": steps,
             "path": "pcmm_mlwe_to_host (K1 row chunks streamed to pinned host memory)" if world == 1
             else "broadcast + pcmm_mlwe + all_gather + D2H on rank 0"}
+
+
+def side_measurements(P, dev):
+    """The other §8 rows, measured in the same run (not the headline metric):
+    Rhombus PCMv at BASELINE config 5 shapes (device ms/op, decrypted precision) and the K2 NTT
+    throughput against HBM (algorithmic bytes = one read + one write per word)."""
+    import torch
+
+    from paper_2601_18511_b200 import (HeContext, clear_pcmv, decrypt_vector, encrypt_vector, make_rhombus_plan,
+                                       native, pcmv_rhombus, rhombus_keygen)
+
+    out = {}
+    try:
+        ctx = HeContext(P, device=dev)
+        sk = ctx.keygen(17)
+        keys = rhombus_keygen(ctx, sk, 23)
+        rh = {}
+        for n_out, n_in in ((4096, 11008), (14336, 4096)):
+            rng = np.random.default_rng(n_out + n_in)
+            v = rng.uniform(-1, 1, n_in)
+            W = rng.uniform(-1, 1, (n_out, n_in)) / math.sqrt(n_in)
+            x = encrypt_vector(ctx, sk, v, seed=5)
+            plan = make_rhombus_plan(ctx, W)
+            for _ in range(2):
+                y = pcmv_rhombus(ctx, plan, keys, x)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                y = pcmv_rhombus(ctx, plan, keys, x)
+            e1.record()
+            torch.cuda.synchronize()
+            err = float(np.abs(decrypt_vector(ctx, keys.s_up_ntt, y) - clear_pcmv(W, v)).max())
+            rh[f"{n_out}x{n_in}"] = {"ms_per_op": round(e0.elapsed_time(e1) / 5, 3),
+                                     "precision_bits": round(-math.log2(err), 1),
+                                     "key_switches": (P.rhombus_degree - 1) * -(-n_out // P.rhombus_degree) + 1}
+            del plan
+        out["rhombus_pcmv"] = {"workload": "BASELINE config 5: Rhombus PCMv at RLWE degree 4096 "
+                                           "(decompose KS -> MVM + PackLWEs -> rescale/compose), 1 GPU", **rh}
+        hbm = measured_hbm()
+        ntt = {}
+        for n, batch in ((65536, 256), (4096, 4096)):
+            q = P.moduli[0]
+            xt = torch.randint(0, q, (batch, n), dtype=torch.int64, device=dev).to(torch.int32)
+            st = ctx.stream()
+            for name in ("he_ntt_forward", "he_ntt_inverse"):
+                for _ in range(3):
+                    native.call(name, ctx.handle, xt.data_ptr(), n, 0, batch, n, st)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(10):
+                    native.call(name, ctx.handle, xt.data_ptr(), n, 0, batch, n, st)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / 10
+                gbs = 2 * 4 * n * batch / (ms * 1e-3) / 1e9
+                ntt[f"{name.split('_')[-1]} n={n} x{batch}"] = {"GB/s": round(gbs), "frac_hbm": round(gbs / hbm, 3)}
+        out["ntt"] = {"peak_GBs": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs", **ntt}
+    except Exception as exc:  # side measurements never break the headline line
+        out["side_measurement_error"] = repr(exc)
+    return out
+
+
+def measured_hbm():
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6650.0
 
 
 def measure_cublas_int8(dev):
