@@ -5,9 +5,10 @@
 // ntt_fwd / ntt_inv), so outputs agree word for word.  n = n1 * n2:
 //   "cols" pass: the log2(n1) outer stages act on n2 independent strided columns; one column per
 //               thread, all n1 (<= 16) elements in registers, twiddles warp-uniform.
-//   "rows" pass: the log2(n2) inner stages act on contiguous n2-word blocks (n2 = 8^R <= 4096), one
-//               CTA per block, n2/8 threads x 8 register-resident elements; each radix-8 round does
-//               3 stages in registers and one shared-memory exchange.
+//   "rows" pass: the log2(n2) inner stages act on contiguous n2-word blocks (n2 = 16^R <= 4096), one
+//               CTA per block, n2/16 threads x 16 register-resident elements; each radix-16 round does
+//               4 stages in registers; the first round reads global memory directly and the last writes
+//               it directly, so a 4096-point block needs two shared-memory exchanges.
 // Butterflies are Harvey-lazy (q < 2^30): values live in [0, 4q) between stages (7 integer ops per
 // butterfly), Shoup twiddles come from an interleaved (W, W') table read as 8/16-byte vectors.
 // Between the two passes of a batch the intermediate is L2-resident when the batch fits L2.
@@ -145,130 +146,155 @@ __global__ void __launch_bounds__(256) ntt_inv_cols(uint32_t* __restrict__ data,
 // smem index padding: one word per 32 to break the power-of-two strides
 HE_D uint32_t pad(uint32_t i) { return i + (i >> 5); }
 
-// forward: rounds of 3 stages, T = N2/8, N2/64, ..., 1
+// One radix-16 round = 4 CT stages on the 16 elements j0 + e*T of this thread (t = 8T .. T).
+// i0: group index of the thread's 16T block at the round's first stage, m0 = n / (16 T).
+HE_D void ct_round16(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t m0, uint32_t i0, uint32_t q2, uint32_t q) {
+  {
+    const uint2 w = __ldg(tw + m0 + i0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ct_bf(x[e], x[e + 8], w, q2, q);
+  }
+  {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(tw + 2 * m0 + 2 * i0));
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      ct_bf(x[e], x[e + 4], make_uint2(w.x, w.y), q2, q);
+      ct_bf(x[8 + e], x[12 + e], make_uint2(w.z, w.w), q2, q);
+    }
+  }
+  {
+    const uint4* p = reinterpret_cast<const uint4*>(tw + 4 * m0 + 4 * i0);
+    const uint4 wa = __ldg(p), wb = __ldg(p + 1);
+    const uint2 ws[4] = {make_uint2(wa.x, wa.y), make_uint2(wa.z, wa.w), make_uint2(wb.x, wb.y), make_uint2(wb.z, wb.w)};
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      ct_bf(x[4 * g], x[4 * g + 2], ws[g], q2, q);
+      ct_bf(x[4 * g + 1], x[4 * g + 3], ws[g], q2, q);
+    }
+  }
+  {
+    const uint4* p = reinterpret_cast<const uint4*>(tw + 8 * m0 + 8 * i0);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const uint4 w = __ldg(p + h);
+      ct_bf(x[4 * h], x[4 * h + 1], make_uint2(w.x, w.y), q2, q);
+      ct_bf(x[4 * h + 2], x[4 * h + 3], make_uint2(w.z, w.w), q2, q);
+    }
+  }
+}
+// One radix-16 GS round = 4 stages t = T .. 8T; h0 = n / (2T).
+HE_D void gs_round16(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t h0, uint32_t i0, uint32_t q2, uint32_t q) {
+  {
+    const uint4* p = reinterpret_cast<const uint4*>(tw + h0 + 8 * i0);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const uint4 w = __ldg(p + h);
+      gs_bf(x[4 * h], x[4 * h + 1], make_uint2(w.x, w.y), q2, q);
+      gs_bf(x[4 * h + 2], x[4 * h + 3], make_uint2(w.z, w.w), q2, q);
+    }
+  }
+  {
+    const uint4* p = reinterpret_cast<const uint4*>(tw + h0 / 2 + 4 * i0);
+    const uint4 wa = __ldg(p), wb = __ldg(p + 1);
+    const uint2 ws[4] = {make_uint2(wa.x, wa.y), make_uint2(wa.z, wa.w), make_uint2(wb.x, wb.y), make_uint2(wb.z, wb.w)};
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      gs_bf(x[4 * g], x[4 * g + 2], ws[g], q2, q);
+      gs_bf(x[4 * g + 1], x[4 * g + 3], ws[g], q2, q);
+    }
+  }
+  {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(tw + h0 / 4 + 2 * i0));
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      gs_bf(x[e], x[e + 4], make_uint2(w.x, w.y), q2, q);
+      gs_bf(x[8 + e], x[12 + e], make_uint2(w.z, w.w), q2, q);
+    }
+  }
+  {
+    const uint2 w = __ldg(tw + h0 / 8 + i0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) gs_bf(x[e], x[e + 8], w, q2, q);
+  }
+}
+
+// forward: rounds of 4 stages, T = N2/16, N2/256, ..., 1; first round straight from global
 template <int N2>
-__global__ void __launch_bounds__(N2 / 8) ntt_fwd_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
-                                                       const uint2* __restrict__ tw, uint32_t q, int final_reduce) {
+__global__ void __launch_bounds__(N2 / 16) ntt_fwd_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
+                                                        const uint2* __restrict__ tw, uint32_t q, int final_reduce) {
   __shared__ uint32_t s[N2 + N2 / 32];
   const uint32_t b = blockIdx.x;
   uint32_t* a = data + blockIdx.y * stride + (size_t)b * N2;
   const uint32_t tau = threadIdx.x;
   const uint32_t q2 = 2 * q;
-  for (uint32_t i = tau; i < N2 / 4; i += N2 / 8) {
-    const uint4 v = reinterpret_cast<const uint4*>(a)[i];
-    s[pad(4 * i)] = v.x;
-    s[pad(4 * i + 1)] = v.y;
-    s[pad(4 * i + 2)] = v.z;
-    s[pad(4 * i + 3)] = v.w;
-  }
-  __syncthreads();
 #pragma unroll
-  for (int T = N2 / 8; T >= 1; T /= 8) {
-    const uint32_t j0 = (tau / T) * 8 * T + (tau % T);
-    uint32_t x[8];
+  for (int T = N2 / 16; T >= 1; T /= 16) {
+    const uint32_t j0 = (tau / T) * 16 * T + (tau % T);
+    uint32_t x[16];
+    if (T == N2 / 16) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) x[e] = s[pad(j0 + e * T)];
-    // global butterfly-group index of this thread's 8T block, and m of the first stage (t = 4T)
-    const uint32_t m0 = n / (8 * T);
-    const uint32_t i0 = b * (N2 / (8 * T)) + tau / T;
-    {
-      const uint2 w = ldtw(tw, m0 + i0);
+      for (int e = 0; e < 16; ++e) x[e] = a[j0 + e * T];  // coalesced across the warp
+    } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) ct_bf(x[e], x[e + 4], w, q2, q);
+      for (int e = 0; e < 16; ++e) x[e] = s[pad(j0 + e * T)];
     }
-    {
-      const uint4 w2 = __ldg(reinterpret_cast<const uint4*>(tw + 2 * m0 + 2 * i0));
-      const uint2 wa = make_uint2(w2.x, w2.y), wb = make_uint2(w2.z, w2.w);
-      ct_bf(x[0], x[2], wa, q2, q);
-      ct_bf(x[1], x[3], wa, q2, q);
-      ct_bf(x[4], x[6], wb, q2, q);
-      ct_bf(x[5], x[7], wb, q2, q);
-    }
-    {
-      const uint4* p = reinterpret_cast<const uint4*>(tw + 4 * m0 + 4 * i0);
-      const uint4 w01 = __ldg(p), w23 = __ldg(p + 1);
-      ct_bf(x[0], x[1], make_uint2(w01.x, w01.y), q2, q);
-      ct_bf(x[2], x[3], make_uint2(w01.z, w01.w), q2, q);
-      ct_bf(x[4], x[5], make_uint2(w23.x, w23.y), q2, q);
-      ct_bf(x[6], x[7], make_uint2(w23.z, w23.w), q2, q);
-    }
+    ct_round16(x, tw, n / (16 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
     if (T == 1) {
-      // last round: 8 contiguous outputs, straight to global
       if (final_reduce) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = reduce4(x[e], q);
+        for (int e = 0; e < 16; ++e) x[e] = reduce4(x[e], q);
       }
-      uint4* dst = reinterpret_cast<uint4*>(a + 8 * tau);
-      dst[0] = make_uint4(x[0], x[1], x[2], x[3]);
-      dst[1] = make_uint4(x[4], x[5], x[6], x[7]);
-    } else {
-      __syncthreads();
+      uint4* dst = reinterpret_cast<uint4*>(a + 16 * tau);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s[pad(j0 + e * T)] = x[e];
+      for (int v = 0; v < 4; ++v) dst[v] = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+    } else {
+      if (T != N2 / 16) __syncthreads();  // everyone has read the previous round's smem
+#pragma unroll
+      for (int e = 0; e < 16; ++e) s[pad(j0 + e * T)] = x[e];
       __syncthreads();
     }
   }
 }
 
-// inverse: rounds of 3 stages, T = 1, 8, 64, ...
+// inverse: rounds of 4 stages, T = 1, 16, 256, ...; first round straight from global (16 contiguous words),
+// last round straight to global (coalesced), optional n^-1 scaling
 template <int N2>
-__global__ void __launch_bounds__(N2 / 8) ntt_inv_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
-                                                       const uint2* __restrict__ tw, uint32_t q, uint32_t ninv,
-                                                       uint32_t ninvp, int do_scale) {
+__global__ void __launch_bounds__(N2 / 16) ntt_inv_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
+                                                        const uint2* __restrict__ tw, uint32_t q, uint32_t ninv,
+                                                        uint32_t ninvp, int do_scale) {
   __shared__ uint32_t s[N2 + N2 / 32];
   const uint32_t b = blockIdx.x;
   uint32_t* a = data + blockIdx.y * stride + (size_t)b * N2;
   const uint32_t tau = threadIdx.x;
   const uint32_t q2 = 2 * q;
 #pragma unroll
-  for (int T = 1; T < N2; T *= 8) {
-    const uint32_t j0 = (tau / T) * 8 * T + (tau % T);
-    uint32_t x[8];
+  for (int T = 1; T < N2; T *= 16) {
+    const uint32_t j0 = (tau / T) * 16 * T + (tau % T);
+    uint32_t x[16];
     if (T == 1) {
-      const uint4* src = reinterpret_cast<const uint4*>(a + 8 * tau);
-      const uint4 v0 = src[0], v1 = src[1];
-      x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
-      x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+      const uint4* src = reinterpret_cast<const uint4*>(a + 16 * tau);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint4 w = src[v];
+        x[4 * v] = w.x;
+        x[4 * v + 1] = w.y;
+        x[4 * v + 2] = w.z;
+        x[4 * v + 3] = w.w;
+      }
     } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) x[e] = s[pad(j0 + e * T)];
+      for (int e = 0; e < 16; ++e) x[e] = s[pad(j0 + e * T)];
     }
-    const uint32_t h0 = n / (2 * T);                 // h of the first stage (t = T)
-    const uint32_t i0 = b * (N2 / (8 * T)) + tau / T;
-    {
-      const uint4* p = reinterpret_cast<const uint4*>(tw + h0 + 4 * i0);
-      const uint4 w01 = __ldg(p), w23 = __ldg(p + 1);
-      gs_bf(x[0], x[1], make_uint2(w01.x, w01.y), q2, q);
-      gs_bf(x[2], x[3], make_uint2(w01.z, w01.w), q2, q);
-      gs_bf(x[4], x[5], make_uint2(w23.x, w23.y), q2, q);
-      gs_bf(x[6], x[7], make_uint2(w23.z, w23.w), q2, q);
-    }
-    {
-      const uint4 w2 = __ldg(reinterpret_cast<const uint4*>(tw + h0 / 2 + 2 * i0));
-      const uint2 wa = make_uint2(w2.x, w2.y), wb = make_uint2(w2.z, w2.w);
-      gs_bf(x[0], x[2], wa, q2, q);
-      gs_bf(x[1], x[3], wa, q2, q);
-      gs_bf(x[4], x[6], wb, q2, q);
-      gs_bf(x[5], x[7], wb, q2, q);
-    }
-    {
-      const uint2 w = ldtw(tw, h0 / 4 + i0);
+    gs_round16(x, tw, n / (2 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
+    if (16 * T == N2) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) gs_bf(x[e], x[e + 4], w, q2, q);
-    }
-    if (T != 1) __syncthreads();
+      for (int e = 0; e < 16; ++e) a[j0 + e * T] = do_scale ? shoup_mul(x[e], ninv, ninvp, q) : x[e];
+    } else {
+      if (T != 1) __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 8; ++e) s[pad(j0 + e * T)] = x[e];
-    __syncthreads();
-  }
-  for (uint32_t i = tau; i < N2 / 4; i += N2 / 8) {
-    uint32_t v[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      uint32_t z = s[pad(4 * i + e)];
-      v[e] = do_scale ? shoup_mul(z, ninv, ninvp, q) : z;
+      for (int e = 0; e < 16; ++e) s[pad(j0 + e * T)] = x[e];
+      __syncthreads();
     }
-    reinterpret_cast<uint4*>(a)[i] = make_uint4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -286,15 +312,15 @@ static cudaError_t with_n1(uint32_t n1, F f) {
 template <typename F>
 static cudaError_t with_n2(uint32_t n2, F f) {
   switch (n2) {
-    case 64: return f(std::integral_constant<int, 64>{});
-    case 512: return f(std::integral_constant<int, 512>{});
+    case 16: return f(std::integral_constant<int, 16>{});
+    case 256: return f(std::integral_constant<int, 256>{});
     case 4096: return f(std::integral_constant<int, 4096>{});
   }
   return cudaErrorInvalidValue;
 }
-// n = n1 * n2 with n2 the largest power of 8 <= min(n, 4096), n1 <= 16
+// n = n1 * n2 with n2 the largest power of 16 <= min(n, 4096), n1 <= 16
 static bool split(uint32_t n, uint32_t& n1, uint32_t& n2) {
-  for (uint32_t c : {4096u, 512u, 64u}) {
+  for (uint32_t c : {4096u, 256u, 16u}) {
     if (c <= n && n % c == 0 && n / c <= 16) {
       n2 = c;
       n1 = n / c;
@@ -320,7 +346,7 @@ cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint6
   }
   return with_n2(n2, [&](auto N2) {
     dim3 g(n1, count);
-    ntt_fwd_rows<decltype(N2)::value><<<g, decltype(N2)::value / 8, 0, st>>>(data, stride, t.n, tw, t.q, 1);
+    ntt_fwd_rows<decltype(N2)::value><<<g, decltype(N2)::value / 16, 0, st>>>(data, stride, t.n, tw, t.q, 1);
     return cudaGetLastError();
   });
 }
@@ -332,8 +358,8 @@ cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint6
   const uint2* tw = reinterpret_cast<const uint2*>(t.iv);
   cudaError_t e = with_n2(n2, [&](auto N2) {
     dim3 g(n1, count);
-    ntt_inv_rows<decltype(N2)::value><<<g, decltype(N2)::value / 8, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv,
-                                                                             t.ninvp, n1 == 1);
+    ntt_inv_rows<decltype(N2)::value><<<g, decltype(N2)::value / 16, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv,
+                                                                              t.ninvp, n1 == 1);
     return cudaGetLastError();
   });
   if (e != cudaSuccess || n1 == 1) return e;
