@@ -112,7 +112,10 @@ def _llama_sample(P, n_out):
     return rows, cols
 
 
-@pytest.mark.parametrize("n_out,n_in", [(4096, 4096), (4096, 11008)])
+LLAMA_SHAPES = [(4096, 4096), (4096, 11008), (11008, 4096), (14336, 4096), (4096, 14336)]
+
+
+@pytest.mark.parametrize("n_out,n_in", LLAMA_SHAPES)
 def test_llama_sampled_words_bit_exact_and_precision(n_out, n_in):
     P = HeParams.llama()
     ctx, sk, A, W, X = setup(P, n_out, n_in)
@@ -128,23 +131,22 @@ def test_llama_sampled_words_bit_exact_and_precision(n_out, n_in):
     assert err < 2 ** -12, err          # paper target 12 bits; measured ~14.5 bits
 
 
-def test_selection_identity_full_output_metric_shape():
-    """Size-independent exact property at 4096 x 11008: with W a 0/1 selection matrix
-    (W~ = q1 at (y, pi(y))) the rescaled output row y equals, word for word, the limb-0
-    MLWE decomposition of input row pi(y) -- checked over ALL 4096 x 65 792 words."""
+def _selection_identity(n_out, n_in, seed=9):
+    """W a 0/1 selection matrix (W~ = q1 at (y, pi(y))): the rescaled output row y equals, word
+    for word, the limb-0 MLWE decomposition of input row pi(y) -- checked over ALL n_out x 65 792
+    output words, a size-independent exact property."""
     import torch
 
+    from paper_2601_18511_b200.layout import block_permutation
+
     P = HeParams.llama()
-    n_out, n_in = 4096, 11008
     ctx = HeContext(P)
-    rng = np.random.default_rng(9)
+    rng = np.random.default_rng(seed)
     A = rng.uniform(-1, 1, (P.tokens, n_in))
     sk = ctx.keygen(3)
     X = ctx.encrypt_acts(sk, A, seed=4)
-    pi = rng.permutation(n_in)[:n_out]
+    pi = rng.integers(0, n_in, n_out)
     # GEMM row y = k r' + t' reads W[k r' + sigma(t')]; GEMM col x reads W[:, k r + sigma(t)]
-    from paper_2601_18511_b200.layout import block_permutation
-
     prow = block_permutation(n_out, P.mlwe_rank)
     pcol = block_permutation(n_in, P.mlwe_rank)
     W = np.zeros((n_out, n_in))
@@ -154,22 +156,48 @@ def test_selection_identity_full_output_metric_shape():
     torch.cuda.synchronize()
     ct = X.data
     d, k, N, q0 = P.mlwe_degree, P.mlwe_rank, P.N, P.moduli[0]
-    # expected a'[y][j][m] = a_r[t - j + k m] (negacyclic), b'[y][m] = b_r[t + k m], limb 0
-    x = torch.as_tensor(pi, device=ct.device)
-    r, t = x // k, x % k
     a0 = ct[:, 0, 0].to(torch.int64)                       # [n_ct, N]
     b0 = ct[:, 0, 1].to(torch.int64)
     j = torch.arange(k, device=ct.device).view(1, k, 1)
     m = torch.arange(d, device=ct.device).view(1, 1, d)
-    c = t.view(-1, 1, 1) - j + k * m                       # [n_out, k, d]
-    neg = c < 0
-    av = a0[r.view(-1, 1, 1), torch.where(neg, c + N, c)]
-    exp_a = torch.where(neg & (av != 0), q0 - av, av).view(n_out, k * d)
-    assert torch.equal(Y.out_a.to(torch.int64) & 0xFFFFFFFF, exp_a)
-    bb = b0[r.view(-1, 1), t.view(-1, 1) + k * torch.arange(d, device=ct.device).view(1, d)]  # [n_out, d]
+    for y0 in range(0, n_out, 2048):                       # expected a'[y][j][m] = a_r[t - j + k m] (negacyclic)
+        y1 = min(n_out, y0 + 2048)
+        x = torch.as_tensor(pi[y0:y1], device=ct.device)
+        r, t = x // k, x % k
+        c = t.view(-1, 1, 1) - j + k * m
+        neg = c < 0
+        av = a0[r.view(-1, 1, 1), torch.where(neg, c + N, c)]
+        exp_a = torch.where(neg & (av != 0), q0 - av, av).view(y1 - y0, k * d)
+        assert torch.equal(Y.out_a[y0:y1].to(torch.int64) & 0xFFFFFFFF, exp_a)
+        del c, neg, av, exp_a
+    x = torch.as_tensor(pi, device=ct.device)
+    r, t = x // k, x % k
+    mm = torch.arange(d, device=ct.device).view(1, d)
+    bb = b0[r.view(-1, 1), t.view(-1, 1) + k * mm]        # [n_out, d]
     y = torch.arange(n_out, device=ct.device)
-    got_b = (Y.out_b.to(torch.int64) & 0xFFFFFFFF)[(y // k).view(-1, 1), (y % k).view(-1, 1) + k * torch.arange(d, device=ct.device).view(1, d)]
+    got_b = (Y.out_b.to(torch.int64) & 0xFFFFFFFF)[(y // k).view(-1, 1), (y % k).view(-1, 1) + k * mm]
     assert torch.equal(got_b, bb)
+
+
+def test_selection_identity_full_output_metric_shape():
+    _selection_identity(4096, 11008)
+
+
+@pytest.mark.parametrize("n_out,n_in", [s for s in LLAMA_SHAPES if s != (4096, 11008)])
+def test_selection_identity_full_output_all_llama_shapes(n_out, n_in):
+    _selection_identity(n_out, n_in)
+
+
+def test_wide_weights_at_llama_size_use_32_column_tiles():
+    """|W| up to 1 -> d_w = 3 at q1 ~ 2^20: the 256x32 CTA-pair instance, sampled parity."""
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, 1024, 4096, scale=1.0)
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    assert plan.d_w == 3
+    Y = pcmm_mlwe(ctx, plan, X)
+    rows, cols = _llama_sample(P, 1024)
+    ref = O.pcmm(P, O.encode_weights(P, W), u32(X.data), rows=rows, cols=cols)
+    assert np.array_equal(gather(P, Y, rows, cols), ref)
 
 
 def test_errors_and_ledger_on_device():

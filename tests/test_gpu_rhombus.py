@@ -50,6 +50,23 @@ def test_toy_pcmv_bit_exact(n_out, n_in):
     assert err < 2 ** -14, err
 
 
+@pytest.mark.parametrize("n_out,n_in", [(1024, 8192), (700, 3000)])
+def test_mid_ring_pcmv_bit_exact(n_out, n_in):
+    """N = 8192 with the Llama primes, Rhombus degree n = 512: 16 input pieces, 2 output pieces,
+    511 Galois key switches per piece -- every output word vs the oracle."""
+    P = HeParams(mlwe_degree=32, mlwe_rank=256, rhombus_degree=512, name="mid")
+    ctx, sk, keys, x, v, W = _setup(P, n_out, n_in)
+    s = O.keygen(P, 7)
+    s_small, s_up, ksk, gal = O.rhombus_keys(P, 99, s)
+    ct = O.encrypt(P, 5, s, O.encode_vector(P, v))[0]
+    assert np.array_equal(u32(x.data), ct)
+    y = pcmv_rhombus(ctx, make_rhombus_plan(ctx, W), keys, x)
+    _, out = O.rhombus_pcmv(P, ct, ksk, gal, O.rhombus_weights(P, W), n_in)
+    assert np.array_equal(u32(y.data)[0], out)
+    err = np.abs(decrypt_vector(ctx, keys.s_up_ntt, y) - clear_pcmv(W, v)).max()
+    assert err < 2 ** -12, err
+
+
 def test_pcmv_errors():
     P = HeParams.toy()
     ctx, sk, keys, x, v, W = _setup(P, 32, 40)
