@@ -89,11 +89,11 @@ __global__ void k_ksk_beta(const uint32_t* alpha, const uint32_t* s_new, uint32_
 // ------------------------------------------------------------------ key switching pieces (batched)
 // digits of c (coefficient form, per limb [2][cnt][n]) lifted to the other moduli:
 //   d_i = c_i * Qhat_i^-1 mod q_i;  D[j][i] = d_i mod m_j for j != i.  D[i][i] comes from the NTT form.
-__global__ void k_modup(const uint32_t* __restrict__ c, const uint32_t* __restrict__ c_ntt, uint64_t cnt_n,
-                        uint32_t q0, uint32_t q1, uint32_t P, uint32_t qhinv0, uint32_t qhinv1, uint32_t* __restrict__ D,
-                        uint32_t q0p, uint32_t q1p) {
-  // D layout: [j (3)][i (2)][cnt * n]
+__global__ void k_modup(const uint32_t* __restrict__ c, const uint32_t* __restrict__ T, uint32_t n, uint64_t cnt_n,
+                        uint32_t q0, uint32_t q1, uint32_t P, uint32_t qhinv0, uint32_t qhinv1, uint32_t* __restrict__ D) {
+  // D layout: [j (3)][i (2)][cnt * n];  T layout [L][cnt][2][n] (NTT form, a part = slot 0)
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t tix = (x / n) * 2 * n + x % n;
     const uint32_t d0 = mul_mod(c[x], qhinv0, q0);
     const uint32_t d1 = mul_mod(c[cnt_n + x], qhinv1, q1);
     D[(0 * 2 + 1) * cnt_n + x] = d1 % q0;
@@ -101,11 +101,9 @@ __global__ void k_modup(const uint32_t* __restrict__ c, const uint32_t* __restri
     D[(2 * 2 + 0) * cnt_n + x] = d0 % P;
     D[(2 * 2 + 1) * cnt_n + x] = d1 % P;
     // own-modulus digits straight from the NTT form (NTT is linear mod q_i)
-    D[(0 * 2 + 0) * cnt_n + x] = mul_mod(c_ntt[x], qhinv0, q0);
-    D[(1 * 2 + 1) * cnt_n + x] = mul_mod(c_ntt[cnt_n + x], qhinv1, q1);
+    D[(0 * 2 + 0) * cnt_n + x] = mul_mod(T[tix], qhinv0, q0);
+    D[(1 * 2 + 1) * cnt_n + x] = mul_mod(T[2 * cnt_n + tix], qhinv1, q1);
   }
-  (void)q0p;
-  (void)q1p;
 }
 // U[j] = sum_i D[j][i] * K[i][0][j],  W[j] = sum_i D[j][i] * K[i][1][j]   (NTT domain)
 // K layout [i][part][j][n];  UW layout [j][2][cnt][n]
@@ -231,41 +229,35 @@ __global__ void k_rh_mvm(const uint32_t* __restrict__ Wpt, const uint32_t* __res
 
 // ------------------------------------------------------------------ packing level
 // A [L][cnt_in][2][n] -> Ut into An [L][cnt_out][2][n]; T = sigma(E - M O) [L][cnt_out][2][n];
-// C = copy of T's a part [L][cnt_out][n] for the INTT.
-__global__ void k_pack_comb1(const uint32_t* __restrict__ A, uint32_t cnt_in, uint32_t half, uint32_t n,
-                             const uint32_t* __restrict__ mono /* [2][n] */, const uint32_t* __restrict__ perm,
-                             uint32_t q0, uint32_t q1, uint32_t* __restrict__ An, uint32_t* __restrict__ T,
-                             uint32_t* __restrict__ C) {
+// C = copy of T's a part [L][cnt_out][n] for the INTT.  One CTA per (limb, combine, a/b): E - M O is
+// built in shared memory with coalesced global reads, then permuted out of it.
+__global__ void __launch_bounds__(512) k_pack_comb1(const uint32_t* __restrict__ A, uint32_t cnt_in, uint32_t half,
+                                                    uint32_t n, const uint32_t* __restrict__ mono /* [2][n] */,
+                                                    const uint32_t* __restrict__ perm, uint32_t q0, uint32_t q1,
+                                                    uint32_t* __restrict__ An, uint32_t* __restrict__ T,
+                                                    uint32_t* __restrict__ C) {
+  extern __shared__ uint32_t sd[];  // [n]  E - M O
   const uint32_t cnt_out = cnt_in / 2;
-  const uint64_t per_l = (uint64_t)cnt_out * n;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * per_l; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t L = (uint32_t)(x / per_l);
-    const uint64_t y = x % per_l;
-    const uint32_t idx = (uint32_t)(y / n), c = (uint32_t)(y % n);
-    const uint32_t o = idx / half, s = idx % half;
-    const uint32_t e_i = o * 2 * half + s, o_i = e_i + half;
-    const uint32_t q = L ? q1 : q0;
-    const uint32_t* Eb = A + (((size_t)L * cnt_in + e_i) * 2) * n;
-    const uint32_t* Ob = A + (((size_t)L * cnt_in + o_i) * 2) * n;
-    const uint32_t* ml = mono + (size_t)L * n;
-    const uint32_t pc = perm[c];
-#pragma unroll
-    for (int ab = 0; ab < 2; ++ab) {
-      const uint32_t mo = mul_mod(Ob[ab * n + c], ml[c], q);
-      An[(((size_t)L * cnt_out + idx) * 2 + ab) * n + c] = add_mod(Eb[ab * n + c], mo, q);
-      const uint32_t t = sub_mod(Eb[ab * n + pc], mul_mod(Ob[ab * n + pc], ml[pc], q), q);
-      T[(((size_t)L * cnt_out + idx) * 2 + ab) * n + c] = t;
-      if (ab == 0) C[((size_t)L * cnt_out + idx) * n + c] = t;
-    }
+  const uint32_t idx = blockIdx.x, ab = blockIdx.y, L = blockIdx.z;
+  const uint32_t o = idx / half, s_ = idx % half;
+  const uint32_t e_i = o * 2 * half + s_, o_i = e_i + half;
+  const uint32_t q = L ? q1 : q0;
+  const uint32_t* Eb = A + (((size_t)L * cnt_in + e_i) * 2 + ab) * n;
+  const uint32_t* Ob = A + (((size_t)L * cnt_in + o_i) * 2 + ab) * n;
+  const uint32_t* ml = mono + (size_t)L * n;
+  uint32_t* un = An + (((size_t)L * cnt_out + idx) * 2 + ab) * n;
+  for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
+    const uint32_t e = Eb[c], mo = mul_mod(Ob[c], ml[c], q);
+    un[c] = add_mod(e, mo, q);
+    sd[c] = sub_mod(e, mo, q);
   }
-}
-// T's a part (NTT form) re-laid out [L][cnt][n] for the own-modulus digits
-__global__ void k_pack_aview(const uint32_t* __restrict__ T, uint32_t cnt, uint32_t n, uint32_t* __restrict__ Ta) {
-  const uint64_t per_l = (uint64_t)cnt * n;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * per_l; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t L = (uint32_t)(x / per_l);
-    const uint64_t y = x % per_l;
-    Ta[x] = T[(((size_t)L * cnt + y / n) * 2) * n + y % n];
+  __syncthreads();
+  uint32_t* t = T + (((size_t)L * cnt_out + idx) * 2 + ab) * n;
+  uint32_t* cc = C + ((size_t)L * cnt_out + idx) * n;
+  for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
+    const uint32_t v = sd[perm[c]];
+    t[c] = v;
+    if (ab == 0) cc[c] = v;
   }
 }
 // An += (u, T_b + w) with u = (U - LB_u) P^-1, w = (W - LB_w) P^-1   (NTT domain)
@@ -553,12 +545,10 @@ extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct
   for (uint32_t lv = 1; lv <= p->logn; ++lv) {
     const uint32_t cnt_out = cnt / 2, half = n >> lv;
     const uint64_t cn = (uint64_t)cnt_out * n;
-    k_pack_comb1<<<grid_for(2 * cn), 256, 0, st>>>(A, cnt, half, n, mono_base + (size_t)(lv - 1) * 2 * n,
-                                                   perm_base + (size_t)(lv - 1) * n, q0, q1, An, w.T, w.C);
+    k_pack_comb1<<<dim3(cnt_out, 2, 2), 512, n * sizeof(uint32_t), st>>>(
+        A, cnt, half, n, mono_base + (size_t)(lv - 1) * 2 * n, perm_base + (size_t)(lv - 1) * n, q0, q1, An, w.T, w.C);
     for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt_rh[L], w.C + (size_t)L * cn, cnt_out, n, st), "INTT(T_a)");
-    // own-modulus digits need T_a in NTT form laid out [L][cnt][n]: reuse UW as that view
-    k_pack_aview<<<grid_for(2 * cn), 256, 0, st>>>(w.T, cnt_out, n, w.UW);
-    k_modup<<<grid_for(cn), 256, 0, st>>>(w.C, w.UW, cn, q0, q1, P, p->qhinv[0], p->qhinv[1], w.D, 0, 0);
+    k_modup<<<grid_for(cn), 256, 0, st>>>(w.C, w.T, n, cn, q0, q1, P, p->qhinv[0], p->qhinv[1], w.D);
     HE_CUDA(ntt_forward(c->ntt_rh[0], w.D + (0 * 2 + 1) * cn, cnt_out, n, st), "NTT(d1 mod q0)");
     HE_CUDA(ntt_forward(c->ntt_rh[1], w.D + (1 * 2 + 0) * cn, cnt_out, n, st), "NTT(d0 mod q1)");
     HE_CUDA(ntt_forward(c->ntt_rh[2], w.D + (2 * 2 + 0) * cn, 2 * cnt_out, n, st), "NTT(d mod P)");
