@@ -476,7 +476,9 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
     grid = tiles < p->ctx->sm_count ? tiles : p->ctx->sm_count;
   } else {
     const int tiles = (int)((rows + 255) / 256) * (int)((p->width + bn2 - 1) / bn2);
-    const int pairs = p->ctx->sm_count / 2;
+    static const int env_pairs = getenv("HE_GEMM_PAIRS") ? atoi(getenv("HE_GEMM_PAIRS")) : 0;  // profiling knob
+    int pairs = p->ctx->sm_count / 2;
+    if (env_pairs > 0 && env_pairs < pairs) pairs = env_pairs;
     grid = 2 * (tiles < pairs ? tiles : pairs);
   }
   HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, tmA, tmB, tmBa, a, grid, (cudaStream_t)stream),
