@@ -127,6 +127,16 @@ he_status he_pcmm_gemm(const he_pcmm_plan* plan, const void* workspace_dev, uint
  * host memory chunk by chunk while the next chunk computes (pcmm_mlwe_to_host). */
 he_status he_pcmm_gemm_rows(const he_pcmm_plan* plan, const void* workspace_dev, uint32_t row0, uint32_t rows,
                             uint32_t* out_b_dev, uint32_t* out_a_dev, void* stream);
+/* Spectral a-part (K7, same output words): the plan's a' columns are computed as blockwise
+ * length-2k cyclic NTT correlations instead of the d*k-column GEMM (b' columns stay on K1).
+ * Step 1 reports the bytes of the spectral weights G^ (caller-allocated device memory, kept
+ * alive by the caller); step 2 fills them from the plan's digit planes and switches the plan's
+ * he_pcmm_run / decompose / gemm(_rows) to the spectral path.  Part of plan construction:
+ * call it before sharing the plan.  Workspace sizes change accordingly. */
+he_status he_pcmm_spectral_weight_bytes(const he_pcmm_plan* plan, uint64_t* bytes);
+he_status he_pcmm_spectral_prepare(he_pcmm_plan* plan, int8_t* spec_weights_dev, void* stream);
+/* 0 = K1 over all columns (direct), 1 = spectral */
+he_status he_pcmm_algo(const he_pcmm_plan* plan, int* algo);
 
 /* ---------------------------------------------------------------- Rhombus PCMv (K6), degree n = rhombus_degree */
 /* Vector layout (App. A + h): element e sits at degree-N coefficient

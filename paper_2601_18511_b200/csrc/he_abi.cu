@@ -64,6 +64,22 @@ static he_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint
   return HE_OK;
 }
 
+// 3-D int8 tensor {inner, rows, planes}, box {box_inner, box_rows, 1}, 64-B swizzle (spectral operands)
+static he_status make_map_sw64(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t planes,
+                               uint32_t box_rows) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {inner, rows, planes};
+  cuuint64_t strides[2] = {inner, inner * rows};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled (sw64) failed (%d)", (int)r);
+  return HE_OK;
+}
+
 // 4-D int8 tensor with explicit strides (bytes), box {128, box_rows, 1, 1}, 128-B swizzle
 static he_status make_map4(CUtensorMap* m, const void* base, const uint64_t dims_in[4], const uint64_t strides_in[3],
                            uint32_t box_rows) {
@@ -383,7 +399,24 @@ static uint64_t fused_stride(const he_pcmm_plan* p) { return (uint64_t)p->ctx->R
 static uint64_t fused_a_bytes(const he_pcmm_plan* p) {
   return 16ull * (p->d0 + p->d1) * (p->n_in / p->ctx->R.k) * fused_stride(p);
 }
+// spectral workspace: [K3 b-column digit planes][A^ limb 0][A^ limb 1][C^ limb 0][C^ limb 1], 256-B aligned
+struct SpecWs {
+  uint64_t bdig, a0, a1, c0, c1, total;
+};
+static uint64_t al256(uint64_t x) { return (x + 255) & ~255ull; }
+static SpecWs spec_ws(const he_pcmm_plan* p) {
+  const uint64_t d = p->ctx->R.d;
+  SpecWs w;
+  w.bdig = 0;
+  w.a0 = al256((uint64_t)(p->d0 + p->d1) * d * p->n_in);
+  w.a1 = w.a0 + al256((uint64_t)p->L * p->dsp[0] * d * p->r_pad);
+  w.c0 = w.a1 + al256((uint64_t)p->L * p->dsp[1] * d * p->r_pad);
+  w.c1 = w.c0 + al256((uint64_t)p->L * p->n_out * d * 4);
+  w.total = w.c1 + al256((uint64_t)p->L * p->n_out * d * 4);
+  return w;
+}
 static uint64_t ws_bytes(const he_pcmm_plan* p) {
+  if (p->algo == 1) return spec_ws(p).total;
   if (fused_path(p))
     return fused_a_bytes(p) + (uint64_t)(p->d0 + p->d1) * (p->n_in / p->ctx->R.k) * p->ctx->R.N;
   return (uint64_t)(p->d0 + p->d1) * p->width * p->n_in;
@@ -400,6 +433,21 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
   if (!p || !ct_in || !ws) return fail(HE_EINVAL, "null argument");
   if (ws_size < ws_bytes(p)) return fail(HE_EINVAL, "workspace too small (%llu < %llu)", (unsigned long long)ws_size,
                                          (unsigned long long)ws_bytes(p));
+  if (p->algo == 1) {
+    const SpecWs w = spec_ws(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    int8_t* base = (int8_t*)ws;
+    HE_CUDA(launch_decompose(p->ctx->R, ct_in, p->n_in, (int)p->d0, (int)p->d1, base + w.bdig,
+                             (uint64_t)p->ctx->R.d * p->n_in, st, 1),
+            "decompose (b columns)");
+    HE_CUDA(cudaMemsetAsync(base + w.a0, 0, w.c0 - w.a0, st), "memset");
+    const uint32_t n_ct = p->n_in / p->ctx->R.k;
+    for (uint32_t L = 0; L < 2; ++L)
+      HE_CUDA(launch_spec_data(p->ctx->R, ct_in, n_ct, L, p->st[L], (int)p->dsp[L], p->r_pad, base + (L ? w.a1 : w.a0),
+                               st),
+              "spectral data transform");
+    return HE_OK;
+  }
   if (fused_path(p)) {
     HE_CUDA(launch_digitize(p->ctx->R, ct_in, p->n_in / p->ctx->R.k, (int)p->d0, (int)p->d1, (uint32_t)fused_stride(p),
                             (int8_t*)ws, (int8_t*)ws + fused_a_bytes(p), (cudaStream_t)stream),
@@ -412,13 +460,59 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
   return HE_OK;
 }
 
+// K7 S3 (per-frequency tcgen05 GEMM, both limbs) + S4 (inverse, rescale, a' store) on rows [row0, row0 + rows)
+static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows, uint32_t* out_a,
+                           cudaStream_t st) {
+  const SpecWs w = spec_ws(p);
+  const int8_t* base = (const int8_t*)ws;
+  static const bool simple = getenv("HE_SPEC_SIMPLE") != nullptr;  // debug: S3 on CUDA cores
+  uint32_t* C[2] = {(uint32_t*)(base + w.c0), (uint32_t*)(base + w.c1)};
+  for (int L = 0; L < 2; ++L) {
+    SpecGemmArgs a;
+    a.n_rows = (int)rows;
+    a.row0 = (int)row0;
+    a.n_out = (int)p->n_out;
+    a.L = (int)p->L;
+    a.d = (int)p->ctx->R.d;
+    a.r_pad = (int)p->r_pad;
+    a.q = p->epi.q[L];
+    a.mu = p->epi.mu[L];
+    a.off64 = p->epi.off64[L];
+    for (int sft = 0; sft < 8; ++sft) a.pw[sft] = (int32_t)p->epi.pw[L][sft];
+    a.out = C[L];
+    const int8_t* A = base + (L ? w.a1 : w.a0);
+    if (simple) {
+      const int8_t* G = p->spec_w + (L ? (uint64_t)p->L * p->dsp[0] * p->n_out * p->r_pad : 0);
+      HE_CUDA(launch_spec_gemm_simple((int)p->dsp[L], G, A, a, st), "spectral gemm (simple)");
+      continue;
+    }
+    CUtensorMap tmB;
+    he_status s = make_map_sw64(&tmB, A, p->r_pad, p->ctx->R.d, (uint64_t)p->L * p->dsp[L], 16);
+    if (s) return s;
+    HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, a, p->ctx->sm_count, st), "spectral gemm");
+  }
+  SpecInvConst c;
+  for (int L = 0; L < 2; ++L) {
+    c.q[L] = p->epi.q[L];
+    c.iv[L] = p->st[L].iv;
+    c.linv[L] = p->st[L].linv;
+    c.linvp[L] = p->st[L].linvp;
+  }
+  c.q1inv = p->epi.q1inv;
+  c.q1invp = p->epi.q1invp;
+  HE_CUDA(launch_spec_inverse(p->ctx->R, C[0], C[1], p->n_out, row0, rows, p->L, c, out_a, st), "spectral inverse");
+  return HE_OK;
+}
+
 extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows,
                                        uint32_t* out_b, uint32_t* out_a, void* stream) {
   if (!p || !ws || !out_b || !out_a) return fail(HE_EINVAL, "null argument");
   if (rows == 0 || row0 % p->ctx->R.k || rows % p->ctx->R.k || row0 + rows > p->n_out)
     return fail(HE_EINVAL, "row range [%u, %u) must be k-aligned and inside [0, %u)", row0, row0 + rows, p->n_out);
-  const int variant = gemm_variant();
-  const bool fused = fused_path(p);
+  const int variant = p->algo == 1 ? 2 : gemm_variant();
+  const bool fused = p->algo != 1 && fused_path(p);
+  const bool spec = p->algo == 1;
+  const uint32_t gemm_width = spec ? p->ctx->R.d : p->width;  // spectral: K1 on the b' columns only
   // profiling knobs (defaults are the tuned choice): HE_GEMM_BN, HE_GEMM_GROUP_M, HE_GEMM_HINT_A/B
   static const int env_bn = getenv("HE_GEMM_BN") ? atoi(getenv("HE_GEMM_BN")) : 0;
   static const int env_gm = getenv("HE_GEMM_GROUP_M") ? atoi(getenv("HE_GEMM_GROUP_M")) : 0;
@@ -445,7 +539,7 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
     s = make_map4(&tmBa, ws, ad, as, bn2 / 2);
     if (s) return s;
   } else {
-    s = make_map(&tmB, ws, p->n_in, p->width, p->d0 + p->d1, variant == 1 ? kGemmBoxRows1 : bn2 / 2);
+    s = make_map(&tmB, ws, p->n_in, gemm_width, p->d0 + p->d1, variant == 1 ? kGemmBoxRows1 : bn2 / 2);
     if (s) return s;
     tmBa = tmB;
   }
@@ -457,7 +551,7 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
   GemmArgs a;
   a.n_out = (int)rows;
   a.n_in = (int)p->n_in;
-  a.width = (int)p->width;
+  a.width = (int)gemm_width;
   a.d = (int)p->ctx->R.d;
   a.k = (int)p->ctx->R.k;
   a.out_b = out_b;
@@ -475,7 +569,7 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
     const int tiles = (int)((rows + 127) / 128) * (int)(p->width / 32);
     grid = tiles < p->ctx->sm_count ? tiles : p->ctx->sm_count;
   } else {
-    const int tiles = (int)((rows + 255) / 256) * (int)((p->width + bn2 - 1) / bn2);
+    const int tiles = (int)((rows + 255) / 256) * (int)((gemm_width + bn2 - 1) / bn2);
     static const int env_pairs = getenv("HE_GEMM_PAIRS") ? atoi(getenv("HE_GEMM_PAIRS")) : 0;  // profiling knob
     int pairs = p->ctx->sm_count / 2;
     if (env_pairs > 0 && env_pairs < pairs) pairs = env_pairs;
@@ -483,6 +577,7 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
   }
   HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, tmA, tmB, tmBa, a, grid, (cudaStream_t)stream),
           "modgemm");
+  if (spec) return spec_rows(p, ws, row0, rows, out_a, (cudaStream_t)stream);
   return HE_OK;
 }
 
@@ -506,5 +601,65 @@ extern "C" he_status he_pcmm_run(const he_pcmm_plan* p, const uint32_t* ct_in, u
     ledger->pc_mults += bo * bi;
     ledger->rescales += bo;
   }
+  return HE_OK;
+}
+
+// ---------------------------------------------------------------- K7 spectral a-part
+static void spec_dims(const he_pcmm_plan* p, uint32_t& L, uint32_t& r_pad, uint32_t dsp[2]) {
+  L = 2 * p->ctx->R.k;
+  r_pad = ((p->n_in / p->ctx->R.k) + 63) / 64 * 64;
+  dsp[0] = (uint32_t)digits_for(p->ctx->R.q[0]);
+  dsp[1] = (uint32_t)digits_for(p->ctx->R.q[1]);
+}
+
+extern "C" he_status he_pcmm_spectral_weight_bytes(const he_pcmm_plan* p, uint64_t* bytes) {
+  if (!p || !bytes) return fail(HE_EINVAL, "null argument");
+  uint32_t L, r_pad, dsp[2];
+  spec_dims(p, L, r_pad, dsp);
+  *bytes = (uint64_t)L * (dsp[0] + dsp[1]) * p->n_out * r_pad;
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, void* stream) {
+  if (!p || !wspec) return fail(HE_EINVAL, "null argument");
+  const he_context* c = p->ctx;
+  if (c->R.d % 32) return fail(HE_EINVAL, "spectral path needs mlwe_degree %% 32 == 0");
+  uint32_t L, r_pad, dsp[2];
+  spec_dims(p, L, r_pad, dsp);
+  // exactness of S3: int32 shift accumulators R * D * 2^14 < 2^31; int64 sum S * R * D * 2^14 * q < 2^62
+  const uint64_t R = p->n_in / c->R.k;
+  for (int i = 0; i < 2; ++i) {
+    if (R * dsp[i] * 16384ull >= (1ull << 31)) return fail(HE_EINVAL, "n_in too large for the spectral accumulators");
+    if ((unsigned __int128)(2 * dsp[i] - 1) * R * dsp[i] * 16384ull * c->R.q[i] >= ((unsigned __int128)1 << 62))
+      return fail(HE_EINVAL, "n_in too large for the spectral recombination");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < 2; ++i) {
+    spec_table_free(p->st[i]);
+    HE_CUDA(spec_table_init(p->st[i], L, c->R.q[i]), "spectral table");
+  }
+  const uint64_t sz0 = (uint64_t)L * dsp[0] * p->n_out * r_pad;
+  const uint64_t total = sz0 + (uint64_t)L * dsp[1] * p->n_out * r_pad;
+  HE_CUDA(cudaMemsetAsync(wspec, 0, total, st), "memset");
+  for (int i = 0; i < 2; ++i)
+    HE_CUDA(launch_spec_weights(p->digits, p->d_w, p->n_out, p->n_in, c->R.k, p->st[i], (int)dsp[i], r_pad,
+                                wspec + (i ? sz0 : 0), st),
+            "spectral weights");
+  for (int i = 0; i < 2; ++i) {
+    he_status s = make_map_sw64(&p->tmSA[i], wspec + (i ? sz0 : 0), r_pad, p->n_out, (uint64_t)L * dsp[i], 128);
+    if (s) return s;
+  }
+  p->L = L;
+  p->r_pad = r_pad;
+  p->dsp[0] = dsp[0];
+  p->dsp[1] = dsp[1];
+  p->spec_w = wspec;
+  p->algo = 1;
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_algo(const he_pcmm_plan* p, int* algo) {
+  if (!p || !algo) return fail(HE_EINVAL, "null argument");
+  *algo = p->algo;
   return HE_OK;
 }

@@ -16,7 +16,8 @@ namespace he {
 // {n = m} U {n = d + d j + m : j < k}, 4 components per thread, one 32-bit store per digit.
 __global__ void __launch_bounds__(256) decompose_kernel(const uint32_t* __restrict__ ct, uint32_t n_in, uint32_t d,
                                                         uint32_t k, uint32_t N, uint32_t q0, uint32_t q1, int d0,
-                                                        int d1, int8_t* __restrict__ planes, uint64_t plane_stride) {
+                                                        int d1, int8_t* __restrict__ planes, uint64_t plane_stride,
+                                                        uint32_t n_rho) {
   extern __shared__ uint32_t win[];  // [2 limbs][2k] a-window, then [2 limbs][k] b-row
   const uint32_t r = blockIdx.x, m = blockIdx.y;
   const uint32_t qs[2] = {q0, q1};
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(256) decompose_kernel(const uint32_t* __restri
   const uint32_t rows_per_pass = blockDim.x / tpr;
   const uint32_t sub = threadIdx.x % tpr, rsel = threadIdx.x / tpr;
   const uint32_t t0 = sub * 4;
-  for (uint32_t rho = rsel; rho < k + 1; rho += rows_per_pass) {
+  for (uint32_t rho = rsel; rho < n_rho; rho += rows_per_pass) {
     // rho = 0: b-row n = m; rho = 1 + j: a-row n = d + d j + m
     const uint32_t n = rho == 0 ? m : d + d * (rho - 1) + m;
 #pragma unroll
@@ -81,10 +82,11 @@ __global__ void __launch_bounds__(256) decompose_kernel(const uint32_t* __restri
 }
 
 cudaError_t launch_decompose(const RingDims& R, const uint32_t* ct, uint32_t n_in, int d0, int d1, int8_t* planes,
-                             uint64_t plane_stride, cudaStream_t s) {
+                             uint64_t plane_stride, cudaStream_t s, int b_only) {
   dim3 grid(n_in / R.k, R.d);
   size_t smem = (size_t)6 * R.k * sizeof(uint32_t);
-  decompose_kernel<<<grid, 256, smem, s>>>(ct, n_in, R.d, R.k, R.N, R.q[0], R.q[1], d0, d1, planes, plane_stride);
+  decompose_kernel<<<grid, 256, smem, s>>>(ct, n_in, R.d, R.k, R.N, R.q[0], R.q[1], d0, d1, planes, plane_stride,
+                                          b_only ? 1u : R.k + 1);
   return cudaGetLastError();
 }
 

@@ -20,6 +20,16 @@ struct he_pcmm_plan {
   const int8_t* digits;
   CUtensorMap tmA;
   he::GemmEpiConst epi;
+  // K7 spectral a-part (he_pcmm_spectral_prepare); algo 0 = K1 over every GEMM column
+  int algo = 0;
+  uint32_t L = 0, r_pad = 0, dsp[2] = {0, 0};
+  const int8_t* spec_w = nullptr;  // caller-owned: G^ limb 0 [L][D0][n_out][r_pad], then limb 1
+  CUtensorMap tmSA[2];
+  he::SpecTable st[2];
+  ~he_pcmm_plan() {
+    he::spec_table_free(st[0]);
+    he::spec_table_free(st[1]);
+  }
 };
 
 he_status fail(he_status s, const char* fmt, ...);

@@ -56,7 +56,42 @@ struct RingDims {
 };
 
 cudaError_t launch_decompose(const RingDims& R, const uint32_t* ct, uint32_t n_in, int d0, int d1, int8_t* planes,
-                             uint64_t plane_stride, cudaStream_t s);
+                             uint64_t plane_stride, cudaStream_t s, int b_only = 0);
+
+// ---- K7: spectral (overlap-save NTT) form of the a-part GEMM (he_spectral.cu)
+struct SpecTable {  // cyclic NTT of length L mod q
+  uint32_t L = 0, q = 0;
+  uint2* fw = nullptr;   // (w^j, Shoup) j < L/2
+  uint2* iv = nullptr;   // (w^-j, Shoup) j < L/2
+  uint32_t linv = 0, linvp = 0;
+};
+cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q);
+void spec_table_free(SpecTable& t);
+
+struct SpecGemmArgs {
+  int n_rows, row0, n_out;  // row range [row0, row0 + n_rows) of n_out
+  int L, d, r_pad;
+  uint32_t q;
+  uint64_t mu, off64;       // Barrett floor(2^64/q); q * ceil(2^62/q)
+  int32_t pw[8];            // 2^(8 s) mod q
+  uint32_t* out;            // C^ [L][n_out][d]
+};
+struct SpecInvConst {
+  uint32_t q[2];
+  const uint2* iv[2];
+  uint32_t linv[2], linvp[2];
+  uint32_t q1inv, q1invp;
+};
+cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out, uint32_t n_in, uint32_t k,
+                                const SpecTable& t, int D, uint32_t r_pad, int8_t* out, cudaStream_t s);
+cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, uint32_t limb, const SpecTable& t,
+                             int D, uint32_t r_pad, int8_t* out, cudaStream_t s);
+cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const SpecGemmArgs& a, int sm_count,
+                             cudaStream_t s);
+cudaError_t launch_spec_gemm_simple(int D, const int8_t* G, const int8_t* A, const SpecGemmArgs& a, cudaStream_t s);
+cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const uint32_t* c1, uint32_t n_out,
+                                uint32_t row0, uint32_t rows, uint32_t L, const SpecInvConst& cst, uint32_t* out_a,
+                                cudaStream_t s);
 cudaError_t launch_digitize(const RingDims& R, const uint32_t* ct, uint32_t n_ct, int d0, int d1, uint32_t S,
                             int8_t* out_a, int8_t* out_b, cudaStream_t s);
 cudaError_t launch_weight_maxabs(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in,

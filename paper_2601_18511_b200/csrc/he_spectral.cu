@@ -1,0 +1,669 @@
+// he_spectral.cu -- the spectral form of the MLWE PCMM's a-part GEMM (K7 = S1..S4).
+//
+// The a-part of the MLWE PCMM is, per limb q and output row y,
+//   v[y][d + d j + m] = sum_r sum_t W~[y][k r + t] * a_r[t - j + k m]        (negacyclic read)
+// i.e. for every input RLWE ct r a length-k correlation of the weight row segment
+// g_{y,r}[t] = W~[y][k r + t] with a_r, sampled at c = k m - j.  The GEMM of K1 spends
+// n_out * n_in * d * k word-MACs on it because it ignores that every column of the
+// decomposed a-matrix is a twisted shift of the same polynomial.  Here the correlation is
+// evaluated blockwise by overlap-save with a cyclic NTT of length L = 2k over Z_q:
+//   window  win_{r,m}[u] = a_r[k m - k + 1 + u],  u < L            (S2, per op)
+//   filter  g'_{y,r}[u]  = g_{y,r}[-u mod L]                        (S1, plan time)
+//   C^_y,m[f] = sum_r  G^_{y,r}[f] * A^_{r,m}[f]   mod q,  f < L    (S3, tcgen05 GEMM per f)
+//   v[y][d + d (k-1-u) + m] = INTT(C^_{y,m})[u],  u < k            (S4, + rescale)
+// The values are the same residues K1 produces (exact modular arithmetic, no rounding), so
+// the output is bit-identical; the work drops from d*k to ~2*L*n_in/k MACs per output word
+// (128x fewer word-MACs at the Llama shapes), at the cost of full-width (not 2-digit)
+// spectral weights and an L x n_out x d spectral intermediate per limb.
+//
+// S3 runs per frequency f a modular GEMM  C^_f (n_out x d) = G^_f (n_out x R) * A^_f (R x d),
+// R = n_in / k, on tcgen05 kind::i8 exactly like K1: both operands split into D balanced
+// int8 digit planes (D = 4 for q0 < 2^30, 3 for q1 ~ 2^20), one MMA per weight digit against
+// the D stacked data planes writing at TMEM column offset 32 a, so digit pair (a, b) lands in
+// the int32 accumulator of shift s = a + b (2D-1 accumulators per word); the epilogue sums
+// acc_s * (2^(8 s) mod q) in int64 and Barrett-reduces.  CTA pairs (cta_group::2), tiles of
+// 256 rows x 32 columns, two TMEM accumulator buffers so the epilogue of one tile overlaps
+// the MMAs of the next; K = R padded to 64 bytes, 64-byte swizzle.
+#include <cuda.h>
+#include <cstdlib>
+#include "he_common.cuh"
+#include "he_tc.cuh"
+#include "he_kernels.h"
+
+namespace he {
+
+// ---------------------------------------------------------------- host tables
+cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
+  t.L = L;
+  t.q = q;
+  if (L < 4 || (L & (L - 1)) || (q - 1) % L) return cudaErrorInvalidValue;
+  uint64_t w = 0;
+  for (uint64_t g = 2; g < q; ++g) {
+    const uint64_t c = powmod_h(g, (q - 1) / L, q);
+    if (powmod_h(c, L / 2, q) != 1) {
+      w = c;
+      break;
+    }
+  }
+  if (!w) return cudaErrorInvalidValue;
+  const uint64_t wi = powmod_h(w, q - 2, q);
+  uint32_t* h = new uint32_t[2 * (size_t)L];  // fw pairs [L/2][2], iv pairs [L/2][2]
+  uint64_t p = 1, pi = 1;
+  for (uint32_t j = 0; j < L / 2; ++j) {
+    h[2 * j] = (uint32_t)p;
+    h[2 * j + 1] = shoup_pre((uint32_t)p, q);
+    h[L + 2 * j] = (uint32_t)pi;
+    h[L + 2 * j + 1] = shoup_pre((uint32_t)pi, q);
+    p = p * w % q;
+    pi = pi * wi % q;
+  }
+  t.linv = (uint32_t)powmod_h(L, q - 2, q);
+  t.linvp = shoup_pre(t.linv, q);
+  uint32_t* dptr = nullptr;
+  cudaError_t e = cudaMalloc(&dptr, 2 * (size_t)L * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemcpy(dptr, h, 2 * (size_t)L * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  delete[] h;
+  if (e != cudaSuccess) return e;
+  t.fw = reinterpret_cast<uint2*>(dptr);
+  t.iv = reinterpret_cast<uint2*>(dptr + L);
+  return cudaSuccess;
+}
+
+void spec_table_free(SpecTable& t) {
+  if (t.fw) cudaFree(t.fw);
+  t.fw = t.iv = nullptr;
+}
+
+// ---------------------------------------------------------------- cooperative cyclic NTTs in shared memory
+// cnt transforms of length L at x + b * ld.  Forward: DIF (natural -> bit-reversed),
+// X[f] = sum_i x[i] w^(f i).  Inverse: DIT (bit-reversed -> natural) with the L^-1 scaling
+// left to the caller.  Values fully reduced in [0, q).
+HE_D void cyc_fwd_smem(uint32_t* x, int cnt, int ld, int L, const uint2* __restrict__ tw, uint32_t q) {
+  const int half = L / 2;
+  for (int len = half, step = 1; len >= 1; len >>= 1, step <<= 1) {
+    for (int i = threadIdx.x; i < cnt * half; i += blockDim.x) {
+      const int b = i / half, j = i % half;
+      const int off = j % len;
+      uint32_t* p = x + b * ld + (j / len) * 2 * len + off;
+      const uint32_t u = p[0], v = p[len];
+      const uint2 w = __ldg(tw + off * step);
+      p[0] = add_mod(u, v, q);
+      p[len] = shoup_mul(sub_mod(u, v, q), w.x, w.y, q);
+    }
+    __syncthreads();
+  }
+}
+HE_D void cyc_inv_smem(uint32_t* x, int cnt, int ld, int L, const uint2* __restrict__ tw, uint32_t q) {
+  const int half = L / 2;
+  for (int len = 1, step = half; len < L; len <<= 1, step >>= 1) {
+    for (int i = threadIdx.x; i < cnt * half; i += blockDim.x) {
+      const int b = i / half, j = i % half;
+      const int off = j % len;
+      uint32_t* p = x + b * ld + (j / len) * 2 * len + off;
+      const uint2 w = __ldg(tw + off * step);
+      const uint32_t u = p[0], v = shoup_mul(p[len], w.x, w.y, q);
+      p[0] = add_mod(u, v, q);
+      p[len] = sub_mod(u, v, q);
+    }
+    __syncthreads();
+  }
+}
+
+HE_D void write_digits(uint32_t v, uint32_t q, int D, int8_t* dst, uint64_t plane_stride) {
+  const uint32_t c = v > (q >> 1) ? v - q : v;        // two's complement of the centred residue
+  const uint32_t w = (c + 0x80808080u) ^ 0x80808080u;  // byte p = balanced digit p (he_crypto.cu K3)
+  for (int p = 0; p < D; ++p) dst[(size_t)p * plane_stride] = (int8_t)(w >> (8 * p));
+}
+
+// ---------------------------------------------------------------- S1: spectral weights (plan time)
+// G^[f][a][y][r_pad] int8 (balanced digit a of the transformed filter g'_{y,r}).
+// One CTA per (row y, chunk of kSpecRChunk input cts).
+constexpr int kSpecRChunk = 16;
+__global__ void __launch_bounds__(256) spec_weights_kernel(const int8_t* __restrict__ wdig, uint32_t d_w, uint32_t n_out,
+                                                           uint32_t n_in, uint32_t k, uint32_t L, uint32_t q, int D,
+                                                           uint32_t r_pad, const uint2* __restrict__ tw, uint32_t linv,
+                                                           uint32_t linvp, int8_t* __restrict__ out) {
+  extern __shared__ uint32_t xs[];  // [kSpecRChunk][L]
+  const uint32_t y = blockIdx.x, r0 = blockIdx.y * kSpecRChunk;
+  const uint32_t R = n_in / k;
+  const int cnt = (int)min((uint32_t)kSpecRChunk, R - r0);
+  for (int i = threadIdx.x; i < cnt * (int)L; i += blockDim.x) xs[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < cnt * (int)k; i += blockDim.x) {
+    const int b = i / (int)k, t = i % (int)k;
+    const size_t x = (size_t)(r0 + b) * k + t;
+    int64_t w = 0;
+    for (int a = (int)d_w - 1; a >= 0; --a) w = w * 256 + wdig[((size_t)a * n_out + y) * n_in + x];
+    int64_t m = w % (int64_t)q;
+    if (m < 0) m += q;
+    xs[b * L + ((L - t) & (L - 1))] = (uint32_t)m;  // g'[-t mod L] = g[t]
+  }
+  __syncthreads();
+  cyc_fwd_smem(xs, cnt, (int)L, (int)L, tw, q);
+  const uint64_t plane = (uint64_t)n_out * r_pad;
+  for (int i = threadIdx.x; i < cnt * (int)L; i += blockDim.x) {
+    const int f = i / cnt, b = i % cnt;  // consecutive threads: consecutive r (bytes)
+    int8_t* dst = out + ((size_t)f * D * n_out + y) * r_pad + r0 + b;
+    write_digits(shoup_mul(xs[b * L + f], linv, linvp, q), q, D, dst, plane);  // L^-1 of the INTT folded in
+  }
+}
+
+// ---------------------------------------------------------------- S2: spectral data windows (per op)
+// A^[f][b][m][r_pad] int8.  One CTA per (block m, chunk of input cts).
+__global__ void __launch_bounds__(256) spec_data_kernel(const uint32_t* __restrict__ ct, uint32_t n_ct, uint32_t limb,
+                                                        uint32_t k, uint32_t d, uint32_t N, uint32_t L, uint32_t q,
+                                                        int D, uint32_t r_pad, const uint2* __restrict__ tw,
+                                                        int8_t* __restrict__ out) {
+  extern __shared__ uint32_t xs[];  // [kSpecRChunk][L]
+  const uint32_t m = blockIdx.x, r0 = blockIdx.y * kSpecRChunk;
+  const int cnt = (int)min((uint32_t)kSpecRChunk, n_ct - r0);
+  for (int i = threadIdx.x; i < cnt * (int)L; i += blockDim.x) {
+    const int b = i / (int)L, u = i % (int)L;
+    const uint32_t* a = ct + ((size_t)(r0 + b) * 2 + limb) * 2 * N;
+    int64_t I = (int64_t)k * m - (int64_t)k + 1 + u;
+    uint32_t v;
+    if (I < 0) {
+      const uint32_t w = a[I + N];
+      v = w ? q - w : 0u;
+    } else if (I >= (int64_t)N) {
+      const uint32_t w = a[I - N];
+      v = w ? q - w : 0u;
+    } else {
+      v = a[I];
+    }
+    xs[i] = v;
+  }
+  __syncthreads();
+  cyc_fwd_smem(xs, cnt, (int)L, (int)L, tw, q);
+  const uint64_t plane = (uint64_t)d * r_pad;
+  for (int i = threadIdx.x; i < cnt * (int)L; i += blockDim.x) {
+    const int f = i / cnt, b = i % cnt;
+    int8_t* dst = out + ((size_t)f * D * d + m) * r_pad + r0 + b;
+    write_digits(xs[b * L + f], q, D, dst, plane);
+  }
+}
+
+// ---------------------------------------------------------------- S4: inverse transform + rescale + store
+// One CTA per (row y, group of 32 blocks m).  C^ limb i: [L][n_out][d] u32.
+constexpr int kSpecMGroup = 32;
+__global__ void __launch_bounds__(256) spec_inverse_kernel(const uint32_t* __restrict__ c0, const uint32_t* __restrict__ c1,
+                                                           uint32_t n_out, uint32_t row0, uint32_t d, uint32_t k,
+                                                           uint32_t L, SpecInvConst cst, uint32_t* __restrict__ out_a) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t ld = L + 1;
+  uint32_t* xs = sm;                       // [32 m][L + 1]
+  uint32_t* keep = sm + kSpecMGroup * ld;  // [32 m][k + 1]: limb-1 result
+  const uint32_t y = row0 + blockIdx.y, m0 = blockIdx.x * kSpecMGroup;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int limb = 1; limb >= 0; --limb) {
+    const uint32_t* src = limb ? c1 : c0;
+    const uint32_t q = cst.q[limb];
+    for (uint32_t f = warp; f < L; f += nw) xs[lane * ld + f] = src[((size_t)f * n_out + y) * d + m0 + lane];
+    __syncthreads();
+    cyc_inv_smem(xs, kSpecMGroup, (int)ld, (int)L, cst.iv[limb], q);
+    if (limb) {
+      for (uint32_t i = threadIdx.x; i < kSpecMGroup * k; i += blockDim.x) {
+        const uint32_t mm = i / k, u = i % k;
+        keep[mm * (k + 1) + u] = xs[mm * ld + u];
+      }
+      __syncthreads();
+    }
+  }
+  const uint32_t q0 = cst.q[0], q1 = cst.q[1];
+  const uint32_t N = d * k;
+  for (uint32_t i = threadIdx.x; i < kSpecMGroup * k; i += blockDim.x) {
+    const uint32_t mm = i & 31, u = i >> 5;
+    const uint32_t x0 = xs[mm * ld + u];
+    const uint32_t x1 = keep[mm * (k + 1) + u];
+    uint32_t t;
+    if (x1 > (q1 >> 1)) t = csub(x0 + (q1 - x1), q0);
+    else t = sub_mod(x0, x1, q0);
+    const uint32_t j = k - 1 - u;
+    out_a[(size_t)(y - row0) * N + (size_t)d * j + m0 + mm] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);
+  }
+}
+
+// Fast S4 for L = 512 (k = 256): one warp per column (m, limb), 16 register-resident elements per lane.
+//   round 1: lane l holds positions 16 l + e (e < 16): DIT stages len = 1, 2, 4, 8 in registers;
+//   round 2: lane l = (l_lo, l_hi) holds l_lo + 16 e + 256 l_hi: stages len = 16 .. 128 in registers,
+//            stage len = 256 across lanes l ^ 16 -- only its lower half (outputs u < 256) is formed.
+// Harvey-lazy butterflies (values in [0, 4q)); the L^-1 of the inverse is folded into G^ (S1).
+// 16 columns per CTA, both limbs resident in smem (row pitch 545 words: pad(p) = p + p/16 keeps
+// all three access patterns conflict-free); results go through smem for 64-byte row stores.
+constexpr int kInv512Cols = 16;
+constexpr int kInv512Ld = 512 + 32 + 1;
+HE_D uint32_t pad16(uint32_t p) { return p + (p >> 4); }
+HE_D void dit_bf(uint32_t& x, uint32_t& y, uint2 w, uint32_t q2, uint32_t q) {  // X, Y in [0, 4q)
+  const uint32_t a = min(x, x - q2);
+  const uint32_t t = y * w.x - __umulhi(y, w.y) * q;
+  x = a + t;
+  y = a + q2 - t;
+}
+HE_D void dit_bf1(uint32_t& x, uint32_t& y, uint32_t q2) {  // twiddle 1, X, Y in [0, 4q)
+  const uint32_t a = min(x, x - q2), b = min(y, y - q2);
+  x = a + b;
+  y = a + q2 - b;
+}
+// one column: in smem (pitch-padded, bit-reversed positions) -> out[e] = INTT value u = l_lo + 16 e (lanes < 16)
+HE_D void inv512_column(uint32_t* col, const uint2* __restrict__ iv, uint32_t q, uint32_t lane, uint32_t (&out)[16]) {
+  const uint32_t q2 = 2 * q;
+  uint32_t x[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = col[17 * lane + e];
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) dit_bf1(x[e], x[e + 1], q2);
+#pragma unroll
+  for (int s = 1; s < 4; ++s) {
+    const int len = 1 << s;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      if (e & len) continue;
+      const int off = e & (len - 1);
+      const uint2 w = __ldg(iv + (off << (8 - s)));
+      dit_bf(x[e], x[e + len], w, q2, q);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 16; ++e) col[17 * lane + e] = x[e];
+  __syncwarp();
+  const uint32_t lo = lane & 15, hi = lane >> 4;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = col[lo + 17 * e + 272 * hi];
+  __syncwarp();
+#pragma unroll
+  for (int s = 4; s < 8; ++s) {
+    const int len = 1 << (s - 4);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      if (e & len) continue;
+      const uint32_t off = lo + 16 * (e & (len - 1));
+      const uint2 w = __ldg(iv + (off << (8 - s)));
+      dit_bf(x[e], x[e + len], w, q2, q);
+    }
+  }
+  // stage len = 256: lower lanes keep X + W Y; the upper lanes supply W Y
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const uint2 w = __ldg(iv + lo + 16 * e);
+    const uint32_t t = x[e] * w.x - __umulhi(x[e], w.y) * q;  // valid on the upper lanes: [0, 2q)
+    const uint32_t tp = __shfl_xor_sync(0xffffffffu, t, 16);
+    uint32_t v = min(x[e], x[e] - q2) + tp;                  // lower lanes: [0, 4q)
+    v = min(v, v - q2);
+    out[e] = min(v, v - q);
+  }
+}
+
+__global__ void __launch_bounds__(256) spec_inverse512_kernel(const uint32_t* __restrict__ c0,
+                                                              const uint32_t* __restrict__ c1, uint32_t n_out,
+                                                              uint32_t row0, uint32_t d, SpecInvConst cst,
+                                                              uint32_t* __restrict__ out_a) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* xs0 = sm;                                // [16 m][545]
+  uint32_t* xs1 = sm + kInv512Cols * kInv512Ld;      // [16 m][545]
+  const uint32_t y = row0 + blockIdx.y, m0 = blockIdx.x * kInv512Cols;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // phase A: C^[p][y][m0 .. m0 + 15] of both limbs -> xs[m][pad(p)] (64-byte rows, 4 rows per warp access)
+  {
+    const uint32_t mq = lane & 3, ps = lane >> 2;
+#pragma unroll 4
+    for (uint32_t p0 = warp * 8; p0 < 512; p0 += 64) {
+      const uint32_t p = p0 + ps;
+      const size_t g = ((size_t)p * n_out + y) * d + m0 + 4 * mq;
+      const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(c0 + g));
+      const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(c1 + g));
+      const uint32_t o = (4 * mq) * kInv512Ld + pad16(p);
+      xs0[o] = v0.x; xs0[o + kInv512Ld] = v0.y; xs0[o + 2 * kInv512Ld] = v0.z; xs0[o + 3 * kInv512Ld] = v0.w;
+      xs1[o] = v1.x; xs1[o + kInv512Ld] = v1.y; xs1[o + 2 * kInv512Ld] = v1.z; xs1[o + 3 * kInv512Ld] = v1.w;
+    }
+  }
+  __syncthreads();
+  const uint32_t q0 = cst.q[0], q1 = cst.q[1];
+  for (uint32_t m = warp; m < kInv512Cols; m += 8) {
+    uint32_t x1[16], x0[16];
+    inv512_column(xs1 + m * kInv512Ld, cst.iv[1], q1, lane, x1);
+    inv512_column(xs0 + m * kInv512Ld, cst.iv[0], q0, lane, x0);
+    if (lane < 16) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        uint32_t t;
+        if (x1[e] > (q1 >> 1)) t = csub(x0[e] + (q1 - x1[e]), q0);
+        else t = sub_mod(x0[e], x1[e], q0);
+        xs1[m * kInv512Ld + lane + 16 * e] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);  // u = lane + 16 e
+      }
+    }
+  }
+  __syncthreads();
+  // phase C: a'[y][d j + m0 + m] = res[m][u = 255 - j]: 64-byte row segments
+  const uint32_t N = d * 256;
+  uint32_t* dst = out_a + (size_t)(y - row0) * N + m0;
+  for (uint32_t i = threadIdx.x; i < 256 * kInv512Cols; i += 256) {
+    const uint32_t m = i & 15, j = i >> 4;
+    dst[(size_t)d * j + m] = xs1[m * kInv512Ld + 255 - j];
+  }
+}
+
+// ---------------------------------------------------------------- S3: per-frequency modular GEMM (tcgen05)
+constexpr int kSpecBN = 32;   // blocks m per tile
+constexpr int kSpecBK = 64;   // K bytes per stage
+constexpr int kSpecEpiWarps = 8;
+constexpr int kSpecThreads = 64 + 32 * kSpecEpiWarps;
+
+// UMMA smem descriptor, K-major, 64-byte swizzle: rows of 64 B, 8-row atoms (SBO = 512 B)
+HE_D uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(512u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)4u << 61;  // SWIZZLE_64B
+  return d;
+}
+
+template <int D>
+struct SpecCfg {
+  static constexpr int S = 2 * D - 1;
+  static constexpr int kChunk = kSpecBN / 2;                // B rows per TMA box (half a plane)
+  static constexpr int kABytes = D * 128 * kSpecBK;         // per CTA per stage
+  static constexpr int kBBytes = D * kChunk * kSpecBK;      // per CTA per stage
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr int kZeroBytes = 8192;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kZeroBytes + 1024 + 256;
+  static constexpr int kBuf = 256;                          // TMEM column stride of the two buffers
+  static_assert(S * kSpecBN <= kBuf, "shift accumulators exceed one TMEM buffer");
+  static_assert(kStages >= 2, "not enough shared memory");
+};
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
+    spec_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const SpecGemmArgs args) {
+  using C = SpecCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint8_t* sZero = sB + C::kStages * C::kBBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sZero + C::kZeroBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tmem_full = empty + C::kStages;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int m_tiles = args.d / kSpecBN;
+  const int y_tiles = (args.n_rows + 255) / 256;
+  const int num_tiles = m_tiles * y_tiles * args.L;
+  const int num_kb = args.r_pad / kSpecBK;
+
+  for (int i = threadIdx.x; i < C::kZeroBytes / 16; i += kSpecThreads)
+    reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 2 * kSpecEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc_2sm(tmem_slot, 512);
+    tmem_relinquish_2sm();
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_coords = [&](int tile, int& f, int& y0, int& m0) {
+    const int mt = tile % m_tiles;
+    const int rest = tile / m_tiles;
+    y0 = args.row0 + (rest % y_tiles) * 256;
+    f = rest / y_tiles;
+    m0 = mt * kSpecBN;
+  };
+
+  if (warp == 0) {
+    // ======================= TMA producer (both CTAs) =======================
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full0_remote = mapa_rank(&full[0], 0);
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        int f, y0, m0;
+        tile_coords(tile, f, y0, m0);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+          else mbar_arrive_cluster(full0_remote + stage * 8);
+          uint8_t* a_dst = sA + stage * C::kABytes;
+          uint8_t* b_dst = sB + stage * C::kBBytes;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+            tma_load_3d_2sm(a_dst + a * 128 * kSpecBK, &tmA, &full[stage], kb * kSpecBK, y0 + (int)rank * 128,
+                            f * D + a, kEvictLast);
+          // stacked operand [P0 | P1 | .. | P(D-1)] x 32 rows: this CTA holds chunks [rank*D, rank*D + D)
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const int g = (int)rank * D + c;
+            tma_load_3d_2sm(b_dst + c * C::kChunk * kSpecBK, &tmB, &full[stage], kb * kSpecBK,
+                            m0 + (g & 1) * C::kChunk, f * D + (g >> 1), kEvictLast);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (leader CTA) =======================
+    if (leader) {
+      constexpr uint32_t kIdesc = idesc_i8(256, D * kSpecBN);
+      constexpr uint32_t kIdescZ = idesc_i8(256, C::S * kSpecBN);
+      const uint64_t zdesc = desc_noswz(smem_u32(sZero), 128, 256);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++iter) {
+        const int buf = iter & 1;
+        const uint32_t acc = tmem_base + buf * C::kBuf;
+        if (iter >= 2) mbar_wait(&tmem_empty[buf], ((iter >> 1) - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) mma_i8_2sm(acc, zdesc, zdesc, kIdescZ, 0);
+        __syncwarp();
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
+            const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+            for (int kk = 0; kk < kSpecBK / 32; ++kk) {
+              const uint64_t bd = desc_sw64(b_base + kk * 32);
+#pragma unroll
+              for (int a = 0; a < D; ++a)
+                mma_i8_2sm(acc + a * kSpecBN, desc_sw64(a_base + a * 128 * kSpecBK + kk * 32), bd, kIdesc, 1);
+            }
+            tc_commit_2sm_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one()) tc_commit_2sm_mc(&tmem_full[buf], 0x3);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ======================= epilogue (both CTAs, 8 warps) =======================
+    const uint32_t ew = warp - 2;
+    const uint32_t quarter = warp & 3;
+    const uint32_t half = ew / 4;                      // columns [16 half, 16 half + 16)
+    const uint32_t lane_addr = (quarter * 32) << 16;
+    const uint32_t tmem_empty_remote = mapa_rank(&tmem_empty[0], 0);
+    const uint32_t q = args.q;
+    int iter = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs, ++iter) {
+      const int buf = iter & 1;
+      int f, y0, m0;
+      tile_coords(tile, f, y0, m0);
+      mbar_wait(&tmem_full[buf], (iter >> 1) & 1);
+      tc_fence_after();
+      const int y = y0 + (int)rank * 128 + (int)(quarter * 32 + lane);
+      uint32_t acc[C::S][16];
+      const uint32_t col = tmem_base + lane_addr + buf * C::kBuf + half * 16;
+#pragma unroll
+      for (int s = 0; s < C::S; ++s) {
+        tmem_ld_x8(col + s * kSpecBN, acc[s]);
+        tmem_ld_x8(col + s * kSpecBN + 8, acc[s] + 8);
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tmem_empty_remote + buf * 8);  // accumulators drained
+      uint32_t res[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        int64_t v = 0;
+#pragma unroll
+        for (int s = 0; s < C::S; ++s) v += (int64_t)(int32_t)acc[s][e] * (int64_t)args.pw[s];
+        const uint64_t u = (uint64_t)v + args.off64;
+        const uint64_t qh = __umul64hi(u, args.mu);
+        res[e] = csub((uint32_t)(u - qh * q), q);
+      }
+      if (y < args.row0 + args.n_rows) {
+        uint4* dst = reinterpret_cast<uint4*>(args.out + ((size_t)f * args.n_out + y) * args.d + m0 + half * 16);
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) dst[v4] = make_uint4(res[4 * v4], res[4 * v4 + 1], res[4 * v4 + 2], res[4 * v4 + 3]);
+      }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, 512);
+  }
+}
+
+// debug/reference form of S3 on CUDA cores (HE_SPEC_SIMPLE=1): same digit operands, exact int64 sums
+__global__ void spec_gemm_simple_kernel(const int8_t* __restrict__ G, const int8_t* __restrict__ A, SpecGemmArgs args,
+                                        int D) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t yy = blockIdx.y, f = blockIdx.z;
+  if (m >= (uint32_t)args.d) return;
+  const uint32_t y = args.row0 + yy;
+  const uint32_t q = args.q;
+  uint64_t accq = 0;
+  for (int r = 0; r < args.r_pad; ++r) {
+    int64_t gv = 0, av = 0;
+    for (int a = D - 1; a >= 0; --a) {
+      gv = gv * 256 + G[(((size_t)f * D + a) * args.n_out + y) * args.r_pad + r];
+      av = av * 256 + A[(((size_t)f * D + a) * args.d + m) * args.r_pad + r];
+    }
+    int64_t gm = gv % (int64_t)q, am = av % (int64_t)q;
+    if (gm < 0) gm += q;
+    if (am < 0) am += q;
+    accq = (accq + (uint64_t)gm * (uint64_t)am) % q;
+  }
+  args.out[((size_t)f * args.n_out + y) * args.d + m] = (uint32_t)accq;
+}
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out, uint32_t n_in, uint32_t k,
+                                const SpecTable& t, int D, uint32_t r_pad, int8_t* out, cudaStream_t s) {
+  const uint32_t R = n_in / k;
+  dim3 grid(n_out, (R + kSpecRChunk - 1) / kSpecRChunk);
+  const size_t smem = (size_t)kSpecRChunk * t.L * sizeof(uint32_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(spec_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  spec_weights_kernel<<<grid, 256, smem, s>>>(wdig, d_w, n_out, n_in, k, t.L, t.q, D, r_pad, t.fw, t.linv, t.linvp,
+                                              out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, uint32_t limb, const SpecTable& t,
+                             int D, uint32_t r_pad, int8_t* out, cudaStream_t s) {
+  dim3 grid(Rg.d, (n_ct + kSpecRChunk - 1) / kSpecRChunk);
+  const size_t smem = (size_t)kSpecRChunk * t.L * sizeof(uint32_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(spec_data_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  spec_data_kernel<<<grid, 256, smem, s>>>(ct, n_ct, limb, Rg.k, Rg.d, Rg.N, t.L, t.q, D, r_pad, t.fw, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const uint32_t* c1, uint32_t n_out,
+                                uint32_t row0, uint32_t rows, uint32_t L, const SpecInvConst& cst, uint32_t* out_a,
+                                cudaStream_t s) {
+  static const bool generic = getenv("HE_SPEC_INV_GENERIC") != nullptr;  // debug: the simple S4
+  if (L == 512 && Rg.k == 256 && Rg.d % kInv512Cols == 0 && !generic) {
+    dim3 grid(Rg.d / kInv512Cols, rows);
+    const size_t smem = (size_t)2 * kInv512Cols * kInv512Ld * sizeof(uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(spec_inverse512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    spec_inverse512_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, Rg.d, cst, out_a);
+    return cudaGetLastError();
+  }
+  if (Rg.d % kSpecMGroup) return cudaErrorInvalidValue;
+  dim3 grid(Rg.d / kSpecMGroup, rows);
+  const size_t smem = ((size_t)kSpecMGroup * (L + 1) + (size_t)kSpecMGroup * (Rg.k + 1)) * sizeof(uint32_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(spec_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  spec_inverse_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, Rg.d, Rg.k, L, cst, out_a);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_spec_gemm_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const SpecGemmArgs& a, int grid,
+                                      cudaStream_t s) {
+  using C = SpecCfg<D>;
+  auto kern = spec_gemm_kernel<D>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kSpecThreads, C::kSmemBytes, s>>>(tmA, tmB, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const SpecGemmArgs& a, int sm_count,
+                             cudaStream_t s) {
+  const int tiles = (a.d / kSpecBN) * ((a.n_rows + 255) / 256) * a.L;
+  const int pairs = sm_count / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  switch (D) {
+    case 1: return launch_spec_gemm_t<1>(tmA, tmB, a, grid, s);
+    case 2: return launch_spec_gemm_t<2>(tmA, tmB, a, grid, s);
+    case 3: return launch_spec_gemm_t<3>(tmA, tmB, a, grid, s);
+    case 4: return launch_spec_gemm_t<4>(tmA, tmB, a, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_spec_gemm_simple(int D, const int8_t* G, const int8_t* A, const SpecGemmArgs& a, cudaStream_t s) {
+  dim3 grid((a.d + 127) / 128, a.n_rows, a.L);
+  spec_gemm_simple_kernel<<<grid, 128, 0, s>>>(G, A, a, D);
+  return cudaGetLastError();
+}
+
+}  // namespace he

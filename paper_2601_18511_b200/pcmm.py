@@ -43,6 +43,8 @@ class MlwePcmmPlan:
     max_abs: int
     digits: object          # torch int8 [d_w, n_out, n_in]
     layout: str = "app_a_coeff"
+    algo: str = "direct"    # "spectral": a' columns by blockwise NTT correlation (K7), b' on K1
+    spec_weights: object = None   # torch int8, the spectral weights G^ (algo == "spectral")
     _handle: object = field(default=None, repr=False)
     _workspace: object = field(default=None, repr=False)
     _stream_bufs: object = field(default=None, repr=False)
@@ -72,14 +74,25 @@ class MlwePcmmPlan:
             pass
 
 
-def make_mlwe_pcmm_plan(ctx: HeContext, weights, d_w: int | None = None) -> MlwePcmmPlan:
+ALGOS = ("spectral", "direct")
+
+
+def make_mlwe_pcmm_plan(ctx: HeContext, weights, d_w: int | None = None, algo: str = "spectral") -> MlwePcmmPlan:
     """Encode the float weights W (n_out x n_in) for the MLWE PCMM.
 
     W~ = round_half_even(q1 * W) (Delta_w = q1 so the op keeps the input scale),
     each k x k block conjugated by sigma (PAPER.md:672 / bitrev.py:57-70 in component
     order), split into ``d_w`` balanced int8 digit planes; ``d_w`` defaults to the
     fewest digits that hold max|W~|.
+
+    ``algo`` picks how the a' columns are computed -- the outputs are the same words:
+      "spectral" (default): blockwise length-2k cyclic NTT correlations (K7: the a-part
+                  GEMM's columns are twisted shifts of one polynomial),
+                  per-frequency modular GEMMs on tcgen05; b' columns on K1;
+      "direct":   K1 over all d (1 + k) GEMM columns (BCHPS24 Alg. 2 as a plain GEMM).
     """
+    if algo not in ALGOS:
+        raise ValueError(f"algo must be one of {ALGOS}, got {algo!r}")
     torch = _torch()
     p = ctx.params
     w = torch.as_tensor(weights, dtype=torch.float64, device=ctx.device)
@@ -107,7 +120,13 @@ def make_mlwe_pcmm_plan(ctx: HeContext, weights, d_w: int | None = None) -> Mlwe
                 ctx.stream())
     h = ctypes.c_void_p()
     native.call("he_pcmm_plan_create", ctx.handle, digits.data_ptr(), n_out, n_in, d_w, ctypes.byref(h))
-    return MlwePcmmPlan(n_out, n_in, d_w, max_abs, digits, _handle=h)
+    plan = MlwePcmmPlan(n_out, n_in, d_w, max_abs, digits, algo=algo, _handle=h)
+    if algo == "spectral":
+        nb = ctypes.c_uint64()
+        native.call("he_pcmm_spectral_weight_bytes", h, ctypes.byref(nb))
+        plan.spec_weights = torch.empty(int(nb.value), dtype=torch.int8, device=ctx.device)
+        native.call("he_pcmm_spectral_prepare", h, plan.spec_weights.data_ptr(), ctx.stream())
+    return plan
 
 
 def _check_operand(ctx: HeContext, plan: MlwePcmmPlan, X) -> None:

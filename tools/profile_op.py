@@ -12,6 +12,7 @@ from paper_2601_18511_b200 import HeContext, HeParams, make_mlwe_pcmm_plan, pcmm
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="4096x11008")
 ap.add_argument("--ops", type=int, default=2)
+ap.add_argument("--algo", default="spectral")
 a = ap.parse_args()
 n_out, n_in = (int(v) for v in a.shape.split("x"))
 P = HeParams.llama()
@@ -21,7 +22,7 @@ W = (torch.rand((n_out, n_in), generator=g, device="cuda", dtype=torch.float64) 
 A = torch.rand((P.tokens, n_in), generator=g, device="cuda", dtype=torch.float64) * 2 - 1
 sk = ctx.keygen(1)
 X = ctx.encrypt_acts(sk, A, seed=2)
-plan = make_mlwe_pcmm_plan(ctx, W)
+plan = make_mlwe_pcmm_plan(ctx, W, algo=a.algo)
 for _ in range(a.ops):
     Y = pcmm_mlwe(ctx, plan, X)
 torch.cuda.synchronize()
