@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--shape", default="4096x11008")
     ap.add_argument("--params", choices=["llama", "wide"], default="llama")
+    ap.add_argument("--algo", choices=["spectral", "direct"], default="spectral",
+                    help="a'-column algorithm (same output words): K7 spectral (default) or K1 direct GEMM")
+    ap.add_argument("--no-direct", action="store_true", help="skip the side measurement of the direct K1 path")
     ap.add_argument("--cpu-rows", type=int, default=64, help="oracle sample rows for cpu_baseline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -138,7 +141,7 @@ def run_ours(a, rank: int, world: int, local: int):
 
     from paper_2601_18511_b200 import HeContext, make_mlwe_pcmm_plan, pcmm_mlwe
     from paper_2601_18511_b200.context import MlweBlocks
-    from paper_2601_18511_b200.pcmm import pcmm_ops
+    from paper_2601_18511_b200.pcmm import pcmm_ops, spectral_gemm_ops, spectral_inverse_bytes
     from paper_2601_18511_b200.sharding import row_shards, shard_slots
 
     torch.cuda.set_device(local)
@@ -161,7 +164,7 @@ def run_ours(a, rank: int, world: int, local: int):
     X = ctx.encrypt_acts(sk, A, seed=11)
     if rows == 0:
         raise SystemExit("more ranks than output row blocks")
-    plan = make_mlwe_pcmm_plan(ctx, W[b0 * k:b1 * k])
+    plan = make_mlwe_pcmm_plan(ctx, W[b0 * k:b1 * k], algo=a.algo)
     out_b = torch.empty((per, N), dtype=torch.int32, device=dev)
     out_a = torch.empty((per * k, N), dtype=torch.int32, device=dev)
     Y = MlweBlocks(out_b[: b1 - b0], out_a[:rows], level=0, n_rows=rows)
@@ -172,14 +175,11 @@ def run_ours(a, rank: int, world: int, local: int):
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream(dev)
-    ev_g0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
-    ev_g1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
 
-    def step(i=None):
+    def step():
         if world > 1:
             dist.broadcast(X.data, src=0)
-        ev = (ev_g0[i], ev_g1[i]) if i is not None else None
-        pcmm_mlwe(ctx, plan, X, out=Y, gemm_events=ev)
+        pcmm_mlwe(ctx, plan, X, out=Y)
         if world > 1:
             dist.all_gather_into_tensor(all_b, out_b)
             dist.all_gather_into_tensor(all_a, out_a)
@@ -190,19 +190,26 @@ def run_ours(a, rank: int, world: int, local: int):
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    plan.profile(True)            # per-stage CUDA events on the launching stream (he_pcmm_profile)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         t0.record(stream)
         for i in range(a.steps):
-            step(i)
+            step()
         t1.record(stream)
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / a.steps
-    gemm_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in zip(ev_g0, ev_g1)]))
+    stages = plan.profile_read()
+    plan.profile(False)
+    stage_ms = {name: v[0] / a.steps for name, v in stages.items()}
+    # stage event pairs per step; the spectral data stage holds two kernel launches (one per limb)
+    launches_per_step = sum(v[1] for v in stages.values()) // a.steps + (1 if a.algo == "spectral" else 0)
     if world > 1:
-        tt = torch.tensor([ms, gemm_ms], dtype=torch.float64, device=dev)
+        names = sorted(stage_ms)
+        tt = torch.tensor([ms] + [stage_ms[n] for n in names], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, gemm_ms = float(tt[0]), float(tt[1])
+        ms = float(tt[0])
+        stage_ms = {n: float(v) for n, v in zip(names, tt[1:].tolist())}
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
@@ -210,22 +217,35 @@ def run_ours(a, rank: int, world: int, local: int):
         e2e = run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a,
                       all_b if world > 1 else None, all_a if world > 1 else None)
 
-    # ---------------- roofline of the dominant kernel (K1)
-    ops = pcmm_ops(P, rows, n_in, plan.d_w)
-    achieved = ops / (gemm_ms * 1e-3) / 1e12
+    # ---------------- roofline of the dominant kernel
     cublas = measure_cublas_int8(dev) if rank == 0 else None
-    traffic = load_traffic(a.shape, plan.d_w)
-    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": INT8_PEAK_TOPS, "unit": "TOPS",
-            "frac": round(achieved / INT8_PEAK_TOPS, 4), "traffic": traffic,
-            "kernel": "he::modgemm_kernel (K1, tcgen05 kind::i8)", "kernel_ms": round(gemm_ms, 3),
-            "int8_ops_per_launch": ops,
-            "peak_note": "NVIDIA dense INT8 spec (4.5 POPS); MEASURED_PEAKS.json has no int8 entry",
-            "cublas_int8_tops_measured": cublas,
-            "frac_of_2x_measured_bf16": round(achieved / (2 * measured_bf16()), 4) if measured_bf16() else None}
+    if a.algo == "direct":
+        roof = k1_roofline(P, rows, n_in, plan.d_w, stage_ms["modgemm"], a.shape, cublas)
+    else:
+        # K7 S4 (spectral inverse + rescale + a' store) dominates: HBM roofline on its algorithmic bytes
+        inv_ms = stage_ms["spectral_inverse"]
+        nbytes = spectral_inverse_bytes(P, rows)
+        gbs = nbytes / (inv_ms * 1e-3) / 1e9
+        hbm = measured_hbm()
+        roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
+                "traffic": load_traffic(a.shape, "spectral_inverse"),
+                "kernel": "he::spec_inverse512_kernel (K7 S4: 512-pt INTT x 2 limbs, rescale, a' store)",
+                "kernel_ms": round(inv_ms, 3), "algorithmic_bytes_per_launch": nbytes,
+                "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
+        gops = sum(spectral_gemm_ops(P, rows, n_in, L) for L in (0, 1))
+        g_ms = stage_ms["spectral_gemm_q0"] + stage_ms["spectral_gemm_q1"]
+        roof["spectral_gemm"] = {
+            "kernel": "he::spec_gemm_kernel<4>/<3> (K7 S3, tcgen05 kind::i8, per-frequency modular GEMM)",
+            "ms": round(g_ms, 3), "int8_ops": gops, "TOPS": round(gops / (g_ms * 1e-3) / 1e12, 1),
+            "frac_int8_peak": round(gops / (g_ms * 1e-3) / 1e12 / INT8_PEAK_TOPS, 4),
+            "traffic": load_traffic(a.shape, "spectral_gemm")}
 
     extras = {}
+    if rank == 0 and world == 1 and a.algo == "spectral" and not a.no_direct:
+        extras["direct_k1"] = direct_side(a, ctx, W_rows=(b0 * k, b1 * k), X=X, Y=Y, P=P, rows=rows, n_in=n_in,
+                                          dev=dev, cublas=cublas, ref=Y)
     if rank == 0 and world == 1 and not a.no_extras:
-        extras = side_measurements(P, dev)
+        extras.update(side_measurements(P, dev))
 
     cpu = None
     if rank == 0 and world == 1 and a.cpu_rows > 0:
@@ -242,21 +262,73 @@ def run_ours(a, rank: int, world: int, local: int):
                        "tokens": P.tokens, "N": N, "mlwe": [P.mlwe_degree, P.mlwe_rank],
                        "moduli": list(P.moduli), "log_delta": P.log_delta,
                        "digits": {"weight": plan.d_w, "ct_q0": d0, "ct_q1": d1},
+                       "algo": a.algo + (" (K7: a' by blockwise 512-pt NTT correlation + per-frequency tcgen05 "
+                                         "GEMMs; b' on K1)" if a.algo == "spectral" else " (K1 over all columns)"),
                        "parallelism": f"row-shard x{world}" + (" + NCCL bcast/all-gather" if world > 1 else ""),
                        "l2": "inputs larger than L2: each op writes and reads a "
-                             f"{plan.workspace_bytes() / 1e9:.2f} GB ciphertext-digit workspace"},
+                             f"{plan.workspace_bytes() / 1e9:.2f} GB workspace"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 2 * a.steps,
+            "gpu_launches": launches_per_step * a.steps,
             "clocks": clk.summary(),
-            "kernels_ms": {"modgemm": round(gemm_ms, 3), "decompose_and_rest": round(ms - gemm_ms, 3)},
+            "kernels_ms": {n: round(v, 3) for n, v in stage_ms.items()},
         }
         line.update(extras)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def k1_roofline(P, rows, n_in, d_w, gemm_ms, shape, cublas):
+    from paper_2601_18511_b200.pcmm import pcmm_ops
+
+    ops = pcmm_ops(P, rows, n_in, d_w)
+    achieved = ops / (gemm_ms * 1e-3) / 1e12
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": INT8_PEAK_TOPS, "unit": "TOPS",
+            "frac": round(achieved / INT8_PEAK_TOPS, 4), "traffic": load_traffic(shape, "modgemm"),
+            "kernel": "he::modgemm2_kernel (K1, tcgen05 kind::i8)", "kernel_ms": round(gemm_ms, 3),
+            "int8_ops_per_launch": ops,
+            "peak_note": "NVIDIA dense INT8 spec (4.5 POPS); MEASURED_PEAKS.json has no int8 entry",
+            "cublas_int8_tops_measured": cublas,
+            "frac_of_2x_measured_bf16": round(achieved / (2 * measured_bf16()), 4) if measured_bf16() else None}
+
+
+def direct_side(a, ctx, W_rows, X, Y, P, rows, n_in, dev, cublas, ref):
+    """The direct K1 path (all d (1 + k) GEMM columns on tcgen05) on the same inputs: ms/op, its
+    K1 roofline, and a word-for-word comparison with the spectral output (side measurement)."""
+    import torch
+
+    from paper_2601_18511_b200 import make_mlwe_pcmm_plan, pcmm_mlwe
+
+    try:
+        g = torch.Generator(device=dev).manual_seed(20260117)
+        n_out = shape_of(a.shape)[0]
+        W = (torch.rand((n_out, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1) / math.sqrt(n_in)
+        plan = make_mlwe_pcmm_plan(ctx, W[W_rows[0]:W_rows[1]], algo="direct")
+        del W
+        out = pcmm_mlwe(ctx, plan, X)
+        same = bool(torch.equal(out.out_a, ref.out_a) and torch.equal(out.out_b, ref.out_b))
+        for _ in range(2):
+            pcmm_mlwe(ctx, plan, X, out=out)
+        plan.profile(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            pcmm_mlwe(ctx, plan, X, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        st = plan.profile_read()
+        plan.profile(False)
+        res = {"ms_per_op": round(e0.elapsed_time(e1) / 5, 3), "words_equal_spectral": same,
+               "roofline": k1_roofline(P, rows, n_in, plan.d_w, st["modgemm"][0] / 5, a.shape, cublas)}
+        del plan, out
+        torch.cuda.empty_cache()
+        return res
+    except Exception as exc:  # side measurement never breaks the headline line
+        return {"error": repr(exc)}
 
 
 def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
@@ -309,7 +381,7 @@ def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
     return {"value": round(ms, 3), "unit": "ms/op", "h2d_bytes_per_step": int(h_in.numel() * 4),
             "d2h_bytes_per_step": int((plan.n_out // ctx.params.mlwe_rank + plan.n_out) * ctx.params.N * 4)
             if world == 1 else int((h_b.numel() + h_a.numel()) * 4), "steps": steps,
-            "path": "pcmm_mlwe_to_host (K1 row chunks streamed to pinned host memory)" if world == 1
+            "path": "pcmm_mlwe_to_host (row chunks streamed to pinned host memory)" if world == 1
             else "broadcast + pcmm_mlwe + all_gather + D2H on rank 0"}
 
 
@@ -411,13 +483,12 @@ def measured_bf16():
         return None
 
 
-def load_traffic(shape: str, d_w: int):
-    """dram bytes per K1 launch from the committed ncu --set full summary, if any."""
+def load_traffic(shape: str, kernel: str):
+    """dram read + write bytes per launch of `kernel` from the committed ncu --set full summary."""
     p = ROOT / "profiles" / "ncu_summary.json"
     try:
-        data = json.loads(p.read_text())
-        ent = data.get("modgemm", {}).get(shape)
-        if ent and ent.get("d_w") == d_w:
+        ent = json.loads(p.read_text()).get(kernel, {}).get(shape)
+        if ent:
             return ent.get("dram_bytes_per_launch")
     except Exception:
         pass

@@ -137,6 +137,12 @@ he_status he_pcmm_spectral_weight_bytes(const he_pcmm_plan* plan, uint64_t* byte
 he_status he_pcmm_spectral_prepare(he_pcmm_plan* plan, int8_t* spec_weights_dev, void* stream);
 /* 0 = K1 over all columns (direct), 1 = spectral */
 he_status he_pcmm_algo(const he_pcmm_plan* plan, int* algo);
+/* Profiling: while enabled, every stage launch of the plan records a CUDA event pair on its
+ * stream; he_pcmm_profile_read synchronizes, returns the summed device ms and launch count per
+ * stage {0 K3 decompose, 1 K7 data transform S2, 2 K1 GEMM, 3 S3 limb 0, 4 S3 limb 1, 5 S4} and
+ * clears them.  Not thread-safe while enabled (mirrors CostLedger's fork/merge rule). */
+he_status he_pcmm_profile(const he_pcmm_plan* plan, int enable);
+he_status he_pcmm_profile_read(const he_pcmm_plan* plan, double* ms, uint32_t* launches, uint32_t n);
 
 /* ---------------------------------------------------------------- Rhombus PCMv (K6), degree n = rhombus_degree */
 /* Vector layout (App. A + h): element e sits at degree-N coefficient

@@ -437,15 +437,19 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
     const SpecWs w = spec_ws(p);
     cudaStream_t st = (cudaStream_t)stream;
     int8_t* base = (int8_t*)ws;
+    p->prof_begin(0, st);
     HE_CUDA(launch_decompose(p->ctx->R, ct_in, p->n_in, (int)p->d0, (int)p->d1, base + w.bdig,
                              (uint64_t)p->ctx->R.d * p->n_in, st, 1),
             "decompose (b columns)");
+    p->prof_end(0, st);
+    p->prof_begin(1, st);
     HE_CUDA(cudaMemsetAsync(base + w.a0, 0, w.c0 - w.a0, st), "memset");
     const uint32_t n_ct = p->n_in / p->ctx->R.k;
     for (uint32_t L = 0; L < 2; ++L)
       HE_CUDA(launch_spec_data(p->ctx->R, ct_in, n_ct, L, p->st[L], (int)p->dsp[L], p->r_pad, base + (L ? w.a1 : w.a0),
                                st),
               "spectral data transform");
+    p->prof_end(1, st);
     return HE_OK;
   }
   if (fused_path(p)) {
@@ -454,9 +458,11 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
             "digitize");
     return HE_OK;
   }
+  p->prof_begin(0, (cudaStream_t)stream);
   HE_CUDA(launch_decompose(p->ctx->R, ct_in, p->n_in, (int)p->d0, (int)p->d1, (int8_t*)ws,
                            (uint64_t)p->width * p->n_in, (cudaStream_t)stream),
           "decompose");
+  p->prof_end(0, (cudaStream_t)stream);
   return HE_OK;
 }
 
@@ -489,18 +495,24 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     CUtensorMap tmB;
     he_status s = make_map_sw64(&tmB, A, p->r_pad, p->ctx->R.d, (uint64_t)p->L * p->dsp[L], 16);
     if (s) return s;
+    p->prof_begin(3 + L, st);
     HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, a, p->ctx->sm_count, st), "spectral gemm");
+    p->prof_end(3 + L, st);
   }
   SpecInvConst c;
   for (int L = 0; L < 2; ++L) {
     c.q[L] = p->epi.q[L];
     c.iv[L] = p->st[L].iv;
+    c.r2[L] = p->st[L].r2;
+    for (int i = 0; i < 11; ++i) c.r1[L][i] = p->st[L].r1[i];
     c.linv[L] = p->st[L].linv;
     c.linvp[L] = p->st[L].linvp;
   }
   c.q1inv = p->epi.q1inv;
   c.q1invp = p->epi.q1invp;
+  p->prof_begin(5, st);
   HE_CUDA(launch_spec_inverse(p->ctx->R, C[0], C[1], p->n_out, row0, rows, p->L, c, out_a, st), "spectral inverse");
+  p->prof_end(5, st);
   return HE_OK;
 }
 
@@ -575,8 +587,10 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
     if (env_pairs > 0 && env_pairs < pairs) pairs = env_pairs;
     grid = 2 * (tiles < pairs ? tiles : pairs);
   }
+  p->prof_begin(2, (cudaStream_t)stream);
   HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, tmA, tmB, tmBa, a, grid, (cudaStream_t)stream),
           "modgemm");
+  p->prof_end(2, (cudaStream_t)stream);
   if (spec) return spec_rows(p, ws, row0, rows, out_a, (cudaStream_t)stream);
   return HE_OK;
 }
@@ -661,5 +675,33 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
 extern "C" he_status he_pcmm_algo(const he_pcmm_plan* p, int* algo) {
   if (!p || !algo) return fail(HE_EINVAL, "null argument");
   *algo = p->algo;
+  return HE_OK;
+}
+
+// ---------------------------------------------------------------- per-stage device times (profiling)
+extern "C" he_status he_pcmm_profile(const he_pcmm_plan* p, int enable) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  p->prof_clear();
+  p->prof_on = enable != 0;
+  return HE_OK;
+}
+
+extern "C" he_status he_pcmm_profile_read(const he_pcmm_plan* p, double* ms, uint32_t* launches, uint32_t n) {
+  if (!p || !ms || !launches) return fail(HE_EINVAL, "null argument");
+  for (uint32_t i = 0; i < n; ++i) {
+    ms[i] = 0;
+    launches[i] = 0;
+  }
+  for (int st = 0; st < he_pcmm_plan::kStages && st < (int)n; ++st) {
+    for (auto& pr : p->prof_ev[st]) {
+      if (!pr.first || !pr.second) continue;
+      HE_CUDA(cudaEventSynchronize(pr.second), "profile sync");
+      float t = 0;
+      HE_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second), "profile elapsed");
+      ms[st] += t;
+      launches[st] += 1;
+    }
+  }
+  p->prof_clear();
   return HE_OK;
 }

@@ -3,6 +3,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+#include <vector>
+
 #include "../../include/he_b200.h"
 #include "he_kernels.h"
 
@@ -26,7 +29,36 @@ struct he_pcmm_plan {
   const int8_t* spec_w = nullptr;  // caller-owned: G^ limb 0 [L][D0][n_out][r_pad], then limb 1
   CUtensorMap tmSA[2];
   he::SpecTable st[2];
+  // he_pcmm_profile: per-stage CUDA events recorded on the launching stream (profiling state only)
+  static constexpr int kStages = 6;
+  mutable bool prof_on = false;
+  mutable std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[kStages];
+  cudaEvent_t prof_begin(int stage, cudaStream_t s) const {
+    if (!prof_on) return nullptr;
+    cudaEvent_t e0 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventRecord(e0, s);
+    prof_ev[stage].emplace_back(e0, nullptr);
+    return e0;
+  }
+  void prof_end(int stage, cudaStream_t s) const {
+    if (!prof_on || prof_ev[stage].empty()) return;
+    cudaEvent_t e1 = nullptr;
+    cudaEventCreate(&e1);
+    cudaEventRecord(e1, s);
+    prof_ev[stage].back().second = e1;
+  }
+  void prof_clear() const {
+    for (auto& v : prof_ev) {
+      for (auto& pr : v) {
+        if (pr.first) cudaEventDestroy(pr.first);
+        if (pr.second) cudaEventDestroy(pr.second);
+      }
+      v.clear();
+    }
+  }
   ~he_pcmm_plan() {
+    prof_clear();
     he::spec_table_free(st[0]);
     he::spec_table_free(st[1]);
   }

@@ -63,6 +63,8 @@ struct SpecTable {  // cyclic NTT of length L mod q
   uint32_t L = 0, q = 0;
   uint2* fw = nullptr;   // (w^j, Shoup) j < L/2
   uint2* iv = nullptr;   // (w^-j, Shoup) j < L/2
+  uint2* r2 = nullptr;   // L = 512: per-stage lane tables of the fast inverse (he_spectral.cu)
+  uint2 r1[11] = {};     // L = 512: round-1 twiddles of the fast inverse (host copy, passed as kernel params)
   uint32_t linv = 0, linvp = 0;
 };
 cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q);
@@ -79,6 +81,8 @@ struct SpecGemmArgs {
 struct SpecInvConst {
   uint32_t q[2];
   const uint2* iv[2];
+  const uint2* r2[2];
+  uint2 r1[2][11];          // L = 512 round-1 twiddles w^-(off << (8 - s)), s = 1..3, off = 1 .. 2^s - 1
   uint32_t linv[2], linvp[2];
   uint32_t q1inv, q1invp;
 };

@@ -47,7 +47,8 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
   }
   if (!w) return cudaErrorInvalidValue;
   const uint64_t wi = powmod_h(w, q - 2, q);
-  uint32_t* h = new uint32_t[2 * (size_t)L];  // fw pairs [L/2][2], iv pairs [L/2][2]
+  const size_t nr2 = L == 512 ? 496 : 0;  // S4 round-2 table (L = 512 only)
+  uint32_t* h = new uint32_t[2 * (size_t)L + 2 * nr2];  // fw pairs [L/2][2], iv pairs [L/2][2], r2 pairs
   uint64_t p = 1, pi = 1;
   for (uint32_t j = 0; j < L / 2; ++j) {
     h[2 * j] = (uint32_t)p;
@@ -57,21 +58,38 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
     p = p * w % q;
     pi = pi * wi % q;
   }
+  // r2: stage s = 4..8 at 16 (2^(s-4) - 1): entry [i][lo] = w^-((lo + 16 i) << (8 - s))
+  for (int st = 4; st <= 8 && nr2; ++st) {
+    const int len = 1 << (st - 4), base = 16 * (len - 1);
+    for (int i = 0; i < len; ++i)
+      for (int lo = 0; lo < 16; ++lo) {
+        const uint32_t j = (uint32_t)(lo + 16 * i) << (8 - st);
+        h[2 * (size_t)L + 2 * (base + 16 * i + lo)] = h[L + 2 * j];
+        h[2 * (size_t)L + 2 * (base + 16 * i + lo) + 1] = h[L + 2 * j + 1];
+      }
+  }
+  for (int st = 1; st <= 3 && nr2; ++st)
+    for (int off = 1; off < (1 << st); ++off) {
+      const uint32_t j = (uint32_t)off << (8 - st);
+      t.r1[(1 << st) - st - 1 + off - 1] = make_uint2(h[L + 2 * j], h[L + 2 * j + 1]);
+    }
   t.linv = (uint32_t)powmod_h(L, q - 2, q);
   t.linvp = shoup_pre(t.linv, q);
   uint32_t* dptr = nullptr;
-  cudaError_t e = cudaMalloc(&dptr, 2 * (size_t)L * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemcpy(dptr, h, 2 * (size_t)L * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  const size_t words = 2 * (size_t)L + 2 * nr2;
+  cudaError_t e = cudaMalloc(&dptr, words * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemcpy(dptr, h, words * sizeof(uint32_t), cudaMemcpyHostToDevice);
   delete[] h;
   if (e != cudaSuccess) return e;
   t.fw = reinterpret_cast<uint2*>(dptr);
   t.iv = reinterpret_cast<uint2*>(dptr + L);
+  t.r2 = nr2 ? reinterpret_cast<uint2*>(dptr + 2 * L) : nullptr;
   return cudaSuccess;
 }
 
 void spec_table_free(SpecTable& t) {
   if (t.fw) cudaFree(t.fw);
-  t.fw = t.iv = nullptr;
+  t.fw = t.iv = t.r2 = nullptr;
 }
 
 // ---------------------------------------------------------------- cooperative cyclic NTTs in shared memory
@@ -223,15 +241,18 @@ __global__ void __launch_bounds__(256) spec_inverse_kernel(const uint32_t* __res
   }
 }
 
-// Fast S4 for L = 512 (k = 256): one warp per column (m, limb), 16 register-resident elements per lane.
-//   round 1: lane l holds positions 16 l + e (e < 16): DIT stages len = 1, 2, 4, 8 in registers;
+// Fast S4 for L = 512 (k = 256): one warp per column m, both limbs interleaved (ILP), 16
+// register-resident elements per lane and limb.
+//   round 1: lane l holds positions 16 l + e (e < 16): DIT stages len = 1, 2, 4, 8 in registers
+//            (lane-uniform twiddles; twiddle-1 butterflies skip the multiply);
 //   round 2: lane l = (l_lo, l_hi) holds l_lo + 16 e + 256 l_hi: stages len = 16 .. 128 in registers,
 //            stage len = 256 across lanes l ^ 16 -- only its lower half (outputs u < 256) is formed.
+//            Round-2 twiddles come from a per-stage [i][l_lo] table (one 128-B line per access).
 // Harvey-lazy butterflies (values in [0, 4q)); the L^-1 of the inverse is folded into G^ (S1).
-// 16 columns per CTA, both limbs resident in smem (row pitch 545 words: pad(p) = p + p/16 keeps
-// all three access patterns conflict-free); results go through smem for 64-byte row stores.
+// 16 columns per CTA, both limbs resident in smem; row pitch 546 words with pad(p) = p + p/16
+// keeps the transposing loads, both rounds and the row-ordered read-out conflict-free.
 constexpr int kInv512Cols = 16;
-constexpr int kInv512Ld = 512 + 32 + 1;
+constexpr int kInv512Ld = 546;
 HE_D uint32_t pad16(uint32_t p) { return p + (p >> 4); }
 HE_D void dit_bf(uint32_t& x, uint32_t& y, uint2 w, uint32_t q2, uint32_t q) {  // X, Y in [0, 4q)
   const uint32_t a = min(x, x - q2);
@@ -244,14 +265,22 @@ HE_D void dit_bf1(uint32_t& x, uint32_t& y, uint32_t q2) {  // twiddle 1, X, Y i
   x = a + b;
   y = a + q2 - b;
 }
-// one column: in smem (pitch-padded, bit-reversed positions) -> out[e] = INTT value u = l_lo + 16 e (lanes < 16)
-HE_D void inv512_column(uint32_t* col, const uint2* __restrict__ iv, uint32_t q, uint32_t lane, uint32_t (&out)[16]) {
-  const uint32_t q2 = 2 * q;
-  uint32_t x[16];
+struct Inv512Limb {
+ uint32_t* col;        // smem column (pitch-padded, bit-reversed positions)
+  const uint2* r2;      // round-2 table: stage s at 16 (2^(s-4) - 1), entry [i][l_lo]
+  uint32_t q;
+};
+// -> out[l][e] = INTT value u = l_lo + 16 e of limb l (valid on lanes < 16)
+HE_D void inv512_pair(const Inv512Limb (&L)[2], const SpecInvConst& cst, uint32_t lane, uint32_t (&out)[2][16]) {
+  uint32_t x[2][16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = col[17 * lane + e];
+  for (int l = 0; l < 2; ++l)
 #pragma unroll
-  for (int e = 0; e < 16; e += 2) dit_bf1(x[e], x[e + 1], q2);
+    for (int e = 0; e < 16; ++e) x[l][e] = L[l].col[17 * lane + e];
+#pragma unroll
+  for (int e = 0; e < 16; e += 2)
+#pragma unroll
+    for (int l = 0; l < 2; ++l) dit_bf1(x[l][e], x[l][e + 1], 2 * L[l].q);
 #pragma unroll
   for (int s = 1; s < 4; ++s) {
     const int len = 1 << s;
@@ -259,75 +288,88 @@ HE_D void inv512_column(uint32_t* col, const uint2* __restrict__ iv, uint32_t q,
     for (int e = 0; e < 16; ++e) {
       if (e & len) continue;
       const int off = e & (len - 1);
-      const uint2 w = __ldg(iv + (off << (8 - s)));
-      dit_bf(x[e], x[e + len], w, q2, q);
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        if (off == 0) dit_bf1(x[l][e], x[l][e + len], 2 * L[l].q);
+        else dit_bf(x[l][e], x[l][e + len], cst.r1[l][(1 << s) - s - 1 + off - 1], 2 * L[l].q, L[l].q);
+      }
     }
   }
 #pragma unroll
-  for (int e = 0; e < 16; ++e) col[17 * lane + e] = x[e];
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) L[l].col[17 * lane + e] = x[l][e];
   __syncwarp();
   const uint32_t lo = lane & 15, hi = lane >> 4;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = col[lo + 17 * e + 272 * hi];
-  __syncwarp();
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) x[l][e] = L[l].col[lo + 17 * e + 272 * hi];
 #pragma unroll
   for (int s = 4; s < 8; ++s) {
     const int len = 1 << (s - 4);
+    const int base = 16 * (len - 1);
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       if (e & len) continue;
-      const uint32_t off = lo + 16 * (e & (len - 1));
-      const uint2 w = __ldg(iv + (off << (8 - s)));
-      dit_bf(x[e], x[e + len], w, q2, q);
+      const int i = e & (len - 1);
+#pragma unroll
+      for (int l = 0; l < 2; ++l)
+        dit_bf(x[l][e], x[l][e + len], __ldg(L[l].r2 + base + 16 * i + lo), 2 * L[l].q, L[l].q);
     }
   }
   // stage len = 256: lower lanes keep X + W Y; the upper lanes supply W Y
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    const uint2 w = __ldg(iv + lo + 16 * e);
-    const uint32_t t = x[e] * w.x - __umulhi(x[e], w.y) * q;  // valid on the upper lanes: [0, 2q)
-    const uint32_t tp = __shfl_xor_sync(0xffffffffu, t, 16);
-    uint32_t v = min(x[e], x[e] - q2) + tp;                  // lower lanes: [0, 4q)
-    v = min(v, v - q2);
-    out[e] = min(v, v - q);
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const uint32_t q = L[l].q, q2 = 2 * q;
+      const uint2 w = __ldg(L[l].r2 + 240 + 16 * e + lo);
+      const uint32_t t = x[l][e] * w.x - __umulhi(x[l][e], w.y) * q;  // upper lanes: [0, 2q)
+      const uint32_t tp = __shfl_xor_sync(0xffffffffu, t, 16);
+      uint32_t v = min(x[l][e], x[l][e] - q2) + tp;                  // lower lanes: [0, 4q)
+      v = min(v, v - q2);
+      out[l][e] = min(v, v - q);
+    }
   }
 }
 
-__global__ void __launch_bounds__(256) spec_inverse512_kernel(const uint32_t* __restrict__ c0,
-                                                              const uint32_t* __restrict__ c1, uint32_t n_out,
-                                                              uint32_t row0, uint32_t d, SpecInvConst cst,
-                                                              uint32_t* __restrict__ out_a) {
+__global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t* __restrict__ c0,
+                                                                 const uint32_t* __restrict__ c1, uint32_t n_out,
+                                                                 uint32_t row0, uint32_t d, SpecInvConst cst,
+                                                                 uint32_t* __restrict__ out_a) {
   extern __shared__ uint32_t sm[];
-  uint32_t* xs0 = sm;                                // [16 m][545]
-  uint32_t* xs1 = sm + kInv512Cols * kInv512Ld;      // [16 m][545]
+  uint32_t* xs0 = sm;                                // [16 m][546]
+  uint32_t* xs1 = sm + kInv512Cols * kInv512Ld;      // [16 m][546]
   const uint32_t y = row0 + blockIdx.y, m0 = blockIdx.x * kInv512Cols;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // phase A: C^[p][y][m0 .. m0 + 15] of both limbs -> xs[m][pad(p)] (64-byte rows, 4 rows per warp access)
+  // phase A: C^[p][y][m0 .. m0 + 15] of both limbs -> xs[m][pad(p)]; one warp access = 2 rows of 64 B
   {
-    const uint32_t mq = lane & 3, ps = lane >> 2;
-#pragma unroll 4
-    for (uint32_t p0 = warp * 8; p0 < 512; p0 += 64) {
-      const uint32_t p = p0 + ps;
-      const size_t g = ((size_t)p * n_out + y) * d + m0 + 4 * mq;
-      const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(c0 + g));
-      const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(c1 + g));
-      const uint32_t o = (4 * mq) * kInv512Ld + pad16(p);
-      xs0[o] = v0.x; xs0[o + kInv512Ld] = v0.y; xs0[o + 2 * kInv512Ld] = v0.z; xs0[o + 3 * kInv512Ld] = v0.w;
-      xs1[o] = v1.x; xs1[o + kInv512Ld] = v1.y; xs1[o + 2 * kInv512Ld] = v1.z; xs1[o + 3 * kInv512Ld] = v1.w;
+    const uint32_t m = lane & 15;
+    const size_t stride = (size_t)16 * n_out * d;    // 16 rows p
+    const uint32_t p_first = warp * 2 + (lane >> 4);
+    const uint32_t* g0 = c0 + ((size_t)p_first * n_out + y) * d + m0 + m;
+    const uint32_t* g1 = c1 + ((size_t)p_first * n_out + y) * d + m0 + m;
+#pragma unroll 8
+    for (uint32_t it = 0; it < 32; ++it) {
+      const uint32_t p = p_first + 16 * it;
+      const uint32_t v0 = __ldg(g0 + it * stride), v1 = __ldg(g1 + it * stride);
+      xs0[m * kInv512Ld + pad16(p)] = v0;
+      xs1[m * kInv512Ld + pad16(p)] = v1;
     }
   }
   __syncthreads();
   const uint32_t q0 = cst.q[0], q1 = cst.q[1];
   for (uint32_t m = warp; m < kInv512Cols; m += 8) {
-    uint32_t x1[16], x0[16];
-    inv512_column(xs1 + m * kInv512Ld, cst.iv[1], q1, lane, x1);
-    inv512_column(xs0 + m * kInv512Ld, cst.iv[0], q0, lane, x0);
+    const Inv512Limb L[2] = {{xs0 + m * kInv512Ld, cst.r2[0], q0}, {xs1 + m * kInv512Ld, cst.r2[1], q1}};
+    uint32_t x[2][16];
+    inv512_pair(L, cst, lane, x);
     if (lane < 16) {
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         uint32_t t;
-        if (x1[e] > (q1 >> 1)) t = csub(x0[e] + (q1 - x1[e]), q0);
-        else t = sub_mod(x0[e], x1[e], q0);
+        if (x[1][e] > (q1 >> 1)) t = csub(x[0][e] + (q1 - x[1][e]), q0);
+        else t = sub_mod(x[0][e], x[1][e], q0);
         xs1[m * kInv512Ld + lane + 16 * e] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);  // u = lane + 16 e
       }
     }
@@ -345,7 +387,8 @@ __global__ void __launch_bounds__(256) spec_inverse512_kernel(const uint32_t* __
 // ---------------------------------------------------------------- S3: per-frequency modular GEMM (tcgen05)
 constexpr int kSpecBN = 32;   // blocks m per tile
 constexpr int kSpecBK = 64;   // K bytes per stage
-constexpr int kSpecEpiWarps = 8;
+constexpr int kSpecEpiWarps = 16;
+constexpr int kSpecEpiCols = kSpecBN / (kSpecEpiWarps / 4);  // columns per epilogue thread
 constexpr int kSpecThreads = 64 + 32 * kSpecEpiWarps;
 
 // UMMA smem descriptor, K-major, 64-byte swizzle: rows of 64 B, 8-row atoms (SBO = 512 B)
@@ -509,10 +552,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
       }
     }
   } else {
-    // ======================= epilogue (both CTAs, 8 warps) =======================
+    // ======================= epilogue (both CTAs, 16 warps) =======================
     const uint32_t ew = warp - 2;
     const uint32_t quarter = warp & 3;
-    const uint32_t half = ew / 4;                      // columns [16 half, 16 half + 16)
+    const uint32_t part = ew / 4;                      // columns [kSpecEpiCols part, .. + kSpecEpiCols)
     const uint32_t lane_addr = (quarter * 32) << 16;
     const uint32_t tmem_empty_remote = mapa_rank(&tmem_empty[0], 0);
     const uint32_t q = args.q;
@@ -524,20 +567,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
       mbar_wait(&tmem_full[buf], (iter >> 1) & 1);
       tc_fence_after();
       const int y = y0 + (int)rank * 128 + (int)(quarter * 32 + lane);
-      uint32_t acc[C::S][16];
-      const uint32_t col = tmem_base + lane_addr + buf * C::kBuf + half * 16;
+      uint32_t acc[C::S][kSpecEpiCols];
+      const uint32_t col = tmem_base + lane_addr + buf * C::kBuf + part * kSpecEpiCols;
 #pragma unroll
-      for (int s = 0; s < C::S; ++s) {
-        tmem_ld_x8(col + s * kSpecBN, acc[s]);
-        tmem_ld_x8(col + s * kSpecBN + 8, acc[s] + 8);
-      }
+      for (int s = 0; s < C::S; ++s)
+#pragma unroll
+        for (int c8 = 0; c8 < kSpecEpiCols / 8; ++c8) tmem_ld_x8(col + s * kSpecBN + 8 * c8, acc[s] + 8 * c8);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tmem_empty_remote + buf * 8);  // accumulators drained
-      uint32_t res[16];
+      uint32_t res[kSpecEpiCols];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
+      for (int e = 0; e < kSpecEpiCols; ++e) {
         int64_t v = 0;
 #pragma unroll
         for (int s = 0; s < C::S; ++s) v += (int64_t)(int32_t)acc[s][e] * (int64_t)args.pw[s];
@@ -546,9 +588,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
         res[e] = csub((uint32_t)(u - qh * q), q);
       }
       if (y < args.row0 + args.n_rows) {
-        uint4* dst = reinterpret_cast<uint4*>(args.out + ((size_t)f * args.n_out + y) * args.d + m0 + half * 16);
+        uint4* dst = reinterpret_cast<uint4*>(args.out + ((size_t)f * args.n_out + y) * args.d + m0 +
+                                              part * kSpecEpiCols);
 #pragma unroll
-        for (int v4 = 0; v4 < 4; ++v4) dst[v4] = make_uint4(res[4 * v4], res[4 * v4 + 1], res[4 * v4 + 2], res[4 * v4 + 3]);
+        for (int v4 = 0; v4 < kSpecEpiCols / 4; ++v4)
+          dst[v4] = make_uint4(res[4 * v4], res[4 * v4 + 1], res[4 * v4 + 2], res[4 * v4 + 3]);
       }
     }
   }

@@ -66,6 +66,20 @@ class MlwePcmmPlan:
             self._workspace = torch.empty(need, dtype=torch.int8, device=device)
         return self._workspace
 
+    STAGES = ("decompose", "spectral_data", "modgemm", "spectral_gemm_q0", "spectral_gemm_q1", "spectral_inverse")
+
+    def profile(self, enable: bool = True) -> None:
+        """Record per-stage CUDA events on every launch of this plan (he_pcmm_profile)."""
+        native.call("he_pcmm_profile", self._handle, 1 if enable else 0)
+
+    def profile_read(self) -> dict:
+        """{stage: (summed device ms, launches)} since profile() / the last read (synchronizes)."""
+        n = len(self.STAGES)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_uint32 * n)()
+        native.call("he_pcmm_profile_read", self._handle, ms, cnt, n)
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(self.STAGES) if cnt[i]}
+
     def __del__(self):
         try:
             if self._handle:
@@ -229,6 +243,19 @@ def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_hos
     ctx.ledger.rescales += plan.n_out // k
     ctx.ledger.observe_level(X.level - 1)
     return MlweBlocks(out_b_host, out_a_host, level=X.level - 1, n_rows=plan.n_out)
+
+
+def spectral_gemm_ops(params, n_out: int, n_in: int, limb: int) -> int:
+    """Algorithmic int8 tensor-core ops of one K7 S3 launch (limb ``limb``): per frequency f < 2k a
+    (n_out x R) x (R x d) product, R = n_in / k, every digit of G^ meeting every digit of A^."""
+    D = params.ct_digits(limb)
+    return 2 * 2 * params.mlwe_rank * n_out * (n_in // params.mlwe_rank) * params.mlwe_degree * D * D
+
+
+def spectral_inverse_bytes(params, n_out: int) -> int:
+    """Algorithmic HBM bytes of one K7 S4 launch: read C^ of both limbs (2k x n_out x d u32 each),
+    write the a' words (n_out x N u32)."""
+    return 2 * 2 * params.mlwe_rank * n_out * params.mlwe_degree * 4 + n_out * params.N * 4
 
 
 def pcmm_ops(params, n_out: int, n_in: int, d_w: int) -> int:

@@ -75,7 +75,7 @@ def test_a04_metric_shape_full_output_exact():
     from test_gpu_pcmm import test_selection_identity_full_output_metric_shape
 
     t0 = time.perf_counter()
-    test_selection_identity_full_output_metric_shape()
+    test_selection_identity_full_output_metric_shape("spectral")
     check_budget(t0, 120)
 
 
@@ -84,7 +84,7 @@ def test_a05_streamed_equals_device():
     from test_gpu_pcmm import test_streamed_to_host_matches_device_output
 
     t0 = time.perf_counter()
-    test_streamed_to_host_matches_device_output()
+    test_streamed_to_host_matches_device_output("spectral")
     check_budget(t0, 60)
 
 

@@ -1,5 +1,9 @@
 """Parity of the CUDA path (through the C ABI) with the CPU oracle, on the GPU.
 
+Both a'-column algorithms are covered: "spectral" (K7, the default: blockwise NTT
+correlations + per-frequency tcgen05 GEMMs) and "direct" (K1 over all GEMM columns); they
+must produce the same words, and each is checked against the oracle.
+
 Bar: bit-exact on every integer ciphertext word (encryption, weight digits, PCMM output)
 at toy size (all rows x all columns) and at Llama sizes (sampled rows x columns, plus the
 exact selection-matrix identity over the FULL output); decrypted outputs within the
@@ -64,14 +68,18 @@ def test_fixture_parity_baseline_config1():
     np.testing.assert_allclose(dec.T, gt["hesim_bsgs"], atol=2 ** -16)
 
 
+ALGOS = ["spectral", "direct"]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("n_out,n_in", [(16, 16), (48, 32), (256, 384), (128, 1024)])
-def test_toy_all_words_bit_exact(n_out, n_in):
+def test_toy_all_words_bit_exact(n_out, n_in, algo):
     P = HeParams.toy()
     ctx, sk, A, W, X = setup(P, n_out, n_in)
     s = O.keygen(P, 7)
     ct = O.encrypt(P, 11, s, O.encode_acts(P, A))
     assert np.array_equal(u32(X.data), ct)
-    plan = make_mlwe_pcmm_plan(ctx, W)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
     Wt = O.encode_weights(P, W)
     dg = plan.digits.cpu().numpy().astype(np.int64)
     assert np.array_equal(sum(dg[i] * 256 ** i for i in range(plan.d_w)), Wt)
@@ -83,22 +91,24 @@ def test_toy_all_words_bit_exact(n_out, n_in):
     assert err < 2 ** -14, err
 
 
-def test_toy_wide_weights_use_more_digits():
+@pytest.mark.parametrize("algo", ALGOS)
+def test_toy_wide_weights_use_more_digits(algo):
     P = HeParams.toy()
     ctx, sk, A, W, X = setup(P, 64, 64, scale=1.0)      # |W| up to 1 -> 3 weight digits
-    plan = make_mlwe_pcmm_plan(ctx, W)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
     assert plan.d_w == 3
-    plan4 = make_mlwe_pcmm_plan(ctx, W, d_w=4)
+    plan4 = make_mlwe_pcmm_plan(ctx, W, d_w=4, algo=algo)
     ref = O.pcmm(P, O.encode_weights(P, W), u32(X.data))
     for pl in (plan, plan4):
         Y = pcmm_mlwe(ctx, pl, X)
         assert np.array_equal(gather(P, Y, range(64), range(P.width)), ref)
 
 
-def test_wide_params_four_digit_limbs():
+@pytest.mark.parametrize("algo", ALGOS)
+def test_wide_params_four_digit_limbs(algo):
     P = HeParams.wide(mlwe_degree=32, mlwe_rank=16, moduli=(1073738753, 1073732609), rhombus_degree=128)
     ctx, sk, A, W, X = setup(P, 32, 48)
-    plan = make_mlwe_pcmm_plan(ctx, W)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
     assert P.ct_digits(1) == 4
     Y = pcmm_mlwe(ctx, plan, X)
     ref = O.pcmm(P, O.encode_weights(P, W), O.encrypt(P, 11, O.keygen(P, 7), O.encode_acts(P, A)))
@@ -115,11 +125,12 @@ def _llama_sample(P, n_out):
 LLAMA_SHAPES = [(4096, 4096), (4096, 11008), (11008, 4096), (14336, 4096), (4096, 14336)]
 
 
+@pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("n_out,n_in", LLAMA_SHAPES)
-def test_llama_sampled_words_bit_exact_and_precision(n_out, n_in):
+def test_llama_sampled_words_bit_exact_and_precision(n_out, n_in, algo):
     P = HeParams.llama()
     ctx, sk, A, W, X = setup(P, n_out, n_in)
-    plan = make_mlwe_pcmm_plan(ctx, W)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
     assert plan.d_w == 2
     Y = pcmm_mlwe(ctx, plan, X)
     rows, cols = _llama_sample(P, n_out)
@@ -131,7 +142,26 @@ def test_llama_sampled_words_bit_exact_and_precision(n_out, n_in):
     assert err < 2 ** -12, err          # paper target 12 bits; measured ~14.5 bits
 
 
-def _selection_identity(n_out, n_in, seed=9):
+@pytest.mark.parametrize("n_out,n_in", LLAMA_SHAPES)
+def test_spectral_equals_direct_every_word(n_out, n_in):
+    """The two a'-column algorithms agree on ALL n_out x 65 792 output words (random weights);
+    the direct K1 words are themselves oracle-pinned on samples and by the selection identity."""
+    import torch
+
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, n_out, n_in, seed=3)
+    ys = {}
+    for algo in ALGOS:
+        plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
+        Y = pcmm_mlwe(ctx, plan, X)
+        ys[algo] = (Y.out_a.clone(), Y.out_b.clone())
+        del plan, Y
+        torch.cuda.empty_cache()
+    assert torch.equal(ys["spectral"][0], ys["direct"][0])
+    assert torch.equal(ys["spectral"][1], ys["direct"][1])
+
+
+def _selection_identity(n_out, n_in, seed=9, algo="spectral"):
     """W a 0/1 selection matrix (W~ = q1 at (y, pi(y))): the rescaled output row y equals, word
     for word, the limb-0 MLWE decomposition of input row pi(y) -- checked over ALL n_out x 65 792
     output words, a size-independent exact property."""
@@ -151,7 +181,7 @@ def _selection_identity(n_out, n_in, seed=9):
     pcol = block_permutation(n_in, P.mlwe_rank)
     W = np.zeros((n_out, n_in))
     W[prow, pcol[pi]] = 1.0                   # GEMM-order W~[y][pi(y)] = q1
-    plan = make_mlwe_pcmm_plan(ctx, W)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
     Y = pcmm_mlwe(ctx, plan, X)
     torch.cuda.synchronize()
     ct = X.data
@@ -179,8 +209,9 @@ def _selection_identity(n_out, n_in, seed=9):
     assert torch.equal(got_b, bb)
 
 
-def test_selection_identity_full_output_metric_shape():
-    _selection_identity(4096, 11008)
+@pytest.mark.parametrize("algo", ALGOS)
+def test_selection_identity_full_output_metric_shape(algo):
+    _selection_identity(4096, 11008, algo=algo)
 
 
 @pytest.mark.parametrize("n_out,n_in", [s for s in LLAMA_SHAPES if s != (4096, 11008)])
@@ -188,11 +219,12 @@ def test_selection_identity_full_output_all_llama_shapes(n_out, n_in):
     _selection_identity(n_out, n_in)
 
 
-def test_wide_weights_at_llama_size_use_32_column_tiles():
+@pytest.mark.parametrize("algo", ALGOS)
+def test_wide_weights_at_llama_size_use_32_column_tiles(algo):
     """|W| up to 1 -> d_w = 3 at q1 ~ 2^20: the 256x32 CTA-pair instance, sampled parity."""
     P = HeParams.llama()
     ctx, sk, A, W, X = setup(P, 1024, 4096, scale=1.0)
-    plan = make_mlwe_pcmm_plan(ctx, W)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
     assert plan.d_w == 3
     Y = pcmm_mlwe(ctx, plan, X)
     rows, cols = _llama_sample(P, 1024)
@@ -241,15 +273,16 @@ def test_ntt_roundtrip_and_product():
             assert np.array_equal(u32(t), a)
 
 
-def test_streamed_to_host_matches_device_output():
-    """pcmm_mlwe_to_host (row chunks of K1 streamed to pinned host memory) == pcmm_mlwe."""
+@pytest.mark.parametrize("algo", ALGOS)
+def test_streamed_to_host_matches_device_output(algo):
+    """pcmm_mlwe_to_host (row chunks streamed to pinned host memory) == pcmm_mlwe."""
     import torch
 
     from paper_2601_18511_b200 import pcmm_mlwe_to_host
 
     P = HeParams.llama()
     ctx, sk, A, W, X = setup(P, 1280, 512)
-    plan = make_mlwe_pcmm_plan(ctx, W)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
     Y = pcmm_mlwe(ctx, plan, X)
     hb = torch.empty(tuple(Y.out_b.shape), dtype=torch.int32, pin_memory=True)
     ha = torch.empty(tuple(Y.out_a.shape), dtype=torch.int32, pin_memory=True)
