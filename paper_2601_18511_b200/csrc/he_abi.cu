@@ -80,6 +80,22 @@ static he_status make_map_sw64(CUtensorMap* m, const void* base, uint64_t inner,
   return HE_OK;
 }
 
+// 3-D u32 tensor {inner, rows, planes}, box {box_inner, box_rows, 1}, 128-B swizzle (box_inner * 4 == 128)
+static he_status make_map_u32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t planes,
+                              uint32_t box_inner, uint32_t box_rows) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {inner, rows, planes};
+  cuuint64_t strides[2] = {inner * 4, inner * rows * 4};
+  cuuint32_t box[3] = {box_inner, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled (u32) failed (%d)", (int)r);
+  return HE_OK;
+}
+
 // 4-D int8 tensor with explicit strides (bytes), box {128, box_rows, 1, 1}, 128-B swizzle
 static he_status make_map4(CUtensorMap* m, const void* base, const uint64_t dims_in[4], const uint64_t strides_in[3],
                            uint32_t box_rows) {
@@ -481,10 +497,13 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     a.L = (int)p->L;
     a.d = (int)p->ctx->R.d;
     a.r_pad = (int)p->r_pad;
-    a.q = p->epi.q[L];
-    a.mu = p->epi.mu[L];
-    a.off64 = p->epi.off64[L];
-    for (int sft = 0; sft < 8; ++sft) a.pw[sft] = (int32_t)p->epi.pw[L][sft];
+    const uint32_t q = p->epi.q[L];
+    a.q = q;
+    uint32_t inv = 1;  // q^-1 mod 2^32 by Newton iteration
+    for (int it = 0; it < 5; ++it) inv *= 2u - q * inv;
+    a.qninv = 0u - inv;
+    a.off64 = (uint64_t)q << 29;
+    for (int sft = 0; sft < 8; ++sft) a.pw[sft] = (int32_t)powmod_h(2, 8ull * sft + 32, q);
     a.out = C[L];
     const int8_t* A = base + (L ? w.a1 : w.a0);
     if (simple) {
@@ -495,8 +514,11 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     CUtensorMap tmB;
     he_status s = make_map_sw64(&tmB, A, p->r_pad, p->ctx->R.d, (uint64_t)p->L * p->dsp[L], 16);
     if (s) return s;
+    CUtensorMap tmC;  // C^ limb L: u32 {d, n_out, 2k}, box {32, 128, 1}, 128-B swizzle (S3's TMA store)
+    s = make_map_u32(&tmC, C[L], p->ctx->R.d, p->n_out, p->L, 32, 128);
+    if (s) return s;
     p->prof_begin(3 + L, st);
-    HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, a, p->ctx->sm_count, st), "spectral gemm");
+    HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, tmC, a, p->ctx->sm_count, st), "spectral gemm");
     p->prof_end(3 + L, st);
   }
   SpecInvConst c;
@@ -640,11 +662,12 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
   if (c->R.d % 32) return fail(HE_EINVAL, "spectral path needs mlwe_degree %% 32 == 0");
   uint32_t L, r_pad, dsp[2];
   spec_dims(p, L, r_pad, dsp);
-  // exactness of S3: int32 shift accumulators R * D * 2^14 < 2^31; int64 sum S * R * D * 2^14 * q < 2^62
+  // exactness of S3: int32 shift accumulators R * D * 2^14 < 2^31; the Montgomery recombination needs
+  // |sum_s acc_s pw_s| < q 2^29 (the offset), i.e. S * R * D * 2^14 < 2^29
   const uint64_t R = p->n_in / c->R.k;
   for (int i = 0; i < 2; ++i) {
     if (R * dsp[i] * 16384ull >= (1ull << 31)) return fail(HE_EINVAL, "n_in too large for the spectral accumulators");
-    if ((unsigned __int128)(2 * dsp[i] - 1) * R * dsp[i] * 16384ull * c->R.q[i] >= ((unsigned __int128)1 << 62))
+    if ((uint64_t)(2 * dsp[i] - 1) * R * dsp[i] * 16384ull >= (1ull << 29))
       return fail(HE_EINVAL, "n_in too large for the spectral recombination");
   }
   cudaStream_t st = (cudaStream_t)stream;

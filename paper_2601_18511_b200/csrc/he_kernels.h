@@ -74,8 +74,9 @@ struct SpecGemmArgs {
   int n_rows, row0, n_out;  // row range [row0, row0 + n_rows) of n_out
   int L, d, r_pad;
   uint32_t q;
-  uint64_t mu, off64;       // Barrett floor(2^64/q); q * ceil(2^62/q)
-  int32_t pw[8];            // 2^(8 s) mod q
+  uint32_t qninv;           // -q^-1 mod 2^32 (Montgomery)
+  uint64_t off64;           // q * 2^29: makes the signed shift sum non-negative
+  int32_t pw[8];            // 2^(8 s + 32) mod q
   uint32_t* out;            // C^ [L][n_out][d]
 };
 struct SpecInvConst {
@@ -90,8 +91,8 @@ cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out
                                 const SpecTable& t, int D, uint32_t r_pad, int8_t* out, cudaStream_t s);
 cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, uint32_t limb, const SpecTable& t,
                              int D, uint32_t r_pad, int8_t* out, cudaStream_t s);
-cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const SpecGemmArgs& a, int sm_count,
-                             cudaStream_t s);
+cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                             const SpecGemmArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_spec_gemm_simple(int D, const int8_t* G, const int8_t* A, const SpecGemmArgs& a, cudaStream_t s);
 cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const uint32_t* c1, uint32_t n_out,
                                 uint32_t row0, uint32_t rows, uint32_t L, const SpecInvConst& cst, uint32_t* out_a,

@@ -391,6 +391,19 @@ constexpr int kSpecEpiWarps = 16;
 constexpr int kSpecEpiCols = kSpecBN / (kSpecEpiWarps / 4);  // columns per epilogue thread
 constexpr int kSpecThreads = 64 + 32 * kSpecEpiWarps;
 
+HE_D void named_bar_sync(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+HE_D void tma_store_3d(const void* map, const void* src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+HE_D void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+HE_D void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+HE_D void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // UMMA smem descriptor, K-major, 64-byte swizzle: rows of 64 B, 8-row atoms (SBO = 512 B)
 HE_D uint64_t desc_sw64(uint32_t saddr) {
   uint64_t d = 0;
@@ -409,9 +422,10 @@ struct SpecCfg {
   static constexpr int kABytes = D * 128 * kSpecBK;         // per CTA per stage
   static constexpr int kBBytes = D * kChunk * kSpecBK;      // per CTA per stage
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr int kOutBytes = 128 * kSpecBN * 4;       // one staged C^ tile (128 rows x 32 u32)
+  static constexpr int kStages = (176 * 1024) / kStageBytes > 8 ? 8 : (176 * 1024) / kStageBytes;
   static constexpr int kZeroBytes = 8192;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kZeroBytes + 1024 + 256;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 2 * kOutBytes + kZeroBytes + 1024 + 256;
   static constexpr int kBuf = 256;                          // TMEM column stride of the two buffers
   static_assert(S * kSpecBN <= kBuf, "shift accumulators exceed one TMEM buffer");
   static_assert(kStages >= 2, "not enough shared memory");
@@ -420,14 +434,15 @@ struct SpecCfg {
 template <int D>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
     spec_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const SpecGemmArgs args) {
+                     const __grid_constant__ CUtensorMap tmC, const SpecGemmArgs args) {
   using C = SpecCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint8_t* sZero = sB + C::kStages * C::kBBytes;
+  uint8_t* sOut = sB + C::kStages * C::kBBytes;       // [2][128 rows][128 B], 128-B swizzled (TMA store)
+  uint8_t* sZero = sOut + 2 * C::kOutBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sZero + C::kZeroBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tmem_full = empty + C::kStages;   // [2]
@@ -469,12 +484,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // m_tiles is a power of two; rest / y_tiles by a 32-bit reciprocal (exact for rest, y_tiles < 2^16)
+  const uint32_t m_shift = (uint32_t)__ffs(m_tiles) - 1;
+  const uint32_t y_magic = (uint32_t)((0xFFFFFFFFull + y_tiles) / y_tiles);
   auto tile_coords = [&](int tile, int& f, int& y0, int& m0) {
-    const int mt = tile % m_tiles;
-    const int rest = tile / m_tiles;
-    y0 = args.row0 + (rest % y_tiles) * 256;
-    f = rest / y_tiles;
-    m0 = mt * kSpecBN;
+    const uint32_t rest = (uint32_t)tile >> m_shift;
+    const uint32_t fq = y_tiles == 1 ? rest : __umulhi(rest, y_magic);
+    f = (int)fq;
+    y0 = args.row0 + (int)(rest - fq * (uint32_t)y_tiles) * 256;
+    m0 = (tile & (m_tiles - 1)) * kSpecBN;
   };
 
   if (warp == 0) {
@@ -577,24 +595,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tmem_empty_remote + buf * 8);  // accumulators drained
+      // sum_s acc_s 2^(8 s) mod q by one Montgomery reduction: v = off + sum_s acc_s (2^(8s+32) mod q)
+      // (off = q 2^29 > |sum| keeps v in [0, q 2^32)), then (v + ((v mod 2^32) (-q^-1) mod 2^32) q) / 2^32
       uint32_t res[kSpecEpiCols];
 #pragma unroll
       for (int e = 0; e < kSpecEpiCols; ++e) {
-        int64_t v = 0;
+        int64_t v = (int64_t)args.off64;
 #pragma unroll
         for (int s = 0; s < C::S; ++s) v += (int64_t)(int32_t)acc[s][e] * (int64_t)args.pw[s];
-        const uint64_t u = (uint64_t)v + args.off64;
-        const uint64_t qh = __umul64hi(u, args.mu);
-        res[e] = csub((uint32_t)(u - qh * q), q);
+        const uint32_t m = (uint32_t)v * args.qninv;
+        const uint32_t t = (uint32_t)(((uint64_t)v + (uint64_t)m * q) >> 32);   // [0, 2q)
+        res[e] = min(t, t - q);
       }
-      if (y < args.row0 + args.n_rows) {
-        uint4* dst = reinterpret_cast<uint4*>(args.out + ((size_t)f * args.n_out + y) * args.d + m0 +
-                                              part * kSpecEpiCols);
+      // stage the 128 x 32 tile in smem (128-B swizzle: 16-B chunk c of row r at c ^ (r & 7)) and
+      // TMA-store it as whole 128-B rows; the buffer of tile iter-2 must have been read out first
+      uint8_t* so = sOut + buf * C::kOutBytes;
+      if (ew == 0 && lane == 0) bulk_wait_read<1>();
+      named_bar_sync(1, 32 * kSpecEpiWarps);
+      const uint32_t r = quarter * 32 + lane;
 #pragma unroll
-        for (int v4 = 0; v4 < kSpecEpiCols / 4; ++v4)
-          dst[v4] = make_uint4(res[4 * v4], res[4 * v4 + 1], res[4 * v4 + 2], res[4 * v4 + 3]);
+      for (int c = 0; c < kSpecEpiCols / 4; ++c) {
+        const uint32_t chunk = (part * (kSpecEpiCols / 4) + c) ^ (r & 7);
+        *reinterpret_cast<uint4*>(so + r * 128 + chunk * 16) =
+            make_uint4(res[4 * c], res[4 * c + 1], res[4 * c + 2], res[4 * c + 3]);
+      }
+      fence_proxy_async();
+      named_bar_sync(1, 32 * kSpecEpiWarps);
+      if (ew == 0 && lane == 0) {
+        tma_store_3d(&tmC, so, m0, y0 + (int)rank * 128, f);
+        bulk_commit();
       }
     }
+    if (ew == 0 && lane == 0) bulk_wait_all();
   }
 
   __syncwarp();
@@ -680,26 +712,26 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
 }
 
 template <int D>
-static cudaError_t launch_spec_gemm_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const SpecGemmArgs& a, int grid,
-                                      cudaStream_t s) {
+static cudaError_t launch_spec_gemm_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                      const SpecGemmArgs& a, int grid, cudaStream_t s) {
   using C = SpecCfg<D>;
   auto kern = spec_gemm_kernel<D>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kSpecThreads, C::kSmemBytes, s>>>(tmA, tmB, a);
+  kern<<<grid, kSpecThreads, C::kSmemBytes, s>>>(tmA, tmB, tmC, a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const SpecGemmArgs& a, int sm_count,
-                             cudaStream_t s) {
+cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                             const SpecGemmArgs& a, int sm_count, cudaStream_t s) {
   const int tiles = (a.d / kSpecBN) * ((a.n_rows + 255) / 256) * a.L;
   const int pairs = sm_count / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
   switch (D) {
-    case 1: return launch_spec_gemm_t<1>(tmA, tmB, a, grid, s);
-    case 2: return launch_spec_gemm_t<2>(tmA, tmB, a, grid, s);
-    case 3: return launch_spec_gemm_t<3>(tmA, tmB, a, grid, s);
-    case 4: return launch_spec_gemm_t<4>(tmA, tmB, a, grid, s);
+    case 1: return launch_spec_gemm_t<1>(tmA, tmB, tmC, a, grid, s);
+    case 2: return launch_spec_gemm_t<2>(tmA, tmB, tmC, a, grid, s);
+    case 3: return launch_spec_gemm_t<3>(tmA, tmB, tmC, a, grid, s);
+    case 4: return launch_spec_gemm_t<4>(tmA, tmB, tmC, a, grid, s);
   }
   return cudaErrorInvalidValue;
 }
