@@ -270,8 +270,8 @@ struct Inv512Limb {
   const uint2* r2;      // round-2 table: stage s at 16 (2^(s-4) - 1), entry [i][l_lo]
   uint32_t q;
 };
-// -> out[l][e] = INTT value u = l_lo + 16 e of limb l (valid on lanes < 16)
-HE_D void inv512_pair(const Inv512Limb (&L)[2], const SpecInvConst& cst, uint32_t lane, uint32_t (&out)[2][16]) {
+// -> out[l][e] = INTT value u = l_lo + 16 (e + 8 l_hi) of limb l, e < 8
+HE_D void inv512_pair(const Inv512Limb (&L)[2], const SpecInvConst& cst, uint32_t lane, uint32_t (&out)[2][8]) {
   uint32_t x[2][16];
 #pragma unroll
   for (int l = 0; l < 2; ++l)
@@ -318,16 +318,19 @@ HE_D void inv512_pair(const Inv512Limb (&L)[2], const SpecInvConst& cst, uint32_
         dit_bf(x[l][e], x[l][e + len], __ldg(L[l].r2 + base + 16 * i + lo), 2 * L[l].q, L[l].q);
     }
   }
-  // stage len = 256: lower lanes keep X + W Y; the upper lanes supply W Y
+  // stage len = 256, pruned to the outputs u < 256 (X + W Y): lanes l and l ^ 16 swap half their elements
+  // so lane (lo, hi) holds the pairs of positions lo + 16 (e + 8 hi), e < 8, and forms those 8 outputs
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
+  for (int e = 0; e < 8; ++e) {
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
       const uint32_t q = L[l].q, q2 = 2 * q;
-      const uint2 w = __ldg(L[l].r2 + 240 + 16 * e + lo);
-      const uint32_t t = x[l][e] * w.x - __umulhi(x[l][e], w.y) * q;  // upper lanes: [0, 2q)
-      const uint32_t tp = __shfl_xor_sync(0xffffffffu, t, 16);
-      uint32_t v = min(x[l][e], x[l][e] - q2) + tp;                  // lower lanes: [0, 4q)
+      const uint32_t send = hi ? x[l][e] : x[l][e + 8];
+      const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 16);
+      const uint32_t X = hi ? recv : x[l][e], Y = hi ? x[l][e + 8] : recv;
+      const uint2 w = __ldg(L[l].r2 + 240 + 16 * (e + 8 * hi) + lo);
+      const uint32_t t = Y * w.x - __umulhi(Y, w.y) * q;  // [0, 2q)
+      uint32_t v = min(X, X - q2) + t;                    // [0, 4q)
       v = min(v, v - q2);
       out[l][e] = min(v, v - q);
     }
@@ -343,35 +346,36 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
   uint32_t* xs1 = sm + kInv512Cols * kInv512Ld;      // [16 m][546]
   const uint32_t y = row0 + blockIdx.y, m0 = blockIdx.x * kInv512Cols;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // phase A: C^[p][y][m0 .. m0 + 15] of both limbs -> xs[m][pad(p)]; one warp access = 2 rows of 64 B
+  // phase A: C^[p][y][m0 .. m0 + 15] of both limbs -> xs[m][pad(p)]; one warp access = 8 rows of 64 B
+  // (16-byte loads; pitch 546 = 2 mod 32 makes the 4 scattered stores per load conflict-free)
   {
-    const uint32_t m = lane & 15;
-    const size_t stride = (size_t)16 * n_out * d;    // 16 rows p
-    const uint32_t p_first = warp * 2 + (lane >> 4);
-    const uint32_t* g0 = c0 + ((size_t)p_first * n_out + y) * d + m0 + m;
-    const uint32_t* g1 = c1 + ((size_t)p_first * n_out + y) * d + m0 + m;
-#pragma unroll 8
-    for (uint32_t it = 0; it < 32; ++it) {
-      const uint32_t p = p_first + 16 * it;
-      const uint32_t v0 = __ldg(g0 + it * stride), v1 = __ldg(g1 + it * stride);
-      xs0[m * kInv512Ld + pad16(p)] = v0;
-      xs1[m * kInv512Ld + pad16(p)] = v1;
+    const uint32_t mq = lane & 3;
+    const size_t stride = (size_t)64 * n_out * d;    // 64 rows p
+    const uint32_t p_first = warp * 8 + (lane >> 2);
+    const size_t g = ((size_t)p_first * n_out + y) * d + m0 + 4 * mq;
+    const uint4* g0 = reinterpret_cast<const uint4*>(c0 + g);
+    const uint4* g1 = reinterpret_cast<const uint4*>(c1 + g);
+#pragma unroll 4
+    for (uint32_t it = 0; it < 8; ++it) {
+      const uint32_t o = 4 * mq * kInv512Ld + pad16(p_first + 64 * it);
+      const uint4 v0 = __ldg(g0 + it * (stride / 4)), v1 = __ldg(g1 + it * (stride / 4));
+      xs0[o] = v0.x; xs0[o + kInv512Ld] = v0.y; xs0[o + 2 * kInv512Ld] = v0.z; xs0[o + 3 * kInv512Ld] = v0.w;
+      xs1[o] = v1.x; xs1[o + kInv512Ld] = v1.y; xs1[o + 2 * kInv512Ld] = v1.z; xs1[o + 3 * kInv512Ld] = v1.w;
     }
   }
   __syncthreads();
   const uint32_t q0 = cst.q[0], q1 = cst.q[1];
   for (uint32_t m = warp; m < kInv512Cols; m += 8) {
     const Inv512Limb L[2] = {{xs0 + m * kInv512Ld, cst.r2[0], q0}, {xs1 + m * kInv512Ld, cst.r2[1], q1}};
-    uint32_t x[2][16];
+    uint32_t x[2][8];
     inv512_pair(L, cst, lane, x);
-    if (lane < 16) {
+    const uint32_t u0 = (lane & 15) + 128 * (lane >> 4);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        uint32_t t;
-        if (x[1][e] > (q1 >> 1)) t = csub(x[0][e] + (q1 - x[1][e]), q0);
-        else t = sub_mod(x[0][e], x[1][e], q0);
-        xs1[m * kInv512Ld + lane + 16 * e] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);  // u = lane + 16 e
-      }
+    for (int e = 0; e < 8; ++e) {
+      uint32_t t;
+      if (x[1][e] > (q1 >> 1)) t = csub(x[0][e] + (q1 - x[1][e]), q0);
+      else t = sub_mod(x[0][e], x[1][e], q0);
+      xs1[m * kInv512Ld + u0 + 16 * e] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);  // u = lo + 16 (e + 8 hi)
     }
   }
   __syncthreads();
