@@ -80,7 +80,7 @@ static he_status make_map_sw64(CUtensorMap* m, const void* base, uint64_t inner,
   return HE_OK;
 }
 
-// 3-D u32 tensor {inner, rows, planes}, box {box_inner, box_rows, 1}, 128-B swizzle (box_inner * 4 == 128)
+// 3-D u32 tensor {inner, rows, planes}, box {box_inner, box_rows, 1}, no swizzle
 static he_status make_map_u32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t planes,
                               uint32_t box_inner, uint32_t box_rows) {
   PFN_encodeTiled_t fn = encode_fn();
@@ -90,7 +90,7 @@ static he_status make_map_u32(CUtensorMap* m, const void* base, uint64_t inner, 
   cuuint32_t box[3] = {box_inner, box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled (u32) failed (%d)", (int)r);
   return HE_OK;
@@ -514,8 +514,8 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     CUtensorMap tmB;
     he_status s = make_map_sw64(&tmB, A, p->r_pad, p->ctx->R.d, (uint64_t)p->L * p->dsp[L], 16);
     if (s) return s;
-    CUtensorMap tmC;  // C^ limb L: u32 {d, n_out, 2k}, box {32, 128, 1}, 128-B swizzle (S3's TMA store)
-    s = make_map_u32(&tmC, C[L], p->ctx->R.d, p->n_out, p->L, 32, 128);
+    CUtensorMap tmC;  // C^ limb L: u32 {d, n_out, 2k}, box {8, 32, 1} (one epilogue warp's TMA store)
+    s = make_map_u32(&tmC, C[L], p->ctx->R.d, p->n_out, p->L, 8, 32);
     if (s) return s;
     p->prof_begin(3 + L, st);
     HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, tmC, a, p->ctx->sm_count, st), "spectral gemm");

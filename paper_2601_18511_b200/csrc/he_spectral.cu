@@ -611,26 +611,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
         const uint32_t t = (uint32_t)(((uint64_t)v + (uint64_t)m * q) >> 32);   // [0, 2q)
         res[e] = min(t, t - q);
       }
-      // stage the 128 x 32 tile in smem (128-B swizzle: 16-B chunk c of row r at c ^ (r & 7)) and
-      // TMA-store it as whole 128-B rows; the buffer of tile iter-2 must have been read out first
-      uint8_t* so = sOut + buf * C::kOutBytes;
-      if (ew == 0 && lane == 0) bulk_wait_read<1>();
-      named_bar_sync(1, 32 * kSpecEpiWarps);
-      const uint32_t r = quarter * 32 + lane;
+      // each warp stages its 32 rows x 8 words (1 KB, double-buffered) and TMA-stores them itself: no
+      // cross-warp barrier; the buffer of tile iter-2 must have been read out by its bulk store first
+      uint8_t* so = sOut + buf * C::kOutBytes + ew * (32 * kSpecEpiCols * 4);
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
 #pragma unroll
-      for (int c = 0; c < kSpecEpiCols / 4; ++c) {
-        const uint32_t chunk = (part * (kSpecEpiCols / 4) + c) ^ (r & 7);
-        *reinterpret_cast<uint4*>(so + r * 128 + chunk * 16) =
+      for (int c = 0; c < kSpecEpiCols / 4; ++c)
+        *reinterpret_cast<uint4*>(so + lane * (kSpecEpiCols * 4) + c * 16) =
             make_uint4(res[4 * c], res[4 * c + 1], res[4 * c + 2], res[4 * c + 3]);
-      }
       fence_proxy_async();
-      named_bar_sync(1, 32 * kSpecEpiWarps);
-      if (ew == 0 && lane == 0) {
-        tma_store_3d(&tmC, so, m0, y0 + (int)rank * 128, f);
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(&tmC, so, m0 + (int)part * kSpecEpiCols, y0 + (int)rank * 128 + (int)quarter * 32, f);
         bulk_commit();
       }
     }
-    if (ew == 0 && lane == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
   }
 
   __syncwarp();
