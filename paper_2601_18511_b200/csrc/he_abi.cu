@@ -425,10 +425,11 @@ static SpecWs spec_ws(const he_pcmm_plan* p) {
   SpecWs w;
   w.bdig = 0;
   w.a0 = al256((uint64_t)(p->d0 + p->d1) * d * p->n_in);
-  w.a1 = w.a0 + al256((uint64_t)p->L * p->dsp[0] * d * p->r_pad);
-  w.c0 = w.a1 + al256((uint64_t)p->L * p->dsp[1] * d * p->r_pad);
-  w.c1 = w.c0 + al256((uint64_t)p->L * p->n_out * d * 4);
-  w.total = w.c1 + al256((uint64_t)p->L * p->n_out * d * 4);
+  const uint64_t nb = p->nbp;
+  w.a1 = w.a0 + al256((uint64_t)p->L * p->dsp[0] * nb * p->r_pad);
+  w.c0 = w.a1 + al256((uint64_t)p->L * p->dsp[1] * nb * p->r_pad);
+  w.c1 = w.c0 + al256((uint64_t)p->L * p->n_out * nb * 4);
+  w.total = w.c1 + al256((uint64_t)p->L * p->n_out * nb * 4);
   return w;
 }
 static uint64_t ws_bytes(const he_pcmm_plan* p) {
@@ -462,8 +463,8 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
     HE_CUDA(cudaMemsetAsync(base + w.a0, 0, w.c0 - w.a0, st), "memset");
     const uint32_t n_ct = p->n_in / p->ctx->R.k;
     for (uint32_t L = 0; L < 2; ++L)
-      HE_CUDA(launch_spec_data(p->ctx->R, ct_in, n_ct, L, p->st[L], (int)p->dsp[L], p->r_pad, base + (L ? w.a1 : w.a0),
-                               st),
+      HE_CUDA(launch_spec_data(p->ctx->R, ct_in, n_ct, L, p->st[L], (int)p->dsp[L], p->r_pad, p->ob, p->nblk, p->nbp,
+                               base + (L ? w.a1 : w.a0), st),
               "spectral data transform");
     p->prof_end(1, st);
     return HE_OK;
@@ -495,7 +496,7 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     a.row0 = (int)row0;
     a.n_out = (int)p->n_out;
     a.L = (int)p->L;
-    a.d = (int)p->ctx->R.d;
+    a.nb = (int)p->nbp;
     a.r_pad = (int)p->r_pad;
     const uint32_t q = p->epi.q[L];
     a.q = q;
@@ -512,10 +513,10 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
       continue;
     }
     CUtensorMap tmB;
-    he_status s = make_map_sw64(&tmB, A, p->r_pad, p->ctx->R.d, (uint64_t)p->L * p->dsp[L], 16);
+    he_status s = make_map_sw64(&tmB, A, p->r_pad, p->nbp, (uint64_t)p->L * p->dsp[L], 16);
     if (s) return s;
     CUtensorMap tmC;  // C^ limb L: u32 {d, n_out, 2k}, box {8, 32, 1} (one epilogue warp's TMA store)
-    s = make_map_u32(&tmC, C[L], p->ctx->R.d, p->n_out, p->L, 8, 32);
+    s = make_map_u32(&tmC, C[L], p->nbp, p->n_out, p->L, 8, 32);
     if (s) return s;
     p->prof_begin(3 + L, st);
     HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, tmC, a, p->ctx->sm_count, st), "spectral gemm");
@@ -526,14 +527,15 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     c.q[L] = p->epi.q[L];
     c.iv[L] = p->st[L].iv;
     c.r2[L] = p->st[L].r2;
-    for (int i = 0; i < 11; ++i) c.r1[L][i] = p->st[L].r1[i];
+    for (int i = 0; i < 26; ++i) c.r1[L][i] = p->st[L].r1[i];
     c.linv[L] = p->st[L].linv;
     c.linvp[L] = p->st[L].linvp;
   }
   c.q1inv = p->epi.q1inv;
   c.q1invp = p->epi.q1invp;
   p->prof_begin(5, st);
-  HE_CUDA(launch_spec_inverse(p->ctx->R, C[0], C[1], p->n_out, row0, rows, p->L, c, out_a, st), "spectral inverse");
+  HE_CUDA(launch_spec_inverse(p->ctx->R, C[0], C[1], p->n_out, row0, rows, p->L, p->nblk, p->nbp, c, out_a, st),
+          "spectral inverse");
   p->prof_end(5, st);
   return HE_OK;
 }
@@ -641,8 +643,15 @@ extern "C" he_status he_pcmm_run(const he_pcmm_plan* p, const uint32_t* ct_in, u
 }
 
 // ---------------------------------------------------------------- K7 spectral a-part
+// transform length: 4k (blocks of 3k outputs: 25% less spectral work than 2k) where the fast inverse
+// exists (k = 256), else 2k; HE_SPEC_L = 512 / 1024 overrides for measurements
+static uint32_t spec_len(const he_context* c) {
+  static const int env = getenv("HE_SPEC_L") ? atoi(getenv("HE_SPEC_L")) : 0;
+  if (c->R.k == 256 && env != 512) return 1024;
+  return 2 * c->R.k;
+}
 static void spec_dims(const he_pcmm_plan* p, uint32_t& L, uint32_t& r_pad, uint32_t dsp[2]) {
-  L = 2 * p->ctx->R.k;
+  L = spec_len(p->ctx);
   r_pad = ((p->n_in / p->ctx->R.k) + 63) / 64 * 64;
   dsp[0] = (uint32_t)digits_for(p->ctx->R.q[0]);
   dsp[1] = (uint32_t)digits_for(p->ctx->R.q[1]);
@@ -687,6 +696,9 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
     if (s) return s;
   }
   p->L = L;
+  p->ob = L - c->R.k;
+  p->nblk = (c->R.N + p->ob - 1) / p->ob;
+  p->nbp = (p->nblk + 31) / 32 * 32;
   p->r_pad = r_pad;
   p->dsp[0] = dsp[0];
   p->dsp[1] = dsp[1];

@@ -64,7 +64,7 @@ struct SpecTable {  // cyclic NTT of length L mod q
   uint2* fw = nullptr;   // (w^j, Shoup) j < L/2
   uint2* iv = nullptr;   // (w^-j, Shoup) j < L/2
   uint2* r2 = nullptr;   // L = 512: per-stage lane tables of the fast inverse (he_spectral.cu)
-  uint2 r1[11] = {};     // L = 512: round-1 twiddles of the fast inverse (host copy, passed as kernel params)
+  uint2 r1[26] = {};     // L = 512 / 1024: round-1 twiddles of the fast inverse (host copy, kernel params)
   uint32_t linv = 0, linvp = 0;
 };
 cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q);
@@ -72,31 +72,32 @@ void spec_table_free(SpecTable& t);
 
 struct SpecGemmArgs {
   int n_rows, row0, n_out;  // row range [row0, row0 + n_rows) of n_out
-  int L, d, r_pad;
+  int L, nb, r_pad;         // transform length, blocks (padded to 32), K bytes
   uint32_t q;
   uint32_t qninv;           // -q^-1 mod 2^32 (Montgomery)
   uint64_t off64;           // q * 2^29: makes the signed shift sum non-negative
   int32_t pw[8];            // 2^(8 s + 32) mod q
-  uint32_t* out;            // C^ [L][n_out][d]
+  uint32_t* out;            // C^ [L][n_out][nb]
 };
 struct SpecInvConst {
   uint32_t q[2];
   const uint2* iv[2];
   const uint2* r2[2];
-  uint2 r1[2][11];          // L = 512 round-1 twiddles w^-(off << (8 - s)), s = 1..3, off = 1 .. 2^s - 1
+  uint2 r1[2][26];          // round-1 twiddles of the fast inverse (spec_table_init)
   uint32_t linv[2], linvp[2];
   uint32_t q1inv, q1invp;
 };
 cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out, uint32_t n_in, uint32_t k,
                                 const SpecTable& t, int D, uint32_t r_pad, int8_t* out, cudaStream_t s);
 cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, uint32_t limb, const SpecTable& t,
-                             int D, uint32_t r_pad, int8_t* out, cudaStream_t s);
+                             int D, uint32_t r_pad, uint32_t ob, uint32_t nblk, uint32_t nbp, int8_t* out,
+                             cudaStream_t s);
 cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                              const SpecGemmArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_spec_gemm_simple(int D, const int8_t* G, const int8_t* A, const SpecGemmArgs& a, cudaStream_t s);
 cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const uint32_t* c1, uint32_t n_out,
-                                uint32_t row0, uint32_t rows, uint32_t L, const SpecInvConst& cst, uint32_t* out_a,
-                                cudaStream_t s);
+                                uint32_t row0, uint32_t rows, uint32_t L, uint32_t nblk, uint32_t nbp,
+                                const SpecInvConst& cst, uint32_t* out_a, cudaStream_t s);
 cudaError_t launch_digitize(const RingDims& R, const uint32_t* ct, uint32_t n_ct, int d0, int d1, uint32_t S,
                             int8_t* out_a, int8_t* out_b, cudaStream_t s);
 cudaError_t launch_weight_maxabs(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in,

@@ -47,7 +47,10 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
   }
   if (!w) return cudaErrorInvalidValue;
   const uint64_t wi = powmod_h(w, q - 2, q);
-  const size_t nr2 = L == 512 ? 496 : 0;  // S4 round-2 table (L = 512 only)
+  // fast-inverse tables (he_spectral.cu S4): L = 512 -> 16 round-2 lanes (stages 4..8), L = 1024 -> 32 lanes
+  // (stages 5..9); entry [i][lane] of stage s = w^-((lane + lanes i) << (log2(L/2) - s)) at lanes (2^(s - s0) - 1)
+  const int lg = ilog2_h(L / 2), s0 = L == 512 ? 4 : 5, lanes = 1 << s0;
+  const size_t nr2 = (L == 512 || L == 1024) ? (size_t)lanes * ((1u << (lg + 1 - s0)) - 1) : 0;
   uint32_t* h = new uint32_t[2 * (size_t)L + 2 * nr2];  // fw pairs [L/2][2], iv pairs [L/2][2], r2 pairs
   uint64_t p = 1, pi = 1;
   for (uint32_t j = 0; j < L / 2; ++j) {
@@ -58,19 +61,19 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
     p = p * w % q;
     pi = pi * wi % q;
   }
-  // r2: stage s = 4..8 at 16 (2^(s-4) - 1): entry [i][lo] = w^-((lo + 16 i) << (8 - s))
-  for (int st = 4; st <= 8 && nr2; ++st) {
-    const int len = 1 << (st - 4), base = 16 * (len - 1);
+  for (int st = s0; st <= lg && nr2; ++st) {
+    const int len = 1 << (st - s0), base = lanes * (len - 1);
     for (int i = 0; i < len; ++i)
-      for (int lo = 0; lo < 16; ++lo) {
-        const uint32_t j = (uint32_t)(lo + 16 * i) << (8 - st);
-        h[2 * (size_t)L + 2 * (base + 16 * i + lo)] = h[L + 2 * j];
-        h[2 * (size_t)L + 2 * (base + 16 * i + lo) + 1] = h[L + 2 * j + 1];
+      for (int lo = 0; lo < lanes; ++lo) {
+        const uint32_t j = (uint32_t)(lo + lanes * i) << (lg - st);
+        h[2 * (size_t)L + 2 * (base + lanes * i + lo)] = h[L + 2 * j];
+        h[2 * (size_t)L + 2 * (base + lanes * i + lo) + 1] = h[L + 2 * j + 1];
       }
   }
-  for (int st = 1; st <= 3 && nr2; ++st)
+  // r1: round-1 (register) stages s = 1 .. s0 - 1, off = 1 .. 2^s - 1 at (2^s - s - 1) + off - 1
+  for (int st = 1; st < s0 && nr2; ++st)
     for (int off = 1; off < (1 << st); ++off) {
-      const uint32_t j = (uint32_t)off << (8 - st);
+      const uint32_t j = (uint32_t)off << (lg - st);
       t.r1[(1 << st) - st - 1 + off - 1] = make_uint2(h[L + 2 * j], h[L + 2 * j + 1]);
     }
   t.linv = (uint32_t)powmod_h(L, q - 2, q);
@@ -167,10 +170,11 @@ __global__ void __launch_bounds__(256) spec_weights_kernel(const int8_t* __restr
 }
 
 // ---------------------------------------------------------------- S2: spectral data windows (per op)
-// A^[f][b][m][r_pad] int8.  One CTA per (block m, chunk of input cts).
+// A^[f][b][blk][r_pad] int8, block blk covering outputs c' = ob blk .. ob blk + ob - 1 (c' = k m - j + k - 1)
+// from the window a_r[ob blk - (k - 1) + u], u < L.  One CTA per (block, chunk of input cts).
 __global__ void __launch_bounds__(256) spec_data_kernel(const uint32_t* __restrict__ ct, uint32_t n_ct, uint32_t limb,
-                                                        uint32_t k, uint32_t d, uint32_t N, uint32_t L, uint32_t q,
-                                                        int D, uint32_t r_pad, const uint2* __restrict__ tw,
+                                                        uint32_t k, uint32_t ob, uint32_t nbp, uint32_t N, uint32_t L,
+                                                        uint32_t q, int D, uint32_t r_pad, const uint2* __restrict__ tw,
                                                         int8_t* __restrict__ out) {
   extern __shared__ uint32_t xs[];  // [kSpecRChunk][L]
   const uint32_t m = blockIdx.x, r0 = blockIdx.y * kSpecRChunk;
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(256) spec_data_kernel(const uint32_t* __restri
   for (int i = threadIdx.x; i < cnt * (int)L; i += blockDim.x) {
     const int b = i / (int)L, u = i % (int)L;
     const uint32_t* a = ct + ((size_t)(r0 + b) * 2 + limb) * 2 * N;
-    int64_t I = (int64_t)k * m - (int64_t)k + 1 + u;
+    int64_t I = (int64_t)ob * m - (int64_t)k + 1 + u;
     uint32_t v;
     if (I < 0) {
       const uint32_t w = a[I + N];
@@ -193,10 +197,10 @@ __global__ void __launch_bounds__(256) spec_data_kernel(const uint32_t* __restri
   }
   __syncthreads();
   cyc_fwd_smem(xs, cnt, (int)L, (int)L, tw, q);
-  const uint64_t plane = (uint64_t)d * r_pad;
+  const uint64_t plane = (uint64_t)nbp * r_pad;
   for (int i = threadIdx.x; i < cnt * (int)L; i += blockDim.x) {
     const int f = i / cnt, b = i % cnt;
-    int8_t* dst = out + ((size_t)f * D * d + m) * r_pad + r0 + b;
+    int8_t* dst = out + ((size_t)f * D * nbp + m) * r_pad + r0 + b;
     write_digits(xs[b * L + f], q, D, dst, plane);
   }
 }
@@ -388,6 +392,128 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
   }
 }
 
+
+// Fast S4 for L = 1024 (k = 256, blocks of ob = 768 outputs = 3 MLWE positions m): one warp per block,
+// limbs in sequence, 32 register-resident elements per lane.
+//   round 1: lane l holds positions 32 l + e: DIT stages len = 1 .. 16 in registers (lane-uniform twiddles);
+//   round 2: lane l holds l + 32 e: stages len = 32 .. 512 in registers (per-stage lane tables); the last
+//            stage forms only the outputs u < 768.
+// 8 blocks per CTA, both limbs in smem (pitch 1060 = 4 mod 8, pad(p) = p + p/32: conflict-free transposing
+// stores and round accesses); a' rows of 3 x 8 positions are written as 96-byte segments.
+constexpr int kInv1kBlocks = 8;
+constexpr int kInv1kLd = 1060;
+HE_D uint32_t pad32(uint32_t p) { return p + (p >> 5); }
+// -> x[e] = INTT value u = lane + 32 e for e < 24, reduced to [0, q)
+HE_D void inv1024_column(uint32_t* col, const uint2 (&r1)[26], const uint2* __restrict__ r2, uint32_t q, uint32_t lane,
+                         uint32_t (&x)[32]) {
+  const uint32_t q2 = 2 * q;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) x[e] = col[33 * lane + e];
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) dit_bf1(x[e], x[e + 1], q2);
+#pragma unroll
+  for (int s = 1; s < 5; ++s) {
+    const int len = 1 << s;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      if (e & len) continue;
+      const int off = e & (len - 1);
+      if (off == 0) dit_bf1(x[e], x[e + len], q2);
+      else dit_bf(x[e], x[e + len], r1[(1 << s) - s - 1 + off - 1], q2, q);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 32; ++e) col[33 * lane + e] = x[e];
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 32; ++e) x[e] = col[lane + 33 * e];
+  __syncwarp();
+#pragma unroll
+  for (int s = 5; s < 9; ++s) {
+    const int len = 1 << (s - 5);
+    const int base = 32 * (len - 1);
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      if (e & len) continue;
+      dit_bf(x[e], x[e + len], __ldg(r2 + base + 32 * (e & (len - 1)) + lane), q2, q);
+    }
+  }
+  // len = 512: pairs (e, e + 16); the upper output u = lane + 32 e + 512 is needed only for e < 8
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const uint2 w = __ldg(r2 + 480 + 32 * e + lane);
+    if (e < 8) {
+      dit_bf(x[e], x[e + 16], w, q2, q);
+    } else {
+      const uint32_t t = x[e + 16] * w.x - __umulhi(x[e + 16], w.y) * q;
+      x[e] = min(x[e], x[e] - q2) + t;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 24; ++e) {
+    const uint32_t v = min(x[e], x[e] - q2);
+    x[e] = min(v, v - q);
+  }
+}
+
+__global__ void __launch_bounds__(256, 3) spec_inverse1024_kernel(const uint32_t* __restrict__ c0,
+                                                                  const uint32_t* __restrict__ c1, uint32_t n_out,
+                                                                  uint32_t row0, uint32_t nbp, uint32_t nblk,
+                                                                  uint32_t d, SpecInvConst cst,
+                                                                  uint32_t* __restrict__ out_a) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* xs0 = sm;                                  // [8 blocks][1060]
+  uint32_t* xs1 = sm + kInv1kBlocks * kInv1kLd;
+  const uint32_t y = row0 + blockIdx.y, b0 = blockIdx.x * kInv1kBlocks;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // phase A: C^[p][y][b0 .. b0 + 7] of both limbs -> xs[b][pad(p)]; one warp access = 16 rows p x 32 B
+  {
+    const uint32_t bq = lane & 1, ps = lane >> 1;
+    const size_t g = ((size_t)(warp * 16 + ps) * n_out + y) * nbp + b0 + 4 * bq;
+    const size_t stride = (size_t)128 * n_out * nbp / 4;   // 128 rows p, in uint4
+    const uint4* g0 = reinterpret_cast<const uint4*>(c0 + g);
+    const uint4* g1 = reinterpret_cast<const uint4*>(c1 + g);
+#pragma unroll 4
+    for (uint32_t it = 0; it < 8; ++it) {
+      const uint32_t o = 4 * bq * kInv1kLd + pad32(warp * 16 + ps + 128 * it);
+      const uint4 v0 = __ldg(g0 + it * stride), v1 = __ldg(g1 + it * stride);
+      xs0[o] = v0.x; xs0[o + kInv1kLd] = v0.y; xs0[o + 2 * kInv1kLd] = v0.z; xs0[o + 3 * kInv1kLd] = v0.w;
+      xs1[o] = v1.x; xs1[o + kInv1kLd] = v1.y; xs1[o + 2 * kInv1kLd] = v1.z; xs1[o + 3 * kInv1kLd] = v1.w;
+    }
+  }
+  __syncthreads();
+  const uint32_t b = warp;
+  if (b0 + b < nblk) {
+    const uint32_t q0 = cst.q[0], q1 = cst.q[1];
+    uint32_t x[32];
+    inv1024_column(xs1 + b * kInv1kLd, cst.r1[1], cst.r2[1], q1, lane, x);
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < 24; ++e) xs1[b * kInv1kLd + lane + 32 * e] = x[e];   // limb-1 words, u = lane + 32 e
+    inv1024_column(xs0 + b * kInv1kLd, cst.r1[0], cst.r2[0], q0, lane, x);
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < 24; ++e) {
+      const uint32_t x1 = xs1[b * kInv1kLd + lane + 32 * e];
+      uint32_t t;
+      if (x1 > (q1 >> 1)) t = csub(x[e] + (q1 - x1), q0);
+      else t = sub_mod(x[e], x1, q0);
+      xs1[b * kInv1kLd + lane + 32 * e] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);
+    }
+  }
+  __syncthreads();
+  // phase C: block b covers c' = 768 (b0 + b) + u  <->  m = 3 (b0 + b) + u / 256, j = 255 - u % 256
+  const uint32_t N = d * 256, mbase = 3 * b0;
+  uint32_t* dst = out_a + (size_t)(y - row0) * N;
+  for (uint32_t i = threadIdx.x; i < 24 * 256; i += 256) {
+    const uint32_t ml = i % 24, j = i / 24;
+    const uint32_t m = mbase + ml;
+    if (m >= d) continue;
+    const uint32_t bl = ml / 3, u = 256 * (ml - 3 * bl) + 255 - j;
+    dst[(size_t)d * j + m] = xs1[bl * kInv1kLd + u];
+  }
+}
+
 // ---------------------------------------------------------------- S3: per-frequency modular GEMM (tcgen05)
 constexpr int kSpecBN = 32;   // blocks m per tile
 constexpr int kSpecBK = 64;   // K bytes per stage
@@ -458,7 +584,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int m_tiles = args.d / kSpecBN;
+  const int m_tiles = args.nb / kSpecBN;
   const int y_tiles = (args.n_rows + 255) / 256;
   const int num_tiles = m_tiles * y_tiles * args.L;
   const int num_kb = args.r_pad / kSpecBK;
@@ -488,15 +614,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // m_tiles is a power of two; rest / y_tiles by a 32-bit reciprocal (exact for rest, y_tiles < 2^16)
-  const uint32_t m_shift = (uint32_t)__ffs(m_tiles) - 1;
+  // tile -> (f, y tile, m tile), m fastest; divisions by 32-bit reciprocals (exact for operands < 2^16)
+  const uint32_t m_magic = (uint32_t)((0xFFFFFFFFull + m_tiles) / m_tiles);
   const uint32_t y_magic = (uint32_t)((0xFFFFFFFFull + y_tiles) / y_tiles);
   auto tile_coords = [&](int tile, int& f, int& y0, int& m0) {
-    const uint32_t rest = (uint32_t)tile >> m_shift;
+    const uint32_t rest = m_tiles == 1 ? (uint32_t)tile : __umulhi((uint32_t)tile, m_magic);
     const uint32_t fq = y_tiles == 1 ? rest : __umulhi(rest, y_magic);
     f = (int)fq;
     y0 = args.row0 + (int)(rest - fq * (uint32_t)y_tiles) * 256;
-    m0 = (tile & (m_tiles - 1)) * kSpecBN;
+    m0 = (int)((uint32_t)tile - rest * (uint32_t)m_tiles) * kSpecBN;
   };
 
   if (warp == 0) {
@@ -644,7 +770,7 @@ __global__ void spec_gemm_simple_kernel(const int8_t* __restrict__ G, const int8
                                         int D) {
   const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t yy = blockIdx.y, f = blockIdx.z;
-  if (m >= (uint32_t)args.d) return;
+  if (m >= (uint32_t)args.nb) return;
   const uint32_t y = args.row0 + yy;
   const uint32_t q = args.q;
   uint64_t accq = 0;
@@ -652,14 +778,14 @@ __global__ void spec_gemm_simple_kernel(const int8_t* __restrict__ G, const int8
     int64_t gv = 0, av = 0;
     for (int a = D - 1; a >= 0; --a) {
       gv = gv * 256 + G[(((size_t)f * D + a) * args.n_out + y) * args.r_pad + r];
-      av = av * 256 + A[(((size_t)f * D + a) * args.d + m) * args.r_pad + r];
+      av = av * 256 + A[(((size_t)f * D + a) * args.nb + m) * args.r_pad + r];
     }
     int64_t gm = gv % (int64_t)q, am = av % (int64_t)q;
     if (gm < 0) gm += q;
     if (am < 0) am += q;
     accq = (accq + (uint64_t)gm * (uint64_t)am) % q;
   }
-  args.out[((size_t)f * args.n_out + y) * args.d + m] = (uint32_t)accq;
+  args.out[((size_t)f * args.n_out + y) * args.nb + m] = (uint32_t)accq;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -678,20 +804,30 @@ cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out
 }
 
 cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, uint32_t limb, const SpecTable& t,
-                             int D, uint32_t r_pad, int8_t* out, cudaStream_t s) {
-  dim3 grid(Rg.d, (n_ct + kSpecRChunk - 1) / kSpecRChunk);
+                             int D, uint32_t r_pad, uint32_t ob, uint32_t nblk, uint32_t nbp, int8_t* out,
+                             cudaStream_t s) {
+  dim3 grid(nblk, (n_ct + kSpecRChunk - 1) / kSpecRChunk);
   const size_t smem = (size_t)kSpecRChunk * t.L * sizeof(uint32_t);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(spec_data_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  spec_data_kernel<<<grid, 256, smem, s>>>(ct, n_ct, limb, Rg.k, Rg.d, Rg.N, t.L, t.q, D, r_pad, t.fw, out);
+  spec_data_kernel<<<grid, 256, smem, s>>>(ct, n_ct, limb, Rg.k, ob, nbp, Rg.N, t.L, t.q, D, r_pad, t.fw, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const uint32_t* c1, uint32_t n_out,
-                                uint32_t row0, uint32_t rows, uint32_t L, const SpecInvConst& cst, uint32_t* out_a,
-                                cudaStream_t s) {
+                                uint32_t row0, uint32_t rows, uint32_t L, uint32_t nblk, uint32_t nbp,
+                                const SpecInvConst& cst, uint32_t* out_a, cudaStream_t s) {
+  if (L == 1024) {
+    if (Rg.k != 256) return cudaErrorInvalidValue;
+    dim3 grid((nblk + kInv1kBlocks - 1) / kInv1kBlocks, rows);
+    const size_t smem = (size_t)2 * kInv1kBlocks * kInv1kLd * sizeof(uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(spec_inverse1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    spec_inverse1024_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, nbp, nblk, Rg.d, cst, out_a);
+    return cudaGetLastError();
+  }
   static const bool generic = getenv("HE_SPEC_INV_GENERIC") != nullptr;  // debug: the simple S4
   if (L == 512 && Rg.k == 256 && Rg.d % kInv512Cols == 0 && !generic) {
     dim3 grid(Rg.d / kInv512Cols, rows);
@@ -725,7 +861,7 @@ static cudaError_t launch_spec_gemm_t(const CUtensorMap& tmA, const CUtensorMap&
 
 cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                              const SpecGemmArgs& a, int sm_count, cudaStream_t s) {
-  const int tiles = (a.d / kSpecBN) * ((a.n_rows + 255) / 256) * a.L;
+  const int tiles = (a.nb / kSpecBN) * ((a.n_rows + 255) / 256) * a.L;
   const int pairs = sm_count / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
   switch (D) {
@@ -738,7 +874,7 @@ cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& t
 }
 
 cudaError_t launch_spec_gemm_simple(int D, const int8_t* G, const int8_t* A, const SpecGemmArgs& a, cudaStream_t s) {
-  dim3 grid((a.d + 127) / 128, a.n_rows, a.L);
+  dim3 grid((a.nb + 127) / 128, a.n_rows, a.L);
   spec_gemm_simple_kernel<<<grid, 128, 0, s>>>(G, A, a, D);
   return cudaGetLastError();
 }
