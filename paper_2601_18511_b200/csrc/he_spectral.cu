@@ -403,14 +403,21 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
 constexpr int kInv1kBlocks = 8;
 constexpr int kInv1kLd = 1060;
 HE_D uint32_t pad32(uint32_t p) { return p + (p >> 5); }
-// -> x[e] = INTT value u = lane + 32 e for e < 24, reduced to [0, q)
-HE_D void inv1024_column(uint32_t* col, const uint2 (&r1)[26], const uint2* __restrict__ r2, uint32_t q, uint32_t lane,
-                         uint32_t (&x)[32]) {
-  const uint32_t q2 = 2 * q;
+// -> x[l][e] = INTT value u = lane + 32 e of limb l for e < 24, reduced to [0, q); both limbs in lockstep
+struct Inv1kLimb {
+  uint32_t* col;
+  const uint2* r2;
+  uint32_t q;
+};
+HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_t lane, uint32_t (&x)[2][32]) {
 #pragma unroll
-  for (int e = 0; e < 32; ++e) x[e] = col[33 * lane + e];
+  for (int l = 0; l < 2; ++l)
 #pragma unroll
-  for (int e = 0; e < 32; e += 2) dit_bf1(x[e], x[e + 1], q2);
+    for (int e = 0; e < 32; ++e) x[l][e] = L[l].col[33 * lane + e];
+#pragma unroll
+  for (int e = 0; e < 32; e += 2)
+#pragma unroll
+    for (int l = 0; l < 2; ++l) dit_bf1(x[l][e], x[l][e + 1], 2 * L[l].q);
 #pragma unroll
   for (int s = 1; s < 5; ++s) {
     const int len = 1 << s;
@@ -418,15 +425,22 @@ HE_D void inv1024_column(uint32_t* col, const uint2 (&r1)[26], const uint2* __re
     for (int e = 0; e < 32; ++e) {
       if (e & len) continue;
       const int off = e & (len - 1);
-      if (off == 0) dit_bf1(x[e], x[e + len], q2);
-      else dit_bf(x[e], x[e + len], r1[(1 << s) - s - 1 + off - 1], q2, q);
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        if (off == 0) dit_bf1(x[l][e], x[l][e + len], 2 * L[l].q);
+        else dit_bf(x[l][e], x[l][e + len], cst.r1[l][(1 << s) - s - 1 + off - 1], 2 * L[l].q, L[l].q);
+      }
     }
   }
 #pragma unroll
-  for (int e = 0; e < 32; ++e) col[33 * lane + e] = x[e];
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int e = 0; e < 32; ++e) L[l].col[33 * lane + e] = x[l][e];
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 32; ++e) x[e] = col[lane + 33 * e];
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int e = 0; e < 32; ++e) x[l][e] = L[l].col[lane + 33 * e];
   __syncwarp();
 #pragma unroll
   for (int s = 5; s < 9; ++s) {
@@ -435,28 +449,36 @@ HE_D void inv1024_column(uint32_t* col, const uint2 (&r1)[26], const uint2* __re
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       if (e & len) continue;
-      dit_bf(x[e], x[e + len], __ldg(r2 + base + 32 * (e & (len - 1)) + lane), q2, q);
+#pragma unroll
+      for (int l = 0; l < 2; ++l)
+        dit_bf(x[l][e], x[l][e + len], __ldg(L[l].r2 + base + 32 * (e & (len - 1)) + lane), 2 * L[l].q, L[l].q);
     }
   }
   // len = 512: pairs (e, e + 16); the upper output u = lane + 32 e + 512 is needed only for e < 8
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    const uint2 w = __ldg(r2 + 480 + 32 * e + lane);
-    if (e < 8) {
-      dit_bf(x[e], x[e + 16], w, q2, q);
-    } else {
-      const uint32_t t = x[e + 16] * w.x - __umulhi(x[e + 16], w.y) * q;
-      x[e] = min(x[e], x[e] - q2) + t;
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const uint32_t q = L[l].q, q2 = 2 * q;
+      const uint2 w = __ldg(L[l].r2 + 480 + 32 * e + lane);
+      if (e < 8) {
+        dit_bf(x[l][e], x[l][e + 16], w, q2, q);
+      } else {
+        const uint32_t t = x[l][e + 16] * w.x - __umulhi(x[l][e + 16], w.y) * q;
+        x[l][e] = min(x[l][e], x[l][e] - q2) + t;
+      }
     }
   }
 #pragma unroll
-  for (int e = 0; e < 24; ++e) {
-    const uint32_t v = min(x[e], x[e] - q2);
-    x[e] = min(v, v - q);
-  }
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int e = 0; e < 24; ++e) {
+      const uint32_t v = min(x[l][e], x[l][e] - 2 * L[l].q);
+      x[l][e] = min(v, v - L[l].q);
+    }
 }
 
-__global__ void __launch_bounds__(256, 3) spec_inverse1024_kernel(const uint32_t* __restrict__ c0,
+__global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t* __restrict__ c0,
                                                                   const uint32_t* __restrict__ c1, uint32_t n_out,
                                                                   uint32_t row0, uint32_t nbp, uint32_t nblk,
                                                                   uint32_t d, SpecInvConst cst,
@@ -485,20 +507,15 @@ __global__ void __launch_bounds__(256, 3) spec_inverse1024_kernel(const uint32_t
   const uint32_t b = warp;
   if (b0 + b < nblk) {
     const uint32_t q0 = cst.q[0], q1 = cst.q[1];
-    uint32_t x[32];
-    inv1024_column(xs1 + b * kInv1kLd, cst.r1[1], cst.r2[1], q1, lane, x);
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < 24; ++e) xs1[b * kInv1kLd + lane + 32 * e] = x[e];   // limb-1 words, u = lane + 32 e
-    inv1024_column(xs0 + b * kInv1kLd, cst.r1[0], cst.r2[0], q0, lane, x);
-    __syncwarp();
+    const Inv1kLimb L[2] = {{xs0 + b * kInv1kLd, cst.r2[0], q0}, {xs1 + b * kInv1kLd, cst.r2[1], q1}};
+    uint32_t x[2][32];
+    inv1024_pair(L, cst, lane, x);
 #pragma unroll
     for (int e = 0; e < 24; ++e) {
-      const uint32_t x1 = xs1[b * kInv1kLd + lane + 32 * e];
       uint32_t t;
-      if (x1 > (q1 >> 1)) t = csub(x[e] + (q1 - x1), q0);
-      else t = sub_mod(x[e], x1, q0);
-      xs1[b * kInv1kLd + lane + 32 * e] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);
+      if (x[1][e] > (q1 >> 1)) t = csub(x[0][e] + (q1 - x[1][e]), q0);
+      else t = sub_mod(x[0][e], x[1][e], q0);
+      xs1[b * kInv1kLd + lane + 32 * e] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);  // u = lane + 32 e
     }
   }
   __syncthreads();
