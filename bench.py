@@ -224,15 +224,16 @@ def run_ours(a, rank: int, world: int, local: int):
     else:
         # K7 S4 (spectral inverse + rescale + a' store) dominates: HBM roofline on its algorithmic bytes
         inv_ms = stage_ms["spectral_inverse"]
-        nbytes = spectral_inverse_bytes(P, rows)
+        si = plan.spectral_info()
+        nbytes = spectral_inverse_bytes(P, rows, si["L"], si["blocks"])
         gbs = nbytes / (inv_ms * 1e-3) / 1e9
         hbm = measured_hbm()
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
                 "traffic": load_traffic(a.shape, "spectral_inverse"),
-                "kernel": "he::spec_inverse512_kernel (K7 S4: 512-pt INTT x 2 limbs, rescale, a' store)",
+                "kernel": f"he::spec_inverse{si['L']}_kernel (K7 S4: {si['L']}-pt INTT x 2 limbs, rescale, a' store)",
                 "kernel_ms": round(inv_ms, 3), "algorithmic_bytes_per_launch": nbytes,
                 "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
-        gops = sum(spectral_gemm_ops(P, rows, n_in, L) for L in (0, 1))
+        gops = sum(spectral_gemm_ops(P, rows, n_in, L, si["L"], si["blocks"]) for L in (0, 1))
         g_ms = stage_ms["spectral_gemm_q0"] + stage_ms["spectral_gemm_q1"]
         roof["spectral_gemm"] = {
             "kernel": "he::spec_gemm_kernel<4>/<3> (K7 S3, tcgen05 kind::i8, per-frequency modular GEMM)",
@@ -262,8 +263,8 @@ def run_ours(a, rank: int, world: int, local: int):
                        "tokens": P.tokens, "N": N, "mlwe": [P.mlwe_degree, P.mlwe_rank],
                        "moduli": list(P.moduli), "log_delta": P.log_delta,
                        "digits": {"weight": plan.d_w, "ct_q0": d0, "ct_q1": d1},
-                       "algo": a.algo + (" (K7: a' by blockwise 512-pt NTT correlation + per-frequency tcgen05 "
-                                         "GEMMs; b' on K1)" if a.algo == "spectral" else " (K1 over all columns)"),
+                       "algo": a.algo + (" (K7: a' by blockwise NTT correlation + per-frequency tcgen05 GEMMs; "
+                              "b' on K1)" if a.algo == "spectral" else " (K1 over all columns)"),
                        "parallelism": f"row-shard x{world}" + (" + NCCL bcast/all-gather" if world > 1 else ""),
                        "l2": "inputs larger than L2: each op writes and reads a "
                              f"{plan.workspace_bytes() / 1e9:.2f} GB workspace"},

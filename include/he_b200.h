@@ -135,6 +135,8 @@ he_status he_pcmm_gemm_rows(const he_pcmm_plan* plan, const void* workspace_dev,
  * call it before sharing the plan.  Workspace sizes change accordingly. */
 he_status he_pcmm_spectral_weight_bytes(const he_pcmm_plan* plan, uint64_t* bytes);
 he_status he_pcmm_spectral_prepare(he_pcmm_plan* plan, int8_t* spec_weights_dev, void* stream);
+/* spectral plans: info[0..3] = {transform length L, outputs per block L - k, blocks, blocks padded to 32} */
+he_status he_pcmm_spectral_info(const he_pcmm_plan* plan, uint32_t* info);
 /* 0 = K1 over all columns (direct), 1 = spectral */
 he_status he_pcmm_algo(const he_pcmm_plan* plan, int* algo);
 /* Profiling: while enabled, every stage launch of the plan records a CUDA event pair on its

@@ -707,6 +707,16 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
   return HE_OK;
 }
 
+extern "C" he_status he_pcmm_spectral_info(const he_pcmm_plan* p, uint32_t* info) {
+  if (!p || !info) return fail(HE_EINVAL, "null argument");
+  if (p->algo != 1) return fail(HE_EINVAL, "plan is not spectral");
+  info[0] = p->L;
+  info[1] = p->ob;
+  info[2] = p->nblk;
+  info[3] = p->nbp;
+  return HE_OK;
+}
+
 extern "C" he_status he_pcmm_algo(const he_pcmm_plan* p, int* algo) {
   if (!p || !algo) return fail(HE_EINVAL, "null argument");
   *algo = p->algo;

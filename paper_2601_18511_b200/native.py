@@ -28,7 +28,7 @@ EXPORTS = (
     "he_encrypt_vector", "he_rhombus_keygen", "he_rhombus_weight_bytes", "he_rhombus_encode_weights",
     "he_rhombus_plan_create", "he_rhombus_plan_destroy", "he_rhombus_workspace_bytes", "he_rhombus_run",
     "he_pcmm_gemm_rows", "he_pcmm_spectral_weight_bytes", "he_pcmm_spectral_prepare", "he_pcmm_algo",
-    "he_pcmm_profile", "he_pcmm_profile_read",
+    "he_pcmm_profile", "he_pcmm_profile_read", "he_pcmm_spectral_info",
 )
 
 
@@ -86,6 +86,7 @@ def lib():
             "he_pcmm_spectral_prepare": (st, [vp, vp, vp]),
             "he_pcmm_algo": (st, [vp, ctypes.POINTER(ctypes.c_int)]),
             "he_pcmm_profile": (st, [vp, i32]),
+            "he_pcmm_spectral_info": (st, [vp, ctypes.POINTER(u32)]),
             "he_pcmm_profile_read": (st, [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u32), u32]),
             "he_encrypt_vector": (st, [vp, vp, vp, u32, u64, u32, vp, vp]),
             "he_rhombus_keygen": (st, [vp, u64, vp, vp, vp, vp, vp, vp, vp]),

@@ -66,6 +66,12 @@ class MlwePcmmPlan:
             self._workspace = torch.empty(need, dtype=torch.int8, device=device)
         return self._workspace
 
+    def spectral_info(self) -> dict:
+        """Spectral plans: transform length L, outputs per block, blocks, padded blocks."""
+        info = (ctypes.c_uint32 * 4)()
+        native.call("he_pcmm_spectral_info", self._handle, info)
+        return {"L": info[0], "block_outputs": info[1], "blocks": info[2], "blocks_padded": info[3]}
+
     STAGES = ("decompose", "spectral_data", "modgemm", "spectral_gemm_q0", "spectral_gemm_q1", "spectral_inverse")
 
     def profile(self, enable: bool = True) -> None:
@@ -245,17 +251,17 @@ def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_hos
     return MlweBlocks(out_b_host, out_a_host, level=X.level - 1, n_rows=plan.n_out)
 
 
-def spectral_gemm_ops(params, n_out: int, n_in: int, limb: int) -> int:
-    """Algorithmic int8 tensor-core ops of one K7 S3 launch (limb ``limb``): per frequency f < 2k a
-    (n_out x R) x (R x d) product, R = n_in / k, every digit of G^ meeting every digit of A^."""
+def spectral_gemm_ops(params, n_out: int, n_in: int, limb: int, L: int, blocks: int) -> int:
+    """Algorithmic int8 tensor-core ops of one K7 S3 launch (limb ``limb``): per frequency f < L a
+    (n_out x R) x (R x blocks) product, R = n_in / k, every digit of G^ meeting every digit of A^."""
     D = params.ct_digits(limb)
-    return 2 * 2 * params.mlwe_rank * n_out * (n_in // params.mlwe_rank) * params.mlwe_degree * D * D
+    return 2 * L * n_out * (n_in // params.mlwe_rank) * blocks * D * D
 
 
-def spectral_inverse_bytes(params, n_out: int) -> int:
-    """Algorithmic HBM bytes of one K7 S4 launch: read C^ of both limbs (2k x n_out x d u32 each),
-    write the a' words (n_out x N u32)."""
-    return 2 * 2 * params.mlwe_rank * n_out * params.mlwe_degree * 4 + n_out * params.N * 4
+def spectral_inverse_bytes(params, n_out: int, L: int, blocks: int) -> int:
+    """Algorithmic HBM bytes of one K7 S4 launch: read C^ of both limbs (L x n_out x blocks u32
+    each), write the a' words (n_out x N u32)."""
+    return 2 * L * n_out * blocks * 4 + n_out * params.N * 4
 
 
 def pcmm_ops(params, n_out: int, n_in: int, d_w: int) -> int:
