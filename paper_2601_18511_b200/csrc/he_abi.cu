@@ -503,8 +503,8 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     uint32_t inv = 1;  // q^-1 mod 2^32 by Newton iteration
     for (int it = 0; it < 5; ++it) inv *= 2u - q * inv;
     a.qninv = 0u - inv;
-    a.off64 = (uint64_t)q << 29;
-    for (int sft = 0; sft < 8; ++sft) a.pw[sft] = (int32_t)powmod_h(2, 8ull * sft + 32, q);
+    a.off64 = p->spec_off[L];
+    for (int i = 0; i < 8; ++i) a.pw[i] = (int32_t)powmod_h(2, 16ull * i + 32, q);
     a.out = C[L];
     const int8_t* A = base + (L ? w.a1 : w.a0);
     if (simple) {
@@ -671,13 +671,17 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
   if (c->R.d % 32) return fail(HE_EINVAL, "spectral path needs mlwe_degree %% 32 == 0");
   uint32_t L, r_pad, dsp[2];
   spec_dims(p, L, r_pad, dsp);
-  // exactness of S3: int32 shift accumulators R * D * 2^14 < 2^31; the Montgomery recombination needs
-  // |sum_s acc_s pw_s| < q 2^29 (the offset), i.e. S * R * D * 2^14 < 2^29
+  // exactness of S3 (|digit product| <= 2^14, K = R = n_in / k terms):
+  //   int32 shift accumulators      R * D * 2^14 < 2^31
+  //   int32 paired shifts           |acc_2i + 256 acc_2i+1| <= R * D * 2^14 * 257 < 2^31
+  //   Montgomery input              off + |sum_i t_i pw_i| < 2 B, B = ceil(S/2) * R * D * 2^14 * 257 * q < q 2^32
   const uint64_t R = p->n_in / c->R.k;
   for (int i = 0; i < 2; ++i) {
-    if (R * dsp[i] * 16384ull >= (1ull << 31)) return fail(HE_EINVAL, "n_in too large for the spectral accumulators");
-    if ((uint64_t)(2 * dsp[i] - 1) * R * dsp[i] * 16384ull >= (1ull << 29))
-      return fail(HE_EINVAL, "n_in too large for the spectral recombination");
+    const uint64_t tmax = R * dsp[i] * 16384ull * 257ull;
+    const unsigned __int128 B = (unsigned __int128)dsp[i] * tmax * c->R.q[i];   // ceil(S/2) = D terms
+    if (tmax >= (1ull << 31) || B >= ((unsigned __int128)c->R.q[i] << 32))
+      return fail(HE_EINVAL, "n_in (%u) too large for the spectral recombination; use algo=direct", p->n_in);
+    p->spec_off[i] = (uint64_t)(B / c->R.q[i] + 1) * c->R.q[i];
   }
   cudaStream_t st = (cudaStream_t)stream;
   for (int i = 0; i < 2; ++i) {

@@ -27,6 +27,7 @@ struct he_pcmm_plan {
   int algo = 0;
   uint32_t L = 0, r_pad = 0, dsp[2] = {0, 0};
   uint32_t ob = 0, nblk = 0, nbp = 0;  // outputs per block (L - k), blocks, blocks padded to 32
+  uint64_t spec_off[2] = {0, 0};       // S3 recombination offsets (multiples of q_i)
   const int8_t* spec_w = nullptr;  // caller-owned: G^ limb 0 [L][D0][n_out][r_pad], then limb 1
   CUtensorMap tmSA[2];
   he::SpecTable st[2];

@@ -75,8 +75,8 @@ struct SpecGemmArgs {
   int L, nb, r_pad;         // transform length, blocks (padded to 32), K bytes
   uint32_t q;
   uint32_t qninv;           // -q^-1 mod 2^32 (Montgomery)
-  uint64_t off64;           // q * 2^29: makes the signed shift sum non-negative
-  int32_t pw[8];            // 2^(8 s + 32) mod q
+  uint64_t off64;           // multiple of q above the recombination bound: makes the sum non-negative
+  int32_t pw[8];            // 2^(16 i + 32) mod q (paired shifts)
   uint32_t* out;            // C^ [L][n_out][nb]
 };
 struct SpecInvConst {

@@ -742,16 +742,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tmem_empty_remote + buf * 8);  // accumulators drained
-      // sum_s acc_s 2^(8 s) mod q by one Montgomery reduction: v = off + sum_s acc_s (2^(8s+32) mod q)
-      // (off = q 2^29 > |sum| keeps v in [0, q 2^32)), then (v + ((v mod 2^32) (-q^-1) mod 2^32) q) / 2^32
+      // sum_s acc_s 2^(8 s) mod q: shifts paired exactly in int32 (t_i = acc_2i + 256 acc_2i+1, plan-time
+      // bound |t_i| < 2^31), v = off + sum_i t_i (2^(16 i + 32) mod q) in int64 (off: a multiple of q above
+      // |sum|), one Montgomery reduction (v + ((v mod 2^32)(-q^-1) mod 2^32) q) / 2^32 in [0, 3q), two csubs
       uint32_t res[kSpecEpiCols];
+      constexpr int T = (C::S + 1) / 2;
 #pragma unroll
       for (int e = 0; e < kSpecEpiCols; ++e) {
         int64_t v = (int64_t)args.off64;
 #pragma unroll
-        for (int s = 0; s < C::S; ++s) v += (int64_t)(int32_t)acc[s][e] * (int64_t)args.pw[s];
+        for (int i = 0; i < T; ++i) {
+          const int32_t lo = (int32_t)acc[2 * i][e];
+          const int32_t t = (2 * i + 1 < C::S) ? lo + ((int32_t)acc[2 * i + 1][e] << 8) : lo;
+          v += (int64_t)t * (int64_t)args.pw[i];
+        }
         const uint32_t m = (uint32_t)v * args.qninv;
-        const uint32_t t = (uint32_t)(((uint64_t)v + (uint64_t)m * q) >> 32);   // [0, 2q)
+        uint32_t t = (uint32_t)(((uint64_t)v + (uint64_t)m * q) >> 32);   // [0, 3q)
+        t = min(t, t - 2 * q);
         res[e] = min(t, t - q);
       }
       // each warp stages its 32 rows x 8 words (1 KB, double-buffered) and TMA-stores them itself: no
