@@ -673,13 +673,20 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
   spec_dims(p, L, r_pad, dsp);
   // exactness of S3 (|digit product| <= 2^14, K = R = n_in / k terms):
   //   int32 shift accumulators      R * D * 2^14 < 2^31
-  //   int32 paired shifts           |acc_2i + 256 acc_2i+1| <= R * D * 2^14 * 257 < 2^31
-  //   Montgomery input              off + |sum_i t_i pw_i| < 2 B, B = ceil(S/2) * R * D * 2^14 * 257 * q < q 2^32
+  //   int32 paired shifts           |t_j| = |acc_2j + 256 acc_2j+1| <= R 2^14 (pairs(2j) + 256 pairs(2j+1)) < 2^31
+  //   Montgomery input              off + |sum_j t_j pw_j| < 2 B, B = q sum_j max|t_j| < q 2^32
   const uint64_t R = p->n_in / c->R.k;
   for (int i = 0; i < 2; ++i) {
-    const uint64_t tmax = R * dsp[i] * 16384ull * 257ull;
-    const unsigned __int128 B = (unsigned __int128)dsp[i] * tmax * c->R.q[i];   // ceil(S/2) = D terms
-    if (tmax >= (1ull << 31) || B >= ((unsigned __int128)c->R.q[i] << 32))
+    const int D = (int)dsp[i], S = 2 * D - 1;
+    auto pairs = [&](int sft) { return sft < 0 || sft >= S ? 0 : (sft < D ? sft + 1 : S - sft); };
+    uint64_t tsum = 0, tmax = 0;
+    for (int j = 0; j < D; ++j) {
+      const uint64_t tj = R * 16384ull * (uint64_t)(pairs(2 * j) + 256 * pairs(2 * j + 1));
+      tsum += tj;
+      tmax = tj > tmax ? tj : tmax;
+    }
+    const unsigned __int128 B = (unsigned __int128)tsum * c->R.q[i];
+    if (R * D * 16384ull >= (1ull << 31) || tmax >= (1ull << 31) || B >= ((unsigned __int128)c->R.q[i] << 32))
       return fail(HE_EINVAL, "n_in (%u) too large for the spectral recombination; use algo=direct", p->n_in);
     p->spec_off[i] = (uint64_t)(B / c->R.q[i] + 1) * c->R.q[i];
   }
