@@ -218,6 +218,14 @@ HE_D void gs_round16(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t h
   }
 }
 
+// smem offset of element j0 + e T relative to pad(j0) for the thread layouts of the rounds below
+// (j0 = (tau / T) 16 T + tau % T with T in {1, 16, 256}: j0 % 32 + e T never carries past the
+// next multiple of 32 except through e T itself, so the offset is a compile-time constant)
+template <int T>
+HE_D constexpr uint32_t poff(int e) {
+  return T >= 32 ? (uint32_t)(e * T + e * T / 32) : (T == 16 ? (uint32_t)(16 * e + e / 2) : (uint32_t)e);
+}
+
 // forward: rounds of 4 stages, T = N2/16, N2/256, ..., 1; first round straight from global
 template <int N2>
 __global__ void __launch_bounds__(N2 / 16) ntt_fwd_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
@@ -227,19 +235,44 @@ __global__ void __launch_bounds__(N2 / 16) ntt_fwd_rows(uint32_t* __restrict__ d
   uint32_t* a = data + blockIdx.y * stride + (size_t)b * N2;
   const uint32_t tau = threadIdx.x;
   const uint32_t q2 = 2 * q;
+  uint32_t x[16];
 #pragma unroll
-  for (int T = N2 / 16; T >= 1; T /= 16) {
-    const uint32_t j0 = (tau / T) * 16 * T + (tau % T);
-    uint32_t x[16];
-    if (T == N2 / 16) {
+  for (int e = 0; e < 16; ++e) x[e] = a[tau + e * (N2 / 16)];  // coalesced across the warp
+  ct_round16(x, tw, n / N2, b, q2, q);
+  if constexpr (N2 == 16) {
+    if (final_reduce) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = a[j0 + e * T];  // coalesced across the warp
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = s[pad(j0 + e * T)];
+      for (int e = 0; e < 16; ++e) x[e] = reduce4(x[e], q);
     }
-    ct_round16(x, tw, n / (16 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
-    if (T == 1) {
+    uint4* dst = reinterpret_cast<uint4*>(a);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+    return;
+  } else {
+    {
+      constexpr int T = N2 / 16;
+      uint32_t* ps = s + pad(tau);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) ps[poff<T>(e)] = x[e];
+      __syncthreads();
+    }
+    if constexpr (N2 == 4096) {
+      constexpr int T = 16;
+      const uint32_t j0 = (tau / T) * 16 * T + (tau % T);
+      uint32_t* ps = s + pad(j0);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = ps[poff<T>(e)];
+      ct_round16(x, tw, n / (16 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) ps[poff<T>(e)] = x[e];
+      __syncthreads();
+    }
+    {
+      uint32_t* ps = s + pad(16 * tau);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = ps[e];
+      ct_round16(x, tw, n / 16, b * (N2 / 16) + tau, q2, q);
       if (final_reduce) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) x[e] = reduce4(x[e], q);
@@ -247,11 +280,6 @@ __global__ void __launch_bounds__(N2 / 16) ntt_fwd_rows(uint32_t* __restrict__ d
       uint4* dst = reinterpret_cast<uint4*>(a + 16 * tau);
 #pragma unroll
       for (int v = 0; v < 4; ++v) dst[v] = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
-    } else {
-      if (T != N2 / 16) __syncthreads();  // everyone has read the previous round's smem
-#pragma unroll
-      for (int e = 0; e < 16; ++e) s[pad(j0 + e * T)] = x[e];
-      __syncthreads();
     }
   }
 }
@@ -267,34 +295,50 @@ __global__ void __launch_bounds__(N2 / 16) ntt_inv_rows(uint32_t* __restrict__ d
   uint32_t* a = data + blockIdx.y * stride + (size_t)b * N2;
   const uint32_t tau = threadIdx.x;
   const uint32_t q2 = 2 * q;
+  uint32_t x[16];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a + 16 * tau);
 #pragma unroll
-  for (int T = 1; T < N2; T *= 16) {
-    const uint32_t j0 = (tau / T) * 16 * T + (tau % T);
-    uint32_t x[16];
-    if (T == 1) {
-      const uint4* src = reinterpret_cast<const uint4*>(a + 16 * tau);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const uint4 w = src[v];
-        x[4 * v] = w.x;
-        x[4 * v + 1] = w.y;
-        x[4 * v + 2] = w.z;
-        x[4 * v + 3] = w.w;
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = s[pad(j0 + e * T)];
+    for (int v = 0; v < 4; ++v) {
+      const uint4 w = src[v];
+      x[4 * v] = w.x;
+      x[4 * v + 1] = w.y;
+      x[4 * v + 2] = w.z;
+      x[4 * v + 3] = w.w;
     }
-    gs_round16(x, tw, n / (2 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
-    if (16 * T == N2) {
+  }
+  gs_round16(x, tw, n / 2, b * (N2 / 16) + tau, q2, q);
+  if constexpr (N2 > 16) {
+    {
+      uint32_t* ps = s + pad(16 * tau);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) a[j0 + e * T] = do_scale ? shoup_mul(x[e], ninv, ninvp, q) : x[e];
-    } else {
-      if (T != 1) __syncthreads();
-#pragma unroll
-      for (int e = 0; e < 16; ++e) s[pad(j0 + e * T)] = x[e];
+      for (int e = 0; e < 16; ++e) ps[e] = x[e];
       __syncthreads();
     }
+    if constexpr (N2 == 4096) {
+      constexpr int T = 16;
+      const uint32_t j0 = (tau / T) * 16 * T + (tau % T);
+      uint32_t* ps = s + pad(j0);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = ps[poff<T>(e)];
+      gs_round16(x, tw, n / (2 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) ps[poff<T>(e)] = x[e];
+      __syncthreads();
+    }
+    {
+      constexpr int T = N2 / 16;
+      uint32_t* ps = s + pad(tau);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = ps[poff<T>(e)];
+      gs_round16(x, tw, n / (2 * T), b, q2, q);
+    }
+  }
+  {
+    constexpr int T = N2 / 16;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) a[tau + e * T] = do_scale ? shoup_mul(x[e], ninv, ninvp, q) : x[e];
   }
 }
 
