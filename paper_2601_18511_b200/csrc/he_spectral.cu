@@ -100,14 +100,15 @@ void spec_table_free(SpecTable& t) {
 // X[f] = sum_i x[i] w^(f i).  Inverse: DIT (bit-reversed -> natural) with the L^-1 scaling
 // left to the caller.  Values fully reduced in [0, q).
 HE_D void cyc_fwd_smem(uint32_t* x, int cnt, int ld, int L, const uint2* __restrict__ tw, uint32_t q) {
-  const int half = L / 2;
-  for (int len = half, step = 1; len >= 1; len >>= 1, step <<= 1) {
+  const int half = L / 2, lh = __ffs(half) - 1;    // L is a power of two: shifts, not divisions
+  for (int ll = lh; ll >= 0; --ll) {
+    const int len = 1 << ll, step_sh = lh - ll;
     for (int i = threadIdx.x; i < cnt * half; i += blockDim.x) {
-      const int b = i / half, j = i % half;
-      const int off = j % len;
-      uint32_t* p = x + b * ld + (j / len) * 2 * len + off;
+      const int b = i >> lh, j = i & (half - 1);
+      const int off = j & (len - 1);
+      uint32_t* p = x + b * ld + ((j >> ll) << (ll + 1)) + off;
       const uint32_t u = p[0], v = p[len];
-      const uint2 w = __ldg(tw + off * step);
+      const uint2 w = __ldg(tw + (off << step_sh));
       p[0] = add_mod(u, v, q);
       p[len] = shoup_mul(sub_mod(u, v, q), w.x, w.y, q);
     }

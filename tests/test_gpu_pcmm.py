@@ -292,3 +292,25 @@ def test_streamed_to_host_matches_device_output(algo):
     torch.cuda.synchronize()
     assert ctx.ledger.diff(before)["rescales"] == 5
     assert torch.equal(ha, Y.out_a.cpu()) and torch.equal(hb, Y.out_b.cpu())
+
+
+def test_spectral_transform_length_512_subprocess():
+    """The L = 2k = 512 spectral variant (HE_SPEC_L=512, read once per process) produces the same
+    words as the direct K1 path at a Llama shape -- run in a child process."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, torch, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import test_gpu_pcmm as G; from paper_2601_18511_b200 import HeParams, make_mlwe_pcmm_plan, pcmm_mlwe;"
+        "P = HeParams.llama(); ctx, sk, A, W, X = G.setup(P, 1024, 4096, seed=4);"
+        "ps = make_mlwe_pcmm_plan(ctx, W); assert ps.spectral_info()['L'] == 512;"
+        "Y1 = pcmm_mlwe(ctx, ps, X); a1, b1 = Y1.out_a.clone(), Y1.out_b.clone();"
+        "Y2 = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W, algo='direct'), X);"
+        "assert torch.equal(a1, Y2.out_a) and torch.equal(b1, Y2.out_b); print('ok')"
+    )
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, HE_SPEC_L="512")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
