@@ -65,6 +65,8 @@ struct SpecTable {  // cyclic NTT of length L mod q
   uint2* iv = nullptr;   // (w^-j, Shoup) j < L/2
   uint2* r2 = nullptr;   // L = 512: per-stage lane tables of the fast inverse (he_spectral.cu)
   uint2 r1[26] = {};     // L = 512 / 1024: round-1 twiddles of the fast inverse (host copy, kernel params)
+  uint2* f2 = nullptr;   // L = 1024: per-stage lane tables of the fast forward (S2)
+  uint2 f1[26] = {};     // L = 1024: lane-uniform twiddles of the fast forward (kernel params)
   uint32_t linv = 0, linvp = 0;
 };
 cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q);

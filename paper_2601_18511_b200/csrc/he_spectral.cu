@@ -51,7 +51,7 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
   // (stages 5..9); entry [i][lane] of stage s = w^-((lane + lanes i) << (log2(L/2) - s)) at lanes (2^(s - s0) - 1)
   const int lg = ilog2_h(L / 2), s0 = L == 512 ? 4 : 5, lanes = 1 << s0;
   const size_t nr2 = (L == 512 || L == 1024) ? (size_t)lanes * ((1u << (lg + 1 - s0)) - 1) : 0;
-  uint32_t* h = new uint32_t[2 * (size_t)L + 2 * nr2];  // fw pairs [L/2][2], iv pairs [L/2][2], r2 pairs
+  uint32_t* h = new uint32_t[2 * (size_t)L + 4 * nr2];  // fw pairs [L/2][2], iv pairs [L/2][2], r2 pairs, f2 pairs
   uint64_t p = 1, pi = 1;
   for (uint32_t j = 0; j < L / 2; ++j) {
     h[2 * j] = (uint32_t)p;
@@ -68,6 +68,8 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
         const uint32_t j = (uint32_t)(lo + lanes * i) << (lg - st);
         h[2 * (size_t)L + 2 * (base + lanes * i + lo)] = h[L + 2 * j];
         h[2 * (size_t)L + 2 * (base + lanes * i + lo) + 1] = h[L + 2 * j + 1];
+        h[2 * (size_t)L + 2 * nr2 + 2 * (base + lanes * i + lo)] = h[2 * j];        // forward (f2)
+        h[2 * (size_t)L + 2 * nr2 + 2 * (base + lanes * i + lo) + 1] = h[2 * j + 1];
       }
   }
   // r1: round-1 (register) stages s = 1 .. s0 - 1, off = 1 .. 2^s - 1 at (2^s - s - 1) + off - 1
@@ -75,11 +77,12 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
     for (int off = 1; off < (1 << st); ++off) {
       const uint32_t j = (uint32_t)off << (lg - st);
       t.r1[(1 << st) - st - 1 + off - 1] = make_uint2(h[L + 2 * j], h[L + 2 * j + 1]);
+      t.f1[(1 << st) - st - 1 + off - 1] = make_uint2(h[2 * j], h[2 * j + 1]);
     }
   t.linv = (uint32_t)powmod_h(L, q - 2, q);
   t.linvp = shoup_pre(t.linv, q);
   uint32_t* dptr = nullptr;
-  const size_t words = 2 * (size_t)L + 2 * nr2;
+  const size_t words = 2 * (size_t)L + 4 * nr2;
   cudaError_t e = cudaMalloc(&dptr, words * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemcpy(dptr, h, words * sizeof(uint32_t), cudaMemcpyHostToDevice);
   delete[] h;
@@ -87,12 +90,13 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
   t.fw = reinterpret_cast<uint2*>(dptr);
   t.iv = reinterpret_cast<uint2*>(dptr + L);
   t.r2 = nr2 ? reinterpret_cast<uint2*>(dptr + 2 * L) : nullptr;
+  t.f2 = nr2 ? reinterpret_cast<uint2*>(dptr + 2 * L + 2 * nr2) : nullptr;
   return cudaSuccess;
 }
 
 void spec_table_free(SpecTable& t) {
   if (t.fw) cudaFree(t.fw);
-  t.fw = t.iv = t.r2 = nullptr;
+  t.fw = t.iv = t.r2 = t.f2 = nullptr;
 }
 
 // ---------------------------------------------------------------- cooperative cyclic NTTs in shared memory
@@ -203,6 +207,103 @@ __global__ void __launch_bounds__(256) spec_data_kernel(const uint32_t* __restri
     const int f = i / cnt, b = i % cnt;
     int8_t* dst = out + ((size_t)f * D * nbp + m) * r_pad + r0 + b;
     write_digits(xs[b * L + f], q, D, dst, plane);
+  }
+}
+
+
+// Fast S2 for L = 1024: one warp per window, 32 register elements per lane, forward DIF (natural ->
+// bit-reversed) in two register rounds -- stages 512 .. 32 apart on elements l + 32 e (per-stage lane
+// tables f2), a per-warp smem transpose, stages 16 .. 1 apart on the lane's 32 contiguous elements
+// (lane-uniform twiddles f1 as kernel parameters) -- then the digits of 16 windows x 1024 frequencies.
+// GS: X, Y in [0, 2q) -> X' = X + Y, Y' = (X - Y) W, both in [0, 2q)
+HE_D void gs_bf(uint32_t& x, uint32_t& y, uint2 w, uint32_t q2, uint32_t q) {
+  const uint32_t s = x + y;
+  const uint32_t d = x + q2 - y;
+  x = min(s, s - q2);
+  y = d * w.x - __umulhi(d, w.y) * q;
+}
+struct SpecFwdConst {
+  const uint2* f2;
+  uint2 f1[26];
+};
+constexpr int kS2Ld = 1057;   // per-warp region pitch: 1024 + 32 + 1 (odd: conflict-free digit read-out)
+__global__ void __launch_bounds__(512) spec_data1024_kernel(const uint32_t* __restrict__ ct, uint32_t n_ct,
+                                                            uint32_t limb, uint32_t k, uint32_t ob, uint32_t nbp,
+                                                            uint32_t N, uint32_t q, int D, uint32_t r_pad,
+                                                            SpecFwdConst cf, int8_t* __restrict__ out) {
+  extern __shared__ uint32_t xs[];                      // [16 windows][1057]
+  const uint32_t m = blockIdx.x, r0 = blockIdx.y * 16;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t q2 = 2 * q;
+  const uint32_t r = r0 + w;
+  uint32_t* col = xs + w * kS2Ld;
+  if (r < n_ct) {
+    const uint32_t* a = ct + ((size_t)r * 2 + limb) * 2 * N;
+    const int64_t I0 = (int64_t)ob * m - (int64_t)k + 1;
+    uint32_t x[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const int64_t I = I0 + lane + 32 * e;
+      uint32_t v;
+      if (I < 0) {
+        const uint32_t t = a[I + N];
+        v = t ? q - t : 0u;
+      } else if (I >= (int64_t)N) {
+        const uint32_t t = a[I - N];
+        v = t ? q - t : 0u;
+      } else {
+        v = a[I];
+      }
+      x[e] = v;
+    }
+    // round 1: len = 512 .. 32 (element distance 16 .. 1), twiddle w^((l + 32 i) << (9 - s))
+#pragma unroll
+    for (int s = 9; s >= 5; --s) {
+      const int h = 1 << (s - 5), base = 32 * (h - 1);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        if (e & h) continue;
+        gs_bf(x[e], x[e + h], __ldg(cf.f2 + base + 32 * (e & (h - 1)) + lane), q2, q);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) col[lane + 33 * e] = x[e];    // pad(l + 32 e)
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < 32; ++e) x[e] = col[33 * lane + e];    // pad(32 l + e)
+    __syncwarp();
+    // round 2: len = 16 .. 1 on the lane's contiguous elements, twiddle w^(off << (9 - s)), off = e mod len
+#pragma unroll
+    for (int s = 4; s >= 0; --s) {
+      const int h = 1 << s;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        if (e & h) continue;
+        const int off = e & (h - 1);
+        if (off == 0) {
+          const uint32_t sm = x[e] + x[e + h], df = x[e] + q2 - x[e + h];
+          x[e] = min(sm, sm - q2);
+          x[e + h] = min(df, df - q2);
+        } else {
+          gs_bf(x[e], x[e + h], cf.f1[(1 << s) - s - 1 + off - 1], q2, q);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) col[32 * lane + e] = min(x[e], x[e] - q);   // position p, [0, q)
+  }
+  __syncthreads();
+  // digits: for each position p the 16 windows' words are 16 consecutive bytes of every digit plane
+  const uint32_t cnt = min(16u, n_ct - r0);
+  const uint64_t plane = (uint64_t)nbp * r_pad;
+  for (uint32_t i = threadIdx.x; i < 1024 * 16; i += 512) {
+    const uint32_t p = i >> 4, rl = i & 15;
+    if (rl >= cnt) continue;
+    int8_t* dst = out + ((size_t)p * D * nbp + m) * r_pad + r0 + rl;
+    const uint32_t v = xs[rl * kS2Ld + p];
+    const uint32_t c = v > (q >> 1) ? v - q : v;
+    const uint32_t wv = (c + 0x80808080u) ^ 0x80808080u;
+    for (int d = 0; d < D; ++d) dst[(size_t)d * plane] = (int8_t)(wv >> (8 * d));
   }
 }
 
@@ -831,6 +932,17 @@ cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out
 cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, uint32_t limb, const SpecTable& t,
                              int D, uint32_t r_pad, uint32_t ob, uint32_t nblk, uint32_t nbp, int8_t* out,
                              cudaStream_t s) {
+  if (t.L == 1024 && t.f2) {
+    dim3 grid(nblk, (n_ct + 15) / 16);
+    const size_t smem = (size_t)16 * kS2Ld * sizeof(uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(spec_data1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    SpecFwdConst cf;
+    cf.f2 = t.f2;
+    for (int i = 0; i < 26; ++i) cf.f1[i] = t.f1[i];
+    spec_data1024_kernel<<<grid, 512, smem, s>>>(ct, n_ct, limb, Rg.k, ob, nbp, Rg.N, t.q, D, r_pad, cf, out);
+    return cudaGetLastError();
+  }
   dim3 grid(nblk, (n_ct + kSpecRChunk - 1) / kSpecRChunk);
   const size_t smem = (size_t)kSpecRChunk * t.L * sizeof(uint32_t);
   if (smem > 48 * 1024) {
