@@ -37,6 +37,11 @@ struct Mods {
   uint32_t m[3];
   uint64_t mu[3];
 };
+HE_D uint32_t mulmod_b(uint32_t a, uint32_t b, uint64_t mu, uint32_t q) { return barrett64((uint64_t)a * b, mu, q); }
+// centred c (|c| < q 2^32) -> c mod q
+HE_D uint32_t lift_b(int64_t c, uint64_t mu, uint32_t q) {
+  return barrett64((uint64_t)(c + ((int64_t)q << 32)), mu, q);
+}
 Mods make_mods(const RingDims& R) {
   Mods M;
   M.m[0] = R.q[0];
@@ -89,28 +94,30 @@ __global__ void k_ksk_beta(const uint32_t* alpha, const uint32_t* s_new, uint32_
 // ------------------------------------------------------------------ key switching pieces (batched)
 // digits of c (coefficient form, per limb [2][cnt][n]) lifted to the other moduli:
 //   d_i = c_i * Qhat_i^-1 mod q_i;  D[j][i] = d_i mod m_j for j != i.  D[i][i] comes from the NTT form.
-__global__ void k_modup(const uint32_t* __restrict__ c, const uint32_t* __restrict__ T, uint32_t n, uint64_t cnt_n,
-                        uint32_t q0, uint32_t q1, uint32_t P, uint32_t qhinv0, uint32_t qhinv1, uint32_t* __restrict__ D) {
+__global__ void k_modup(const uint32_t* __restrict__ c, const uint32_t* __restrict__ T, uint32_t logn, uint64_t cnt_n,
+                        Mods M, uint32_t qhinv0, uint32_t qhinv1, uint32_t* __restrict__ D) {
   // D layout: [j (3)][i (2)][cnt * n];  T layout [L][cnt][2][n] (NTT form, a part = slot 0)
+  const uint32_t q0 = M.m[0], q1 = M.m[1], P = M.m[2];
+  const uint64_t nmask = (1ull << logn) - 1;
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t tix = (x / n) * 2 * n + x % n;
-    const uint32_t d0 = mul_mod(c[x], qhinv0, q0);
-    const uint32_t d1 = mul_mod(c[cnt_n + x], qhinv1, q1);
-    D[(0 * 2 + 1) * cnt_n + x] = d1 % q0;
-    D[(1 * 2 + 0) * cnt_n + x] = d0 % q1;
-    D[(2 * 2 + 0) * cnt_n + x] = d0 % P;
-    D[(2 * 2 + 1) * cnt_n + x] = d1 % P;
+    const uint64_t tix = ((x >> logn) << (logn + 1)) + (x & nmask);
+    const uint32_t d0 = mulmod_b(c[x], qhinv0, M.mu[0], q0);
+    const uint32_t d1 = mulmod_b(c[cnt_n + x], qhinv1, M.mu[1], q1);
+    D[(0 * 2 + 1) * cnt_n + x] = barrett64(d1, M.mu[0], q0);
+    D[(1 * 2 + 0) * cnt_n + x] = barrett64(d0, M.mu[1], q1);
+    D[(2 * 2 + 0) * cnt_n + x] = barrett64(d0, M.mu[2], P);
+    D[(2 * 2 + 1) * cnt_n + x] = barrett64(d1, M.mu[2], P);
     // own-modulus digits straight from the NTT form (NTT is linear mod q_i)
-    D[(0 * 2 + 0) * cnt_n + x] = mul_mod(T[tix], qhinv0, q0);
-    D[(1 * 2 + 1) * cnt_n + x] = mul_mod(T[2 * cnt_n + tix], qhinv1, q1);
+    D[(0 * 2 + 0) * cnt_n + x] = mulmod_b(T[tix], qhinv0, M.mu[0], q0);
+    D[(1 * 2 + 1) * cnt_n + x] = mulmod_b(T[2 * cnt_n + tix], qhinv1, M.mu[1], q1);
   }
 }
-// U[j] = sum_i D[j][i] * K[i][0][j],  W[j] = sum_i D[j][i] * K[i][1][j]   (NTT domain)
+// U[j] = sum_i D[j][i] * K[i][0][j],  W[j] = sum_i D[j][i] * K[i][1][j]   (NTT domain, n a power of two)
 // K layout [i][part][j][n];  UW layout [j][2][cnt][n]
 __global__ void k_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict__ K, uint32_t n, uint64_t cnt_n,
                       Mods M, uint32_t* __restrict__ UW) {
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = (uint32_t)(x % n);
+    const uint32_t c = (uint32_t)(x & (n - 1));
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       const uint64_t dd0 = D[(j * 2 + 0) * cnt_n + x], dd1 = D[(j * 2 + 1) * cnt_n + x];
@@ -122,13 +129,13 @@ __global__ void k_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict
   }
 }
 // ModDown, first half: centred lift of the (coefficient-form) P parts to q0, q1.  LB [j][2][cnt][n]
-__global__ void k_moddown_lift(const uint32_t* __restrict__ UWP, uint64_t cnt_n, uint32_t P, uint32_t q0, uint32_t q1,
-                               uint32_t* __restrict__ LB) {
+__global__ void k_moddown_lift(const uint32_t* __restrict__ UWP, uint64_t cnt_n, Mods M, uint32_t* __restrict__ LB) {
+  const uint32_t P = M.m[2];
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t v = UWP[x];
     const int64_t c = v > P / 2 ? (int64_t)v - P : (int64_t)v;
-    LB[x] = from_i64(c, q0);
-    LB[2 * cnt_n + x] = from_i64(c, q1);
+    LB[x] = lift_b(c, M.mu[0], M.m[0]);
+    LB[2 * cnt_n + x] = lift_b(c, M.mu[1], M.m[1]);
   }
 }
 
@@ -202,13 +209,12 @@ __global__ void k_rh_weights(const double* __restrict__ W, uint32_t n_out, uint3
 
 // rows [L][leaf][2][n] = sum_p Wpt[L][leaf][p][.] * pieces[L][p][ab][.]   (NTT domain)
 __global__ void k_rh_mvm(const uint32_t* __restrict__ Wpt, const uint32_t* __restrict__ pieces, uint64_t leaves,
-                         uint32_t p_in, uint32_t n, Mods M, uint32_t* __restrict__ rows) {
-  const uint64_t per_l = leaves * n;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * per_l; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t L = (uint32_t)(x / per_l);
-    const uint64_t y = x % per_l;
-    const uint64_t leaf = y / n;
-    const uint32_t c = (uint32_t)(y % n);
+                         uint32_t p_in, uint32_t logn, Mods M, uint32_t* __restrict__ rows) {
+  const uint32_t n = 1u << logn, L = blockIdx.y;
+  const uint64_t per_l = leaves << logn;
+  for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < per_l; y += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t leaf = y >> logn;
+    const uint32_t c = (uint32_t)(y & (n - 1));
     const uint32_t* w = Wpt + ((size_t)L * leaves + leaf) * p_in * n + c;
     const uint32_t* pc = pieces + (size_t)L * p_in * 2 * n + c;
     uint64_t acc_a = 0, acc_b = 0;
@@ -233,7 +239,7 @@ __global__ void k_rh_mvm(const uint32_t* __restrict__ Wpt, const uint32_t* __res
 // built in shared memory with coalesced global reads, then permuted out of it.
 __global__ void __launch_bounds__(512) k_pack_comb1(const uint32_t* __restrict__ A, uint32_t cnt_in, uint32_t half,
                                                     uint32_t n, const uint32_t* __restrict__ mono /* [2][n] */,
-                                                    const uint32_t* __restrict__ perm, uint32_t q0, uint32_t q1,
+                                                    const uint32_t* __restrict__ perm, Mods M,
                                                     uint32_t* __restrict__ An, uint32_t* __restrict__ T,
                                                     uint32_t* __restrict__ C) {
   extern __shared__ uint32_t sd[];  // [n]  E - M O
@@ -241,13 +247,14 @@ __global__ void __launch_bounds__(512) k_pack_comb1(const uint32_t* __restrict__
   const uint32_t idx = blockIdx.x, ab = blockIdx.y, L = blockIdx.z;
   const uint32_t o = idx / half, s_ = idx % half;
   const uint32_t e_i = o * 2 * half + s_, o_i = e_i + half;
-  const uint32_t q = L ? q1 : q0;
+  const uint32_t q = M.m[L];
+  const uint64_t mu = M.mu[L];
   const uint32_t* Eb = A + (((size_t)L * cnt_in + e_i) * 2 + ab) * n;
   const uint32_t* Ob = A + (((size_t)L * cnt_in + o_i) * 2 + ab) * n;
   const uint32_t* ml = mono + (size_t)L * n;
   uint32_t* un = An + (((size_t)L * cnt_out + idx) * 2 + ab) * n;
   for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
-    const uint32_t e = Eb[c], mo = mul_mod(Ob[c], ml[c], q);
+    const uint32_t e = Eb[c], mo = mulmod_b(Ob[c], ml[c], mu, q);
     un[c] = add_mod(e, mo, q);
     sd[c] = sub_mod(e, mo, q);
   }
@@ -262,16 +269,17 @@ __global__ void __launch_bounds__(512) k_pack_comb1(const uint32_t* __restrict__
 }
 // An += (u, T_b + w) with u = (U - LB_u) P^-1, w = (W - LB_w) P^-1   (NTT domain)
 __global__ void k_pack_comb2(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ LB,
-                             const uint32_t* __restrict__ T, uint32_t cnt, uint32_t n, uint32_t q0, uint32_t q1,
-                             uint32_t pinv0, uint32_t pinv1, uint32_t* __restrict__ An) {
-  const uint64_t cnt_n = (uint64_t)cnt * n;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t L = (uint32_t)(x / cnt_n);
-    const uint64_t y = x % cnt_n;
-    const uint32_t idx = (uint32_t)(y / n), c = (uint32_t)(y % n);
-    const uint32_t q = L ? q1 : q0, pinv = L ? pinv1 : pinv0;
-    const uint32_t u = mul_mod(sub_mod(UW[(L * 2 + 0) * cnt_n + y], LB[(L * 2 + 0) * cnt_n + y], q), pinv, q);
-    const uint32_t w = mul_mod(sub_mod(UW[(L * 2 + 1) * cnt_n + y], LB[(L * 2 + 1) * cnt_n + y], q), pinv, q);
+                             const uint32_t* __restrict__ T, uint32_t cnt, uint32_t logn, Mods M, uint32_t pinv0,
+                             uint32_t pinv1, uint32_t* __restrict__ An) {
+  const uint32_t n = 1u << logn, L = blockIdx.y;
+  const uint64_t cnt_n = (uint64_t)cnt << logn;
+  const uint32_t q = M.m[L], pinv = L ? pinv1 : pinv0;
+  const uint64_t mu = M.mu[L];
+  for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < cnt_n; y += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t idx = y >> logn;
+    const uint32_t c = (uint32_t)(y & (n - 1));
+    const uint32_t u = mulmod_b(sub_mod(UW[(L * 2 + 0) * cnt_n + y], LB[(L * 2 + 0) * cnt_n + y], q), pinv, mu, q);
+    const uint32_t w = mulmod_b(sub_mod(UW[(L * 2 + 1) * cnt_n + y], LB[(L * 2 + 1) * cnt_n + y], q), pinv, mu, q);
     uint32_t* dst = An + (((size_t)L * cnt + idx) * 2) * n + c;
     const uint32_t tb = T[(((size_t)L * cnt + idx) * 2 + 1) * n + c];
     dst[0] = add_mod(dst[0], u, q);
@@ -535,7 +543,11 @@ extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct
     HE_CUDA(ntt_forward(c->ntt_rh[L], w.pieces + (size_t)L * p->p_in * 2 * n, p->p_in * 2, n, st), "NTT(pieces)");
   // (M) row ciphertexts
   const uint64_t leaves = leaves_of(p);
-  k_rh_mvm<<<grid_for(2 * leaves * n), 256, 0, st>>>(p->wpt, w.pieces, leaves, p->p_in, n, p->M, w.A0);
+  {
+    dim3 g = grid_for(leaves * n);
+    g.y = 2;
+    k_rh_mvm<<<g, 256, 0, st>>>(p->wpt, w.pieces, leaves, p->p_in, p->logn, p->M, w.A0);
+  }
   // (P) PackLWEs, one batched level at a time
   uint32_t* A = w.A0;
   uint32_t* An = w.A1;
@@ -546,18 +558,22 @@ extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct
     const uint32_t cnt_out = cnt / 2, half = n >> lv;
     const uint64_t cn = (uint64_t)cnt_out * n;
     k_pack_comb1<<<dim3(cnt_out, 2, 2), 512, n * sizeof(uint32_t), st>>>(
-        A, cnt, half, n, mono_base + (size_t)(lv - 1) * 2 * n, perm_base + (size_t)(lv - 1) * n, q0, q1, An, w.T, w.C);
+        A, cnt, half, n, mono_base + (size_t)(lv - 1) * 2 * n, perm_base + (size_t)(lv - 1) * n, p->M, An, w.T, w.C);
     for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt_rh[L], w.C + (size_t)L * cn, cnt_out, n, st), "INTT(T_a)");
-    k_modup<<<grid_for(cn), 256, 0, st>>>(w.C, w.T, n, cn, q0, q1, P, p->qhinv[0], p->qhinv[1], w.D);
+    k_modup<<<grid_for(cn), 256, 0, st>>>(w.C, w.T, p->logn, cn, p->M, p->qhinv[0], p->qhinv[1], w.D);
     HE_CUDA(ntt_forward(c->ntt_rh[0], w.D + (0 * 2 + 1) * cn, cnt_out, n, st), "NTT(d1 mod q0)");
     HE_CUDA(ntt_forward(c->ntt_rh[1], w.D + (1 * 2 + 0) * cn, cnt_out, n, st), "NTT(d0 mod q1)");
     HE_CUDA(ntt_forward(c->ntt_rh[2], w.D + (2 * 2 + 0) * cn, 2 * cnt_out, n, st), "NTT(d mod P)");
     k_mac<<<grid_for(cn), 256, 0, st>>>(w.D, gal + (size_t)(lv - 1) * 12 * n, n, cn, p->M, w.UW);
     HE_CUDA(ntt_inverse(c->ntt_rh[2], w.UW + 2 * 2 * cn, 2 * cnt_out, n, st), "INTT(U_P, W_P)");
-    k_moddown_lift<<<grid_for(2 * cn), 256, 0, st>>>(w.UW + 2 * 2 * cn, cn, P, q0, q1, w.LB);
+    k_moddown_lift<<<grid_for(2 * cn), 256, 0, st>>>(w.UW + 2 * 2 * cn, cn, p->M, w.LB);
     HE_CUDA(ntt_forward(c->ntt_rh[0], w.LB, 2 * cnt_out, n, st), "NTT(lift q0)");
     HE_CUDA(ntt_forward(c->ntt_rh[1], w.LB + 2 * cn, 2 * cnt_out, n, st), "NTT(lift q1)");
-    k_pack_comb2<<<grid_for(2 * cn), 256, 0, st>>>(w.UW, w.LB, w.T, cnt_out, n, q0, q1, p->pinv[0], p->pinv[1], An);
+    {
+      dim3 g = grid_for(cn);
+      g.y = 2;
+      k_pack_comb2<<<g, 256, 0, st>>>(w.UW, w.LB, w.T, cnt_out, p->logn, p->M, p->pinv[0], p->pinv[1], An);
+    }
     uint32_t* tmp = A;
     A = An;
     An = (lv == 1) ? w.A0 : tmp;  // level 1 frees A0 for reuse as the next output
