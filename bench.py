@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--algo", choices=["spectral", "direct"], default="spectral",
                     help="a'-column algorithm (same output words): K7 spectral (default) or K1 direct GEMM")
     ap.add_argument("--no-direct", action="store_true", help="skip the side measurement of the direct K1 path")
+    ap.add_argument("--no-fused", action="store_true", help="N > 1: NCCL all-gather instead of the fused peer stores")
     ap.add_argument("--cpu-rows", type=int, default=64, help="oracle sample rows for cpu_baseline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -142,7 +143,8 @@ def run_ours(a, rank: int, world: int, local: int):
     from paper_2601_18511_b200 import HeContext, make_mlwe_pcmm_plan, pcmm_mlwe
     from paper_2601_18511_b200.context import MlweBlocks
     from paper_2601_18511_b200.pcmm import pcmm_ops, spectral_gemm_ops, spectral_inverse_bytes
-    from paper_2601_18511_b200.sharding import row_shards, shard_slots
+    from paper_2601_18511_b200.sharding import (pcmm_mlwe_sharded_fused, row_shards, shard_slots,
+                                                symmetric_outputs)
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -168,6 +170,7 @@ def run_ours(a, rank: int, world: int, local: int):
     out_b = torch.empty((per, N), dtype=torch.int32, device=dev)
     out_a = torch.empty((per * k, N), dtype=torch.int32, device=dev)
     Y = MlweBlocks(out_b[: b1 - b0], out_a[:rows], level=0, n_rows=rows)
+    sym = symmetric_outputs(ctx, n_out) if world > 1 and not a.no_fused else None
     if world > 1:
         all_b = torch.empty((per * world, N), dtype=torch.int32, device=dev)
         all_a = torch.empty((per * world * k, N), dtype=torch.int32, device=dev)
@@ -177,6 +180,9 @@ def run_ours(a, rank: int, world: int, local: int):
     stream = torch.cuda.current_stream(dev)
 
     def step():
+        if sym is not None:   # output all-gather fused into the kernels' stores (peer memory over NVLink)
+            pcmm_mlwe_sharded_fused(ctx, plan, X, n_out, b0 * k, sym)
+            return
         if world > 1:
             dist.broadcast(X.data, src=0)
         pcmm_mlwe(ctx, plan, X, out=Y)
@@ -265,7 +271,9 @@ def run_ours(a, rank: int, world: int, local: int):
                        "digits": {"weight": plan.d_w, "ct_q0": d0, "ct_q1": d1},
                        "algo": a.algo + (" (K7: a' by blockwise NTT correlation + per-frequency tcgen05 GEMMs; "
                               "b' on K1)" if a.algo == "spectral" else " (K1 over all columns)"),
-                       "parallelism": f"row-shard x{world}" + (" + NCCL bcast/all-gather" if world > 1 else ""),
+                       "parallelism": f"row-shard x{world}" + (
+                           "" if world == 1 else " + NCCL bcast + output all-gather fused into the kernels' peer "
+                           "stores (symmetric memory)" if sym is not None else " + NCCL bcast/all-gather"),
                        "l2": "inputs larger than L2: each op writes and reads a "
                              f"{plan.workspace_bytes() / 1e9:.2f} GB workspace"},
             "roofline": roof,

@@ -127,6 +127,15 @@ he_status he_pcmm_gemm(const he_pcmm_plan* plan, const void* workspace_dev, uint
  * host memory chunk by chunk while the next chunk computes (pcmm_mlwe_to_host). */
 he_status he_pcmm_gemm_rows(const he_pcmm_plan* plan, const void* workspace_dev, uint32_t row0, uint32_t rows,
                             uint32_t* out_b_dev, uint32_t* out_a_dev, void* stream);
+/* Fused output all-gather (row-sharded multi-GPU): like he_pcmm_gemm_rows, but the
+ * output stage stores every word into each of the n_peers (<= 8) FULL output buffers -- device pointers
+ * reachable from this GPU (peer memory over NVLink: CUDA IPC / symmetric memory) -- at destination rows
+ * dst_row0 + (y - row0), so the all-gather rides on the kernels' own stores instead of a separate
+ * collective.  out_*_peers are HOST arrays of device pointers (b' [n_out/k][N], a' [n_out][k*d] each).
+ * Spectral plans need the L = 1024 path (k = 256). */
+he_status he_pcmm_gemm_rows_peers(const he_pcmm_plan* plan, const void* workspace_dev, uint32_t row0, uint32_t rows,
+                                  uint32_t* const* out_b_peers, uint32_t* const* out_a_peers, uint32_t n_peers,
+                                  uint32_t dst_row0, void* stream);
 /* Spectral a-part (K7, same output words): the plan's a' columns are computed as blockwise
  * length-2k cyclic NTT correlations instead of the d*k-column GEMM (b' columns stay on K1).
  * Step 1 reports the bytes of the spectral weights G^ (caller-allocated device memory, kept

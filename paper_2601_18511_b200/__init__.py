@@ -9,7 +9,8 @@ from .errors import NeedsBootstrapError
 from .params import HeParams
 from .context import CostLedger, CtBlocks, HeContext, MlweBlocks, SecretKey, LEDGER_COUNTERS
 from .layout import bit_reverse, byte_mix, half_reverse, rotate_bits_down, shuffle_matrix, sigma_table
-from .pcmm import MlwePcmmPlan, clear_pcmm, make_mlwe_pcmm_plan, pcmm_mlwe, pcmm_mlwe_to_host
+from .pcmm import (MlwePcmmPlan, clear_pcmm, make_mlwe_pcmm_plan, pcmm_mlwe, pcmm_mlwe_into_peers,
+                   pcmm_mlwe_to_host)
 from .rhombus import (CtVector, RhombusKeys, RhombusPlan, clear_pcmv, decrypt_vector, encrypt_vector,
                       make_rhombus_plan, pcmv_rhombus, rhombus_keygen)
 
@@ -17,6 +18,7 @@ __all__ = [
     "NeedsBootstrapError", "HeParams", "CostLedger", "CtBlocks", "HeContext", "MlweBlocks", "SecretKey",
     "LEDGER_COUNTERS", "bit_reverse", "byte_mix", "half_reverse", "rotate_bits_down", "shuffle_matrix",
     "sigma_table", "MlwePcmmPlan", "clear_pcmm", "make_mlwe_pcmm_plan", "pcmm_mlwe", "pcmm_mlwe_to_host",
+    "pcmm_mlwe_into_peers",
     "CtVector", "RhombusKeys", "RhombusPlan", "clear_pcmv", "decrypt_vector", "encrypt_vector",
     "make_rhombus_plan", "pcmv_rhombus", "rhombus_keygen",
 ]

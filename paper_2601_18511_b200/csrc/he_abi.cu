@@ -485,7 +485,7 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
 
 // K7 S3 (per-frequency tcgen05 GEMM, both limbs) + S4 (inverse, rescale, a' store) on rows [row0, row0 + rows)
 static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows, uint32_t* out_a,
-                           cudaStream_t st) {
+                           const OutPeers& peers, cudaStream_t st) {
   const SpecWs w = spec_ws(p);
   const int8_t* base = (const int8_t*)ws;
   static const bool simple = getenv("HE_SPEC_SIMPLE") != nullptr;  // debug: S3 on CUDA cores
@@ -534,15 +534,15 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
   c.q1inv = p->epi.q1inv;
   c.q1invp = p->epi.q1invp;
   p->prof_begin(5, st);
-  HE_CUDA(launch_spec_inverse(p->ctx->R, C[0], C[1], p->n_out, row0, rows, p->L, p->nblk, p->nbp, c, out_a, st),
+  HE_CUDA(launch_spec_inverse(p->ctx->R, C[0], C[1], p->n_out, row0, rows, p->L, p->nblk, p->nbp, c, out_a, peers, st),
           "spectral inverse");
   p->prof_end(5, st);
   return HE_OK;
 }
 
-extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows,
-                                       uint32_t* out_b, uint32_t* out_a, void* stream) {
-  if (!p || !ws || !out_b || !out_a) return fail(HE_EINVAL, "null argument");
+static he_status gemm_rows_impl(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows, uint32_t* out_b,
+                                uint32_t* out_a, const OutPeers& peers, void* stream) {
+  if (!p || !ws || (peers.n == 0 && (!out_b || !out_a))) return fail(HE_EINVAL, "null argument");
   if (rows == 0 || row0 % p->ctx->R.k || rows % p->ctx->R.k || row0 + rows > p->n_out)
     return fail(HE_EINVAL, "row range [%u, %u) must be k-aligned and inside [0, %u)", row0, row0 + rows, p->n_out);
   const int variant = p->algo == 1 ? 2 : gemm_variant();
@@ -592,6 +592,7 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
   a.k = (int)p->ctx->R.k;
   a.out_b = out_b;
   a.out_a = out_a;
+  a.peers = peers;
   a.c = p->epi;
   a.group_m = env_gm > 0 ? env_gm : 8;
   a.tile_n = bn2;
@@ -615,8 +616,34 @@ extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, ui
   HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, tmA, tmB, tmBa, a, grid, (cudaStream_t)stream),
           "modgemm");
   p->prof_end(2, (cudaStream_t)stream);
-  if (spec) return spec_rows(p, ws, row0, rows, out_a, (cudaStream_t)stream);
+  if (spec) return spec_rows(p, ws, row0, rows, out_a, peers, (cudaStream_t)stream);
   return HE_OK;
+}
+
+extern "C" he_status he_pcmm_gemm_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows,
+                                       uint32_t* out_b, uint32_t* out_a, void* stream) {
+  OutPeers none{};
+  none.n = 0;
+  return gemm_rows_impl(p, ws, row0, rows, out_b, out_a, none, stream);
+}
+
+extern "C" he_status he_pcmm_gemm_rows_peers(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows,
+                                             uint32_t* const* out_b_peers, uint32_t* const* out_a_peers,
+                                             uint32_t n_peers, uint32_t dst_row0, void* stream) {
+  if (!p || !out_b_peers || !out_a_peers) return fail(HE_EINVAL, "null argument");
+  if (n_peers < 1 || n_peers > (uint32_t)kMaxPeers) return fail(HE_EINVAL, "n_peers must be in [1, %d]", kMaxPeers);
+  if (dst_row0 % p->ctx->R.k) return fail(HE_EINVAL, "dst_row0 (%u) must be a multiple of k", dst_row0);
+  if (p->algo == 1 && p->L != 1024)
+    return fail(HE_EINVAL, "fused peer output needs the L = 1024 spectral path or the direct path");
+  OutPeers pe{};
+  pe.n = (int)n_peers;
+  pe.dst_row0 = dst_row0;
+  for (uint32_t i = 0; i < n_peers; ++i) {
+    if (!out_b_peers[i] || !out_a_peers[i]) return fail(HE_EINVAL, "null peer pointer %u", i);
+    pe.a[i] = out_a_peers[i];
+    pe.b[i] = out_b_peers[i];
+  }
+  return gemm_rows_impl(p, ws, row0, rows, nullptr, nullptr, pe, stream);
 }
 
 extern "C" he_status he_pcmm_gemm(const he_pcmm_plan* p, const void* ws, uint32_t* out_b, uint32_t* out_a,

@@ -20,6 +20,16 @@ struct GemmEpiConst {
   uint64_t mu[2];       // floor(2^64 / q) (Barrett)
 };
 
+// fused output all-gather: the output stage stores every word into each rank's full output buffer (peer
+// device pointers, e.g. from CUDA IPC / symmetric memory over NVLink) at destination row dst_row0 + local row
+constexpr int kMaxPeers = 8;
+struct OutPeers {
+  uint32_t* a[kMaxPeers];
+  uint32_t* b[kMaxPeers];
+  int n;                 // 0: plain local output (out_a / out_b)
+  uint32_t dst_row0;     // k-aligned
+};
+
 struct GemmArgs {
   int n_out, n_in, width, d, k;
   int group_m;          // raster: pair-rows per group (v2)
@@ -29,6 +39,7 @@ struct GemmArgs {
   int fused;            // 1: B tiles come straight from the compact digit planes (K3 fused into K1)
   uint32_t* out_b;
   uint32_t* out_a;
+  OutPeers peers;
   GemmEpiConst c;
 };
 
@@ -99,7 +110,7 @@ cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& t
 cudaError_t launch_spec_gemm_simple(int D, const int8_t* G, const int8_t* A, const SpecGemmArgs& a, cudaStream_t s);
 cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const uint32_t* c1, uint32_t n_out,
                                 uint32_t row0, uint32_t rows, uint32_t L, uint32_t nblk, uint32_t nbp,
-                                const SpecInvConst& cst, uint32_t* out_a, cudaStream_t s);
+                                const SpecInvConst& cst, uint32_t* out_a, const OutPeers& peers, cudaStream_t s);
 cudaError_t launch_digitize(const RingDims& R, const uint32_t* ct, uint32_t n_ct, int d0, int d1, uint32_t S,
                             int8_t* out_a, int8_t* out_b, cudaStream_t s);
 cudaError_t launch_weight_maxabs(const RingDims& R, const double* W, uint32_t n_out, uint32_t n_in,

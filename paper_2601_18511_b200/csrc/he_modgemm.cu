@@ -529,14 +529,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           res[e] = shoup_mul(t, c.q1inv, c.q1invp, c.q[0]);
         }
         if (row_ok) {
-          if (n < args.d) {
-            uint32_t* dst = args.out_b + (size_t)(y / args.k) * N + (y % args.k);
+          const int np = args.peers.n > 0 ? args.peers.n : 1;
+          const size_t yd = args.peers.n > 0 ? (size_t)args.peers.dst_row0 + y : (size_t)y;
+          for (int pr = 0; pr < np; ++pr) {
+            if (n < args.d) {
+              uint32_t* ob = args.peers.n > 0 ? args.peers.b[pr] : args.out_b;
+              uint32_t* dst = ob + (yd / args.k) * N + (yd % args.k);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) dst[(size_t)args.k * (n + e)] = res[e];
-          } else {
-            uint4* dst = reinterpret_cast<uint4*>(args.out_a + (size_t)y * N + (n - args.d));
-            dst[0] = make_uint4(res[0], res[1], res[2], res[3]);
-            dst[1] = make_uint4(res[4], res[5], res[6], res[7]);
+              for (int e = 0; e < 8; ++e) dst[(size_t)args.k * (n + e)] = res[e];
+            } else {
+              uint32_t* oa = args.peers.n > 0 ? args.peers.a[pr] : args.out_a;
+              uint4* dst = reinterpret_cast<uint4*>(oa + yd * N + (n - args.d));
+              dst[0] = make_uint4(res[0], res[1], res[2], res[3]);
+              dst[1] = make_uint4(res[4], res[5], res[6], res[7]);
+            }
           }
         }
       }

@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
                                                                   const uint32_t* __restrict__ c1, uint32_t n_out,
                                                                   uint32_t row0, uint32_t nbp, uint32_t nblk,
                                                                   uint32_t d, SpecInvConst cst,
-                                                                  uint32_t* __restrict__ out_a) {
+                                                                  uint32_t* __restrict__ out_a, OutPeers peers) {
   extern __shared__ uint32_t sm[];
   uint32_t* xs0 = sm;                                  // [8 blocks][1060]
   uint32_t* xs1 = sm + kInv1kBlocks * kInv1kLd;
@@ -623,13 +623,25 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
   __syncthreads();
   // phase C: block b covers c' = 768 (b0 + b) + u  <->  m = 3 (b0 + b) + u / 256, j = 255 - u % 256
   const uint32_t N = d * 256, mbase = 3 * b0;
-  uint32_t* dst = out_a + (size_t)(y - row0) * N;
-  for (uint32_t i = threadIdx.x; i < 24 * 256; i += 256) {
-    const uint32_t ml = i % 24, j = i / 24;
-    const uint32_t m = mbase + ml;
-    if (m >= d) continue;
-    const uint32_t bl = ml / 3, u = 256 * (ml - 3 * bl) + 255 - j;
-    dst[(size_t)d * j + m] = xs1[bl * kInv1kLd + u];
+  if (peers.n == 0) {
+    uint32_t* dst = out_a + (size_t)(y - row0) * N;
+    for (uint32_t i = threadIdx.x; i < 24 * 256; i += 256) {
+      const uint32_t ml = i % 24, j = i / 24;
+      const uint32_t m = mbase + ml;
+      if (m >= d) continue;
+      const uint32_t bl = ml / 3, u = 256 * (ml - 3 * bl) + 255 - j;
+      dst[(size_t)d * j + m] = xs1[bl * kInv1kLd + u];
+    }
+  } else {  // fused all-gather: the same words into every rank's full output at row dst_row0 + (y - row0)
+    const size_t yd = (size_t)peers.dst_row0 + (y - row0);
+    for (uint32_t i = threadIdx.x; i < 24 * 256; i += 256) {
+      const uint32_t ml = i % 24, j = i / 24;
+      const uint32_t m = mbase + ml;
+      if (m >= d) continue;
+      const uint32_t bl = ml / 3, u = 256 * (ml - 3 * bl) + 255 - j;
+      const uint32_t v = xs1[bl * kInv1kLd + u];
+      for (int pr = 0; pr < peers.n; ++pr) peers.a[pr][yd * N + (size_t)d * j + m] = v;
+    }
   }
 }
 
@@ -955,14 +967,15 @@ cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_
 
 cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const uint32_t* c1, uint32_t n_out,
                                 uint32_t row0, uint32_t rows, uint32_t L, uint32_t nblk, uint32_t nbp,
-                                const SpecInvConst& cst, uint32_t* out_a, cudaStream_t s) {
+                                const SpecInvConst& cst, uint32_t* out_a, const OutPeers& peers, cudaStream_t s) {
+  if (peers.n > 0 && L != 1024) return cudaErrorNotSupported;  // fused output only on the L = 1024 fast path
   if (L == 1024) {
     if (Rg.k != 256) return cudaErrorInvalidValue;
     dim3 grid((nblk + kInv1kBlocks - 1) / kInv1kBlocks, rows);
     const size_t smem = (size_t)2 * kInv1kBlocks * kInv1kLd * sizeof(uint32_t);
     cudaError_t e = cudaFuncSetAttribute(spec_inverse1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    spec_inverse1024_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, nbp, nblk, Rg.d, cst, out_a);
+    spec_inverse1024_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, nbp, nblk, Rg.d, cst, out_a, peers);
     return cudaGetLastError();
   }
   static const bool generic = getenv("HE_SPEC_INV_GENERIC") != nullptr;  // debug: the simple S4

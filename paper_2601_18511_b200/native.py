@@ -28,7 +28,7 @@ EXPORTS = (
     "he_encrypt_vector", "he_rhombus_keygen", "he_rhombus_weight_bytes", "he_rhombus_encode_weights",
     "he_rhombus_plan_create", "he_rhombus_plan_destroy", "he_rhombus_workspace_bytes", "he_rhombus_run",
     "he_pcmm_gemm_rows", "he_pcmm_spectral_weight_bytes", "he_pcmm_spectral_prepare", "he_pcmm_algo",
-    "he_pcmm_profile", "he_pcmm_profile_read", "he_pcmm_spectral_info",
+    "he_pcmm_profile", "he_pcmm_profile_read", "he_pcmm_spectral_info", "he_pcmm_gemm_rows_peers",
 )
 
 
@@ -82,6 +82,7 @@ def lib():
             "he_pcmm_decompose": (st, [vp, vp, vp, u64, vp]),
             "he_pcmm_gemm": (st, [vp, vp, vp, vp, vp]),
             "he_pcmm_gemm_rows": (st, [vp, vp, u32, u32, vp, vp, vp]),
+            "he_pcmm_gemm_rows_peers": (st, [vp, vp, u32, u32, ctypes.POINTER(vp), ctypes.POINTER(vp), u32, u32, vp]),
             "he_pcmm_spectral_weight_bytes": (st, [vp, ctypes.POINTER(u64)]),
             "he_pcmm_spectral_prepare": (st, [vp, vp, vp]),
             "he_pcmm_algo": (st, [vp, ctypes.POINTER(ctypes.c_int)]),

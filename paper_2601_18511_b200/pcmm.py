@@ -199,6 +199,28 @@ def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks |
     return out
 
 
+def pcmm_mlwe_into_peers(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_ptrs, out_a_ptrs,
+                         dst_row0: int) -> None:
+    """This rank's rows of the op with the output all-gather fused into the output stage: every
+    word is stored into each pointer pair of ``out_b_ptrs`` / ``out_a_ptrs`` -- the FULL output
+    buffers of all ranks (peer memory over NVLink, e.g. symmetric memory) -- at rows
+    ``dst_row0 + y`` (he_pcmm_gemm_rows_peers).  Same ledger effect as pcmm_mlwe."""
+    _check_operand(ctx, plan, X)
+    n = len(out_a_ptrs)
+    if n != len(out_b_ptrs) or not 1 <= n <= 8:
+        raise ValueError("need 1..8 peer output pointer pairs")
+    ws = plan.workspace(ctx.device)
+    st = ctx.stream()
+    native.call("he_pcmm_decompose", plan._handle, X.data.data_ptr(), ws.data_ptr(), ws.numel(), st)
+    pb = (ctypes.c_void_p * n)(*[int(v) for v in out_b_ptrs])
+    pa = (ctypes.c_void_p * n)(*[int(v) for v in out_a_ptrs])
+    native.call("he_pcmm_gemm_rows_peers", plan._handle, ws.data_ptr(), 0, plan.n_out, pb, pa, n, dst_row0, st)
+    k = ctx.params.mlwe_rank
+    ctx.ledger.pc_mults += (plan.n_out // k) * (plan.n_in // k)
+    ctx.ledger.rescales += plan.n_out // k
+    ctx.ledger.observe_level(X.level - 1)
+
+
 def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_host, out_a_host,
                       x_host=None, chunk_rows: int = 512) -> MlweBlocks:
     """The same op as ``pcmm_mlwe`` with the level-0 output streamed into (pinned) host

@@ -70,6 +70,41 @@ def gather_row_shards(local_b, local_a, k: int, n_out: int, group=None):
     return keep_b, keep_a
 
 
+def symmetric_outputs(ctx, n_out: int, group=None):
+    """Full-size output buffers in symmetric (peer-mappable) memory plus every rank's pointers to them,
+    or None when symmetric memory is unavailable (no NVLink P2P, single rank, older torch)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return None
+    try:
+        import torch.distributed._symmetric_memory as symm
+
+        p = ctx.params
+        grp = group if group is not None else dist.group.WORLD
+        out_b = symm.empty((n_out // p.mlwe_rank, p.N), dtype=torch.int32, device=ctx.device)
+        out_a = symm.empty((n_out, p.N), dtype=torch.int32, device=ctx.device)
+        hb = symm.rendezvous(out_b, grp)
+        ha = symm.rendezvous(out_a, grp)
+        return out_b, out_a, list(hb.buffer_ptrs), list(ha.buffer_ptrs), hb
+    except Exception:  # pragma: no cover - depends on the box
+        return None
+
+
+def pcmm_mlwe_sharded_fused(ctx, plan, X, n_out: int, row0: int, sym, group=None):
+    """Row-sharded op with the output all-gather fused into the kernels' stores: this rank's rows
+    [row0, row0 + plan.n_out) go straight into every rank's full output (symmetric memory over
+    NVLink, ``sym`` from symmetric_outputs); a barrier on the symmetric handle publishes them."""
+    from .pcmm import pcmm_mlwe_into_peers
+
+    out_b, out_a, ptr_b, ptr_a, handle = sym
+    broadcast_input(X.data, group)
+    pcmm_mlwe_into_peers(ctx, plan, X, ptr_b, ptr_a, row0)
+    handle.barrier()
+    return out_b, out_a
+
+
 def pcmm_mlwe_sharded(ctx, plan, X, n_out: int, group=None, out_b=None, out_a=None):
     """Run this rank's shard (``plan`` holds rows [b0*k, b1*k) of W) between the input
     broadcast and the output all-gather.  Returns the gathered (out_b, out_a)."""

@@ -314,3 +314,37 @@ def test_spectral_transform_length_512_subprocess():
     env = dict(os.environ, HE_SPEC_L="512")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_fused_peer_output_writes_every_destination(algo):
+    """he_pcmm_gemm_rows_peers (the fused output all-gather): the shard's words land, identical to
+    pcmm_mlwe's, in every one of several full-size destination buffers at rows dst_row0 + y; rows
+    outside the shard are untouched.  (Two local buffers stand in for two ranks' peer memory.)"""
+    import torch
+
+    from paper_2601_18511_b200 import pcmm_mlwe_into_peers
+
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, 512, 1024, seed=6)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
+    ref = pcmm_mlwe(ctx, plan, X)
+    ref_a, ref_b = ref.out_a.clone(), ref.out_b.clone()
+    n_full, row0, k = 1536, 768, P.mlwe_rank
+    dst = [(torch.full((n_full // k, P.N), -7, dtype=torch.int32, device="cuda"),
+            torch.full((n_full, P.N), -7, dtype=torch.int32, device="cuda")) for _ in range(2)]
+    pcmm_mlwe_into_peers(ctx, plan, X, [b.data_ptr() for b, _ in dst], [a.data_ptr() for _, a in dst], row0)
+    torch.cuda.synchronize()
+    for b, a in dst:
+        assert torch.equal(a[row0:row0 + 512], ref_a) and torch.equal(b[row0 // k:(row0 + 512) // k], ref_b)
+        assert bool((a[:row0] == -7).all()) and bool((a[row0 + 512:] == -7).all())
+        assert bool((b[:row0 // k] == -7).all()) and bool((b[(row0 + 512) // k:] == -7).all())
+
+
+def test_fused_sharded_symmetric_memory_single_rank():
+    """The symmetric-memory fused path degrades to None at world size 1 (plain local output)."""
+    from paper_2601_18511_b200.sharding import symmetric_outputs
+
+    P = HeParams.llama()
+    ctx = HeContext(P)
+    assert symmetric_outputs(ctx, 512) is None
