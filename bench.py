@@ -88,8 +88,8 @@ class ClockSampler:
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index: int, period: float = 0.005):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+    def __init__(self, index: int, period: float = 0.002):
+        self.samples, self.reasons, self.max_mhz, self._raw = [], set(), None, []
         self._stop = threading.Event()
         self.ok = False
         try:
@@ -109,14 +109,21 @@ class ClockSampler:
         nv = self._nv
         while not self._stop.is_set():
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                t = time.perf_counter()
+                mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and bit != 0x1:
-                        self.reasons.add(name)
+                self._raw.append((t, mhz, mask))
             except Exception:
                 pass
             self._stop.wait(self.period)
+
+    def window(self, t0: float, t1: float):
+        """Keep the samples taken inside the host-time window [t0, t1] (the timed region)."""
+        inside = [r for r in self._raw if t0 <= r[0] <= t1]
+        if not inside and self._raw:   # a region shorter than one sampling period: nearest sample
+            inside = [min(self._raw, key=lambda r: abs(r[0] - (t0 + t1) / 2))]
+        self.samples = [r[1] for r in inside]
+        self.reasons = {name for _, _, mask in inside for bit, name in self.REASONS.items() if mask & bit and bit != 0x1}
 
     def __enter__(self):
         if self.ok:
@@ -198,12 +205,16 @@ def run_ours(a, rank: int, world: int, local: int):
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     plan.profile(True)            # per-stage CUDA events on the launching stream (he_pcmm_profile)
     with ClockSampler(local) as clk:
+        time.sleep(0.05)          # sampler at its steady rate before the timed region opens
         torch.cuda.synchronize()
+        h0 = time.perf_counter()
         t0.record(stream)
         for i in range(a.steps):
             step()
         t1.record(stream)
         torch.cuda.synchronize()
+        h1 = time.perf_counter()
+    clk.window(h0, h1)
     ms = t0.elapsed_time(t1) / a.steps
     stages = plan.profile_read()
     plan.profile(False)
