@@ -146,75 +146,98 @@ __global__ void __launch_bounds__(256) ntt_inv_cols(uint32_t* __restrict__ data,
 // smem index padding: one word per 32 to break the power-of-two strides
 HE_D uint32_t pad(uint32_t i) { return i + (i >> 5); }
 
-// One radix-16 round = 4 CT stages on the 16 elements j0 + e*T of this thread (t = 8T .. T).
+// One radix-16 round = 4 CT stages on the 16 elements j0 + e*T of this thread (t = 8T .. T), for NP
+// transforms at once (same twiddles: NP polys of one batch, block b of each) -- NP-fold ILP per load.
 // i0: group index of the thread's 16T block at the round's first stage, m0 = n / (16 T).
-HE_D void ct_round16(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t m0, uint32_t i0, uint32_t q2, uint32_t q) {
+template <int NP>
+HE_D void ct_round16(uint32_t (&x)[NP][16], const uint2* __restrict__ tw, uint32_t m0, uint32_t i0, uint32_t q2,
+                     uint32_t q) {
   {
     const uint2 w = __ldg(tw + m0 + i0);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ct_bf(x[e], x[e + 8], w, q2, q);
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) ct_bf(x[p][e], x[p][e + 8], w, q2, q);
   }
   {
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(tw + 2 * m0 + 2 * i0));
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      ct_bf(x[e], x[e + 4], make_uint2(w.x, w.y), q2, q);
-      ct_bf(x[8 + e], x[12 + e], make_uint2(w.z, w.w), q2, q);
-    }
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        ct_bf(x[p][e], x[p][e + 4], make_uint2(w.x, w.y), q2, q);
+        ct_bf(x[p][8 + e], x[p][12 + e], make_uint2(w.z, w.w), q2, q);
+      }
   }
   {
-    const uint4* p = reinterpret_cast<const uint4*>(tw + 4 * m0 + 4 * i0);
-    const uint4 wa = __ldg(p), wb = __ldg(p + 1);
+    const uint4* pp = reinterpret_cast<const uint4*>(tw + 4 * m0 + 4 * i0);
+    const uint4 wa = __ldg(pp), wb = __ldg(pp + 1);
     const uint2 ws[4] = {make_uint2(wa.x, wa.y), make_uint2(wa.z, wa.w), make_uint2(wb.x, wb.y), make_uint2(wb.z, wb.w)};
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      ct_bf(x[4 * g], x[4 * g + 2], ws[g], q2, q);
-      ct_bf(x[4 * g + 1], x[4 * g + 3], ws[g], q2, q);
-    }
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        ct_bf(x[p][4 * g], x[p][4 * g + 2], ws[g], q2, q);
+        ct_bf(x[p][4 * g + 1], x[p][4 * g + 3], ws[g], q2, q);
+      }
   }
   {
-    const uint4* p = reinterpret_cast<const uint4*>(tw + 8 * m0 + 8 * i0);
+    const uint4* pp = reinterpret_cast<const uint4*>(tw + 8 * m0 + 8 * i0);
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
-      const uint4 w = __ldg(p + h);
-      ct_bf(x[4 * h], x[4 * h + 1], make_uint2(w.x, w.y), q2, q);
-      ct_bf(x[4 * h + 2], x[4 * h + 3], make_uint2(w.z, w.w), q2, q);
+      const uint4 w = __ldg(pp + h);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        ct_bf(x[p][4 * h], x[p][4 * h + 1], make_uint2(w.x, w.y), q2, q);
+        ct_bf(x[p][4 * h + 2], x[p][4 * h + 3], make_uint2(w.z, w.w), q2, q);
+      }
     }
   }
 }
 // One radix-16 GS round = 4 stages t = T .. 8T; h0 = n / (2T).
-HE_D void gs_round16(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t h0, uint32_t i0, uint32_t q2, uint32_t q) {
+template <int NP>
+HE_D void gs_round16(uint32_t (&x)[NP][16], const uint2* __restrict__ tw, uint32_t h0, uint32_t i0, uint32_t q2,
+                     uint32_t q) {
   {
-    const uint4* p = reinterpret_cast<const uint4*>(tw + h0 + 8 * i0);
+    const uint4* pp = reinterpret_cast<const uint4*>(tw + h0 + 8 * i0);
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
-      const uint4 w = __ldg(p + h);
-      gs_bf(x[4 * h], x[4 * h + 1], make_uint2(w.x, w.y), q2, q);
-      gs_bf(x[4 * h + 2], x[4 * h + 3], make_uint2(w.z, w.w), q2, q);
+      const uint4 w = __ldg(pp + h);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        gs_bf(x[p][4 * h], x[p][4 * h + 1], make_uint2(w.x, w.y), q2, q);
+        gs_bf(x[p][4 * h + 2], x[p][4 * h + 3], make_uint2(w.z, w.w), q2, q);
+      }
     }
   }
   {
-    const uint4* p = reinterpret_cast<const uint4*>(tw + h0 / 2 + 4 * i0);
-    const uint4 wa = __ldg(p), wb = __ldg(p + 1);
+    const uint4* pp = reinterpret_cast<const uint4*>(tw + h0 / 2 + 4 * i0);
+    const uint4 wa = __ldg(pp), wb = __ldg(pp + 1);
     const uint2 ws[4] = {make_uint2(wa.x, wa.y), make_uint2(wa.z, wa.w), make_uint2(wb.x, wb.y), make_uint2(wb.z, wb.w)};
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      gs_bf(x[4 * g], x[4 * g + 2], ws[g], q2, q);
-      gs_bf(x[4 * g + 1], x[4 * g + 3], ws[g], q2, q);
-    }
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        gs_bf(x[p][4 * g], x[p][4 * g + 2], ws[g], q2, q);
+        gs_bf(x[p][4 * g + 1], x[p][4 * g + 3], ws[g], q2, q);
+      }
   }
   {
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(tw + h0 / 4 + 2 * i0));
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      gs_bf(x[e], x[e + 4], make_uint2(w.x, w.y), q2, q);
-      gs_bf(x[8 + e], x[12 + e], make_uint2(w.z, w.w), q2, q);
-    }
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        gs_bf(x[p][e], x[p][e + 4], make_uint2(w.x, w.y), q2, q);
+        gs_bf(x[p][8 + e], x[p][12 + e], make_uint2(w.z, w.w), q2, q);
+      }
   }
   {
     const uint2 w = __ldg(tw + h0 / 8 + i0);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) gs_bf(x[e], x[e + 8], w, q2, q);
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) gs_bf(x[p][e], x[p][e + 8], w, q2, q);
   }
 }
 
@@ -226,119 +249,147 @@ HE_D constexpr uint32_t poff(int e) {
   return T >= 32 ? (uint32_t)(e * T + e * T / 32) : (T == 16 ? (uint32_t)(16 * e + e / 2) : (uint32_t)e);
 }
 
-// forward: rounds of 4 stages, T = N2/16, N2/256, ..., 1; first round straight from global
-template <int N2>
+// forward: rounds of 4 stages, T = N2/16, N2/256, ..., 1; first round straight from global.  NP transforms
+// (polys blockIdx.y * NP .. + NP - 1 of the batch, block b of each) per CTA share every twiddle load.
+template <int N2, int NP>
 __global__ void __launch_bounds__(N2 / 16) ntt_fwd_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
                                                         const uint2* __restrict__ tw, uint32_t q, int final_reduce) {
-  __shared__ uint32_t s[N2 + N2 / 32];
+  __shared__ uint32_t s[NP][N2 + N2 / 32];
   const uint32_t b = blockIdx.x;
-  uint32_t* a = data + blockIdx.y * stride + (size_t)b * N2;
+  uint32_t* a[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) a[p] = data + ((size_t)blockIdx.y * NP + p) * stride + (size_t)b * N2;
   const uint32_t tau = threadIdx.x;
   const uint32_t q2 = 2 * q;
-  uint32_t x[16];
+  uint32_t x[NP][16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = a[tau + e * (N2 / 16)];  // coalesced across the warp
-  ct_round16(x, tw, n / N2, b, q2, q);
+  for (int p = 0; p < NP; ++p)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) x[p][e] = a[p][tau + e * (N2 / 16)];  // coalesced across the warp
+  ct_round16<NP>(x, tw, n / N2, b, q2, q);
   if constexpr (N2 == 16) {
-    if (final_reduce) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = reduce4(x[e], q);
+    for (int p = 0; p < NP; ++p) {
+      if (final_reduce) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[p][e] = reduce4(x[p][e], q);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(a[p]);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dst[v] = make_uint4(x[p][4 * v], x[p][4 * v + 1], x[p][4 * v + 2], x[p][4 * v + 3]);
     }
-    uint4* dst = reinterpret_cast<uint4*>(a);
-#pragma unroll
-    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
     return;
   } else {
     {
       constexpr int T = N2 / 16;
-      uint32_t* ps = s + pad(tau);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) ps[poff<T>(e)] = x[e];
+      for (int p = 0; p < NP; ++p) {
+        uint32_t* ps = s[p] + pad(tau);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) ps[poff<T>(e)] = x[p][e];
+      }
       __syncthreads();
     }
     if constexpr (N2 == 4096) {
       constexpr int T = 16;
       const uint32_t j0 = (tau / T) * 16 * T + (tau % T);
-      uint32_t* ps = s + pad(j0);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = ps[poff<T>(e)];
-      ct_round16(x, tw, n / (16 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[p][e] = s[p][pad(j0) + poff<T>(e)];
+      ct_round16<NP>(x, tw, n / (16 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
       __syncthreads();
 #pragma unroll
-      for (int e = 0; e < 16; ++e) ps[poff<T>(e)] = x[e];
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) s[p][pad(j0) + poff<T>(e)] = x[p][e];
       __syncthreads();
     }
     {
-      uint32_t* ps = s + pad(16 * tau);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = ps[e];
-      ct_round16(x, tw, n / 16, b * (N2 / 16) + tau, q2, q);
-      if (final_reduce) {
+      for (int p = 0; p < NP; ++p)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = reduce4(x[e], q);
+        for (int e = 0; e < 16; ++e) x[p][e] = s[p][pad(16 * tau) + e];
+      ct_round16<NP>(x, tw, n / 16, b * (N2 / 16) + tau, q2, q);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        if (final_reduce) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) x[p][e] = reduce4(x[p][e], q);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(a[p] + 16 * tau);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dst[v] = make_uint4(x[p][4 * v], x[p][4 * v + 1], x[p][4 * v + 2], x[p][4 * v + 3]);
       }
-      uint4* dst = reinterpret_cast<uint4*>(a + 16 * tau);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) dst[v] = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
     }
   }
 }
 
 // inverse: rounds of 4 stages, T = 1, 16, 256, ...; first round straight from global (16 contiguous words),
 // last round straight to global (coalesced), optional n^-1 scaling
-template <int N2>
+template <int N2, int NP>
 __global__ void __launch_bounds__(N2 / 16) ntt_inv_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
                                                         const uint2* __restrict__ tw, uint32_t q, uint32_t ninv,
                                                         uint32_t ninvp, int do_scale) {
-  __shared__ uint32_t s[N2 + N2 / 32];
+  __shared__ uint32_t s[NP][N2 + N2 / 32];
   const uint32_t b = blockIdx.x;
-  uint32_t* a = data + blockIdx.y * stride + (size_t)b * N2;
+  uint32_t* a[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) a[p] = data + ((size_t)blockIdx.y * NP + p) * stride + (size_t)b * N2;
   const uint32_t tau = threadIdx.x;
   const uint32_t q2 = 2 * q;
-  uint32_t x[16];
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(a + 16 * tau);
+  uint32_t x[NP][16];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const uint4* src = reinterpret_cast<const uint4*>(a[p] + 16 * tau);
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const uint4 w = src[v];
-      x[4 * v] = w.x;
-      x[4 * v + 1] = w.y;
-      x[4 * v + 2] = w.z;
-      x[4 * v + 3] = w.w;
+      x[p][4 * v] = w.x;
+      x[p][4 * v + 1] = w.y;
+      x[p][4 * v + 2] = w.z;
+      x[p][4 * v + 3] = w.w;
     }
   }
-  gs_round16(x, tw, n / 2, b * (N2 / 16) + tau, q2, q);
+  gs_round16<NP>(x, tw, n / 2, b * (N2 / 16) + tau, q2, q);
   if constexpr (N2 > 16) {
     {
-      uint32_t* ps = s + pad(16 * tau);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) ps[e] = x[e];
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) s[p][pad(16 * tau) + e] = x[p][e];
       __syncthreads();
     }
     if constexpr (N2 == 4096) {
       constexpr int T = 16;
       const uint32_t j0 = (tau / T) * 16 * T + (tau % T);
-      uint32_t* ps = s + pad(j0);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = ps[poff<T>(e)];
-      gs_round16(x, tw, n / (2 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[p][e] = s[p][pad(j0) + poff<T>(e)];
+      gs_round16<NP>(x, tw, n / (2 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
       __syncthreads();
 #pragma unroll
-      for (int e = 0; e < 16; ++e) ps[poff<T>(e)] = x[e];
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) s[p][pad(j0) + poff<T>(e)] = x[p][e];
       __syncthreads();
     }
     {
       constexpr int T = N2 / 16;
-      uint32_t* ps = s + pad(tau);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = ps[poff<T>(e)];
-      gs_round16(x, tw, n / (2 * T), b, q2, q);
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[p][e] = s[p][pad(tau) + poff<T>(e)];
+      gs_round16<NP>(x, tw, n / (2 * T), b, q2, q);
     }
   }
   {
     constexpr int T = N2 / 16;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) a[tau + e * T] = do_scale ? shoup_mul(x[e], ninv, ninvp, q) : x[e];
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) a[p][tau + e * T] = do_scale ? shoup_mul(x[p][e], ninv, ninvp, q) : x[p][e];
   }
 }
 
@@ -389,8 +440,15 @@ cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint6
     if (e != cudaSuccess) return e;
   }
   return with_n2(n2, [&](auto N2) {
-    dim3 g(n1, count);
-    ntt_fwd_rows<decltype(N2)::value><<<g, decltype(N2)::value / 16, 0, st>>>(data, stride, t.n, tw, t.q, 1);
+    constexpr int K = decltype(N2)::value;
+    if (count / 2) {
+      dim3 g(n1, count / 2);
+      ntt_fwd_rows<K, 2><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, 1);
+    }
+    if (count & 1) {
+      dim3 g(n1, 1);
+      ntt_fwd_rows<K, 1><<<g, K / 16, 0, st>>>(data + (size_t)(count - 1) * stride, stride, t.n, tw, t.q, 1);
+    }
     return cudaGetLastError();
   });
 }
@@ -401,9 +459,16 @@ cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint6
   if (count == 0) return cudaSuccess;
   const uint2* tw = reinterpret_cast<const uint2*>(t.iv);
   cudaError_t e = with_n2(n2, [&](auto N2) {
-    dim3 g(n1, count);
-    ntt_inv_rows<decltype(N2)::value><<<g, decltype(N2)::value / 16, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv,
-                                                                              t.ninvp, n1 == 1);
+    constexpr int K = decltype(N2)::value;
+    if (count / 2) {
+      dim3 g(n1, count / 2);
+      ntt_inv_rows<K, 2><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv, t.ninvp, n1 == 1);
+    }
+    if (count & 1) {
+      dim3 g(n1, 1);
+      ntt_inv_rows<K, 1><<<g, K / 16, 0, st>>>(data + (size_t)(count - 1) * stride, stride, t.n, tw, t.q, t.ninv,
+                                               t.ninvp, n1 == 1);
+    }
     return cudaGetLastError();
   });
   if (e != cudaSuccess || n1 == 1) return e;
