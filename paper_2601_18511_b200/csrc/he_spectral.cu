@@ -597,12 +597,17 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
     const size_t stride = (size_t)128 * n_out * nbp / 4;   // 128 rows p, in uint4
     const uint4* g0 = reinterpret_cast<const uint4*>(c0 + g);
     const uint4* g1 = reinterpret_cast<const uint4*>(c1 + g);
-#pragma unroll 4
+    uint4 v0[8], v1[8];   // all 16 loads in flight before the first store
+#pragma unroll
+    for (uint32_t it = 0; it < 8; ++it) {
+      v0[it] = __ldg(g0 + it * stride);
+      v1[it] = __ldg(g1 + it * stride);
+    }
+#pragma unroll
     for (uint32_t it = 0; it < 8; ++it) {
       const uint32_t o = 4 * bq * kInv1kLd + pad32(warp * 16 + ps + 128 * it);
-      const uint4 v0 = __ldg(g0 + it * stride), v1 = __ldg(g1 + it * stride);
-      xs0[o] = v0.x; xs0[o + kInv1kLd] = v0.y; xs0[o + 2 * kInv1kLd] = v0.z; xs0[o + 3 * kInv1kLd] = v0.w;
-      xs1[o] = v1.x; xs1[o + kInv1kLd] = v1.y; xs1[o + 2 * kInv1kLd] = v1.z; xs1[o + 3 * kInv1kLd] = v1.w;
+      xs0[o] = v0[it].x; xs0[o + kInv1kLd] = v0[it].y; xs0[o + 2 * kInv1kLd] = v0[it].z; xs0[o + 3 * kInv1kLd] = v0[it].w;
+      xs1[o] = v1[it].x; xs1[o + kInv1kLd] = v1[it].y; xs1[o + 2 * kInv1kLd] = v1[it].z; xs1[o + 3 * kInv1kLd] = v1[it].w;
     }
   }
   __syncthreads();
@@ -622,25 +627,20 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
   }
   __syncthreads();
   // phase C: block b covers c' = 768 (b0 + b) + u  <->  m = 3 (b0 + b) + u / 256, j = 255 - u % 256
-  const uint32_t N = d * 256, mbase = 3 * b0;
-  if (peers.n == 0) {
-    uint32_t* dst = out_a + (size_t)(y - row0) * N;
-    for (uint32_t i = threadIdx.x; i < 24 * 256; i += 256) {
-      const uint32_t ml = i % 24, j = i / 24;
-      const uint32_t m = mbase + ml;
-      if (m >= d) continue;
-      const uint32_t bl = ml / 3, u = 256 * (ml - 3 * bl) + 255 - j;
-      dst[(size_t)d * j + m] = xs1[bl * kInv1kLd + u];
-    }
-  } else {  // fused all-gather: the same words into every rank's full output at row dst_row0 + (y - row0)
-    const size_t yd = (size_t)peers.dst_row0 + (y - row0);
-    for (uint32_t i = threadIdx.x; i < 24 * 256; i += 256) {
-      const uint32_t ml = i % 24, j = i / 24;
-      const uint32_t m = mbase + ml;
-      if (m >= d) continue;
-      const uint32_t bl = ml / 3, u = 256 * (ml - 3 * bl) + 255 - j;
-      const uint32_t v = xs1[bl * kInv1kLd + u];
-      for (int pr = 0; pr < peers.n; ++pr) peers.a[pr][yd * N + (size_t)d * j + m] = v;
+  // lane ml < 24 owns position m = 3 b0 + ml (block ml / 3, third ml % 3); the 8 warps stride over j
+  const uint32_t N = d * 256, m = 3 * b0 + lane;
+  if (lane < 24 && m < d) {
+    const uint32_t bl = lane / 3, src = bl * kInv1kLd + 256 * (lane - 3 * bl) + 255;
+    if (peers.n == 0) {
+      uint32_t* dst = out_a + (size_t)(y - row0) * N + m;
+#pragma unroll 4
+      for (uint32_t j = warp; j < 256; j += 8) dst[(size_t)d * j] = xs1[src - j];
+    } else {  // fused all-gather: the same words into every rank's full output at row dst_row0 + (y - row0)
+      const size_t yd = (size_t)peers.dst_row0 + (y - row0);
+      for (uint32_t j = warp; j < 256; j += 8) {
+        const uint32_t v = xs1[src - j];
+        for (int pr = 0; pr < peers.n; ++pr) peers.a[pr][yd * N + (size_t)d * j + m] = v;
+      }
     }
   }
 }
