@@ -622,7 +622,8 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
       uint32_t t;
       if (x[1][e] > (q1 >> 1)) t = csub(x[0][e] + (q1 - x[1][e]), q0);
       else t = sub_mod(x[0][e], x[1][e], q0);
-      xs1[b * kInv1kLd + lane + 32 * e] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);  // u = lane + 32 e
+      // u = lane + 32 e stored at u + u / 256 (the three thirds of a block one bank apart for phase C)
+      xs1[b * kInv1kLd + lane + 32 * e + (e >> 3)] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);
     }
   }
   __syncthreads();
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
   // lane ml < 24 owns position m = 3 b0 + ml (block ml / 3, third ml % 3); the 8 warps stride over j
   const uint32_t N = d * 256, m = 3 * b0 + lane;
   if (lane < 24 && m < d) {
-    const uint32_t bl = lane / 3, src = bl * kInv1kLd + 256 * (lane - 3 * bl) + 255;
+    const uint32_t bl = lane / 3, r3 = lane - 3 * bl, src = bl * kInv1kLd + 257 * r3 + 255;
     if (peers.n == 0) {
       uint32_t* dst = out_a + (size_t)(y - row0) * N + m;
 #pragma unroll 4
