@@ -15,9 +15,13 @@ block (slotsim.py:330-370):
         -> clear_pcmm(W, acts)
 
 Work split (all on the device, through the C ABI in include/he_b200.h):
-  plan:  W -> W~ = round(q1 W), k x k blocks conjugated by sigma, balanced int8 digit planes
-  run:   K3 RLWE -> MLWE digit decomposition, then K1 tcgen05 modular GEMM with the digit
-         recombination, reduction mod q_i, rescale and b' compose fused in its epilogue.
+  plan:  W -> W~ = round(q1 W), k x k blocks conjugated by sigma, balanced int8 digit planes;
+         spectral plans (the default) also hold G^ = NTT_L(weight segments) as int8 digit planes (K7 S1)
+  run:   spectral -- K3 digits of the b' columns, K7 S2 window NTTs, K1 on the b' columns, K7 S3
+         per-frequency tcgen05 modular GEMMs, K7 S4 inverse NTT + rescale + a' store;
+         direct   -- K3 RLWE -> MLWE digit decomposition, then K1 tcgen05 modular GEMM over every
+         column with the digit recombination, reduction mod q_i, rescale and b' compose fused in
+         its epilogue.  Both produce the same words.
 """
 
 from __future__ import annotations
@@ -169,8 +173,8 @@ def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks |
               gemm_events=None) -> MlweBlocks:
     """Level-1 RLWE block batch (encrypting A, (d/2) x n_in) -> level-0 MLWE blocks
     encrypting A @ W^T ((d/2) x n_out).  Exactly one level, one rescale per output block,
-    zero ciphertext rotations.  ``gemm_events`` (two torch.cuda.Event) bracket the K1
-    launch on the current stream, for profiling."""
+    zero ciphertext rotations.  ``gemm_events`` (two torch.cuda.Event) bracket the output
+    stage (he_pcmm_gemm: K1, plus S3/S4 for spectral plans) on the current stream."""
     torch = _torch()
     _check_operand(ctx, plan, X)
     p = ctx.params
@@ -224,9 +228,9 @@ def pcmm_mlwe_into_peers(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_
 def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_host, out_a_host,
                       x_host=None, chunk_rows: int = 512) -> MlweBlocks:
     """The same op as ``pcmm_mlwe`` with the level-0 output streamed into (pinned) host
-    buffers ``out_b_host`` [n_out/k, N] and ``out_a_host`` [n_out, N]: K1 runs over row
-    chunks into two alternating device slices while a second stream copies the previous
-    chunk to the host, so the 1 GB device->host transfer overlaps the GEMM.  ``x_host``
+    buffers ``out_b_host`` [n_out/k, N] and ``out_a_host`` [n_out, N]: the output stage runs
+    over row chunks into two alternating device slices while a second stream copies the
+    previous chunk to the host, so the 1 GB device->host transfer overlaps the compute.  ``x_host``
     (pinned, X.data's shape) is first copied into ``X.data`` on the current stream."""
     torch = _torch()
     _check_operand(ctx, plan, X)
