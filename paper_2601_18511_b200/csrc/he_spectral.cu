@@ -553,7 +553,7 @@ HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_
       if (e & len) continue;
 #pragma unroll
       for (int l = 0; l < 2; ++l)
-        dit_bf(x[l][e], x[l][e + len], __ldg(L[l].r2 + base + 32 * (e & (len - 1)) + lane), 2 * L[l].q, L[l].q);
+        dit_bf(x[l][e], x[l][e + len], L[l].r2[base + 32 * (e & (len - 1)) + lane], 2 * L[l].q, L[l].q);
     }
   }
   // len = 512: pairs (e, e + 16); the upper output u = lane + 32 e + 512 is needed only for e < 8
@@ -562,7 +562,7 @@ HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
       const uint32_t q = L[l].q, q2 = 2 * q;
-      const uint2 w = __ldg(L[l].r2 + 480 + 32 * e + lane);
+      const uint2 w = L[l].r2[480 + 32 * e + lane];
       if (e < 8) {
         dit_bf(x[l][e], x[l][e + 16], w, q2, q);
       } else {
@@ -588,8 +588,13 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
   extern __shared__ uint32_t sm[];
   uint32_t* xs0 = sm;                                  // [8 blocks][1060]
   uint32_t* xs1 = sm + kInv1kBlocks * kInv1kLd;
+  uint2* tws = reinterpret_cast<uint2*>(xs1 + kInv1kBlocks * kInv1kLd);   // round-2 lane tables [2][992]
   const uint32_t y = row0 + blockIdx.y, b0 = blockIdx.x * kInv1kBlocks;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < 496; i += 256) {   // 992 uint2 = 496 uint4 per limb
+    reinterpret_cast<uint4*>(tws)[i] = __ldg(reinterpret_cast<const uint4*>(cst.r2[0]) + i);
+    reinterpret_cast<uint4*>(tws + 992)[i] = __ldg(reinterpret_cast<const uint4*>(cst.r2[1]) + i);
+  }
   // phase A: C^[p][y][b0 .. b0 + 7] of both limbs -> xs[b][pad(p)]; one warp access = 16 rows p x 32 B
   {
     const uint32_t bq = lane & 1, ps = lane >> 1;
@@ -614,7 +619,7 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
   const uint32_t b = warp;
   if (b0 + b < nblk) {
     const uint32_t q0 = cst.q[0], q1 = cst.q[1];
-    const Inv1kLimb L[2] = {{xs0 + b * kInv1kLd, cst.r2[0], q0}, {xs1 + b * kInv1kLd, cst.r2[1], q1}};
+    const Inv1kLimb L[2] = {{xs0 + b * kInv1kLd, tws, q0}, {xs1 + b * kInv1kLd, tws + 992, q1}};
     uint32_t x[2][32];
     inv1024_pair(L, cst, lane, x);
 #pragma unroll
@@ -973,7 +978,7 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
   if (L == 1024) {
     if (Rg.k != 256) return cudaErrorInvalidValue;
     dim3 grid((nblk + kInv1kBlocks - 1) / kInv1kBlocks, rows);
-    const size_t smem = (size_t)2 * kInv1kBlocks * kInv1kLd * sizeof(uint32_t);
+    const size_t smem = (size_t)2 * kInv1kBlocks * kInv1kLd * sizeof(uint32_t) + 2 * 992 * sizeof(uint2);
     cudaError_t e = cudaFuncSetAttribute(spec_inverse1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     spec_inverse1024_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, nbp, nblk, Rg.d, cst, out_a, peers);
