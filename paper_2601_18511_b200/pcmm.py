@@ -64,11 +64,19 @@ class MlwePcmmPlan:
         return int(n.value)
 
     def workspace(self, device):
+        """Scratch for one call: a per-device buffer shared by every plan (grown to the largest need),
+        so the projections of a layer do not each pin their own multi-GB workspace.  Calls that share
+        it must be ordered on one stream (the C ABI itself takes any caller-provided workspace)."""
         torch = _torch()
         need = self.workspace_bytes()
-        if self._workspace is None or self._workspace.numel() < need:
-            self._workspace = torch.empty(need, dtype=torch.int8, device=device)
-        return self._workspace
+        key = torch.device(device)
+        ws = _SHARED_WS.get(key)
+        if ws is None or ws.numel() < need:
+            _SHARED_WS.pop(key, None)
+            ws = torch.empty(need, dtype=torch.int8, device=key)
+            _SHARED_WS[key] = ws
+        self._workspace = ws
+        return ws
 
     def spectral_info(self) -> dict:
         """Spectral plans: transform length L, outputs per block, blocks, padded blocks."""
@@ -99,6 +107,7 @@ class MlwePcmmPlan:
 
 
 ALGOS = ("spectral", "direct")
+_SHARED_WS: dict = {}   # torch.device -> int8 workspace tensor (MlwePcmmPlan.workspace)
 
 
 def make_mlwe_pcmm_plan(ctx: HeContext, weights, d_w: int | None = None, algo: str = "spectral") -> MlwePcmmPlan:
