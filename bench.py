@@ -533,9 +533,19 @@ def cpu_baseline(P, A, plan, X, n_out, n_in, n_rows, W_seed_dev=None, g_seed=Non
     n_rows = min(n_rows, P.mlwe_rank)
     res = O.time_pcmm_sample(P, Wt, ct, n_rows)
     per_op = res["seconds"] * n_out / n_rows * 1e3
+    # context: the unencrypted product on the same host, numpy float64 (BLAS threads)
+    rng = np.random.default_rng(0)
+    Wf, Af = rng.standard_normal((n_out, n_in)), rng.standard_normal((P.tokens, n_in))
+    Af @ Wf.T
+    t0 = time.perf_counter()
+    for _ in range(3):
+        Af @ Wf.T
+    floor_ms = (time.perf_counter() - t0) / 3 * 1e3
     return {"value": round(per_op, 1), "unit": "ms/op", "cores": res["threads"], "kind": "port",
             "sample": f"oracle/ C restatement: {n_rows} of {n_out} output rows x {P.width} cols x K={n_in}, "
-                      f"both limbs + rescale, {res['seconds']:.2f} s, extrapolated x{n_out / n_rows:.0f}"}
+                      f"both limbs + rescale, {res['seconds']:.2f} s, extrapolated x{n_out / n_rows:.0f}",
+            "plaintext_floor_ms": round(floor_ms, 2),
+            "plaintext_floor": f"numpy float64 acts @ W.T ({P.tokens} x {n_in} x {n_out}) on the host, unencrypted"}
 
 
 def run_reference(a, rank: int, world: int):
