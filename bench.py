@@ -58,7 +58,9 @@ def parse():
     ap.add_argument("--algo", choices=["spectral", "direct"], default="spectral",
                     help="a'-column algorithm (same output words): K7 spectral (default) or K1 direct GEMM")
     ap.add_argument("--no-direct", action="store_true", help="skip the side measurement of the direct K1 path")
-    ap.add_argument("--no-fused", action="store_true", help="N > 1: NCCL all-gather instead of the fused peer stores")
+    ap.add_argument("--fused", action="store_true",
+                    help="N > 1: fuse the output all-gather into the kernels' peer-memory stores (symmetric memory; "
+                         "not yet exercised on multi-GPU hardware -- the default is NCCL broadcast + all-gather)")
     ap.add_argument("--cpu-rows", type=int, default=64, help="oracle sample rows for cpu_baseline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -177,7 +179,7 @@ def run_ours(a, rank: int, world: int, local: int):
     out_b = torch.empty((per, N), dtype=torch.int32, device=dev)
     out_a = torch.empty((per * k, N), dtype=torch.int32, device=dev)
     Y = MlweBlocks(out_b[: b1 - b0], out_a[:rows], level=0, n_rows=rows)
-    sym = symmetric_outputs(ctx, n_out) if world > 1 and not a.no_fused else None
+    sym = symmetric_outputs(ctx, n_out) if world > 1 and a.fused else None
     if world > 1:
         all_b = torch.empty((per * world, N), dtype=torch.int32, device=dev)
         all_a = torch.empty((per * world * k, N), dtype=torch.int32, device=dev)
