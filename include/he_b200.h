@@ -56,6 +56,7 @@ typedef struct {
 typedef struct he_context he_context;     /* NTT tables, device constants       */
 typedef struct he_pcmm_plan he_pcmm_plan; /* weight side of the MLWE PCMM       */
 typedef struct he_rhombus_plan he_rhombus_plan; /* weight side of the Rhombus PCMv */
+typedef struct he_ring_pack_plan he_ring_pack_plan; /* MLWE -> RLWE ring packing tables */
 
 /* Operation counters, same field names as hesim.CostLedger (slotsim.py:31-83). */
 typedef struct {
@@ -181,6 +182,32 @@ he_status he_rhombus_workspace_bytes(const he_rhombus_plan* plan, uint64_t* byte
 he_status he_rhombus_run(const he_rhombus_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
                          const uint32_t* ksk_dec_dev, const uint32_t* gal_dev, uint32_t* out_dev, void* workspace_dev,
                          uint64_t workspace_bytes, void* stream, he_ledger* ledger);
+
+/* ---------------------------------------------------------------- MLWE -> RLWE ring packing
+ * The step after the PCMM toward Half-Bootstrap: each block of k MLWE output rows
+ * becomes ONE RLWE ciphertext under s whose phase at coefficient t + k m is row (block, t)'s phase
+ * at m -- the activation layout he_encrypt_acts produces, so the packed output is the next
+ * layer's input format.  hesim has no counterpart (its PCMM output stays in slots); the oracle is
+ * or_ring_pack in oracle/he_oracle_rhombus.c.
+ *
+ * Step 1: the PCMM at level 1 WITHOUT the rescale: raw_b [2 limbs][n_out/k][N] (b' in RLWE order,
+ * like out_b), raw_a [2 limbs][n_out][k*d] (a' MLWE rows, like out_a), words mod q0 / q1. */
+he_status he_pcmm_run_level1(const he_pcmm_plan* plan, const uint32_t* ct_in_dev, uint32_t level, uint32_t* raw_b_dev,
+                             uint32_t* raw_a_dev, void* workspace_dev, uint64_t workspace_bytes, void* stream);
+/* Galois keys sigma_g(s) -> s, g = 1 + 2^l d, l = 1 .. log2 k: u32 [log2 k][2][2][3][N] (NTT domain,
+ * moduli q0 q1 P; key ids 0x100 + l) */
+he_status he_ring_pack_keygen(const he_context* ctx, uint64_t seed, const int32_t* s_dev, uint32_t* gal_dev,
+                              void* stream);
+/* n_out must be a multiple of k */
+he_status he_ring_pack_plan_create(const he_context* ctx, uint32_t n_out, he_ring_pack_plan** out);
+he_status he_ring_pack_plan_destroy(he_ring_pack_plan* plan);
+he_status he_ring_pack_workspace_bytes(const he_ring_pack_plan* plan, uint64_t* bytes);
+/* step 2: raw words of step 1 -> level-0 RLWE ciphertexts out [n_out/k][2 (a, b)][N] under s.
+ * PackLWEs over the subring Z[X^k] with hybrid key switching (dnum 2, special prime P), then
+ * rescale by q1.  ledger: ct_rotations += (k - 1) n_out/k, rescales += n_out/k. */
+he_status he_ring_pack_run(const he_ring_pack_plan* plan, const uint32_t* raw_b_dev, const uint32_t* raw_a_dev,
+                           const uint32_t* gal_dev, uint32_t* out_dev, void* workspace_dev, uint64_t workspace_bytes,
+                           void* stream, he_ledger* ledger);
 
 #ifdef __cplusplus
 }

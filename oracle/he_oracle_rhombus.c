@@ -220,9 +220,11 @@ static void ct_apply_sigma_ks(const uint32_t* ct, uint32_t n, uint32_t k, const 
   free(w);
 }
 
-/* PackLWEs, recursive (CDKS21): v = list of 2^l cts (each [2][2][n]) with stride `step` in `base`. */
-static void pack_rec(const uint32_t* const* v, uint32_t count, uint32_t step, uint32_t n, const uint32_t* const* gal,
-                     const uint32_t* m, uint32_t* out) {
+/* PackLWEs, recursive (CDKS21): v = list of 2^l cts (each [2][2][n]).  Level l (count = 2^l) combines
+ *   E + X^{sb / 2^l} O + sigma_{1 + gm 2^l}(E - X^{sb / 2^l} O)
+ * Rhombus: sb = n, gm = 1 (the full ring); ring packing: sb = k, gm = d (the subring Z[X^k], N = d k). */
+static void pack_rec(const uint32_t* const* v, uint32_t count, uint32_t sb, uint32_t gm, uint32_t n,
+                     const uint32_t* const* gal, const uint32_t* m, uint32_t* out) {
   const size_t cw = (size_t)4 * n;
   if (count == 1) {
     memcpy(out, v[0], sizeof(uint32_t) * cw);
@@ -237,10 +239,10 @@ static void pack_rec(const uint32_t* const* v, uint32_t count, uint32_t step, ui
   }
   uint32_t* E = (uint32_t*)malloc(sizeof(uint32_t) * cw);
   uint32_t* O = (uint32_t*)malloc(sizeof(uint32_t) * cw);
-  pack_rec(ev, half, step, n, gal, m, E);
-  pack_rec(od, half, step, n, gal, m, O);
+  pack_rec(ev, half, sb, gm, n, gal, m, E);
+  pack_rec(od, half, sb, gm, n, gal, m, O);
   const int l = ilog2u(count);
-  const uint32_t e = n >> l;  /* X^{n / 2^l} */
+  const uint32_t e = sb >> l;  /* X^{sb / 2^l} */
   uint32_t* MO = (uint32_t*)malloc(sizeof(uint32_t) * cw);
   uint32_t* T = (uint32_t*)malloc(sizeof(uint32_t) * cw);
   uint32_t* ST = (uint32_t*)malloc(sizeof(uint32_t) * cw);
@@ -252,7 +254,7 @@ static void pack_rec(const uint32_t* const* v, uint32_t count, uint32_t step, ui
       size_t x = (size_t)L * 2 * n + i;
       T[x] = (uint32_t)(((uint64_t)E[x] + m[L] - MO[x]) % m[L]);
     }
-  ct_apply_sigma_ks(T, n, (1u << l) + 1, gal[l - 1], m, ST);
+  ct_apply_sigma_ks(T, n, (gm << l) + 1, gal[l - 1], m, ST);
   for (int L = 0; L < 2; ++L)
     for (size_t i = 0; i < (size_t)2 * n; ++i) {
       size_t x = (size_t)L * 2 * n + i;
@@ -338,7 +340,7 @@ int or_rhombus_pcmv(uint32_t N, uint32_t n, const uint32_t* m, const uint32_t* c
   uint32_t* packed = (uint32_t*)malloc(sizeof(uint32_t) * cw * p_out);
   for (uint32_t o = 0; o < p_out; ++o) {
     for (uint32_t j = 0; j < n; ++j) leaves[j] = rows + ((size_t)o * n + j) * cw;
-    pack_rec(leaves, n, 1, n, gk, m, packed + (size_t)o * cw);
+    pack_rec(leaves, n, n, 1, n, gk, m, packed + (size_t)o * cw);
   }
   if (pieces_out) memcpy(pieces_out, packed, sizeof(uint32_t) * cw * p_out);
   /* (R) rescale, (C) compose */
@@ -376,4 +378,69 @@ void or_decode_vector(const int64_t* phase, uint32_t n_vals, uint32_t N, uint32_
     const uint32_t p = e / n, k = or_half_reverse(e % n, n);
     v[e] = (double)phase[p + (size_t)rho * k] / delta;
   }
+}
+
+/* ================================================================== MLWE -> RLWE ring packing
+ *
+ * The PCMM's MLWE output row y (component t' of output block Y, y = k Y + t') is component 0 of the
+ * level-1 RLWE product C_y = sum_r w_{y,r}(X) ct_r, w_{y,r} = sum_t W~[y][k r + t] X^-t, whose
+ *   a-polynomial  A_y[k m - j] = a'_y[j][m]   (negacyclic: A_y[N + c] = -a'_y[j][0] for c = -j < 0)
+ * is fully determined by the un-rescaled a' words, while only component 0 of its b-polynomial,
+ * B_y[k m] = b'_y[m], is known -- which is all the trace needs.  PackLWEs over the subring Z[X^k]
+ * (pack_rec with sb = k, gm = d: log2 k levels, automorphisms sigma_{1 + 2^l d} fixing X^{k/2^(l-1)}
+ * and negating X^{k/2^l}) sums the k leaves of a block into one RLWE ciphertext whose phase is
+ * k sum_t' X^t' phase_{kY+t'}(X^k), so the leaves are pre-scaled by k^-1; a final rescale by q1
+ * gives level 0.  The packed phase of block Y at coefficient t' + k m is row (Y, t')'s phase at m:
+ * the activation layout of or_encode_acts, i.e. the packed output is the next layer's input format.
+ */
+
+/* Galois key of sigma_g, g = 1 + 2^l d, at degree N: from sigma_g(s) to s  (key id 0x100 + l) */
+void or_ring_galois_ksk(uint64_t seed, uint32_t l, const int32_t* s, uint32_t N, uint32_t d, const uint32_t* m,
+                        uint32_t* ksk) {
+  const uint64_t g = ((uint64_t)d << l) + 1;
+  int32_t* ss = (int32_t*)malloc(sizeof(int32_t) * N);
+  for (uint32_t i = 0; i < N; ++i) {
+    uint64_t j = ((uint64_t)i * g) % (2ull * N);
+    if (j < N) ss[j] = s[i];
+    else ss[j - N] = -s[i];
+  }
+  or_ksk_gen(seed, 0x100 + l, ss, s, N, m, ksk);
+  free(ss);
+}
+
+/*
+ * leaves  [cnt][2 limbs][2 (a, b)][N]  level-1 leaf ciphertexts C_y (already scaled by k^-1), cnt = blocks k
+ * gal     [log2 k][2][2][3][N]         keys of or_ring_galois_ksk, l = 1 .. log2 k
+ * packed  [blocks][2][2][N]            level-1 packed ciphertexts (optional)
+ * out     [blocks][2 (a, b)][N]        rescaled, level 0
+ */
+int or_ring_pack(uint32_t N, uint32_t d, uint32_t k, const uint32_t* m, const uint32_t* leaves, uint32_t cnt,
+                 const uint32_t* gal, uint32_t* packed, uint32_t* out) {
+  if (N != d * k || cnt % k) return 1;
+  const int lg = ilog2u(k);
+  const uint32_t blocks = cnt / k;
+  const size_t cw = (size_t)4 * N;
+  const uint32_t** gk = (const uint32_t**)malloc(sizeof(void*) * (lg ? lg : 1));
+  for (int l = 0; l < lg; ++l) gk[l] = gal + (size_t)l * 12 * N;
+  const uint32_t q0 = m[0], q1 = m[1];
+  const uint64_t q1inv = powmod(q1 % q0, q0 - 2, q0);
+  int rc = 0;
+#pragma omp parallel for schedule(dynamic)
+  for (uint32_t o = 0; o < blocks; ++o) {
+    const uint32_t** lv = (const uint32_t**)malloc(sizeof(void*) * k);
+    uint32_t* pk = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+    for (uint32_t j = 0; j < k; ++j) lv[j] = leaves + ((size_t)o * k + j) * cw;
+    pack_rec(lv, k, k, d, N, gk, m, pk);
+    if (packed) memcpy(packed + (size_t)o * cw, pk, sizeof(uint32_t) * cw);
+    for (int ab = 0; ab < 2; ++ab)
+      for (uint32_t c = 0; c < N; ++c) {
+        const uint32_t x0 = pk[(size_t)ab * N + c], x1 = pk[((size_t)2 + ab) * N + c];
+        const int64_t x1c = x1 > q1 / 2 ? (int64_t)x1 - q1 : (int64_t)x1;
+        out[((size_t)o * 2 + ab) * N + c] = (uint32_t)mulmod(modq_i64((int64_t)x0 - x1c, q0), q1inv, q0);
+      }
+    free(lv);
+    free(pk);
+  }
+  free(gk);
+  return rc;
 }

@@ -17,7 +17,8 @@ __all__ = [
     "negacyclic_mul", "negacyclic_mul_schoolbook", "sigma_table", "clear_pcmm", "mlwe_column",
     "py_mlwe_components", "py_pcmm_rows", "num_threads", "time_pcmm_sample", "rng",
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
-    "decode_vector", "rhombus_pcmv", "rhombus_weights", "decrypt_under",
+    "decode_vector", "rhombus_pcmv", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
+    "ring_pack", "pcmm_ring_pack",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -436,3 +437,72 @@ def decrypt_under(params, a: np.ndarray, b: np.ndarray, s: np.ndarray, q: int) -
     prod = negacyclic_mul(np.ascontiguousarray(a, dtype=np.uint32), np.ascontiguousarray(s, dtype=np.int32), q)
     v = (prod.astype(np.int64) + b.astype(np.int64)) % q
     return np.where(v > q // 2, v - q, v)
+
+
+# ---------------------------------------------------------------- MLWE -> RLWE ring packing (§8f1)
+def _rp_lib():
+    L = _rh_lib()
+    if not getattr(L, "_rp_bound", False):
+        u32p, i32p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32)
+        u32, u64 = ctypes.c_uint32, ctypes.c_uint64
+        L.or_ring_galois_ksk.restype = None
+        L.or_ring_galois_ksk.argtypes = [u64, u32, i32p, u32, u32, u32p, u32p]
+        L.or_ring_pack.restype = ctypes.c_int
+        L.or_ring_pack.argtypes = [u32, u32, u32, u32p, u32p, u32, u32p, u32p, u32p]
+        L._rp_bound = True
+    return L
+
+
+def ring_pack_keys(params, seed: int, s: np.ndarray) -> np.ndarray:
+    """Galois keys sigma_{1 + 2^l d}: sigma(s) -> s at degree N, l = 1 .. log2 k -> [log k, 2, 2, 3, N]."""
+    N, d, k = params.N, params.mlwe_degree, params.mlwe_rank
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    lg = k.bit_length() - 1
+    gal = np.zeros((lg, 2, 2, 3, N), np.uint32)
+    for lv in range(1, lg + 1):
+        g = np.zeros((2, 2, 3, N), np.uint32)
+        _rp_lib().or_ring_galois_ksk(seed, lv, _i32(np.ascontiguousarray(s, dtype=np.int32)), N, d, _u32(m), _u32(g))
+        gal[lv - 1] = g
+    return gal
+
+
+def ring_pack_leaves(params, raw: list) -> np.ndarray:
+    """Leaf ciphertexts C_y [n_out, 2 limbs, 2, N] (scaled by k^-1) from the un-rescaled MLWE words
+    raw[limb] = [n_out, d + d k] (pcmm_limb):  A_y[k m - j] = a'_y[j][m] (negacyclic), B_y[k m] = b'_y[m]."""
+    N, d, k = params.N, params.mlwe_degree, params.mlwe_rank
+    n_out = raw[0].shape[0]
+    j = np.arange(k)[:, None]
+    mm = np.arange(d)[None, :]
+    c = (k * mm - j).ravel()                 # position of a'[j][m] (flattened j-major like the words)
+    neg = c < 0
+    c = np.where(neg, c + N, c)
+    leaves = np.zeros((n_out, 2, 2, N), np.uint32)
+    for L in range(2):
+        q = int(params.moduli[L])
+        kinv = pow(k, q - 2, q)
+        v = raw[L].astype(np.int64)
+        a = v[:, d:]
+        a = np.where(neg[None, :], (q - a) % q, a)
+        leaves[:, L, 0, c] = (a * kinv % q).astype(np.uint32)
+        leaves[:, L, 1, k * np.arange(d)] = (v[:, :d] * kinv % q).astype(np.uint32)
+    return leaves
+
+
+def ring_pack(params, leaves: np.ndarray, gal: np.ndarray):
+    """-> (packed level-1 [blocks, 2, 2, N], out level-0 [blocks, 2 (a, b), N]); see he_oracle_rhombus.c."""
+    N, d, k = params.N, params.mlwe_degree, params.mlwe_rank
+    cnt = leaves.shape[0]
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    packed = np.zeros((cnt // k, 2, 2, N), np.uint32)
+    out = np.zeros((cnt // k, 2, N), np.uint32)
+    rc = _rp_lib().or_ring_pack(N, d, k, _u32(m), _u32(np.ascontiguousarray(leaves, dtype=np.uint32)), cnt,
+                                _u32(np.ascontiguousarray(gal, dtype=np.uint32)), _u32(packed), _u32(out))
+    if rc:
+        raise ValueError("ring pack: bad shape")
+    return packed, out
+
+
+def pcmm_ring_pack(params, Wt, ct, gal):
+    """Reference MLWE PCMM followed by ring packing: level-0 RLWE output blocks [n_out / k, 2, N]."""
+    raw = [pcmm_limb(params, Wt, ct, L) for L in range(2)]
+    return ring_pack(params, ring_pack_leaves(params, raw), gal)[1]

@@ -13,6 +13,8 @@ from .pcmm import (MlwePcmmPlan, clear_pcmm, make_mlwe_pcmm_plan, pcmm_mlwe, pcm
                    pcmm_mlwe_to_host)
 from .rhombus import (CtVector, RhombusKeys, RhombusPlan, clear_pcmv, decrypt_vector, encrypt_vector,
                       make_rhombus_plan, pcmv_rhombus, rhombus_keygen)
+from .ringpack import (RingPackKeys, RingPackPlan, make_ring_pack_plan, pcmm_level1, pcmm_packed, ring_pack,
+                       ring_pack_keygen)
 
 __all__ = [
     "NeedsBootstrapError", "HeParams", "CostLedger", "CtBlocks", "HeContext", "MlweBlocks", "SecretKey",
@@ -21,6 +23,8 @@ __all__ = [
     "pcmm_mlwe_into_peers",
     "CtVector", "RhombusKeys", "RhombusPlan", "clear_pcmv", "decrypt_vector", "encrypt_vector",
     "make_rhombus_plan", "pcmv_rhombus", "rhombus_keygen",
+    "RingPackKeys", "RingPackPlan", "make_ring_pack_plan", "pcmm_level1", "pcmm_packed", "ring_pack",
+    "ring_pack_keygen",
 ]
 
 __version__ = "0.1.0"

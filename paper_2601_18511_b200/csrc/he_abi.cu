@@ -485,7 +485,7 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
 
 // K7 S3 (per-frequency tcgen05 GEMM, both limbs) + S4 (inverse, rescale, a' store) on rows [row0, row0 + rows)
 static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows, uint32_t* out_a,
-                           const OutPeers& peers, cudaStream_t st) {
+                           uint32_t* out1_a, const OutPeers& peers, cudaStream_t st) {
   const SpecWs w = spec_ws(p);
   const int8_t* base = (const int8_t*)ws;
   static const bool simple = getenv("HE_SPEC_SIMPLE") != nullptr;  // debug: S3 on CUDA cores
@@ -533,6 +533,7 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
   }
   c.q1inv = p->epi.q1inv;
   c.q1invp = p->epi.q1invp;
+  c.out1 = out1_a;
   p->prof_begin(5, st);
   HE_CUDA(launch_spec_inverse(p->ctx->R, C[0], C[1], p->n_out, row0, rows, p->L, p->nblk, p->nbp, c, out_a, peers, st),
           "spectral inverse");
@@ -541,11 +542,12 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
 }
 
 static he_status gemm_rows_impl(const he_pcmm_plan* p, const void* ws, uint32_t row0, uint32_t rows, uint32_t* out_b,
-                                uint32_t* out_a, const OutPeers& peers, void* stream) {
+                                uint32_t* out_a, const OutPeers& peers, void* stream, uint32_t* out1_b = nullptr,
+                                uint32_t* out1_a = nullptr) {
   if (!p || !ws || (peers.n == 0 && (!out_b || !out_a))) return fail(HE_EINVAL, "null argument");
   if (rows == 0 || row0 % p->ctx->R.k || rows % p->ctx->R.k || row0 + rows > p->n_out)
     return fail(HE_EINVAL, "row range [%u, %u) must be k-aligned and inside [0, %u)", row0, row0 + rows, p->n_out);
-  const int variant = p->algo == 1 ? 2 : gemm_variant();
+  const int variant = (p->algo == 1 || out1_b) ? 2 : gemm_variant();
   const bool fused = p->algo != 1 && fused_path(p);
   const bool spec = p->algo == 1;
   const uint32_t gemm_width = spec ? p->ctx->R.d : p->width;  // spectral: K1 on the b' columns only
@@ -592,6 +594,8 @@ static he_status gemm_rows_impl(const he_pcmm_plan* p, const void* ws, uint32_t 
   a.k = (int)p->ctx->R.k;
   a.out_b = out_b;
   a.out_a = out_a;
+  a.out1_b = out1_b;
+  a.out1_a = out1_a;
   a.peers = peers;
   a.c = p->epi;
   a.group_m = env_gm > 0 ? env_gm : 8;
@@ -616,7 +620,7 @@ static he_status gemm_rows_impl(const he_pcmm_plan* p, const void* ws, uint32_t 
   HE_CUDA(launch_modgemm(variant, (int)p->d_w, (int)p->d0, (int)p->d1, tmA, tmB, tmBa, a, grid, (cudaStream_t)stream),
           "modgemm");
   p->prof_end(2, (cudaStream_t)stream);
-  if (spec) return spec_rows(p, ws, row0, rows, out_a, peers, (cudaStream_t)stream);
+  if (spec) return spec_rows(p, ws, row0, rows, out_a, out1_a, peers, (cudaStream_t)stream);
   return HE_OK;
 }
 
@@ -667,6 +671,22 @@ extern "C" he_status he_pcmm_run(const he_pcmm_plan* p, const uint32_t* ct_in, u
     ledger->rescales += bo;
   }
   return HE_OK;
+}
+
+// level-1 words of both limbs (no rescale): the ring-packing input (he_ring_pack_run)
+extern "C" he_status he_pcmm_run_level1(const he_pcmm_plan* p, const uint32_t* ct_in, uint32_t level, uint32_t* raw_b,
+                                        uint32_t* raw_a, void* ws, uint64_t ws_size, void* stream) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmm needs one level");
+  if (level != 1) return fail(HE_EINVAL, "the MLWE PCMM runs at level 1 (got %u); switch levels first", level);
+  if (!raw_b || !raw_a) return fail(HE_EINVAL, "null argument");
+  he_status s = he_pcmm_decompose(p, ct_in, ws, ws_size, stream);
+  if (s) return s;
+  const uint64_t N = p->ctx->R.N;
+  OutPeers none{};
+  none.n = 0;
+  return gemm_rows_impl(p, ws, 0, p->n_out, raw_b, raw_a, none, stream, raw_b + (uint64_t)(p->n_out / p->ctx->R.k) * N,
+                        raw_a + (uint64_t)p->n_out * N);
 }
 
 // ---------------------------------------------------------------- K7 spectral a-part

@@ -39,6 +39,8 @@ struct GemmArgs {
   int fused;            // 1: B tiles come straight from the compact digit planes (K3 fused into K1)
   uint32_t* out_b;
   uint32_t* out_a;
+  uint32_t* out1_b = nullptr;  // level-1 mode: no rescale; limb-1 words here, limb-0 words in out_b / out_a
+  uint32_t* out1_a = nullptr;
   OutPeers peers;
   GemmEpiConst c;
 };
@@ -99,6 +101,7 @@ struct SpecInvConst {
   uint2 r1[2][26];          // round-1 twiddles of the fast inverse (spec_table_init)
   uint32_t linv[2], linvp[2];
   uint32_t q1inv, q1invp;
+  uint32_t* out1 = nullptr;  // level-1 mode: no rescale; limb-0 words -> out_a, limb-1 words -> out1 (same layout)
 };
 cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out, uint32_t n_in, uint32_t k,
                                 const SpecTable& t, int D, uint32_t r_pad, int8_t* out, cudaStream_t s);

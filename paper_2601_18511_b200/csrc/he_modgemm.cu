@@ -519,6 +519,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         tmem_ld_wait();
         if (args.epi_skip) continue;
         uint32_t res[8];
+        if (args.out1_b) {  // level-1 mode: both limbs' words, no rescale (same layouts)
+          uint32_t r1[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            res[e] = recombine<C::S0>(acc0, e, c, 0);
+            r1[e] = recombine<C::S1>(acc1, e, c, 1);
+          }
+          if (row_ok) {
+            if (n < args.d) {
+              const size_t o = (size_t)(y / args.k) * N + (y % args.k);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                args.out_b[o + (size_t)args.k * (n + e)] = res[e];
+                args.out1_b[o + (size_t)args.k * (n + e)] = r1[e];
+              }
+            } else {
+              const size_t o = (size_t)y * N + (n - args.d);
+              uint4* d0 = reinterpret_cast<uint4*>(args.out_a + o);
+              uint4* d1 = reinterpret_cast<uint4*>(args.out1_a + o);
+              d0[0] = make_uint4(res[0], res[1], res[2], res[3]);
+              d0[1] = make_uint4(res[4], res[5], res[6], res[7]);
+              d1[0] = make_uint4(r1[0], r1[1], r1[2], r1[3]);
+              d1[1] = make_uint4(r1[4], r1[5], r1[6], r1[7]);
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const uint32_t x0 = recombine<C::S0>(acc0, e, c, 0);

@@ -326,6 +326,32 @@ struct he_rhombus_plan {
 
 static uint64_t leaves_of(const he_rhombus_plan* p) { return (uint64_t)p->p_out * p->n; }
 
+// Hybrid key-switching key from s_old to s_new (degree deg; moduli q0, q1, P), NTT domain:
+//   ksk[i][0][j] = alpha (uniform),  ksk[i][1][j] = g_{i,j} s_old + e - alpha s_new   (oracle or_ksk_gen)
+static he_status make_ksk_dev(const Mods& M, uint64_t seed, uint32_t id, const int32_t* s_old, const int32_t* s_new,
+                              uint32_t deg, const NttTable* tabs, uint32_t* ksk, cudaStream_t st) {
+  uint32_t* snew = nullptr;  // s_new NTT per modulus [3][deg]
+  HE_CUDA(cudaMallocAsync(&snew, 3ull * deg * sizeof(uint32_t), st), "alloc");
+  for (int j = 0; j < 3; ++j) {
+    k_reduce_signed<<<grid_for(deg), 256, 0, st>>>(s_new, deg, M.m[j], snew + (size_t)j * deg);
+    HE_CUDA(ntt_forward(tabs[j], snew + (size_t)j * deg, 1, deg, st), "NTT(s_new)");
+  }
+  for (uint32_t i = 0; i < 2; ++i)
+    for (uint32_t j = 0; j < 3; ++j) {
+      const uint32_t q = M.m[j];
+      // g_{i,j} = P * Qhat_i mod q_j for j == i, else 0  (Qhat_0 = q1, Qhat_1 = q0)
+      const uint32_t g = (j == i) ? (uint32_t)((uint64_t)(M.m[2] % q) * (M.m[1 - i] % q) % q) : 0u;
+      uint32_t* alpha = ksk + ((size_t)(i * 2 + 0) * 3 + j) * deg;
+      uint32_t* beta = ksk + ((size_t)(i * 2 + 1) * 3 + j) * deg;
+      k_ksk_prep<<<grid_for(deg), 256, 0, st>>>(seed, id, i, j, q, g, s_old, deg, alpha, beta);
+      HE_CUDA(ntt_forward(tabs[j], alpha, 1, deg, st), "NTT(alpha)");
+      HE_CUDA(ntt_forward(tabs[j], beta, 1, deg, st), "NTT(t)");
+      k_ksk_beta<<<grid_for(deg), 256, 0, st>>>(alpha, snew + (size_t)j * deg, deg, q, beta);
+    }
+  cudaFreeAsync(snew, st);
+  return HE_OK;
+}
+
 extern "C" he_status he_rhombus_keygen(const he_context* c, uint64_t seed, const int32_t* s_dev, int32_t* s_small_dev,
                                        int32_t* s_up_dev, uint32_t* s_up_ntt_dev, uint32_t* ksk_dec_dev,
                                        uint32_t* gal_dev, void* stream) {
@@ -341,30 +367,8 @@ extern "C" he_status he_rhombus_keygen(const he_context* c, uint64_t seed, const
     k_reduce_signed<<<grid_for(N), 256, 0, st>>>(s_up_dev, N, M.m[L], dst);
     HE_CUDA(ntt_forward(c->ntt[L], dst, 1, N, st), "NTT(s_up)");
   }
-  // scratch: s_new NTT per modulus [3][deg] + signed s_old [deg]
   auto make_ksk = [&](uint32_t id, const int32_t* s_old, const int32_t* s_new, uint32_t deg, const NttTable* tabs,
-                      uint32_t* ksk) -> he_status {
-    uint32_t* snew = nullptr;
-    HE_CUDA(cudaMallocAsync(&snew, 3ull * deg * sizeof(uint32_t), st), "alloc");
-    for (int j = 0; j < 3; ++j) {
-      k_reduce_signed<<<grid_for(deg), 256, 0, st>>>(s_new, deg, M.m[j], snew + (size_t)j * deg);
-      HE_CUDA(ntt_forward(tabs[j], snew + (size_t)j * deg, 1, deg, st), "NTT(s_new)");
-    }
-    for (uint32_t i = 0; i < 2; ++i)
-      for (uint32_t j = 0; j < 3; ++j) {
-        const uint32_t q = M.m[j];
-        // g_{i,j} = P * Qhat_i mod q_j for j == i, else 0  (Qhat_0 = q1, Qhat_1 = q0)
-        const uint32_t g = (j == i) ? (uint32_t)((uint64_t)(M.m[2] % q) * (M.m[1 - i] % q) % q) : 0u;
-        uint32_t* alpha = ksk + ((size_t)(i * 2 + 0) * 3 + j) * deg;
-        uint32_t* beta = ksk + ((size_t)(i * 2 + 1) * 3 + j) * deg;
-        k_ksk_prep<<<grid_for(deg), 256, 0, st>>>(seed, id, i, j, q, g, s_old, deg, alpha, beta);
-        HE_CUDA(ntt_forward(tabs[j], alpha, 1, deg, st), "NTT(alpha)");
-        HE_CUDA(ntt_forward(tabs[j], beta, 1, deg, st), "NTT(t)");
-        k_ksk_beta<<<grid_for(deg), 256, 0, st>>>(alpha, snew + (size_t)j * deg, deg, q, beta);
-      }
-    cudaFreeAsync(snew, st);
-    return HE_OK;
-  };
+                      uint32_t* ksk) { return make_ksk_dev(M, seed, id, s_old, s_new, deg, tabs, ksk, st); };
   he_status s = make_ksk(0, s_dev, s_up_dev, N, c->ntt, ksk_dec_dev);
   if (s) return s;
   int32_t* sk = nullptr;
@@ -589,6 +593,303 @@ extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct
     ledger->pc_mults += (int64_t)p->n_out * p->p_in;
     ledger->ct_rotations += (int64_t)(n - 1) * p->p_out;
     ledger->rescales += 1;
+  }
+  return HE_OK;
+}
+
+// ======================================================================== MLWE -> RLWE ring packing
+// SURVEY.md §8f1; restated from oracle/he_oracle_rhombus.c (or_ring_pack), bit-exact.  The leaves are
+// the level-1 PCMM products C_y (he_pcmm_run_level1): A_y[k m - j] = a'_y[j][m], B_y[k m] = b'_y[m],
+// scaled by k^-1.  PackLWEs over the subring Z[X^k] runs the K6 packing level at degree N: level l
+// combines E + X^{k/2^l} O + sigma_g(E - X^{k/2^l} O), g = 1 + 2^l d, with one hybrid Galois key
+// switch per combine; log2 k levels turn each k-row block into one RLWE ciphertext, then rescale.
+namespace {
+
+// leaves a part [L][cnt][2][N] (coefficient form) from the MLWE-layout words raw_a [L][n_out][k][d]:
+// one CTA per (32 positions m, row, limb): transposing tile [j][m] in smem, coalesced on both sides
+__global__ void __launch_bounds__(256) k_rp_leaves_a(const uint32_t* __restrict__ raw_a, uint64_t limb_stride,
+                                                     uint32_t y0, uint32_t d, uint32_t k, uint32_t N, uint32_t cnt,
+                                                     uint32_t kinv0, uint32_t kinvp0, uint32_t kinv1, uint32_t kinvp1,
+                                                     uint32_t q0, uint32_t q1, uint32_t* __restrict__ leaves) {
+  __shared__ uint32_t tile[256 * 33];  // [j][m], k <= 256
+  const uint32_t m0 = blockIdx.x * 32, yl = blockIdx.y, L = blockIdx.z;
+  const uint32_t q = L ? q1 : q0, kinv = L ? kinv1 : kinv0, kinvp = L ? kinvp1 : kinvp0;
+  const uint32_t* src = raw_a + L * limb_stride + (size_t)(y0 + yl) * N + m0;
+  for (uint32_t i = threadIdx.x; i < 32 * k; i += blockDim.x) tile[(i >> 5) * 33 + (i & 31)] = src[(size_t)d * (i >> 5) + (i & 31)];
+  __syncthreads();
+  uint32_t* dst = leaves + (((size_t)L * cnt + yl) * 2 + 0) * N;
+  for (uint32_t i = threadIdx.x; i < 32 * k; i += blockDim.x) {
+    const uint32_t mm = i / k, j = k - 1 - (i % k);
+    uint32_t v = tile[j * 33 + mm];
+    int64_t c = (int64_t)k * (m0 + mm) - j;
+    if (c < 0) {
+      c += N;
+      v = v ? q - v : 0;
+    }
+    dst[c] = shoup_mul(v, kinv, kinvp, q);
+  }
+}
+// leaves b part: B_y[c] = b'_y[c / k] for c = 0 mod k, else 0;  raw_b [L][n_out/k][N] (RLWE order)
+__global__ void k_rp_leaves_b(const uint32_t* __restrict__ raw_b, uint64_t limb_stride, uint32_t y0, uint32_t k,
+                              uint32_t logN, uint32_t cnt, uint32_t kinv0, uint32_t kinvp0, uint32_t kinv1,
+                              uint32_t kinvp1, uint32_t q0, uint32_t q1, uint32_t* __restrict__ leaves) {
+  const uint32_t N = 1u << logN, L = blockIdx.y;
+  const uint32_t q = L ? q1 : q0, kinv = L ? kinv1 : kinv0, kinvp = L ? kinvp1 : kinvp0;
+  const uint64_t total = (uint64_t)cnt << logN;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t yl = (uint32_t)(x >> logN), c = (uint32_t)(x & (N - 1)), y = y0 + yl;
+    uint32_t v = 0;
+    if (c % k == 0) v = shoup_mul(raw_b[L * limb_stride + (size_t)(y / k) * N + (y % k) + c], kinv, kinvp, q);
+    leaves[(((size_t)L * cnt + yl) * 2 + 1) * N + c] = v;
+  }
+}
+// packing level at degree N (no smem staging: the polynomial does not fit), see k_pack_comb1
+__global__ void k_rp_comb1(const uint32_t* __restrict__ A, uint32_t cnt_in, uint32_t half, uint32_t logN,
+                           const uint32_t* __restrict__ mono /* [2][N] */, const uint32_t* __restrict__ perm, Mods M,
+                           uint32_t* __restrict__ An, uint32_t* __restrict__ T, uint32_t* __restrict__ C) {
+  const uint32_t N = 1u << logN, ab = blockIdx.y, L = blockIdx.z, cnt_out = cnt_in / 2;
+  const uint32_t q = M.m[L];
+  const uint64_t mu = M.mu[L];
+  const uint32_t* ml = mono + (size_t)L * N;
+  const uint64_t total = (uint64_t)cnt_out << logN;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t idx = (uint32_t)(x >> logN), c = (uint32_t)(x & (N - 1));
+    const uint32_t o = idx / half, s_ = idx % half;
+    const uint32_t e_i = o * 2 * half + s_, o_i = e_i + half;
+    const uint32_t* Eb = A + (((size_t)L * cnt_in + e_i) * 2 + ab) * N;
+    const uint32_t* Ob = A + (((size_t)L * cnt_in + o_i) * 2 + ab) * N;
+    const uint32_t e = Eb[c], mo = mulmod_b(Ob[c], ml[c], mu, q);
+    An[(((size_t)L * cnt_out + idx) * 2 + ab) * N + c] = add_mod(e, mo, q);
+    const uint32_t pc = perm[c];
+    const uint32_t v = sub_mod(Eb[pc], mulmod_b(Ob[pc], ml[pc], mu, q), q);
+    T[(((size_t)L * cnt_out + idx) * 2 + ab) * N + c] = v;
+    if (ab == 0) C[((size_t)L * cnt_out + idx) * N + c] = v;
+  }
+}
+// rescale by q1: A [L][nb][2][N] coefficient form -> out [nb][2][N]
+__global__ void k_rp_rescale(const uint32_t* __restrict__ A, uint64_t per_l, uint32_t q0, uint32_t q1, uint32_t q1inv,
+                             uint32_t q1invp, uint32_t* __restrict__ out) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < per_l; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x0 = A[x], x1 = A[per_l + x];
+    uint32_t t;
+    if (x1 > (q1 >> 1)) t = csub(x0 + (q1 - x1), q0);
+    else t = sub_mod(x0, x1, q0);
+    out[x] = shoup_mul(t, q1inv, q1invp, q0);
+  }
+}
+
+uint64_t find_psi(uint32_t q, uint32_t n) {  // the root ntt_table_init uses
+  for (uint64_t g = 2; g < q; ++g) {
+    const uint64_t cand = powmod_h(g, (q - 1) / (2ull * n), q);
+    if (powmod_h(cand, n, q) == q - 1) return cand;
+  }
+  return 0;
+}
+
+}  // namespace
+
+struct he_ring_pack_plan {
+  const he_context* ctx;
+  uint32_t n_out, blocks, chunk, d, k, N, logN, logk;
+  uint32_t* tables;  // owned: perm [logk][N], mono [logk][2][N]
+  Mods M;
+  uint32_t qhinv[2], pinv[2], q1inv, q1invp, kinv[2], kinvp[2];
+};
+
+extern "C" he_status he_ring_pack_keygen(const he_context* c, uint64_t seed, const int32_t* s_dev, uint32_t* gal_dev,
+                                         void* stream) {
+  if (!c || !s_dev || !gal_dev) return fail(HE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N, d = c->R.d;
+  const int logk = ilog2_u(c->R.k);
+  const Mods M = make_mods(c->R);
+  int32_t* sk = nullptr;
+  HE_CUDA(cudaMallocAsync(&sk, N * sizeof(int32_t), st), "alloc");
+  he_status s = HE_OK;
+  for (int lv = 1; lv <= logk && !s; ++lv) {
+    k_secret_auto<<<grid_for(N), 256, 0, st>>>(s_dev, N, (d << lv) + 1, sk);
+    s = make_ksk_dev(M, seed, 0x100 + lv, sk, s_dev, N, c->ntt, gal_dev + (size_t)(lv - 1) * 12 * N, st);
+  }
+  cudaFreeAsync(sk, st);
+  if (s) return s;
+  return cudaGetLastError() == cudaSuccess ? HE_OK : fail(HE_ECUDA, "ring pack keygen launch failed");
+}
+
+extern "C" he_status he_ring_pack_plan_create(const he_context* c, uint32_t n_out, he_ring_pack_plan** out) {
+  if (!c || !out) return fail(HE_EINVAL, "null argument");
+  const uint32_t k = c->R.k;
+  if (n_out == 0 || n_out % k) return fail(HE_EINVAL, "n_out (%u) must be a positive multiple of k = %u", n_out, k);
+  if (k > 256 || c->R.d % 32) return fail(HE_EINVAL, "ring packing needs k <= 256 and d a multiple of 32");
+  he_ring_pack_plan* p = new (std::nothrow) he_ring_pack_plan();
+  if (!p) return fail(HE_ENOMEM, "out of host memory");
+  p->ctx = c;
+  p->n_out = n_out;
+  p->d = c->R.d;
+  p->k = k;
+  p->N = c->R.N;
+  p->logN = (uint32_t)ilog2_u(p->N);
+  p->logk = (uint32_t)ilog2_u(k);
+  p->blocks = n_out / k;
+  static const int env_chunk = getenv("HE_RP_CHUNK") ? atoi(getenv("HE_RP_CHUNK")) : 0;  // blocks per pass
+  p->chunk = env_chunk > 0 ? (uint32_t)env_chunk : 8;
+  if (p->chunk > p->blocks) p->chunk = p->blocks;
+  p->M = make_mods(c->R);
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t qi = p->M.m[i];
+    p->qhinv[i] = (uint32_t)powmod_h(p->M.m[1 - i] % qi, qi - 2, qi);
+    p->pinv[i] = (uint32_t)powmod_h(p->M.m[2] % qi, qi - 2, qi);
+    p->kinv[i] = (uint32_t)powmod_h(k, qi - 2, qi);
+    p->kinvp[i] = shoup_pre(p->kinv[i], qi);
+  }
+  p->q1inv = (uint32_t)powmod_h(p->M.m[1] % p->M.m[0], p->M.m[0] - 2, p->M.m[0]);
+  p->q1invp = shoup_pre(p->q1inv, p->M.m[0]);
+  // NTT-domain tables at degree N: output c of the forward transform holds p(psi^{2 brv(c) + 1})
+  const uint32_t N = p->N, logN = p->logN, logk = p->logk;
+  std::vector<uint32_t> h((size_t)logk * N * 3);
+  uint32_t* perm = h.data();
+  uint32_t* mono = h.data() + (size_t)logk * N;
+  std::vector<uint32_t> pw(2ull * N);
+  for (int L = 0; L < 2; ++L) {
+    const uint32_t q = p->M.m[L];
+    const uint64_t psi = find_psi(q, N);
+    if (!psi) {
+      delete p;
+      return fail(HE_EINVAL, "q%d is not NTT-friendly at degree %u", L, N);
+    }
+    uint64_t acc = 1;
+    for (uint64_t e = 0; e < 2ull * N; ++e, acc = acc * psi % q) pw[e] = (uint32_t)acc;
+    for (uint32_t lv = 1; lv <= logk; ++lv) {
+      const uint64_t ex = k >> lv;  // X^{k / 2^l}
+      for (uint32_t cc = 0; cc < N; ++cc) {
+        const uint64_t e = 2ull * bitrev_h(cc, (int)logN) + 1;
+        mono[((size_t)(lv - 1) * 2 + L) * N + cc] = pw[(e * ex) % (2ull * N)];
+      }
+    }
+  }
+  for (uint32_t lv = 1; lv <= logk; ++lv) {
+    const uint64_t g = ((uint64_t)p->d << lv) + 1;
+    for (uint32_t cc = 0; cc < N; ++cc) {
+      const uint64_t e = 2ull * bitrev_h(cc, (int)logN) + 1;
+      const uint64_t eg = (e * g) % (2ull * N);
+      perm[(size_t)(lv - 1) * N + cc] = bitrev_h((uint32_t)((eg - 1) / 2), (int)logN);
+    }
+  }
+  if (cudaMalloc(&p->tables, h.size() * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemcpy(p->tables, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+    delete p;
+    return fail(HE_ECUDA, "ring pack tables");
+  }
+  *out = p;
+  return HE_OK;
+}
+
+extern "C" he_status he_ring_pack_plan_destroy(he_ring_pack_plan* p) {
+  if (p) {
+    if (p->tables) cudaFree(p->tables);
+    delete p;
+  }
+  return HE_OK;
+}
+
+struct RpWs {
+  uint32_t *A0, *A1, *T, *C, *D, *UW, *LB;
+};
+static uint64_t rp_ws_words(const he_ring_pack_plan* p, RpWs* w, uint32_t* base) {
+  const uint64_t N = p->N, cnt = (uint64_t)p->chunk * p->k, c1 = cnt / 2;
+  uint64_t off = 0;
+  auto take = [&](uint32_t*& ptr, uint64_t words) {
+    if (w) ptr = base + off;
+    off += (words + 63) & ~63ull;
+  };
+  RpWs dummy;
+  RpWs& r = w ? *w : dummy;
+  take(r.A0, 2ull * cnt * 2 * N);
+  take(r.A1, 2ull * c1 * 2 * N);
+  take(r.T, 2ull * c1 * 2 * N);
+  take(r.C, 2ull * c1 * N);
+  take(r.D, 6ull * c1 * N);
+  take(r.UW, 6ull * c1 * N);
+  take(r.LB, 4ull * c1 * N);
+  return off;
+}
+
+extern "C" he_status he_ring_pack_workspace_bytes(const he_ring_pack_plan* p, uint64_t* bytes) {
+  if (!p || !bytes) return fail(HE_EINVAL, "null argument");
+  *bytes = rp_ws_words(p, nullptr, nullptr) * sizeof(uint32_t);
+  return HE_OK;
+}
+
+extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t* raw_b, const uint32_t* raw_a,
+                                      const uint32_t* gal, uint32_t* out, void* ws_dev, uint64_t ws_bytes,
+                                      void* stream, he_ledger* ledger) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  if (!raw_b || !raw_a || !gal || !out || !ws_dev) return fail(HE_EINVAL, "null argument");
+  const uint64_t need = rp_ws_words(p, nullptr, nullptr) * sizeof(uint32_t);
+  if (ws_bytes < need)
+    return fail(HE_EINVAL, "workspace too small (%llu < %llu)", (unsigned long long)ws_bytes, (unsigned long long)need);
+  cudaStream_t st = (cudaStream_t)stream;
+  const he_context* c = p->ctx;
+  const uint32_t N = p->N, k = p->k, d = p->d, q0 = p->M.m[0], q1 = p->M.m[1];
+  RpWs w;
+  rp_ws_words(p, &w, (uint32_t*)ws_dev);
+  const uint32_t* perm_base = p->tables;
+  const uint32_t* mono_base = p->tables + (size_t)p->logk * N;
+  for (uint32_t b0 = 0; b0 < p->blocks; b0 += p->chunk) {
+    const uint32_t nb = (p->blocks - b0 < p->chunk) ? p->blocks - b0 : p->chunk;
+    uint32_t cnt = nb * k;
+    const uint32_t y0 = b0 * k;
+    k_rp_leaves_a<<<dim3(d / 32, cnt, 2), 256, 0, st>>>(raw_a, (uint64_t)p->n_out * N, y0, d, k, N, cnt, p->kinv[0],
+                                                         p->kinvp[0], p->kinv[1], p->kinvp[1], q0, q1, w.A0);
+    {
+      dim3 g = grid_for((uint64_t)cnt * N);
+      g.y = 2;
+      k_rp_leaves_b<<<g, 256, 0, st>>>(raw_b, (uint64_t)p->blocks * N, y0, k, p->logN, cnt, p->kinv[0], p->kinvp[0],
+                                       p->kinv[1], p->kinvp[1], q0, q1, w.A0);
+    }
+    for (int L = 0; L < 2; ++L)
+      HE_CUDA(ntt_forward(c->ntt[L], w.A0 + (size_t)L * cnt * 2 * N, cnt * 2, N, st), "NTT(leaves)");
+    uint32_t* A = w.A0;
+    uint32_t* An = w.A1;
+    for (uint32_t lv = 1; lv <= p->logk; ++lv) {
+      const uint32_t cnt_out = cnt / 2, half = k >> lv;
+      const uint64_t cn = (uint64_t)cnt_out * N;
+      {
+        dim3 g = grid_for(cn);
+        g.y = 2;
+        g.z = 2;
+        k_rp_comb1<<<g, 256, 0, st>>>(A, cnt, half, p->logN, mono_base + (size_t)(lv - 1) * 2 * N,
+                                      perm_base + (size_t)(lv - 1) * N, p->M, An, w.T, w.C);
+      }
+      for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt[L], w.C + (size_t)L * cn, cnt_out, N, st), "INTT(T_a)");
+      k_modup<<<grid_for(cn), 256, 0, st>>>(w.C, w.T, p->logN, cn, p->M, p->qhinv[0], p->qhinv[1], w.D);
+      HE_CUDA(ntt_forward(c->ntt[0], w.D + (0 * 2 + 1) * cn, cnt_out, N, st), "NTT(d1 mod q0)");
+      HE_CUDA(ntt_forward(c->ntt[1], w.D + (1 * 2 + 0) * cn, cnt_out, N, st), "NTT(d0 mod q1)");
+      HE_CUDA(ntt_forward(c->ntt[2], w.D + (2 * 2 + 0) * cn, 2 * cnt_out, N, st), "NTT(d mod P)");
+      k_mac<<<grid_for(cn), 256, 0, st>>>(w.D, gal + (size_t)(lv - 1) * 12 * N, N, cn, p->M, w.UW);
+      HE_CUDA(ntt_inverse(c->ntt[2], w.UW + 2 * 2 * cn, 2 * cnt_out, N, st), "INTT(U_P, W_P)");
+      k_moddown_lift<<<grid_for(2 * cn), 256, 0, st>>>(w.UW + 2 * 2 * cn, cn, p->M, w.LB);
+      HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2 * cnt_out, N, st), "NTT(lift q0)");
+      HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2 * cn, 2 * cnt_out, N, st), "NTT(lift q1)");
+      {
+        dim3 g = grid_for(cn);
+        g.y = 2;
+        k_pack_comb2<<<g, 256, 0, st>>>(w.UW, w.LB, w.T, cnt_out, p->logN, p->M, p->pinv[0], p->pinv[1], An);
+      }
+      uint32_t* tmp = A;
+      A = An;
+      An = (lv == 1) ? w.A0 : tmp;
+      cnt = cnt_out;
+    }
+    // cnt == nb: INTT and rescale into out [b0 ..][2][N]
+    for (int L = 0; L < 2; ++L)
+      HE_CUDA(ntt_inverse(c->ntt[L], A + (size_t)L * nb * 2 * N, nb * 2, N, st), "INTT(packed)");
+    k_rp_rescale<<<grid_for((uint64_t)nb * 2 * N), 256, 0, st>>>(A, (uint64_t)nb * 2 * N, q0, q1, p->q1inv, p->q1invp,
+                                                                  out + (size_t)b0 * 2 * N);
+  }
+  HE_CUDA(cudaGetLastError(), "ring pack launch");
+  if (ledger) {
+    ledger->ct_rotations += (int64_t)(k - 1) * p->blocks;
+    ledger->rescales += p->blocks;
   }
   return HE_OK;
 }

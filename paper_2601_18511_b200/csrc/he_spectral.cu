@@ -343,7 +343,13 @@ __global__ void __launch_bounds__(256) spec_inverse_kernel(const uint32_t* __res
     if (x1 > (q1 >> 1)) t = csub(x0 + (q1 - x1), q0);
     else t = sub_mod(x0, x1, q0);
     const uint32_t j = k - 1 - u;
-    out_a[(size_t)(y - row0) * N + (size_t)d * j + m0 + mm] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);
+    const size_t o = (size_t)(y - row0) * N + (size_t)d * j + m0 + mm;
+    if (cst.out1) {  // level-1 words of both limbs
+      out_a[o] = x0;
+      cst.out1[o] = x1;
+      continue;
+    }
+    out_a[o] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);
   }
 }
 
@@ -478,6 +484,11 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
     const uint32_t u0 = (lane & 15) + 128 * (lane >> 4);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
+      if (cst.out1) {  // level-1 mode: both limbs, no rescale
+        xs0[m * kInv512Ld + u0 + 16 * e] = x[0][e];
+        xs1[m * kInv512Ld + u0 + 16 * e] = x[1][e];
+        continue;
+      }
       uint32_t t;
       if (x[1][e] > (q1 >> 1)) t = csub(x[0][e] + (q1 - x[1][e]), q0);
       else t = sub_mod(x[0][e], x[1][e], q0);
@@ -487,10 +498,12 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
   __syncthreads();
   // phase C: a'[y][d j + m0 + m] = res[m][u = 255 - j]: 64-byte row segments
   const uint32_t N = d * 256;
-  uint32_t* dst = out_a + (size_t)(y - row0) * N + m0;
+  const size_t off = (size_t)(y - row0) * N + m0;
+  const uint32_t* res = cst.out1 ? xs0 : xs1;
   for (uint32_t i = threadIdx.x; i < 256 * kInv512Cols; i += 256) {
     const uint32_t m = i & 15, j = i >> 4;
-    dst[(size_t)d * j + m] = xs1[m * kInv512Ld + 255 - j];
+    out_a[off + (size_t)d * j + m] = res[m * kInv512Ld + 255 - j];
+    if (cst.out1) cst.out1[off + (size_t)d * j + m] = xs1[m * kInv512Ld + 255 - j];
   }
 }
 
@@ -622,6 +635,13 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
     const Inv1kLimb L[2] = {{xs0 + b * kInv1kLd, tws, q0}, {xs1 + b * kInv1kLd, tws + 992, q1}};
     uint32_t x[2][32];
     inv1024_pair(L, cst, lane, x);
+    if (cst.out1) {  // level-1 mode: both limbs, no rescale
+#pragma unroll
+      for (int e = 0; e < 24; ++e) {
+        xs0[b * kInv1kLd + lane + 32 * e + (e >> 3)] = x[0][e];
+        xs1[b * kInv1kLd + lane + 32 * e + (e >> 3)] = x[1][e];
+      }
+    } else
 #pragma unroll
     for (int e = 0; e < 24; ++e) {
       uint32_t t;
@@ -637,7 +657,13 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
   const uint32_t N = d * 256, m = 3 * b0 + lane;
   if (lane < 24 && m < d) {
     const uint32_t bl = lane / 3, r3 = lane - 3 * bl, src = bl * kInv1kLd + 257 * r3 + 255;
-    if (peers.n == 0) {
+    if (cst.out1) {
+      const size_t o = (size_t)(y - row0) * N + m;
+      for (uint32_t j = warp; j < 256; j += 8) {
+        out_a[o + (size_t)d * j] = xs0[src - j];
+        cst.out1[o + (size_t)d * j] = xs1[src - j];
+      }
+    } else if (peers.n == 0) {
       uint32_t* dst = out_a + (size_t)(y - row0) * N + m;
 #pragma unroll 4
       for (uint32_t j = warp; j < 256; j += 8) dst[(size_t)d * j] = xs1[src - j];
@@ -975,6 +1001,7 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
                                 uint32_t row0, uint32_t rows, uint32_t L, uint32_t nblk, uint32_t nbp,
                                 const SpecInvConst& cst, uint32_t* out_a, const OutPeers& peers, cudaStream_t s) {
   if (peers.n > 0 && L != 1024) return cudaErrorNotSupported;  // fused output only on the L = 1024 fast path
+  if (peers.n > 0 && cst.out1) return cudaErrorNotSupported;
   if (L == 1024) {
     if (Rg.k != 256) return cudaErrorInvalidValue;
     dim3 grid((nblk + kInv1kBlocks - 1) / kInv1kBlocks, rows);

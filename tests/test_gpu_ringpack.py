@@ -1,0 +1,141 @@
+"""MLWE -> RLWE ring packing on the GPU against the CPU oracle.
+
+Bar: bit-exact on every word -- the level-1 (un-rescaled) PCMM words of both limbs, the Galois
+keys, and the packed level-0 RLWE ciphertexts -- at toy size against oracle.pcmm_limb /
+oracle.ring_pack_keys / oracle.pcmm_ring_pack; at Llama sizes the level-1 words must rescale to
+exactly the words of the (separately tested) level-0 PCMM output, and the packed ciphertexts must
+decrypt to A @ W^T within the stated CKKS precision (>= 14 bits; paper target 12)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2601_18511_b200 import (HeParams, make_mlwe_pcmm_plan, make_ring_pack_plan, pcmm_level1, pcmm_mlwe,
+                                   pcmm_packed, ring_pack_keygen)
+
+from test_gpu_pcmm import setup, u32
+
+pytestmark = pytest.mark.gpu
+ALGOS = ["spectral", "direct"]
+
+
+def _raw_oracle(P, W, A):
+    ct = O.encrypt(P, 11, O.keygen(P, 7), O.encode_acts(P, A))
+    Wt = O.encode_weights(P, W)
+    return Wt, ct, [O.pcmm_limb(P, Wt, ct, L) for L in range(2)]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("n_out,n_in", [(16, 16), (64, 48), (32, 256)])
+def test_toy_level1_words_bit_exact(n_out, n_in, algo):
+    P = HeParams.toy()
+    ctx, sk, A, W, X = setup(P, n_out, n_in)
+    _, _, raw = _raw_oracle(P, W, A)
+    d, k = P.mlwe_degree, P.mlwe_rank
+    rb, ra = pcmm_level1(ctx, make_mlwe_pcmm_plan(ctx, W, algo=algo), X)
+    rb, ra = u32(rb), u32(ra)
+    for L in range(2):
+        assert np.array_equal(ra[L], raw[L][:, d:]), f"limb {L} a' words"
+        for y in range(n_out):
+            assert np.array_equal(rb[L, y // k, y % k + k * np.arange(d)], raw[L][y, :d]), f"limb {L} b' row {y}"
+
+
+def test_toy_galois_keys_match_oracle():
+    P = HeParams.toy()
+    ctx, sk, A, W, X = setup(P, 16, 16)
+    keys = ring_pack_keygen(ctx, sk, seed=5)
+    ref = O.ring_pack_keys(P, 5, O.keygen(P, 7))
+    # device keys are NTT-domain: compare after the inverse transform per modulus
+    import torch
+
+    g = keys.gal.clone()
+    lg, N = g.shape[0], P.N
+    for j in range(3):
+        blk = g[:, :, :, j, :].contiguous().reshape(-1, N)
+        ctx_ntt_inverse(ctx, blk, j)
+        g[:, :, :, j, :] = blk.reshape(lg, 2, 2, N)
+    torch.cuda.synchronize()
+    assert np.array_equal(u32(g), ref)
+
+
+def ctx_ntt_inverse(ctx, data, limb):
+    from paper_2601_18511_b200 import native
+
+    native.call("he_ntt_inverse", ctx.handle, data.data_ptr(), ctx.params.N, limb, int(data.shape[0]), ctx.params.N,
+                ctx.stream())
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("n_out,n_in", [(16, 16), (64, 48), (48, 128)])
+def test_toy_packed_ciphertexts_bit_exact_and_decrypt(n_out, n_in, algo):
+    P = HeParams.toy()
+    ctx, sk, A, W, X = setup(P, n_out, n_in, seed=n_out + n_in)
+    Wt, ct, raw = _raw_oracle(P, W, A)
+    gal = O.ring_pack_keys(P, 5, O.keygen(P, 7))
+    ref = O.ring_pack(P, O.ring_pack_leaves(P, raw), gal)[1]
+    keys = ring_pack_keygen(ctx, sk, seed=5)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
+    rp = make_ring_pack_plan(ctx, n_out)
+    before = ctx.ledger.snapshot()
+    Y = pcmm_packed(ctx, plan, rp, keys, X)
+    diff = ctx.ledger.diff(before)
+    k = P.mlwe_rank
+    assert diff["ct_rotations"] == (k - 1) * n_out // k and diff["rescales"] == n_out // k
+    assert Y.level == 0 and Y.n_cols == n_out and tuple(Y.data.shape) == (n_out // k, 1, 2, P.N)
+    got = u32(Y.data)[:, 0]
+    assert np.array_equal(got, ref), f"{int((got != ref).sum())} words differ"
+    dec = ctx.decrypt_acts(sk, Y)
+    refm = A @ W.T
+    err = np.abs(dec - refm).max()
+    assert err < np.abs(refm).max() * 2.0 ** -14
+
+
+def test_ring_pack_errors():
+    P = HeParams.toy()
+    ctx, sk, A, W, X = setup(P, 16, 16)
+    with pytest.raises(ValueError):
+        make_ring_pack_plan(ctx, 24)   # not a multiple of k
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    with pytest.raises(ValueError):
+        pcmm_packed(ctx, plan, make_ring_pack_plan(ctx, 32), ring_pack_keygen(ctx, sk, 5), X)
+
+
+def _rescale(P, x0, x1):
+    import torch
+
+    q0, q1 = int(P.moduli[0]), int(P.moduli[1])
+    x0 = x0.to(torch.int64) & 0xFFFFFFFF
+    x1 = x1.to(torch.int64) & 0xFFFFFFFF
+    x1c = torch.where(x1 > q1 // 2, x1 - q1, x1)
+    t = torch.remainder(x0 - x1c, q0)
+    return torch.remainder(t * pow(q1, q0 - 2, q0), q0)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_llama_level1_words_rescale_to_pcmm_output(algo):
+    """Full-output property at a Llama shape: rescale(level-1 words) == the level-0 PCMM words."""
+    import torch
+
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, 512, 1024, seed=3)
+    plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
+    Y = pcmm_mlwe(ctx, plan, X)
+    rb, ra = pcmm_level1(ctx, plan, X)
+    torch.cuda.synchronize()
+    assert torch.equal(_rescale(P, ra[0], ra[1]), Y.out_a.to(torch.int64) & 0xFFFFFFFF)
+    assert torch.equal(_rescale(P, rb[0], rb[1]), Y.out_b.to(torch.int64) & 0xFFFFFFFF)
+
+
+@pytest.mark.parametrize("n_out,n_in", [(512, 1024), (1024, 4096)])
+def test_llama_packed_decrypts_to_product(n_out, n_in):
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, n_out, n_in, seed=5)
+    keys = ring_pack_keygen(ctx, sk, seed=9)
+    Y = pcmm_packed(ctx, make_mlwe_pcmm_plan(ctx, W), make_ring_pack_plan(ctx, n_out), keys, X)
+    dec = ctx.decrypt_acts(sk, Y)
+    ref = A @ W.T
+    err = np.abs(dec - ref).max()
+    bits = -math.log2(err / np.abs(ref).max())
+    assert bits >= 14, f"{bits:.1f} bits"

@@ -121,3 +121,48 @@ def test_baseline_config1_matches_hesim():
     np.testing.assert_allclose(got.T, gt["hesim_bsgs"], atol=2 ** -16)
     np.testing.assert_array_equal(gt["pin_clear_2x2_power1"], [[1.0, 8.0], [6.0, 2.0]])
     assert int(gt["hesim_level_drop"]) == 1      # the reference kernel also consumes one level
+
+
+def test_ring_pack_decrypts_to_product_in_activation_layout():
+    """§8f1 oracle: PCMM at level 1 + PackLWEs over Z[X^k] + rescale gives level-0 RLWE blocks whose
+    decryption, decoded in the INPUT activation layout, is A @ W^T; and BASELINE config 1's toy
+    product packs to hesim's golden values."""
+    rng = np.random.default_rng(3)
+    n_out, n_in = 32, 48
+    A = rng.uniform(-1, 1, (P.tokens, n_in))
+    W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
+    s = O.keygen(P, 7)
+    ct = O.encrypt(P, 11, s, O.encode_acts(P, A))
+    gal = O.ring_pack_keys(P, 5, s)
+    out = O.pcmm_ring_pack(P, O.encode_weights(P, W), ct, gal)
+    assert out.shape == (n_out // P.mlwe_rank, 2, P.N)
+    ph = np.stack([O.decrypt_under(P, out[b, 0], out[b, 1], s, P.moduli[0]) for b in range(out.shape[0])])
+    dec = O.decode_acts(P, ph, n_out)
+    ref = A @ W.T
+    assert np.abs(dec - ref).max() < np.abs(ref).max() * 2.0 ** -14
+    gt = np.load(GOLD / "pcmm_toy_golden.npz")
+    ct = O.encrypt(P, 11, s, O.encode_acts(P, gt["M"].T.copy()))
+    out = O.pcmm_ring_pack(P, O.encode_weights(P, gt["W"]), ct, gal)
+    ph = O.decrypt_under(P, out[0, 0], out[0, 1], s, P.moduli[0])[None]
+    np.testing.assert_allclose(O.decode_acts(P, ph, 16).T, gt["hesim_clear"], atol=2 ** -14)
+
+
+def test_ring_pack_leaves_trace_keeps_component_zero():
+    """The leaf construction: component 0 of C_y's phase (A_y s + B_y, scaled back by k) is the MLWE
+    row's phase -- the identity the subring trace relies on."""
+    rng = np.random.default_rng(4)
+    n_out, n_in = 16, 32
+    A = rng.uniform(-1, 1, (P.tokens, n_in))
+    W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
+    s = O.keygen(P, 7)
+    ct = O.encrypt(P, 11, s, O.encode_acts(P, A))
+    Wt = O.encode_weights(P, W)
+    raw = [O.pcmm_limb(P, Wt, ct, L) for L in range(2)]
+    leaves = O.ring_pack_leaves(P, raw)
+    d, k, q = P.mlwe_degree, P.mlwe_rank, int(P.moduli[0])
+    for y in (0, 5, 15):
+        ph = O.decrypt_under(P, leaves[y, 0, 0], leaves[y, 0, 1], s, q)[::k] * k % q
+        row = np.concatenate([raw[0][y]])[None]
+        # MLWE phase of row y at level 1, limb 0 (decrypt_mlwe takes level-0 words; compare mod q0)
+        ref = O.decrypt_mlwe(P, s, row)[0] % q
+        assert np.array_equal(ph % q, ref)
