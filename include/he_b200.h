@@ -194,19 +194,29 @@ he_status he_rhombus_run(const he_rhombus_plan* plan, const uint32_t* ct_in_dev,
  * like out_b), raw_a [2 limbs][n_out][k*d] (a' MLWE rows, like out_a), words mod q0 / q1. */
 he_status he_pcmm_run_level1(const he_pcmm_plan* plan, const uint32_t* ct_in_dev, uint32_t level, uint32_t* raw_b_dev,
                              uint32_t* raw_a_dev, void* workspace_dev, uint64_t workspace_bytes, void* stream);
-/* Galois keys sigma_g(s) -> s, g = 1 + 2^l d, l = 1 .. log2 k: u32 [log2 k][2][2][3][N] (NTT domain,
- * moduli q0 q1 P; key ids 0x100 + l) */
-he_status he_ring_pack_keygen(const he_context* ctx, uint64_t seed, const int32_t* s_dev, uint32_t* gal_dev,
-                              void* stream);
+/* Packing methods:
+ *   HE_RING_PACK_KEYSWITCH (default): MLWE -> RLWE key switching (HERMES / BCHPS style, SURVEY.md
+ *     App. B.4): block Y's packed phase is b'_Y + sum_j alpha_j(X) s_j(X^k) with alpha_j the
+ *     interleave of the block's a' component j; one hybrid key switch per j from s_j(X^k) to s,
+ *     summed before a single ModDown.  Keys: u32 [k][2][2][3][N] (ids 0x200 + j).
+ *   HE_RING_PACK_TRACE: PackLWEs over the subring Z[X^k] (CDKS21): log2 k levels of
+ *     E + X^{k/2^l} O + sigma_g(E - X^{k/2^l} O), g = 1 + 2^l d, one Galois key switch per combine.
+ *     Keys sigma_g(s) -> s: u32 [log2 k][2][2][3][N] (ids 0x100 + l).
+ * Keys are NTT domain, moduli q0 q1 P; both methods give identical plaintexts (different noise). */
+#define HE_RING_PACK_KEYSWITCH 0
+#define HE_RING_PACK_TRACE 1
+he_status he_ring_pack_key_bytes(const he_context* ctx, int method, uint64_t* bytes);
+he_status he_ring_pack_keygen(const he_context* ctx, int method, uint64_t seed, const int32_t* s_dev,
+                              uint32_t* keys_dev, void* stream);
 /* n_out must be a multiple of k */
-he_status he_ring_pack_plan_create(const he_context* ctx, uint32_t n_out, he_ring_pack_plan** out);
+he_status he_ring_pack_plan_create(const he_context* ctx, uint32_t n_out, int method, he_ring_pack_plan** out);
 he_status he_ring_pack_plan_destroy(he_ring_pack_plan* plan);
 he_status he_ring_pack_workspace_bytes(const he_ring_pack_plan* plan, uint64_t* bytes);
-/* step 2: raw words of step 1 -> level-0 RLWE ciphertexts out [n_out/k][2 (a, b)][N] under s.
- * PackLWEs over the subring Z[X^k] with hybrid key switching (dnum 2, special prime P), then
- * rescale by q1.  ledger: ct_rotations += (k - 1) n_out/k, rescales += n_out/k. */
+/* step 2: raw words of step 1 -> level-0 RLWE ciphertexts out [n_out/k][2 (a, b)][N] under s
+ * (hybrid key switching with dnum 2 and special prime P, then rescale by q1).  ledger: rescales +=
+ * n_out/k; the trace method also ct_rotations += (k - 1) n_out/k. */
 he_status he_ring_pack_run(const he_ring_pack_plan* plan, const uint32_t* raw_b_dev, const uint32_t* raw_a_dev,
-                           const uint32_t* gal_dev, uint32_t* out_dev, void* workspace_dev, uint64_t workspace_bytes,
+                           const uint32_t* keys_dev, uint32_t* out_dev, void* workspace_dev, uint64_t workspace_bytes,
                            void* stream, he_ledger* ledger);
 
 #ifdef __cplusplus

@@ -135,12 +135,12 @@ void or_ksk_gen(uint64_t seed, uint32_t id, const int32_t* s_old, const int32_t*
  *   ModDown: x_j = (X_j - [X_P]_centred) * P^-1 mod q_j
  * so that w + u s_new = c s_old + small.
  */
-void or_keyswitch(const uint32_t* c, const uint32_t* ksk, uint32_t n, const uint32_t* m, uint32_t* u, uint32_t* w) {
+/* ModUp + key product of one term, accumulated into U, W [3][n] (mod m_j) */
+static void ks_accumulate(const uint32_t* c, const uint32_t* ksk, uint32_t n, const uint32_t* m, uint32_t* U,
+                          uint32_t* W) {
   uint32_t* d[2];
   uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * n);
   uint32_t* dl = (uint32_t*)malloc(sizeof(uint32_t) * n);
-  uint32_t* U = (uint32_t*)calloc((size_t)3 * n, sizeof(uint32_t));
-  uint32_t* W = (uint32_t*)calloc((size_t)3 * n, sizeof(uint32_t));
   for (int i = 0; i < 2; ++i) {
     d[i] = (uint32_t*)malloc(sizeof(uint32_t) * n);
     const uint32_t qi = m[i];
@@ -157,6 +157,13 @@ void or_keyswitch(const uint32_t* c, const uint32_t* ksk, uint32_t n, const uint
       for (uint32_t k = 0; k < n; ++k) W[(size_t)j * n + k] = (uint32_t)(((uint64_t)W[(size_t)j * n + k] + t[k]) % q);
     }
   }
+  free(d[0]);
+  free(d[1]);
+  free(t);
+  free(dl);
+}
+/* ModDown: x_j = (X_j - [X_P]_centred) * P^-1 mod q_j */
+static void ks_moddown(const uint32_t* U, const uint32_t* W, uint32_t n, const uint32_t* m, uint32_t* u, uint32_t* w) {
   const uint32_t P = m[2];
   for (int j = 0; j < 2; ++j) {
     const uint32_t q = m[j];
@@ -169,10 +176,12 @@ void or_keyswitch(const uint32_t* c, const uint32_t* ksk, uint32_t n, const uint
       w[(size_t)j * n + k] = (uint32_t)mulmod(modq_i64((int64_t)W[(size_t)j * n + k] - wp, q), pinv, q);
     }
   }
-  free(d[0]);
-  free(d[1]);
-  free(t);
-  free(dl);
+}
+void or_keyswitch(const uint32_t* c, const uint32_t* ksk, uint32_t n, const uint32_t* m, uint32_t* u, uint32_t* w) {
+  uint32_t* U = (uint32_t*)calloc((size_t)3 * n, sizeof(uint32_t));
+  uint32_t* W = (uint32_t*)calloc((size_t)3 * n, sizeof(uint32_t));
+  ks_accumulate(c, ksk, n, m, U, W);
+  ks_moddown(U, W, n, m, u, w);
   free(U);
   free(W);
 }
@@ -443,4 +452,68 @@ int or_ring_pack(uint32_t N, uint32_t d, uint32_t k, const uint32_t* m, const ui
   }
   free(gk);
   return rc;
+}
+
+/* ------------------------------------------------------------------ MLWE -> RLWE key switching
+ * The cheaper packing (HERMES / BCHPS-style): block Y's packed phase
+ *   Phi = sum_t X^t (b'_t + sum_j a'_{t,j} * s_j)(X^k) = b_Y + sum_j alpha_j(X) s^_j(X)
+ * with b_Y the composed b' words (RLWE order), alpha_j[t + k m] = a'_{kY+t}[j][m] and
+ * s^_j(X) = s_j(X^k) (s^_j[k m] = s[j + k m]).  One hybrid key switch per component j from s^_j to s,
+ * summed BEFORE the single ModDown:  (a, b) = (sum_j u_j, b_Y + sum_j w_j), then rescale by q1.
+ * k key switches per block (no automorphisms, no k^-1 pre-scale, noise grows ~sqrt(k)).
+ */
+/* key from s^_j = s_j(X^k) to s  (key id 0x200 + j) */
+void or_mlwe_ksk(uint64_t seed, uint32_t j, const int32_t* s, uint32_t N, uint32_t k, const uint32_t* m, uint32_t* ksk) {
+  int32_t* sj = (int32_t*)calloc(N, sizeof(int32_t));
+  for (uint32_t c = 0; c < N; c += k) sj[c] = s[j + c];
+  or_ksk_gen(seed, 0x200 + j, sj, s, N, m, ksk);
+  free(sj);
+}
+/*
+ * raw_b [2 limbs][n_out/k][N]      un-rescaled b' words, RLWE order (he_pcmm_run_level1)
+ * raw_a [2 limbs][n_out][k d]      un-rescaled a' words, MLWE layout a'[j][m] at d j + m
+ * ksk   [k][2][2][3][N]            or_mlwe_ksk, j = 0 .. k-1
+ * out   [n_out/k][2 (a, b)][N]     level 0
+ */
+int or_mlwe_to_rlwe(uint32_t d, uint32_t k, const uint32_t* m, const uint32_t* raw_b, const uint32_t* raw_a,
+                    uint32_t n_out, const uint32_t* ksk, uint32_t* out) {
+  const uint32_t N = d * k;
+  if (n_out % k) return 1;
+  const uint32_t blocks = n_out / k;
+  const uint32_t q0 = m[0], q1 = m[1];
+  const uint64_t q1inv = powmod(q1 % q0, q0 - 2, q0);
+#pragma omp parallel for schedule(dynamic)
+  for (uint32_t Y = 0; Y < blocks; ++Y) {
+    uint32_t* U = (uint32_t*)calloc((size_t)3 * N, sizeof(uint32_t));
+    uint32_t* W = (uint32_t*)calloc((size_t)3 * N, sizeof(uint32_t));
+    uint32_t* al = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+    uint32_t* u = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+    uint32_t* w = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+    for (uint32_t j = 0; j < k; ++j) {
+      for (int L = 0; L < 2; ++L)
+        for (uint32_t t = 0; t < k; ++t)
+          for (uint32_t mm = 0; mm < d; ++mm)
+            al[(size_t)L * N + t + (size_t)k * mm] =
+                raw_a[((size_t)L * n_out + (size_t)Y * k + t) * N + (size_t)d * j + mm];
+      ks_accumulate(al, ksk + (size_t)j * 12 * N, N, m, U, W);
+    }
+    ks_moddown(U, W, N, m, u, w);
+    for (uint32_t c = 0; c < N; ++c) {
+      uint32_t x[2][2];
+      for (int L = 0; L < 2; ++L) {
+        x[L][0] = u[(size_t)L * N + c];
+        x[L][1] = (uint32_t)(((uint64_t)raw_b[((size_t)L * blocks + Y) * N + c] + w[(size_t)L * N + c]) % m[L]);
+      }
+      for (int ab = 0; ab < 2; ++ab) {
+        const int64_t x1c = x[1][ab] > q1 / 2 ? (int64_t)x[1][ab] - q1 : (int64_t)x[1][ab];
+        out[((size_t)Y * 2 + ab) * N + c] = (uint32_t)mulmod(modq_i64((int64_t)x[0][ab] - x1c, q0), q1inv, q0);
+      }
+    }
+    free(U);
+    free(W);
+    free(al);
+    free(u);
+    free(w);
+  }
+  return 0;
 }

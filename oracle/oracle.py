@@ -18,7 +18,7 @@ __all__ = [
     "py_mlwe_components", "py_pcmm_rows", "num_threads", "time_pcmm_sample", "rng",
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
     "decode_vector", "rhombus_pcmv", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
-    "ring_pack", "pcmm_ring_pack",
+    "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -506,3 +506,57 @@ def pcmm_ring_pack(params, Wt, ct, gal):
     """Reference MLWE PCMM followed by ring packing: level-0 RLWE output blocks [n_out / k, 2, N]."""
     raw = [pcmm_limb(params, Wt, ct, L) for L in range(2)]
     return ring_pack(params, ring_pack_leaves(params, raw), gal)[1]
+
+
+def _ms_bind():
+    L = _rp_lib()
+    if not getattr(L, "_ms_bound", False):
+        u32p, i32p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32)
+        u32, u64 = ctypes.c_uint32, ctypes.c_uint64
+        L.or_mlwe_ksk.restype = None
+        L.or_mlwe_ksk.argtypes = [u64, u32, i32p, u32, u32, u32p, u32p]
+        L.or_mlwe_to_rlwe.restype = ctypes.c_int
+        L.or_mlwe_to_rlwe.argtypes = [u32, u32, u32p, u32p, u32p, u32, u32p, u32p]
+        L._ms_bound = True
+    return L
+
+
+def mlwe_ks_keys(params, seed: int, s: np.ndarray) -> np.ndarray:
+    """MLWE -> RLWE key-switching keys s_j(X^k) -> s, j = 0 .. k-1 -> [k, 2, 2, 3, N] (coefficient form)."""
+    N, k = params.N, params.mlwe_rank
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    out = np.zeros((k, 2, 2, 3, N), np.uint32)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    for j in range(k):
+        g = np.zeros((2, 2, 3, N), np.uint32)
+        _ms_bind().or_mlwe_ksk(seed, j, _i32(s), N, k, _u32(m), _u32(g))
+        out[j] = g
+    return out
+
+
+def raw_device_layout(params, raw: list):
+    """pcmm_limb words [limb] -> (raw_b [2, n_out/k, N] RLWE order, raw_a [2, n_out, k d]) as
+    he_pcmm_run_level1 writes them."""
+    N, d, k = params.N, params.mlwe_degree, params.mlwe_rank
+    n_out = raw[0].shape[0]
+    raw_b = np.zeros((2, n_out // k, N), np.uint32)
+    raw_a = np.zeros((2, n_out, N), np.uint32)
+    for L in range(2):
+        raw_a[L] = raw[L][:, d:]
+        for y in range(n_out):
+            raw_b[L, y // k, y % k + k * np.arange(d)] = raw[L][y, :d]
+    return raw_b, raw_a
+
+
+def mlwe_to_rlwe(params, raw_b: np.ndarray, raw_a: np.ndarray, ksk: np.ndarray) -> np.ndarray:
+    """MLWE -> RLWE key-switch packing (he_oracle_rhombus.c or_mlwe_to_rlwe) -> [n_out/k, 2, N] level 0."""
+    d, k, N = params.mlwe_degree, params.mlwe_rank, params.N
+    n_out = raw_a.shape[1]
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    out = np.zeros((n_out // k, 2, N), np.uint32)
+    rc = _ms_bind().or_mlwe_to_rlwe(d, k, _u32(m), _u32(np.ascontiguousarray(raw_b, dtype=np.uint32)),
+                                    _u32(np.ascontiguousarray(raw_a, dtype=np.uint32)), n_out,
+                                    _u32(np.ascontiguousarray(ksk, dtype=np.uint32)), _u32(out))
+    if rc:
+        raise ValueError("mlwe_to_rlwe: bad shape")
+    return out

@@ -678,6 +678,99 @@ __global__ void k_rp_rescale(const uint32_t* __restrict__ A, uint64_t per_l, uin
   }
 }
 
+// ---- MLWE -> RLWE key-switch packing (default method; oracle or_mlwe_to_rlwe)
+// digits of alpha_j (alpha_j[t + k m] = a'_{kY+t}[j][m]) for a chunk of (j, Y) pairs, coefficient form,
+// lifted to all three moduli:  D [mod][i][cnt][N], index jj * Yc + Y.  One CTA per (32 positions m, pair):
+// the [t][m] tile is transposed through smem so both the reads and the writes are coalesced.
+__global__ void __launch_bounds__(256) k_ms_digits(const uint32_t* __restrict__ raw_a, uint32_t n_out, uint32_t Y0,
+                                                   uint32_t j0, uint32_t Yc, uint32_t cnt, uint32_t d, uint32_t k,
+                                                   uint32_t N, Mods M, uint32_t qh0, uint32_t qh0p, uint32_t qh1,
+                                                   uint32_t qh1p, uint32_t* __restrict__ D) {
+  __shared__ uint32_t tile[256 * 33];  // [t][m], k <= 256
+  const uint32_t m0 = blockIdx.x * 32, idx = blockIdx.y, jj = idx / Yc, Y = idx % Yc, j = j0 + jj;
+  const size_t plane = (size_t)cnt * N;
+  for (uint32_t L = 0; L < 2; ++L) {
+    const uint32_t* src = raw_a + ((size_t)L * n_out + (size_t)(Y0 + Y) * k) * N + (size_t)d * j + m0;
+    for (uint32_t i = threadIdx.x; i < 32 * k; i += blockDim.x) tile[(i >> 5) * 33 + (i & 31)] = src[(size_t)(i >> 5) * N + (i & 31)];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 32 * k; i += blockDim.x) {
+      const uint32_t mm = i / k, t = i % k;
+      const size_t c = (size_t)idx * N + t + (size_t)k * (m0 + mm);
+      const uint32_t v = tile[t * 33 + mm];
+      // own-limb digit d_L = alpha * Qhat_L^-1 mod q_L, then its residues mod the other two moduli
+      const uint32_t dg = L ? shoup_mul(v, qh1, qh1p, M.m[1]) : shoup_mul(v, qh0, qh0p, M.m[0]);
+#pragma unroll
+      for (int mod = 0; mod < 3; ++mod)
+        D[(size_t)(mod * 2 + L) * plane + c] = (mod == (int)L) ? dg : barrett64(dg, M.mu[mod], M.m[mod]);
+    }
+    __syncthreads();
+  }
+}
+// UW [mod][part][Yc][N] += sum_jj sum_i D^[mod][i][jj Yc + Y] * K_{j0+jj}[i][part][mod]   (NTT domain)
+// one thread per (frequency, block, modulus): contiguous streams per warp; the key words are shared by
+// the Yc blocks through L1/L2
+constexpr int kMsMaxYc = 16;
+__global__ void __launch_bounds__(256) k_ms_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict__ K,
+                                                uint32_t jc, uint32_t Yc, uint32_t logN, Mods M,
+                                                uint32_t* __restrict__ UW) {
+  const uint32_t N = 1u << logN, mod = blockIdx.y;
+  const uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // Y * N + f
+  if (x >= ((uint64_t)Yc << logN)) return;
+  const uint32_t f = (uint32_t)(x & (N - 1));
+  const uint32_t q = mod == 0 ? M.m[0] : (mod == 1 ? M.m[1] : M.m[2]);
+  const uint64_t mu = mod == 0 ? M.mu[0] : (mod == 1 ? M.mu[1] : M.mu[2]);
+  const size_t plane = (size_t)jc * Yc * N;
+  const uint32_t* d0 = D + (size_t)(mod * 2 + 0) * plane + x;
+  const uint32_t* d1 = D + (size_t)(mod * 2 + 1) * plane + x;
+  uint64_t au = 0, aw = 0;
+  for (uint32_t jj = 0; jj < jc; ++jj) {
+    const uint32_t* Kj = K + (size_t)jj * 12 * N + f;
+    const uint64_t x0 = __ldcs(d0 + (size_t)jj * Yc * N), x1 = __ldcs(d1 + (size_t)jj * Yc * N);
+    au += x0 * __ldg(Kj + (size_t)((0 * 2 + 0) * 3 + mod) * N) + x1 * __ldg(Kj + (size_t)((1 * 2 + 0) * 3 + mod) * N);
+    aw += x0 * __ldg(Kj + (size_t)((0 * 2 + 1) * 3 + mod) * N) + x1 * __ldg(Kj + (size_t)((1 * 2 + 1) * 3 + mod) * N);
+    if (jj & 1) {  // two products of < 2^60 per step: reduce every second step (< 2^63)
+      au = barrett64(au, mu, q);
+      aw = barrett64(aw, mu, q);
+    }
+  }
+  uint32_t* U = UW + (size_t)(mod * 2 + 0) * Yc * N + x;
+  uint32_t* W = UW + (size_t)(mod * 2 + 1) * Yc * N + x;
+  *U = add_mod(*U, barrett64(au, mu, q), q);
+  *W = add_mod(*W, barrett64(aw, mu, q), q);
+}
+// ModDown of the summed (U, W) (coefficient form), b += composed b', rescale by q1 -> out [Y][2][N]
+__global__ void k_ms_finish(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ raw_b, uint32_t blocks,
+                            uint32_t Y0, uint32_t Yc, uint32_t logN, Mods M, uint32_t pinv0, uint32_t pinv1,
+                            uint32_t q1inv, uint32_t q1invp, uint32_t* __restrict__ out) {
+  const uint32_t N = 1u << logN, P = M.m[2], q0 = M.m[0], q1 = M.m[1];
+  const uint64_t per = (uint64_t)Yc << logN;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < per; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t Y = (uint32_t)(x >> logN), c = (uint32_t)(x & (N - 1));
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const uint32_t vp = UW[(size_t)(2 * 2 + part) * per + x];
+      const int64_t cp = vp > P / 2 ? (int64_t)vp - P : (int64_t)vp;
+      uint32_t v[2];
+#pragma unroll
+      for (int L = 0; L < 2; ++L) {
+        const uint32_t q = M.m[L];
+        v[L] = mulmod_b(sub_mod(UW[(size_t)(L * 2 + part) * per + x], lift_b(cp, M.mu[L], q), q), L ? pinv1 : pinv0,
+                        M.mu[L], q);
+        if (part) v[L] = add_mod(v[L], raw_b[((size_t)L * blocks + Y0 + Y) * N + c], q);
+      }
+      uint32_t t;
+      if (v[1] > (q1 >> 1)) t = csub(v[0] + (q1 - v[1]), q0);
+      else t = sub_mod(v[0], v[1], q0);
+      out[((size_t)(Y0 + Y) * 2 + part) * N + c] = shoup_mul(t, q1inv, q1invp, q0);
+    }
+  }
+}
+// s^_j = s_j(X^k): s^_j[c] = s[j + c] for c = 0 mod k, else 0
+__global__ void k_ms_component(const int32_t* s, uint32_t N, uint32_t k, uint32_t j, int32_t* out) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x)
+    out[c] = (c % k == 0) ? s[j + c] : 0;
+}
+
 uint64_t find_psi(uint32_t q, uint32_t n) {  // the root ntt_table_init uses
   for (uint64_t g = 2; g < q; ++g) {
     const uint64_t cand = powmod_h(g, (q - 1) / (2ull * n), q);
@@ -690,39 +783,63 @@ uint64_t find_psi(uint32_t q, uint32_t n) {  // the root ntt_table_init uses
 
 struct he_ring_pack_plan {
   const he_context* ctx;
+  int method;        // HE_RING_PACK_KEYSWITCH (0) or HE_RING_PACK_TRACE (1)
+  uint32_t jc;       // keyswitch: components j per pass
   uint32_t n_out, blocks, chunk, d, k, N, logN, logk;
   uint32_t* tables;  // owned: perm [logk][N], mono [logk][2][N]
   Mods M;
   uint32_t qhinv[2], pinv[2], q1inv, q1invp, kinv[2], kinvp[2];
 };
 
-extern "C" he_status he_ring_pack_keygen(const he_context* c, uint64_t seed, const int32_t* s_dev, uint32_t* gal_dev,
-                                         void* stream) {
-  if (!c || !s_dev || !gal_dev) return fail(HE_EINVAL, "null argument");
+static uint64_t ring_pack_key_words(const he_context* c, int method) {
+  const uint64_t n_keys = method == HE_RING_PACK_TRACE ? (uint64_t)ilog2_u(c->R.k) : (uint64_t)c->R.k;
+  return n_keys * 12ull * c->R.N;
+}
+extern "C" he_status he_ring_pack_key_bytes(const he_context* c, int method, uint64_t* bytes) {
+  if (!c || !bytes) return fail(HE_EINVAL, "null argument");
+  if (method != HE_RING_PACK_KEYSWITCH && method != HE_RING_PACK_TRACE) return fail(HE_EINVAL, "unknown method %d", method);
+  *bytes = ring_pack_key_words(c, method) * sizeof(uint32_t);
+  return HE_OK;
+}
+
+extern "C" he_status he_ring_pack_keygen(const he_context* c, int method, uint64_t seed, const int32_t* s_dev,
+                                         uint32_t* keys_dev, void* stream) {
+  if (!c || !s_dev || !keys_dev) return fail(HE_EINVAL, "null argument");
+  if (method != HE_RING_PACK_KEYSWITCH && method != HE_RING_PACK_TRACE) return fail(HE_EINVAL, "unknown method %d", method);
   cudaStream_t st = (cudaStream_t)stream;
-  const uint32_t N = c->R.N, d = c->R.d;
-  const int logk = ilog2_u(c->R.k);
+  const uint32_t N = c->R.N, d = c->R.d, k = c->R.k;
+  const int logk = ilog2_u(k);
   const Mods M = make_mods(c->R);
   int32_t* sk = nullptr;
   HE_CUDA(cudaMallocAsync(&sk, N * sizeof(int32_t), st), "alloc");
   he_status s = HE_OK;
-  for (int lv = 1; lv <= logk && !s; ++lv) {
-    k_secret_auto<<<grid_for(N), 256, 0, st>>>(s_dev, N, (d << lv) + 1, sk);
-    s = make_ksk_dev(M, seed, 0x100 + lv, sk, s_dev, N, c->ntt, gal_dev + (size_t)(lv - 1) * 12 * N, st);
+  if (method == HE_RING_PACK_TRACE) {
+    for (int lv = 1; lv <= logk && !s; ++lv) {  // sigma_g(s) -> s, g = 1 + 2^l d
+      k_secret_auto<<<grid_for(N), 256, 0, st>>>(s_dev, N, (d << lv) + 1, sk);
+      s = make_ksk_dev(M, seed, 0x100 + lv, sk, s_dev, N, c->ntt, keys_dev + (size_t)(lv - 1) * 12 * N, st);
+    }
+  } else {
+    for (uint32_t j = 0; j < k && !s; ++j) {     // s_j(X^k) -> s
+      k_ms_component<<<grid_for(N), 256, 0, st>>>(s_dev, N, k, j, sk);
+      s = make_ksk_dev(M, seed, 0x200 + j, sk, s_dev, N, c->ntt, keys_dev + (size_t)j * 12 * N, st);
+    }
   }
   cudaFreeAsync(sk, st);
   if (s) return s;
   return cudaGetLastError() == cudaSuccess ? HE_OK : fail(HE_ECUDA, "ring pack keygen launch failed");
 }
 
-extern "C" he_status he_ring_pack_plan_create(const he_context* c, uint32_t n_out, he_ring_pack_plan** out) {
+extern "C" he_status he_ring_pack_plan_create(const he_context* c, uint32_t n_out, int method,
+                                              he_ring_pack_plan** out) {
   if (!c || !out) return fail(HE_EINVAL, "null argument");
+  if (method != HE_RING_PACK_KEYSWITCH && method != HE_RING_PACK_TRACE) return fail(HE_EINVAL, "unknown method %d", method);
   const uint32_t k = c->R.k;
   if (n_out == 0 || n_out % k) return fail(HE_EINVAL, "n_out (%u) must be a positive multiple of k = %u", n_out, k);
   if (k > 256 || c->R.d % 32) return fail(HE_EINVAL, "ring packing needs k <= 256 and d a multiple of 32");
   he_ring_pack_plan* p = new (std::nothrow) he_ring_pack_plan();
   if (!p) return fail(HE_ENOMEM, "out of host memory");
   p->ctx = c;
+  p->method = method;
   p->n_out = n_out;
   p->d = c->R.d;
   p->k = k;
@@ -731,7 +848,15 @@ extern "C" he_status he_ring_pack_plan_create(const he_context* c, uint32_t n_ou
   p->logk = (uint32_t)ilog2_u(k);
   p->blocks = n_out / k;
   static const int env_chunk = getenv("HE_RP_CHUNK") ? atoi(getenv("HE_RP_CHUNK")) : 0;  // blocks per pass
-  p->chunk = env_chunk > 0 ? (uint32_t)env_chunk : 8;
+  static const int env_jc = getenv("HE_MS_JC") ? atoi(getenv("HE_MS_JC")) : 0;       // components per pass
+  if (method == HE_RING_PACK_TRACE) {
+    p->chunk = env_chunk > 0 ? (uint32_t)env_chunk : 8;
+  } else {
+    p->chunk = env_chunk > 0 && env_chunk <= kMsMaxYc ? (uint32_t)env_chunk : kMsMaxYc;
+    p->jc = env_jc > 0 ? (uint32_t)env_jc : 32;  // measured: 4 -> 14.6, 16 -> 11.8, 32 -> 11.0, 64 -> 10.8 ms
+    if (p->jc > k) p->jc = k;
+    while (k % p->jc) --p->jc;
+  }
   if (p->chunk > p->blocks) p->chunk = p->blocks;
   p->M = make_mods(c->R);
   for (int i = 0; i < 2; ++i) {
@@ -803,6 +928,11 @@ static uint64_t rp_ws_words(const he_ring_pack_plan* p, RpWs* w, uint32_t* base)
   };
   RpWs dummy;
   RpWs& r = w ? *w : dummy;
+  if (p->method == HE_RING_PACK_KEYSWITCH) {  // D [3][2][jc * Yc][N], UW [3][2][Yc][N]
+    take(r.D, 6ull * p->jc * p->chunk * N);
+    take(r.UW, 6ull * p->chunk * N);
+    return off;
+  }
   take(r.A0, 2ull * cnt * 2 * N);
   take(r.A1, 2ull * c1 * 2 * N);
   take(r.T, 2ull * c1 * 2 * N);
@@ -832,6 +962,29 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
   const uint32_t N = p->N, k = p->k, d = p->d, q0 = p->M.m[0], q1 = p->M.m[1];
   RpWs w;
   rp_ws_words(p, &w, (uint32_t*)ws_dev);
+  if (p->method == HE_RING_PACK_KEYSWITCH) {
+    const uint32_t qh0p = shoup_pre(p->qhinv[0], q0), qh1p = shoup_pre(p->qhinv[1], q1);
+    for (uint32_t Y0 = 0; Y0 < p->blocks; Y0 += p->chunk) {
+      const uint32_t Yc = (p->blocks - Y0 < p->chunk) ? p->blocks - Y0 : p->chunk;
+      const uint32_t cnt = p->jc * Yc;
+      HE_CUDA(cudaMemsetAsync(w.UW, 0, 6ull * Yc * N * sizeof(uint32_t), st), "memset");
+      for (uint32_t j0 = 0; j0 < k; j0 += p->jc) {
+        k_ms_digits<<<dim3(d / 32, cnt), 256, 0, st>>>(raw_a, p->n_out, Y0, j0, Yc, cnt, d, k, N, p->M, p->qhinv[0],
+                                                      qh0p, p->qhinv[1], qh1p, w.D);
+        for (int mod = 0; mod < 3; ++mod)
+          HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * 2 * cnt * N, 2 * cnt, N, st), "NTT(digits)");
+        k_ms_mac<<<dim3((unsigned)(((uint64_t)Yc * N + 255) / 256), 3), 256, 0, st>>>(w.D, gal + (size_t)j0 * 12 * N, p->jc,
+                                                                                   Yc, p->logN, p->M, w.UW);
+      }
+      for (int mod = 0; mod < 3; ++mod)
+        HE_CUDA(ntt_inverse(c->ntt[mod], w.UW + (size_t)mod * 2 * Yc * N, 2 * Yc, N, st), "INTT(U, W)");
+      k_ms_finish<<<grid_for((uint64_t)Yc * N), 256, 0, st>>>(w.UW, raw_b, p->blocks, Y0, Yc, p->logN, p->M, p->pinv[0],
+                                                               p->pinv[1], p->q1inv, p->q1invp, out);
+    }
+    HE_CUDA(cudaGetLastError(), "ring pack launch");
+    if (ledger) ledger->rescales += p->blocks;  // k key switches per block, no rotations
+    return HE_OK;
+  }
   const uint32_t* perm_base = p->tables;
   const uint32_t* mono_base = p->tables + (size_t)p->logk * N;
   for (uint32_t b0 = 0; b0 < p->blocks; b0 += p->chunk) {

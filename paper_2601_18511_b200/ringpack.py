@@ -7,12 +7,16 @@ in the activation coefficient layout of ``HeContext.encrypt_acts`` (so the resul
 ``CtBlocks`` the next projection can consume, and its all-gather shrinks ~128x).
 
 Pipeline (all on the device, include/he_b200.h he_pcmm_run_level1 / he_ring_pack_*;
-restated in oracle/he_oracle_rhombus.c or_ring_pack):
-  PCMM at level 1 without the rescale (both limbs' words)
-  leaves C_y: A_y[k m - j] = a'_y[j][m], B_y[k m] = b'_y[m], scaled by k^-1
-  PackLWEs over the subring Z[X^k]: log2 k levels of E + X^{k/2^l} O + sigma_g(E - X^{k/2^l} O),
-  g = 1 + 2^l d, each automorphism followed by a hybrid Galois key switch (dnum 2, special prime P)
-  rescale by q1 -> level 0.
+restated in oracle/he_oracle_rhombus.c): the PCMM at level 1 without the rescale (both limbs'
+words), then one of two packings, then the rescale by q1 -> level 0:
+  "keyswitch" (default, or_mlwe_to_rlwe): MLWE -> RLWE key switching -- block Y's packed phase is
+      b'_Y + sum_j alpha_j(X) s_j(X^k), alpha_j[t + k m] = a'_{kY+t}[j][m]; one hybrid key switch
+      (dnum 2, special prime P) per component j from s_j(X^k) to s, summed before one ModDown.
+      k keys (~805 MB at Llama parameters), 6 NTTs per (block, j), no automorphisms.
+  "trace" (or_ring_pack): PackLWEs over the subring Z[X^k] on leaves C_y with A_y[k m - j] =
+      a'_y[j][m], B_y[k m] = b'_y[m] scaled by k^-1: log2 k levels of E + X^{k/2^l} O +
+      sigma_g(E - X^{k/2^l} O), g = 1 + 2^l d, each automorphism followed by a Galois key switch.
+      log2 k keys, ~16 NTTs per row.
 hesim has no counterpart (its PCMM output stays in slots); the calling convention follows
 its PCMM (matmul.py:152-162) like the rest of this package.
 """
@@ -27,14 +31,26 @@ from .context import CtBlocks, HeContext, SecretKey, _torch
 from .pcmm import MlwePcmmPlan, _check_operand
 
 
+METHODS = {"keyswitch": 0, "trace": 1}
+
+
+def _method(method: str) -> int:
+    if method not in METHODS:
+        raise ValueError(f"unknown ring packing method {method!r} (expected one of {sorted(METHODS)})")
+    return METHODS[method]
+
+
 @dataclass
 class RingPackKeys:
-    gal: object          # u32 [log2 k, 2, 2, 3, N] Galois keys sigma_{1 + 2^l d}(s) -> s, NTT domain
+    gal: object          # keyswitch: u32 [k, 2, 2, 3, N] keys s_j(X^k) -> s; trace: u32 [log2 k, 2, 2, 3, N]
+                         # Galois keys sigma_{1 + 2^l d}(s) -> s; NTT domain
+    method: str = "keyswitch"
 
 
 @dataclass
 class RingPackPlan:
     n_out: int
+    method: str = "keyswitch"
     _handle: object = field(default=None, repr=False)
     _workspace: object = field(default=None, repr=False)
     _raw: tuple = field(default=None, repr=False)
@@ -64,19 +80,21 @@ class RingPackPlan:
             pass
 
 
-def ring_pack_keygen(ctx: HeContext, sk: SecretKey, seed: int) -> RingPackKeys:
+def ring_pack_keygen(ctx: HeContext, sk: SecretKey, seed: int, method: str = "keyswitch") -> RingPackKeys:
     torch = _torch()
-    p = ctx.params
-    lg = p.mlwe_rank.bit_length() - 1
-    gal = torch.empty((lg, 2, 2, 3, p.N), dtype=torch.int32, device=ctx.device)
-    native.call("he_ring_pack_keygen", ctx.handle, seed, sk.s.data_ptr(), gal.data_ptr(), ctx.stream())
-    return RingPackKeys(gal)
+    m = _method(method)
+    nb = ctypes.c_uint64()
+    native.call("he_ring_pack_key_bytes", ctx.handle, m, ctypes.byref(nb))
+    gal = torch.empty((nb.value // (4 * 12 * ctx.params.N), 2, 2, 3, ctx.params.N), dtype=torch.int32,
+                      device=ctx.device)
+    native.call("he_ring_pack_keygen", ctx.handle, m, seed, sk.s.data_ptr(), gal.data_ptr(), ctx.stream())
+    return RingPackKeys(gal, method)
 
 
-def make_ring_pack_plan(ctx: HeContext, n_out: int) -> RingPackPlan:
+def make_ring_pack_plan(ctx: HeContext, n_out: int, method: str = "keyswitch") -> RingPackPlan:
     h = ctypes.c_void_p()
-    native.call("he_ring_pack_plan_create", ctx.handle, int(n_out), ctypes.byref(h))
-    return RingPackPlan(int(n_out), _handle=h)
+    native.call("he_ring_pack_plan_create", ctx.handle, int(n_out), _method(method), ctypes.byref(h))
+    return RingPackPlan(int(n_out), method, _handle=h)
 
 
 def pcmm_level1(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, raw_b=None, raw_a=None):
@@ -97,6 +115,8 @@ def pcmm_level1(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, raw_b=None, raw
 def ring_pack(ctx: HeContext, rp: RingPackPlan, keys: RingPackKeys, raw_b, raw_a, out=None) -> CtBlocks:
     torch = _torch()
     p = ctx.params
+    if keys.method != rp.method:
+        raise ValueError(f"key/plan mismatch: keys for {keys.method!r}, plan for {rp.method!r}")
     if out is None:
         out = torch.empty((rp.n_out // p.mlwe_rank, 1, 2, p.N), dtype=torch.int32, device=ctx.device)
     ws = rp.workspace(ctx.device)

@@ -19,6 +19,7 @@ from test_gpu_pcmm import setup, u32
 
 pytestmark = pytest.mark.gpu
 ALGOS = ["spectral", "direct"]
+METHODS = ["keyswitch", "trace"]
 
 
 def _raw_oracle(P, W, A):
@@ -42,11 +43,12 @@ def test_toy_level1_words_bit_exact(n_out, n_in, algo):
             assert np.array_equal(rb[L, y // k, y % k + k * np.arange(d)], raw[L][y, :d]), f"limb {L} b' row {y}"
 
 
-def test_toy_galois_keys_match_oracle():
+@pytest.mark.parametrize("method", METHODS)
+def test_toy_keys_match_oracle(method):
     P = HeParams.toy()
     ctx, sk, A, W, X = setup(P, 16, 16)
-    keys = ring_pack_keygen(ctx, sk, seed=5)
-    ref = O.ring_pack_keys(P, 5, O.keygen(P, 7))
+    keys = ring_pack_keygen(ctx, sk, seed=5, method=method)
+    ref = (O.ring_pack_keys if method == "trace" else O.mlwe_ks_keys)(P, 5, O.keygen(P, 7))
     # device keys are NTT-domain: compare after the inverse transform per modulus
     import torch
 
@@ -67,22 +69,27 @@ def ctx_ntt_inverse(ctx, data, limb):
                 ctx.stream())
 
 
+@pytest.mark.parametrize("method", METHODS)
 @pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("n_out,n_in", [(16, 16), (64, 48), (48, 128)])
-def test_toy_packed_ciphertexts_bit_exact_and_decrypt(n_out, n_in, algo):
+def test_toy_packed_ciphertexts_bit_exact_and_decrypt(n_out, n_in, algo, method):
     P = HeParams.toy()
     ctx, sk, A, W, X = setup(P, n_out, n_in, seed=n_out + n_in)
     Wt, ct, raw = _raw_oracle(P, W, A)
-    gal = O.ring_pack_keys(P, 5, O.keygen(P, 7))
-    ref = O.ring_pack(P, O.ring_pack_leaves(P, raw), gal)[1]
-    keys = ring_pack_keygen(ctx, sk, seed=5)
+    s = O.keygen(P, 7)
+    if method == "trace":
+        ref = O.ring_pack(P, O.ring_pack_leaves(P, raw), O.ring_pack_keys(P, 5, s))[1]
+    else:
+        ref = O.mlwe_to_rlwe(P, *O.raw_device_layout(P, raw), O.mlwe_ks_keys(P, 5, s))
+    keys = ring_pack_keygen(ctx, sk, seed=5, method=method)
     plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
-    rp = make_ring_pack_plan(ctx, n_out)
+    rp = make_ring_pack_plan(ctx, n_out, method=method)
     before = ctx.ledger.snapshot()
     Y = pcmm_packed(ctx, plan, rp, keys, X)
     diff = ctx.ledger.diff(before)
     k = P.mlwe_rank
-    assert diff["ct_rotations"] == (k - 1) * n_out // k and diff["rescales"] == n_out // k
+    rot = (k - 1) * n_out // k if method == "trace" else 0
+    assert diff["ct_rotations"] == rot and diff["rescales"] == n_out // k
     assert Y.level == 0 and Y.n_cols == n_out and tuple(Y.data.shape) == (n_out // k, 1, 2, P.N)
     got = u32(Y.data)[:, 0]
     assert np.array_equal(got, ref), f"{int((got != ref).sum())} words differ"
@@ -100,6 +107,10 @@ def test_ring_pack_errors():
     plan = make_mlwe_pcmm_plan(ctx, W)
     with pytest.raises(ValueError):
         pcmm_packed(ctx, plan, make_ring_pack_plan(ctx, 32), ring_pack_keygen(ctx, sk, 5), X)
+    with pytest.raises(ValueError):
+        make_ring_pack_plan(ctx, 16, method="bogus")
+    with pytest.raises(ValueError):   # keys of the other method
+        pcmm_packed(ctx, plan, make_ring_pack_plan(ctx, 16), ring_pack_keygen(ctx, sk, 5, method="trace"), X)
 
 
 def _rescale(P, x0, x1):
@@ -128,12 +139,13 @@ def test_llama_level1_words_rescale_to_pcmm_output(algo):
     assert torch.equal(_rescale(P, rb[0], rb[1]), Y.out_b.to(torch.int64) & 0xFFFFFFFF)
 
 
+@pytest.mark.parametrize("method", METHODS)
 @pytest.mark.parametrize("n_out,n_in", [(512, 1024), (1024, 4096)])
-def test_llama_packed_decrypts_to_product(n_out, n_in):
+def test_llama_packed_decrypts_to_product(n_out, n_in, method):
     P = HeParams.llama()
     ctx, sk, A, W, X = setup(P, n_out, n_in, seed=5)
-    keys = ring_pack_keygen(ctx, sk, seed=9)
-    Y = pcmm_packed(ctx, make_mlwe_pcmm_plan(ctx, W), make_ring_pack_plan(ctx, n_out), keys, X)
+    keys = ring_pack_keygen(ctx, sk, seed=9, method=method)
+    Y = pcmm_packed(ctx, make_mlwe_pcmm_plan(ctx, W), make_ring_pack_plan(ctx, n_out, method=method), keys, X)
     dec = ctx.decrypt_acts(sk, Y)
     ref = A @ W.T
     err = np.abs(dec - ref).max()

@@ -166,3 +166,23 @@ def test_ring_pack_leaves_trace_keeps_component_zero():
         # MLWE phase of row y at level 1, limb 0 (decrypt_mlwe takes level-0 words; compare mod q0)
         ref = O.decrypt_mlwe(P, s, row)[0] % q
         assert np.array_equal(ph % q, ref)
+
+
+def test_mlwe_keyswitch_packing_matches_trace_packing_plaintext():
+    """The two packings (MLWE -> RLWE key switch; subring PackLWEs) give ciphertexts of the same
+    plaintext: decryptions agree to the key-switching noise and decode to A @ W^T."""
+    rng = np.random.default_rng(6)
+    n_out, n_in = 32, 32
+    A = rng.uniform(-1, 1, (P.tokens, n_in))
+    W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
+    s = O.keygen(P, 7)
+    ct = O.encrypt(P, 11, s, O.encode_acts(P, A))
+    raw = [O.pcmm_limb(P, O.encode_weights(P, W), ct, L) for L in range(2)]
+    ks = O.mlwe_to_rlwe(P, *O.raw_device_layout(P, raw), O.mlwe_ks_keys(P, 5, s))
+    tr = O.ring_pack(P, O.ring_pack_leaves(P, raw), O.ring_pack_keys(P, 5, s))[1]
+    q = P.moduli[0]
+    ph_ks = np.stack([O.decrypt_under(P, ks[b, 0], ks[b, 1], s, q) for b in range(ks.shape[0])])
+    ph_tr = np.stack([O.decrypt_under(P, tr[b, 0], tr[b, 1], s, q) for b in range(tr.shape[0])])
+    assert np.abs(ph_ks - ph_tr).max() < 64
+    ref = A @ W.T
+    assert np.abs(O.decode_acts(P, ph_ks, n_out) - ref).max() < np.abs(ref).max() * 2.0 ** -14
