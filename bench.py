@@ -464,7 +464,64 @@ def side_measurements(P, dev):
         out["ntt"] = {"peak_GBs": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs", **ntt}
     except Exception as exc:  # side measurements never break the headline line
         out["side_measurement_error"] = repr(exc)
+    try:
+        out["ring_pack"] = ring_pack_side(P, dev)
+    except Exception as exc:
+        out["ring_pack_error"] = repr(exc)
     return out
+
+
+def ring_pack_side(P, dev, shape="4096x11008", reps=3):
+    """§8f1: the PCMM followed by MLWE -> RLWE ring packing (the packed op), at the metric shape:
+    device ms of the packing alone and of the whole packed op, the packed op end to end (pinned host
+    input -> packed level-0 RLWE output on the host) and the decrypted precision."""
+    import torch
+
+    from paper_2601_18511_b200 import (HeContext, make_mlwe_pcmm_plan, make_ring_pack_plan, pcmm_level1,
+                                       pcmm_packed, ring_pack, ring_pack_keygen)
+
+    n_out, n_in = shape_of(shape)
+    ctx = HeContext(P, device=dev)
+    g = torch.Generator(device=dev).manual_seed(31)
+    W = (torch.rand((n_out, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1) / math.sqrt(n_in)
+    A = torch.rand((P.tokens, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+    sk = ctx.keygen(41)
+    X = ctx.encrypt_acts(sk, A, seed=43)
+    keys = ring_pack_keygen(ctx, sk, seed=47)
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    rp = make_ring_pack_plan(ctx, n_out)
+    Y = pcmm_packed(ctx, plan, rp, keys, X)
+    torch.cuda.synchronize()
+    ref = (A @ W.T).cpu().numpy()
+    err = float(np.abs(ctx.decrypt_acts(sk, Y) - ref).max())
+    raw_b, raw_a = rp.raw(ctx)
+    x_host = X.data.cpu().pin_memory()
+    y_host = torch.empty(Y.data.shape, dtype=Y.data.dtype).pin_memory()
+
+    def e2e():
+        X.data.copy_(x_host, non_blocking=True)
+        pcmm_packed(ctx, plan, rp, keys, X, Y.data)
+        y_host.copy_(Y.data, non_blocking=True)
+
+    res = {}
+    for name, fn in (("ring_pack_ms", lambda: ring_pack(ctx, rp, keys, raw_b, raw_a, Y.data)),
+                     ("packed_op_ms", lambda: pcmm_packed(ctx, plan, rp, keys, X, Y.data)),
+                     ("packed_e2e_ms", e2e)):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        res[name] = round(float(np.median(ts)), 3)
+    return {"workload": f"{shape} PCMM + MLWE->RLWE key-switch packing (k = {P.mlwe_rank} hybrid key switches "
+                        f"per block, dnum 2) -> {n_out // P.mlwe_rank} level-0 RLWE ciphertexts, 1 GPU",
+            **res, "precision_bits": round(-math.log2(err / float(np.abs(ref).max())), 1),
+            "output_bytes": int(Y.data.numel() * 4), "h2d_bytes": int(x_host.numel() * 4)}
 
 
 def measured_hbm():
