@@ -58,9 +58,12 @@ def parse():
     ap.add_argument("--algo", choices=["spectral", "direct"], default="spectral",
                     help="a'-column algorithm (same output words): K7 spectral (default) or K1 direct GEMM")
     ap.add_argument("--no-direct", action="store_true", help="skip the side measurement of the direct K1 path")
-    ap.add_argument("--fused", action="store_true",
-                    help="N > 1: fuse the output all-gather into the kernels' peer-memory stores (symmetric memory; "
-                         "not yet exercised on multi-GPU hardware -- the default is NCCL broadcast + all-gather)")
+    ap.add_argument("--no-fused", dest="fused", action="store_false",
+                    help="N > 1: gather the output with NCCL all-gather instead of fusing it into the kernels' "
+                         "peer-memory stores (the default, verified against the NCCL gather before timing)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="testing only: gloo with --one-device runs the N > 1 code path with every rank on cuda:0")
+    ap.add_argument("--one-device", action="store_true", help="testing only: all ranks share cuda:0")
     ap.add_argument("--cpu-rows", type=int, default=64, help="oracle sample rows for cpu_baseline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -152,13 +155,18 @@ def run_ours(a, rank: int, world: int, local: int):
     from paper_2601_18511_b200 import HeContext, make_mlwe_pcmm_plan, pcmm_mlwe
     from paper_2601_18511_b200.context import MlweBlocks
     from paper_2601_18511_b200.pcmm import pcmm_ops, spectral_gemm_ops, spectral_inverse_bytes
-    from paper_2601_18511_b200.sharding import (pcmm_mlwe_sharded_fused, row_shards, shard_slots,
-                                                symmetric_outputs)
+    from paper_2601_18511_b200.sharding import (all_gather_into, all_reduce_max, broadcast_input,
+                                                pcmm_mlwe_sharded_fused, row_shards, shard_slots, symmetric_outputs)
 
+    if a.one_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(a.dist_backend)
     P = params_of(a.params)
     k, N = P.mlwe_rank, P.N
     n_out, n_in = shape_of(a.shape)
@@ -185,6 +193,23 @@ def run_ours(a, rank: int, world: int, local: int):
         all_a = torch.empty((per * world * k, N), dtype=torch.int32, device=dev)
     del W
     torch.cuda.synchronize()
+    fused_check = None
+    if sym is not None:
+        # one op each way before timing: the fused peer stores must equal the NCCL gather word for word
+        fb, fa = pcmm_mlwe_sharded_fused(ctx, plan, X, n_out, b0 * k, sym)
+        broadcast_input(X.data)
+        pcmm_mlwe(ctx, plan, X, out=Y)
+        all_gather_into(all_b, out_b)
+        all_gather_into(all_a, out_a)
+        spans = row_shards(n_out, k, world)
+        ok = all(torch.equal(fb[c0:c1], all_b[r * per: r * per + (c1 - c0)]) and
+                 torch.equal(fa[c0 * k:c1 * k], all_a[r * per * k:(r * per + (c1 - c0)) * k])
+                 for r, (c0, c1) in enumerate(spans))
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        flag = -all_reduce_max(-flag)
+        fused_check = "equal to the NCCL all-gather" if int(flag) else "MISMATCH vs NCCL all-gather: fell back to NCCL"
+        if not int(flag):
+            sym = None
 
     stream = torch.cuda.current_stream(dev)
 
@@ -193,11 +218,11 @@ def run_ours(a, rank: int, world: int, local: int):
             pcmm_mlwe_sharded_fused(ctx, plan, X, n_out, b0 * k, sym)
             return
         if world > 1:
-            dist.broadcast(X.data, src=0)
+            broadcast_input(X.data)
         pcmm_mlwe(ctx, plan, X, out=Y)
         if world > 1:
-            dist.all_gather_into_tensor(all_b, out_b)
-            dist.all_gather_into_tensor(all_a, out_a)
+            all_gather_into(all_b, out_b)
+            all_gather_into(all_a, out_a)
 
     for _ in range(a.warmup):
         step()
@@ -226,7 +251,7 @@ def run_ours(a, rank: int, world: int, local: int):
     if world > 1:
         names = sorted(stage_ms)
         tt = torch.tensor([ms] + [stage_ms[n] for n in names], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tt = all_reduce_max(tt)
         ms = float(tt[0])
         stage_ms = {n: float(v) for n, v in zip(names, tt[1:].tolist())}
 
@@ -286,7 +311,9 @@ def run_ours(a, rank: int, world: int, local: int):
                               "b' on K1)" if a.algo == "spectral" else " (K1 over all columns)"),
                        "parallelism": f"row-shard x{world}" + (
                            "" if world == 1 else " + NCCL bcast + output all-gather fused into the kernels' peer "
-                           "stores (symmetric memory)" if sym is not None else " + NCCL bcast/all-gather"),
+                           "stores (symmetric memory / CUDA IPC over NVLink; " + str(fused_check) + ")"
+                           if sym is not None else " + NCCL bcast/all-gather" + (
+                               f" ({fused_check})" if fused_check else "")),
                        "l2": "inputs larger than L2: each op writes and reads a "
                              f"{plan.workspace_bytes() / 1e9:.2f} GB workspace"},
             "roofline": roof,
@@ -362,6 +389,7 @@ def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
     import torch.distributed as dist
 
     from paper_2601_18511_b200 import pcmm_mlwe, pcmm_mlwe_to_host
+    from paper_2601_18511_b200.sharding import all_gather_into, all_reduce_max, broadcast_input
 
     steps = a.e2e_steps or max(1, min(a.steps, 5))
     h_in = torch.empty(X.data.shape, dtype=torch.int32, pin_memory=True)
@@ -377,10 +405,10 @@ def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
             return
         if rank == 0:
             X.data.copy_(h_in, non_blocking=True)
-        dist.broadcast(X.data, src=0)
+        broadcast_input(X.data)
         pcmm_mlwe(ctx, plan, X, out=Y)
-        dist.all_gather_into_tensor(all_b, out_b)
-        dist.all_gather_into_tensor(all_a, out_a)
+        all_gather_into(all_b, out_b)
+        all_gather_into(all_a, out_a)
         if rank == 0:
             h_b.copy_(src_b, non_blocking=True)
             h_a.copy_(src_a, non_blocking=True)
@@ -398,7 +426,7 @@ def run_e2e(a, ctx, plan, X, Y, rank, world, dev, out_b, out_a, all_b, all_a):
     ms = t0.elapsed_time(t1) / steps
     if world > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tt = all_reduce_max(tt)
         ms = float(tt[0])
     return {"value": round(ms, 3), "unit": "ms/op", "h2d_bytes_per_step": int(h_in.numel() * 4),
             "d2h_bytes_per_step": int((plan.n_out // ctx.params.mlwe_rank + plan.n_out) * ctx.params.N * 4)

@@ -182,6 +182,20 @@ he_status he_rhombus_workspace_bytes(const he_rhombus_plan* plan, uint64_t* byte
 he_status he_rhombus_run(const he_rhombus_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
                          const uint32_t* ksk_dec_dev, const uint32_t* gal_dev, uint32_t* out_dev, void* workspace_dev,
                          uint64_t workspace_bytes, void* stream, he_ledger* ledger);
+/* Multi-GPU shards: a plan over a column slice W[:, n piece0 ..] and/or a
+ * row slice W[n opiece0 .., :] (piece = n = rhombus_degree elements) runs on the full input
+ * ciphertext and writes its LEVEL-1 composed partial output out_l1 [2 limbs][2 (a, b)][N] (zeros
+ * outside its output pieces; no rescale).  Row shards own disjoint output pieces (their words equal
+ * the unsharded run's); column shards produce partial sums of the same pieces.  he_rhombus_combine
+ * sums `count` such outputs mod q_i (parts [count][2][2][N], e.g. after an all-gather) and rescales
+ * once -> level-0 ct [2][N].  ledger: the shard run counts pc_mults / ct_rotations, the combine
+ * the one rescale. */
+he_status he_rhombus_run_shard(const he_rhombus_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
+                               const uint32_t* ksk_dec_dev, const uint32_t* gal_dev, uint32_t piece0, uint32_t opiece0,
+                               uint32_t* out_l1_dev, void* workspace_dev, uint64_t workspace_bytes, void* stream,
+                               he_ledger* ledger);
+he_status he_rhombus_combine(const he_context* ctx, const uint32_t* parts_dev, uint32_t count, uint32_t* out_dev,
+                             void* stream, he_ledger* ledger);
 
 /* ---------------------------------------------------------------- MLWE -> RLWE ring packing
  * The step after the PCMM toward Half-Bootstrap: each block of k MLWE output rows

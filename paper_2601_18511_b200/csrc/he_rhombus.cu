@@ -157,13 +157,13 @@ __global__ void k_decomp_modup(const uint32_t* __restrict__ ct, uint32_t N, uint
 // (u, w) mod q_j from UW (coefficient form, [j][2][N]), then the X^rho split:
 //   pieces [L][p][2][n]:  a = u[p + rho k],  b = b_in[p + rho k] + w[p + rho k]
 __global__ void k_decomp_split(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ ct, uint32_t N,
-                               uint32_t n, uint32_t p_in, uint32_t q0, uint32_t q1, uint32_t P, uint32_t pinv0,
-                               uint32_t pinv1, uint32_t* __restrict__ pieces) {
+                               uint32_t n, uint32_t p_in, uint32_t piece0, uint32_t q0, uint32_t q1, uint32_t P,
+                               uint32_t pinv0, uint32_t pinv1, uint32_t* __restrict__ pieces) {
   const uint32_t rho = N / n;
   const uint32_t total = p_in * n;
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const uint32_t p = x / n, k = x % n;
-    const size_t src = p + (size_t)rho * k;
+    const size_t src = piece0 + p + (size_t)rho * k;   // input piece piece0 + p of the degree-N vector
 #pragma unroll
     for (int L = 0; L < 2; ++L) {
       const uint32_t q = L ? q1 : q0, pinv = L ? pinv1 : pinv0;
@@ -284,6 +284,34 @@ __global__ void k_pack_comb2(const uint32_t* __restrict__ UW, const uint32_t* __
     const uint32_t tb = T[(((size_t)L * cnt + idx) * 2 + 1) * n + c];
     dst[0] = add_mod(dst[0], u, q);
     dst[n] = add_mod(dst[n], add_mod(tb, w, q), q);
+  }
+}
+// shard output (level 1, no rescale), composed: out [L][ab][N], piece o at o0 + o + rho k (zeros elsewhere)
+__global__ void k_rh_compose_l1(const uint32_t* __restrict__ A, uint32_t p_out, uint32_t o0, uint32_t n, uint32_t N,
+                                uint32_t* __restrict__ out) {
+  const uint32_t rho = N / n;
+  const uint64_t per_l = (uint64_t)p_out * 2 * n;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * per_l; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t L = (uint32_t)(x / per_l);
+    const uint64_t r = x % per_l;
+    const uint32_t k = (uint32_t)(r % n), ab = (uint32_t)((r / n) % 2), o = (uint32_t)(r / (2ull * n));
+    out[((size_t)L * 2 + ab) * N + o0 + o + (size_t)rho * k] = A[x];
+  }
+}
+// sum of shard outputs mod q_L, then rescale by q1:  parts [count][2 limbs][2][N] -> out [2][N]
+__global__ void k_rh_combine(const uint32_t* __restrict__ parts, uint32_t count, uint32_t N, uint32_t q0, uint32_t q1,
+                             uint32_t q1inv, uint32_t q1invp, uint32_t* __restrict__ out) {
+  const size_t per = (size_t)4 * N;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 2 * N; x += gridDim.x * blockDim.x) {
+    uint32_t s0 = 0, s1 = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+      s0 = add_mod(s0, parts[i * per + x], q0);
+      s1 = add_mod(s1, parts[i * per + 2 * (size_t)N + x], q1);
+    }
+    uint32_t t;
+    if (s1 > (q1 >> 1)) t = csub(s0 + (q1 - s1), q0);
+    else t = sub_mod(s0, s1, q0);
+    out[x] = shoup_mul(t, q1inv, q1invp, q0);
   }
 }
 // rescale by q1 and compose: out[ab][o + rho k]  (A coefficient form [L][p_out][2][n])
@@ -521,10 +549,14 @@ extern "C" he_status he_rhombus_workspace_bytes(const he_rhombus_plan* p, uint64
   return HE_OK;
 }
 
-extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level,
-                                    const uint32_t* ksk_dec, const uint32_t* gal, uint32_t* out, void* ws_dev,
-                                    uint64_t ws_bytes, void* stream, he_ledger* ledger) {
+static he_status rhombus_run_impl(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level,
+                                  const uint32_t* ksk_dec, const uint32_t* gal, uint32_t* out, void* ws_dev,
+                                  uint64_t ws_bytes, void* stream, he_ledger* ledger, uint32_t piece0, int shard,
+                                  uint32_t opiece0) {
   if (!p) return fail(HE_EINVAL, "null plan");
+  if (shard && (piece0 + p->p_in > p->N / p->n || opiece0 + p->p_out > p->N / p->n))
+    return fail(HE_EINVAL, "shard pieces [%u, %u) in / [%u, %u) out exceed the %u pieces of one ciphertext", piece0,
+                piece0 + p->p_in, opiece0, opiece0 + p->p_out, p->N / p->n);
   if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmv needs one level");
   if (level != 1) return fail(HE_EINVAL, "the Rhombus PCMv runs at level 1 (got %u)", level);
   if (!ct_in || !ksk_dec || !gal || !out || !ws_dev) return fail(HE_EINVAL, "null argument");
@@ -541,8 +573,8 @@ extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct
   for (int j = 0; j < 3; ++j) HE_CUDA(ntt_forward(c->ntt[j], w.dD + (size_t)j * 2 * N, 2, N, st), "NTT(digits)");
   k_mac<<<grid_for(N), 256, 0, st>>>(w.dD, ksk_dec, N, N, p->M, w.dUW);
   for (int j = 0; j < 3; ++j) HE_CUDA(ntt_inverse(c->ntt[j], w.dUW + (size_t)j * 2 * N, 2, N, st), "INTT(U,W)");
-  k_decomp_split<<<grid_for((uint64_t)p->p_in * n), 256, 0, st>>>(w.dUW, ct_in, N, n, p->p_in, q0, q1, P, p->pinv[0],
-                                                                   p->pinv[1], w.pieces);
+  k_decomp_split<<<grid_for((uint64_t)p->p_in * n), 256, 0, st>>>(w.dUW, ct_in, N, n, p->p_in, piece0, q0, q1, P,
+                                                                   p->pinv[0], p->pinv[1], w.pieces);
   for (int L = 0; L < 2; ++L)
     HE_CUDA(ntt_forward(c->ntt_rh[L], w.pieces + (size_t)L * p->p_in * 2 * n, p->p_in * 2, n, st), "NTT(pieces)");
   // (M) row ciphertexts
@@ -586,14 +618,45 @@ extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct
   // (R) + (C)
   for (int L = 0; L < 2; ++L)
     HE_CUDA(ntt_inverse(c->ntt_rh[L], A + (size_t)L * cnt * 2 * n, cnt * 2, n, st), "INTT(packed)");
-  HE_CUDA(cudaMemsetAsync(out, 0, 2ull * N * sizeof(uint32_t), st), "memset");
-  k_rh_rescale_compose<<<grid_for((uint64_t)cnt * 2 * n), 256, 0, st>>>(A, cnt, n, N, q0, q1, p->q1inv, p->q1invp, out);
+  if (shard) {
+    HE_CUDA(cudaMemsetAsync(out, 0, 4ull * N * sizeof(uint32_t), st), "memset");
+    k_rh_compose_l1<<<grid_for((uint64_t)cnt * 4 * n), 256, 0, st>>>(A, cnt, opiece0, n, N, out);
+  } else {
+    HE_CUDA(cudaMemsetAsync(out, 0, 2ull * N * sizeof(uint32_t), st), "memset");
+    k_rh_rescale_compose<<<grid_for((uint64_t)cnt * 2 * n), 256, 0, st>>>(A, cnt, n, N, q0, q1, p->q1inv, p->q1invp, out);
+  }
   HE_CUDA(cudaGetLastError(), "rhombus launch");
   if (ledger) {
     ledger->pc_mults += (int64_t)p->n_out * p->p_in;
     ledger->ct_rotations += (int64_t)(n - 1) * p->p_out;
-    ledger->rescales += 1;
+    ledger->rescales += shard ? 0 : 1;
   }
+  return HE_OK;
+}
+
+extern "C" he_status he_rhombus_run(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level,
+                                    const uint32_t* ksk_dec, const uint32_t* gal, uint32_t* out, void* ws_dev,
+                                    uint64_t ws_bytes, void* stream, he_ledger* ledger) {
+  return rhombus_run_impl(p, ct_in, level, ksk_dec, gal, out, ws_dev, ws_bytes, stream, ledger, 0, 0, 0);
+}
+
+extern "C" he_status he_rhombus_run_shard(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level,
+                                          const uint32_t* ksk_dec, const uint32_t* gal, uint32_t piece0,
+                                          uint32_t opiece0, uint32_t* out_l1, void* ws_dev, uint64_t ws_bytes,
+                                          void* stream, he_ledger* ledger) {
+  return rhombus_run_impl(p, ct_in, level, ksk_dec, gal, out_l1, ws_dev, ws_bytes, stream, ledger, piece0, 1, opiece0);
+}
+
+extern "C" he_status he_rhombus_combine(const he_context* c, const uint32_t* parts, uint32_t count, uint32_t* out,
+                                        void* stream, he_ledger* ledger) {
+  if (!c || !parts || !out) return fail(HE_EINVAL, "null argument");
+  if (count == 0) return fail(HE_EINVAL, "no shard outputs to combine");
+  const uint32_t q0 = c->R.q[0], q1 = c->R.q[1];
+  const uint32_t q1inv = (uint32_t)powmod_h(q1 % q0, q0 - 2, q0);
+  k_rh_combine<<<grid_for(2ull * c->R.N), 256, 0, (cudaStream_t)stream>>>(parts, count, c->R.N, q0, q1, q1inv,
+                                                                           shoup_pre(q1inv, q0), out);
+  HE_CUDA(cudaGetLastError(), "rhombus combine");
+  if (ledger) ledger->rescales += 1;
   return HE_OK;
 }
 

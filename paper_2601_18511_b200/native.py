@@ -30,7 +30,7 @@ EXPORTS = (
     "he_pcmm_gemm_rows", "he_pcmm_spectral_weight_bytes", "he_pcmm_spectral_prepare", "he_pcmm_algo",
     "he_pcmm_profile", "he_pcmm_profile_read", "he_pcmm_spectral_info", "he_pcmm_gemm_rows_peers",
     "he_pcmm_run_level1", "he_ring_pack_key_bytes", "he_ring_pack_keygen", "he_ring_pack_plan_create", "he_ring_pack_plan_destroy",
-    "he_ring_pack_workspace_bytes", "he_ring_pack_run",
+    "he_ring_pack_workspace_bytes", "he_ring_pack_run", "he_rhombus_run_shard", "he_rhombus_combine",
 )
 
 
@@ -100,6 +100,8 @@ def lib():
             "he_rhombus_workspace_bytes": (st, [vp, ctypes.POINTER(u64)]),
             "he_rhombus_run": (st, [vp, vp, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_pcmm_run_level1": (st, [vp, vp, u32, vp, vp, vp, u64, vp]),
+            "he_rhombus_run_shard": (st, [vp, vp, u32, vp, vp, u32, u32, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
+            "he_rhombus_combine": (st, [vp, vp, u32, vp, vp, ctypes.POINTER(HeLedgerC)]),
             "he_ring_pack_key_bytes": (st, [vp, i32, ctypes.POINTER(u64)]),
             "he_ring_pack_keygen": (st, [vp, i32, u64, vp, vp, vp]),
             "he_ring_pack_plan_create": (st, [vp, u32, i32, ctypes.POINTER(vp)]),

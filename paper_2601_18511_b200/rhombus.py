@@ -177,3 +177,38 @@ def decode_vector(params, phase: np.ndarray, n_vals: int) -> np.ndarray:
 
 def clear_pcmv(weights, v) -> np.ndarray:
     return np.asarray(weights, float) @ np.asarray(v, float)
+
+
+def pcmv_rhombus_shard(ctx: HeContext, plan: RhombusPlan, keys: RhombusKeys, x: CtVector, piece0: int = 0,
+                       opiece0: int = 0):
+    """One shard of a sharded PCMv (sharding.pcmv_rhombus_sharded): `plan` covers W[n opiece0 ..,
+    n piece0 ..]; returns its LEVEL-1 composed partial output, int32 view of u32 [2 limbs, 2, N]."""
+    torch = _torch()
+    if not isinstance(x, CtVector):
+        raise TypeError("pcmv consumes a ciphertext operand")
+    if x.key != "s":
+        raise ValueError("pcmv input must be under the degree-N secret s")
+    require_level(x.level)
+    if x.level != 1:
+        raise ValueError(f"the Rhombus PCMv runs at level 1, operand is at level {x.level}")
+    out = torch.empty((2, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
+    ws = plan.workspace(ctx.device)
+    led = native.HeLedgerC()
+    native.call("he_rhombus_run_shard", plan._handle, x.data.data_ptr(), x.level, keys.ksk_dec.data_ptr(),
+                keys.gal.data_ptr(), int(piece0), int(opiece0), out.data_ptr(), ws.data_ptr(), ws.numel() * 4,
+                ctx.stream(), ctypes.byref(led))
+    ctx.ledger.add_c(led)
+    return out
+
+
+def combine_rhombus_parts(ctx: HeContext, parts, n_vals: int) -> CtVector:
+    """Sum level-1 shard outputs [count, 2, 2, N] mod q_i and rescale once -> level-0 CtVector."""
+    torch = _torch()
+    parts = parts.contiguous()
+    out = torch.empty((1, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
+    led = native.HeLedgerC()
+    native.call("he_rhombus_combine", ctx.handle, parts.data_ptr(), int(parts.shape[0]), out.data_ptr(), ctx.stream(),
+                ctypes.byref(led))
+    ctx.ledger.add_c(led)
+    ctx.ledger.observe_level(0)
+    return CtVector(out, level=0, n_vals=n_vals, key="s_up")

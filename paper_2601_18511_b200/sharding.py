@@ -37,12 +37,37 @@ def shard_slots(n_out: int, k: int, world: int) -> int:
     return math.ceil((n_out // k) / world)
 
 
+def _staged(t, group) -> bool:
+    """gloo moves host tensors: device tensors are staged through host memory (CPU tests and
+    several ranks sharing one GPU); NCCL moves device memory directly over NVLink."""
+    import torch.distributed as dist
+
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
+def all_gather_into(out, t, group=None):
+    import torch.distributed as dist
+
+    if _staged(t, group):
+        host = out.new_empty(out.shape, device="cpu")
+        dist.all_gather_into_tensor(host, t.contiguous().cpu(), group=group)
+        out.copy_(host)
+    else:
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    return out
+
+
 def broadcast_input(data, group=None, src: int = 0):
     """C2: every rank needs the whole input ciphertext batch."""
     import torch.distributed as dist
 
     if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.broadcast(data, src=src, group=group)
+        if _staged(data, group):
+            host = data.cpu()
+            dist.broadcast(host, src=src, group=group)
+            data.copy_(host)
+        else:
+            dist.broadcast(data, src=src, group=group)
     return data
 
 
@@ -61,8 +86,8 @@ def gather_row_shards(local_b, local_a, k: int, n_out: int, group=None):
     per = local_b.shape[0]
     all_b = torch.empty((per * world,) + tuple(local_b.shape[1:]), dtype=local_b.dtype, device=local_b.device)
     all_a = torch.empty((per * world * k,) + tuple(local_a.shape[1:]), dtype=local_a.dtype, device=local_a.device)
-    dist.all_gather_into_tensor(all_b, local_b.contiguous(), group=group)
-    dist.all_gather_into_tensor(all_a, local_a.contiguous(), group=group)
+    all_gather_into(all_b, local_b, group)
+    all_gather_into(all_a, local_a, group)
     # every shard is padded at its end to `per` slots; keep each rank's real blocks
     spans = row_shards(n_out, k, world)
     keep_b = torch.cat([all_b[r * per: r * per + (b1 - b0)] for r, (b0, b1) in enumerate(spans)])
@@ -89,7 +114,95 @@ def symmetric_outputs(ctx, n_out: int, group=None):
         ha = symm.rendezvous(out_a, grp)
         return out_b, out_a, list(hb.buffer_ptrs), list(ha.buffer_ptrs), hb
     except Exception:  # pragma: no cover - depends on the box
+        pass
+    try:
+        return ipc_outputs(ctx, n_out, group)
+    except Exception:  # pragma: no cover - no CUDA IPC on this box
         return None
+
+
+class _IpcBuffers:
+    """Full-size output buffers allocated with cudaMalloc and mapped into every rank with CUDA IPC
+    (cudaIpcGetMemHandle / cudaIpcOpenMemHandle, peer access over NVLink enabled lazily): the
+    symmetric-memory fallback for process groups without it (e.g. gloo).  barrier() publishes the
+    peer stores: device sync, then a group barrier."""
+
+    def __init__(self, nbytes: list, device, group):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        class Handle(ctypes.Structure):  # cudaIpcMemHandle_t, passed by value
+            _fields_ = [("reserved", ctypes.c_char * 64)]
+
+        self.group = group
+        self.rt = ctypes.CDLL("libcudart.so.12")
+        self.rt.cudaMalloc.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t]
+        self.rt.cudaIpcGetMemHandle.argtypes = [ctypes.POINTER(Handle), ctypes.c_void_p]
+        self.rt.cudaIpcOpenMemHandle.argtypes = [ctypes.POINTER(ctypes.c_void_p), Handle, ctypes.c_uint]
+        torch.cuda.set_device(device)
+        self.local, self.opened = [], []
+        handles = []
+        for nb in nbytes:
+            ptr = ctypes.c_void_p()
+            if self.rt.cudaMalloc(ctypes.byref(ptr), nb):
+                raise RuntimeError("cudaMalloc failed")
+            self.local.append(ptr.value)
+            h = Handle()
+            if self.rt.cudaIpcGetMemHandle(ctypes.byref(h), ptr):
+                self.rt.cudaGetLastError()
+                raise RuntimeError("cudaIpcGetMemHandle failed")
+            handles.append(ctypes.string_at(ctypes.addressof(h), 64))
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        every = [None] * world
+        dist.all_gather_object(every, handles, group=group)
+        self.ptrs = []   # ptrs[i][r]: buffer i of rank r as seen from this rank
+        for i in range(len(nbytes)):
+            row = []
+            for r in range(world):
+                if r == rank:
+                    row.append(self.local[i])
+                    continue
+                p = ctypes.c_void_p()
+                if self.rt.cudaIpcOpenMemHandle(ctypes.byref(p), Handle.from_buffer_copy(every[r][i]), 1):
+                    self.rt.cudaGetLastError()
+                    raise RuntimeError("cudaIpcOpenMemHandle failed")
+                self.opened.append(p.value)
+                row.append(p.value)
+            self.ptrs.append(row)
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+
+
+def _device_view(ptr: int, shape, device):
+    """int32 torch tensor over raw device memory (kept alive by the _IpcBuffers owner)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i4", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+
+    return torch.as_tensor(_Arr(), device=device)
+
+
+def ipc_outputs(ctx, n_out: int, group=None):
+    import torch.distributed as dist
+
+    p = ctx.params
+    shp_b, shp_a = (n_out // p.mlwe_rank, p.N), (n_out, p.N)
+    bufs = _IpcBuffers([shp_b[0] * shp_b[1] * 4, shp_a[0] * shp_a[1] * 4], ctx.device, group)
+    out_b = _device_view(bufs.local[0], shp_b, ctx.device)
+    out_a = _device_view(bufs.local[1], shp_a, ctx.device)
+    out_b._ipc_owner = bufs   # keep the mappings alive with the views
+    del dist
+    return out_b, out_a, bufs.ptrs[0], bufs.ptrs[1], bufs
 
 
 def pcmm_mlwe_sharded_fused(ctx, plan, X, n_out: int, row0: int, sym, group=None):
@@ -125,3 +238,79 @@ def pcmm_mlwe_sharded(ctx, plan, X, n_out: int, group=None, out_b=None, out_a=No
     broadcast_input(X.data, group)
     pcmm_mlwe(ctx, plan, X, out=MlweBlocks(out_b[: rows // k], out_a[:rows], level=0, n_rows=rows))
     return gather_row_shards(out_b, out_a, k, n_out, group)
+
+
+# ---------------------------------------------------------------- Rhombus PCMv over several GPUs
+def rhombus_shards(n_out: int, n_in: int, n: int, world: int, strategy: str = "auto") -> list[dict]:
+    """Piece-aligned slices of W for the Rhombus PCMv.
+
+    A piece is n = rhombus_degree vector elements.  "rows": split the output pieces (each rank packs
+    whole output pieces -- no reduction, words identical to one GPU); "cols": split the input pieces
+    (every rank packs partial sums of all output pieces -- a ciphertext sum mod q, then one rescale);
+    "auto": whichever dimension has more pieces (rows on ties).  Returns per rank
+    {"rows": (r0, r1), "cols": (c0, c1), "opiece0": .., "piece0": ..}; a rank with nothing to do gets
+    an empty slice (r0 == r1 or c0 == c1) and contributes a zero partial."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    p_out, p_in = -(-n_out // n), -(-n_in // n)
+    if strategy == "auto":
+        strategy = "rows" if p_out >= p_in else "cols"
+    if strategy not in ("rows", "cols"):
+        raise ValueError(f"unknown Rhombus shard strategy {strategy!r}")
+    pieces = p_out if strategy == "rows" else p_in
+    base, extra = divmod(pieces, world)
+    out, p0 = [], 0
+    for r in range(world):
+        p1 = p0 + base + (1 if r < extra else 0)
+        if strategy == "rows":
+            out.append({"strategy": "rows", "rows": (min(p0 * n, n_out), min(p1 * n, n_out)), "cols": (0, n_in),
+                        "opiece0": p0, "piece0": 0})
+        else:
+            out.append({"strategy": "cols", "rows": (0, n_out), "cols": (min(p0 * n, n_in), min(p1 * n, n_in)),
+                        "opiece0": 0, "piece0": p0})
+        p0 = p1
+    return out
+
+
+def pcmv_rhombus_sharded(ctx, W, keys, x, group=None, strategy: str = "auto"):
+    """Rhombus PCMv with W sliced over the ranks of `group`: each rank builds the plan of its slice,
+    runs it on the (broadcast) input to a level-1 partial output, the partials are all-gathered
+    (2 x 2 x N words each) and summed mod q_i with one rescale (he_rhombus_combine).  Returns the
+    same level-0 CtVector on every rank."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from .rhombus import combine_rhombus_parts, make_rhombus_plan, pcmv_rhombus_shard
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    W = np.asarray(W, dtype=np.float64) if not isinstance(W, torch.Tensor) else W
+    broadcast_input(x.data, group)
+    n_out, n_in = int(W.shape[0]), int(W.shape[1])
+    sl = rhombus_shards(n_out, n_in, ctx.params.rhombus_degree, world, strategy)[rank]
+    (r0, r1), (c0, c1) = sl["rows"], sl["cols"]
+    N = ctx.params.N
+    if r1 > r0 and c1 > c0:
+        plan = make_rhombus_plan(ctx, W[r0:r1, c0:c1])
+        part = pcmv_rhombus_shard(ctx, plan, keys, x, sl["piece0"], sl["opiece0"])
+    else:
+        part = torch.zeros((2, 2, N), dtype=torch.int32, device=ctx.device)
+    if world > 1:
+        parts = torch.empty((world, 2, 2, N), dtype=torch.int32, device=ctx.device)
+        all_gather_into(parts, part[None], group)
+    else:
+        parts = part[None]
+    return combine_rhombus_parts(ctx, parts, n_out)
+
+
+def all_reduce_max(t, group=None):
+    """MAX all-reduce (timings: the max over ranks), staged through the host for gloo."""
+    import torch.distributed as dist
+
+    if _staged(t, group):
+        host = t.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.MAX, group=group)
+        return host.to(t.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t

@@ -89,3 +89,44 @@ def test_llama_pcmv_precision(n_out, n_in):
     res = decrypt_vector(ctx, keys.s_up_ntt, y)
     err = np.abs(res - clear_pcmv(W, v)).max()
     assert err < 2 ** -12, err
+
+
+@pytest.mark.parametrize("params,n_out,n_in,strategy,world", [
+    ("toy", 300, 200, "rows", 3),        # toy pieces are n = 128 elements
+    ("toy", 100, 300, "cols", 2),
+    ("llama", 8192, 4096, "rows", 2),
+    ("llama", 14336, 4096, "rows", 3),
+    ("llama", 4096, 11008, "cols", 3),
+    ("llama", 4096, 11008, "auto", 8),   # 3 input pieces over 8 ranks: 5 idle ranks add zeros
+])
+def test_sharded_pcmv_emulated_ranks(params, n_out, n_in, strategy, world):
+    """§8e Rhombus sharding, every rank's work run on this one GPU: row shards reproduce the
+    one-GPU output words exactly; column shards (a ciphertext sum, different key-switching noise)
+    decrypt to the same W v within the stated precision."""
+    import torch
+
+    from paper_2601_18511_b200.rhombus import combine_rhombus_parts, pcmv_rhombus_shard
+    from paper_2601_18511_b200.sharding import rhombus_shards
+
+    P = HeParams.toy() if params == "toy" else HeParams.llama()
+    ctx, sk, keys, x, v, W = _setup(P, n_out, n_in, seed=n_out)
+    full = pcmv_rhombus(ctx, make_rhombus_plan(ctx, W), keys, x)
+    parts = []
+    slices = rhombus_shards(n_out, n_in, P.rhombus_degree, world, strategy)
+    for sl in slices:
+        (r0, r1), (c0, c1) = sl["rows"], sl["cols"]
+        if r1 > r0 and c1 > c0:
+            parts.append(pcmv_rhombus_shard(ctx, make_rhombus_plan(ctx, W[r0:r1, c0:c1]), keys, x, sl["piece0"],
+                                            sl["opiece0"]))
+        else:
+            parts.append(torch.zeros((2, 2, P.N), dtype=torch.int32, device=ctx.device))
+    y = combine_rhombus_parts(ctx, torch.stack(parts), n_out)
+    ref = clear_pcmv(W, v)
+    res = decrypt_vector(ctx, keys.s_up_ntt, y)
+    if slices[0]["strategy"] == "rows":
+        assert torch.equal(y.data, full.data)
+    else:
+        full_res = decrypt_vector(ctx, keys.s_up_ntt, full)
+        assert np.abs(res - full_res).max() < 2 ** -18
+    err = np.abs(res - ref).max()
+    assert err < np.abs(ref).max() * 2 ** -13, err

@@ -84,3 +84,26 @@ def test_row_sharded_pcmm_gathers_exact_output(world, n_out):
     for p in procs:
         p.join(timeout=60)
     assert res == {r: "ok" for r in range(world)}
+
+
+def test_rhombus_shards_cover_the_matrix_once():
+    from paper_2601_18511_b200.sharding import rhombus_shards
+
+    n = 4096
+    for n_out, n_in in ((4096, 11008), (14336, 4096), (8192, 4096), (4096, 4096)):
+        for world in (1, 2, 3, 4, 8):
+            sl = rhombus_shards(n_out, n_in, n, world)
+            assert len(sl) == world
+            strat = sl[0]["strategy"]
+            assert strat == ("rows" if -(-n_out // n) >= -(-n_in // n) else "cols")
+            spans = [s["rows"] if strat == "rows" else s["cols"] for s in sl]
+            total = n_out if strat == "rows" else n_in
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0 and a0 <= a1
+            for s in sl:   # piece-aligned offsets (idle ranks: empty slice at the end)
+                lo, hi = s["rows"] if strat == "rows" else s["cols"]
+                if hi > lo:
+                    assert lo % n == 0 and (s["opiece0"] if strat == "rows" else s["piece0"]) == lo // n
+    with pytest.raises(ValueError):
+        rhombus_shards(4096, 4096, n, 2, strategy="diagonal")
