@@ -632,7 +632,22 @@ def cpu_baseline(P, A, plan, X, n_out, n_in, n_rows, W_seed_dev=None, g_seed=Non
             "sample": f"oracle/ C restatement: {n_rows} of {n_out} output rows x {P.width} cols x K={n_in}, "
                       f"both limbs + rescale, {res['seconds']:.2f} s, extrapolated x{n_out / n_rows:.0f}",
             "plaintext_floor_ms": round(floor_ms, 2),
-            "plaintext_floor": f"numpy float64 acts @ W.T ({P.tokens} x {n_in} x {n_out}) on the host, unencrypted"}
+            "plaintext_floor": f"numpy float64 acts @ W.T ({P.tokens} x {n_in} x {n_out}) on the host, unencrypted",
+            "hesim_context": hesim_context()}
+
+
+def hesim_context():
+    """the reference's own slot-domain pcmm_bsgs (float simulator) at its largest
+    feasible size, measured in the build container by tools/hesim_context_timing.py (the reference is
+    not on the GPU box) and committed under profiles/r01/."""
+    f = Path(__file__).resolve().parent / "profiles" / "r01" / "hesim_pcmm_bsgs_cpu.json"
+    try:
+        d = json.loads(f.read_text())
+        r = d["results"]["128"]
+        return {"d": 128, "pcmm_bsgs_ms": round(1e3 * r["pcmm_bsgs_s"], 2), "plan_ms": round(1e3 * r["plan_s"], 2),
+                "source": "profiles/r01/hesim_pcmm_bsgs_cpu.json (build container, not this host)"}
+    except Exception:
+        return None
 
 
 def run_reference(a, rank: int, world: int):
