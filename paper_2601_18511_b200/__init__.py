@@ -9,8 +9,8 @@ from .errors import NeedsBootstrapError
 from .params import HeParams
 from .context import CostLedger, CtBlocks, HeContext, MlweBlocks, SecretKey, LEDGER_COUNTERS
 from .layout import bit_reverse, byte_mix, half_reverse, rotate_bits_down, shuffle_matrix, sigma_table
-from .pcmm import (MlwePcmmPlan, clear_pcmm, make_mlwe_pcmm_plan, pcmm_mlwe, pcmm_mlwe_into_peers,
-                   pcmm_mlwe_to_host)
+from .pcmm import (MlwePcmmPlan, clear_pcmm, load_mlwe_pcmm_plan, load_plan_bundle, make_mlwe_pcmm_plan, pcmm_mlwe,
+                   pcmm_mlwe_into_peers, pcmm_mlwe_to_host, save_mlwe_pcmm_plan, save_plan_bundle)
 from .rhombus import (CtVector, RhombusKeys, RhombusPlan, clear_pcmv, decrypt_vector, encrypt_vector,
                       make_rhombus_plan, pcmv_rhombus, rhombus_keygen)
 from .ringpack import (RingPackKeys, RingPackPlan, make_ring_pack_plan, pcmm_level1, pcmm_packed, ring_pack,
@@ -20,7 +20,7 @@ __all__ = [
     "NeedsBootstrapError", "HeParams", "CostLedger", "CtBlocks", "HeContext", "MlweBlocks", "SecretKey",
     "LEDGER_COUNTERS", "bit_reverse", "byte_mix", "half_reverse", "rotate_bits_down", "shuffle_matrix",
     "sigma_table", "MlwePcmmPlan", "clear_pcmm", "make_mlwe_pcmm_plan", "pcmm_mlwe", "pcmm_mlwe_to_host",
-    "pcmm_mlwe_into_peers",
+    "pcmm_mlwe_into_peers", "save_mlwe_pcmm_plan", "load_mlwe_pcmm_plan", "save_plan_bundle", "load_plan_bundle",
     "CtVector", "RhombusKeys", "RhombusPlan", "clear_pcmv", "decrypt_vector", "encrypt_vector",
     "make_rhombus_plan", "pcmv_rhombus", "rhombus_keygen",
     "RingPackKeys", "RingPackPlan", "make_ring_pack_plan", "pcmm_level1", "pcmm_packed", "ring_pack",

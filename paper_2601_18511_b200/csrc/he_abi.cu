@@ -81,11 +81,12 @@ static he_status make_map_sw64(CUtensorMap* m, const void* base, uint64_t inner,
 }
 
 // 3-D u32 tensor {inner, rows, planes}, box {box_inner, box_rows, 1}, no swizzle
+// extent <= inner: TMA clips stores past `extent` (the padding columns of a row of pitch `inner`)
 static he_status make_map_u32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t planes,
-                              uint32_t box_inner, uint32_t box_rows) {
+                              uint32_t box_inner, uint32_t box_rows, uint64_t extent = 0) {
   PFN_encodeTiled_t fn = encode_fn();
   if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {inner, rows, planes};
+  cuuint64_t dims[3] = {extent ? extent : inner, rows, planes};
   cuuint64_t strides[2] = {inner * 4, inner * rows * 4};
   cuuint32_t box[3] = {box_inner, box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
@@ -516,7 +517,7 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     he_status s = make_map_sw64(&tmB, A, p->r_pad, p->nbp, (uint64_t)p->L * p->dsp[L], 16);
     if (s) return s;
     CUtensorMap tmC;  // C^ limb L: u32 {d, n_out, 2k}, box {8, 32, 1} (one epilogue warp's TMA store)
-    s = make_map_u32(&tmC, C[L], p->nbp, p->n_out, p->L, 8, 32);
+    s = make_map_u32(&tmC, C[L], p->nbp, p->n_out, p->L, 8, 32, p->nblk);  // padding blocks are never stored
     if (s) return s;
     p->prof_begin(3 + L, st);
     HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, tmC, a, p->ctx->sm_count, st), "spectral gemm");

@@ -151,6 +151,12 @@ def make_mlwe_pcmm_plan(ctx: HeContext, weights, d_w: int | None = None, algo: s
     digits = torch.empty((d_w, n_out, n_in), dtype=torch.int8, device=ctx.device)
     native.call("he_pcmm_encode_weights", ctx.handle, w.data_ptr(), n_out, n_in, d_w, digits.data_ptr(),
                 ctx.stream())
+    return _plan_from_digits(ctx, digits, n_out, n_in, d_w, max_abs, algo)
+
+
+def _plan_from_digits(ctx: HeContext, digits, n_out: int, n_in: int, d_w: int, max_abs: int,
+                      algo: str) -> MlwePcmmPlan:
+    torch = _torch()
     h = ctypes.c_void_p()
     native.call("he_pcmm_plan_create", ctx.handle, digits.data_ptr(), n_out, n_in, d_w, ctypes.byref(h))
     plan = MlwePcmmPlan(n_out, n_in, d_w, max_abs, digits, algo=algo, _handle=h)
@@ -160,6 +166,79 @@ def make_mlwe_pcmm_plan(ctx: HeContext, weights, d_w: int | None = None, algo: s
         plan.spec_weights = torch.empty(int(nb.value), dtype=torch.int8, device=ctx.device)
         native.call("he_pcmm_spectral_prepare", h, plan.spec_weights.data_ptr(), ctx.stream())
     return plan
+
+
+# ---------------------------------------------------------------- on-disk plan format
+PLAN_FORMAT = "he-b200/mlwe-pcmm-plan/1"
+
+
+def _param_key(params) -> dict:
+    """The parameters a plan's digits depend on (ring, moduli, weight scale = q1)."""
+    return {"N": int(params.N), "mlwe_degree": int(params.mlwe_degree), "mlwe_rank": int(params.mlwe_rank),
+            "moduli": [int(q) for q in params.moduli], "delta_w": int(params.delta_w)}
+
+
+def save_mlwe_pcmm_plan(ctx: HeContext, plan: MlwePcmmPlan, path) -> None:
+    """Write the plan's pre-shuffled balanced int8 digit planes [d_w, n_out, n_in] (the expensive,
+    weight-only part) plus a JSON header to one uncompressed .npz.  The spectral weights are not
+    stored: he_pcmm_spectral_prepare rebuilds them from the digits on the device at load."""
+    import json
+
+    meta = {"format": PLAN_FORMAT, "params": _param_key(ctx.params), "n_out": plan.n_out, "n_in": plan.n_in,
+            "d_w": plan.d_w, "max_abs": plan.max_abs, "layout": plan.layout, "algo": plan.algo}
+    np.savez(path, meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8),
+             digits=plan.digits.cpu().numpy())
+
+
+def load_mlwe_pcmm_plan(ctx: HeContext, path, algo: str | None = None) -> MlwePcmmPlan:
+    """Rebuild a plan from save_mlwe_pcmm_plan's file on ctx's device (algo: the stored one unless
+    given).  Raises ValueError if the file was made for other parameters or another format."""
+    import json
+
+    torch = _torch()
+    with np.load(path) as z:
+        meta = json.loads(bytes(z["meta"]).decode())
+        if meta.get("format") != PLAN_FORMAT:
+            raise ValueError(f"not an MLWE PCMM plan file ({meta.get('format')!r})")
+        if meta["params"] != _param_key(ctx.params):
+            raise ValueError(f"plan was encoded for {meta['params']}, context has {_param_key(ctx.params)}")
+        digits = z["digits"]
+    n_out, n_in, d_w = int(meta["n_out"]), int(meta["n_in"]), int(meta["d_w"])
+    if digits.shape != (d_w, n_out, n_in) or digits.dtype != np.int8:
+        raise ValueError(f"digit planes have shape {digits.shape} / {digits.dtype}")
+    algo = algo or meta["algo"]
+    if algo not in ALGOS:
+        raise ValueError(f"algo must be one of {ALGOS}, got {algo!r}")
+    dev = torch.from_numpy(np.ascontiguousarray(digits)).to(ctx.device)
+    return _plan_from_digits(ctx, dev, n_out, n_in, d_w, int(meta["max_abs"]), algo)
+
+
+def save_plan_bundle(ctx: HeContext, plans: dict, directory) -> None:
+    """A model's projections (e.g. 32 layers x {q, k, v, o, up, gate, down}): one plan file per
+    name plus index.json."""
+    import json
+    from pathlib import Path
+
+    d = Path(directory)
+    d.mkdir(parents=True, exist_ok=True)
+    index = {"format": PLAN_FORMAT, "plans": {}}
+    for name, plan in plans.items():
+        fn = f"{name}.npz"
+        save_mlwe_pcmm_plan(ctx, plan, d / fn)
+        index["plans"][name] = {"file": fn, "shape": [plan.n_out, plan.n_in], "d_w": plan.d_w}
+    (d / "index.json").write_text(json.dumps(index, indent=1))
+
+
+def load_plan_bundle(ctx: HeContext, directory, algo: str | None = None, names=None) -> dict:
+    import json
+    from pathlib import Path
+
+    d = Path(directory)
+    index = json.loads((d / "index.json").read_text())
+    if index.get("format") != PLAN_FORMAT:
+        raise ValueError(f"not a plan bundle ({index.get('format')!r})")
+    return {n: load_mlwe_pcmm_plan(ctx, d / e["file"], algo) for n, e in index["plans"].items()
+            if names is None or n in names}
 
 
 def _check_operand(ctx: HeContext, plan: MlwePcmmPlan, X) -> None:

@@ -348,3 +348,29 @@ def test_fused_sharded_symmetric_memory_single_rank():
     P = HeParams.llama()
     ctx = HeContext(P)
     assert symmetric_outputs(ctx, 512) is None
+
+
+def test_plan_files_round_trip(tmp_path):
+    """On-disk plan format (§8f 4): saved digit planes reload to a plan with the same output words;
+    files made for other parameters or other formats are refused."""
+    import torch
+
+    from paper_2601_18511_b200 import load_mlwe_pcmm_plan, load_plan_bundle, save_mlwe_pcmm_plan, save_plan_bundle
+
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, 512, 1024, seed=8)
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    ref = pcmm_mlwe(ctx, plan, X)
+    ra, rb = ref.out_a.clone(), ref.out_b.clone()
+    save_mlwe_pcmm_plan(ctx, plan, tmp_path / "p.npz")
+    for algo in (None, "direct"):
+        p2 = load_mlwe_pcmm_plan(ctx, tmp_path / "p.npz", algo=algo)
+        assert p2.algo == (algo or "spectral") and p2.shape == plan.shape and p2.d_w == plan.d_w
+        Y = pcmm_mlwe(ctx, p2, X)
+        torch.cuda.synchronize()
+        assert torch.equal(Y.out_a, ra) and torch.equal(Y.out_b, rb)
+    save_plan_bundle(ctx, {"layer0.down": plan}, tmp_path / "bundle")
+    b = load_plan_bundle(ctx, tmp_path / "bundle")
+    assert list(b) == ["layer0.down"] and torch.equal(pcmm_mlwe(ctx, b["layer0.down"], X).out_a, ra)
+    with pytest.raises(ValueError):
+        load_mlwe_pcmm_plan(HeContext(HeParams.toy()), tmp_path / "p.npz")
