@@ -57,6 +57,7 @@ typedef struct he_context he_context;     /* NTT tables, device constants       
 typedef struct he_pcmm_plan he_pcmm_plan; /* weight side of the MLWE PCMM       */
 typedef struct he_rhombus_plan he_rhombus_plan; /* weight side of the Rhombus PCMv */
 typedef struct he_ring_pack_plan he_ring_pack_plan; /* MLWE -> RLWE ring packing tables */
+typedef struct he_slot_pcmm_plan he_slot_pcmm_plan; /* slot-domain BSGS PCMM (hesim pcmm_bsgs) */
 
 /* Operation counters, same field names as hesim.CostLedger (slotsim.py:31-83). */
 typedef struct {
@@ -232,6 +233,34 @@ he_status he_ring_pack_workspace_bytes(const he_ring_pack_plan* plan, uint64_t* 
 he_status he_ring_pack_run(const he_ring_pack_plan* plan, const uint32_t* raw_b_dev, const uint32_t* raw_a_dev,
                            const uint32_t* keys_dev, uint32_t* out_dev, void* workspace_dev, uint64_t workspace_bytes,
                            void* stream, he_ledger* ledger);
+
+/* ---------------------------------------------------------------- slot-domain PCMM
+ * hesim's own PCMM, pcmm_bsgs (matmul.py:165-176), on real CKKS ciphertexts: a d x d matrix row-major
+ * in the slots (tiled, packing.py:1-17), left slot rotation by r = X -> X^(5^r) + hybrid key switch.
+ * baby_i = rot(ct, i d) (hoisted digits), inner_j = sum_i pt_{i + j b} baby_i, out = rescale(sum_j
+ * rot(inner_j, j b d)).  Plaintext blocks are CKKS slot encodings (canonical embedding, scale q1)
+ * computed by the caller (paper_2601_18511_b200/slots.py) as signed int64 coefficients.
+ * Oracle: or_slot_pcmm (oracle/he_oracle_rhombus.c). */
+/* encrypt raw integer plaintext polynomials pt [n_ct][N] (int64, signed) at level 1 */
+he_status he_encrypt_poly(const he_context* ctx, const uint32_t* s_ntt_dev, const int64_t* pt_dev, uint32_t n_ct,
+                          uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream);
+/* rotation keys sigma_{5^r}(s) -> s for the host list steps[n]: keys_dev [n][4][2][3][N] (NTT domain; gadget
+ * hybrid keys: each of the 2 RNS digits split into 2 sub-digits of 15 bits, ids 0x10000 + r) */
+he_status he_slot_rotation_keygen(const he_context* ctx, uint64_t seed, const int32_t* s_dev, const int32_t* steps,
+                                  uint32_t n_steps, uint32_t* keys_dev, void* stream);
+/* int64 plaintext polys [count][N] -> NTT-domain residues [count][2][N] */
+he_status he_slot_pcmm_encode_pts(const he_context* ctx, const int64_t* pt_dev, uint32_t count, uint32_t* pts_ntt_dev,
+                                  void* stream);
+/* pts_ntt_dev [d][2][N] (block k = i + j b) stays caller-owned; b * g == d, d^2 <= N/2 */
+he_status he_slot_pcmm_plan_create(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t d, uint32_t b,
+                                   uint32_t g, he_slot_pcmm_plan** out);
+he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* plan);
+he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* plan, uint64_t* bytes);
+/* ct_in [2][2][N] level 1 -> out [2 (a, b)][N] level 0.  keys_baby: steps i d (i = 1 .. b-1), keys_giant:
+ * steps j b d (j = 1 .. g-1).  ledger: ct_rotations += (b-1) + (g-1), pc_mults += d, rescales += 1 */
+he_status he_slot_pcmm_run(const he_slot_pcmm_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
+                           const uint32_t* keys_baby_dev, const uint32_t* keys_giant_dev, uint32_t* out_dev,
+                           void* workspace_dev, uint64_t workspace_bytes, void* stream, he_ledger* ledger);
 
 #ifdef __cplusplus
 }

@@ -517,3 +517,173 @@ int or_mlwe_to_rlwe(uint32_t d, uint32_t k, const uint32_t* m, const uint32_t* r
   }
   return 0;
 }
+
+/* ================================================================== slot-domain BSGS PCMM
+ * hesim pcmm_bsgs (matmul.py:165-176) on real CKKS ciphertexts: the input matrix sits row-major in the
+ * slots (tiled), a left slot rotation by r is the automorphism X -> X^(5^r) followed by a hybrid key
+ * switch (dnum 2, special prime P) from sigma(s) back to s.  Integer algorithm (the CUDA path is
+ * bit-exact with it):
+ *   D = digits of ct.a (RNS digits d_i = a_i Qhat_i^-1 mod q_i, lifted to q0, q1, P)      -- once (hoisting)
+ *   baby_i = (KS_{5^(i d)}(sigma(D)), sigma(ct.b) + ...)  i = 1 .. b-1;  baby_0 = ct
+ *   inner_j = sum_i pt_{i + j b} * baby_i                                        (level 1, scale Delta q1)
+ *   partial_j = inner_j (j = 0) or its rotation by j b d (digits of inner_j.a, then the same key switch)
+ *   out = rescale_q1(sum_j partial_j)                                            (level 0, scale Delta)
+ * where KS_g(sigma(D)) = ModDown(sum_i sigma_g(D_i) * ksk_g[i])  (sigma applied to the lifted digits).
+ */
+/* Gadget hybrid key (the slot rotations): each RNS digit d_i is further split into SD = 2 sub-digits of
+ * SW = 15 bits (d_i = lo + 2^15 hi), so the key-switching noise sum_t d_t e_t / P is ~2^15 smaller than with
+ * the plain dnum-2 key -- needed because the baby rotations act on the input at scale Delta = 2^26.
+ *   ksk[t = i SD + h][0][j] = alpha,  ksk[t][1][j] = -alpha s_new + g_{t,j} s_old + e_t,
+ *   g_{t,j} = P Qhat_i 2^(15 h) mod q_j for j == i, else 0.   Layout [t][part][j][n], t < 4. */
+#define SD 2
+#define SW 15
+void or_ksk_gen_gadget(uint64_t seed, uint32_t id, const int32_t* s_old, const int32_t* s_new, uint32_t n,
+                       const uint32_t* m, uint32_t* ksk) {
+  int32_t* e = (int32_t*)malloc(sizeof(int32_t) * n);
+  uint32_t* as = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  for (uint32_t t = 0; t < 2 * SD; ++t) {
+    const uint32_t i = t / SD, h = t % SD;
+    or_sample_cbd(seed, STREAM_KSK_E(id, t), e, n);
+    for (uint32_t j = 0; j < 3; ++j) {
+      const uint32_t q = m[j];
+      uint32_t* alpha = ksk + ((size_t)(t * 2 + 0) * 3 + j) * n;
+      uint32_t* beta = ksk + ((size_t)(t * 2 + 1) * 3 + j) * n;
+      or_sample_uniform(seed, STREAM_KSK_A(id, t, j), q, alpha, n);
+      or_negacyclic_mul(alpha, s_new, n, q, as);
+      uint64_t g = 0;
+      if (j == i) g = mulmod(mulmod(m[2] % q, m[1 - i] % q, q), powmod(2, (uint64_t)SW * h, q), q);
+      for (uint32_t c = 0; c < n; ++c) {
+        uint64_t v = (uint64_t)(q - as[c]) + modq_i64(e[c], q) + mulmod(g, modq_i64(s_old[c], q), q);
+        beta[c] = (uint32_t)(v % q);
+      }
+    }
+  }
+  free(e);
+  free(as);
+}
+void or_rotation_ksk(uint64_t seed, uint32_t r, const int32_t* s, uint32_t N, const uint32_t* m, uint32_t* ksk) {
+  uint64_t g = 1;
+  for (uint32_t t = 0; t < r % (N / 2); ++t) g = g * 5 % (2ull * N);
+  int32_t* ss = (int32_t*)malloc(sizeof(int32_t) * N);
+  for (uint32_t i = 0; i < N; ++i) {
+    uint64_t j = ((uint64_t)i * g) % (2ull * N);
+    if (j < N) ss[j] = s[i];
+    else ss[j - N] = -s[i];
+  }
+  or_ksk_gen_gadget(seed, 0x10000 + r, ss, s, N, m, ksk);
+  free(ss);
+}
+/* gadget digits D [3 mod][t < 4][n] of the a-part c [2 limbs][n]: sub-digits of d_i (< 2^15, so the
+ * same value under every modulus) */
+static void ks_digits(const uint32_t* c, uint32_t n, const uint32_t* m, uint32_t* D) {
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t qi = m[i];
+    const uint64_t inv = powmod(m[1 - i] % qi, qi - 2, qi);
+    for (uint32_t k = 0; k < n; ++k) {
+      const uint32_t dg = (uint32_t)mulmod(c[(size_t)i * n + k], inv, qi);
+      for (int h = 0; h < SD; ++h) {
+        const uint32_t sd = (dg >> (SW * h)) & ((1u << SW) - 1u);
+        for (int j = 0; j < 3; ++j) D[((size_t)j * 2 * SD + i * SD + h) * n + k] = sd % m[j];
+      }
+    }
+  }
+}
+/* (u, w) = ModDown(sum_t sigma_g(D_t) ksk[t])  [2 limbs][n] each */
+static void ks_from_digits(const uint32_t* D, uint32_t n, uint64_t g, const uint32_t* ksk, const uint32_t* m,
+                           uint32_t* u, uint32_t* w) {
+  uint32_t* U = (uint32_t*)calloc((size_t)3 * n, sizeof(uint32_t));
+  uint32_t* W = (uint32_t*)calloc((size_t)3 * n, sizeof(uint32_t));
+  uint32_t* sd = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 2 * SD; ++i) {
+      or_automorphism(D + ((size_t)j * 2 * SD + i) * n, n, (uint32_t)g, m[j], sd);
+      polymul(sd, ksk + ((size_t)(i * 2 + 0) * 3 + j) * n, n, m[j], t);
+      for (uint32_t k = 0; k < n; ++k) U[(size_t)j * n + k] = (uint32_t)(((uint64_t)U[(size_t)j * n + k] + t[k]) % m[j]);
+      polymul(sd, ksk + ((size_t)(i * 2 + 1) * 3 + j) * n, n, m[j], t);
+      for (uint32_t k = 0; k < n; ++k) W[(size_t)j * n + k] = (uint32_t)(((uint64_t)W[(size_t)j * n + k] + t[k]) % m[j]);
+    }
+  ks_moddown(U, W, n, m, u, w);
+  free(U);
+  free(W);
+  free(sd);
+  free(t);
+}
+/* rotate ct [2 limbs][2][n] given the lifted digits of its a-part */
+static void rotate_with_digits(const uint32_t* ct, const uint32_t* D, uint32_t n, uint32_t r, const uint32_t* ksk,
+                               const uint32_t* m, uint32_t* out) {
+  uint64_t g = 1;
+  for (uint32_t t = 0; t < r % (n / 2); ++t) g = g * 5 % (2ull * n);
+  uint32_t* u = (uint32_t*)malloc(sizeof(uint32_t) * 2 * n);
+  uint32_t* w = (uint32_t*)malloc(sizeof(uint32_t) * 2 * n);
+  uint32_t* sb = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  ks_from_digits(D, n, g, ksk, m, u, w);
+  for (int L = 0; L < 2; ++L) {
+    or_automorphism(ct + ((size_t)L * 2 + 1) * n, n, (uint32_t)g, m[L], sb);
+    for (uint32_t k = 0; k < n; ++k) {
+      out[((size_t)L * 2 + 0) * n + k] = u[(size_t)L * n + k];
+      out[((size_t)L * 2 + 1) * n + k] = (uint32_t)(((uint64_t)sb[k] + w[(size_t)L * n + k]) % m[L]);
+    }
+  }
+  free(u);
+  free(w);
+  free(sb);
+}
+/*
+ * ct_in [2][2][N] level 1; pts [d][2 limbs][N] coefficient form mod q_L (block k = i + j b);
+ * keys_baby [b-1][4][2][3][N] (gadget keys) for steps i d, keys_giant [g-1][..] for steps j b d; out [2][N].
+ */
+int or_slot_pcmm(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t g, const uint32_t* ct_in,
+                 const uint32_t* pts, const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out) {
+  if (b * g != d) return 1;
+  const size_t cw = (size_t)4 * N;
+  uint32_t* D = (uint32_t*)malloc(sizeof(uint32_t) * 6 * SD * N);
+  uint32_t* a_in = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+  for (int L = 0; L < 2; ++L) memcpy(a_in + (size_t)L * N, ct_in + ((size_t)L * 2 + 0) * N, sizeof(uint32_t) * N);
+  ks_digits(a_in, N, m, D);
+  uint32_t* baby = (uint32_t*)malloc(sizeof(uint32_t) * cw * b);
+  memcpy(baby, ct_in, sizeof(uint32_t) * cw);
+  for (uint32_t i = 1; i < b; ++i) rotate_with_digits(ct_in, D, N, i * d, keys_baby + (size_t)(i - 1) * 24 * N, m, baby + i * cw);
+  uint32_t* acc = (uint32_t*)calloc(cw, sizeof(uint32_t));
+  uint32_t* inner = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  uint32_t* rot = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  for (uint32_t j = 0; j < g; ++j) {
+    memset(inner, 0, sizeof(uint32_t) * cw);
+    for (uint32_t i = 0; i < b; ++i)
+      for (int L = 0; L < 2; ++L)
+        for (int ab = 0; ab < 2; ++ab) {
+          polymul(baby + i * cw + ((size_t)L * 2 + ab) * N, pts + ((size_t)(i + j * b) * 2 + L) * N, N, m[L], t);
+          uint32_t* dst = inner + ((size_t)L * 2 + ab) * N;
+          for (uint32_t k = 0; k < N; ++k) dst[k] = (uint32_t)(((uint64_t)dst[k] + t[k]) % m[L]);
+        }
+    const uint32_t* part = inner;
+    if (j > 0) {
+      for (int L = 0; L < 2; ++L) memcpy(a_in + (size_t)L * N, inner + ((size_t)L * 2 + 0) * N, sizeof(uint32_t) * N);
+      ks_digits(a_in, N, m, D);
+      rotate_with_digits(inner, D, N, j * b * d, keys_giant + (size_t)(j - 1) * 24 * N, m, rot);
+      part = rot;
+    }
+    for (int L = 0; L < 2; ++L)
+      for (size_t k = 0; k < (size_t)2 * N; ++k) {
+        const size_t x = (size_t)L * 2 * N + k;
+        acc[x] = (uint32_t)(((uint64_t)acc[x] + part[x]) % m[L]);
+      }
+  }
+  const uint32_t q0 = m[0], q1 = m[1];
+  const uint64_t q1inv = powmod(q1 % q0, q0 - 2, q0);
+  for (int ab = 0; ab < 2; ++ab)
+    for (uint32_t k = 0; k < N; ++k) {
+      const uint32_t x0 = acc[(size_t)ab * N + k], x1 = acc[((size_t)2 + ab) * N + k];
+      const int64_t x1c = x1 > q1 / 2 ? (int64_t)x1 - q1 : (int64_t)x1;
+      out[(size_t)ab * N + k] = (uint32_t)mulmod(modq_i64((int64_t)x0 - x1c, q0), q1inv, q0);
+    }
+  free(D);
+  free(a_in);
+  free(baby);
+  free(acc);
+  free(inner);
+  free(rot);
+  free(t);
+  return 0;
+}

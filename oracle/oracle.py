@@ -18,7 +18,7 @@ __all__ = [
     "py_mlwe_components", "py_pcmm_rows", "num_threads", "time_pcmm_sample", "rng",
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
     "decode_vector", "rhombus_pcmv", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
-    "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe",
+    "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe", "rotation_keys", "slot_pcmm",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -559,4 +559,45 @@ def mlwe_to_rlwe(params, raw_b: np.ndarray, raw_a: np.ndarray, ksk: np.ndarray) 
                                     _u32(np.ascontiguousarray(ksk, dtype=np.uint32)), _u32(out))
     if rc:
         raise ValueError("mlwe_to_rlwe: bad shape")
+    return out
+
+
+# ---------------------------------------------------------------- slot-domain BSGS PCMM (§8f3)
+def _sd_bind():
+    L = _rh_lib()
+    if not getattr(L, "_sd_bound", False):
+        u32p, i32p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32)
+        u32, u64 = ctypes.c_uint32, ctypes.c_uint64
+        L.or_rotation_ksk.restype = None
+        L.or_rotation_ksk.argtypes = [u64, u32, i32p, u32, u32p, u32p]
+        L.or_slot_pcmm.restype = ctypes.c_int
+        L.or_slot_pcmm.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
+        L._sd_bound = True
+    return L
+
+
+def rotation_keys(params, seed: int, s: np.ndarray, steps) -> np.ndarray:
+    """Gadget keys sigma_{5^r}(s) -> s for each step r -> [len(steps), 4, 2, 3, N] (coefficient form)."""
+    N = params.N
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    out = np.zeros((len(steps), 4, 2, 3, N), np.uint32)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    for t, r in enumerate(steps):
+        g = np.zeros((4, 2, 3, N), np.uint32)
+        _sd_bind().or_rotation_ksk(seed, int(r) % (N // 2), _i32(s), N, _u32(m), _u32(g))
+        out[t] = g
+    return out
+
+
+def slot_pcmm(params, ct_in: np.ndarray, pts: np.ndarray, d: int, b: int, g: int, keys_baby, keys_giant) -> np.ndarray:
+    """or_slot_pcmm: ct_in [2, 2, N] level 1, pts [d, 2, N] residues (coefficient form) -> [2, N] level 0."""
+    N = params.N
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    out = np.zeros((2, N), np.uint32)
+    kb = np.ascontiguousarray(keys_baby if len(keys_baby) else np.zeros((1, 4, 2, 3, N), np.uint32), dtype=np.uint32)
+    kg = np.ascontiguousarray(keys_giant if len(keys_giant) else np.zeros((1, 4, 2, 3, N), np.uint32), dtype=np.uint32)
+    rc = _sd_bind().or_slot_pcmm(N, _u32(m), d, b, g, _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
+                                 _u32(np.ascontiguousarray(pts, dtype=np.uint32)), _u32(kb), _u32(kg), _u32(out))
+    if rc:
+        raise ValueError("slot_pcmm: split does not cover d")
     return out

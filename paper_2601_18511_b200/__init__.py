@@ -13,6 +13,8 @@ from .pcmm import (MlwePcmmPlan, clear_pcmm, load_mlwe_pcmm_plan, load_plan_bund
                    pcmm_mlwe_into_peers, pcmm_mlwe_to_host, save_mlwe_pcmm_plan, save_plan_bundle)
 from .rhombus import (CtVector, RhombusKeys, RhombusPlan, clear_pcmv, decrypt_vector, encrypt_vector,
                       make_rhombus_plan, pcmv_rhombus, rhombus_keygen)
+from .slotpcmm import (BsgsSplit, PackedCt, SlotPcmmKeys, SlotPcmmPlan, clear_slot_pcmm, decrypt_packed,
+                       encrypt_packed, make_slot_pcmm_plan, pcmm_slot_bsgs, slot_pcmm_keygen)
 from .ringpack import (RingPackKeys, RingPackPlan, make_ring_pack_plan, pcmm_level1, pcmm_packed, ring_pack,
                        ring_pack_keygen)
 
@@ -25,6 +27,8 @@ __all__ = [
     "make_rhombus_plan", "pcmv_rhombus", "rhombus_keygen",
     "RingPackKeys", "RingPackPlan", "make_ring_pack_plan", "pcmm_level1", "pcmm_packed", "ring_pack",
     "ring_pack_keygen",
+    "BsgsSplit", "PackedCt", "SlotPcmmKeys", "SlotPcmmPlan", "clear_slot_pcmm", "decrypt_packed", "encrypt_packed",
+    "make_slot_pcmm_plan", "pcmm_slot_bsgs", "slot_pcmm_keygen",
 ]
 
 __version__ = "0.1.0"

@@ -228,6 +228,25 @@ extern "C" he_status he_encrypt_vector(const he_context* c, const uint32_t* s_nt
   return HE_OK;
 }
 
+extern "C" he_status he_encrypt_poly(const he_context* c, const uint32_t* s_ntt_dev, const int64_t* pt_dev,
+                                     uint32_t n_ct, uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream) {
+  if (!c || !s_ntt_dev || !pt_dev || !ct_dev) return fail(HE_EINVAL, "null argument");
+  if (n_ct == 0) return fail(HE_EINVAL, "no plaintexts");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N;
+  HE_CUDA(launch_gen_a(c->R, seed, r0, n_ct, ct_dev, st), "sample a");
+  for (uint32_t L = 0; L < 2; ++L) {
+    uint32_t* bslots = ct_dev + (size_t)L * 2 * N + N;
+    HE_CUDA(ntt_forward(c->ntt[L], bslots, n_ct, 4ull * N, st), "NTT(a)");
+    HE_CUDA(launch_pointwise_mul(bslots, 4ull * N, s_ntt_dev + (size_t)L * N, N, n_ct, c->R.q[L], bslots, 4ull * N, st),
+            "a^ * s^");
+    HE_CUDA(ntt_inverse(c->ntt[L], bslots, n_ct, 4ull * N, st), "INTT(a s)");
+  }
+  HE_CUDA(launch_finish_encrypt(c->R, reinterpret_cast<const double*>(pt_dev), N, seed, r0, n_ct, ct_dev, st, 2),
+          "finish encrypt");
+  return HE_OK;
+}
+
 extern "C" he_status he_decrypt_rlwe(const he_context* c, const uint32_t* s_ntt_dev, const uint32_t* ct_dev,
                                      uint32_t n_ct, uint32_t limbs, uint32_t limb, int64_t* phase_dev, void* stream) {
   if (!c || !s_ntt_dev || !ct_dev || !phase_dev) return fail(HE_EINVAL, "null argument");

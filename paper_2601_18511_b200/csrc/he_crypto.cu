@@ -289,6 +289,8 @@ __global__ void finish_encrypt_kernel(const double* __restrict__ acts, uint32_t 
         const double v = acts[(size_t)bitrev_h(m, lh) * n_in + (size_t)k * r + sigma_h(t, logk)];
         pt = __double2ll_rn(__dmul_rn(delta, v));
       }
+    } else if (layout == 2) {  // raw integer plaintext polynomials int64 [n_ct][N] (slot encodings)
+      pt = reinterpret_cast<const long long*>(acts)[(size_t)r * N + c];
     } else {
       const uint32_t rho = N / n_rh, p = c % rho, kk = c / rho;
       const uint32_t hk = (kk & (n_rh >> 1)) | bitrev_h(kk & ((n_rh >> 1) - 1), lrh - 1);

@@ -1109,3 +1109,324 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
   }
   return HE_OK;
 }
+
+// ======================================================================== slot-domain BSGS PCMM (§8f3)
+// hesim pcmm_bsgs (matmul.py:165-176) on real CKKS ciphertexts at degree N; restated from
+// oracle/he_oracle_rhombus.c (or_slot_pcmm), bit-exact.  Ciphertexts live in the NTT domain between
+// steps; a left slot rotation by r is X -> X^(5^r) (an index permutation of NTT values) plus a
+// hybrid key switch of the lifted digits (hoisted: the digits of the input are formed and
+// transformed once for all b - 1 baby rotations).
+namespace {
+
+// Gadget key switching for the slot rotations (oracle or_ksk_gen_gadget): each RNS digit d_i is split
+// into kSdSub = 2 sub-digits of kSdBits = 15 bits, so the key-switching noise is ~2^15 below the plain
+// dnum-2 key's -- the baby rotations act on the input at scale Delta = 2^26.  Sub-digits are < 2^15,
+// i.e. the same value under every modulus: D [mod][t = i kSdSub + h][N] (coefficient form).
+constexpr int kSdSub = 2;
+constexpr int kSdBits = 15;
+constexpr int kSdT = 2 * kSdSub;   // digit polys per modulus
+__global__ void k_sd_digits(const uint32_t* __restrict__ a, uint64_t ls, uint32_t N, Mods M, uint32_t qh0,
+                            uint32_t qh0p, uint32_t qh1, uint32_t qh1p, uint32_t* __restrict__ D) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
+    const uint32_t dg[2] = {shoup_mul(a[x], qh0, qh0p, M.m[0]), shoup_mul(a[ls + x], qh1, qh1p, M.m[1])};
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int h = 0; h < kSdSub; ++h) {
+        const uint32_t v = (dg[i] >> (kSdBits * h)) & ((1u << kSdBits) - 1u);
+#pragma unroll
+        for (int mod = 0; mod < 3; ++mod) D[(size_t)(mod * kSdT + i * kSdSub + h) * N + x] = v;
+      }
+  }
+}
+// UW [mod][part][N] = sum_t D^[mod][t][perm c] K[t][part][mod][c]   (sigma applied to the digits)
+__global__ void k_sd_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict__ perm,
+                         const uint32_t* __restrict__ K, uint32_t N, Mods M, uint32_t* __restrict__ UW) {
+  const uint32_t mod = blockIdx.y;
+  const uint32_t q = mod == 0 ? M.m[0] : (mod == 1 ? M.m[1] : M.m[2]);
+  const uint64_t mu = mod == 0 ? M.mu[0] : (mod == 1 ? M.mu[1] : M.mu[2]);
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+    const uint32_t pc = perm[c];
+    uint64_t u = 0, w = 0;   // 4 products < 2^60 each
+#pragma unroll
+    for (int t = 0; t < kSdT; ++t) {
+      const uint64_t dv = D[(size_t)(mod * kSdT + t) * N + pc];
+      u += dv * K[(size_t)((t * 2 + 0) * 3 + mod) * N + c];
+      w += dv * K[(size_t)((t * 2 + 1) * 3 + mod) * N + c];
+    }
+    UW[(size_t)(mod * 2 + 0) * N + c] = barrett64(u, mu, q);
+    UW[(size_t)(mod * 2 + 1) * N + c] = barrett64(w, mu, q);
+  }
+}
+// rotated ct (NTT domain) [L][ab][N]: a = (U - LB_u) P^-1, b = sigma(b^) + (W - LB_w) P^-1
+__global__ void k_sd_combine(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ LB,
+                             const uint32_t* __restrict__ bh, uint64_t bls, const uint32_t* __restrict__ perm,
+                             uint32_t N, Mods M, uint32_t pinv0, uint32_t pinv1, uint32_t* __restrict__ out) {
+  const uint32_t L = blockIdx.y, q = M.m[L], pinv = L ? pinv1 : pinv0;
+  const uint64_t mu = M.mu[L];
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+    const uint32_t u = mulmod_b(sub_mod(UW[(size_t)(L * 2 + 0) * N + c], LB[(size_t)(L * 2 + 0) * N + c], q), pinv, mu, q);
+    const uint32_t w = mulmod_b(sub_mod(UW[(size_t)(L * 2 + 1) * N + c], LB[(size_t)(L * 2 + 1) * N + c], q), pinv, mu, q);
+    out[(size_t)(L * 2 + 0) * N + c] = u;
+    out[(size_t)(L * 2 + 1) * N + c] = add_mod(bh[L * bls + perm[c]], w, q);
+  }
+}
+// inner [L][ab][N] = sum_{i < b} pt[i + j b][L] * baby[i][L][ab]   (NTT domain)
+__global__ void k_sd_inner(const uint32_t* __restrict__ baby, const uint32_t* __restrict__ pts, uint32_t b, uint32_t j,
+                           uint32_t N, Mods M, uint32_t* __restrict__ inner) {
+  const uint32_t L = blockIdx.y, q = M.m[L];
+  const uint64_t mu = M.mu[L];
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+    uint64_t aa = 0, ab = 0;
+    for (uint32_t i = 0; i < b; ++i) {
+      const uint64_t p = pts[((size_t)(i + j * b) * 2 + L) * N + c];
+      const uint32_t* bi = baby + ((size_t)i * 4 + L * 2) * N + c;
+      aa = barrett64(aa + p * bi[0], mu, q);
+      ab = barrett64(ab + p * bi[N], mu, q);
+    }
+    inner[(size_t)(L * 2 + 0) * N + c] = (uint32_t)aa;
+    inner[(size_t)(L * 2 + 1) * N + c] = (uint32_t)ab;
+  }
+}
+__global__ void k_sd_accumulate(uint32_t* __restrict__ acc, const uint32_t* __restrict__ part, uint32_t N, Mods M) {
+  const uint32_t L = blockIdx.y, q = M.m[L];
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 2 * N; x += gridDim.x * blockDim.x)
+    acc[(size_t)L * 2 * N + x] = add_mod(acc[(size_t)L * 2 * N + x], part[(size_t)L * 2 * N + x], q);
+}
+// signed int64 plaintext polys [count][N] -> [count][2 limbs][N] residues (NTT'd afterwards)
+__global__ void k_sd_reduce_pts(const int64_t* __restrict__ pt, uint64_t total, uint32_t logN, Mods M,
+                                uint32_t* __restrict__ out) {
+  const uint32_t N = 1u << logN;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = x >> logN;
+    const uint32_t c = (uint32_t)(x & (N - 1));
+    const int64_t v = pt[x];
+#pragma unroll
+    for (int L = 0; L < 2; ++L) {
+      const int64_t r = v % (int64_t)M.m[L];
+      out[(k * 2 + L) * N + c] = (uint32_t)(r < 0 ? r + M.m[L] : r);
+    }
+  }
+}
+
+}  // namespace
+
+struct he_slot_pcmm_plan {
+  const he_context* ctx;
+  uint32_t d, b, g, N, logN;
+  const uint32_t* pts;   // caller-owned [d][2][N] NTT domain
+  uint32_t* perms;       // owned [b - 1 + g - 1][N]
+  Mods M;
+  uint32_t qhinv[2], qhinvp[2], pinv[2], q1inv, q1invp;
+};
+
+// gadget key (layout [t][part][mod][deg], t = i kSdSub + h), NTT domain; streams use t as the digit index
+static he_status make_ksk_gadget_dev(const Mods& M, uint64_t seed, uint32_t id, const int32_t* s_old,
+                                     const int32_t* s_new, uint32_t deg, const NttTable* tabs, uint32_t* ksk,
+                                     cudaStream_t st) {
+  uint32_t* snew = nullptr;
+  HE_CUDA(cudaMallocAsync(&snew, 3ull * deg * sizeof(uint32_t), st), "alloc");
+  for (int j = 0; j < 3; ++j) {
+    k_reduce_signed<<<grid_for(deg), 256, 0, st>>>(s_new, deg, M.m[j], snew + (size_t)j * deg);
+    HE_CUDA(ntt_forward(tabs[j], snew + (size_t)j * deg, 1, deg, st), "NTT(s_new)");
+  }
+  for (uint32_t t = 0; t < (uint32_t)kSdT; ++t) {
+    const uint32_t i = t / kSdSub, h = t % kSdSub;
+    for (uint32_t j = 0; j < 3; ++j) {
+      const uint32_t q = M.m[j];
+      uint32_t g = 0;
+      if (j == i)
+        g = (uint32_t)((uint64_t)((uint64_t)(M.m[2] % q) * (M.m[1 - i] % q) % q) * powmod_h(2, (uint64_t)kSdBits * h, q) % q);
+      uint32_t* alpha = ksk + ((size_t)(t * 2 + 0) * 3 + j) * deg;
+      uint32_t* beta = ksk + ((size_t)(t * 2 + 1) * 3 + j) * deg;
+      k_ksk_prep<<<grid_for(deg), 256, 0, st>>>(seed, id, t, j, q, g, s_old, deg, alpha, beta);
+      HE_CUDA(ntt_forward(tabs[j], alpha, 1, deg, st), "NTT(alpha)");
+      HE_CUDA(ntt_forward(tabs[j], beta, 1, deg, st), "NTT(t)");
+      k_ksk_beta<<<grid_for(deg), 256, 0, st>>>(alpha, snew + (size_t)j * deg, deg, q, beta);
+    }
+  }
+  cudaFreeAsync(snew, st);
+  return HE_OK;
+}
+
+extern "C" he_status he_slot_rotation_keygen(const he_context* c, uint64_t seed, const int32_t* s_dev,
+                                             const int32_t* steps, uint32_t n_steps, uint32_t* keys_dev,
+                                             void* stream) {
+  if (!c || !s_dev || !steps || (!keys_dev && n_steps)) return fail(HE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N;
+  const Mods M = make_mods(c->R);
+  int32_t* sk = nullptr;
+  HE_CUDA(cudaMallocAsync(&sk, N * sizeof(int32_t), st), "alloc");
+  he_status s = HE_OK;
+  for (uint32_t t = 0; t < n_steps && !s; ++t) {
+    const uint32_t r = (uint32_t)(((int64_t)steps[t] % (N / 2) + N / 2) % (N / 2));
+    const uint32_t g = (uint32_t)powmod_h(5, r, 2ull * N);
+    k_secret_auto<<<grid_for(N), 256, 0, st>>>(s_dev, N, g, sk);
+    s = make_ksk_gadget_dev(M, seed, 0x10000 + r, sk, s_dev, N, c->ntt, keys_dev + (size_t)t * 24 * N, st);
+  }
+  cudaFreeAsync(sk, st);
+  if (s) return s;
+  return cudaGetLastError() == cudaSuccess ? HE_OK : fail(HE_ECUDA, "rotation keygen launch failed");
+}
+
+extern "C" he_status he_slot_pcmm_encode_pts(const he_context* c, const int64_t* pt_dev, uint32_t count,
+                                             uint32_t* pts_ntt_dev, void* stream) {
+  if (!c || !pt_dev || !pts_ntt_dev) return fail(HE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N;
+  const Mods M = make_mods(c->R);
+  k_sd_reduce_pts<<<grid_for((uint64_t)count * N), 256, 0, st>>>(pt_dev, (uint64_t)count * N, (uint32_t)ilog2_u(N), M,
+                                                                   pts_ntt_dev);
+  for (int L = 0; L < 2; ++L)
+    HE_CUDA(ntt_forward(c->ntt[L], pts_ntt_dev + (size_t)L * N, count, 2ull * N, st), "NTT(pt)");
+  return HE_OK;
+}
+
+extern "C" he_status he_slot_pcmm_plan_create(const he_context* c, const uint32_t* pts_ntt_dev, uint32_t d, uint32_t b,
+                                              uint32_t g, he_slot_pcmm_plan** out) {
+  if (!c || !pts_ntt_dev || !out) return fail(HE_EINVAL, "null argument");
+  if (d == 0 || b == 0 || g == 0 || b * g != d) return fail(HE_EINVAL, "split %ux%u does not cover dim %u", b, g, d);
+  const uint32_t N = c->R.N;
+  if ((uint64_t)d * d > N / 2) return fail(HE_EINVAL, "%ux%u does not fit in %u slots", d, d, N / 2);
+  he_slot_pcmm_plan* p = new (std::nothrow) he_slot_pcmm_plan();
+  if (!p) return fail(HE_ENOMEM, "out of host memory");
+  p->ctx = c;
+  p->d = d;
+  p->b = b;
+  p->g = g;
+  p->N = N;
+  p->logN = (uint32_t)ilog2_u(N);
+  p->pts = pts_ntt_dev;
+  p->M = make_mods(c->R);
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t qi = p->M.m[i];
+    p->qhinv[i] = (uint32_t)powmod_h(p->M.m[1 - i] % qi, qi - 2, qi);
+    p->qhinvp[i] = shoup_pre(p->qhinv[i], qi);
+    p->pinv[i] = (uint32_t)powmod_h(p->M.m[2] % qi, qi - 2, qi);
+  }
+  p->q1inv = (uint32_t)powmod_h(p->M.m[1] % p->M.m[0], p->M.m[0] - 2, p->M.m[0]);
+  p->q1invp = shoup_pre(p->q1inv, p->M.m[0]);
+  const uint32_t nrot = (b - 1) + (g - 1);
+  std::vector<uint32_t> h((size_t)(nrot ? nrot : 1) * N);
+  for (uint32_t t = 0; t < nrot; ++t) {
+    const uint64_t r = t < b - 1 ? (uint64_t)(t + 1) * d : (uint64_t)(t - (b - 1) + 1) * b * d;
+    const uint64_t gal = powmod_h(5, r % (N / 2), 2ull * N);
+    for (uint32_t cc = 0; cc < N; ++cc) {
+      const uint64_t e = 2ull * bitrev_h(cc, (int)p->logN) + 1;
+      h[(size_t)t * N + cc] = bitrev_h((uint32_t)(((e * gal) % (2ull * N) - 1) / 2), (int)p->logN);
+    }
+  }
+  if (cudaMalloc(&p->perms, h.size() * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemcpy(p->perms, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+    delete p;
+    return fail(HE_ECUDA, "slot pcmm tables");
+  }
+  *out = p;
+  return HE_OK;
+}
+
+extern "C" he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* p) {
+  if (p) {
+    if (p->perms) cudaFree(p->perms);
+    delete p;
+  }
+  return HE_OK;
+}
+
+struct SdWs {
+  uint32_t *D, *X, *baby, *inner, *rot, *acc, *UW, *LB;
+};
+static uint64_t sd_ws_words(const he_slot_pcmm_plan* p, SdWs* w, uint32_t* base) {
+  const uint64_t N = p->N;
+  uint64_t off = 0;
+  auto take = [&](uint32_t*& ptr, uint64_t words) {
+    if (w) ptr = base + off;
+    off += (words + 63) & ~63ull;
+  };
+  SdWs dummy;
+  SdWs& r = w ? *w : dummy;
+  take(r.D, 3ull * kSdT * N);
+  take(r.X, 4 * N);
+  take(r.baby, 4ull * p->b * N);
+  take(r.inner, 4 * N);
+  take(r.rot, 4 * N);
+  take(r.acc, 4 * N);
+  take(r.UW, 6 * N);
+  take(r.LB, 4 * N);
+  return off;
+}
+
+extern "C" he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* p, uint64_t* bytes) {
+  if (!p || !bytes) return fail(HE_EINVAL, "null argument");
+  *bytes = sd_ws_words(p, nullptr, nullptr) * sizeof(uint32_t);
+  return HE_OK;
+}
+
+extern "C" he_status he_slot_pcmm_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint32_t level,
+                                      const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out, void* ws_dev,
+                                      uint64_t ws_bytes, void* stream, he_ledger* ledger) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmm needs one level");
+  if (level != 1) return fail(HE_EINVAL, "the slot-domain PCMM runs at level 1 (got %u)", level);
+  if (!ct_in || !out || !ws_dev || (p->b > 1 && !keys_baby) || (p->g > 1 && !keys_giant))
+    return fail(HE_EINVAL, "null argument");
+  if (ws_bytes < sd_ws_words(p, nullptr, nullptr) * sizeof(uint32_t)) return fail(HE_EINVAL, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const he_context* c = p->ctx;
+  const uint32_t N = p->N;
+  SdWs w;
+  sd_ws_words(p, &w, (uint32_t*)ws_dev);
+  const dim3 g1 = grid_for(N);
+  dim3 g2 = g1, g3 = g1;
+  g2.y = 2;
+  g3.y = 3;
+  // rotation of the ciphertext whose lifted digits D^ (NTT) and b^ (NTT, limb stride 2N) are given
+  auto rotate = [&](const uint32_t* bh, uint32_t t, const uint32_t* key, uint32_t* dst) -> he_status {
+    const uint32_t* perm = p->perms + (size_t)t * N;
+    k_sd_mac<<<g3, 256, 0, st>>>(w.D, perm, key, N, p->M, w.UW);
+    HE_CUDA(ntt_inverse(c->ntt[2], w.UW + 4ull * N, 2, N, st), "INTT(U_P, W_P)");
+    k_moddown_lift<<<grid_for(2ull * N), 256, 0, st>>>(w.UW + 4ull * N, N, p->M, w.LB);
+    HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2, N, st), "NTT(lift q0)");
+    HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2ull * N, 2, N, st), "NTT(lift q1)");
+    k_sd_combine<<<g2, 256, 0, st>>>(w.UW, w.LB, bh, 2ull * N, perm, N, p->M, p->pinv[0], p->pinv[1], dst);
+    return HE_OK;
+  };
+  auto digits = [&](const uint32_t* a_coeff) -> he_status {
+    k_sd_digits<<<g1, 256, 0, st>>>(a_coeff, 2ull * N, N, p->M, p->qhinv[0], p->qhinvp[0], p->qhinv[1], p->qhinvp[1],
+                                    w.D);
+    for (int mod = 0; mod < 3; ++mod)
+      HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * kSdT * N, kSdT, N, st), "NTT(D)");
+    return HE_OK;
+  };
+  // baby steps (hoisted: one digit decomposition of the input)
+  he_status s = digits(ct_in);
+  if (s) return s;
+  HE_CUDA(cudaMemcpyAsync(w.X, ct_in, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
+  for (int L = 0; L < 2; ++L) HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
+  HE_CUDA(cudaMemcpyAsync(w.baby, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
+  for (uint32_t i = 1; i < p->b; ++i) {
+    s = rotate(w.X + N, i - 1, keys_baby + (size_t)(i - 1) * 24 * N, w.baby + (size_t)i * 4 * N);
+    if (s) return s;
+  }
+  // giant groups
+  for (uint32_t j = 0; j < p->g; ++j) {
+    k_sd_inner<<<g2, 256, 0, st>>>(w.baby, p->pts, p->b, j, N, p->M, j == 0 ? w.acc : w.inner);
+    if (j == 0) continue;
+    for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt[L], w.inner + (size_t)L * 2 * N, 1, N, st), "INTT(inner a)");
+    s = digits(w.inner);
+    if (s) return s;
+    s = rotate(w.inner + N, (p->b - 1) + (j - 1), keys_giant + (size_t)(j - 1) * 24 * N, w.rot);
+    if (s) return s;
+    k_sd_accumulate<<<g2, 256, 0, st>>>(w.acc, w.rot, N, p->M);
+  }
+  for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt[L], w.acc + (size_t)L * 2 * N, 2, N, st), "INTT(acc)");
+  k_rh_combine<<<grid_for(2ull * N), 256, 0, st>>>(w.acc, 1, N, p->M.m[0], p->M.m[1], p->q1inv, p->q1invp, out);
+  HE_CUDA(cudaGetLastError(), "slot pcmm launch");
+  if (ledger) {
+    ledger->ct_rotations += (int64_t)(p->b - 1) + (p->g - 1);
+    ledger->pc_mults += p->d;
+    ledger->rescales += 1;
+  }
+  return HE_OK;
+}

@@ -31,6 +31,8 @@ EXPORTS = (
     "he_pcmm_profile", "he_pcmm_profile_read", "he_pcmm_spectral_info", "he_pcmm_gemm_rows_peers",
     "he_pcmm_run_level1", "he_ring_pack_key_bytes", "he_ring_pack_keygen", "he_ring_pack_plan_create", "he_ring_pack_plan_destroy",
     "he_ring_pack_workspace_bytes", "he_ring_pack_run", "he_rhombus_run_shard", "he_rhombus_combine",
+    "he_encrypt_poly", "he_slot_rotation_keygen", "he_slot_pcmm_encode_pts", "he_slot_pcmm_plan_create",
+    "he_slot_pcmm_plan_destroy", "he_slot_pcmm_workspace_bytes", "he_slot_pcmm_run",
 )
 
 
@@ -102,6 +104,13 @@ def lib():
             "he_pcmm_run_level1": (st, [vp, vp, u32, vp, vp, vp, u64, vp]),
             "he_rhombus_run_shard": (st, [vp, vp, u32, vp, vp, u32, u32, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_rhombus_combine": (st, [vp, vp, u32, vp, vp, ctypes.POINTER(HeLedgerC)]),
+            "he_encrypt_poly": (st, [vp, vp, vp, u32, u64, u32, vp, vp]),
+            "he_slot_rotation_keygen": (st, [vp, u64, vp, vp, u32, vp, vp]),
+            "he_slot_pcmm_encode_pts": (st, [vp, vp, u32, vp, vp]),
+            "he_slot_pcmm_plan_create": (st, [vp, vp, u32, u32, u32, ctypes.POINTER(vp)]),
+            "he_slot_pcmm_plan_destroy": (st, [vp]),
+            "he_slot_pcmm_workspace_bytes": (st, [vp, ctypes.POINTER(u64)]),
+            "he_slot_pcmm_run": (st, [vp, vp, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_ring_pack_key_bytes": (st, [vp, i32, ctypes.POINTER(u64)]),
             "he_ring_pack_keygen": (st, [vp, i32, u64, vp, vp, vp]),
             "he_ring_pack_plan_create": (st, [vp, u32, i32, ctypes.POINTER(vp)]),

@@ -1,0 +1,242 @@
+"""Slot-domain τ-PCMM on the GPU: hesim's own PCMM (pcmm_bsgs, matmul.py:165-176) on real CKKS
+ciphertexts (the kernel behind PC-attention).
+
+Same operator API and semantics as the reference:
+  make_slot_pcmm_plan(ctx, W, shear_power=0, split=None)   ~ make_pcmm_plan (matmul.py:77-100)
+  pcmm_slot_bsgs(ctx, plan, keys, B)                       ~ pcmm_bsgs      (matmul.py:165-176)
+  encrypt_packed(ctx, sk, M, shear_power, seed)            ~ pack_sheared   (packing.py:81-91)
+A d x d matrix lives row-major in d^2 slots, tiled across the N/2 CKKS slots; the plan's weight
+blocks are col_shear(shift_rows(W), l) rolled per (k, jb) exactly as _block_clear (matmul.py:103-105),
+CKKS-encoded at scale Delta_w = q1 (slots.py); the op spends (b - 1) + (g - 1) rotations, d
+plaintext products and one rescale, like the reference's ledger.  The error contract is the
+reference's (_check_operand, matmul.py:139-149), raised before any launch.
+
+Device pipeline (he_slot_pcmm_run, he_rhombus.cu): hoisted baby rotations (one digit decomposition
+of the input, X -> X^(5^(i d)) as NTT-index permutations of the digits, one hybrid key switch each),
+per giant group a fused NTT-domain multiply-accumulate, the giant rotation at level 1, one rescale.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import native, slots
+from .context import HeContext, SecretKey, _torch, require_level
+from .errors import NeedsBootstrapError
+
+
+# ---- cleartext permutations (restated from hesim packing.py:95-130)
+def shift_rows(m: np.ndarray) -> np.ndarray:
+    d = m.shape[0]
+    i, j = np.indices((d, d))
+    return m[i, (i + j) % d]
+
+
+def shift_cols(m: np.ndarray) -> np.ndarray:
+    d = m.shape[0]
+    i, j = np.indices((d, d))
+    return m[(i + j) % d, j]
+
+
+def col_shear(m: np.ndarray, power: int) -> np.ndarray:
+    """M[(i + l j) % d, j]  (shift_cols iterated l times)."""
+    d = m.shape[0]
+    i, j = np.indices((d, d))
+    return np.asarray(m)[(i + power * j) % d, j]
+
+
+def clear_slot_pcmm(A, B, shear_power: int) -> np.ndarray:
+    """What the kernel decodes to: col_shear(A @ B, l) (hesim clear_pcmm, matmul.py:179-181)."""
+    return col_shear(np.asarray(A, float) @ np.asarray(B, float), shear_power)
+
+
+@dataclass(frozen=True)
+class BsgsSplit:
+    baby: int
+    giant: int
+
+    def __post_init__(self):
+        if self.baby < 1 or self.giant < 1:
+            raise ValueError("split factors must be positive")
+
+
+def default_split(d: int) -> BsgsSplit:
+    """b = g = sqrt(d) when square, else the smallest divisor >= sqrt(d) (matmul.py:49-55)."""
+    r = math.isqrt(d)
+    if r * r == d:
+        return BsgsSplit(r, d // r)
+    b = next(b for b in range(r + 1, d + 1) if d % b == 0)
+    return BsgsSplit(b, d // b)
+
+
+@dataclass
+class PackedCt:
+    """A d x d matrix in the slots of one RLWE ciphertext (hesim PackedMatrix with a ciphertext
+    payload).  data: int32 view of u32 [limbs, 2 (a, b), N]."""
+
+    data: object
+    level: int
+    dim: int
+    shear_power: int = 0
+
+    @property
+    def is_ct(self) -> bool:
+        return True
+
+
+@dataclass
+class SlotPcmmKeys:
+    baby: object       # [b - 1, 4, 2, 3, N] gadget rotation keys for steps i d
+    giant: object      # [g - 1, 4, 2, 3, N] gadget rotation keys for steps j b d
+    steps: tuple = ()
+
+
+@dataclass
+class SlotPcmmPlan:
+    dim: int
+    shear_power: int
+    split: BsgsSplit
+    base_clear: np.ndarray
+    pts: object = None                  # u32 [d, 2, N] NTT domain (block k = i + j b)
+    _handle: object = field(default=None, repr=False)
+    _workspace: object = field(default=None, repr=False)
+
+    def workspace(self, device):
+        torch = _torch()
+        n = ctypes.c_uint64()
+        native.call("he_slot_pcmm_workspace_bytes", self._handle, ctypes.byref(n))
+        if self._workspace is None or self._workspace.numel() * 4 < n.value:
+            self._workspace = torch.empty((n.value + 3) // 4, dtype=torch.int32, device=device)
+        return self._workspace
+
+    def __del__(self):
+        try:
+            if self._handle:
+                native.lib().he_slot_pcmm_plan_destroy(self._handle)
+        except Exception:
+            pass
+
+
+def block_clear(plan: SlotPcmmPlan, k: int, jb: int) -> np.ndarray:
+    """matmul.py:103-105: roll(roll(base, -k, axis=1), -r, axis=0), r = -l k - jb."""
+    r = -plan.shear_power * k - jb
+    return np.roll(np.roll(plan.base_clear, -k, axis=1), -r, axis=0)
+
+
+def plan_blocks(plan: SlotPcmmPlan) -> list:
+    """The d weight blocks in kernel order k = i + j b (block (i, j) = _block_clear(i + j b, j b))."""
+    b, g = plan.split.baby, plan.split.giant
+    return [block_clear(plan, i + j * b, j * b) for j in range(g) for i in range(b)]
+
+
+def encode_blocks(params, plan: SlotPcmmPlan) -> np.ndarray:
+    """int64 [d, N]: each block flattened row-major, tiled, CKKS-encoded at scale q1."""
+    return np.stack([slots.encode(blk.reshape(-1), params.N, float(params.delta_w)) for blk in plan_blocks(plan)])
+
+
+def make_slot_pcmm_plan(ctx: HeContext, weights, shear_power: int = 0, split: BsgsSplit | None = None) -> SlotPcmmPlan:
+    torch = _torch()
+    w = np.asarray(weights, dtype=float)
+    d = w.shape[0]
+    if w.ndim != 2 or w.shape != (d, d):
+        raise ValueError("weights must be square")
+    if shear_power < 0:
+        raise ValueError("shear_power must be non-negative")
+    if split is None:
+        split = default_split(d)
+    if split.baby * split.giant != d:
+        raise ValueError(f"split {split.baby}x{split.giant} does not cover dim {d}")
+    if d * d > ctx.params.N // 2 or (ctx.params.N // 2) % (d * d):
+        raise ValueError(f"{d}x{d} does not tile the {ctx.params.N // 2} slots")
+    if not np.isfinite(w).all():
+        raise ValueError("weights must be finite")
+    plan = SlotPcmmPlan(d, shear_power, split, col_shear(shift_rows(w), shear_power))
+    pt = torch.from_numpy(encode_blocks(ctx.params, plan)).to(ctx.device)
+    plan.pts = torch.empty((d, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
+    native.call("he_slot_pcmm_encode_pts", ctx.handle, pt.data_ptr(), d, plan.pts.data_ptr(), ctx.stream())
+    h = ctypes.c_void_p()
+    native.call("he_slot_pcmm_plan_create", ctx.handle, plan.pts.data_ptr(), d, split.baby, split.giant,
+                ctypes.byref(h))
+    plan._handle = h
+    return plan
+
+
+def slot_pcmm_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: int) -> SlotPcmmKeys:
+    """Rotation keys the plan's BSGS schedule needs: baby steps i d, giant steps j b d."""
+    torch = _torch()
+    d, b, g = plan.dim, plan.split.baby, plan.split.giant
+    N = ctx.params.N
+
+    def gen(steps):
+        keys = torch.empty((max(len(steps), 1), 4, 2, 3, N), dtype=torch.int32, device=ctx.device)
+        if steps:
+            arr = (ctypes.c_int32 * len(steps))(*steps)
+            native.call("he_slot_rotation_keygen", ctx.handle, seed, sk.s.data_ptr(), arr, len(steps), keys.data_ptr(),
+                        ctx.stream())
+        return keys
+
+    baby = [i * d for i in range(1, b)]
+    giant = [j * b * d for j in range(1, g)]
+    return SlotPcmmKeys(gen(baby), gen(giant), tuple(baby + giant))
+
+
+def encrypt_packed(ctx: HeContext, sk: SecretKey, mat, shear_power: int, seed: int, r0: int = 0) -> PackedCt:
+    """Encrypt col_shear(mat, l) row-major in the slots at scale Delta, level 1 (hesim pack_sheared)."""
+    torch = _torch()
+    m = np.asarray(mat, dtype=float)
+    d = m.shape[0]
+    if m.shape != (d, d):
+        raise ValueError("only square matrices are packed")
+    if d * d > ctx.params.N // 2 or (ctx.params.N // 2) % (d * d):
+        raise ValueError(f"{d}x{d} does not tile the {ctx.params.N // 2} slots")
+    pt = torch.from_numpy(slots.encode(col_shear(m, shear_power).reshape(-1), ctx.params.N, ctx.params.delta)[None])
+    pt = pt.to(ctx.device)
+    out = torch.empty((2, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
+    native.call("he_encrypt_poly", ctx.handle, sk.s_ntt.data_ptr(), pt.data_ptr(), 1, seed, r0, out.data_ptr(),
+                ctx.stream())
+    return PackedCt(out, level=1, dim=d, shear_power=shear_power)
+
+
+def _check_operand(plan: SlotPcmmPlan, B) -> None:
+    """matmul.py:139-149, before any launch."""
+    if not getattr(B, "is_ct", False) or not isinstance(B, PackedCt):
+        raise TypeError("pcmm consumes a ciphertext operand")
+    if B.dim != plan.dim:
+        raise ValueError(f"dim mismatch: plan {plan.dim}, operand {B.dim}")
+    if B.shear_power != plan.shear_power + 1:
+        raise ValueError(f"shear chain broken: plan expects operand power {plan.shear_power + 1}, "
+                         f"got {B.shear_power}")
+    if B.level < 1:
+        raise NeedsBootstrapError("pcmm needs one level")
+
+
+def pcmm_slot_bsgs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, B: PackedCt) -> PackedCt:
+    """hesim pcmm_bsgs on the GPU: B (shear power l + 1, level 1) -> A B (shear power l, level 0)."""
+    torch = _torch()
+    _check_operand(plan, B)
+    require_level(B.level)
+    if B.level != 1:
+        raise ValueError(f"the slot-domain PCMM runs at level 1, operand is at level {B.level}")
+    out = torch.empty((1, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
+    ws = plan.workspace(ctx.device)
+    led = native.HeLedgerC()
+    native.call("he_slot_pcmm_run", plan._handle, B.data.data_ptr(), B.level, keys.baby.data_ptr(),
+                keys.giant.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel() * 4, ctx.stream(), ctypes.byref(led))
+    ctx.ledger.add_c(led)
+    ctx.ledger.observe_level(B.level - 1)
+    return PackedCt(out, level=B.level - 1, dim=plan.dim, shear_power=plan.shear_power)
+
+
+def decrypt_packed(ctx: HeContext, sk: SecretKey, Y: PackedCt) -> np.ndarray:
+    """Decrypt (limb 0) and decode the first d x d tile of the slots (hesim decode_packed)."""
+    torch = _torch()
+    limbs = int(Y.data.shape[0])
+    ph = torch.empty((1, ctx.params.N), dtype=torch.int64, device=ctx.device)
+    native.call("he_decrypt_rlwe", ctx.handle, sk.s_ntt.data_ptr(), Y.data.data_ptr(), 1, limbs, 0, ph.data_ptr(),
+                ctx.stream())
+    z = slots.decode(ph[0].cpu().numpy(), ctx.params.N, ctx.params.delta, Y.dim * Y.dim)
+    return z.reshape(Y.dim, Y.dim)
