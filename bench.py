@@ -496,7 +496,46 @@ def side_measurements(P, dev):
         out["ring_pack"] = ring_pack_side(P, dev)
     except Exception as exc:
         out["ring_pack_error"] = repr(exc)
+    try:
+        out["slot_pcmm"] = slot_pcmm_side(P, dev)
+    except Exception as exc:
+        out["slot_pcmm_error"] = repr(exc)
     return out
+
+
+def slot_pcmm_side(P, dev, reps=5):
+    """§8f3: hesim's own pcmm_bsgs schedule on real CKKS ciphertexts (slotpcmm.py), d x d in the N/2 slots:
+    device ms/op and decrypted precision against clear_pcmm."""
+    import torch
+
+    from paper_2601_18511_b200 import (HeContext, clear_slot_pcmm, decrypt_packed, encrypt_packed,
+                                       make_slot_pcmm_plan, pcmm_slot_bsgs, slot_pcmm_keygen)
+
+    ctx = HeContext(P, device=dev)
+    sk = ctx.keygen(51)
+    res = {}
+    for d in (128, 64):
+        rng = np.random.default_rng(d)
+        W = rng.uniform(-1, 1, (d, d)) / math.sqrt(d)
+        B = rng.uniform(-1, 1, (d, d))
+        plan = make_slot_pcmm_plan(ctx, W, shear_power=0)
+        keys = slot_pcmm_keygen(ctx, sk, plan, seed=53)
+        X = encrypt_packed(ctx, sk, B, 1, seed=55)
+        Y = pcmm_slot_bsgs(ctx, plan, keys, X)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            Y = pcmm_slot_bsgs(ctx, plan, keys, X)
+        e1.record()
+        torch.cuda.synchronize()
+        ref = clear_slot_pcmm(W, B, 0)
+        err = float(np.abs(decrypt_packed(ctx, sk, Y) - ref).max())
+        res[f"d{d}"] = {"ms_per_op": round(e0.elapsed_time(e1) / reps, 3),
+                        "rotations": plan.split.baby + plan.split.giant - 2, "split": [plan.split.baby, plan.split.giant],
+                        "precision_bits": round(-math.log2(err / float(np.abs(ref).max())), 1)}
+    return {"workload": f"hesim pcmm_bsgs schedule on CKKS ciphertexts, N = {P.N}, d x d in {P.N // 2} slots "
+                        "(hoisted baby rotations, gadget key switching), 1 GPU", **res}
 
 
 def ring_pack_side(P, dev, shape="4096x11008", reps=3):

@@ -1125,56 +1125,70 @@ namespace {
 constexpr int kSdSub = 2;
 constexpr int kSdBits = 15;
 constexpr int kSdT = 2 * kSdSub;   // digit polys per modulus
-__global__ void k_sd_digits(const uint32_t* __restrict__ a, uint64_t ls, uint32_t N, Mods M, uint32_t qh0,
-                            uint32_t qh0p, uint32_t qh1, uint32_t qh1p, uint32_t* __restrict__ D) {
+// Batched over z = blockIdx.z sources (all baby rotations, or all giant groups, in one launch).
+// digits of source z: a-part at a + z * as (limb stride ls) -> D [mod][z][t][N]  (cnt sources)
+__global__ void k_sd_digits(const uint32_t* __restrict__ a, uint64_t as, uint64_t ls, uint32_t N, uint32_t cnt, Mods M,
+                            uint32_t qh0, uint32_t qh0p, uint32_t qh1, uint32_t qh1p, uint32_t* __restrict__ D) {
+  const uint32_t z = blockIdx.z;
+  const uint32_t* src = a + z * as;
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
-    const uint32_t dg[2] = {shoup_mul(a[x], qh0, qh0p, M.m[0]), shoup_mul(a[ls + x], qh1, qh1p, M.m[1])};
+    const uint32_t dg[2] = {shoup_mul(src[x], qh0, qh0p, M.m[0]), shoup_mul(src[ls + x], qh1, qh1p, M.m[1])};
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int h = 0; h < kSdSub; ++h) {
         const uint32_t v = (dg[i] >> (kSdBits * h)) & ((1u << kSdBits) - 1u);
 #pragma unroll
-        for (int mod = 0; mod < 3; ++mod) D[(size_t)(mod * kSdT + i * kSdSub + h) * N + x] = v;
+        for (int mod = 0; mod < 3; ++mod) D[(((size_t)mod * cnt + z) * kSdT + i * kSdSub + h) * N + x] = v;
       }
   }
 }
-// UW [mod][part][N] = sum_t D^[mod][t][perm c] K[t][part][mod][c]   (sigma applied to the digits)
-__global__ void k_sd_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict__ perm,
-                         const uint32_t* __restrict__ K, uint32_t N, Mods M, uint32_t* __restrict__ UW) {
-  const uint32_t mod = blockIdx.y;
+// rotation z: UW [mod][z][part][N] = sum_t D^[mod][dz][t][perm_z c] K_z[t][part][mod][c]   (dz = hoist ? 0 : z)
+__global__ void k_sd_mac(const uint32_t* __restrict__ D, uint32_t dcnt, int hoist, const uint32_t* __restrict__ perms,
+                         const uint32_t* __restrict__ K, uint32_t N, uint32_t cnt, Mods M, uint32_t* __restrict__ UW) {
+  const uint32_t mod = blockIdx.y, z = blockIdx.z, dz = hoist ? 0 : z;
   const uint32_t q = mod == 0 ? M.m[0] : (mod == 1 ? M.m[1] : M.m[2]);
   const uint64_t mu = mod == 0 ? M.mu[0] : (mod == 1 ? M.mu[1] : M.mu[2]);
+  const uint32_t* perm = perms + (size_t)z * N;
+  const uint32_t* Kz = K + (size_t)z * 24 * N;
+  const uint32_t* Dz = D + ((size_t)mod * dcnt + dz) * kSdT * N;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
     const uint32_t pc = perm[c];
     uint64_t u = 0, w = 0;   // 4 products < 2^60 each
 #pragma unroll
     for (int t = 0; t < kSdT; ++t) {
-      const uint64_t dv = D[(size_t)(mod * kSdT + t) * N + pc];
-      u += dv * K[(size_t)((t * 2 + 0) * 3 + mod) * N + c];
-      w += dv * K[(size_t)((t * 2 + 1) * 3 + mod) * N + c];
+      const uint64_t dv = Dz[(size_t)t * N + pc];
+      u += dv * Kz[(size_t)((t * 2 + 0) * 3 + mod) * N + c];
+      w += dv * Kz[(size_t)((t * 2 + 1) * 3 + mod) * N + c];
     }
-    UW[(size_t)(mod * 2 + 0) * N + c] = barrett64(u, mu, q);
-    UW[(size_t)(mod * 2 + 1) * N + c] = barrett64(w, mu, q);
+    UW[(((size_t)mod * cnt + z) * 2 + 0) * N + c] = barrett64(u, mu, q);
+    UW[(((size_t)mod * cnt + z) * 2 + 1) * N + c] = barrett64(w, mu, q);
   }
 }
-// rotated ct (NTT domain) [L][ab][N]: a = (U - LB_u) P^-1, b = sigma(b^) + (W - LB_w) P^-1
+// rotated ct z (NTT domain) [L][ab][N] at out + z * os: a = (U - LB_u) P^-1, b = sigma(b^_z) + (W - LB_w) P^-1
+// (LB [L][z][part][N]; b^_z at bh + z * bs, limb stride bls)
 __global__ void k_sd_combine(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ LB,
-                             const uint32_t* __restrict__ bh, uint64_t bls, const uint32_t* __restrict__ perm,
-                             uint32_t N, Mods M, uint32_t pinv0, uint32_t pinv1, uint32_t* __restrict__ out) {
-  const uint32_t L = blockIdx.y, q = M.m[L], pinv = L ? pinv1 : pinv0;
+                             const uint32_t* __restrict__ bh, uint64_t bs, uint64_t bls,
+                             const uint32_t* __restrict__ perms, uint32_t N, uint32_t cnt, Mods M, uint32_t pinv0,
+                             uint32_t pinv1, uint32_t* __restrict__ out, uint64_t os) {
+  const uint32_t L = blockIdx.y, z = blockIdx.z, q = M.m[L], pinv = L ? pinv1 : pinv0;
   const uint64_t mu = M.mu[L];
+  const uint32_t* perm = perms + (size_t)z * N;
+  const uint32_t* U = UW + (((size_t)L * cnt + z) * 2) * N;
+  const uint32_t* lb = LB + (((size_t)L * cnt + z) * 2) * N;
+  const uint32_t* b = bh + z * bs + L * bls;
+  uint32_t* o = out + z * os + (size_t)L * 2 * N;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
-    const uint32_t u = mulmod_b(sub_mod(UW[(size_t)(L * 2 + 0) * N + c], LB[(size_t)(L * 2 + 0) * N + c], q), pinv, mu, q);
-    const uint32_t w = mulmod_b(sub_mod(UW[(size_t)(L * 2 + 1) * N + c], LB[(size_t)(L * 2 + 1) * N + c], q), pinv, mu, q);
-    out[(size_t)(L * 2 + 0) * N + c] = u;
-    out[(size_t)(L * 2 + 1) * N + c] = add_mod(bh[L * bls + perm[c]], w, q);
+    const uint32_t u = mulmod_b(sub_mod(U[c], lb[c], q), pinv, mu, q);
+    const uint32_t w = mulmod_b(sub_mod(U[N + c], lb[N + c], q), pinv, mu, q);
+    o[c] = u;
+    o[N + c] = add_mod(b[perm[c]], w, q);
   }
 }
-// inner [L][ab][N] = sum_{i < b} pt[i + j b][L] * baby[i][L][ab]   (NTT domain)
-__global__ void k_sd_inner(const uint32_t* __restrict__ baby, const uint32_t* __restrict__ pts, uint32_t b, uint32_t j,
-                           uint32_t N, Mods M, uint32_t* __restrict__ inner) {
-  const uint32_t L = blockIdx.y, q = M.m[L];
+// inner_z [L][ab][N] = sum_{i < b} pt[i + z b][L] * baby[i][L][ab]   (NTT domain), z = giant group
+__global__ void k_sd_inner(const uint32_t* __restrict__ baby, const uint32_t* __restrict__ pts, uint32_t b, uint32_t N,
+                           Mods M, uint32_t* __restrict__ inner) {
+  const uint32_t L = blockIdx.y, j = blockIdx.z, q = M.m[L];
   const uint64_t mu = M.mu[L];
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
     uint64_t aa = 0, ab = 0;
@@ -1184,14 +1198,19 @@ __global__ void k_sd_inner(const uint32_t* __restrict__ baby, const uint32_t* __
       aa = barrett64(aa + p * bi[0], mu, q);
       ab = barrett64(ab + p * bi[N], mu, q);
     }
-    inner[(size_t)(L * 2 + 0) * N + c] = (uint32_t)aa;
-    inner[(size_t)(L * 2 + 1) * N + c] = (uint32_t)ab;
+    inner[((size_t)j * 4 + L * 2 + 0) * N + c] = (uint32_t)aa;
+    inner[((size_t)j * 4 + L * 2 + 1) * N + c] = (uint32_t)ab;
   }
 }
-__global__ void k_sd_accumulate(uint32_t* __restrict__ acc, const uint32_t* __restrict__ part, uint32_t N, Mods M) {
+// acc [L][ab][N] = inner_0 + sum_{z < cnt} rot_z
+__global__ void k_sd_accumulate(const uint32_t* __restrict__ inner0, const uint32_t* __restrict__ rot, uint32_t cnt,
+                                uint32_t N, Mods M, uint32_t* __restrict__ acc) {
   const uint32_t L = blockIdx.y, q = M.m[L];
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 2 * N; x += gridDim.x * blockDim.x)
-    acc[(size_t)L * 2 * N + x] = add_mod(acc[(size_t)L * 2 * N + x], part[(size_t)L * 2 * N + x], q);
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < 2 * N; x += gridDim.x * blockDim.x) {
+    uint32_t v = inner0[(size_t)L * 2 * N + x];
+    for (uint32_t z = 0; z < cnt; ++z) v = add_mod(v, rot[(size_t)z * 4 * N + (size_t)L * 2 * N + x], q);
+    acc[(size_t)L * 2 * N + x] = v;
+  }
 }
 // signed int64 plaintext polys [count][N] -> [count][2 limbs][N] residues (NTT'd afterwards)
 __global__ void k_sd_reduce_pts(const int64_t* __restrict__ pt, uint64_t total, uint32_t logN, Mods M,
@@ -1338,7 +1357,7 @@ struct SdWs {
   uint32_t *D, *X, *baby, *inner, *rot, *acc, *UW, *LB;
 };
 static uint64_t sd_ws_words(const he_slot_pcmm_plan* p, SdWs* w, uint32_t* base) {
-  const uint64_t N = p->N;
+  const uint64_t N = p->N, T = (p->b > p->g ? p->b : p->g);   // rotations per batched pass < T
   uint64_t off = 0;
   auto take = [&](uint32_t*& ptr, uint64_t words) {
     if (w) ptr = base + off;
@@ -1346,14 +1365,14 @@ static uint64_t sd_ws_words(const he_slot_pcmm_plan* p, SdWs* w, uint32_t* base)
   };
   SdWs dummy;
   SdWs& r = w ? *w : dummy;
-  take(r.D, 3ull * kSdT * N);
+  take(r.D, 3ull * kSdT * T * N);
   take(r.X, 4 * N);
   take(r.baby, 4ull * p->b * N);
-  take(r.inner, 4 * N);
-  take(r.rot, 4 * N);
+  take(r.inner, 4ull * p->g * N);
+  take(r.rot, 4ull * T * N);
   take(r.acc, 4 * N);
-  take(r.UW, 6 * N);
-  take(r.LB, 4 * N);
+  take(r.UW, 6ull * T * N);
+  take(r.LB, 4ull * T * N);
   return off;
 }
 
@@ -1374,57 +1393,65 @@ extern "C" he_status he_slot_pcmm_run(const he_slot_pcmm_plan* p, const uint32_t
   if (ws_bytes < sd_ws_words(p, nullptr, nullptr) * sizeof(uint32_t)) return fail(HE_EINVAL, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   const he_context* c = p->ctx;
-  const uint32_t N = p->N;
+  const uint32_t N = p->N, b = p->b, g = p->g;
   SdWs w;
   sd_ws_words(p, &w, (uint32_t*)ws_dev);
   const dim3 g1 = grid_for(N);
-  dim3 g2 = g1, g3 = g1;
-  g2.y = 2;
-  g3.y = 3;
-  // rotation of the ciphertext whose lifted digits D^ (NTT) and b^ (NTT, limb stride 2N) are given
-  auto rotate = [&](const uint32_t* bh, uint32_t t, const uint32_t* key, uint32_t* dst) -> he_status {
-    const uint32_t* perm = p->perms + (size_t)t * N;
-    k_sd_mac<<<g3, 256, 0, st>>>(w.D, perm, key, N, p->M, w.UW);
-    HE_CUDA(ntt_inverse(c->ntt[2], w.UW + 4ull * N, 2, N, st), "INTT(U_P, W_P)");
-    k_moddown_lift<<<grid_for(2ull * N), 256, 0, st>>>(w.UW + 4ull * N, N, p->M, w.LB);
-    HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2, N, st), "NTT(lift q0)");
-    HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2ull * N, 2, N, st), "NTT(lift q1)");
-    k_sd_combine<<<g2, 256, 0, st>>>(w.UW, w.LB, bh, 2ull * N, perm, N, p->M, p->pinv[0], p->pinv[1], dst);
-    return HE_OK;
+  auto grid3 = [&](uint32_t y, uint32_t z) {
+    dim3 gg = g1;
+    gg.y = y;
+    gg.z = z;
+    return gg;
   };
-  auto digits = [&](const uint32_t* a_coeff) -> he_status {
-    k_sd_digits<<<g1, 256, 0, st>>>(a_coeff, 2ull * N, N, p->M, p->qhinv[0], p->qhinvp[0], p->qhinv[1], p->qhinvp[1],
-                                    w.D);
+  // digits of cnt sources (a-part of source z at a + z * as) -> D^ [mod][z][t][N] (NTT)
+  auto digits = [&](const uint32_t* a, uint64_t as, uint32_t cnt) -> he_status {
+    k_sd_digits<<<grid3(1, cnt), 256, 0, st>>>(a, as, 2ull * N, N, cnt, p->M, p->qhinv[0], p->qhinvp[0], p->qhinv[1],
+                                               p->qhinvp[1], w.D);
     for (int mod = 0; mod < 3; ++mod)
-      HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * kSdT * N, kSdT, N, st), "NTT(D)");
+      HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * cnt * kSdT * N, cnt * kSdT, N, st), "NTT(D)");
     return HE_OK;
   };
-  // baby steps (hoisted: one digit decomposition of the input)
-  he_status s = digits(ct_in);
+  // cnt rotations in one pass: rotation z uses perm table t0 + z, key z, digits dz (hoist: all z share D^ 0),
+  // source b^ at bh + z * bs; result z at dst + z * 4N (NTT domain)
+  auto rotate = [&](uint32_t cnt, int hoist, uint32_t dcnt, uint32_t t0, const uint32_t* keys, const uint32_t* bh,
+                    uint64_t bs, uint32_t* dst) -> he_status {
+    k_sd_mac<<<grid3(3, cnt), 256, 0, st>>>(w.D, dcnt, hoist, p->perms + (size_t)t0 * N, keys, N, cnt, p->M, w.UW);
+    uint32_t* UWP = w.UW + (size_t)2 * cnt * 2 * N;   // [z][part][N] of modulus P
+    HE_CUDA(ntt_inverse(c->ntt[2], UWP, 2 * cnt, N, st), "INTT(U_P, W_P)");
+    k_moddown_lift<<<grid_for(2ull * cnt * N), 256, 0, st>>>(UWP, (uint64_t)cnt * N, p->M, w.LB);
+    HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2 * cnt, N, st), "NTT(lift q0)");
+    HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2ull * cnt * N, 2 * cnt, N, st), "NTT(lift q1)");
+    k_sd_combine<<<grid3(2, cnt), 256, 0, st>>>(w.UW, w.LB, bh, bs, 2ull * N, p->perms + (size_t)t0 * N, N, cnt, p->M,
+                                               p->pinv[0], p->pinv[1], dst, 4ull * N);
+    return HE_OK;
+  };
+  // baby steps: one hoisted digit decomposition of the input, all b - 1 rotations in one pass
+  he_status s = digits(ct_in, 0, 1);
   if (s) return s;
   HE_CUDA(cudaMemcpyAsync(w.X, ct_in, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
   for (int L = 0; L < 2; ++L) HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
   HE_CUDA(cudaMemcpyAsync(w.baby, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
-  for (uint32_t i = 1; i < p->b; ++i) {
-    s = rotate(w.X + N, i - 1, keys_baby + (size_t)(i - 1) * 24 * N, w.baby + (size_t)i * 4 * N);
+  if (b > 1) {
+    s = rotate(b - 1, 1, 1, 0, keys_baby, w.X + N, 0, w.baby + 4ull * N);
     if (s) return s;
   }
-  // giant groups
-  for (uint32_t j = 0; j < p->g; ++j) {
-    k_sd_inner<<<g2, 256, 0, st>>>(w.baby, p->pts, p->b, j, N, p->M, j == 0 ? w.acc : w.inner);
-    if (j == 0) continue;
-    for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt[L], w.inner + (size_t)L * 2 * N, 1, N, st), "INTT(inner a)");
-    s = digits(w.inner);
+  // giant groups: all products in one launch, all g - 1 rotations in one pass
+  k_sd_inner<<<grid3(2, g), 256, 0, st>>>(w.baby, p->pts, b, N, p->M, w.inner);
+  if (g > 1) {
+    uint32_t* in1 = w.inner + 4ull * N;   // groups 1 .. g-1
+    for (int L = 0; L < 2; ++L)
+      HE_CUDA(ntt_inverse(c->ntt[L], in1 + (size_t)L * 2 * N, g - 1, 4ull * N, st), "INTT(inner a)");
+    s = digits(in1, 4ull * N, g - 1);
     if (s) return s;
-    s = rotate(w.inner + N, (p->b - 1) + (j - 1), keys_giant + (size_t)(j - 1) * 24 * N, w.rot);
+    s = rotate(g - 1, 0, g - 1, b - 1, keys_giant, in1 + N, 4ull * N, w.rot);
     if (s) return s;
-    k_sd_accumulate<<<g2, 256, 0, st>>>(w.acc, w.rot, N, p->M);
   }
+  k_sd_accumulate<<<grid3(2, 1), 256, 0, st>>>(w.inner, w.rot, g - 1, N, p->M, w.acc);
   for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt[L], w.acc + (size_t)L * 2 * N, 2, N, st), "INTT(acc)");
   k_rh_combine<<<grid_for(2ull * N), 256, 0, st>>>(w.acc, 1, N, p->M.m[0], p->M.m[1], p->q1inv, p->q1invp, out);
   HE_CUDA(cudaGetLastError(), "slot pcmm launch");
   if (ledger) {
-    ledger->ct_rotations += (int64_t)(p->b - 1) + (p->g - 1);
+    ledger->ct_rotations += (int64_t)(b - 1) + (g - 1);
     ledger->pc_mults += p->d;
     ledger->rescales += 1;
   }
