@@ -465,7 +465,8 @@ def side_measurements(P, dev):
             e1.record()
             torch.cuda.synchronize()
             err = float(np.abs(decrypt_vector(ctx, keys.s_up_ntt, y) - clear_pcmv(W, v)).max())
-            rh[f"{n_out}x{n_in}"] = {"ms_per_op": round(e0.elapsed_time(e1) / 5, 3),
+            gms = graph_ms(lambda: pcmv_rhombus(ctx, plan, keys, x))
+            rh[f"{n_out}x{n_in}"] = {"ms_per_op": round(e0.elapsed_time(e1) / 5, 3), "ms_per_op_cuda_graph": gms,
                                      "precision_bits": round(-math.log2(err), 1),
                                      "key_switches": (P.rhombus_degree - 1) * -(-n_out // P.rhombus_degree) + 1}
             del plan
@@ -503,6 +504,27 @@ def side_measurements(P, dev):
     return out
 
 
+def graph_ms(fn, reps=5):
+    """Device ms per replay of the op captured into a CUDA graph (paper_2601_18511_b200.OpGraph)."""
+    import torch
+
+    from paper_2601_18511_b200 import OpGraph
+
+    try:
+        g = OpGraph(fn)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return round(e0.elapsed_time(e1) / reps, 3)
+    except Exception:
+        return None
+
+
 def slot_pcmm_side(P, dev, reps=5):
     """§8f3: hesim's own pcmm_bsgs schedule on real CKKS ciphertexts (slotpcmm.py), d x d in the N/2 slots:
     device ms/op and decrypted precision against clear_pcmm."""
@@ -531,7 +553,8 @@ def slot_pcmm_side(P, dev, reps=5):
         torch.cuda.synchronize()
         ref = clear_slot_pcmm(W, B, 0)
         err = float(np.abs(decrypt_packed(ctx, sk, Y) - ref).max())
-        res[f"d{d}"] = {"ms_per_op": round(e0.elapsed_time(e1) / reps, 3),
+        gms = graph_ms(lambda: pcmm_slot_bsgs(ctx, plan, keys, X))
+        res[f"d{d}"] = {"ms_per_op": round(e0.elapsed_time(e1) / reps, 3), "ms_per_op_cuda_graph": gms,
                         "rotations": plan.split.baby + plan.split.giant - 2, "split": [plan.split.baby, plan.split.giant],
                         "precision_bits": round(-math.log2(err / float(np.abs(ref).max())), 1)}
     return {"workload": f"hesim pcmm_bsgs schedule on CKKS ciphertexts, N = {P.N}, d x d in {P.N // 2} slots "

@@ -130,3 +130,20 @@ def test_sharded_pcmv_emulated_ranks(params, n_out, n_in, strategy, world):
         assert np.abs(res - full_res).max() < 2 ** -18
     err = np.abs(res - ref).max()
     assert err < np.abs(ref).max() * 2 ** -13, err
+
+
+def test_graph_replay_same_words():
+    """OpGraph: a captured PCMv replays to the same output words as the eager call."""
+    import torch
+
+    from paper_2601_18511_b200 import OpGraph
+
+    P = HeParams.llama()
+    ctx, sk, keys, x, v, W = _setup(P, 4096, 4096, seed=3)
+    plan = make_rhombus_plan(ctx, W)
+    ref = pcmv_rhombus(ctx, plan, keys, x).data.clone()
+    g = OpGraph(lambda: pcmv_rhombus(ctx, plan, keys, x))
+    g.result.data.zero_()
+    y = g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y.data, ref)

@@ -134,3 +134,24 @@ def test_llama_ring_precision(d, shear):
     # rounding by ~sqrt(N) = 256: ~2^-14 per weight slot, ~2^-10 after d = 128 terms (the reason the paper
     # moves the projections to coefficient encoding, where the MLWE PCMM keeps >= 14 bits)
     assert err < np.abs(ref).max() * 2.0 ** -9
+
+
+def test_graph_replay_same_words():
+    import torch
+
+    from paper_2601_18511_b200 import OpGraph
+
+    P = HeParams.llama()
+    ctx = HeContext(P)
+    sk = ctx.keygen(3)
+    rng = np.random.default_rng(1)
+    d = 64
+    plan = make_slot_pcmm_plan(ctx, rng.uniform(-1, 1, (d, d)) / np.sqrt(d))
+    keys = slot_pcmm_keygen(ctx, sk, plan, seed=5)
+    X = encrypt_packed(ctx, sk, rng.uniform(-1, 1, (d, d)), 1, seed=6)
+    ref = pcmm_slot_bsgs(ctx, plan, keys, X).data.clone()
+    g = OpGraph(lambda: pcmm_slot_bsgs(ctx, plan, keys, X))
+    g.result.data.zero_()
+    y = g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y.data, ref)
