@@ -14,7 +14,7 @@ from .pcmm import (MlwePcmmPlan, clear_pcmm, load_mlwe_pcmm_plan, load_plan_bund
 from .rhombus import (CtVector, RhombusKeys, RhombusPlan, clear_pcmv, decrypt_vector, encrypt_vector,
                       make_rhombus_plan, pcmv_rhombus, rhombus_keygen)
 from .slotpcmm import (BsgsSplit, PackedCt, SlotPcmmKeys, SlotPcmmPlan, clear_slot_pcmm, decrypt_packed,
-                       encrypt_packed, make_slot_pcmm_plan, pcmm_slot_bsgs, slot_pcmm_keygen)
+                       encrypt_packed, make_slot_pcmm_plan, pcmm_slot_bsgs, pcmm_slot_depth1, slot_pcmm_keygen)
 from .graphs import OpGraph
 from .ringpack import (RingPackKeys, RingPackPlan, make_ring_pack_plan, pcmm_level1, pcmm_packed, ring_pack,
                        ring_pack_keygen)
@@ -29,7 +29,7 @@ __all__ = [
     "RingPackKeys", "RingPackPlan", "make_ring_pack_plan", "pcmm_level1", "pcmm_packed", "ring_pack",
     "ring_pack_keygen",
     "BsgsSplit", "PackedCt", "SlotPcmmKeys", "SlotPcmmPlan", "clear_slot_pcmm", "decrypt_packed", "encrypt_packed",
-    "make_slot_pcmm_plan", "pcmm_slot_bsgs", "slot_pcmm_keygen", "OpGraph",
+    "make_slot_pcmm_plan", "pcmm_slot_bsgs", "pcmm_slot_depth1", "slot_pcmm_keygen", "OpGraph",
 ]
 
 __version__ = "0.1.0"

@@ -231,6 +231,16 @@ def pcmm_slot_bsgs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, B: Pa
     return PackedCt(out, level=B.level - 1, dim=plan.dim, shear_power=plan.shear_power)
 
 
+def pcmm_slot_depth1(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, B: PackedCt) -> PackedCt:
+    """hesim pcmm_depth1 (matmul.py:152-162): the full k-sum with d - 1 input rotations and one fused
+    multiply-accumulate -- the b = d, g = 1 corner of the BSGS schedule, so it runs on a plan made with
+    split=BsgsSplit(d, 1) (its blocks are exactly depth1's (k, 0) blocks); the input rotations are
+    hoisted and batched into one pass."""
+    if plan.split.giant != 1:
+        raise ValueError("pcmm_slot_depth1 needs a plan made with split=BsgsSplit(d, 1)")
+    return pcmm_slot_bsgs(ctx, plan, keys, B)
+
+
 def decrypt_packed(ctx: HeContext, sk: SecretKey, Y: PackedCt) -> np.ndarray:
     """Decrypt (limb 0) and decode the first d x d tile of the slots (hesim decode_packed)."""
     torch = _torch()

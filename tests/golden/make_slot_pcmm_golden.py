@@ -8,7 +8,7 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
-from hesim import SimParams, SlotContext, make_pcmm_plan, pack_sheared, pcmm_bsgs  # noqa: E402
+from hesim import SimParams, SlotContext, make_pcmm_plan, pack_sheared, pcmm_bsgs, pcmm_depth1  # noqa: E402
 from hesim.packing import unpack_matrix  # noqa: E402
 
 out = {}
@@ -24,5 +24,6 @@ for d, shear in ((16, 0), (16, 2), (8, 1)):
     out[key + "_B"] = B
     out[key + "_hesim_bsgs"] = unpack_matrix(r.payload.slots, d)
     out[key + "_split"] = np.array([plan.split.baby, plan.split.giant])
+    out[key + "_hesim_depth1"] = unpack_matrix(pcmm_depth1(ctx, plan, pack_sheared(ctx, B, shear + 1)).payload.slots, d)
 np.savez(Path(__file__).with_name("slot_pcmm_golden.npz"), **out)
 print("wrote", sorted(out))

@@ -155,3 +155,25 @@ def test_graph_replay_same_words():
     y = g.replay()
     torch.cuda.synchronize()
     assert torch.equal(y.data, ref)
+
+
+@pytest.mark.parametrize("key", ["d16_l0", "d8_l1"])
+def test_depth1_schedule_matches_hesim_depth1(key):
+    """pcmm_depth1 = the (b, g) = (d, 1) corner: d - 1 hoisted input rotations, one fused MAC."""
+    from paper_2601_18511_b200.slotpcmm import pcmm_slot_depth1
+
+    g = np.load(GOLD / "slot_pcmm_golden.npz")
+    W, B, ref = g[key + "_W"], g[key + "_B"], g[key + "_hesim_depth1"]
+    shear = int(key.split("_l")[1])
+    d = W.shape[0]
+    P = HeParams.toy()
+    ctx = HeContext(P)
+    sk = ctx.keygen(7)
+    plan = make_slot_pcmm_plan(ctx, W, shear_power=shear, split=BsgsSplit(d, 1))
+    keys = slot_pcmm_keygen(ctx, sk, plan, seed=13)
+    before = ctx.ledger.snapshot()
+    Y = pcmm_slot_depth1(ctx, plan, keys, encrypt_packed(ctx, sk, B, shear + 1, seed=11))
+    assert ctx.ledger.diff(before)["ct_rotations"] == d - 1
+    assert np.abs(decrypt_packed(ctx, sk, Y) - ref).max() < 2.0 ** -13
+    with pytest.raises(ValueError):
+        pcmm_slot_depth1(ctx, make_slot_pcmm_plan(ctx, W, shear_power=shear), keys, Y)
