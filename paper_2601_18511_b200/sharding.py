@@ -314,3 +314,28 @@ def all_reduce_max(t, group=None):
         return host.to(t.device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t
+
+
+def pcmm_packed_sharded(ctx, plan, rp, keys, X, n_out: int, group=None):
+    """Row-sharded PCMM + ring packing: this rank's plans cover output row-blocks [b0, b1) (row_shards);
+    each rank packs its own blocks and the packed level-0 RLWE blocks (2 N words each, ~128x less than
+    the MLWE rows) are all-gathered.  Returns CtBlocks [n_out/k, 1, 2, N] on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from .context import CtBlocks
+    from .ringpack import pcmm_packed
+
+    p = ctx.params
+    k = p.mlwe_rank
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    per = shard_slots(n_out, k, world)
+    broadcast_input(X.data, group)
+    local = torch.zeros((per, 1, 2, p.N), dtype=torch.int32, device=ctx.device)
+    pcmm_packed(ctx, plan, rp, keys, X, out=local[: rp.n_out // k])
+    if world == 1:
+        return CtBlocks(local[: n_out // k], level=0, n_cols=n_out)
+    allp = torch.empty((per * world, 1, 2, p.N), dtype=torch.int32, device=ctx.device)
+    all_gather_into(allp, local, group)
+    keep = torch.cat([allp[r * per: r * per + (b1 - b0)] for r, (b0, b1) in enumerate(row_shards(n_out, k, world))])
+    return CtBlocks(keep, level=0, n_cols=n_out)

@@ -44,6 +44,14 @@ def main():
         torch.cuda.synchronize()
         assert torch.equal(fb, ref.out_b) and torch.equal(fa, ref.out_a), "fused peer-store PCMM words differ"
         fused = "ok"
+    # PCMM + ring packing, row-sharded (each rank packs its blocks, packed blocks all-gathered)
+    from paper_2601_18511_b200 import make_ring_pack_plan, pcmm_packed, ring_pack_keygen
+    from paper_2601_18511_b200.sharding import pcmm_packed_sharded
+
+    rkeys = ring_pack_keygen(ctx, sk, seed=21)
+    full_p = pcmm_packed(ctx, make_mlwe_pcmm_plan(ctx, W), make_ring_pack_plan(ctx, n_out), rkeys, X)
+    Yp = pcmm_packed_sharded(ctx, plan, make_ring_pack_plan(ctx, (b1 - b0) * k), rkeys, X, n_out)
+    assert torch.equal(Yp.data, full_p.data), "sharded packed output differs"
     # Rhombus PCMv, both strategies
     for (n_o, n_i, strat) in ((8192, 4096, "rows"), (4096, 8192, "cols")):
         v = rng.uniform(-1, 1, n_i)
