@@ -1307,7 +1307,8 @@ extern "C" he_status he_slot_pcmm_plan_create(const he_context* c, const uint32_
   if (!c || !pts_ntt_dev || !out) return fail(HE_EINVAL, "null argument");
   if (d == 0 || b == 0 || g == 0 || b * g != d) return fail(HE_EINVAL, "split %ux%u does not cover dim %u", b, g, d);
   const uint32_t N = c->R.N;
-  if ((uint64_t)d * d > N / 2) return fail(HE_EINVAL, "%ux%u does not fit in %u slots", d, d, N / 2);
+  if ((uint64_t)d * d > N / 2 || (N / 2) % (d * d))
+    return fail(HE_EINVAL, "%ux%u does not tile the %u slots (d^2 must divide N/2)", d, d, N / 2);
   he_slot_pcmm_plan* p = new (std::nothrow) he_slot_pcmm_plan();
   if (!p) return fail(HE_ENOMEM, "out of host memory");
   p->ctx = c;

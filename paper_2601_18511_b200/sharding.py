@@ -13,6 +13,7 @@ moves them.
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 
@@ -179,6 +180,17 @@ class _IpcBuffers:
 
         torch.cuda.synchronize()
         dist.barrier(group=self.group)
+
+    def __del__(self):  # unmap the peers' buffers, then free our own
+        try:
+            self.rt.cudaIpcCloseMemHandle.argtypes = [ctypes.c_void_p]
+            self.rt.cudaFree.argtypes = [ctypes.c_void_p]
+            for ptr in self.opened:
+                self.rt.cudaIpcCloseMemHandle(ptr)
+            for ptr in self.local:
+                self.rt.cudaFree(ptr)
+        except Exception:
+            pass
 
 
 def _device_view(ptr: int, shape, device):
