@@ -213,6 +213,7 @@ def ipc_outputs(ctx, n_out: int, group=None):
     out_b = _device_view(bufs.local[0], shp_b, ctx.device)
     out_a = _device_view(bufs.local[1], shp_a, ctx.device)
     out_b._ipc_owner = bufs   # keep the mappings alive with the views
+    out_a._ipc_owner = bufs
     del dist
     return out_b, out_a, bufs.ptrs[0], bufs.ptrs[1], bufs
 
