@@ -340,8 +340,11 @@ def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_hos
     cs = plan._copy_stream
     native.call("he_pcmm_decompose", plan._handle, X.data.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
     copied = [None, None]
-    for c, row0 in enumerate(range(0, plan.n_out, chunk_rows)):
-        rows = min(chunk_rows, plan.n_out - row0)
+    # a short first chunk starts the device->host stream sooner (the copies, not the compute, set the pace)
+    first = min(256, chunk_rows) if plan.n_out > chunk_rows else chunk_rows
+    starts = [0] + list(range(first, plan.n_out, chunk_rows))
+    for c, row0 in enumerate(starts):
+        rows = min(first if c == 0 else chunk_rows, plan.n_out - row0)
         slot = c % 2
         if copied[slot] is not None:
             st.wait_event(copied[slot])               # the slot's previous chunk has left the device
