@@ -374,3 +374,22 @@ def test_plan_files_round_trip(tmp_path):
     assert list(b) == ["layer0.down"] and torch.equal(pcmm_mlwe(ctx, b["layer0.down"], X).out_a, ra)
     with pytest.raises(ValueError):
         load_mlwe_pcmm_plan(HeContext(HeParams.toy()), tmp_path / "p.npz")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_llama_minimal_and_zero_operands(algo):
+    """Edge shapes at the Llama ring: one output block x one input ciphertext (n_out = n_in = k) checked
+    word for word against the oracle; an all-zero weight matrix gives outputs that decrypt to 0 and a
+    zero activation block decrypts to 0 (noise only)."""
+    P = HeParams.llama()
+    k = P.mlwe_rank
+    ctx, sk, A, W, X = setup(P, k, k, seed=12)
+    Y = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W, algo=algo), X)
+    rows, cols = _llama_sample(P, k)
+    rows = [r for r in rows if r < k]
+    ref = O.pcmm(P, O.encode_weights(P, W), u32(X.data), rows=rows, cols=cols)
+    assert np.array_equal(gather(P, Y, rows, cols), ref)
+    Z = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, np.zeros_like(W), algo=algo), X)
+    assert np.abs(ctx.decrypt_pcmm(sk, Z)).max() < 2 ** -20
+    X0 = ctx.encrypt_acts(sk, np.zeros_like(A), seed=13)
+    assert np.abs(ctx.decrypt_pcmm(sk, pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W, algo=algo), X0))).max() < 2 ** -14
