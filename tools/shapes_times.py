@@ -8,16 +8,19 @@ import torch
 
 from paper_2601_18511_b200 import HeContext, HeParams, make_mlwe_pcmm_plan, pcmm_mlwe
 
+SHAPES = sys.argv[1].split(",") if len(sys.argv) > 1 else ["4096x4096", "4096x11008", "11008x4096", "14336x4096",
+                                                            "4096x14336"]
+ALGOS = sys.argv[2].split(",") if len(sys.argv) > 2 else ["spectral", "direct"]
 P = HeParams.llama()
 ctx = HeContext(P)
 g = torch.Generator(device="cuda").manual_seed(1)
-for shp in ["4096x4096", "4096x11008", "11008x4096", "14336x4096", "4096x14336"]:
+for shp in SHAPES:
     n_out, n_in = (int(v) for v in shp.split("x"))
     W = (torch.rand((n_out, n_in), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) / math.sqrt(n_in)
     A = torch.rand((P.tokens, n_in), generator=g, device="cuda", dtype=torch.float64) * 2 - 1
     X = ctx.encrypt_acts(ctx.keygen(1), A, seed=2)
     row = [shp]
-    for algo in ("spectral", "direct"):
+    for algo in ALGOS:
         plan = make_mlwe_pcmm_plan(ctx, W, algo=algo)
         Y = pcmm_mlwe(ctx, plan, X)
         for _ in range(2):
