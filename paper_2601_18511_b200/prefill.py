@@ -155,3 +155,41 @@ def chunked_prefill(tokens, ptok: int, cfg: ToyConfig, ctx: HeContext | None = N
         forward_chunk(tokens[:ptok], cache, cfg, layers)
     x = forward_chunk(tokens[ptok:], cache, cfg, layers, proj, ctx, sk)
     return rms_norm(x[-1]) @ w_out, cache
+
+
+# ---------------------------------------------------------------- generation: the Rhombus PCMv plug-in point
+@dataclass
+class EncryptedVectorProjections:
+    """Generation-stage projections of one token: each x @ w is an encrypted
+    vector -> Rhombus PCMv (plan of w^T) -> decryption under the output key s'(X^rho)."""
+    plans: list
+    keys: object
+    seed: int = 2000
+    calls: int = 0
+
+    def apply(self, ctx: HeContext, sk: SecretKey, layer: int, name: str, x: np.ndarray) -> np.ndarray:
+        from .rhombus import decrypt_vector, encrypt_vector, pcmv_rhombus
+
+        rows = []
+        for row in np.atleast_2d(x):
+            self.calls += 1
+            ct = encrypt_vector(ctx, sk, row, seed=self.seed + self.calls)
+            rows.append(decrypt_vector(ctx, self.keys.s_up_ntt, pcmv_rhombus(ctx, self.plans[layer][name], self.keys, ct)))
+        return np.stack(rows)
+
+
+def make_vector_projection_plans(ctx: HeContext, sk: SecretKey, layers, seed: int = 77) -> EncryptedVectorProjections:
+    from .rhombus import make_rhombus_plan, rhombus_keygen
+
+    keys = rhombus_keygen(ctx, sk, seed)
+    return EncryptedVectorProjections([{n: make_rhombus_plan(ctx, np.ascontiguousarray(w.T))
+                                        for n, w in zip(NAMES, lw)} for lw in layers], keys)
+
+
+def decode_step(cache: Cache, token, cfg: ToyConfig, ctx: HeContext | None = None, sk: SecretKey | None = None,
+                proj=None):
+    """pipeline.py:240-247: one autoregressive row against the cache; with ``proj`` (e.g. the Rhombus
+    PCMv projections) the seven projections run on ciphertexts.  Returns (logits, cache)."""
+    layers, w_out = make_weights(cfg)
+    x = forward_chunk(np.atleast_2d(np.asarray(token, dtype=float)), cache, cfg, layers, proj, ctx, sk)
+    return rms_norm(x[-1]) @ w_out, cache

@@ -7,7 +7,7 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
-from hesim.pipeline import PrefillSplit, ToyModelConfig, chunked_prefill, demo_tokens  # noqa: E402
+from hesim.pipeline import PrefillSplit, ToyModelConfig, chunked_prefill, decode_step, demo_tokens  # noqa: E402
 
 out = {}
 for name, cfg, ntok, ptok in (("toy", ToyModelConfig(d_model=32, d_head=16, n_heads=2, d_ff=64, n_layers=1, seed=0),
@@ -22,5 +22,8 @@ for name, cfg, ntok, ptok in (("toy", ToyModelConfig(d_model=32, d_head=16, n_he
     for li in range(cfg.n_layers):
         out[f"{name}_k{li}"] = cache.k[li]
         out[f"{name}_v{li}"] = cache.v[li]
+    nxt = demo_tokens(1, cfg.d_model, seed=11)[0]
+    out[name + "_next"] = nxt
+    out[name + "_decode_logits"] = decode_step(cache, nxt, cfg)[0]
 np.savez(Path(__file__).with_name("prefill_golden.npz"), **out)
 print("wrote", sorted(out))
