@@ -271,9 +271,9 @@ def decode_mlwe_rows(params: HeParams, phase: np.ndarray, row0: int, n_out: int)
     br = bit_reverse_table(half.bit_length() - 1)
     sig = sigma_table(k)
     out = np.full((half, n_out), np.nan)
-    for i in range(phase.shape[0]):
-        y = row0 + i
-        out[br, (y // k) * k + sig[y % k]] = phase[i, :half] / params.delta
+    y = row0 + np.arange(phase.shape[0])
+    cols = (y // k) * k + np.asarray(sig)[y % k]
+    out[np.asarray(br)[:, None], cols[None, :]] = (phase[:, :half] / params.delta).T
     return out
 
 

@@ -275,8 +275,28 @@ extern "C" he_status he_decrypt_mlwe(const he_context* c, const int32_t* s_dev, 
   if (!c || !s_dev || !out_b_dev || !out_a_dev || !phase_dev) return fail(HE_EINVAL, "null argument");
   if (row0 + n_rows > n_out || n_out % c->R.k) return fail(HE_EINVAL, "row range outside the output");
   if (n_rows == 0) return HE_OK;
-  HE_CUDA(launch_decrypt_mlwe(c->R, s_dev, out_b_dev, out_a_dev, n_out, row0, n_rows, phase_dev, (cudaStream_t)stream),
-          "decrypt mlwe");
+  cudaStream_t st = (cudaStream_t)stream;
+  static const bool direct = getenv("HE_DECRYPT_MLWE_DIRECT") != nullptr;   // the O(k d^2) convolution kernel
+  if (direct || c->R.k > 256 || c->R.d % 32) {
+    HE_CUDA(launch_decrypt_mlwe(c->R, s_dev, out_b_dev, out_a_dev, n_out, row0, n_rows, phase_dev, st), "decrypt mlwe");
+    return HE_OK;
+  }
+  // RLWE view: one degree-N NTT product per row (rows in chunks of 256: 64 MB of scratch)
+  const uint32_t N = c->R.N, chunk = n_rows < 256 ? n_rows : 256;
+  uint32_t* buf = nullptr;
+  HE_CUDA(cudaMallocAsync(&buf, ((size_t)chunk + 1) * N * sizeof(uint32_t), st), "alloc");
+  uint32_t* sh = buf + (size_t)chunk * N;
+  HE_CUDA(launch_reduce_secret(c->R, s_dev, 0, sh, st), "s mod q0");
+  HE_CUDA(ntt_forward(c->ntt[0], sh, 1, N, st), "NTT(s)");
+  for (uint32_t r0 = 0; r0 < n_rows; r0 += chunk) {
+    const uint32_t rows = n_rows - r0 < chunk ? n_rows - r0 : chunk;
+    HE_CUDA(launch_mlwe_rows_to_poly(c->R, out_a_dev, row0 + r0, rows, buf, st), "a' -> A");
+    HE_CUDA(ntt_forward(c->ntt[0], buf, rows, N, st), "NTT(A)");
+    HE_CUDA(launch_pointwise_mul(buf, N, sh, N, rows, c->R.q[0], buf, N, st), "A^ s^");
+    HE_CUDA(ntt_inverse(c->ntt[0], buf, rows, N, st), "INTT(A s)");
+    HE_CUDA(launch_mlwe_phase(c->R, buf, out_b_dev, row0 + r0, rows, phase_dev + (size_t)r0 * c->R.d, st), "phase");
+  }
+  cudaFreeAsync(buf, st);
   return HE_OK;
 }
 

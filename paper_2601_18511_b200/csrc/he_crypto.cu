@@ -373,4 +373,52 @@ cudaError_t launch_decrypt_mlwe(const RingDims& R, const int32_t* s, const uint3
   return cudaGetLastError();
 }
 
+// Fast MLWE decryption through the RLWE view: row y's phase is component 0 of A_y s (degree N) plus b',
+// with A_y[k m - j] = a'_y[j][m] (negacyclic) -- one NTT product per row instead of k length-d convolutions.
+// A [rows][N] (q0 residues) from the a' rows [row0, row0 + rows): one CTA per (32 positions m, row)
+__global__ void __launch_bounds__(256) mlwe_rows_to_poly_kernel(const uint32_t* __restrict__ out_a, uint32_t row0,
+                                                                uint32_t d, uint32_t k, uint32_t N, uint32_t q0,
+                                                                uint32_t* __restrict__ A) {
+  __shared__ uint32_t tile[256 * 33];   // [j][m], k <= 256
+  const uint32_t m0 = blockIdx.x * 32, r = blockIdx.y;
+  const uint32_t* src = out_a + (size_t)(row0 + r) * N + m0;
+  for (uint32_t i = threadIdx.x; i < 32 * k; i += blockDim.x) tile[(i >> 5) * 33 + (i & 31)] = src[(size_t)d * (i >> 5) + (i & 31)];
+  __syncthreads();
+  uint32_t* dst = A + (size_t)r * N;
+  for (uint32_t i = threadIdx.x; i < 32 * k; i += blockDim.x) {
+    const uint32_t mm = i / k, j = k - 1 - (i % k);
+    uint32_t v = tile[j * 33 + mm];
+    int64_t c = (int64_t)k * (m0 + mm) - j;
+    if (c < 0) {
+      c += N;
+      v = v ? q0 - v : 0;
+    }
+    dst[c] = v;
+  }
+}
+// phase [rows][d] = centred (prod[r][k m] + b'_y[m]) mod q0   (prod = A_y s, coefficient form)
+__global__ void mlwe_phase_kernel(const uint32_t* __restrict__ prod, const uint32_t* __restrict__ out_b, uint32_t row0,
+                                  uint32_t rows, uint32_t d, uint32_t k, uint32_t N, uint32_t q0,
+                                  int64_t* __restrict__ phase) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < rows * d; x += gridDim.x * blockDim.x) {
+    const uint32_t r = x / d, m = x % d, y = row0 + r;
+    const uint32_t b = out_b[(size_t)(y / k) * N + (y % k) + (size_t)k * m];
+    const uint32_t v = add_mod(prod[(size_t)r * N + (size_t)k * m], b, q0);
+    phase[x] = v > q0 / 2 ? (int64_t)v - q0 : (int64_t)v;
+  }
+}
+cudaError_t launch_mlwe_rows_to_poly(const RingDims& R, const uint32_t* out_a, uint32_t row0, uint32_t rows, uint32_t* A,
+                                     cudaStream_t st) {
+  if (R.k > 256 || R.d % 32) return cudaErrorInvalidValue;
+  mlwe_rows_to_poly_kernel<<<dim3(R.d / 32, rows), 256, 0, st>>>(out_a, row0, R.d, R.k, R.N, R.q[0], A);
+  return cudaGetLastError();
+}
+cudaError_t launch_mlwe_phase(const RingDims& R, const uint32_t* prod, const uint32_t* out_b, uint32_t row0,
+                              uint32_t rows, int64_t* phase, cudaStream_t st) {
+  const uint32_t total = rows * R.d;
+  mlwe_phase_kernel<<<(total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32, 256, 0, st>>>(
+      prod, out_b, row0, rows, R.d, R.k, R.N, R.q[0], phase);
+  return cudaGetLastError();
+}
+
 }  // namespace he

@@ -130,6 +130,10 @@ cudaError_t launch_finish_encrypt(const RingDims& R, const double* acts, uint32_
                                   uint32_t n_ct, uint32_t* ct, cudaStream_t st, int layout = 0);
 cudaError_t launch_phase(const uint32_t* b, uint64_t b_stride, const uint32_t* as, uint64_t as_stride, uint32_t n,
                          uint32_t count, uint32_t q, int64_t* phase, cudaStream_t st);
+cudaError_t launch_mlwe_rows_to_poly(const RingDims& R, const uint32_t* out_a, uint32_t row0, uint32_t rows, uint32_t* A,
+                                     cudaStream_t st);
+cudaError_t launch_mlwe_phase(const RingDims& R, const uint32_t* prod, const uint32_t* out_b, uint32_t row0,
+                              uint32_t rows, int64_t* phase, cudaStream_t st);
 cudaError_t launch_decrypt_mlwe(const RingDims& R, const int32_t* s, const uint32_t* out_b, const uint32_t* out_a,
                                 uint32_t n_out, uint32_t row0, uint32_t n_rows, int64_t* phase, cudaStream_t st);
 

@@ -393,3 +393,30 @@ def test_llama_minimal_and_zero_operands(algo):
     assert np.abs(ctx.decrypt_pcmm(sk, Z)).max() < 2 ** -20
     X0 = ctx.encrypt_acts(sk, np.zeros_like(A), seed=13)
     assert np.abs(ctx.decrypt_pcmm(sk, pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W, algo=algo), X0))).max() < 2 ** -14
+
+
+@pytest.mark.parametrize("params", ["toy", "llama"])
+def test_mlwe_decryption_matches_oracle_and_direct_kernel(params):
+    """he_decrypt_mlwe (one NTT product per row through the RLWE view) gives the oracle's centred phases
+    (or_decrypt_mlwe, the O(k d^2) definition) on every row checked."""
+    import torch
+
+    from paper_2601_18511_b200 import native
+
+    P = HeParams.toy() if params == "toy" else HeParams.llama()
+    n_out, n_in = (64, 48) if params == "toy" else (512, 1024)
+    ctx, sk, A, W, X = setup(P, n_out, n_in, seed=21)
+    Y = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W), X)
+    rows = list(range(n_out)) if params == "toy" else [0, 1, 255, 256, 300, 511]
+    ph = torch.empty((n_out, P.mlwe_degree), dtype=torch.int64, device=ctx.device)
+    native.call("he_decrypt_mlwe", ctx.handle, sk.s.data_ptr(), Y.out_b.data_ptr(), Y.out_a.data_ptr(), n_out, 0, n_out,
+                ph.data_ptr(), ctx.stream())
+    got = ph.cpu().numpy()
+    d, k = P.mlwe_degree, P.mlwe_rank
+    ob, oa = u32(Y.out_b), u32(Y.out_a)
+    full = np.zeros((len(rows), P.width), np.uint32)
+    for i, y in enumerate(rows):
+        full[i, :d] = ob[y // k, y % k + k * np.arange(d)]
+        full[i, d:] = oa[y]
+    ref = O.decrypt_mlwe(P, sk.s.cpu().numpy(), full)
+    assert np.array_equal(got[rows], ref)
