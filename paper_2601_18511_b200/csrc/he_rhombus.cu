@@ -207,29 +207,43 @@ __global__ void k_rh_weights(const double* __restrict__ W, uint32_t n_out, uint3
   }
 }
 
-// rows [L][leaf][2][n] = sum_p Wpt[L][leaf][p][.] * pieces[L][p][ab][.]   (NTT domain)
+// rows [L][leaf][2][n] = sum_p Wpt[L][leaf][p][.] * pieces[L][p][ab][.]   (NTT domain); 4 coefficients per
+// thread (16-byte loads and stores: the kernel streams the 0.5-2 GB of plaintexts once)
 __global__ void k_rh_mvm(const uint32_t* __restrict__ Wpt, const uint32_t* __restrict__ pieces, uint64_t leaves,
                          uint32_t p_in, uint32_t logn, Mods M, uint32_t* __restrict__ rows) {
   const uint32_t n = 1u << logn, L = blockIdx.y;
-  const uint64_t per_l = leaves << logn;
-  for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < per_l; y += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t leaf = y >> logn;
+  const uint64_t per_l4 = (leaves << logn) >> 2;
+  const uint32_t q = M.m[L];
+  const uint64_t mu = M.mu[L];
+  for (uint64_t y4 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y4 < per_l4; y4 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t y = y4 << 2, leaf = y >> logn;
     const uint32_t c = (uint32_t)(y & (n - 1));
     const uint32_t* w = Wpt + ((size_t)L * leaves + leaf) * p_in * n + c;
     const uint32_t* pc = pieces + (size_t)L * p_in * 2 * n + c;
-    uint64_t acc_a = 0, acc_b = 0;
+    uint64_t aa[4] = {0, 0, 0, 0}, ab[4] = {0, 0, 0, 0};
     for (uint32_t p = 0; p < p_in; ++p) {
-      const uint64_t wv = w[(size_t)p * n];
-      acc_a += wv * pc[(size_t)p * 2 * n];
-      acc_b += wv * pc[(size_t)p * 2 * n + n];
-      if ((p & 7) == 7) {  // keep the sum below 2^64: 8 products < 2^63
-        acc_a = barrett64(acc_a, M.mu[L], M.m[L]);
-        acc_b = barrett64(acc_b, M.mu[L], M.m[L]);
+      const uint4 wv = __ldcs(reinterpret_cast<const uint4*>(w + (size_t)p * n));
+      const uint4 xa = __ldg(reinterpret_cast<const uint4*>(pc + (size_t)p * 2 * n));
+      const uint4 xb = __ldg(reinterpret_cast<const uint4*>(pc + (size_t)p * 2 * n + n));
+      const uint32_t wvs[4] = {wv.x, wv.y, wv.z, wv.w}, xas[4] = {xa.x, xa.y, xa.z, xa.w}, xbs[4] = {xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        aa[e] += (uint64_t)wvs[e] * xas[e];
+        ab[e] += (uint64_t)wvs[e] * xbs[e];
+      }
+      if ((p & 7) == 7) {  // keep the sums below 2^64: 8 products < 2^63
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          aa[e] = barrett64(aa[e], mu, q);
+          ab[e] = barrett64(ab[e], mu, q);
+        }
       }
     }
     uint32_t* dst = rows + (((size_t)L * leaves + leaf) * 2) * n + c;
-    dst[0] = barrett64(acc_a, M.mu[L], M.m[L]);
-    dst[n] = barrett64(acc_b, M.mu[L], M.m[L]);
+    reinterpret_cast<uint4*>(dst)[0] = make_uint4(barrett64(aa[0], mu, q), barrett64(aa[1], mu, q),
+                                                  barrett64(aa[2], mu, q), barrett64(aa[3], mu, q));
+    reinterpret_cast<uint4*>(dst + n)[0] = make_uint4(barrett64(ab[0], mu, q), barrett64(ab[1], mu, q),
+                                                      barrett64(ab[2], mu, q), barrett64(ab[3], mu, q));
   }
 }
 
@@ -249,22 +263,28 @@ __global__ void __launch_bounds__(512) k_pack_comb1(const uint32_t* __restrict__
   const uint32_t e_i = o * 2 * half + s_, o_i = e_i + half;
   const uint32_t q = M.m[L];
   const uint64_t mu = M.mu[L];
-  const uint32_t* Eb = A + (((size_t)L * cnt_in + e_i) * 2 + ab) * n;
-  const uint32_t* Ob = A + (((size_t)L * cnt_in + o_i) * 2 + ab) * n;
-  const uint32_t* ml = mono + (size_t)L * n;
-  uint32_t* un = An + (((size_t)L * cnt_out + idx) * 2 + ab) * n;
-  for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
-    const uint32_t e = Eb[c], mo = mulmod_b(Ob[c], ml[c], mu, q);
-    un[c] = add_mod(e, mo, q);
-    sd[c] = sub_mod(e, mo, q);
+  const uint4* Eb = reinterpret_cast<const uint4*>(A + (((size_t)L * cnt_in + e_i) * 2 + ab) * n);
+  const uint4* Ob = reinterpret_cast<const uint4*>(A + (((size_t)L * cnt_in + o_i) * 2 + ab) * n);
+  const uint4* ml = reinterpret_cast<const uint4*>(mono + (size_t)L * n);
+  uint4* un = reinterpret_cast<uint4*>(An + (((size_t)L * cnt_out + idx) * 2 + ab) * n);
+  // 4 coefficients per thread and step: 16-byte global and shared accesses
+  for (uint32_t c4 = threadIdx.x; c4 < n / 4; c4 += blockDim.x) {
+    const uint4 e = Eb[c4], od = Ob[c4], mm = __ldg(ml + c4);
+    const uint32_t mo0 = mulmod_b(od.x, mm.x, mu, q), mo1 = mulmod_b(od.y, mm.y, mu, q);
+    const uint32_t mo2 = mulmod_b(od.z, mm.z, mu, q), mo3 = mulmod_b(od.w, mm.w, mu, q);
+    un[c4] = make_uint4(add_mod(e.x, mo0, q), add_mod(e.y, mo1, q), add_mod(e.z, mo2, q), add_mod(e.w, mo3, q));
+    reinterpret_cast<uint4*>(sd)[c4] =
+        make_uint4(sub_mod(e.x, mo0, q), sub_mod(e.y, mo1, q), sub_mod(e.z, mo2, q), sub_mod(e.w, mo3, q));
   }
   __syncthreads();
-  uint32_t* t = T + (((size_t)L * cnt_out + idx) * 2 + ab) * n;
-  uint32_t* cc = C + ((size_t)L * cnt_out + idx) * n;
-  for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
-    const uint32_t v = sd[perm[c]];
-    t[c] = v;
-    if (ab == 0) cc[c] = v;
+  uint4* t = reinterpret_cast<uint4*>(T + (((size_t)L * cnt_out + idx) * 2 + ab) * n);
+  uint4* cc = reinterpret_cast<uint4*>(C + ((size_t)L * cnt_out + idx) * n);
+  const uint4* pp = reinterpret_cast<const uint4*>(perm);
+  for (uint32_t c4 = threadIdx.x; c4 < n / 4; c4 += blockDim.x) {
+    const uint4 pc = __ldg(pp + c4);
+    const uint4 v = make_uint4(sd[pc.x], sd[pc.y], sd[pc.z], sd[pc.w]);
+    t[c4] = v;
+    if (ab == 0) cc[c4] = v;
   }
 }
 // An += (u, T_b + w) with u = (U - LB_u) P^-1, w = (W - LB_w) P^-1   (NTT domain)
@@ -275,15 +295,26 @@ __global__ void k_pack_comb2(const uint32_t* __restrict__ UW, const uint32_t* __
   const uint64_t cnt_n = (uint64_t)cnt << logn;
   const uint32_t q = M.m[L], pinv = L ? pinv1 : pinv0;
   const uint64_t mu = M.mu[L];
-  for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < cnt_n; y += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t idx = y >> logn;
+  const uint4* U = reinterpret_cast<const uint4*>(UW + (L * 2 + 0) * cnt_n);
+  const uint4* W = reinterpret_cast<const uint4*>(UW + (L * 2 + 1) * cnt_n);
+  const uint4* LU = reinterpret_cast<const uint4*>(LB + (L * 2 + 0) * cnt_n);
+  const uint4* LW = reinterpret_cast<const uint4*>(LB + (L * 2 + 1) * cnt_n);
+  for (uint64_t y4 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y4 < cnt_n / 4; y4 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t y = y4 * 4, idx = y >> logn;
     const uint32_t c = (uint32_t)(y & (n - 1));
-    const uint32_t u = mulmod_b(sub_mod(UW[(L * 2 + 0) * cnt_n + y], LB[(L * 2 + 0) * cnt_n + y], q), pinv, mu, q);
-    const uint32_t w = mulmod_b(sub_mod(UW[(L * 2 + 1) * cnt_n + y], LB[(L * 2 + 1) * cnt_n + y], q), pinv, mu, q);
-    uint32_t* dst = An + (((size_t)L * cnt + idx) * 2) * n + c;
-    const uint32_t tb = T[(((size_t)L * cnt + idx) * 2 + 1) * n + c];
-    dst[0] = add_mod(dst[0], u, q);
-    dst[n] = add_mod(dst[n], add_mod(tb, w, q), q);
+    const uint4 u4 = U[y4], w4 = W[y4], lu = LU[y4], lw = LW[y4];
+    uint4* dst = reinterpret_cast<uint4*>(An + (((size_t)L * cnt + idx) * 2) * n + c);
+    const uint4 tb = *reinterpret_cast<const uint4*>(T + (((size_t)L * cnt + idx) * 2 + 1) * n + c);
+    const uint4 a0 = dst[0], b0 = dst[n / 4];
+    auto ua = [&](uint32_t uu, uint32_t ll, uint32_t acc) {
+      return add_mod(acc, mulmod_b(sub_mod(uu, ll, q), pinv, mu, q), q);
+    };
+    auto wb = [&](uint32_t ww, uint32_t ll, uint32_t t, uint32_t acc) {
+      return add_mod(acc, add_mod(t, mulmod_b(sub_mod(ww, ll, q), pinv, mu, q), q), q);
+    };
+    dst[0] = make_uint4(ua(u4.x, lu.x, a0.x), ua(u4.y, lu.y, a0.y), ua(u4.z, lu.z, a0.z), ua(u4.w, lu.w, a0.w));
+    dst[n / 4] = make_uint4(wb(w4.x, lw.x, tb.x, b0.x), wb(w4.y, lw.y, tb.y, b0.y), wb(w4.z, lw.z, tb.z, b0.z),
+                            wb(w4.w, lw.w, tb.w, b0.w));
   }
 }
 // shard output (level 1, no rescale), composed: out [L][ab][N], piece o at o0 + o + rho k (zeros elsewhere)
@@ -580,7 +611,7 @@ static he_status rhombus_run_impl(const he_rhombus_plan* p, const uint32_t* ct_i
   // (M) row ciphertexts
   const uint64_t leaves = leaves_of(p);
   {
-    dim3 g = grid_for(leaves * n);
+    dim3 g = grid_for(leaves * n / 4);
     g.y = 2;
     k_rh_mvm<<<g, 256, 0, st>>>(p->wpt, w.pieces, leaves, p->p_in, p->logn, p->M, w.A0);
   }
@@ -606,7 +637,7 @@ static he_status rhombus_run_impl(const he_rhombus_plan* p, const uint32_t* ct_i
     HE_CUDA(ntt_forward(c->ntt_rh[0], w.LB, 2 * cnt_out, n, st), "NTT(lift q0)");
     HE_CUDA(ntt_forward(c->ntt_rh[1], w.LB + 2 * cn, 2 * cnt_out, n, st), "NTT(lift q1)");
     {
-      dim3 g = grid_for(cn);
+      dim3 g = grid_for(cn / 4);
       g.y = 2;
       k_pack_comb2<<<g, 256, 0, st>>>(w.UW, w.LB, w.T, cnt_out, p->logn, p->M, p->pinv[0], p->pinv[1], An);
     }
@@ -1087,7 +1118,7 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
       HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2 * cnt_out, N, st), "NTT(lift q0)");
       HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2 * cn, 2 * cnt_out, N, st), "NTT(lift q1)");
       {
-        dim3 g = grid_for(cn);
+        dim3 g = grid_for(cn / 4);
         g.y = 2;
         k_pack_comb2<<<g, 256, 0, st>>>(w.UW, w.LB, w.T, cnt_out, p->logN, p->M, p->pinv[0], p->pinv[1], An);
       }
