@@ -96,46 +96,77 @@ __global__ void k_ksk_beta(const uint32_t* alpha, const uint32_t* s_new, uint32_
 //   d_i = c_i * Qhat_i^-1 mod q_i;  D[j][i] = d_i mod m_j for j != i.  D[i][i] comes from the NTT form.
 __global__ void k_modup(const uint32_t* __restrict__ c, const uint32_t* __restrict__ T, uint32_t logn, uint64_t cnt_n,
                         Mods M, uint32_t qhinv0, uint32_t qhinv1, uint32_t* __restrict__ D) {
-  // D layout: [j (3)][i (2)][cnt * n];  T layout [L][cnt][2][n] (NTT form, a part = slot 0)
+  // D layout: [j (3)][i (2)][cnt * n];  T layout [L][cnt][2][n] (NTT form, a part = slot 0).  4 words per step.
   const uint32_t q0 = M.m[0], q1 = M.m[1], P = M.m[2];
   const uint64_t nmask = (1ull << logn) - 1;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t x4 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x4 < cnt_n / 4; x4 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = x4 * 4;
     const uint64_t tix = ((x >> logn) << (logn + 1)) + (x & nmask);
-    const uint32_t d0 = mulmod_b(c[x], qhinv0, M.mu[0], q0);
-    const uint32_t d1 = mulmod_b(c[cnt_n + x], qhinv1, M.mu[1], q1);
-    D[(0 * 2 + 1) * cnt_n + x] = barrett64(d1, M.mu[0], q0);
-    D[(1 * 2 + 0) * cnt_n + x] = barrett64(d0, M.mu[1], q1);
-    D[(2 * 2 + 0) * cnt_n + x] = barrett64(d0, M.mu[2], P);
-    D[(2 * 2 + 1) * cnt_n + x] = barrett64(d1, M.mu[2], P);
+    const uint4 c0 = reinterpret_cast<const uint4*>(c)[x4], c1 = reinterpret_cast<const uint4*>(c + cnt_n)[x4];
+    const uint4 t0 = *reinterpret_cast<const uint4*>(T + tix), t1 = *reinterpret_cast<const uint4*>(T + 2 * cnt_n + tix);
+    const uint32_t d0[4] = {mulmod_b(c0.x, qhinv0, M.mu[0], q0), mulmod_b(c0.y, qhinv0, M.mu[0], q0),
+                            mulmod_b(c0.z, qhinv0, M.mu[0], q0), mulmod_b(c0.w, qhinv0, M.mu[0], q0)};
+    const uint32_t d1[4] = {mulmod_b(c1.x, qhinv1, M.mu[1], q1), mulmod_b(c1.y, qhinv1, M.mu[1], q1),
+                            mulmod_b(c1.z, qhinv1, M.mu[1], q1), mulmod_b(c1.w, qhinv1, M.mu[1], q1)};
+    auto put = [&](int slot, uint32_t a, uint32_t b, uint32_t cc, uint32_t dd) {
+      reinterpret_cast<uint4*>(D + (size_t)slot * cnt_n)[x4] = make_uint4(a, b, cc, dd);
+    };
+    put(0 * 2 + 1, barrett64(d1[0], M.mu[0], q0), barrett64(d1[1], M.mu[0], q0), barrett64(d1[2], M.mu[0], q0),
+        barrett64(d1[3], M.mu[0], q0));
+    put(1 * 2 + 0, barrett64(d0[0], M.mu[1], q1), barrett64(d0[1], M.mu[1], q1), barrett64(d0[2], M.mu[1], q1),
+        barrett64(d0[3], M.mu[1], q1));
+    put(2 * 2 + 0, barrett64(d0[0], M.mu[2], P), barrett64(d0[1], M.mu[2], P), barrett64(d0[2], M.mu[2], P),
+        barrett64(d0[3], M.mu[2], P));
+    put(2 * 2 + 1, barrett64(d1[0], M.mu[2], P), barrett64(d1[1], M.mu[2], P), barrett64(d1[2], M.mu[2], P),
+        barrett64(d1[3], M.mu[2], P));
     // own-modulus digits straight from the NTT form (NTT is linear mod q_i)
-    D[(0 * 2 + 0) * cnt_n + x] = mulmod_b(T[tix], qhinv0, M.mu[0], q0);
-    D[(1 * 2 + 1) * cnt_n + x] = mulmod_b(T[2 * cnt_n + tix], qhinv1, M.mu[1], q1);
+    put(0 * 2 + 0, mulmod_b(t0.x, qhinv0, M.mu[0], q0), mulmod_b(t0.y, qhinv0, M.mu[0], q0),
+        mulmod_b(t0.z, qhinv0, M.mu[0], q0), mulmod_b(t0.w, qhinv0, M.mu[0], q0));
+    put(1 * 2 + 1, mulmod_b(t1.x, qhinv1, M.mu[1], q1), mulmod_b(t1.y, qhinv1, M.mu[1], q1),
+        mulmod_b(t1.z, qhinv1, M.mu[1], q1), mulmod_b(t1.w, qhinv1, M.mu[1], q1));
   }
 }
 // U[j] = sum_i D[j][i] * K[i][0][j],  W[j] = sum_i D[j][i] * K[i][1][j]   (NTT domain, n a power of two)
-// K layout [i][part][j][n];  UW layout [j][2][cnt][n]
+// K layout [i][part][j][n];  UW layout [j][2][cnt][n].  4 words per step.
 __global__ void k_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict__ K, uint32_t n, uint64_t cnt_n,
                       Mods M, uint32_t* __restrict__ UW) {
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = (uint32_t)(x & (n - 1));
+  for (uint64_t x4 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x4 < cnt_n / 4; x4 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c4 = (uint32_t)((x4 * 4) & (n - 1)) / 4;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const uint64_t dd0 = D[(j * 2 + 0) * cnt_n + x], dd1 = D[(j * 2 + 1) * cnt_n + x];
-      const uint64_t u = dd0 * K[((0 * 2 + 0) * 3 + j) * (size_t)n + c] + dd1 * K[((1 * 2 + 0) * 3 + j) * (size_t)n + c];
-      const uint64_t w = dd0 * K[((0 * 2 + 1) * 3 + j) * (size_t)n + c] + dd1 * K[((1 * 2 + 1) * 3 + j) * (size_t)n + c];
-      UW[(j * 2 + 0) * cnt_n + x] = barrett64(u, M.mu[j], M.m[j]);
-      UW[(j * 2 + 1) * cnt_n + x] = barrett64(w, M.mu[j], M.m[j]);
+      const uint4 a = reinterpret_cast<const uint4*>(D + (size_t)(j * 2 + 0) * cnt_n)[x4];
+      const uint4 b = reinterpret_cast<const uint4*>(D + (size_t)(j * 2 + 1) * cnt_n)[x4];
+      const uint4 k00 = __ldg(reinterpret_cast<const uint4*>(K + ((size_t)(0 * 2 + 0) * 3 + j) * n) + c4);
+      const uint4 k10 = __ldg(reinterpret_cast<const uint4*>(K + ((size_t)(1 * 2 + 0) * 3 + j) * n) + c4);
+      const uint4 k01 = __ldg(reinterpret_cast<const uint4*>(K + ((size_t)(0 * 2 + 1) * 3 + j) * n) + c4);
+      const uint4 k11 = __ldg(reinterpret_cast<const uint4*>(K + ((size_t)(1 * 2 + 1) * 3 + j) * n) + c4);
+      const uint64_t mu = M.mu[j];
+      const uint32_t q = M.m[j];
+      auto f = [&](uint32_t d0, uint32_t d1, uint32_t x0, uint32_t x1) {
+        return barrett64((uint64_t)d0 * x0 + (uint64_t)d1 * x1, mu, q);
+      };
+      reinterpret_cast<uint4*>(UW + (size_t)(j * 2 + 0) * cnt_n)[x4] =
+          make_uint4(f(a.x, b.x, k00.x, k10.x), f(a.y, b.y, k00.y, k10.y), f(a.z, b.z, k00.z, k10.z), f(a.w, b.w, k00.w, k10.w));
+      reinterpret_cast<uint4*>(UW + (size_t)(j * 2 + 1) * cnt_n)[x4] =
+          make_uint4(f(a.x, b.x, k01.x, k11.x), f(a.y, b.y, k01.y, k11.y), f(a.z, b.z, k01.z, k11.z), f(a.w, b.w, k01.w, k11.w));
     }
   }
 }
 // ModDown, first half: centred lift of the (coefficient-form) P parts to q0, q1.  LB [j][2][cnt][n]
 __global__ void k_moddown_lift(const uint32_t* __restrict__ UWP, uint64_t cnt_n, Mods M, uint32_t* __restrict__ LB) {
   const uint32_t P = M.m[2];
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < 2 * cnt_n; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = UWP[x];
-    const int64_t c = v > P / 2 ? (int64_t)v - P : (int64_t)v;
-    LB[x] = lift_b(c, M.mu[0], M.m[0]);
-    LB[2 * cnt_n + x] = lift_b(c, M.mu[1], M.m[1]);
+  for (uint64_t x4 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x4 < cnt_n / 2; x4 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(UWP)[x4];
+    const uint32_t vs[4] = {v.x, v.y, v.z, v.w};
+    uint32_t l0[4], l1[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t c = vs[e] > P / 2 ? (int64_t)vs[e] - P : (int64_t)vs[e];
+      l0[e] = lift_b(c, M.mu[0], M.m[0]);
+      l1[e] = lift_b(c, M.mu[1], M.m[1]);
+    }
+    reinterpret_cast<uint4*>(LB)[x4] = make_uint4(l0[0], l0[1], l0[2], l0[3]);
+    reinterpret_cast<uint4*>(LB + 2 * cnt_n)[x4] = make_uint4(l1[0], l1[1], l1[2], l1[3]);
   }
 }
 
