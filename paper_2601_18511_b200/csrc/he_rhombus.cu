@@ -839,29 +839,43 @@ __global__ void __launch_bounds__(256) k_ms_mac(const uint32_t* __restrict__ D, 
                                                 uint32_t jc, uint32_t Yc, uint32_t logN, Mods M,
                                                 uint32_t* __restrict__ UW) {
   const uint32_t N = 1u << logN, mod = blockIdx.y;
-  const uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // Y * N + f
-  if (x >= ((uint64_t)Yc << logN)) return;
-  const uint32_t f = (uint32_t)(x & (N - 1));
+  const uint64_t x4 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // (Y * N + f) / 4: 4 frequencies per thread
+  if (x4 >= ((uint64_t)Yc << logN) / 4) return;
+  const uint32_t f4 = (uint32_t)((x4 * 4) & (N - 1)) / 4;
   const uint32_t q = mod == 0 ? M.m[0] : (mod == 1 ? M.m[1] : M.m[2]);
   const uint64_t mu = mod == 0 ? M.mu[0] : (mod == 1 ? M.mu[1] : M.mu[2]);
-  const size_t plane = (size_t)jc * Yc * N;
-  const uint32_t* d0 = D + (size_t)(mod * 2 + 0) * plane + x;
-  const uint32_t* d1 = D + (size_t)(mod * 2 + 1) * plane + x;
-  uint64_t au = 0, aw = 0;
+  const size_t plane4 = (size_t)jc * Yc * N / 4, yn4 = (size_t)Yc * N / 4, n4 = N / 4;
+  const uint4* d0 = reinterpret_cast<const uint4*>(D) + (size_t)(mod * 2 + 0) * plane4 + x4;
+  const uint4* d1 = reinterpret_cast<const uint4*>(D) + (size_t)(mod * 2 + 1) * plane4 + x4;
+  uint64_t au[4] = {0, 0, 0, 0}, aw[4] = {0, 0, 0, 0};
   for (uint32_t jj = 0; jj < jc; ++jj) {
-    const uint32_t* Kj = K + (size_t)jj * 12 * N + f;
-    const uint64_t x0 = __ldcs(d0 + (size_t)jj * Yc * N), x1 = __ldcs(d1 + (size_t)jj * Yc * N);
-    au += x0 * __ldg(Kj + (size_t)((0 * 2 + 0) * 3 + mod) * N) + x1 * __ldg(Kj + (size_t)((1 * 2 + 0) * 3 + mod) * N);
-    aw += x0 * __ldg(Kj + (size_t)((0 * 2 + 1) * 3 + mod) * N) + x1 * __ldg(Kj + (size_t)((1 * 2 + 1) * 3 + mod) * N);
+    const uint4* Kj = reinterpret_cast<const uint4*>(K + (size_t)jj * 12 * N) + f4;
+    const uint4 x0 = __ldcs(d0 + jj * yn4), x1 = __ldcs(d1 + jj * yn4);
+    const uint4 k00 = __ldg(Kj + ((0 * 2 + 0) * 3 + mod) * n4), k10 = __ldg(Kj + ((1 * 2 + 0) * 3 + mod) * n4);
+    const uint4 k01 = __ldg(Kj + ((0 * 2 + 1) * 3 + mod) * n4), k11 = __ldg(Kj + ((1 * 2 + 1) * 3 + mod) * n4);
+    const uint32_t a0[4] = {x0.x, x0.y, x0.z, x0.w}, a1[4] = {x1.x, x1.y, x1.z, x1.w};
+    const uint32_t u0[4] = {k00.x, k00.y, k00.z, k00.w}, u1[4] = {k10.x, k10.y, k10.z, k10.w};
+    const uint32_t w0[4] = {k01.x, k01.y, k01.z, k01.w}, w1[4] = {k11.x, k11.y, k11.z, k11.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      au[e] += (uint64_t)a0[e] * u0[e] + (uint64_t)a1[e] * u1[e];
+      aw[e] += (uint64_t)a0[e] * w0[e] + (uint64_t)a1[e] * w1[e];
+    }
     if (jj & 1) {  // two products of < 2^60 per step: reduce every second step (< 2^63)
-      au = barrett64(au, mu, q);
-      aw = barrett64(aw, mu, q);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        au[e] = barrett64(au[e], mu, q);
+        aw[e] = barrett64(aw[e], mu, q);
+      }
     }
   }
-  uint32_t* U = UW + (size_t)(mod * 2 + 0) * Yc * N + x;
-  uint32_t* W = UW + (size_t)(mod * 2 + 1) * Yc * N + x;
-  *U = add_mod(*U, barrett64(au, mu, q), q);
-  *W = add_mod(*W, barrett64(aw, mu, q), q);
+  uint4* U = reinterpret_cast<uint4*>(UW) + (size_t)(mod * 2 + 0) * yn4 + x4;
+  uint4* W = reinterpret_cast<uint4*>(UW) + (size_t)(mod * 2 + 1) * yn4 + x4;
+  const uint4 uo = *U, wo = *W;
+  *U = make_uint4(add_mod(uo.x, barrett64(au[0], mu, q), q), add_mod(uo.y, barrett64(au[1], mu, q), q),
+                  add_mod(uo.z, barrett64(au[2], mu, q), q), add_mod(uo.w, barrett64(au[3], mu, q), q));
+  *W = make_uint4(add_mod(wo.x, barrett64(aw[0], mu, q), q), add_mod(wo.y, barrett64(aw[1], mu, q), q),
+                  add_mod(wo.z, barrett64(aw[2], mu, q), q), add_mod(wo.w, barrett64(aw[3], mu, q), q));
 }
 // ModDown of the summed (U, W) (coefficient form), b += composed b', rescale by q1 -> out [Y][2][N]
 __global__ void k_ms_finish(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ raw_b, uint32_t blocks,
@@ -1098,7 +1112,7 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
                                                       qh0p, p->qhinv[1], qh1p, w.D);
         for (int mod = 0; mod < 3; ++mod)
           HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * 2 * cnt * N, 2 * cnt, N, st), "NTT(digits)");
-        k_ms_mac<<<dim3((unsigned)(((uint64_t)Yc * N + 255) / 256), 3), 256, 0, st>>>(w.D, gal + (size_t)j0 * 12 * N, p->jc,
+        k_ms_mac<<<dim3((unsigned)(((uint64_t)Yc * N / 4 + 255) / 256), 3), 256, 0, st>>>(w.D, gal + (size_t)j0 * 12 * N, p->jc,
                                                                                    Yc, p->logN, p->M, w.UW);
       }
       for (int mod = 0; mod < 3; ++mod)
