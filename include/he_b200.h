@@ -80,6 +80,12 @@ he_status he_keygen(const he_context* ctx, uint64_t seed, int32_t* s_dev, uint32
  * Block r uses RNG streams of global block index r0 + r. */
 he_status he_encrypt_acts(const he_context* ctx, const uint32_t* s_ntt_dev, const double* acts_dev, uint32_t n_in,
                           uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream);
+/* ModRaise, the hand-off to (Half-)Bootstrapping: level-0 ciphertexts mod q0
+ * [n_ct][2][N] -> the centred lift of every coefficient into each of the n_primes (<= 64) target primes
+ * (device array): out [n_ct][n_primes][2][N].  The raised phase is phase_q0 + q0 I(X) with a small integer
+ * I (the term bootstrapping's EvalMod removes). */
+he_status he_mod_raise(const he_context* ctx, const uint32_t* ct_dev, uint32_t n_ct, const uint32_t* primes_dev,
+                       uint32_t n_primes, uint32_t* out_dev, void* stream);
 /* centred phase of limb `limb` of an RLWE batch: int64 [n_ct][N] */
 he_status he_decrypt_rlwe(const he_context* ctx, const uint32_t* s_ntt_dev, const uint32_t* ct_dev, uint32_t n_ct,
                           uint32_t limbs, uint32_t limb, int64_t* phase_dev, void* stream);

@@ -16,7 +16,7 @@ from .rhombus import (CtVector, RhombusKeys, RhombusPlan, clear_pcmv, decrypt_ve
 from .slotpcmm import (BsgsSplit, PackedCt, SlotPcmmKeys, SlotPcmmPlan, clear_slot_pcmm, decrypt_packed,
                        encrypt_packed, make_slot_pcmm_plan, pcmm_slot_bsgs, pcmm_slot_depth1, slot_pcmm_keygen)
 from .graphs import OpGraph
-from .ringpack import (RingPackKeys, RingPackPlan, make_ring_pack_plan, pcmm_level1, pcmm_packed, ring_pack,
+from .ringpack import (RingPackKeys, RingPackPlan, make_ring_pack_plan, mod_raise, pcmm_level1, pcmm_packed, ring_pack,
                        ring_pack_keygen)
 
 __all__ = [
@@ -27,7 +27,7 @@ __all__ = [
     "CtVector", "RhombusKeys", "RhombusPlan", "clear_pcmv", "decrypt_vector", "encrypt_vector",
     "make_rhombus_plan", "pcmv_rhombus", "rhombus_keygen",
     "RingPackKeys", "RingPackPlan", "make_ring_pack_plan", "pcmm_level1", "pcmm_packed", "ring_pack",
-    "ring_pack_keygen",
+    "ring_pack_keygen", "mod_raise",
     "BsgsSplit", "PackedCt", "SlotPcmmKeys", "SlotPcmmPlan", "clear_slot_pcmm", "decrypt_packed", "encrypt_packed",
     "make_slot_pcmm_plan", "pcmm_slot_bsgs", "pcmm_slot_depth1", "slot_pcmm_keygen", "OpGraph",
 ]

@@ -247,6 +247,14 @@ extern "C" he_status he_encrypt_poly(const he_context* c, const uint32_t* s_ntt_
   return HE_OK;
 }
 
+extern "C" he_status he_mod_raise(const he_context* c, const uint32_t* ct_dev, uint32_t n_ct, const uint32_t* primes_dev,
+                                  uint32_t n_primes, uint32_t* out_dev, void* stream) {
+  if (!c || !ct_dev || !primes_dev || !out_dev) return fail(HE_EINVAL, "null argument");
+  if (n_ct == 0 || n_primes == 0 || n_primes > 64) return fail(HE_EINVAL, "need 1..64 target primes and >= 1 ciphertext");
+  HE_CUDA(launch_mod_raise(c->R, ct_dev, n_ct, primes_dev, n_primes, out_dev, (cudaStream_t)stream), "mod raise");
+  return HE_OK;
+}
+
 extern "C" he_status he_decrypt_rlwe(const he_context* c, const uint32_t* s_ntt_dev, const uint32_t* ct_dev,
                                      uint32_t n_ct, uint32_t limbs, uint32_t limb, int64_t* phase_dev, void* stream) {
   if (!c || !s_ntt_dev || !ct_dev || !phase_dev) return fail(HE_EINVAL, "null argument");

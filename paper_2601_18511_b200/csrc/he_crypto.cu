@@ -421,4 +421,30 @@ cudaError_t launch_mlwe_phase(const RingDims& R, const uint32_t* prod, const uin
   return cudaGetLastError();
 }
 
+// ModRaise (the Half-Bootstrap hand-off): level-0 ciphertexts mod q0 [n_ct][2][N] ->
+// the centred lift of every coefficient into each target prime: out [n_ct][n_primes][2][N]
+__global__ void mod_raise_kernel(const uint32_t* __restrict__ ct, uint64_t words, uint32_t q0,
+                                 const uint32_t* __restrict__ primes, uint32_t n_primes, uint32_t N,
+                                 uint32_t* __restrict__ out) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < words; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = x / (2ull * N), w = x % (2ull * N);
+    const uint32_t v = ct[x];
+    const int64_t c = v > q0 / 2 ? (int64_t)v - q0 : (int64_t)v;
+    for (uint32_t i = 0; i < n_primes; ++i) {
+      const int64_t p = primes[i];
+      int64_t m = c % p;
+      if (m < 0) m += p;
+      out[(r * n_primes + i) * 2ull * N + w] = (uint32_t)m;
+    }
+  }
+}
+cudaError_t launch_mod_raise(const RingDims& R, const uint32_t* ct, uint32_t n_ct, const uint32_t* primes_dev,
+                             uint32_t n_primes, uint32_t* out, cudaStream_t st) {
+  const uint64_t words = (uint64_t)n_ct * 2 * R.N;
+  const uint64_t blocks = (words + 255) / 256;
+  mod_raise_kernel<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, st>>>(ct, words, R.q[0], primes_dev,
+                                                                                      n_primes, R.N, out);
+  return cudaGetLastError();
+}
+
 }  // namespace he

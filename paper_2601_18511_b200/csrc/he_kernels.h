@@ -134,6 +134,8 @@ cudaError_t launch_mlwe_rows_to_poly(const RingDims& R, const uint32_t* out_a, u
                                      cudaStream_t st);
 cudaError_t launch_mlwe_phase(const RingDims& R, const uint32_t* prod, const uint32_t* out_b, uint32_t row0,
                               uint32_t rows, int64_t* phase, cudaStream_t st);
+cudaError_t launch_mod_raise(const RingDims& R, const uint32_t* ct, uint32_t n_ct, const uint32_t* primes_dev,
+                             uint32_t n_primes, uint32_t* out, cudaStream_t st);
 cudaError_t launch_decrypt_mlwe(const RingDims& R, const int32_t* s, const uint32_t* out_b, const uint32_t* out_a,
                                 uint32_t n_out, uint32_t row0, uint32_t n_rows, int64_t* phase, cudaStream_t st);
 

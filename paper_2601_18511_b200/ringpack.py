@@ -24,6 +24,8 @@ its PCMM (matmul.py:152-162) like the rest of this package.
 from __future__ import annotations
 
 import ctypes
+
+import numpy as np
 from dataclasses import dataclass, field
 
 from . import native
@@ -142,3 +144,18 @@ def pcmm_packed(ctx: HeContext, plan: MlwePcmmPlan, rp: RingPackPlan, keys: Ring
     Y = ring_pack(ctx, rp, keys, raw_b, raw_a, out)
     ctx.ledger.observe_level(X.level - 1)
     return Y
+
+
+def mod_raise(ctx: HeContext, Y: CtBlocks, primes) -> object:
+    """ModRaise of level-0 RLWE blocks (e.g. the packed PCMM output) into the primes of a bootstrapping
+    chain: int32 view of u32 [n_ct, len(primes), 2, N] (he_mod_raise).  The hand-off to Half-Bootstrap
+    (PAPER.md:64); the bootstrapping itself is not part of this repository."""
+    torch = _torch()
+    if Y.level != 0:
+        raise ValueError(f"ModRaise takes level-0 ciphertexts, got level {Y.level}")
+    pr = torch.as_tensor(np.asarray(primes, dtype=np.int64).astype(np.uint32).view(np.int32), device=ctx.device)
+    n_ct = int(Y.data.shape[0])
+    out = torch.empty((n_ct, len(primes), 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
+    native.call("he_mod_raise", ctx.handle, Y.data.data_ptr(), n_ct, pr.data_ptr(), len(primes), out.data_ptr(),
+                ctx.stream())
+    return out

@@ -151,3 +151,30 @@ def test_llama_packed_decrypts_to_product(n_out, n_in, method):
     err = np.abs(dec - ref).max()
     bits = -math.log2(err / np.abs(ref).max())
     assert bits >= 14, f"{bits:.1f} bits"
+
+
+def test_mod_raise_of_packed_output():
+    """ModRaise (the Half-Bootstrap hand-off): the packed level-0 output lifted into two fresh primes
+    decrypts, via CRT, to phase_q0 + q0 I(X) with a small integer I -- the form EvalMod expects."""
+    from paper_2601_18511_b200 import mod_raise
+    from paper_2601_18511_b200.params import ntt_primes
+
+    P = HeParams.toy()
+    ctx, sk, A, W, X = setup(P, 32, 48, seed=4)
+    Y = pcmm_packed(ctx, make_mlwe_pcmm_plan(ctx, W), make_ring_pack_plan(ctx, 32), ring_pack_keygen(ctx, sk, 5), X)
+    primes = [p for p in ntt_primes(2 * P.N, 1 << 30, 4) if p not in P.ks_moduli][:2]
+    R = u32(mod_raise(ctx, Y, primes))                                       # [n_ct, 2, 2, N]
+    s = sk.s.cpu().numpy()
+    q0 = P.moduli[0]
+    for b in range(R.shape[0]):
+        ph0 = O.decrypt_under(P, u32(Y.data)[b, 0, 0], u32(Y.data)[b, 0, 1], s, q0)
+        ph = [O.decrypt_under(P, R[b, i, 0], R[b, i, 1], s, p) for i, p in enumerate(primes)]
+        p1, p2 = primes
+        # CRT of the two centred residues -> the integer phase (|.| < p1 p2 / 2)
+        t = ((ph[1] - ph[0]) % p2) * pow(p1, -1, p2) % p2
+        full = ph[0].astype(object) + p1 * t.astype(object)
+        full = np.array([v - p1 * p2 if v > p1 * p2 // 2 else v for v in full], dtype=object)
+        diff = full - ph0.astype(object)
+        assert all(v % q0 == 0 for v in diff)
+        I = np.array([v // q0 for v in diff], dtype=np.int64)
+        assert np.abs(I).max() <= P.N
