@@ -260,6 +260,11 @@ he_status he_slot_pcmm_encode_pts(const he_context* ctx, const int64_t* pt_dev, 
 /* pts_ntt_dev [d][2][N] (block k = i + j b) stays caller-owned; b * g == d, d^2 <= N/2 */
 he_status he_slot_pcmm_plan_create(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t d, uint32_t b,
                                    uint32_t g, he_slot_pcmm_plan** out);
+/* general slot linear map over rotated copies: out = rescale(sum_t pt_t * rot(ct, steps[t])) with steps[0] = 0
+ * (hesim pc_linear terms, slotsim.py:330-370; rope_packed, pipeline.py:291-307); runs through
+ * he_slot_pcmm_run with keys_baby = rotation keys of steps[1..], keys_giant unused */
+he_status he_slot_lt_plan_create(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t n_terms,
+                                 const int32_t* steps, he_slot_pcmm_plan** out);
 he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* plan);
 he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* plan, uint64_t* bytes);
 /* ct_in [2][2][N] level 1 -> out [2 (a, b)][N] level 0.  keys_baby: steps i d (i = 1 .. b-1), keys_giant:

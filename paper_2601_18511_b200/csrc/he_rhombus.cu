@@ -1378,13 +1378,10 @@ extern "C" he_status he_slot_pcmm_encode_pts(const he_context* c, const int64_t*
   return HE_OK;
 }
 
-extern "C" he_status he_slot_pcmm_plan_create(const he_context* c, const uint32_t* pts_ntt_dev, uint32_t d, uint32_t b,
-                                              uint32_t g, he_slot_pcmm_plan** out) {
-  if (!c || !pts_ntt_dev || !out) return fail(HE_EINVAL, "null argument");
-  if (d == 0 || b == 0 || g == 0 || b * g != d) return fail(HE_EINVAL, "split %ux%u does not cover dim %u", b, g, d);
+// plan over rotation steps: steps[t] for the b - 1 baby and g - 1 giant rotations, in run order
+static he_status slot_plan_make(const he_context* c, const uint32_t* pts_ntt_dev, uint32_t d, uint32_t b, uint32_t g,
+                                const std::vector<uint64_t>& steps, he_slot_pcmm_plan** out) {
   const uint32_t N = c->R.N;
-  if ((uint64_t)d * d > N / 2 || (N / 2) % (d * d))
-    return fail(HE_EINVAL, "%ux%u does not tile the %u slots (d^2 must divide N/2)", d, d, N / 2);
   he_slot_pcmm_plan* p = new (std::nothrow) he_slot_pcmm_plan();
   if (!p) return fail(HE_ENOMEM, "out of host memory");
   p->ctx = c;
@@ -1403,14 +1400,12 @@ extern "C" he_status he_slot_pcmm_plan_create(const he_context* c, const uint32_
   }
   p->q1inv = (uint32_t)powmod_h(p->M.m[1] % p->M.m[0], p->M.m[0] - 2, p->M.m[0]);
   p->q1invp = shoup_pre(p->q1inv, p->M.m[0]);
-  const uint32_t nrot = (b - 1) + (g - 1);
-  std::vector<uint32_t> h((size_t)(nrot ? nrot : 1) * N);
-  for (uint32_t t = 0; t < nrot; ++t) {
-    const uint64_t r = t < b - 1 ? (uint64_t)(t + 1) * d : (uint64_t)(t - (b - 1) + 1) * b * d;
-    const uint64_t gal = powmod_h(5, r % (N / 2), 2ull * N);
+  std::vector<uint32_t> h((size_t)(steps.empty() ? 1 : steps.size()) * N);
+  for (size_t t = 0; t < steps.size(); ++t) {
+    const uint64_t gal = powmod_h(5, steps[t] % (N / 2), 2ull * N);
     for (uint32_t cc = 0; cc < N; ++cc) {
       const uint64_t e = 2ull * bitrev_h(cc, (int)p->logN) + 1;
-      h[(size_t)t * N + cc] = bitrev_h((uint32_t)(((e * gal) % (2ull * N) - 1) / 2), (int)p->logN);
+      h[t * N + cc] = bitrev_h((uint32_t)(((e * gal) % (2ull * N) - 1) / 2), (int)p->logN);
     }
   }
   if (cudaMalloc(&p->perms, h.size() * sizeof(uint32_t)) != cudaSuccess ||
@@ -1420,6 +1415,31 @@ extern "C" he_status he_slot_pcmm_plan_create(const he_context* c, const uint32_
   }
   *out = p;
   return HE_OK;
+}
+
+extern "C" he_status he_slot_pcmm_plan_create(const he_context* c, const uint32_t* pts_ntt_dev, uint32_t d, uint32_t b,
+                                              uint32_t g, he_slot_pcmm_plan** out) {
+  if (!c || !pts_ntt_dev || !out) return fail(HE_EINVAL, "null argument");
+  if (d == 0 || b == 0 || g == 0 || b * g != d) return fail(HE_EINVAL, "split %ux%u does not cover dim %u", b, g, d);
+  const uint32_t N = c->R.N;
+  if ((uint64_t)d * d > N / 2 || (N / 2) % (d * d))
+    return fail(HE_EINVAL, "%ux%u does not tile the %u slots (d^2 must divide N/2)", d, d, N / 2);
+  std::vector<uint64_t> steps;
+  for (uint32_t i = 1; i < b; ++i) steps.push_back((uint64_t)i * d);
+  for (uint32_t j = 1; j < g; ++j) steps.push_back((uint64_t)j * b * d);
+  return slot_plan_make(c, pts_ntt_dev, d, b, g, steps, out);
+}
+
+// general slot linear map out = rescale(sum_t pt_t * rot(ct, steps[t])), steps[0] = 0 (hesim pc_linear over
+// rotated copies, slotsim.py:330-370; e.g. rope_packed, pipeline.py:291-307): the BSGS run with g = 1
+extern "C" he_status he_slot_lt_plan_create(const he_context* c, const uint32_t* pts_ntt_dev, uint32_t n_terms,
+                                            const int32_t* steps, he_slot_pcmm_plan** out) {
+  if (!c || !pts_ntt_dev || !steps || !out) return fail(HE_EINVAL, "null argument");
+  if (n_terms == 0 || steps[0] != 0) return fail(HE_EINVAL, "need >= 1 term and steps[0] == 0");
+  const int64_t half = c->R.N / 2;
+  std::vector<uint64_t> st;
+  for (uint32_t t = 1; t < n_terms; ++t) st.push_back((uint64_t)((steps[t] % half + half) % half));
+  return slot_plan_make(c, pts_ntt_dev, n_terms, n_terms, 1, st, out);
 }
 
 extern "C" he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* p) {

@@ -250,3 +250,71 @@ def decrypt_packed(ctx: HeContext, sk: SecretKey, Y: PackedCt) -> np.ndarray:
                 ctx.stream())
     z = slots.decode(ph[0].cpu().numpy(), ctx.params.N, ctx.params.delta, Y.dim * Y.dim)
     return z.reshape(Y.dim, Y.dim)
+
+
+# ---------------------------------------------------------------- general slot linear maps (pc_linear over rotations)
+def make_slot_linear_plan(ctx: HeContext, masks, steps) -> SlotPcmmPlan:
+    """out = rescale(sum_t masks[t] * rot(ct, steps[t])), steps[0] = 0: hesim's pc_linear over rotated
+    copies (slotsim.py:330-370) as one device op (he_slot_lt_plan_create + he_slot_pcmm_run); masks are
+    slot vectors (tiled) encoded at scale q1."""
+    torch = _torch()
+    steps = [int(v) for v in steps]
+    if len(masks) != len(steps) or not steps or steps[0] != 0:
+        raise ValueError("need one mask per step and steps[0] == 0")
+    N = ctx.params.N
+    pt = torch.from_numpy(np.stack([slots.encode(np.asarray(m, float).reshape(-1), N, float(ctx.params.delta_w))
+                                    for m in masks])).to(ctx.device)
+    n = len(steps)
+    plan = SlotPcmmPlan(n, 0, BsgsSplit(n, 1), np.zeros((0, 0)))
+    plan.pts = torch.empty((n, 2, N), dtype=torch.int32, device=ctx.device)
+    native.call("he_slot_pcmm_encode_pts", ctx.handle, pt.data_ptr(), n, plan.pts.data_ptr(), ctx.stream())
+    arr = (ctypes.c_int32 * n)(*steps)
+    h = ctypes.c_void_p()
+    native.call("he_slot_lt_plan_create", ctx.handle, plan.pts.data_ptr(), n, arr, ctypes.byref(h))
+    plan._handle = h
+    plan.steps = tuple(steps)
+    return plan
+
+
+def slot_linear_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: int) -> SlotPcmmKeys:
+    torch = _torch()
+    N = ctx.params.N
+    st = list(plan.steps[1:])
+    keys = torch.empty((max(len(st), 1), 4, 2, 3, N), dtype=torch.int32, device=ctx.device)
+    if st:
+        arr = (ctypes.c_int32 * len(st))(*st)
+        native.call("he_slot_rotation_keygen", ctx.handle, seed, sk.s.data_ptr(), arr, len(st), keys.data_ptr(),
+                    ctx.stream())
+    return SlotPcmmKeys(keys, keys[:1], tuple(st))
+
+
+def slot_linear(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, X: PackedCt) -> PackedCt:
+    torch = _torch()
+    if not isinstance(X, PackedCt):
+        raise TypeError("slot_linear consumes a ciphertext operand")
+    require_level(X.level)
+    if X.level != 1:
+        raise ValueError(f"slot linear maps run at level 1, operand is at level {X.level}")
+    out = torch.empty((1, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
+    ws = plan.workspace(ctx.device)
+    led = native.HeLedgerC()
+    native.call("he_slot_pcmm_run", plan._handle, X.data.data_ptr(), X.level, keys.baby.data_ptr(), keys.giant.data_ptr(),
+                out.data_ptr(), ws.data_ptr(), ws.numel() * 4, ctx.stream(), ctypes.byref(led))
+    ctx.ledger.add_c(led)
+    ctx.ledger.observe_level(X.level - 1)
+    return PackedCt(out, level=X.level - 1, dim=X.dim, shear_power=X.shear_power)
+
+
+def rope_masks(d: int, positions) -> tuple:
+    """pipeline.py:280-288: cos/sin masks for column-packed vectors (dimension i, token j)."""
+    th = np.asarray(positions, float)[:, None] * (10.0 ** (-4.0 * np.arange(d // 2) / d))[None, :]
+    c = np.vstack([th.T, th.T])
+    cos, sin = np.cos(c), np.sin(c)
+    sin[: d // 2] *= -1.0
+    return cos, sin
+
+
+def make_rope_plan(ctx: HeContext, d: int, positions, shear_power: int) -> SlotPcmmPlan:
+    """hesim rope_packed (pipeline.py:291-307): cos * x + sin * rowrot(x, d/2) -- one rotation, one level."""
+    cos, sin = rope_masks(d, positions)
+    return make_slot_linear_plan(ctx, [col_shear(cos, shear_power), col_shear(sin, shear_power)], [0, (d // 2) * d])

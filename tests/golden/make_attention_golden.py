@@ -6,7 +6,9 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
-from hesim.pipeline import clear_pc_attention, rope_columns  # noqa: E402
+from hesim import SimParams, SlotContext  # noqa: E402
+from hesim.packing import pack_sheared, unpack_matrix  # noqa: E402
+from hesim.pipeline import clear_pc_attention, rope_columns, rope_packed  # noqa: E402
 
 out = {}
 for d, seed in ((8, 0), (16, 1), (64, 2)):
@@ -18,5 +20,7 @@ for d, seed in ((8, 0), (16, 1), (64, 2)):
     positions = d + np.arange(d)
     out[f"d{d}_q"], out[f"d{d}_k"], out[f"d{d}_v"] = q, k_pub, v_pub
     out[f"d{d}_out"] = clear_pc_attention(q, k_pub, v_pub, positions)
+    ctx = SlotContext(SimParams(slot_count=max(64, d * d)))
+    out[f"d{d}_rope2"] = unpack_matrix(rope_packed(ctx, pack_sheared(ctx, q, 2), positions).payload.slots, d)
 np.savez(Path(__file__).with_name("attention_golden.npz"), **out)
 print("wrote", sorted(out))
