@@ -1,0 +1,85 @@
+"""Error contract of the newer entry points (the reference's matmul.py:139-149 rules: TypeError for a
+non-ciphertext operand, ValueError for shape/layout/level misuse, NeedsBootstrapError when no level is
+left), raised before any launch, and the C ABI's status codes surfacing as those exceptions."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2601_18511_b200 import (CtBlocks, HeContext, HeParams, make_mlwe_pcmm_plan, make_ring_pack_plan, mod_raise,
+                                   native, pcmm_level1, pcmm_packed, ring_pack_keygen)
+from paper_2601_18511_b200.errors import NeedsBootstrapError
+from paper_2601_18511_b200.rhombus import encrypt_vector, make_rhombus_plan, pcmv_rhombus_shard, rhombus_keygen
+from paper_2601_18511_b200.slotpcmm import PackedCt, encrypt_packed, make_rope_plan, slot_linear, slot_linear_keygen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def toy():
+    P = HeParams.toy()
+    ctx = HeContext(P)
+    sk = ctx.keygen(7)
+    rng = np.random.default_rng(0)
+    W = rng.uniform(-1, 1, (32, 32)) / 8
+    X = ctx.encrypt_acts(sk, rng.uniform(-1, 1, (P.tokens, 32)), seed=1)
+    return P, ctx, sk, W, X
+
+
+def test_packed_op_levels_and_types(toy):
+    P, ctx, sk, W, X = toy
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    rp = make_ring_pack_plan(ctx, 32)
+    keys = ring_pack_keygen(ctx, sk, 3)
+    with pytest.raises(TypeError):
+        pcmm_packed(ctx, plan, rp, keys, X.data)
+    with pytest.raises(NeedsBootstrapError):
+        pcmm_level1(ctx, plan, CtBlocks(X.data, level=0, n_cols=32))
+    with pytest.raises(ValueError, match="layout mismatch"):
+        pcmm_level1(ctx, plan, CtBlocks(X.data, level=1, n_cols=32, layout="rhombus_h"))
+    Y = pcmm_packed(ctx, plan, rp, keys, X)
+    with pytest.raises(ValueError):
+        mod_raise(ctx, X, [1073707009])          # level 1: ModRaise takes level-0 ciphertexts
+    assert tuple(mod_raise(ctx, Y, [1073707009]).shape) == (2, 1, 2, P.N)
+
+
+def test_rhombus_shard_offsets_checked(toy):
+    P, ctx, sk, W, X = toy
+    keys = rhombus_keygen(ctx, sk, 9)
+    x = encrypt_vector(ctx, sk, np.ones(32) / 4, seed=2)
+    plan = make_rhombus_plan(ctx, W)
+    with pytest.raises(ValueError, match="exceed"):
+        pcmv_rhombus_shard(ctx, plan, keys, x, piece0=P.N // P.rhombus_degree)   # past the last input piece
+    part = pcmv_rhombus_shard(ctx, plan, keys, x)
+    assert tuple(part.shape) == (2, 2, P.N)
+
+
+def test_slot_linear_levels(toy):
+    P, ctx, sk, W, X = toy
+    plan = make_rope_plan(ctx, 16, 16 + np.arange(16), shear_power=2)
+    keys = slot_linear_keygen(ctx, sk, plan, 4)
+    Xp = encrypt_packed(ctx, sk, np.eye(16) / 4, 2, seed=5)
+    with pytest.raises(TypeError):
+        slot_linear(ctx, plan, keys, Xp.data)
+    with pytest.raises(NeedsBootstrapError):
+        slot_linear(ctx, plan, keys, PackedCt(Xp.data, level=0, dim=16, shear_power=2))
+    assert slot_linear(ctx, plan, keys, Xp).level == 0
+
+
+def test_c_abi_status_codes(toy):
+    P, ctx, sk, W, X = toy
+    h = ctypes.c_void_p()
+    with pytest.raises(ValueError):        # n_out not a multiple of k
+        native.call("he_ring_pack_plan_create", ctx.handle, 24, 0, ctypes.byref(h))
+    with pytest.raises(ValueError):        # unknown packing method
+        native.call("he_ring_pack_plan_create", ctx.handle, 32, 7, ctypes.byref(h))
+    with pytest.raises(ValueError):        # split does not cover d
+        native.call("he_slot_pcmm_plan_create", ctx.handle, X.data.data_ptr(), 16, 3, 5, ctypes.byref(h))
+    with pytest.raises(ValueError):        # steps[0] must be 0
+        arr = (ctypes.c_int32 * 2)(1, 2)
+        native.call("he_slot_lt_plan_create", ctx.handle, X.data.data_ptr(), 2, arr, ctypes.byref(h))
+    with pytest.raises(ValueError):        # no primes
+        native.call("he_mod_raise", ctx.handle, X.data.data_ptr(), 1, X.data.data_ptr(), 0, X.data.data_ptr(),
+                    ctx.stream())
+    torch.cuda.synchronize()
