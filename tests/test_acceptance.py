@@ -10,6 +10,9 @@ per test, each with a hard wall-clock budget (check_budget, test_acceptance.py:4
   a07  App. A index maps equal the reference's bitrev tables           (CPU)
   a08  oracle float semantics equal hesim's clear_pcmm / pcmm_bsgs      (CPU)
   a09  row-sharded gather reassembles the unsharded output exactly     (CPU, gloo)
+  a10  slot-domain PCMM at d = 16: BSGS spends 6 rotations, depth-1 15 (reference c03,
+       test_acceptance.py:79-90), one level each, both decrypt to clear_pcmm
+  a11  ring packing: the packed level-0 output decrypts to A W^T in the input's own layout
 """
 
 import time
@@ -124,3 +127,50 @@ def test_a09_row_sharded_gather_exact():
     t0 = time.perf_counter()
     T.test_row_sharded_pcmm_gathers_exact_output(2, 64)
     check_budget(t0, 120)
+
+
+@pytest.mark.gpu
+def test_a10_slot_pcmm_rotation_counts_like_reference_c03():
+    from paper_2601_18511_b200 import HeContext, HeParams
+    from paper_2601_18511_b200.slotpcmm import (BsgsSplit, clear_slot_pcmm, decrypt_packed, encrypt_packed,
+                                                make_slot_pcmm_plan, pcmm_slot_bsgs, pcmm_slot_depth1,
+                                                slot_pcmm_keygen)
+
+    t0 = time.perf_counter()
+    P = HeParams.toy()
+    ctx = HeContext(P)
+    sk = ctx.keygen(1)
+    rng = np.random.default_rng(3)
+    d = 16
+    W, B = rng.uniform(-1, 1, (d, d)) / 4, rng.uniform(-1, 1, (d, d))
+    X = encrypt_packed(ctx, sk, B, 1, seed=2)
+    rots = {}
+    for name, split, fn in (("bsgs", None, pcmm_slot_bsgs), ("depth1", BsgsSplit(d, 1), pcmm_slot_depth1)):
+        plan = make_slot_pcmm_plan(ctx, W, shear_power=0, split=split)
+        keys = slot_pcmm_keygen(ctx, sk, plan, 5)
+        snap = ctx.ledger.snapshot()
+        Y = fn(ctx, plan, keys, X)
+        diff = ctx.ledger.diff(snap)
+        rots[name] = diff["ct_rotations"]
+        assert X.level - Y.level == 1 and diff["rescales"] == 1
+        assert np.abs(decrypt_packed(ctx, sk, Y) - clear_slot_pcmm(W, B, 0)).max() < 2 ** -13
+    assert rots == {"bsgs": 6, "depth1": 15}
+    check_budget(t0, 60)
+
+
+@pytest.mark.gpu
+def test_a11_ring_packed_output_decrypts_in_input_layout():
+    from paper_2601_18511_b200 import (HeContext, HeParams, make_mlwe_pcmm_plan, make_ring_pack_plan, pcmm_packed,
+                                       ring_pack_keygen)
+
+    t0 = time.perf_counter()
+    P = HeParams.toy()
+    ctx = HeContext(P)
+    sk = ctx.keygen(1)
+    rng = np.random.default_rng(4)
+    A, W = rng.uniform(-1, 1, (P.tokens, 48)), rng.uniform(-1, 1, (64, 48)) / 8
+    Y = pcmm_packed(ctx, make_mlwe_pcmm_plan(ctx, W), make_ring_pack_plan(ctx, 64), ring_pack_keygen(ctx, sk, 2),
+                    ctx.encrypt_acts(sk, A, seed=3))
+    assert Y.level == 0 and Y.layout == "app_a_coeff" and Y.n_cols == 64
+    assert np.abs(ctx.decrypt_acts(sk, Y) - A @ W.T).max() < 2 ** -14
+    check_budget(t0, 60)
