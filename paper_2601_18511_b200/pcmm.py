@@ -27,6 +27,7 @@ Work split (all on the device, through the C ABI in include/he_b200.h):
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -330,8 +331,23 @@ def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_hos
         raise ValueError("host output buffers have the wrong shape")
     dev = ctx.device
     st = torch.cuda.current_stream(dev)
-    if x_host is not None:
+    if x_host is not None and os.environ.get("HE_E2E_SERIAL_H2D"):   # measurement knob: the unoverlapped order
         X.data.copy_(x_host, non_blocking=True)
+        x_host = None
+    if x_host is not None:
+        # the input goes up on its own stream: it only waits until the previous call's decompose has read
+        # X.data, so back-to-back calls overlap it with the previous call's device->host tail (the two
+        # directions use separate copy engines)
+        if getattr(plan, "_h2d_stream", None) is None:
+            plan._h2d_stream = torch.cuda.Stream(dev)
+        hs = plan._h2d_stream
+        if getattr(plan, "_x_consumed", None) is not None:
+            hs.wait_event(plan._x_consumed)
+        with torch.cuda.stream(hs):
+            X.data.copy_(x_host, non_blocking=True)
+        up = torch.cuda.Event()
+        up.record(hs)
+        st.wait_event(up)
     ws = plan.workspace(dev)
     if getattr(plan, "_stream_bufs", None) is None or plan._stream_bufs[0][1].shape[0] != chunk_rows:
         plan._stream_bufs = [(torch.empty((chunk_rows // k, N), dtype=torch.int32, device=dev),
@@ -339,6 +355,8 @@ def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_hos
         plan._copy_stream = torch.cuda.Stream(dev)
     cs = plan._copy_stream
     native.call("he_pcmm_decompose", plan._handle, X.data.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+    plan._x_consumed = torch.cuda.Event()
+    plan._x_consumed.record(st)
     copied = [None, None]
     # a short first chunk starts the device->host stream sooner (the copies, not the compute, set the pace)
     first = min(256, chunk_rows) if plan.n_out > chunk_rows else chunk_rows
