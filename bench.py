@@ -64,7 +64,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="testing only: gloo with --one-device runs the N > 1 code path with every rank on cuda:0")
     ap.add_argument("--one-device", action="store_true", help="testing only: all ranks share cuda:0")
-    ap.add_argument("--cpu-rows", type=int, default=64, help="oracle sample rows for cpu_baseline (0: skip)")
+    ap.add_argument("--cpu-rows", type=int, default=256,
+                    help="oracle sample rows for cpu_baseline: 256 = one output block, ~10 s on 16 host threads (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the Rhombus PCMv / NTT side measurements")
@@ -728,7 +729,7 @@ def run_reference(a, rank: int, world: int):
     s = O.keygen(P, 7)
     ct = O.encrypt(P, 11, s, O.encode_acts(P, A))
     Wt = O.encode_weights(P, W0)
-    rows = max(1, min(a.cpu_rows, k) // 4)
+    rows = max(1, min(a.cpu_rows, k) // 16)
     for _ in range(a.warmup):
         O.pcmm(P, Wt, ct, rows=list(range(1)), cols=list(range(64)))
     vals = []
