@@ -8,6 +8,13 @@
 //   (R)(C)         : rescale by q1 and the free X^rho interleave back to degree N.
 // Every stage is a batched kernel launch (all combines of a packing level at once) around the K2
 // NTT; nothing runs on the host but the launch sequence.
+//
+// The file also holds the other key-switching paths, which share the hybrid-key machinery above:
+//   - MLWE -> RLWE ring packing of the PCMM output (he_ring_pack_*: key-switch and trace methods),
+//   - the slot-domain BSGS PCMM and general slot linear maps (he_slot_*: hoisted rotations with
+//     gadget keys),
+//   - multi-GPU shards of the PCMv (he_rhombus_run_shard / he_rhombus_combine).
+// Each is restated in oracle/he_oracle_rhombus.c and bit-exact with it.
 #include <vector>
 
 #include "he_common.cuh"
