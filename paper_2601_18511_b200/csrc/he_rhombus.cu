@@ -1273,16 +1273,23 @@ __global__ void k_sd_inner(const uint32_t* __restrict__ baby, const uint32_t* __
                            Mods M, uint32_t* __restrict__ inner) {
   const uint32_t L = blockIdx.y, j = blockIdx.z, q = M.m[L];
   const uint64_t mu = M.mu[L];
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
-    uint64_t aa = 0, ab = 0;
+  for (uint32_t c4 = blockIdx.x * blockDim.x + threadIdx.x; c4 < N / 4; c4 += gridDim.x * blockDim.x) {
+    uint64_t aa[4] = {0, 0, 0, 0}, ab[4] = {0, 0, 0, 0};   // 4 coefficients per thread: 16-byte accesses
     for (uint32_t i = 0; i < b; ++i) {
-      const uint64_t p = pts[((size_t)(i + j * b) * 2 + L) * N + c];
-      const uint32_t* bi = baby + ((size_t)i * 4 + L * 2) * N + c;
-      aa = barrett64(aa + p * bi[0], mu, q);
-      ab = barrett64(ab + p * bi[N], mu, q);
+      const uint4 p = __ldg(reinterpret_cast<const uint4*>(pts + ((size_t)(i + j * b) * 2 + L) * N) + c4);
+      const uint4 x = reinterpret_cast<const uint4*>(baby + ((size_t)i * 4 + L * 2) * N)[c4];
+      const uint4 y = reinterpret_cast<const uint4*>(baby + ((size_t)i * 4 + L * 2 + 1) * N)[c4];
+      const uint32_t ps[4] = {p.x, p.y, p.z, p.w}, xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        aa[e] = barrett64(aa[e] + (uint64_t)ps[e] * xs[e], mu, q);
+        ab[e] = barrett64(ab[e] + (uint64_t)ps[e] * ys[e], mu, q);
+      }
     }
-    inner[((size_t)j * 4 + L * 2 + 0) * N + c] = (uint32_t)aa;
-    inner[((size_t)j * 4 + L * 2 + 1) * N + c] = (uint32_t)ab;
+    reinterpret_cast<uint4*>(inner + ((size_t)j * 4 + L * 2 + 0) * N)[c4] =
+        make_uint4((uint32_t)aa[0], (uint32_t)aa[1], (uint32_t)aa[2], (uint32_t)aa[3]);
+    reinterpret_cast<uint4*>(inner + ((size_t)j * 4 + L * 2 + 1) * N)[c4] =
+        make_uint4((uint32_t)ab[0], (uint32_t)ab[1], (uint32_t)ab[2], (uint32_t)ab[3]);
   }
 }
 // acc [L][ab][N] = inner_0 + sum_{z < cnt} rot_z
