@@ -265,6 +265,11 @@ he_status he_slot_pcmm_plan_create(const he_context* ctx, const uint32_t* pts_nt
  * he_slot_pcmm_run with keys_baby = rotation keys of steps[1..], keys_giant unused */
 he_status he_slot_lt_plan_create(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t n_terms,
                                  const int32_t* steps, he_slot_pcmm_plan** out);
+/* general BSGS slot linear map over n = b * g diagonals (SlotToCoeffs, PAPER.md:639-643 + App. A bit-reversal;
+ * no reference interface -- hesim has no StC): baby steps i * stride, giant steps j * b * stride; pts_ntt_dev
+ * [b g][2][N] in order i + j b, diagonal i + j b pre-rotated by -j b stride; runs through he_slot_pcmm_run */
+he_status he_slot_bsgs_plan_create(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t b, uint32_t g,
+                                   uint32_t stride, he_slot_pcmm_plan** out);
 he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* plan);
 he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* plan, uint64_t* bytes);
 /* ct_in [2][2][N] level 1 -> out [2 (a, b)][N] level 0.  keys_baby: steps i d (i = 1 .. b-1), keys_giant:

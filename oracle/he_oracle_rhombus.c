@@ -240,8 +240,8 @@ static void pack_rec(const uint32_t* const* v, uint32_t count, uint32_t sb, uint
     return;
   }
   const uint32_t half = count / 2;
-  const uint32_t** ev = (const uint32_t**)malloc(sizeof(void*) * half);
-  const uint32_t** od = (const uint32_t**)malloc(sizeof(void*) * half);
+  const uint32_t** ev = (const uint32_t**)calloc(half, sizeof(void*));
+  const uint32_t** od = (const uint32_t**)calloc(half, sizeof(void*));
   for (uint32_t i = 0; i < half; ++i) {
     ev[i] = v[2 * i];
     od[i] = v[2 * i + 1];
@@ -630,12 +630,13 @@ static void rotate_with_digits(const uint32_t* ct, const uint32_t* D, uint32_t n
   free(sb);
 }
 /*
- * ct_in [2][2][N] level 1; pts [d][2 limbs][N] coefficient form mod q_L (block k = i + j b);
+ * BSGS slot linear map with stride d (d = block dim for the PCMM, 1 for SlotToCoeffs):
+ * ct_in [2][2][N] level 1; pts [b g][2 limbs][N] coefficient form mod q_L (term k = i + j b);
  * keys_baby [b-1][4][2][3][N] (gadget keys) for steps i d, keys_giant [g-1][..] for steps j b d; out [2][N].
  */
-int or_slot_pcmm(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t g, const uint32_t* ct_in,
+int or_slot_bsgs(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t g, const uint32_t* ct_in,
                  const uint32_t* pts, const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out) {
-  if (b * g != d) return 1;
+  if ((uint64_t)b * g * d > N / 2) return 1;
   const size_t cw = (size_t)4 * N;
   uint32_t* D = (uint32_t*)malloc(sizeof(uint32_t) * 6 * SD * N);
   uint32_t* a_in = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
@@ -686,4 +687,11 @@ int or_slot_pcmm(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t
   free(rot);
   free(t);
   return 0;
+}
+
+/* hesim pcmm_bsgs (matmul.py:165-176): the BSGS map with stride d over the d blocks */
+int or_slot_pcmm(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t g, const uint32_t* ct_in,
+                 const uint32_t* pts, const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out) {
+  if (b * g != d) return 1;
+  return or_slot_bsgs(N, m, d, b, g, ct_in, pts, keys_baby, keys_giant, out);
 }

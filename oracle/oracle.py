@@ -19,6 +19,7 @@ __all__ = [
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
     "decode_vector", "rhombus_pcmv", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
     "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe", "rotation_keys", "slot_pcmm",
+    "slot_bsgs",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -572,6 +573,8 @@ def _sd_bind():
         L.or_rotation_ksk.argtypes = [u64, u32, i32p, u32, u32p, u32p]
         L.or_slot_pcmm.restype = ctypes.c_int
         L.or_slot_pcmm.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
+        L.or_slot_bsgs.restype = ctypes.c_int
+        L.or_slot_bsgs.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
         L._sd_bound = True
     return L
 
@@ -600,4 +603,20 @@ def slot_pcmm(params, ct_in: np.ndarray, pts: np.ndarray, d: int, b: int, g: int
                                  _u32(np.ascontiguousarray(pts, dtype=np.uint32)), _u32(kb), _u32(kg), _u32(out))
     if rc:
         raise ValueError("slot_pcmm: split does not cover d")
+    return out
+
+
+def slot_bsgs(params, ct_in: np.ndarray, pts: np.ndarray, stride: int, b: int, g: int, keys_baby,
+              keys_giant) -> np.ndarray:
+    """or_slot_bsgs: the general BSGS slot map (baby steps i stride, giant steps j b stride) -- SlotToCoeffs
+    with stride 1.  pts [b g, 2, N] residues (coefficient form) -> [2, N] level 0."""
+    N = params.N
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    out = np.zeros((2, N), np.uint32)
+    kb = np.ascontiguousarray(keys_baby if len(keys_baby) else np.zeros((1, 4, 2, 3, N), np.uint32), dtype=np.uint32)
+    kg = np.ascontiguousarray(keys_giant if len(keys_giant) else np.zeros((1, 4, 2, 3, N), np.uint32), dtype=np.uint32)
+    rc = _sd_bind().or_slot_bsgs(N, _u32(m), stride, b, g, _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
+                                 _u32(np.ascontiguousarray(pts, dtype=np.uint32)), _u32(kb), _u32(kg), _u32(out))
+    if rc:
+        raise ValueError("slot_bsgs: split x stride exceeds the slots")
     return out

@@ -1456,6 +1456,20 @@ extern "C" he_status he_slot_lt_plan_create(const he_context* c, const uint32_t*
   return slot_plan_make(c, pts_ntt_dev, n_terms, n_terms, 1, st, out);
 }
 
+// general BSGS slot linear map over n = b g diagonals: baby steps i * stride (i < b), giant steps j * b * stride
+// (j < g); pts in kernel order i + j b, each already rotated by -j b stride (e.g. SlotToCoeffs: stride 1, n = N/2)
+extern "C" he_status he_slot_bsgs_plan_create(const he_context* c, const uint32_t* pts_ntt_dev, uint32_t b, uint32_t g,
+                                              uint32_t stride, he_slot_pcmm_plan** out) {
+  if (!c || !pts_ntt_dev || !out) return fail(HE_EINVAL, "null argument");
+  const uint64_t half = c->R.N / 2;
+  if (b == 0 || g == 0 || stride == 0 || (uint64_t)b * g * stride > half)
+    return fail(HE_EINVAL, "split %ux%u with stride %u exceeds the %llu slots", b, g, stride, (unsigned long long)half);
+  std::vector<uint64_t> steps;
+  for (uint32_t i = 1; i < b; ++i) steps.push_back((uint64_t)i * stride);
+  for (uint32_t j = 1; j < g; ++j) steps.push_back((uint64_t)j * b * stride);
+  return slot_plan_make(c, pts_ntt_dev, b * g, b, g, steps, out);
+}
+
 extern "C" he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* p) {
   if (p) {
     if (p->perms) cudaFree(p->perms);

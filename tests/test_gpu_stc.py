@@ -1,0 +1,102 @@
+"""SlotToCoeffs on the GPU: bit-exact against the integer oracle (or_slot_bsgs, stride 1)
+at toy size, decrypting to the App. A coefficient layout the MLWE PCMM consumes (decrypt_acts), the ledger
+and error contract; at N = 2^16 (32 768 slots, 256 x 128 BSGS) the decryption matches the activations."""
+import time
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2601_18511_b200 import HeContext, HeParams, slots
+from paper_2601_18511_b200.errors import NeedsBootstrapError
+from paper_2601_18511_b200.pcmm import make_mlwe_pcmm_plan, pcmm_mlwe
+from paper_2601_18511_b200.stc import (SlotBlocks, encrypt_slots, make_slot_to_coeffs_plan, slot_to_coeffs,
+                                       slot_to_coeffs_keygen, slot_vectors, stc_plaintexts)
+
+pytestmark = pytest.mark.gpu
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def test_toy_bit_exact_and_layout():
+    P = HeParams.toy()
+    ctx = HeContext(P)
+    sk = ctx.keygen(7)
+    d, k, N, n = P.mlwe_degree, P.mlwe_rank, P.N, P.N // 2
+    A = np.random.default_rng(3).uniform(-1, 1, (d // 2, 2 * k))
+    plan = make_slot_to_coeffs_plan(ctx)
+    b, g = plan.split.baby, plan.split.giant
+    keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=13)
+    X = encrypt_slots(ctx, sk, A, seed=11)
+    before = ctx.ledger.snapshot()
+    Y = slot_to_coeffs(ctx, plan, keys, X)
+    diff = ctx.ledger.diff(before)
+    assert diff["ct_rotations"] == 2 * ((b - 1) + (g - 1)) and diff["pc_mults"] == 2 * n and diff["rescales"] == 2
+    assert Y.level == 0 and Y.layout == "app_a_coeff" and Y.n_cols == 2 * k
+    # the oracle on the same integers (ct 0)
+    s = O.keygen(P, 7)
+    ct = O.encrypt(P, 11, s, slots.encode(slot_vectors(P, A)[0], N, P.delta)[None])[0]
+    assert np.array_equal(u32(X.data[0]), ct)
+    pt = stc_plaintexts(P, plan.split, 0, n).numpy()
+    pts = np.stack([np.stack([(pt[t] % q).astype(np.uint32) for q in P.moduli]) for t in range(n)])
+    want = O.slot_bsgs(P, ct, pts, 1, b, g, O.rotation_keys(P, 13, s, list(range(1, b))),
+                       O.rotation_keys(P, 13, s, [j * b for j in range(1, g)]))
+    got = u32(Y.data[0, 0])
+    assert np.array_equal(got, want), f"{int((got != want).sum())} words differ"
+    # decrypts to the App. A coefficient layout of A: exactly what encrypt_acts encodes
+    np.testing.assert_allclose(ctx.decrypt_acts(sk, Y), A, atol=2.0 ** -14)
+    ph = ctx.decrypt_phase(sk, Y).cpu().numpy()
+    assert np.abs(ph - O.encode_acts(P, A)).max() < P.delta * 2.0 ** -14
+
+
+def test_error_contract():
+    P = HeParams.toy()
+    ctx = HeContext(P)
+    sk = ctx.keygen(7)
+    plan = make_slot_to_coeffs_plan(ctx)
+    keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=13)
+    A = np.zeros((P.mlwe_degree // 2, P.mlwe_rank))
+    with pytest.raises(TypeError):
+        slot_to_coeffs(ctx, plan, keys, ctx.encrypt_acts(sk, A, seed=1))      # already coefficient-encoded
+    X = encrypt_slots(ctx, sk, A, seed=1)
+    Y = slot_to_coeffs(ctx, plan, keys, X)
+    with pytest.raises(NeedsBootstrapError):
+        slot_to_coeffs(ctx, plan, keys, SlotBlocks(Y.data, level=0, n_cols=Y.n_cols))
+    # the StC output carries the PCMM's layout tag but no level left on this two-prime chain
+    W = np.eye(P.mlwe_rank)
+    with pytest.raises(NeedsBootstrapError):
+        pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W), Y)
+    with pytest.raises(ValueError):
+        encrypt_slots(ctx, sk, np.zeros((3, P.mlwe_rank)), seed=1)
+
+
+def test_llama_ring():
+    import torch
+
+    P = HeParams()
+    ctx = HeContext(P)
+    sk = ctx.keygen(7)
+    d, k = P.mlwe_degree, P.mlwe_rank
+    t0 = time.perf_counter()
+    plan = make_slot_to_coeffs_plan(ctx)
+    keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=13)
+    torch.cuda.synchronize()
+    t_plan = time.perf_counter() - t0
+    A = np.random.default_rng(4).uniform(-1, 1, (d // 2, 2 * k))
+    X = encrypt_slots(ctx, sk, A, seed=11)
+    Y = slot_to_coeffs(ctx, plan, keys, X)                 # warm-up
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(torch.cuda.current_stream())
+    reps = 3
+    for _ in range(reps):
+        Y = slot_to_coeffs(ctx, plan, keys, X)
+    ev[1].record(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / reps / X.n_ct
+    err = np.abs(ctx.decrypt_acts(sk, Y) - A).max()
+    print(f"\nStC N=2^16 ({plan.split.baby}x{plan.split.giant} BSGS): {ms:.2f} ms/ct, plan+keys {t_plan:.1f} s, "
+          f"max err {err:.2e} ({-np.log2(err):.1f} bits)")
+    assert err < 2.0 ** -10
