@@ -1292,6 +1292,50 @@ __global__ void k_sd_inner(const uint32_t* __restrict__ baby, const uint32_t* __
         make_uint4((uint32_t)ab[0], (uint32_t)ab[1], (uint32_t)ab[2], (uint32_t)ab[3]);
   }
 }
+// the same sums for JG giant groups per thread (2 coefficients per thread): each baby word is read once per JG
+// groups instead of once per group (StC: b = 256 baby cts = 268 MB, re-read g = 128 times without this);
+// products < 2^60 accumulate lazily, reduced every 8 terms
+template <int JG>
+__global__ void k_sd_inner_g(const uint32_t* __restrict__ baby, const uint32_t* __restrict__ pts, uint32_t b,
+                             uint32_t g, uint32_t N, Mods M, uint32_t* __restrict__ inner) {
+  const uint32_t L = blockIdx.y, j0 = blockIdx.z * JG, q = M.m[L];
+  const uint64_t mu = M.mu[L];
+  for (uint32_t c2 = blockIdx.x * blockDim.x + threadIdx.x; c2 < N / 2; c2 += gridDim.x * blockDim.x) {
+    uint64_t acc[JG][4];
+#pragma unroll
+    for (int jj = 0; jj < JG; ++jj)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[jj][e] = 0;
+    for (uint32_t i = 0; i < b; ++i) {
+      const uint2 x = reinterpret_cast<const uint2*>(baby + ((size_t)i * 4 + L * 2) * N)[c2];
+      const uint2 y = reinterpret_cast<const uint2*>(baby + ((size_t)i * 4 + L * 2 + 1) * N)[c2];
+#pragma unroll
+      for (int jj = 0; jj < JG; ++jj) {
+        if (j0 + jj < g) {
+          const uint2 p = __ldg(reinterpret_cast<const uint2*>(pts + ((size_t)(i + (j0 + jj) * b) * 2 + L) * N) + c2);
+          acc[jj][0] += (uint64_t)p.x * x.x;
+          acc[jj][1] += (uint64_t)p.y * x.y;
+          acc[jj][2] += (uint64_t)p.x * y.x;
+          acc[jj][3] += (uint64_t)p.y * y.y;
+        }
+      }
+      if ((i & 7) == 7) {
+#pragma unroll
+        for (int jj = 0; jj < JG; ++jj)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[jj][e] = barrett64(acc[jj][e], mu, q);
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < JG; ++jj) {
+      if (j0 + jj < g) {
+        uint32_t* o = inner + ((size_t)(j0 + jj) * 4 + L * 2) * N;
+        reinterpret_cast<uint2*>(o)[c2] = make_uint2(barrett64(acc[jj][0], mu, q), barrett64(acc[jj][1], mu, q));
+        reinterpret_cast<uint2*>(o + N)[c2] = make_uint2(barrett64(acc[jj][2], mu, q), barrett64(acc[jj][3], mu, q));
+      }
+    }
+  }
+}
 // acc [L][ab][N] = inner_0 + sum_{z < cnt} rot_z
 __global__ void k_sd_accumulate(const uint32_t* __restrict__ inner0, const uint32_t* __restrict__ rot, uint32_t cnt,
                                 uint32_t N, Mods M, uint32_t* __restrict__ acc) {
@@ -1561,7 +1605,15 @@ extern "C" he_status he_slot_pcmm_run(const he_slot_pcmm_plan* p, const uint32_t
     if (s) return s;
   }
   // giant groups: all products in one launch, all g - 1 rotations in one pass
-  k_sd_inner<<<grid3(2, g), 256, 0, st>>>(w.baby, p->pts, b, N, p->M, w.inner);
+  static const bool inner_simple = getenv("HE_SD_INNER_SIMPLE") != nullptr;
+  if (g >= 8 && !inner_simple) {
+    dim3 gi = grid_for(N / 2);
+    gi.y = 2;
+    gi.z = (g + 7) / 8;
+    k_sd_inner_g<8><<<gi, 256, 0, st>>>(w.baby, p->pts, b, g, N, p->M, w.inner);
+  } else {
+    k_sd_inner<<<grid3(2, g), 256, 0, st>>>(w.baby, p->pts, b, N, p->M, w.inner);
+  }
   if (g > 1) {
     uint32_t* in1 = w.inner + 4ull * N;   // groups 1 .. g-1
     for (int L = 0; L < 2; ++L)
