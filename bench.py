@@ -502,6 +502,10 @@ def side_measurements(P, dev):
         out["slot_pcmm"] = slot_pcmm_side(P, dev)
     except Exception as exc:
         out["slot_pcmm_error"] = repr(exc)
+    try:
+        out["slot_to_coeffs"] = stc_side(P, dev)
+    except Exception as exc:
+        out["slot_to_coeffs_error"] = repr(exc)
     return out
 
 
@@ -560,6 +564,40 @@ def slot_pcmm_side(P, dev, reps=5):
                         "precision_bits": round(-math.log2(err / float(np.abs(ref).max())), 1)}
     return {"workload": f"hesim pcmm_bsgs schedule on CKKS ciphertexts, N = {P.N}, d x d in {P.N // 2} slots "
                         "(hoisted baby rotations, gadget key switching), 1 GPU", **res}
+
+
+def stc_side(P, dev, reps=3):
+    """§8f2: SlotToCoeffs (stc.py), slot-encoded activations -> the App. A coefficient layout: device ms per
+    ciphertext and the decrypted precision against the activations."""
+    import torch
+
+    from paper_2601_18511_b200 import HeContext
+    from paper_2601_18511_b200.stc import (encrypt_slots, make_slot_to_coeffs_plan, slot_to_coeffs,
+                                           slot_to_coeffs_keygen)
+
+    ctx = HeContext(P, device=dev)
+    sk = ctx.keygen(61)
+    plan = make_slot_to_coeffs_plan(ctx)
+    keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=63)
+    A = np.random.default_rng(65).uniform(-1, 1, (P.mlwe_degree // 2, 2 * P.mlwe_rank))
+    X = encrypt_slots(ctx, sk, A, seed=67)
+    Y = slot_to_coeffs(ctx, plan, keys, X)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(torch.cuda.current_stream())
+    for _ in range(reps):
+        Y = slot_to_coeffs(ctx, plan, keys, X)
+    e1.record(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    err = float(np.abs(ctx.decrypt_acts(sk, Y) - A).max())
+    b, g = plan.split.baby, plan.split.giant
+    res = {"workload": f"SlotToCoeffs, N = {P.N}: one {b}x{g} BSGS map over the {P.N // 2} diagonals per ct "
+                       "(App. A bit-reversal fused), 1 GPU",
+           "ms_per_ct": round(e0.elapsed_time(e1) / reps / X.n_ct, 3), "rotations_per_ct": b + g - 2,
+           "plaintext_bytes": int(plan.pts.numel() * 4), "precision_bits": round(-math.log2(err), 1)}
+    del plan, keys, X, Y
+    torch.cuda.empty_cache()
+    return res
 
 
 def ring_pack_side(P, dev, shape="4096x11008", reps=3):

@@ -18,6 +18,7 @@ from .slotpcmm import (BsgsSplit, PackedCt, SlotPcmmKeys, SlotPcmmPlan, clear_sl
 from .graphs import OpGraph
 from .ringpack import (RingPackKeys, RingPackPlan, make_ring_pack_plan, mod_raise, pcmm_level1, pcmm_packed, ring_pack,
                        ring_pack_keygen)
+from .stc import SlotBlocks, encrypt_slots, make_slot_to_coeffs_plan, slot_to_coeffs, slot_to_coeffs_keygen
 
 __all__ = [
     "NeedsBootstrapError", "HeParams", "CostLedger", "CtBlocks", "HeContext", "MlweBlocks", "SecretKey",
@@ -30,6 +31,7 @@ __all__ = [
     "ring_pack_keygen", "mod_raise",
     "BsgsSplit", "PackedCt", "SlotPcmmKeys", "SlotPcmmPlan", "clear_slot_pcmm", "decrypt_packed", "encrypt_packed",
     "make_slot_pcmm_plan", "pcmm_slot_bsgs", "pcmm_slot_depth1", "slot_pcmm_keygen", "OpGraph",
+    "SlotBlocks", "encrypt_slots", "make_slot_to_coeffs_plan", "slot_to_coeffs", "slot_to_coeffs_keygen",
 ]
 
 __version__ = "0.1.0"
