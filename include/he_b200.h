@@ -277,6 +277,12 @@ he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* plan, uint64_t* 
 he_status he_slot_pcmm_run(const he_slot_pcmm_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
                            const uint32_t* keys_baby_dev, const uint32_t* keys_giant_dev, uint32_t* out_dev,
                            void* workspace_dev, uint64_t workspace_bytes, void* stream, he_ledger* ledger);
+/* n_ct ciphertexts [n_ct][2][2][N] -> out [n_ct][2][N] under one plan; big maps (b g >= 4096) stream each
+ * plaintext once per chunk of up to 3 ciphertexts.  ledger: the per-ct counts times n_ct */
+he_status he_slot_pcmm_run_batch(const he_slot_pcmm_plan* plan, const uint32_t* ct_in_dev, uint32_t n_ct,
+                                 uint32_t level, const uint32_t* keys_baby_dev, const uint32_t* keys_giant_dev,
+                                 uint32_t* out_dev, void* workspace_dev, uint64_t workspace_bytes, void* stream,
+                                 he_ledger* ledger);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,7 @@
 //     gadget keys),
 //   - multi-GPU shards of the PCMv (he_rhombus_run_shard / he_rhombus_combine).
 // Each is restated in oracle/he_oracle_rhombus.c and bit-exact with it.
+#include <algorithm>
 #include <vector>
 
 #include "he_common.cuh"
@@ -1336,6 +1337,81 @@ __global__ void k_sd_inner_g(const uint32_t* __restrict__ baby, const uint32_t* 
     }
   }
 }
+// the products for CT ciphertexts at once (big maps, e.g. SlotToCoeffs: 32 768 plaintexts = 17 GiB): a CTA owns 32
+// coefficients of one limb, stages the CT baby sets of that tile in shared memory ([ct][i][lane][a, b] pairs,
+// CT b 256 B) and streams every plaintext word of the tile exactly once, using it for all CT ciphertexts; warp w
+// runs the groups 2w, 2w + 1 (+32 ...), 16 plaintext terms per group loaded ahead.  b % 16 == 0 and q < 2^30:
+// 16 products < 2^60 plus a residue stay below 2^64, so the sums are reduced once per 16 terms
+constexpr int kSdTile = 32;
+constexpr int kSdSharedThreads = 512;
+template <int CT>
+__global__ void __launch_bounds__(kSdSharedThreads, 1)
+    k_sd_inner_s(const uint32_t* __restrict__ baby, uint64_t baby_cs, const uint32_t* __restrict__ pts, uint32_t b,
+                 uint32_t g, uint32_t N, Mods M, uint32_t* __restrict__ inner, uint64_t inner_cs) {
+  extern __shared__ __align__(16) uint32_t sbaby[];
+  const uint32_t L = blockIdx.y, c0 = blockIdx.x * kSdTile, q = M.m[L];
+  const uint64_t mu = M.mu[L];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // stage: row r = ct b + i holds 32 (a, b) pairs; 8 threads per row, 4 coefficients each
+  for (uint32_t r = threadIdx.x >> 3; r < CT * b; r += blockDim.x >> 3) {
+    const uint32_t ct = r / b, i = r % b, t = threadIdx.x & 7;
+    const uint32_t* src = baby + ct * baby_cs + ((size_t)i * 4 + L * 2) * N + c0;
+    const uint4 va = reinterpret_cast<const uint4*>(src)[t];
+    const uint4 vb = reinterpret_cast<const uint4*>(src + N)[t];
+    uint4* dst = reinterpret_cast<uint4*>(sbaby + (size_t)r * 2 * kSdTile) + 2 * t;
+    dst[0] = make_uint4(va.x, vb.x, va.y, vb.y);
+    dst[1] = make_uint4(va.z, vb.z, va.w, vb.w);
+  }
+  __syncthreads();
+  const size_t tstride = 2ull * N;   // words between consecutive terms
+  const uint2* sl = reinterpret_cast<const uint2*>(sbaby) + lane;
+  for (uint32_t j0 = warp * 2; j0 < g; j0 += 2 * (blockDim.x >> 5)) {
+    const bool two = j0 + 1 < g;
+    const uint32_t* P0 = pts + ((size_t)j0 * b * 2 + L) * N + c0 + lane;
+    const uint32_t* P1 = two ? P0 + (size_t)b * tstride : P0;
+    uint64_t acc[2][CT][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct) acc[h][ct][0] = acc[h][ct][1] = 0;
+    for (uint32_t i0 = 0; i0 < b; i0 += 16) {
+      uint32_t p0[16], p1[16];
+      const uint32_t* a0 = P0 + (size_t)i0 * tstride;
+      const uint32_t* a1 = P1 + (size_t)i0 * tstride;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        p0[u] = __ldg(a0 + u * tstride);
+        p1[u] = __ldg(a1 + u * tstride);
+      }
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct) {
+        const uint2* sr = sl + (size_t)(ct * b + i0) * kSdTile;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const uint2 xy = sr[u * kSdTile];
+          acc[0][ct][0] += (uint64_t)p0[u] * xy.x;
+          acc[0][ct][1] += (uint64_t)p0[u] * xy.y;
+          acc[1][ct][0] += (uint64_t)p1[u] * xy.x;
+          acc[1][ct][1] += (uint64_t)p1[u] * xy.y;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          acc[h][ct][0] = barrett64(acc[h][ct][0], mu, q);
+          acc[h][ct][1] = barrett64(acc[h][ct][1], mu, q);
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !two) break;
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+        for (int ab = 0; ab < 2; ++ab)
+          inner[ct * inner_cs + ((size_t)(j0 + h) * 4 + L * 2 + ab) * N + c0 + lane] = (uint32_t)acc[h][ct][ab];
+    }
+  }
+}
 // acc [L][ab][N] = inner_0 + sum_{z < cnt} rot_z
 __global__ void k_sd_accumulate(const uint32_t* __restrict__ inner0, const uint32_t* __restrict__ rot, uint32_t cnt,
                                 uint32_t N, Mods M, uint32_t* __restrict__ acc) {
@@ -1371,6 +1447,7 @@ struct he_slot_pcmm_plan {
   uint32_t* perms;       // owned [b - 1 + g - 1][N]
   Mods M;
   uint32_t qhinv[2], qhinvp[2], pinv[2], q1inv, q1invp;
+  uint32_t chunk;        // ciphertexts per shared-plaintext pass (1: per-ct kernels; 2-3: k_sd_inner_s)
 };
 
 // gadget key (layout [t][part][mod][deg], t = i kSdSub + h), NTT domain; streams use t as the digit index
@@ -1458,6 +1535,15 @@ static he_status slot_plan_make(const he_context* c, const uint32_t* pts_ntt_dev
   }
   p->q1inv = (uint32_t)powmod_h(p->M.m[1] % p->M.m[0], p->M.m[0] - 2, p->M.m[0]);
   p->q1invp = shoup_pre(p->q1inv, p->M.m[0]);
+  // big maps stream their plaintexts once per up-to-3 ciphertexts (shared-memory baby tiles, CT b 256 B)
+  p->chunk = 1;
+  const bool shared_ok = b % 16 == 0 && N % kSdTile == 0 && p->M.m[0] < (1u << 30) && p->M.m[1] < (1u << 30);
+  if (((uint64_t)b * g >= 4096 || getenv("HE_SD_SHARED")) && shared_ok && !getenv("HE_SD_PER_CT"))
+    for (uint32_t c = 3; c >= 2; --c)
+      if ((uint64_t)c * b * 2 * kSdTile * 4 <= 200 * 1024) {
+        p->chunk = c;
+        break;
+      }
   std::vector<uint32_t> h((size_t)(steps.empty() ? 1 : steps.size()) * N);
   for (size_t t = 0; t < steps.size(); ++t) {
     const uint64_t gal = powmod_h(5, steps[t] % (N / 2), 2ull * N);
@@ -1526,7 +1612,7 @@ struct SdWs {
   uint32_t *D, *X, *baby, *inner, *rot, *acc, *UW, *LB;
 };
 static uint64_t sd_ws_words(const he_slot_pcmm_plan* p, SdWs* w, uint32_t* base) {
-  const uint64_t N = p->N, T = (p->b > p->g ? p->b : p->g);   // rotations per batched pass < T
+  const uint64_t N = p->N, T = (p->b > p->g ? p->b : p->g), C = p->chunk;   // rotations per batched pass < T
   uint64_t off = 0;
   auto take = [&](uint32_t*& ptr, uint64_t words) {
     if (w) ptr = base + off;
@@ -1536,8 +1622,8 @@ static uint64_t sd_ws_words(const he_slot_pcmm_plan* p, SdWs* w, uint32_t* base)
   SdWs& r = w ? *w : dummy;
   take(r.D, 3ull * kSdT * T * N);
   take(r.X, 4 * N);
-  take(r.baby, 4ull * p->b * N);
-  take(r.inner, 4ull * p->g * N);
+  take(r.baby, 4ull * p->b * N * C);
+  take(r.inner, 4ull * p->g * N * C);
   take(r.rot, 4ull * T * N);
   take(r.acc, 4 * N);
   take(r.UW, 6ull * T * N);
@@ -1551,16 +1637,21 @@ extern "C" he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* p, ui
   return HE_OK;
 }
 
-extern "C" he_status he_slot_pcmm_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint32_t level,
-                                      const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out, void* ws_dev,
-                                      uint64_t ws_bytes, void* stream, he_ledger* ledger) {
-  if (!p) return fail(HE_EINVAL, "null plan");
-  if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmm needs one level");
-  if (level != 1) return fail(HE_EINVAL, "the slot-domain PCMM runs at level 1 (got %u)", level);
-  if (!ct_in || !out || !ws_dev || (p->b > 1 && !keys_baby) || (p->g > 1 && !keys_giant))
-    return fail(HE_EINVAL, "null argument");
-  if (ws_bytes < sd_ws_words(p, nullptr, nullptr) * sizeof(uint32_t)) return fail(HE_EINVAL, "workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
+template <int CT>
+static cudaError_t launch_sd_inner_s(const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts, uint32_t b,
+                                     uint32_t g, uint32_t N, const Mods& M, uint32_t* inner, uint64_t inner_cs,
+                                     cudaStream_t st) {
+  const int smem = CT * (int)b * 2 * kSdTile * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_sd_inner_s<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_sd_inner_s<CT><<<dim3(N / kSdTile, 2), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, M, inner, inner_cs);
+  return cudaGetLastError();
+}
+
+// n_ct ciphertexts [n_ct][2][2][N] level 1 -> out [n_ct][2][N] level 0, in chunks of p->chunk sharing each
+// plaintext read
+static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint32_t n_ct, const uint32_t* keys_baby,
+                        const uint32_t* keys_giant, uint32_t* out, void* ws_dev, cudaStream_t st) {
   const he_context* c = p->ctx;
   const uint32_t N = p->N, b = p->b, g = p->g;
   SdWs w;
@@ -1594,43 +1685,89 @@ extern "C" he_status he_slot_pcmm_run(const he_slot_pcmm_plan* p, const uint32_t
                                                p->pinv[0], p->pinv[1], dst, 4ull * N);
     return HE_OK;
   };
-  // baby steps: one hoisted digit decomposition of the input, all b - 1 rotations in one pass
-  he_status s = digits(ct_in, 0, 1);
-  if (s) return s;
-  HE_CUDA(cudaMemcpyAsync(w.X, ct_in, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
-  for (int L = 0; L < 2; ++L) HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
-  HE_CUDA(cudaMemcpyAsync(w.baby, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
-  if (b > 1) {
-    s = rotate(b - 1, 1, 1, 0, keys_baby, w.X + N, 0, w.baby + 4ull * N);
-    if (s) return s;
-  }
-  // giant groups: all products in one launch, all g - 1 rotations in one pass
   static const bool inner_simple = getenv("HE_SD_INNER_SIMPLE") != nullptr;
-  if (g >= 8 && !inner_simple) {
-    dim3 gi = grid_for(N / 2);
-    gi.y = 2;
-    gi.z = (g + 7) / 8;
-    k_sd_inner_g<8><<<gi, 256, 0, st>>>(w.baby, p->pts, b, g, N, p->M, w.inner);
-  } else {
-    k_sd_inner<<<grid3(2, g), 256, 0, st>>>(w.baby, p->pts, b, N, p->M, w.inner);
+  const uint64_t baby_cs = 4ull * b * N, inner_cs = 4ull * g * N;
+  for (uint32_t c0 = 0; c0 < n_ct; c0 += p->chunk) {
+    const uint32_t cc = std::min(p->chunk, n_ct - c0);
+    // baby steps per ciphertext: one hoisted digit decomposition, all b - 1 rotations in one pass
+    for (uint32_t z = 0; z < cc; ++z) {
+      const uint32_t* ct = ct_in + (size_t)(c0 + z) * 4 * N;
+      uint32_t* bz = w.baby + z * baby_cs;
+      he_status s = digits(ct, 0, 1);
+      if (s) return s;
+      HE_CUDA(cudaMemcpyAsync(w.X, ct, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
+      for (int L = 0; L < 2; ++L) HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
+      HE_CUDA(cudaMemcpyAsync(bz, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
+      if (b > 1) {
+        s = rotate(b - 1, 1, 1, 0, keys_baby, w.X + N, 0, bz + 4ull * N);
+        if (s) return s;
+      }
+    }
+    // giant-group products: all groups (and all cc ciphertexts) in one launch
+    if (p->chunk > 1) {
+      cudaError_t e = cc == 3   ? launch_sd_inner_s<3>(w.baby, baby_cs, p->pts, b, g, N, p->M, w.inner, inner_cs, st)
+                      : cc == 2 ? launch_sd_inner_s<2>(w.baby, baby_cs, p->pts, b, g, N, p->M, w.inner, inner_cs, st)
+                                : launch_sd_inner_s<1>(w.baby, baby_cs, p->pts, b, g, N, p->M, w.inner, inner_cs, st);
+      HE_CUDA(e, "slot map products (shared)");
+    } else if (g >= 8 && !inner_simple) {
+      dim3 gi = grid_for(N / 2);
+      gi.y = 2;
+      gi.z = (g + 7) / 8;
+      k_sd_inner_g<8><<<gi, 256, 0, st>>>(w.baby, p->pts, b, g, N, p->M, w.inner);
+    } else {
+      k_sd_inner<<<grid3(2, g), 256, 0, st>>>(w.baby, p->pts, b, N, p->M, w.inner);
+    }
+    // giant rotations per ciphertext (one pass each), sum, one rescale
+    for (uint32_t z = 0; z < cc; ++z) {
+      uint32_t* iz = w.inner + z * inner_cs;
+      if (g > 1) {
+        uint32_t* in1 = iz + 4ull * N;   // groups 1 .. g-1
+        for (int L = 0; L < 2; ++L)
+          HE_CUDA(ntt_inverse(c->ntt[L], in1 + (size_t)L * 2 * N, g - 1, 4ull * N, st), "INTT(inner a)");
+        he_status s = digits(in1, 4ull * N, g - 1);
+        if (s) return s;
+        s = rotate(g - 1, 0, g - 1, b - 1, keys_giant, in1 + N, 4ull * N, w.rot);
+        if (s) return s;
+      }
+      k_sd_accumulate<<<grid3(2, 1), 256, 0, st>>>(iz, w.rot, g - 1, N, p->M, w.acc);
+      for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt[L], w.acc + (size_t)L * 2 * N, 2, N, st), "INTT(acc)");
+      k_rh_combine<<<grid_for(2ull * N), 256, 0, st>>>(w.acc, 1, N, p->M.m[0], p->M.m[1], p->q1inv, p->q1invp,
+                                                       out + (size_t)(c0 + z) * 2 * N);
+    }
   }
-  if (g > 1) {
-    uint32_t* in1 = w.inner + 4ull * N;   // groups 1 .. g-1
-    for (int L = 0; L < 2; ++L)
-      HE_CUDA(ntt_inverse(c->ntt[L], in1 + (size_t)L * 2 * N, g - 1, 4ull * N, st), "INTT(inner a)");
-    s = digits(in1, 4ull * N, g - 1);
-    if (s) return s;
-    s = rotate(g - 1, 0, g - 1, b - 1, keys_giant, in1 + N, 4ull * N, w.rot);
-    if (s) return s;
-  }
-  k_sd_accumulate<<<grid3(2, 1), 256, 0, st>>>(w.inner, w.rot, g - 1, N, p->M, w.acc);
-  for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt[L], w.acc + (size_t)L * 2 * N, 2, N, st), "INTT(acc)");
-  k_rh_combine<<<grid_for(2ull * N), 256, 0, st>>>(w.acc, 1, N, p->M.m[0], p->M.m[1], p->q1inv, p->q1invp, out);
   HE_CUDA(cudaGetLastError(), "slot pcmm launch");
+  return HE_OK;
+}
+
+static he_status sd_run_checked(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint32_t n_ct, uint32_t level,
+                                const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out, void* ws_dev,
+                                uint64_t ws_bytes, void* stream, he_ledger* ledger) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmm needs one level");
+  if (level != 1) return fail(HE_EINVAL, "the slot-domain PCMM runs at level 1 (got %u)", level);
+  if (!ct_in || !out || !ws_dev || (p->b > 1 && !keys_baby) || (p->g > 1 && !keys_giant))
+    return fail(HE_EINVAL, "null argument");
+  if (ws_bytes < sd_ws_words(p, nullptr, nullptr) * sizeof(uint32_t)) return fail(HE_EINVAL, "workspace too small");
+  he_status s = sd_run(p, ct_in, n_ct, keys_baby, keys_giant, out, ws_dev, (cudaStream_t)stream);
+  if (s) return s;
   if (ledger) {
-    ledger->ct_rotations += (int64_t)(b - 1) + (g - 1);
-    ledger->pc_mults += p->d;
-    ledger->rescales += 1;
+    ledger->ct_rotations += (int64_t)n_ct * ((p->b - 1) + (p->g - 1));
+    ledger->pc_mults += (int64_t)n_ct * p->d;
+    ledger->rescales += n_ct;
   }
   return HE_OK;
+}
+
+extern "C" he_status he_slot_pcmm_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint32_t level,
+                                      const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out, void* ws_dev,
+                                      uint64_t ws_bytes, void* stream, he_ledger* ledger) {
+  return sd_run_checked(p, ct_in, 1, level, keys_baby, keys_giant, out, ws_dev, ws_bytes, stream, ledger);
+}
+
+extern "C" he_status he_slot_pcmm_run_batch(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint32_t n_ct,
+                                            uint32_t level, const uint32_t* keys_baby, const uint32_t* keys_giant,
+                                            uint32_t* out, void* ws_dev, uint64_t ws_bytes, void* stream,
+                                            he_ledger* ledger) {
+  if (n_ct == 0) return fail(HE_EINVAL, "empty batch");
+  return sd_run_checked(p, ct_in, n_ct, level, keys_baby, keys_giant, out, ws_dev, ws_bytes, stream, ledger);
 }

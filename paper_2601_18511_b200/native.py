@@ -32,7 +32,7 @@ EXPORTS = (
     "he_pcmm_run_level1", "he_ring_pack_key_bytes", "he_ring_pack_keygen", "he_ring_pack_plan_create", "he_ring_pack_plan_destroy",
     "he_ring_pack_workspace_bytes", "he_ring_pack_run", "he_rhombus_run_shard", "he_rhombus_combine",
     "he_encrypt_poly", "he_slot_rotation_keygen", "he_slot_pcmm_encode_pts", "he_slot_pcmm_plan_create",
-    "he_slot_pcmm_plan_destroy", "he_slot_pcmm_workspace_bytes", "he_slot_pcmm_run", "he_mod_raise",
+    "he_slot_pcmm_plan_destroy", "he_slot_pcmm_workspace_bytes", "he_slot_pcmm_run", "he_slot_pcmm_run_batch", "he_mod_raise",
     "he_slot_lt_plan_create", "he_slot_bsgs_plan_create",
 )
 
@@ -115,6 +115,7 @@ def lib():
             "he_slot_pcmm_plan_destroy": (st, [vp]),
             "he_slot_pcmm_workspace_bytes": (st, [vp, ctypes.POINTER(u64)]),
             "he_slot_pcmm_run": (st, [vp, vp, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
+            "he_slot_pcmm_run_batch": (st, [vp, vp, u32, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_ring_pack_key_bytes": (st, [vp, i32, ctypes.POINTER(u64)]),
             "he_ring_pack_keygen": (st, [vp, i32, u64, vp, vp, vp]),
             "he_ring_pack_plan_create": (st, [vp, u32, i32, ctypes.POINTER(vp)]),

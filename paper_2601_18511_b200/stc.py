@@ -166,11 +166,9 @@ def slot_to_coeffs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, X: Sl
     N = ctx.params.N
     out = torch.empty((X.n_ct, 1, 2, N), dtype=torch.int32, device=ctx.device)
     ws = plan.workspace(ctx.device)
-    for r in range(X.n_ct):
-        led = native.HeLedgerC()
-        native.call("he_slot_pcmm_run", plan._handle, X.data[r].data_ptr(), X.level, keys.baby.data_ptr(),
-                    keys.giant.data_ptr(), out[r].data_ptr(), ws.data_ptr(), ws.numel() * 4, ctx.stream(),
-                    ctypes.byref(led))
-        ctx.ledger.add_c(led)
+    led = native.HeLedgerC()
+    native.call("he_slot_pcmm_run_batch", plan._handle, X.data.data_ptr(), X.n_ct, X.level, keys.baby.data_ptr(),
+                keys.giant.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel() * 4, ctx.stream(), ctypes.byref(led))
+    ctx.ledger.add_c(led)
     ctx.ledger.observe_level(X.level - 1)
     return CtBlocks(out, level=X.level - 1, n_cols=X.n_cols)

@@ -51,6 +51,34 @@ def test_toy_bit_exact_and_layout():
     assert np.abs(ph - O.encode_acts(P, A)).max() < P.delta * 2.0 ** -14
 
 
+@pytest.mark.parametrize("n_ct", [4])
+def test_toy_batched_shared_path_bit_exact(n_ct, monkeypatch):
+    """The shared-memory multi-ciphertext products (forced at toy size; chunks of 3 + 1) give the oracle's
+    words for every ciphertext."""
+    monkeypatch.setenv("HE_SD_SHARED", "1")
+    P = HeParams.toy()
+    ctx = HeContext(P)
+    sk = ctx.keygen(7)
+    d, k, N, n = P.mlwe_degree, P.mlwe_rank, P.N, P.N // 2
+    A = np.random.default_rng(5).uniform(-1, 1, (d // 2, n_ct * k))
+    plan = make_slot_to_coeffs_plan(ctx)
+    b, g = plan.split.baby, plan.split.giant
+    keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=13)
+    X = encrypt_slots(ctx, sk, A, seed=11)
+    Y = slot_to_coeffs(ctx, plan, keys, X)
+    s = O.keygen(P, 7)
+    ct = O.encrypt(P, 11, s, np.stack([slots.encode(v, N, P.delta) for v in slot_vectors(P, A)]))
+    assert np.array_equal(u32(X.data), ct)
+    pt = stc_plaintexts(P, plan.split, 0, n).numpy()
+    pts = np.stack([np.stack([(pt[t] % q).astype(np.uint32) for q in P.moduli]) for t in range(n)])
+    kb = O.rotation_keys(P, 13, s, list(range(1, b)))
+    kg = O.rotation_keys(P, 13, s, [j * b for j in range(1, g)])
+    for r in range(n_ct):
+        want = O.slot_bsgs(P, ct[r], pts, 1, b, g, kb, kg)
+        assert np.array_equal(u32(Y.data[r, 0]), want), f"ct {r}"
+    np.testing.assert_allclose(ctx.decrypt_acts(sk, Y), A, atol=2.0 ** -14)
+
+
 def test_error_contract():
     P = HeParams.toy()
     ctx = HeContext(P)
@@ -84,7 +112,7 @@ def test_llama_ring():
     keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=13)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t0
-    A = np.random.default_rng(4).uniform(-1, 1, (d // 2, 2 * k))
+    A = np.random.default_rng(4).uniform(-1, 1, (d // 2, 3 * k))
     X = encrypt_slots(ctx, sk, A, seed=11)
     Y = slot_to_coeffs(ctx, plan, keys, X)                 # warm-up
     torch.cuda.synchronize()
