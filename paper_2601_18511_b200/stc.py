@@ -36,6 +36,9 @@ from .layout import bit_reverse_table, coeff_table
 from .slotpcmm import BsgsSplit, SlotPcmmKeys, SlotPcmmPlan
 
 
+DEFAULT_PT_SHIFT = -1   # plaintexts at q1 / 2, input slots at 2 Delta (see make_slot_to_coeffs_plan)
+
+
 @dataclass
 class SlotBlocks:
     """Slot-encoded activation ciphertexts: data [n_ct, limbs, 2, N]; ct r carries columns k r .. k r + k - 1
@@ -44,6 +47,7 @@ class SlotBlocks:
     data: object
     level: int
     n_cols: int
+    scale: float = 0.0
     layout: str = "app_a_slots"
 
     @property
@@ -83,8 +87,9 @@ def slot_vectors(params, acts) -> np.ndarray:
     return out
 
 
-def stc_plaintexts(params, split: BsgsSplit, k0: int, count: int, device="cpu"):
-    """int64 [count, N] coefficients of terms k0 .. k0 + count - 1 (term k = i + j b), encoded at scale q1."""
+def stc_plaintexts(params, split: BsgsSplit, k0: int, count: int, device="cpu", pt_shift: int = 0):
+    """int64 [count, N] coefficients of terms k0 .. k0 + count - 1 (term k = i + j b), encoded at scale
+    q1 2^pt_shift."""
     torch = _torch()
     N, n, b = params.N, params.N // 2, split.baby
     e = torch.as_tensor(slots.slot_exponents(N), device=device)
@@ -99,11 +104,17 @@ def stc_plaintexts(params, split: BsgsSplit, k0: int, count: int, device="cpu"):
     Z[:, e] = z
     Z[:, (2 * N - e) % (2 * N)] = z.conj()
     m = torch.fft.fft(Z, dim=1)[:, :N].real / N
-    return torch.round(m * float(params.delta_w)).to(torch.int64)
+    return torch.round(m * float(params.delta_w) * 2.0 ** pt_shift).to(torch.int64)
 
 
-def make_slot_to_coeffs_plan(ctx: HeContext, split: BsgsSplit | None = None, batch: int = 256) -> SlotPcmmPlan:
-    """The n = N/2 diagonals of M, BSGS-ordered and NTT'd into [n, 2, N] device residues."""
+def make_slot_to_coeffs_plan(ctx: HeContext, split: BsgsSplit | None = None, batch: int = 256,
+                             pt_shift: int = DEFAULT_PT_SHIFT) -> SlotPcmmPlan:
+    """The n = N/2 diagonals of M, BSGS-ordered and NTT'd into [n, 2, N] device residues, encoded at scale
+    q1 2^pt_shift: the output keeps scale Delta when the input slots carry Delta / 2^pt_shift
+    (plan.input_scale, what encrypt_slots uses).  The error has two parts (tools/stc_precision.py, N = 2^16):
+    the baby rotations' ModDown rounding noise (~60 per coefficient, amplified sqrt(n) by the map, so it
+    scales as 1 / input_scale) and the plaintext rounding (scales as 1 / (q1 2^pt_shift)); they balance
+    at pt_shift = -1: 11.6 bits (10.7 at 0, 11.1 at -2)."""
     torch = _torch()
     N, n = ctx.params.N, ctx.params.N // 2
     split = split or stc_split(n)
@@ -113,7 +124,7 @@ def make_slot_to_coeffs_plan(ctx: HeContext, split: BsgsSplit | None = None, bat
     plan.pts = torch.empty((n, 2, N), dtype=torch.int32, device=ctx.device)
     for k0 in range(0, n, batch):
         cnt = min(batch, n - k0)
-        pt = stc_plaintexts(ctx.params, split, k0, cnt, ctx.device).contiguous()
+        pt = stc_plaintexts(ctx.params, split, k0, cnt, ctx.device, pt_shift).contiguous()
         native.call("he_slot_pcmm_encode_pts", ctx.handle, pt.data_ptr(), cnt, plan.pts[k0].data_ptr(), ctx.stream())
     h = ctypes.c_void_p()
     native.call("he_slot_bsgs_plan_create", ctx.handle, plan.pts.data_ptr(), split.baby, split.giant, 1,
@@ -121,6 +132,8 @@ def make_slot_to_coeffs_plan(ctx: HeContext, split: BsgsSplit | None = None, bat
     plan._handle = h
     b, g = split.baby, split.giant
     plan.steps = tuple(range(1, b)) + tuple(j * b for j in range(1, g))
+    plan.pt_shift = pt_shift
+    plan.input_scale = ctx.params.delta / 2.0 ** pt_shift
     return plan
 
 
@@ -141,16 +154,18 @@ def slot_to_coeffs_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, see
     return SlotPcmmKeys(gen(baby), gen(giant), tuple(baby + giant))
 
 
-def encrypt_slots(ctx: HeContext, sk: SecretKey, acts, seed: int, r0: int = 0) -> SlotBlocks:
-    """Slot-encode (scale Delta) and encrypt a (d/2) x n_in activation block at level 1, one ct per k columns
-    -- the state the attention phase leaves behind."""
+def encrypt_slots(ctx: HeContext, sk: SecretKey, acts, seed: int, r0: int = 0, scale: float | None = None) -> SlotBlocks:
+    """Slot-encode and encrypt a (d/2) x n_in activation block at level 1, one ct per k columns -- the state
+    the attention phase leaves behind.  scale: the plan's input_scale (Delta 2^-pt_shift,
+    2 Delta by default) so that StC lands at Delta; None = the default plan's."""
     torch = _torch()
     z = slot_vectors(ctx.params, acts)
-    pt = torch.from_numpy(np.stack([slots.encode(v, ctx.params.N, ctx.params.delta) for v in z])).to(ctx.device)
+    sc = ctx.params.delta / 2.0 ** DEFAULT_PT_SHIFT if scale is None else float(scale)
+    pt = torch.from_numpy(np.stack([slots.encode(v, ctx.params.N, sc) for v in z])).to(ctx.device)
     out = torch.empty((z.shape[0], 2, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
     native.call("he_encrypt_poly", ctx.handle, sk.s_ntt.data_ptr(), pt.data_ptr(), z.shape[0], seed, r0,
                 out.data_ptr(), ctx.stream())
-    return SlotBlocks(out, level=1, n_cols=int(np.asarray(acts).shape[1]))
+    return SlotBlocks(out, level=1, n_cols=int(np.asarray(acts).shape[1]), scale=sc)
 
 
 def slot_to_coeffs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, X: SlotBlocks) -> CtBlocks:
@@ -163,6 +178,8 @@ def slot_to_coeffs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, X: Sl
     require_level(X.level)
     if X.level != 1:
         raise ValueError(f"slot_to_coeffs runs at level 1 on this two-prime chain, operand is at level {X.level}")
+    if X.scale and X.scale != plan.input_scale:
+        raise ValueError(f"scale mismatch: plan expects input scale {plan.input_scale}, operand has {X.scale}")
     N = ctx.params.N
     out = torch.empty((X.n_ct, 1, 2, N), dtype=torch.int32, device=ctx.device)
     ws = plan.workspace(ctx.device)

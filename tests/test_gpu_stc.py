@@ -37,9 +37,9 @@ def test_toy_bit_exact_and_layout():
     assert Y.level == 0 and Y.layout == "app_a_coeff" and Y.n_cols == 2 * k
     # the oracle on the same integers (ct 0)
     s = O.keygen(P, 7)
-    ct = O.encrypt(P, 11, s, slots.encode(slot_vectors(P, A)[0], N, P.delta)[None])[0]
+    ct = O.encrypt(P, 11, s, slots.encode(slot_vectors(P, A)[0], N, plan.input_scale)[None])[0]
     assert np.array_equal(u32(X.data[0]), ct)
-    pt = stc_plaintexts(P, plan.split, 0, n).numpy()
+    pt = stc_plaintexts(P, plan.split, 0, n, pt_shift=plan.pt_shift).numpy()
     pts = np.stack([np.stack([(pt[t] % q).astype(np.uint32) for q in P.moduli]) for t in range(n)])
     want = O.slot_bsgs(P, ct, pts, 1, b, g, O.rotation_keys(P, 13, s, list(range(1, b))),
                        O.rotation_keys(P, 13, s, [j * b for j in range(1, g)]))
@@ -67,9 +67,9 @@ def test_toy_batched_shared_path_bit_exact(n_ct, monkeypatch):
     X = encrypt_slots(ctx, sk, A, seed=11)
     Y = slot_to_coeffs(ctx, plan, keys, X)
     s = O.keygen(P, 7)
-    ct = O.encrypt(P, 11, s, np.stack([slots.encode(v, N, P.delta) for v in slot_vectors(P, A)]))
+    ct = O.encrypt(P, 11, s, np.stack([slots.encode(v, N, plan.input_scale) for v in slot_vectors(P, A)]))
     assert np.array_equal(u32(X.data), ct)
-    pt = stc_plaintexts(P, plan.split, 0, n).numpy()
+    pt = stc_plaintexts(P, plan.split, 0, n, pt_shift=plan.pt_shift).numpy()
     pts = np.stack([np.stack([(pt[t] % q).astype(np.uint32) for q in P.moduli]) for t in range(n)])
     kb = O.rotation_keys(P, 13, s, list(range(1, b)))
     kg = O.rotation_keys(P, 13, s, [j * b for j in range(1, g)])
@@ -98,6 +98,8 @@ def test_error_contract():
         pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W), Y)
     with pytest.raises(ValueError):
         encrypt_slots(ctx, sk, np.zeros((3, P.mlwe_rank)), seed=1)
+    with pytest.raises(ValueError):
+        slot_to_coeffs(ctx, plan, keys, encrypt_slots(ctx, sk, A, seed=1, scale=P.delta))   # scale mismatch
 
 
 def test_llama_ring():
@@ -127,4 +129,4 @@ def test_llama_ring():
     err = np.abs(ctx.decrypt_acts(sk, Y) - A).max()
     print(f"\nStC N=2^16 ({plan.split.baby}x{plan.split.giant} BSGS): {ms:.2f} ms/ct, plan+keys {t_plan:.1f} s, "
           f"max err {err:.2e} ({-np.log2(err):.1f} bits)")
-    assert err < 2.0 ** -10
+    assert err < 2.0 ** -11
