@@ -270,6 +270,14 @@ he_status he_slot_lt_plan_create(const he_context* ctx, const uint32_t* pts_ntt_
  * [b g][2][N] in order i + j b, diagonal i + j b pre-rotated by -j b stride; runs through he_slot_pcmm_run */
 he_status he_slot_bsgs_plan_create(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t b, uint32_t g,
                                    uint32_t stride, he_slot_pcmm_plan** out);
+/* flags for he_slot_bsgs_plan_create_ext */
+#define HE_SLOT_LAZY_MODDOWN 1u /* baby rotations kept mod (q0, q1, P), one ModDown per giant group; pts
+                                   [b g][3][N] (he_slot_pcmm_encode_pts_ext with n_mods = 3); b % 16 == 0 */
+he_status he_slot_bsgs_plan_create_ext(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t b, uint32_t g,
+                                       uint32_t stride, uint32_t flags, he_slot_pcmm_plan** out);
+/* int64 plaintext polys [count][N] -> NTT-domain residues [count][n_mods][N] (n_mods 2: q0, q1; 3: + P) */
+he_status he_slot_pcmm_encode_pts_ext(const he_context* ctx, const int64_t* pt_dev, uint32_t count, uint32_t n_mods,
+                                      uint32_t* pts_ntt_dev, void* stream);
 he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* plan);
 he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* plan, uint64_t* bytes);
 /* ct_in [2][2][N] level 1 -> out [2 (a, b)][N] level 0.  keys_baby: steps i d (i = 1 .. b-1), keys_giant:

@@ -689,6 +689,106 @@ int or_slot_bsgs(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t
   return 0;
 }
 
+/*
+ * The same map with lazy ModDown (hoisted BSGS, baby rotations kept in the PQ basis): baby_i = (U, P sigma(b) + W)
+ * mod (q0, q1, P) straight from the key MAC (baby_0 = P ct), the products taken mod q0, q1 and P, and one
+ * ModDown per giant group sum -- so the baby rotations' rounding noise is never multiplied by the
+ * plaintexts.  pts [b g][3 moduli][N] coefficient form.  Then giant rotations, sum, rescale as above.
+ */
+int or_slot_bsgs_lazy(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t g, const uint32_t* ct_in,
+                      const uint32_t* pts, const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out) {
+  if ((uint64_t)b * g * d > N / 2) return 1;
+  const size_t cw = (size_t)4 * N, bw = (size_t)6 * N;   /* Q ct [2][2][N]; PQ ct [3][2][N] */
+  const uint32_t P = m[2];
+  uint32_t* D = (uint32_t*)malloc(sizeof(uint32_t) * 6 * SD * N);
+  uint32_t* a_in = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+  for (int L = 0; L < 2; ++L) memcpy(a_in + (size_t)L * N, ct_in + ((size_t)L * 2 + 0) * N, sizeof(uint32_t) * N);
+  ks_digits(a_in, N, m, D);
+  uint32_t* baby = (uint32_t*)calloc(bw * b, sizeof(uint32_t));
+  uint32_t* U = (uint32_t*)malloc(sizeof(uint32_t) * 3 * N);
+  uint32_t* W = (uint32_t*)malloc(sizeof(uint32_t) * 3 * N);
+  uint32_t* sd = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  for (int L = 0; L < 2; ++L)
+    for (int ab = 0; ab < 2; ++ab)
+      for (uint32_t k = 0; k < N; ++k)
+        baby[((size_t)L * 2 + ab) * N + k] = (uint32_t)mulmod(ct_in[((size_t)L * 2 + ab) * N + k], P % m[L], m[L]);
+  for (uint32_t i = 1; i < b; ++i) {
+    uint64_t gal = 1;
+    for (uint64_t e = 0; e < ((uint64_t)i * d) % (N / 2); ++e) gal = gal * 5 % (2ull * N);
+    const uint32_t* ksk = keys_baby + (size_t)(i - 1) * 24 * N;
+    memset(U, 0, sizeof(uint32_t) * 3 * N);
+    memset(W, 0, sizeof(uint32_t) * 3 * N);
+    for (int j = 0; j < 3; ++j)
+      for (int x = 0; x < 2 * SD; ++x) {
+        or_automorphism(D + ((size_t)j * 2 * SD + x) * N, N, (uint32_t)gal, m[j], sd);
+        polymul(sd, ksk + ((size_t)(x * 2 + 0) * 3 + j) * N, N, m[j], t);
+        for (uint32_t k = 0; k < N; ++k) U[(size_t)j * N + k] = (uint32_t)(((uint64_t)U[(size_t)j * N + k] + t[k]) % m[j]);
+        polymul(sd, ksk + ((size_t)(x * 2 + 1) * 3 + j) * N, N, m[j], t);
+        for (uint32_t k = 0; k < N; ++k) W[(size_t)j * N + k] = (uint32_t)(((uint64_t)W[(size_t)j * N + k] + t[k]) % m[j]);
+      }
+    uint32_t* bi = baby + i * bw;
+    for (int j = 0; j < 3; ++j) {
+      if (j < 2) or_automorphism(ct_in + ((size_t)j * 2 + 1) * N, N, (uint32_t)gal, m[j], sd);
+      for (uint32_t k = 0; k < N; ++k) {
+        bi[((size_t)j * 2 + 0) * N + k] = U[(size_t)j * N + k];
+        const uint64_t pb = j < 2 ? mulmod(sd[k], P % m[j], m[j]) : 0;
+        bi[((size_t)j * 2 + 1) * N + k] = (uint32_t)((pb + W[(size_t)j * N + k]) % m[j]);
+      }
+    }
+  }
+  uint32_t* acc = (uint32_t*)calloc(cw, sizeof(uint32_t));
+  uint32_t* inner = (uint32_t*)malloc(sizeof(uint32_t) * bw);
+  uint32_t* innerq = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  uint32_t* rot = (uint32_t*)malloc(sizeof(uint32_t) * cw);
+  uint32_t* XA = (uint32_t*)malloc(sizeof(uint32_t) * 3 * N);
+  uint32_t* XB = (uint32_t*)malloc(sizeof(uint32_t) * 3 * N);
+  uint32_t* xa = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+  uint32_t* xb = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+  for (uint32_t j = 0; j < g; ++j) {
+    memset(inner, 0, sizeof(uint32_t) * bw);
+    for (uint32_t i = 0; i < b; ++i)
+      for (int L = 0; L < 3; ++L)
+        for (int ab = 0; ab < 2; ++ab) {
+          polymul(baby + i * bw + ((size_t)L * 2 + ab) * N, pts + ((size_t)(i + j * b) * 3 + L) * N, N, m[L], t);
+          uint32_t* dst = inner + ((size_t)L * 2 + ab) * N;
+          for (uint32_t k = 0; k < N; ++k) dst[k] = (uint32_t)(((uint64_t)dst[k] + t[k]) % m[L]);
+        }
+    for (int L = 0; L < 3; ++L) {   /* [mod][n] views of the a and b parts for ks_moddown */
+      memcpy(XA + (size_t)L * N, inner + ((size_t)L * 2 + 0) * N, sizeof(uint32_t) * N);
+      memcpy(XB + (size_t)L * N, inner + ((size_t)L * 2 + 1) * N, sizeof(uint32_t) * N);
+    }
+    ks_moddown(XA, XB, N, m, xa, xb);
+    for (int L = 0; L < 2; ++L) {
+      memcpy(innerq + ((size_t)L * 2 + 0) * N, xa + (size_t)L * N, sizeof(uint32_t) * N);
+      memcpy(innerq + ((size_t)L * 2 + 1) * N, xb + (size_t)L * N, sizeof(uint32_t) * N);
+    }
+    const uint32_t* part = innerq;
+    if (j > 0) {
+      for (int L = 0; L < 2; ++L) memcpy(a_in + (size_t)L * N, innerq + ((size_t)L * 2 + 0) * N, sizeof(uint32_t) * N);
+      ks_digits(a_in, N, m, D);
+      rotate_with_digits(innerq, D, N, j * b * d, keys_giant + (size_t)(j - 1) * 24 * N, m, rot);
+      part = rot;
+    }
+    for (int L = 0; L < 2; ++L)
+      for (size_t k = 0; k < (size_t)2 * N; ++k) {
+        const size_t x = (size_t)L * 2 * N + k;
+        acc[x] = (uint32_t)(((uint64_t)acc[x] + part[x]) % m[L]);
+      }
+  }
+  const uint32_t q0 = m[0], q1 = m[1];
+  const uint64_t q1inv = powmod(q1 % q0, q0 - 2, q0);
+  for (int ab = 0; ab < 2; ++ab)
+    for (uint32_t k = 0; k < N; ++k) {
+      const uint32_t x0 = acc[(size_t)ab * N + k], x1 = acc[((size_t)2 + ab) * N + k];
+      const int64_t x1c = x1 > q1 / 2 ? (int64_t)x1 - q1 : (int64_t)x1;
+      out[(size_t)ab * N + k] = (uint32_t)mulmod(modq_i64((int64_t)x0 - x1c, q0), q1inv, q0);
+    }
+  free(D); free(a_in); free(baby); free(U); free(W); free(sd); free(t); free(acc); free(inner); free(innerq);
+  free(rot); free(XA); free(XB); free(xa); free(xb);
+  return 0;
+}
+
 /* hesim pcmm_bsgs (matmul.py:165-176): the BSGS map with stride d over the d blocks */
 int or_slot_pcmm(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t g, const uint32_t* ct_in,
                  const uint32_t* pts, const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out) {

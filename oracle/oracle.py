@@ -575,6 +575,8 @@ def _sd_bind():
         L.or_slot_pcmm.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
         L.or_slot_bsgs.restype = ctypes.c_int
         L.or_slot_bsgs.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
+        L.or_slot_bsgs_lazy.restype = ctypes.c_int
+        L.or_slot_bsgs_lazy.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
         L._sd_bound = True
     return L
 
@@ -607,15 +609,17 @@ def slot_pcmm(params, ct_in: np.ndarray, pts: np.ndarray, d: int, b: int, g: int
 
 
 def slot_bsgs(params, ct_in: np.ndarray, pts: np.ndarray, stride: int, b: int, g: int, keys_baby,
-              keys_giant) -> np.ndarray:
+              keys_giant, lazy: bool = False) -> np.ndarray:
     """or_slot_bsgs: the general BSGS slot map (baby steps i stride, giant steps j b stride) -- SlotToCoeffs
-    with stride 1.  pts [b g, 2, N] residues (coefficient form) -> [2, N] level 0."""
+    with stride 1.  pts [b g, 2, N] residues (coefficient form) -> [2, N] level 0.  lazy: or_slot_bsgs_lazy
+    (baby rotations kept mod PQ, one ModDown per group), pts [b g, 3, N] (q0, q1, P)."""
     N = params.N
     m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
     out = np.zeros((2, N), np.uint32)
     kb = np.ascontiguousarray(keys_baby if len(keys_baby) else np.zeros((1, 4, 2, 3, N), np.uint32), dtype=np.uint32)
     kg = np.ascontiguousarray(keys_giant if len(keys_giant) else np.zeros((1, 4, 2, 3, N), np.uint32), dtype=np.uint32)
-    rc = _sd_bind().or_slot_bsgs(N, _u32(m), stride, b, g, _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
+    fn = _sd_bind().or_slot_bsgs_lazy if lazy else _sd_bind().or_slot_bsgs
+    rc = fn(N, _u32(m), stride, b, g, _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
                                  _u32(np.ascontiguousarray(pts, dtype=np.uint32)), _u32(kb), _u32(kg), _u32(out))
     if rc:
         raise ValueError("slot_bsgs: split x stride exceeds the slots")

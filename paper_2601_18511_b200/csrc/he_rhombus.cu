@@ -1249,6 +1249,33 @@ __global__ void k_sd_mac(const uint32_t* __restrict__ D, uint32_t dcnt, int hois
     UW[(((size_t)mod * cnt + z) * 2 + 1) * N + c] = barrett64(w, mu, q);
   }
 }
+// lazy form of k_sd_mac for the baby steps: the key MAC written straight as the PQ-basis rotation
+// baby'_z [mod][ab][N] = (U, W + P sigma(b^)) at out + z 6N (k_sd_lazy_baby fused in: no UW round trip)
+__global__ void k_sd_mac_lazy(const uint32_t* __restrict__ D, const uint32_t* __restrict__ perms,
+                              const uint32_t* __restrict__ K, const uint32_t* __restrict__ bh, uint64_t bls, uint32_t N,
+                              Mods M, uint32_t* __restrict__ out) {
+  const uint32_t mod = blockIdx.y, z = blockIdx.z;
+  const uint32_t q = mod == 0 ? M.m[0] : (mod == 1 ? M.m[1] : M.m[2]);
+  const uint64_t mu = mod == 0 ? M.mu[0] : (mod == 1 ? M.mu[1] : M.mu[2]);
+  const uint32_t pm = M.m[2] % q;
+  const uint32_t* perm = perms + (size_t)z * N;
+  const uint32_t* Kz = K + (size_t)z * 24 * N;
+  const uint32_t* Dz = D + (size_t)mod * kSdT * N;
+  uint32_t* o = out + (size_t)z * 6 * N + (size_t)mod * 2 * N;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+    const uint32_t pc = perm[c];
+    uint64_t u = 0, w = 0;
+#pragma unroll
+    for (int t = 0; t < kSdT; ++t) {
+      const uint64_t dv = Dz[(size_t)t * N + pc];
+      u += dv * Kz[(size_t)((t * 2 + 0) * 3 + mod) * N + c];
+      w += dv * Kz[(size_t)((t * 2 + 1) * 3 + mod) * N + c];
+    }
+    o[c] = barrett64(u, mu, q);
+    const uint32_t wr = barrett64(w, mu, q);
+    o[N + c] = mod < 2 ? add_mod(wr, mulmod_b(bh[mod * bls + pc], pm, mu, q), q) : wr;
+  }
+}
 // rotated ct z (NTT domain) [L][ab][N] at out + z * os: a = (U - LB_u) P^-1, b = sigma(b^_z) + (W - LB_w) P^-1
 // (LB [L][z][part][N]; b^_z at bh + z * bs, limb stride bls)
 __global__ void k_sd_combine(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ LB,
@@ -1347,7 +1374,7 @@ constexpr int kSdSharedThreads = 512;
 template <int CT>
 __global__ void __launch_bounds__(kSdSharedThreads, 1)
     k_sd_inner_s(const uint32_t* __restrict__ baby, uint64_t baby_cs, const uint32_t* __restrict__ pts, uint32_t b,
-                 uint32_t g, uint32_t N, Mods M, uint32_t* __restrict__ inner, uint64_t inner_cs) {
+                 uint32_t g, uint32_t N, uint32_t nl, Mods M, uint32_t* __restrict__ inner, uint64_t inner_cs) {
   extern __shared__ __align__(16) uint32_t sbaby[];
   const uint32_t L = blockIdx.y, c0 = blockIdx.x * kSdTile, q = M.m[L];
   const uint64_t mu = M.mu[L];
@@ -1355,7 +1382,7 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
   // stage: row r = ct b + i holds 32 (a, b) pairs; 8 threads per row, 4 coefficients each
   for (uint32_t r = threadIdx.x >> 3; r < CT * b; r += blockDim.x >> 3) {
     const uint32_t ct = r / b, i = r % b, t = threadIdx.x & 7;
-    const uint32_t* src = baby + ct * baby_cs + ((size_t)i * 4 + L * 2) * N + c0;
+    const uint32_t* src = baby + ct * baby_cs + ((size_t)i * nl + L) * 2 * N + c0;
     const uint4 va = reinterpret_cast<const uint4*>(src)[t];
     const uint4 vb = reinterpret_cast<const uint4*>(src + N)[t];
     uint4* dst = reinterpret_cast<uint4*>(sbaby + (size_t)r * 2 * kSdTile) + 2 * t;
@@ -1363,11 +1390,11 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
     dst[1] = make_uint4(va.z, vb.z, va.w, vb.w);
   }
   __syncthreads();
-  const size_t tstride = 2ull * N;   // words between consecutive terms
+  const size_t tstride = (size_t)nl * N;   // words between consecutive terms
   const uint2* sl = reinterpret_cast<const uint2*>(sbaby) + lane;
   for (uint32_t j0 = warp * 2; j0 < g; j0 += 2 * (blockDim.x >> 5)) {
     const bool two = j0 + 1 < g;
-    const uint32_t* P0 = pts + ((size_t)j0 * b * 2 + L) * N + c0 + lane;
+    const uint32_t* P0 = pts + ((size_t)j0 * b * nl + L) * N + c0 + lane;
     const uint32_t* P1 = two ? P0 + (size_t)b * tstride : P0;
     uint64_t acc[2][CT][2];
 #pragma unroll
@@ -1408,7 +1435,7 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
       for (int ct = 0; ct < CT; ++ct)
 #pragma unroll
         for (int ab = 0; ab < 2; ++ab)
-          inner[ct * inner_cs + ((size_t)(j0 + h) * 4 + L * 2 + ab) * N + c0 + lane] = (uint32_t)acc[h][ct][ab];
+          inner[ct * inner_cs + (((size_t)(j0 + h) * nl + L) * 2 + ab) * N + c0 + lane] = (uint32_t)acc[h][ct][ab];
     }
   }
 }
@@ -1423,18 +1450,48 @@ __global__ void k_sd_accumulate(const uint32_t* __restrict__ inner0, const uint3
   }
 }
 // signed int64 plaintext polys [count][N] -> [count][2 limbs][N] residues (NTT'd afterwards)
-__global__ void k_sd_reduce_pts(const int64_t* __restrict__ pt, uint64_t total, uint32_t logN, Mods M,
+__global__ void k_sd_reduce_pts(const int64_t* __restrict__ pt, uint64_t total, uint32_t logN, uint32_t nl, Mods M,
                                 uint32_t* __restrict__ out) {
   const uint32_t N = 1u << logN;
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = x >> logN;
     const uint32_t c = (uint32_t)(x & (N - 1));
     const int64_t v = pt[x];
-#pragma unroll
-    for (int L = 0; L < 2; ++L) {
+    for (uint32_t L = 0; L < nl; ++L) {
       const int64_t r = v % (int64_t)M.m[L];
-      out[(k * 2 + L) * N + c] = (uint32_t)(r < 0 ? r + M.m[L] : r);
+      out[(k * nl + L) * N + c] = (uint32_t)(r < 0 ? r + M.m[L] : r);
     }
+  }
+}
+// lazy ModDown (hoisted BSGS; baby rotations from k_sd_mac_lazy):
+// baby'_0 = P ct (q0, q1), 0 mod P
+__global__ void k_sd_lazy_baby0(const uint32_t* __restrict__ X, uint32_t N, Mods M, uint32_t* __restrict__ out) {
+  const uint32_t mod = blockIdx.y, q = M.m[mod];
+  const uint64_t mu = M.mu[mod];
+  const uint32_t pm = M.m[2] % q;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < 2 * N; c += gridDim.x * blockDim.x)
+    out[(size_t)mod * 2 * N + c] = mod < 2 ? mulmod_b(X[(size_t)mod * 2 * N + c], pm, mu, q) : 0u;
+}
+// ModDown of the g group sums [j][3][ab][N] (P part already inverse-NTT'd): LB [L][j][ab][N] = centred lift
+__global__ void k_sd_lazy_lift(const uint32_t* __restrict__ X, uint32_t g, uint32_t N, Mods M, uint32_t* __restrict__ LB) {
+  const uint32_t L = blockIdx.y, q = M.m[L], P = M.m[2];
+  const uint64_t tot = 2ull * g * N;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < tot; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = x / (2ull * N), r = x % (2ull * N);
+    const uint32_t v = X[j * 6 * N + 4ull * N + r];
+    const uint32_t vq = v % q;
+    LB[(uint64_t)L * tot + x] = v > P / 2 ? sub_mod(vq, P % q, q) : vq;   // v - P when v is "negative"
+  }
+}
+// inner_j [L][ab][N] = (X_L - LB_L) P^-1 mod q_L  (NTT domain; Q layout [j][4N] for the giant step)
+__global__ void k_sd_lazy_down(const uint32_t* __restrict__ X, const uint32_t* __restrict__ LB, uint32_t g,
+                               uint32_t N, Mods M, uint32_t pinv0, uint32_t pinv1, uint32_t* __restrict__ out) {
+  const uint32_t L = blockIdx.y, q = M.m[L], pinv = L ? pinv1 : pinv0;
+  const uint64_t mu = M.mu[L], tot = 2ull * g * N;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < tot; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = x / (2ull * N), r = x % (2ull * N);
+    out[j * 4 * N + (uint64_t)L * 2 * N + r] =
+        mulmod_b(sub_mod(X[j * 6 * N + (uint64_t)L * 2 * N + r], LB[(uint64_t)L * tot + x], q), pinv, mu, q);
   }
 }
 
@@ -1448,6 +1505,8 @@ struct he_slot_pcmm_plan {
   Mods M;
   uint32_t qhinv[2], qhinvp[2], pinv[2], q1inv, q1invp;
   uint32_t chunk;        // ciphertexts per shared-plaintext pass (1: per-ct kernels; 2-3: k_sd_inner_s)
+  uint32_t shared;       // products through k_sd_inner_s
+  uint32_t lazy;         // lazy ModDown: baby rotations kept mod PQ, pts carry 3 moduli, one ModDown per group
 };
 
 // gadget key (layout [t][part][mod][deg], t = i kSdSub + h), NTT domain; streams use t as the digit index
@@ -1506,10 +1565,24 @@ extern "C" he_status he_slot_pcmm_encode_pts(const he_context* c, const int64_t*
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t N = c->R.N;
   const Mods M = make_mods(c->R);
-  k_sd_reduce_pts<<<grid_for((uint64_t)count * N), 256, 0, st>>>(pt_dev, (uint64_t)count * N, (uint32_t)ilog2_u(N), M,
-                                                                   pts_ntt_dev);
+  k_sd_reduce_pts<<<grid_for((uint64_t)count * N), 256, 0, st>>>(pt_dev, (uint64_t)count * N, (uint32_t)ilog2_u(N), 2u,
+                                                                   M, pts_ntt_dev);
   for (int L = 0; L < 2; ++L)
     HE_CUDA(ntt_forward(c->ntt[L], pts_ntt_dev + (size_t)L * N, count, 2ull * N, st), "NTT(pt)");
+  return HE_OK;
+}
+
+extern "C" he_status he_slot_pcmm_encode_pts_ext(const he_context* c, const int64_t* pt_dev, uint32_t count,
+                                                 uint32_t n_mods, uint32_t* pts_ntt_dev, void* stream) {
+  if (!c || !pt_dev || !pts_ntt_dev) return fail(HE_EINVAL, "null argument");
+  if (n_mods != 2 && n_mods != 3) return fail(HE_EINVAL, "n_mods must be 2 (q0, q1) or 3 (q0, q1, P)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N;
+  const Mods M = make_mods(c->R);
+  k_sd_reduce_pts<<<grid_for((uint64_t)count * N), 256, 0, st>>>(pt_dev, (uint64_t)count * N, (uint32_t)ilog2_u(N),
+                                                                   n_mods, M, pts_ntt_dev);
+  for (uint32_t L = 0; L < n_mods; ++L)
+    HE_CUDA(ntt_forward(c->ntt[L], pts_ntt_dev + (size_t)L * N, count, (uint64_t)n_mods * N, st), "NTT(pt)");
   return HE_OK;
 }
 
@@ -1537,11 +1610,14 @@ static he_status slot_plan_make(const he_context* c, const uint32_t* pts_ntt_dev
   p->q1invp = shoup_pre(p->q1inv, p->M.m[0]);
   // big maps stream their plaintexts once per up-to-3 ciphertexts (shared-memory baby tiles, CT b 256 B)
   p->chunk = 1;
+  p->shared = 0;
+  p->lazy = 0;
   const bool shared_ok = b % 16 == 0 && N % kSdTile == 0 && p->M.m[0] < (1u << 30) && p->M.m[1] < (1u << 30);
   if (((uint64_t)b * g >= 4096 || getenv("HE_SD_SHARED")) && shared_ok && !getenv("HE_SD_PER_CT"))
     for (uint32_t c = 3; c >= 2; --c)
       if ((uint64_t)c * b * 2 * kSdTile * 4 <= 200 * 1024) {
         p->chunk = c;
+        p->shared = 1;
         break;
       }
   std::vector<uint32_t> h((size_t)(steps.empty() ? 1 : steps.size()) * N);
@@ -1600,6 +1676,21 @@ extern "C" he_status he_slot_bsgs_plan_create(const he_context* c, const uint32_
   return slot_plan_make(c, pts_ntt_dev, b * g, b, g, steps, out);
 }
 
+extern "C" he_status he_slot_bsgs_plan_create_ext(const he_context* c, const uint32_t* pts_ntt_dev, uint32_t b,
+                                                  uint32_t g, uint32_t stride, uint32_t flags, he_slot_pcmm_plan** out) {
+  if (!(flags & HE_SLOT_LAZY_MODDOWN)) return he_slot_bsgs_plan_create(c, pts_ntt_dev, b, g, stride, out);
+  if (!c || !out) return fail(HE_EINVAL, "null argument");
+  const Mods M = make_mods(c->R);
+  if (b % 16 || c->R.N % kSdTile || (uint64_t)b * 2 * kSdTile * 4 > 200 * 1024 || M.m[0] >= (1u << 30) ||
+      M.m[1] >= (1u << 30) || M.m[2] >= (1u << 30))
+    return fail(HE_EINVAL, "lazy ModDown needs b %% 16 == 0, b <= 400 and 30-bit moduli (b = %u)", b);
+  he_status s = he_slot_bsgs_plan_create(c, pts_ntt_dev, b, g, stride, out);
+  if (s) return s;
+  (*out)->lazy = 1;
+  (*out)->shared = 1;
+  return HE_OK;
+}
+
 extern "C" he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* p) {
   if (p) {
     if (p->perms) cudaFree(p->perms);
@@ -1609,7 +1700,7 @@ extern "C" he_status he_slot_pcmm_plan_destroy(he_slot_pcmm_plan* p) {
 }
 
 struct SdWs {
-  uint32_t *D, *X, *baby, *inner, *rot, *acc, *UW, *LB;
+  uint32_t *D, *X, *baby, *inner, *innerq, *rot, *acc, *UW, *LB;
 };
 static uint64_t sd_ws_words(const he_slot_pcmm_plan* p, SdWs* w, uint32_t* base) {
   const uint64_t N = p->N, T = (p->b > p->g ? p->b : p->g), C = p->chunk;   // rotations per batched pass < T
@@ -1622,8 +1713,10 @@ static uint64_t sd_ws_words(const he_slot_pcmm_plan* p, SdWs* w, uint32_t* base)
   SdWs& r = w ? *w : dummy;
   take(r.D, 3ull * kSdT * T * N);
   take(r.X, 4 * N);
-  take(r.baby, 4ull * p->b * N * C);
-  take(r.inner, 4ull * p->g * N * C);
+  const uint64_t cw = p->lazy ? 6 : 4;   // words per N of a baby / group ct (3 moduli when lazy)
+  take(r.baby, cw * p->b * N * C);
+  take(r.inner, cw * p->g * N * C);
+  take(r.innerq, p->lazy ? 4ull * p->g * N : 0);
   take(r.rot, 4ull * T * N);
   take(r.acc, 4 * N);
   take(r.UW, 6ull * T * N);
@@ -1639,12 +1732,13 @@ extern "C" he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* p, ui
 
 template <int CT>
 static cudaError_t launch_sd_inner_s(const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts, uint32_t b,
-                                     uint32_t g, uint32_t N, const Mods& M, uint32_t* inner, uint64_t inner_cs,
-                                     cudaStream_t st) {
+                                     uint32_t g, uint32_t N, uint32_t nl, const Mods& M, uint32_t* inner,
+                                     uint64_t inner_cs, cudaStream_t st) {
   const int smem = CT * (int)b * 2 * kSdTile * 4;
   cudaError_t e = cudaFuncSetAttribute(k_sd_inner_s<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_sd_inner_s<CT><<<dim3(N / kSdTile, 2), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, M, inner, inner_cs);
+  k_sd_inner_s<CT><<<dim3(N / kSdTile, nl), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, nl, M, inner,
+                                                                          inner_cs);
   return cudaGetLastError();
 }
 
@@ -1686,7 +1780,8 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
     return HE_OK;
   };
   static const bool inner_simple = getenv("HE_SD_INNER_SIMPLE") != nullptr;
-  const uint64_t baby_cs = 4ull * b * N, inner_cs = 4ull * g * N;
+  const uint32_t nl = p->lazy ? 3 : 2;   // moduli the products run over
+  const uint64_t baby_cs = 2ull * nl * b * N, inner_cs = 2ull * nl * g * N;
   for (uint32_t c0 = 0; c0 < n_ct; c0 += p->chunk) {
     const uint32_t cc = std::min(p->chunk, n_ct - c0);
     // baby steps per ciphertext: one hoisted digit decomposition, all b - 1 rotations in one pass
@@ -1697,17 +1792,27 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
       if (s) return s;
       HE_CUDA(cudaMemcpyAsync(w.X, ct, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
       for (int L = 0; L < 2; ++L) HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
-      HE_CUDA(cudaMemcpyAsync(bz, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
-      if (b > 1) {
-        s = rotate(b - 1, 1, 1, 0, keys_baby, w.X + N, 0, bz + 4ull * N);
-        if (s) return s;
+      if (p->lazy) {
+        // P ct, then the rotations straight from the key MAC (no ModDown): [i][3 moduli][ab][N]
+        k_sd_lazy_baby0<<<grid3(3, 1), 256, 0, st>>>(w.X, N, p->M, bz);
+        if (b > 1) {
+          k_sd_mac_lazy<<<grid3(3, b - 1), 256, 0, st>>>(w.D, p->perms, keys_baby, w.X + N, 2ull * N, N, p->M,
+                                                        bz + 6ull * N);
+        }
+      } else {
+        HE_CUDA(cudaMemcpyAsync(bz, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
+        if (b > 1) {
+          s = rotate(b - 1, 1, 1, 0, keys_baby, w.X + N, 0, bz + 4ull * N);
+          if (s) return s;
+        }
       }
     }
     // giant-group products: all groups (and all cc ciphertexts) in one launch
-    if (p->chunk > 1) {
-      cudaError_t e = cc == 3   ? launch_sd_inner_s<3>(w.baby, baby_cs, p->pts, b, g, N, p->M, w.inner, inner_cs, st)
-                      : cc == 2 ? launch_sd_inner_s<2>(w.baby, baby_cs, p->pts, b, g, N, p->M, w.inner, inner_cs, st)
-                                : launch_sd_inner_s<1>(w.baby, baby_cs, p->pts, b, g, N, p->M, w.inner, inner_cs, st);
+    if (p->shared) {
+      cudaError_t e =
+          cc == 3   ? launch_sd_inner_s<3>(w.baby, baby_cs, p->pts, b, g, N, nl, p->M, w.inner, inner_cs, st)
+          : cc == 2 ? launch_sd_inner_s<2>(w.baby, baby_cs, p->pts, b, g, N, nl, p->M, w.inner, inner_cs, st)
+                    : launch_sd_inner_s<1>(w.baby, baby_cs, p->pts, b, g, N, nl, p->M, w.inner, inner_cs, st);
       HE_CUDA(e, "slot map products (shared)");
     } else if (g >= 8 && !inner_simple) {
       dim3 gi = grid_for(N / 2);
@@ -1720,6 +1825,18 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
     // giant rotations per ciphertext (one pass each), sum, one rescale
     for (uint32_t z = 0; z < cc; ++z) {
       uint32_t* iz = w.inner + z * inner_cs;
+      if (p->lazy) {
+        // one ModDown per group sum: INTT of the P parts, centred lift, NTT, (X - lift) P^-1 -> [j][4N]
+        for (int ab = 0; ab < 2; ++ab)
+          HE_CUDA(ntt_inverse(c->ntt[2], iz + (4ull + ab) * N, g, 6ull * N, st), "INTT(group sums, P)");
+        dim3 gl = grid_for(2ull * g * N);
+        gl.y = 2;
+        k_sd_lazy_lift<<<gl, 256, 0, st>>>(iz, g, N, p->M, w.LB);
+        HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2 * g, N, st), "NTT(lift q0)");
+        HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2ull * g * N, 2 * g, N, st), "NTT(lift q1)");
+        k_sd_lazy_down<<<gl, 256, 0, st>>>(iz, w.LB, g, N, p->M, p->pinv[0], p->pinv[1], w.innerq);
+        iz = w.innerq;
+      }
       if (g > 1) {
         uint32_t* in1 = iz + 4ull * N;   // groups 1 .. g-1
         for (int L = 0; L < 2; ++L)

@@ -36,7 +36,7 @@ from .layout import bit_reverse_table, coeff_table
 from .slotpcmm import BsgsSplit, SlotPcmmKeys, SlotPcmmPlan
 
 
-DEFAULT_PT_SHIFT = -1   # plaintexts at q1 / 2, input slots at 2 Delta (see make_slot_to_coeffs_plan)
+DEFAULT_PT_SHIFT = 1    # plaintexts at 2 q1, input slots at Delta / 2 (see make_slot_to_coeffs_plan)
 
 
 @dataclass
@@ -108,27 +108,32 @@ def stc_plaintexts(params, split: BsgsSplit, k0: int, count: int, device="cpu", 
 
 
 def make_slot_to_coeffs_plan(ctx: HeContext, split: BsgsSplit | None = None, batch: int = 256,
-                             pt_shift: int = DEFAULT_PT_SHIFT) -> SlotPcmmPlan:
+                             pt_shift: int = DEFAULT_PT_SHIFT, lazy: bool = True) -> SlotPcmmPlan:
     """The n = N/2 diagonals of M, BSGS-ordered and NTT'd into [n, 2, N] device residues, encoded at scale
     q1 2^pt_shift: the output keeps scale Delta when the input slots carry Delta / 2^pt_shift
-    (plan.input_scale, what encrypt_slots uses).  The error has two parts (tools/stc_precision.py, N = 2^16):
-    the baby rotations' ModDown rounding noise (~60 per coefficient, amplified sqrt(n) by the map, so it
-    scales as 1 / input_scale) and the plaintext rounding (scales as 1 / (q1 2^pt_shift)); they balance
-    at pt_shift = -1: 11.6 bits (10.7 at 0, 11.1 at -2)."""
+    (plan.input_scale, what encrypt_slots uses).  lazy (default): the baby rotations stay in the PQ basis
+    straight from the key MAC and each giant group sum is ModDown'd once after the products (plaintexts also
+    mod P, HE_SLOT_LAZY_MODDOWN), so their ModDown rounding noise (~60 per coefficient with the dense key) is
+    never amplified by the map.  Error (tools/stc_precision.py, N = 2^16): lazy 13.1 / 13.5 / 12.5 bits at
+    pt_shift 0 / 1 / 2 (plaintext rounding vs input noise balance at 1); eager ModDown 10.7 bits at 0, 11.6
+    at -1 (rotation noise, amplified sqrt(n), dominates)."""
     torch = _torch()
     N, n = ctx.params.N, ctx.params.N // 2
     split = split or stc_split(n)
     if split.baby * split.giant != n:
         raise ValueError(f"split {split.baby}x{split.giant} does not cover the {n} slots")
     plan = SlotPcmmPlan(n, 0, split, np.zeros((0, 0)))
-    plan.pts = torch.empty((n, 2, N), dtype=torch.int32, device=ctx.device)
+    nm = 3 if lazy else 2
+    plan.pts = torch.empty((n, nm, N), dtype=torch.int32, device=ctx.device)
     for k0 in range(0, n, batch):
         cnt = min(batch, n - k0)
         pt = stc_plaintexts(ctx.params, split, k0, cnt, ctx.device, pt_shift).contiguous()
-        native.call("he_slot_pcmm_encode_pts", ctx.handle, pt.data_ptr(), cnt, plan.pts[k0].data_ptr(), ctx.stream())
+        native.call("he_slot_pcmm_encode_pts_ext", ctx.handle, pt.data_ptr(), cnt, nm, plan.pts[k0].data_ptr(),
+                    ctx.stream())
     h = ctypes.c_void_p()
-    native.call("he_slot_bsgs_plan_create", ctx.handle, plan.pts.data_ptr(), split.baby, split.giant, 1,
-                ctypes.byref(h))
+    native.call("he_slot_bsgs_plan_create_ext", ctx.handle, plan.pts.data_ptr(), split.baby, split.giant, 1,
+                1 if lazy else 0, ctypes.byref(h))
+    plan.lazy = lazy
     plan._handle = h
     b, g = split.baby, split.giant
     plan.steps = tuple(range(1, b)) + tuple(j * b for j in range(1, g))
@@ -157,7 +162,7 @@ def slot_to_coeffs_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, see
 def encrypt_slots(ctx: HeContext, sk: SecretKey, acts, seed: int, r0: int = 0, scale: float | None = None) -> SlotBlocks:
     """Slot-encode and encrypt a (d/2) x n_in activation block at level 1, one ct per k columns -- the state
     the attention phase leaves behind.  scale: the plan's input_scale (Delta 2^-pt_shift,
-    2 Delta by default) so that StC lands at Delta; None = the default plan's."""
+    Delta / 2 by default) so that StC lands at Delta; None = the default plan's."""
     torch = _torch()
     z = slot_vectors(ctx.params, acts)
     sc = ctx.params.delta / 2.0 ** DEFAULT_PT_SHIFT if scale is None else float(scale)

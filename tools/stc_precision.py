@@ -15,14 +15,15 @@ sk = ctx.keygen(1)
 P = ctx.params
 n = P.N // 2
 A = np.random.default_rng(0).uniform(-1, 1, (P.mlwe_degree // 2, P.mlwe_rank))
-for t in [int(v) for v in sys.argv[1:]] or [0, 2, 4, 6]:
-    plan = make_slot_to_coeffs_plan(ctx, pt_shift=t)
+lazy = "--lazy" in sys.argv
+for t in [int(v) for v in sys.argv[1:] if v != "--lazy"] or [0, 2, 4, 6]:
+    plan = make_slot_to_coeffs_plan(ctx, pt_shift=t, lazy=lazy)
     keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=2)
     X = encrypt_slots(ctx, sk, A, seed=3, scale=plan.input_scale)
     Y = slot_to_coeffs(ctx, plan, keys, X)
     ph = ctx.decrypt_phase(sk, Y).cpu().numpy()[0].astype(float) / P.delta
     err = np.abs(ctx.decrypt_acts(sk, Y) - A)
-    print(f"pt_shift {t}: max err {err.max():.2e} ({-np.log2(err.max()):.1f} bits), rms {np.sqrt((err ** 2).mean()):.2e}, "
+    print(f"{'lazy ' if lazy else ''}pt_shift {t}: max err {err.max():.2e} ({-np.log2(err.max()):.1f} bits), rms {np.sqrt((err ** 2).mean()):.2e}, "
           f"imag half max {np.abs(ph[n:]).max():.2e}", flush=True)
     del plan, keys, X, Y
     torch.cuda.empty_cache()
