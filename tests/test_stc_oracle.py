@@ -52,7 +52,9 @@ def test_plaintexts_are_the_rotated_diagonals():
             assert np.abs(got - want).max() < 1e-3
 
 
-def test_oracle_stc_decrypts_to_app_a_coefficients():
+@pytest.mark.parametrize("lazy", [False, True])
+def test_oracle_stc_decrypts_to_app_a_coefficients(lazy):
+    """Both BSGS forms (per-rotation ModDown; lazy ModDown in the PQ basis, plaintexts also mod P)."""
     rng = np.random.default_rng(2)
     d, k = P.mlwe_degree, P.mlwe_rank
     N, n = P.N, P.N // 2
@@ -60,12 +62,13 @@ def test_oracle_stc_decrypts_to_app_a_coefficients():
     split = stc_split(n)
     b, g = split.baby, split.giant
     pt = stc_plaintexts(P, split, 0, n).numpy()
-    pts = np.stack([np.stack([(pt[t] % q).astype(np.uint32) for q in P.moduli]) for t in range(n)])
+    mods = P.ks_moduli if lazy else P.moduli
+    pts = np.stack([np.stack([(pt[t] % q).astype(np.uint32) for q in mods]) for t in range(n)])
     s = O.keygen(P, 7)
     ct = O.encrypt(P, 11, s, slots.encode(slot_vectors(P, A)[0], N, P.delta)[None])[0]
     kb = O.rotation_keys(P, 13, s, list(range(1, b)))
     kg = O.rotation_keys(P, 13, s, [j * b for j in range(1, g)])
-    out = O.slot_bsgs(P, ct, pts, 1, b, g, kb, kg)
+    out = O.slot_bsgs(P, ct, pts, 1, b, g, kb, kg, lazy=lazy)
     ph = O.decrypt_under(P, out[0], out[1], s, P.moduli[0])
     want = O.encode_acts(P, A)[0]
     err = np.abs(ph - want)
@@ -73,4 +76,4 @@ def test_oracle_stc_decrypts_to_app_a_coefficients():
     assert err[n:].max() < P.delta * 2.0 ** -12          # imaginary half: noise only
     np.testing.assert_allclose(O.decode_acts(P, ph[None], k), A, atol=2.0 ** -12)
     with pytest.raises(ValueError):
-        O.slot_bsgs(P, ct, pts, 2, b, g, kb, kg)          # 2 b g > N/2
+        O.slot_bsgs(P, ct, pts, 2, b, g, kb, kg, lazy=lazy)   # 2 b g > N/2
