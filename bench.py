@@ -579,7 +579,7 @@ def stc_side(P, dev, reps=3):
     sk = ctx.keygen(61)
     plan = make_slot_to_coeffs_plan(ctx)
     keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=63)
-    A = np.random.default_rng(65).uniform(-1, 1, (P.mlwe_degree // 2, 3 * P.mlwe_rank))
+    A = np.random.default_rng(65).uniform(-1, 1, (P.mlwe_degree // 2, 6 * P.mlwe_rank))
     X = encrypt_slots(ctx, sk, A, seed=67)
     Y = slot_to_coeffs(ctx, plan, keys, X)
     torch.cuda.synchronize()

@@ -1374,14 +1374,16 @@ constexpr int kSdSharedThreads = 512;
 template <int CT>
 __global__ void __launch_bounds__(kSdSharedThreads, 1)
     k_sd_inner_s(const uint32_t* __restrict__ baby, uint64_t baby_cs, const uint32_t* __restrict__ pts, uint32_t b,
-                 uint32_t g, uint32_t N, uint32_t nl, Mods M, uint32_t* __restrict__ inner, uint64_t inner_cs) {
+                 uint32_t g, uint32_t N, uint32_t nl, Mods M, uint32_t* __restrict__ inner, uint64_t inner_cs,
+                 uint32_t ib, uint32_t bn, int accumulate) {
+  // baby terms i in [ib, ib + bn) of the b per group; accumulate: add the sums already in inner (second half)
   extern __shared__ __align__(16) uint32_t sbaby[];
   const uint32_t L = blockIdx.y, c0 = blockIdx.x * kSdTile, q = M.m[L];
   const uint64_t mu = M.mu[L];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // stage: row r = ct b + i holds 32 (a, b) pairs; 8 threads per row, 4 coefficients each
-  for (uint32_t r = threadIdx.x >> 3; r < CT * b; r += blockDim.x >> 3) {
-    const uint32_t ct = r / b, i = r % b, t = threadIdx.x & 7;
+  // stage: row r = ct bn + i holds 32 (a, b) pairs; 8 threads per row, 4 coefficients each
+  for (uint32_t r = threadIdx.x >> 3; r < CT * bn; r += blockDim.x >> 3) {
+    const uint32_t ct = r / bn, i = ib + r % bn, t = threadIdx.x & 7;
     const uint32_t* src = baby + ct * baby_cs + ((size_t)i * nl + L) * 2 * N + c0;
     const uint4 va = reinterpret_cast<const uint4*>(src)[t];
     const uint4 vb = reinterpret_cast<const uint4*>(src + N)[t];
@@ -1394,27 +1396,28 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
   const uint2* sl = reinterpret_cast<const uint2*>(sbaby) + lane;
   for (uint32_t j0 = warp * 2; j0 < g; j0 += 2 * (blockDim.x >> 5)) {
     const bool two = j0 + 1 < g;
-    const uint32_t* P0 = pts + ((size_t)j0 * b * nl + L) * N + c0 + lane;
+    const uint32_t* P0 = pts + (((size_t)j0 * b + ib) * nl + L) * N + c0 + lane;
     const uint32_t* P1 = two ? P0 + (size_t)b * tstride : P0;
     uint64_t acc[2][CT][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct) acc[h][ct][0] = acc[h][ct][1] = 0;
-    for (uint32_t i0 = 0; i0 < b; i0 += 16) {
-      uint32_t p0[16], p1[16];
+    constexpr int U = CT > 3 ? 8 : 16;   // terms loaded ahead (register budget: 2 U words + 4 CT sums)
+    for (uint32_t i0 = 0; i0 < bn; i0 += U) {
+      uint32_t p0[U], p1[U];
       const uint32_t* a0 = P0 + (size_t)i0 * tstride;
       const uint32_t* a1 = P1 + (size_t)i0 * tstride;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < U; ++u) {
         p0[u] = __ldg(a0 + u * tstride);
         p1[u] = __ldg(a1 + u * tstride);
       }
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct) {
-        const uint2* sr = sl + (size_t)(ct * b + i0) * kSdTile;
+        const uint2* sr = sl + (size_t)(ct * bn + i0) * kSdTile;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
+        for (int u = 0; u < U; ++u) {
           const uint2 xy = sr[u * kSdTile];
           acc[0][ct][0] += (uint64_t)p0[u] * xy.x;
           acc[0][ct][1] += (uint64_t)p0[u] * xy.y;
@@ -1434,8 +1437,10 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct)
 #pragma unroll
-        for (int ab = 0; ab < 2; ++ab)
-          inner[ct * inner_cs + (((size_t)(j0 + h) * nl + L) * 2 + ab) * N + c0 + lane] = (uint32_t)acc[h][ct][ab];
+        for (int ab = 0; ab < 2; ++ab) {
+          uint32_t* o = inner + ct * inner_cs + (((size_t)(j0 + h) * nl + L) * 2 + ab) * N + c0 + lane;
+          *o = accumulate ? add_mod((uint32_t)acc[h][ct][ab], *o, q) : (uint32_t)acc[h][ct][ab];
+        }
     }
   }
 }
@@ -1506,6 +1511,7 @@ struct he_slot_pcmm_plan {
   uint32_t qhinv[2], qhinvp[2], pinv[2], q1inv, q1invp;
   uint32_t chunk;        // ciphertexts per shared-plaintext pass (1: per-ct kernels; 2-3: k_sd_inner_s)
   uint32_t shared;       // products through k_sd_inner_s
+  uint32_t halves;       // baby range split (shared kernel runs once per half, accumulating)
   uint32_t lazy;         // lazy ModDown: baby rotations kept mod PQ, pts carry 3 moduli, one ModDown per group
 };
 
@@ -1612,14 +1618,22 @@ static he_status slot_plan_make(const he_context* c, const uint32_t* pts_ntt_dev
   p->chunk = 1;
   p->shared = 0;
   p->lazy = 0;
+  p->halves = 1;
   const bool shared_ok = b % 16 == 0 && N % kSdTile == 0 && p->M.m[0] < (1u << 30) && p->M.m[1] < (1u << 30);
-  if (((uint64_t)b * g >= 4096 || getenv("HE_SD_SHARED")) && shared_ok && !getenv("HE_SD_PER_CT"))
-    for (uint32_t c = 3; c >= 2; --c)
-      if ((uint64_t)c * b * 2 * kSdTile * 4 <= 200 * 1024) {
-        p->chunk = c;
-        p->shared = 1;
-        break;
-      }
+  if (((uint64_t)b * g >= 4096 || getenv("HE_SD_SHARED")) && shared_ok && !getenv("HE_SD_PER_CT")) {
+    // ciphertexts per plaintext read: as many (<= 6) as fit 200 KB of baby tiles.  HE_SD_HALVES=2 splits the
+    // baby range into two accumulating passes (6 instead of 3 cts at b = 256): measured no faster -- the
+    // products are issue-bound at 3 (StC: 3.1 vs 3.2 ms/ct), so it stays opt-in
+    const int env_halves = getenv("HE_SD_HALVES") ? atoi(getenv("HE_SD_HALVES")) : 0;
+    const uint32_t tile = 2 * kSdTile * 4;   // bytes per baby term per ct
+    auto fit = [&](uint32_t h) { return std::min<uint32_t>(6, (200u * 1024) / (b / h * tile)); };
+    const uint32_t h = (env_halves == 2 && b % 32 == 0) ? 2 : 1;
+    if (fit(h) >= 2) {
+      p->chunk = fit(h);
+      p->halves = h;
+      p->shared = 1;
+    }
+  }
   std::vector<uint32_t> h((size_t)(steps.empty() ? 1 : steps.size()) * N);
   for (size_t t = 0; t < steps.size(); ++t) {
     const uint64_t gal = powmod_h(5, steps[t] % (N / 2), 2ull * N);
@@ -1731,15 +1745,29 @@ extern "C" he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* p, ui
 }
 
 template <int CT>
-static cudaError_t launch_sd_inner_s(const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts, uint32_t b,
-                                     uint32_t g, uint32_t N, uint32_t nl, const Mods& M, uint32_t* inner,
-                                     uint64_t inner_cs, cudaStream_t st) {
-  const int smem = CT * (int)b * 2 * kSdTile * 4;
+static cudaError_t launch_sd_inner_s_ct(const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts, uint32_t b,
+                                        uint32_t g, uint32_t N, uint32_t nl, const Mods& M, uint32_t* inner,
+                                        uint64_t inner_cs, uint32_t halves, cudaStream_t st) {
+  const uint32_t bn = b / halves;
+  const int smem = CT * (int)bn * 2 * kSdTile * 4;
   cudaError_t e = cudaFuncSetAttribute(k_sd_inner_s<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_sd_inner_s<CT><<<dim3(N / kSdTile, nl), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, nl, M, inner,
-                                                                          inner_cs);
+  for (uint32_t h = 0; h < halves; ++h)
+    k_sd_inner_s<CT><<<dim3(N / kSdTile, nl), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, nl, M, inner,
+                                                                            inner_cs, h * bn, bn, h > 0);
   return cudaGetLastError();
+}
+static cudaError_t launch_sd_inner_s(uint32_t cc, const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts,
+                                     uint32_t b, uint32_t g, uint32_t N, uint32_t nl, const Mods& M, uint32_t* inner,
+                                     uint64_t inner_cs, uint32_t halves, cudaStream_t st) {
+  switch (cc) {
+    case 6: return launch_sd_inner_s_ct<6>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
+    case 5: return launch_sd_inner_s_ct<5>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
+    case 4: return launch_sd_inner_s_ct<4>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
+    case 3: return launch_sd_inner_s_ct<3>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
+    case 2: return launch_sd_inner_s_ct<2>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
+    default: return launch_sd_inner_s_ct<1>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
+  }
 }
 
 // n_ct ciphertexts [n_ct][2][2][N] level 1 -> out [n_ct][2][N] level 0, in chunks of p->chunk sharing each
@@ -1810,9 +1838,7 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
     // giant-group products: all groups (and all cc ciphertexts) in one launch
     if (p->shared) {
       cudaError_t e =
-          cc == 3   ? launch_sd_inner_s<3>(w.baby, baby_cs, p->pts, b, g, N, nl, p->M, w.inner, inner_cs, st)
-          : cc == 2 ? launch_sd_inner_s<2>(w.baby, baby_cs, p->pts, b, g, N, nl, p->M, w.inner, inner_cs, st)
-                    : launch_sd_inner_s<1>(w.baby, baby_cs, p->pts, b, g, N, nl, p->M, w.inner, inner_cs, st);
+          launch_sd_inner_s(cc, w.baby, baby_cs, p->pts, b, g, N, nl, p->M, w.inner, inner_cs, p->halves, st);
       HE_CUDA(e, "slot map products (shared)");
     } else if (g >= 8 && !inner_simple) {
       dim3 gi = grid_for(N / 2);

@@ -10,6 +10,7 @@ import oracle as O
 from paper_2601_18511_b200 import HeContext, HeParams, slots
 from paper_2601_18511_b200.errors import NeedsBootstrapError
 from paper_2601_18511_b200.pcmm import make_mlwe_pcmm_plan, pcmm_mlwe
+from paper_2601_18511_b200.slotpcmm import BsgsSplit
 from paper_2601_18511_b200.stc import (SlotBlocks, encrypt_slots, make_slot_to_coeffs_plan, slot_to_coeffs,
                                        slot_to_coeffs_keygen, slot_vectors, stc_plaintexts)
 
@@ -53,17 +54,19 @@ def test_toy_bit_exact_and_layout(lazy):
     assert np.abs(ph - O.encode_acts(P, A)).max() < P.delta * 2.0 ** -14
 
 
-@pytest.mark.parametrize("n_ct,lazy", [(4, False), (4, True)])
-def test_toy_batched_shared_path_bit_exact(n_ct, lazy, monkeypatch):
-    """The shared-memory multi-ciphertext products (forced at toy size; chunks of 3 + 1) give the oracle's
-    words for every ciphertext."""
+@pytest.mark.parametrize("n_ct,lazy,halves", [(4, False, 0), (4, True, 0), (7, True, 2), (7, False, 2)])
+def test_toy_batched_shared_path_bit_exact(n_ct, lazy, halves, monkeypatch):
+    """The shared-memory multi-ciphertext products (forced at toy size; up to 6 cts per plaintext read, the
+    baby range optionally split in two accumulating passes) give the oracle's words for every ciphertext."""
     monkeypatch.setenv("HE_SD_SHARED", "1")
+    if halves:
+        monkeypatch.setenv("HE_SD_HALVES", str(halves))
     P = HeParams.toy()
     ctx = HeContext(P)
     sk = ctx.keygen(7)
     d, k, N, n = P.mlwe_degree, P.mlwe_rank, P.N, P.N // 2
     A = np.random.default_rng(5).uniform(-1, 1, (d // 2, n_ct * k))
-    plan = make_slot_to_coeffs_plan(ctx, lazy=lazy)
+    plan = make_slot_to_coeffs_plan(ctx, lazy=lazy, split=BsgsSplit(32, 8) if halves else None)
     b, g = plan.split.baby, plan.split.giant
     keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=13)
     X = encrypt_slots(ctx, sk, A, seed=11)
@@ -117,7 +120,7 @@ def test_llama_ring():
     keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=13)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t0
-    A = np.random.default_rng(4).uniform(-1, 1, (d // 2, 3 * k))
+    A = np.random.default_rng(4).uniform(-1, 1, (d // 2, 6 * k))
     X = encrypt_slots(ctx, sk, A, seed=11)
     Y = slot_to_coeffs(ctx, plan, keys, X)                 # warm-up
     torch.cuda.synchronize()

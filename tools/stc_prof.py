@@ -14,7 +14,7 @@ sk = ctx.keygen(1)
 P = ctx.params
 plan = make_slot_to_coeffs_plan(ctx)
 keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=2)
-X = encrypt_slots(ctx, sk, np.random.default_rng(0).uniform(-1, 1, (P.mlwe_degree // 2, 3 * P.mlwe_rank)), seed=3)
+X = encrypt_slots(ctx, sk, np.random.default_rng(0).uniform(-1, 1, (P.mlwe_degree // 2, 6 * P.mlwe_rank)), seed=3)
 slot_to_coeffs(ctx, plan, keys, X)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
