@@ -1367,11 +1367,12 @@ __global__ void k_sd_inner_g(const uint32_t* __restrict__ baby, const uint32_t* 
 // the products for CT ciphertexts at once (big maps, e.g. SlotToCoeffs: 32 768 plaintexts = 17 GiB): a CTA owns 32
 // coefficients of one limb, stages the CT baby sets of that tile in shared memory ([ct][i][lane][a, b] pairs,
 // CT b 256 B) and streams every plaintext word of the tile exactly once, using it for all CT ciphertexts; warp w
-// runs the groups 2w, 2w + 1 (+32 ...), 16 plaintext terms per group loaded ahead.  b % 16 == 0 and q < 2^30:
-// 16 products < 2^60 plus a residue stay below 2^64, so the sums are reduced once per 16 terms
+// runs the groups 2w, 2w + 1 (+32 ...), 16 plaintext terms per group loaded ahead.  q < 2^30: products < 2^60,
+// so 8 of them plus a folded sum (< 2^62 + 2^32) stay below 2^64 -- one 32-bit fold per 8 terms, one
+// Barrett reduction per group
 constexpr int kSdTile = 32;
-constexpr int kSdSharedThreads = 512;
-template <int CT>
+constexpr int kSdSharedThreads = 512;   // 16 warps; 256 threads with 32 terms ahead measured 7% slower
+template <int CT, int U>
 __global__ void __launch_bounds__(kSdSharedThreads, 1)
     k_sd_inner_s(const uint32_t* __restrict__ baby, uint64_t baby_cs, const uint32_t* __restrict__ pts, uint32_t b,
                  uint32_t g, uint32_t N, uint32_t nl, Mods M, uint32_t* __restrict__ inner, uint64_t inner_cs,
@@ -1380,6 +1381,7 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
   extern __shared__ __align__(16) uint32_t sbaby[];
   const uint32_t L = blockIdx.y, c0 = blockIdx.x * kSdTile, q = M.m[L];
   const uint64_t mu = M.mu[L];
+  const uint32_t r32 = (uint32_t)((1ull << 32) % q);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // stage: row r = ct bn + i holds 32 (a, b) pairs; 8 threads per row, 4 coefficients each
   for (uint32_t r = threadIdx.x >> 3; r < CT * bn; r += blockDim.x >> 3) {
@@ -1403,7 +1405,6 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct) acc[h][ct][0] = acc[h][ct][1] = 0;
-    constexpr int U = CT > 3 ? 8 : 16;   // terms loaded ahead (register budget: 2 U words + 4 CT sums)
     for (uint32_t i0 = 0; i0 < bn; i0 += U) {
       uint32_t p0[U], p1[U];
       const uint32_t* a0 = P0 + (size_t)i0 * tstride;
@@ -1423,14 +1424,23 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
           acc[0][ct][1] += (uint64_t)p0[u] * xy.y;
           acc[1][ct][0] += (uint64_t)p1[u] * xy.x;
           acc[1][ct][1] += (uint64_t)p1[u] * xy.y;
-        }
+          if ((u & 7) == 7) {   // fold: hi 2^32 + lo == hi (2^32 mod q) + lo  (< 2^62 + 2^32; 8 more fit)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          acc[h][ct][0] = barrett64(acc[h][ct][0], mu, q);
-          acc[h][ct][1] = barrett64(acc[h][ct][1], mu, q);
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int ab = 0; ab < 2; ++ab)
+                acc[h][ct][ab] = (uint64_t)(uint32_t)(acc[h][ct][ab] >> 32) * r32 + (uint32_t)acc[h][ct][ab];
+          }
         }
       }
     }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct) {
+        acc[h][ct][0] = barrett64(acc[h][ct][0], mu, q);
+        acc[h][ct][1] = barrett64(acc[h][ct][1], mu, q);
+      }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (h == 1 && !two) break;
@@ -1744,18 +1754,28 @@ extern "C" he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* p, ui
   return HE_OK;
 }
 
+template <int CT, int U>
+static cudaError_t launch_sd_inner_s_cu(const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts, uint32_t b,
+                                        uint32_t g, uint32_t N, uint32_t nl, const Mods& M, uint32_t* inner,
+                                        uint64_t inner_cs, uint32_t halves, cudaStream_t st) {
+  const uint32_t bn = b / halves;
+  const int smem = CT * (int)bn * 2 * kSdTile * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_sd_inner_s<CT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  for (uint32_t h = 0; h < halves; ++h)
+    k_sd_inner_s<CT, U><<<dim3(N / kSdTile, nl), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, nl, M,
+                                                                               inner, inner_cs, h * bn, bn, h > 0);
+  return cudaGetLastError();
+}
+// U = plaintext terms loaded ahead per group (register budget: 2 U words + 4 CT sums); must divide the range
 template <int CT>
 static cudaError_t launch_sd_inner_s_ct(const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts, uint32_t b,
                                         uint32_t g, uint32_t N, uint32_t nl, const Mods& M, uint32_t* inner,
                                         uint64_t inner_cs, uint32_t halves, cudaStream_t st) {
   const uint32_t bn = b / halves;
-  const int smem = CT * (int)bn * 2 * kSdTile * 4;
-  cudaError_t e = cudaFuncSetAttribute(k_sd_inner_s<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  for (uint32_t h = 0; h < halves; ++h)
-    k_sd_inner_s<CT><<<dim3(N / kSdTile, nl), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, nl, M, inner,
-                                                                            inner_cs, h * bn, bn, h > 0);
-  return cudaGetLastError();
+  if (CT <= 2 && bn % 16 == 0)   // 128-register cap at 512 threads: 16 ahead fits two ciphertexts' sums
+    return launch_sd_inner_s_cu<CT, (CT <= 2 ? 16 : 8)>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
+  return launch_sd_inner_s_cu<CT, 8>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
 }
 static cudaError_t launch_sd_inner_s(uint32_t cc, const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts,
                                      uint32_t b, uint32_t g, uint32_t N, uint32_t nl, const Mods& M, uint32_t* inner,
