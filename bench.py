@@ -592,7 +592,8 @@ def stc_side(P, dev, reps=3):
     err = float(np.abs(ctx.decrypt_acts(sk, Y) - A).max())
     b, g = plan.split.baby, plan.split.giant
     res = {"workload": f"SlotToCoeffs, N = {P.N}: one {b}x{g} BSGS map over the {P.N // 2} diagonals per ct "
-                       "(App. A bit-reversal fused), 1 GPU",
+                       f"(App. A bit-reversal fused, {'lazy' if plan.lazy else 'eager'} ModDown, {X.n_ct} cts "
+                       "under one plan), 1 GPU",
            "ms_per_ct": round(e0.elapsed_time(e1) / reps / X.n_ct, 3), "rotations_per_ct": b + g - 2,
            "plaintext_bytes": int(plan.pts.numel() * 4), "precision_bits": round(-math.log2(err), 1)}
     del plan, keys, X, Y
