@@ -1249,31 +1249,40 @@ __global__ void k_sd_mac(const uint32_t* __restrict__ D, uint32_t dcnt, int hois
     UW[(((size_t)mod * cnt + z) * 2 + 1) * N + c] = barrett64(w, mu, q);
   }
 }
-// lazy form of k_sd_mac for the baby steps: the key MAC written straight as the PQ-basis rotation
-// baby'_z [mod][ab][N] = (U, W + P sigma(b^)) at out + z 6N (k_sd_lazy_baby fused in: no UW round trip)
-__global__ void k_sd_mac_lazy(const uint32_t* __restrict__ D, const uint32_t* __restrict__ perms,
-                              const uint32_t* __restrict__ K, const uint32_t* __restrict__ bh, uint64_t bls, uint32_t N,
-                              Mods M, uint32_t* __restrict__ out) {
+// lazy form of k_sd_mac for the baby steps of cc ciphertexts (one key read serves all; 6.3 MB per rotation):
+// each rotation written straight as the PQ-basis ct (U, W + P sigma(b^)) -- no ModDown, no UW round trip;
+// digits D^ [mod][ct][t][N], NTT'd cts X [ct][L][ab][N], rotation z of ct -> out + ct os + z 6N
+__global__ void k_sd_mac_lazy_multi(const uint32_t* __restrict__ D, uint32_t cc, const uint32_t* __restrict__ perms,
+                                    const uint32_t* __restrict__ K, const uint32_t* __restrict__ X, uint32_t N, Mods M,
+                                    uint32_t* __restrict__ out, uint64_t os) {
   const uint32_t mod = blockIdx.y, z = blockIdx.z;
   const uint32_t q = mod == 0 ? M.m[0] : (mod == 1 ? M.m[1] : M.m[2]);
   const uint64_t mu = mod == 0 ? M.mu[0] : (mod == 1 ? M.mu[1] : M.mu[2]);
   const uint32_t pm = M.m[2] % q;
   const uint32_t* perm = perms + (size_t)z * N;
   const uint32_t* Kz = K + (size_t)z * 24 * N;
-  const uint32_t* Dz = D + (size_t)mod * kSdT * N;
-  uint32_t* o = out + (size_t)z * 6 * N + (size_t)mod * 2 * N;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
     const uint32_t pc = perm[c];
-    uint64_t u = 0, w = 0;
+    uint32_t ku[kSdT], kw[kSdT];
 #pragma unroll
     for (int t = 0; t < kSdT; ++t) {
-      const uint64_t dv = Dz[(size_t)t * N + pc];
-      u += dv * Kz[(size_t)((t * 2 + 0) * 3 + mod) * N + c];
-      w += dv * Kz[(size_t)((t * 2 + 1) * 3 + mod) * N + c];
+      ku[t] = Kz[(size_t)((t * 2 + 0) * 3 + mod) * N + c];
+      kw[t] = Kz[(size_t)((t * 2 + 1) * 3 + mod) * N + c];
     }
-    o[c] = barrett64(u, mu, q);
-    const uint32_t wr = barrett64(w, mu, q);
-    o[N + c] = mod < 2 ? add_mod(wr, mulmod_b(bh[mod * bls + pc], pm, mu, q), q) : wr;
+    for (uint32_t ct = 0; ct < cc; ++ct) {
+      const uint32_t* Dz = D + ((size_t)mod * cc + ct) * kSdT * N;
+      uint64_t u = 0, w = 0;
+#pragma unroll
+      for (int t = 0; t < kSdT; ++t) {
+        const uint64_t dv = Dz[(size_t)t * N + pc];
+        u += dv * ku[t];
+        w += dv * kw[t];
+      }
+      uint32_t* o = out + ct * os + (size_t)z * 6 * N + (size_t)mod * 2 * N;
+      o[c] = barrett64(u, mu, q);
+      const uint32_t wr = barrett64(w, mu, q);
+      o[N + c] = mod < 2 ? add_mod(wr, mulmod_b(X[(size_t)ct * 4 * N + mod * 2 * N + N + pc], pm, mu, q), q) : wr;
+    }
   }
 }
 // rotated ct z (NTT domain) [L][ab][N] at out + z * os: a = (U - LB_u) P^-1, b = sigma(b^_z) + (W - LB_w) P^-1
@@ -1478,7 +1487,7 @@ __global__ void k_sd_reduce_pts(const int64_t* __restrict__ pt, uint64_t total, 
     }
   }
 }
-// lazy ModDown (hoisted BSGS; baby rotations from k_sd_mac_lazy):
+// lazy ModDown (hoisted BSGS; baby rotations from k_sd_mac_lazy_multi):
 // baby'_0 = P ct (q0, q1), 0 mod P
 __global__ void k_sd_lazy_baby0(const uint32_t* __restrict__ X, uint32_t N, Mods M, uint32_t* __restrict__ out) {
   const uint32_t mod = blockIdx.y, q = M.m[mod];
@@ -1736,7 +1745,7 @@ static uint64_t sd_ws_words(const he_slot_pcmm_plan* p, SdWs* w, uint32_t* base)
   SdWs dummy;
   SdWs& r = w ? *w : dummy;
   take(r.D, 3ull * kSdT * T * N);
-  take(r.X, 4 * N);
+  take(r.X, 4 * N * C);
   const uint64_t cw = p->lazy ? 6 : 4;   // words per N of a baby / group ct (3 moduli when lazy)
   take(r.baby, cw * p->b * N * C);
   take(r.inner, cw * p->g * N * C);
@@ -1832,27 +1841,34 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
   const uint64_t baby_cs = 2ull * nl * b * N, inner_cs = 2ull * nl * g * N;
   for (uint32_t c0 = 0; c0 < n_ct; c0 += p->chunk) {
     const uint32_t cc = std::min(p->chunk, n_ct - c0);
+    if (p->lazy) {
+      // baby steps of all cc ciphertexts together: digits and NTT'd copies of each, P ct, then one key MAC
+      // pass per rotation serving every ciphertext (PQ basis, no ModDown): [ct][i][3 moduli][ab][N]
+      he_status s = digits(ct_in + (size_t)c0 * 4 * N, 4ull * N, cc);
+      if (s) return s;
+      HE_CUDA(cudaMemcpyAsync(w.X, ct_in + (size_t)c0 * 4 * N, 4ull * N * cc * sizeof(uint32_t),
+                              cudaMemcpyDeviceToDevice, st), "copy");
+      for (uint32_t z = 0; z < cc; ++z) {
+        for (int L = 0; L < 2; ++L)
+          HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)z * 4 * N + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
+        k_sd_lazy_baby0<<<grid3(3, 1), 256, 0, st>>>(w.X + (size_t)z * 4 * N, N, p->M, w.baby + z * baby_cs);
+      }
+      if (b > 1)
+        k_sd_mac_lazy_multi<<<grid3(3, b - 1), 256, 0, st>>>(w.D, cc, p->perms, keys_baby, w.X, N, p->M,
+                                                              w.baby + 6ull * N, baby_cs);
+    }
     // baby steps per ciphertext: one hoisted digit decomposition, all b - 1 rotations in one pass
-    for (uint32_t z = 0; z < cc; ++z) {
+    for (uint32_t z = 0; z < cc && !p->lazy; ++z) {
       const uint32_t* ct = ct_in + (size_t)(c0 + z) * 4 * N;
       uint32_t* bz = w.baby + z * baby_cs;
       he_status s = digits(ct, 0, 1);
       if (s) return s;
       HE_CUDA(cudaMemcpyAsync(w.X, ct, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
       for (int L = 0; L < 2; ++L) HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
-      if (p->lazy) {
-        // P ct, then the rotations straight from the key MAC (no ModDown): [i][3 moduli][ab][N]
-        k_sd_lazy_baby0<<<grid3(3, 1), 256, 0, st>>>(w.X, N, p->M, bz);
-        if (b > 1) {
-          k_sd_mac_lazy<<<grid3(3, b - 1), 256, 0, st>>>(w.D, p->perms, keys_baby, w.X + N, 2ull * N, N, p->M,
-                                                        bz + 6ull * N);
-        }
-      } else {
-        HE_CUDA(cudaMemcpyAsync(bz, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
-        if (b > 1) {
-          s = rotate(b - 1, 1, 1, 0, keys_baby, w.X + N, 0, bz + 4ull * N);
-          if (s) return s;
-        }
+      HE_CUDA(cudaMemcpyAsync(bz, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
+      if (b > 1) {
+        s = rotate(b - 1, 1, 1, 0, keys_baby, w.X + N, 0, bz + 4ull * N);
+        if (s) return s;
       }
     }
     // giant-group products: all groups (and all cc ciphertexts) in one launch
