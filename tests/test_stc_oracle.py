@@ -77,3 +77,34 @@ def test_oracle_stc_decrypts_to_app_a_coefficients(lazy):
     np.testing.assert_allclose(O.decode_acts(P, ph[None], k), A, atol=2.0 ** -12)
     with pytest.raises(ValueError):
         O.slot_bsgs(P, ct, pts, 2, b, g, kb, kg, lazy=lazy)   # 2 b g > N/2
+
+
+def test_llama_ring_layout_matches_paper_numbers():
+    """At the paper's sizes (N = 2^16, 128 x 256 per ct): ct_s[i + 128 j] = A[i][f(j, 8)] and
+    slot bitReverse(c, 15) lands at coefficient c = t + 256 m <-> A[bitReverse(m, 7)][sigma(t)]."""
+    from paper_2601_18511_b200.layout import sigma_table
+
+    L = HeParams()
+    assert (L.N, L.mlwe_degree, L.mlwe_rank) == (65536, 256, 256)
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((128, 512))
+    z = slot_vectors(L, A)
+    i = rng.integers(0, 128, 64)
+    j = rng.integers(0, 256, 64)
+    for r in range(2):
+        assert np.array_equal(z[r, i + 128 * j], A[i, 256 * r + np.array([rotate_bits_down(int(v), 8) for v in j])])
+    c = rng.integers(0, 32768, 64)
+    t, m = c % 256, c // 256
+    sig = sigma_table(256)
+    s = np.array([bit_reverse(int(v), 15) for v in c])
+    want = A[[bit_reverse(int(v), 7) for v in m], sig[t]]
+    assert np.array_equal(z[0, s], want)
+
+
+def test_split_and_shape_errors():
+    assert (stc_split(32768).baby, stc_split(32768).giant) == (256, 128)
+    assert (stc_split(256).baby, stc_split(256).giant) == (16, 16)
+    with pytest.raises(ValueError):
+        slot_vectors(P, np.zeros((P.mlwe_degree // 2 + 1, P.mlwe_rank)))
+    with pytest.raises(ValueError):
+        slot_vectors(P, np.zeros((P.mlwe_degree // 2, P.mlwe_rank + 1)))
