@@ -272,7 +272,7 @@ he_status he_slot_bsgs_plan_create(const he_context* ctx, const uint32_t* pts_nt
                                    uint32_t stride, he_slot_pcmm_plan** out);
 /* flags for he_slot_bsgs_plan_create_ext */
 #define HE_SLOT_LAZY_MODDOWN 1u /* baby rotations kept mod (q0, q1, P), one ModDown per giant group; pts
-                                   [b g][3][N] (he_slot_pcmm_encode_pts_ext with n_mods = 3); b % 16 == 0 */
+                                   [b g][3][N] (he_slot_pcmm_encode_pts_ext with n_mods = 3); b % 8 == 0 */
 he_status he_slot_bsgs_plan_create_ext(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t b, uint32_t g,
                                        uint32_t stride, uint32_t flags, he_slot_pcmm_plan** out);
 /* int64 plaintext polys [count][N] -> NTT-domain residues [count][n_mods][N] (n_mods 2: q0, q1; 3: + P) */

@@ -1714,9 +1714,9 @@ extern "C" he_status he_slot_bsgs_plan_create_ext(const he_context* c, const uin
   if (!(flags & HE_SLOT_LAZY_MODDOWN)) return he_slot_bsgs_plan_create(c, pts_ntt_dev, b, g, stride, out);
   if (!c || !out) return fail(HE_EINVAL, "null argument");
   const Mods M = make_mods(c->R);
-  if (b % 16 || c->R.N % kSdTile || (uint64_t)b * 2 * kSdTile * 4 > 200 * 1024 || M.m[0] >= (1u << 30) ||
+  if (b % 8 || c->R.N % kSdTile || (uint64_t)b * 2 * kSdTile * 4 > 200 * 1024 || M.m[0] >= (1u << 30) ||
       M.m[1] >= (1u << 30) || M.m[2] >= (1u << 30))
-    return fail(HE_EINVAL, "lazy ModDown needs b %% 16 == 0, b <= 400 and 30-bit moduli (b = %u)", b);
+    return fail(HE_EINVAL, "lazy ModDown needs b %% 8 == 0, b <= 800 and 30-bit moduli (b = %u)", b);
   he_status s = he_slot_bsgs_plan_create(c, pts_ntt_dev, b, g, stride, out);
   if (s) return s;
   (*out)->lazy = 1;

@@ -82,6 +82,7 @@ class PackedCt:
     level: int
     dim: int
     shear_power: int = 0
+    scale: float = 0.0   # encoding scale when known (checked against the plan's input_scale)
 
     @property
     def is_ct(self) -> bool:
@@ -133,12 +134,19 @@ def plan_blocks(plan: SlotPcmmPlan) -> list:
     return [block_clear(plan, i + j * b, j * b) for j in range(g) for i in range(b)]
 
 
-def encode_blocks(params, plan: SlotPcmmPlan) -> np.ndarray:
-    """int64 [d, N]: each block flattened row-major, tiled, CKKS-encoded at scale q1."""
-    return np.stack([slots.encode(blk.reshape(-1), params.N, float(params.delta_w)) for blk in plan_blocks(plan)])
+def encode_blocks(params, plan: SlotPcmmPlan, pt_shift: int = 0) -> np.ndarray:
+    """int64 [d, N]: each block flattened row-major, tiled, CKKS-encoded at scale q1 2^pt_shift."""
+    sc = float(params.delta_w) * 2.0 ** pt_shift
+    return np.stack([slots.encode(blk.reshape(-1), params.N, sc) for blk in plan_blocks(plan)])
 
 
-def make_slot_pcmm_plan(ctx: HeContext, weights, shear_power: int = 0, split: BsgsSplit | None = None) -> SlotPcmmPlan:
+def make_slot_pcmm_plan(ctx: HeContext, weights, shear_power: int = 0, split: BsgsSplit | None = None,
+                        pt_shift: int = 0, lazy: bool = False) -> SlotPcmmPlan:
+    """hesim make_pcmm_plan (matmul.py:77-100) on the device.  Defaults reproduce hesim's scales (weights at
+    q1, operand at Delta).  Precision options: lazy -- lazy-ModDown BSGS (baby rotations
+    kept mod PQ, weight blocks also mod P, one ModDown per group; needs split.baby % 8 == 0); pt_shift t --
+    weight blocks at q1 2^t with the operand encrypted at plan.input_scale = Delta / 2^t (the product still
+    lands at Delta), trading the weights' rounding error for operand noise."""
     torch = _torch()
     w = np.asarray(weights, dtype=float)
     d = w.shape[0]
@@ -155,13 +163,20 @@ def make_slot_pcmm_plan(ctx: HeContext, weights, shear_power: int = 0, split: Bs
     if not np.isfinite(w).all():
         raise ValueError("weights must be finite")
     plan = SlotPcmmPlan(d, shear_power, split, col_shear(shift_rows(w), shear_power))
-    pt = torch.from_numpy(encode_blocks(ctx.params, plan)).to(ctx.device)
-    plan.pts = torch.empty((d, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
-    native.call("he_slot_pcmm_encode_pts", ctx.handle, pt.data_ptr(), d, plan.pts.data_ptr(), ctx.stream())
+    pt = torch.from_numpy(encode_blocks(ctx.params, plan, pt_shift)).to(ctx.device)
+    nm = 3 if lazy else 2
+    plan.pts = torch.empty((d, nm, ctx.params.N), dtype=torch.int32, device=ctx.device)
+    native.call("he_slot_pcmm_encode_pts_ext", ctx.handle, pt.data_ptr(), d, nm, plan.pts.data_ptr(), ctx.stream())
     h = ctypes.c_void_p()
-    native.call("he_slot_pcmm_plan_create", ctx.handle, plan.pts.data_ptr(), d, split.baby, split.giant,
-                ctypes.byref(h))
+    if lazy:
+        native.call("he_slot_bsgs_plan_create_ext", ctx.handle, plan.pts.data_ptr(), split.baby, split.giant, d, 1,
+                    ctypes.byref(h))
+    else:
+        native.call("he_slot_pcmm_plan_create", ctx.handle, plan.pts.data_ptr(), d, split.baby, split.giant,
+                    ctypes.byref(h))
     plan._handle = h
+    plan.lazy, plan.pt_shift = lazy, pt_shift
+    plan.input_scale = ctx.params.delta / 2.0 ** pt_shift
     return plan
 
 
@@ -184,8 +199,10 @@ def slot_pcmm_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: in
     return SlotPcmmKeys(gen(baby), gen(giant), tuple(baby + giant))
 
 
-def encrypt_packed(ctx: HeContext, sk: SecretKey, mat, shear_power: int, seed: int, r0: int = 0) -> PackedCt:
-    """Encrypt col_shear(mat, l) row-major in the slots at scale Delta, level 1 (hesim pack_sheared)."""
+def encrypt_packed(ctx: HeContext, sk: SecretKey, mat, shear_power: int, seed: int, r0: int = 0,
+                   scale: float | None = None) -> PackedCt:
+    """Encrypt col_shear(mat, l) row-major in the slots at scale Delta (or a plan's input_scale), level 1
+    (hesim pack_sheared)."""
     torch = _torch()
     m = np.asarray(mat, dtype=float)
     d = m.shape[0]
@@ -193,12 +210,13 @@ def encrypt_packed(ctx: HeContext, sk: SecretKey, mat, shear_power: int, seed: i
         raise ValueError("only square matrices are packed")
     if d * d > ctx.params.N // 2 or (ctx.params.N // 2) % (d * d):
         raise ValueError(f"{d}x{d} does not tile the {ctx.params.N // 2} slots")
-    pt = torch.from_numpy(slots.encode(col_shear(m, shear_power).reshape(-1), ctx.params.N, ctx.params.delta)[None])
+    sc = ctx.params.delta if scale is None else float(scale)
+    pt = torch.from_numpy(slots.encode(col_shear(m, shear_power).reshape(-1), ctx.params.N, sc)[None])
     pt = pt.to(ctx.device)
     out = torch.empty((2, 2, ctx.params.N), dtype=torch.int32, device=ctx.device)
     native.call("he_encrypt_poly", ctx.handle, sk.s_ntt.data_ptr(), pt.data_ptr(), 1, seed, r0, out.data_ptr(),
                 ctx.stream())
-    return PackedCt(out, level=1, dim=d, shear_power=shear_power)
+    return PackedCt(out, level=1, dim=d, shear_power=shear_power, scale=sc)
 
 
 def _check_operand(plan: SlotPcmmPlan, B) -> None:
@@ -212,6 +230,9 @@ def _check_operand(plan: SlotPcmmPlan, B) -> None:
                          f"got {B.shear_power}")
     if B.level < 1:
         raise NeedsBootstrapError("pcmm needs one level")
+    want = getattr(plan, "input_scale", None)
+    if B.scale and want and B.scale != want:
+        raise ValueError(f"scale mismatch: plan expects operand scale {want}, got {B.scale}")
 
 
 def pcmm_slot_bsgs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, B: PackedCt) -> PackedCt:
@@ -228,7 +249,7 @@ def pcmm_slot_bsgs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, B: Pa
                 keys.giant.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel() * 4, ctx.stream(), ctypes.byref(led))
     ctx.ledger.add_c(led)
     ctx.ledger.observe_level(B.level - 1)
-    return PackedCt(out, level=B.level - 1, dim=plan.dim, shear_power=plan.shear_power)
+    return PackedCt(out, level=B.level - 1, dim=plan.dim, shear_power=plan.shear_power, scale=ctx.params.delta)
 
 
 def pcmm_slot_depth1(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, B: PackedCt) -> PackedCt:
@@ -302,7 +323,7 @@ def slot_linear(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, X: Packe
                 out.data_ptr(), ws.data_ptr(), ws.numel() * 4, ctx.stream(), ctypes.byref(led))
     ctx.ledger.add_c(led)
     ctx.ledger.observe_level(X.level - 1)
-    return PackedCt(out, level=X.level - 1, dim=X.dim, shear_power=X.shear_power)
+    return PackedCt(out, level=X.level - 1, dim=X.dim, shear_power=X.shear_power, scale=X.scale)
 
 
 def rope_masks(d: int, positions) -> tuple:

@@ -177,3 +177,31 @@ def test_depth1_schedule_matches_hesim_depth1(key):
     assert np.abs(decrypt_packed(ctx, sk, Y) - ref).max() < 2.0 ** -13
     with pytest.raises(ValueError):
         pcmm_slot_depth1(ctx, make_slot_pcmm_plan(ctx, W, shear_power=shear), keys, Y)
+
+
+def test_toy_lazy_and_scale_split_bit_exact():
+    """Plan options: lazy-ModDown BSGS (weights also mod P) with the weight/operand scale split -- the GPU words
+    equal or_slot_bsgs_lazy's at stride d, the values hesim's; a mismatched operand scale is refused."""
+    g = np.load(GOLD / "slot_pcmm_golden.npz")
+    W, B, ref = g["d16_l0_W"], g["d16_l0_B"], g["d16_l0_hesim_bsgs"]
+    d = W.shape[0]
+    P = HeParams.toy()
+    ctx = HeContext(P)
+    sk = ctx.keygen(7)
+    split = BsgsSplit(8, 2)
+    plan = make_slot_pcmm_plan(ctx, W, shear_power=0, split=split, pt_shift=2, lazy=True)
+    keys = slot_pcmm_keygen(ctx, sk, plan, seed=13)
+    X = encrypt_packed(ctx, sk, B, 1, seed=11, scale=plan.input_scale)
+    Y = pcmm_slot_bsgs(ctx, plan, keys, X)
+    s = O.keygen(P, 7)
+    ct = O.encrypt(P, 11, s, slots.encode(col_shear(B, 1).reshape(-1), P.N, plan.input_scale)[None])[0]
+    assert np.array_equal(u32(X.data), ct)
+    pt = encode_blocks(P, plan, pt_shift=2)
+    pts = np.stack([np.stack([(pt[k] % q).astype(np.uint32) for q in P.ks_moduli]) for k in range(d)])
+    kb = O.rotation_keys(P, 13, s, [i * d for i in range(1, split.baby)])
+    kg = O.rotation_keys(P, 13, s, [j * split.baby * d for j in range(1, split.giant)])
+    want = O.slot_bsgs(P, ct, pts, d, split.baby, split.giant, kb, kg, lazy=True)
+    assert np.array_equal(u32(Y.data)[0], want)
+    assert np.abs(decrypt_packed(ctx, sk, Y) - ref).max() < 2.0 ** -13
+    with pytest.raises(ValueError):
+        pcmm_slot_bsgs(ctx, plan, keys, encrypt_packed(ctx, sk, B, 1, seed=11))   # operand at Delta, plan wants Delta/4
