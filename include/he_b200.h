@@ -273,6 +273,12 @@ he_status he_slot_bsgs_plan_create(const he_context* ctx, const uint32_t* pts_nt
 /* flags for he_slot_bsgs_plan_create_ext */
 #define HE_SLOT_LAZY_MODDOWN 1u /* baby rotations kept mod (q0, q1, P), one ModDown per giant group; pts
                                    [b g][3][N] (he_slot_pcmm_encode_pts_ext with n_mods = 3); b % 8 == 0 */
+#define HE_SLOT_PLAIN_GIANT 2u  /* with HE_SLOT_LAZY_MODDOWN: giant rotations use plain dnum-2 keys
+                                   (he_slot_rotation_keygen_plain, [g-1][2][2][3][N]) -- their noise lands at
+                                   scale Delta q1 -- halving the giant digits' NTTs and key bytes */
+/* plain dnum-2 rotation keys sigma_{5^r}(s) -> s, keys_dev [n_steps][2][2][3][N] NTT domain */
+he_status he_slot_rotation_keygen_plain(const he_context* ctx, uint64_t seed, const int32_t* s_dev,
+                                        const int32_t* steps, uint32_t n_steps, uint32_t* keys_dev, void* stream);
 he_status he_slot_bsgs_plan_create_ext(const he_context* ctx, const uint32_t* pts_ntt_dev, uint32_t b, uint32_t g,
                                        uint32_t stride, uint32_t flags, he_slot_pcmm_plan** out);
 /* int64 plaintext polys [count][N] -> NTT-domain residues [count][n_mods][N] (n_mods 2: q0, q1; 3: + P) */

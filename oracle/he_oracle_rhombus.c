@@ -573,6 +573,19 @@ void or_rotation_ksk(uint64_t seed, uint32_t r, const int32_t* s, uint32_t N, co
   or_ksk_gen_gadget(seed, 0x10000 + r, ss, s, N, m, ksk);
   free(ss);
 }
+/* plain (dnum-2 hybrid) rotation key sigma_{5^r}(s) -> s, layout [i < 2][part][mod][N] */
+void or_rotation_ksk_plain(uint64_t seed, uint32_t r, const int32_t* s, uint32_t N, const uint32_t* m, uint32_t* ksk) {
+  uint64_t g = 1;
+  for (uint32_t t = 0; t < r % (N / 2); ++t) g = g * 5 % (2ull * N);
+  int32_t* ss = (int32_t*)malloc(sizeof(int32_t) * N);
+  for (uint32_t i = 0; i < N; ++i) {
+    uint64_t j = ((uint64_t)i * g) % (2ull * N);
+    if (j < N) ss[j] = s[i];
+    else ss[j - N] = -s[i];
+  }
+  or_ksk_gen(seed, 0x30000 + r, ss, s, N, m, ksk);
+  free(ss);
+}
 /* gadget digits D [3 mod][t < 4][n] of the a-part c [2 limbs][n]: sub-digits of d_i (< 2^15, so the
  * same value under every modulus) */
 static void ks_digits(const uint32_t* c, uint32_t n, const uint32_t* m, uint32_t* D) {
@@ -696,7 +709,8 @@ int or_slot_bsgs(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t
  * plaintexts.  pts [b g][3 moduli][N] coefficient form.  Then giant rotations, sum, rescale as above.
  */
 int or_slot_bsgs_lazy(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uint32_t g, const uint32_t* ct_in,
-                      const uint32_t* pts, const uint32_t* keys_baby, const uint32_t* keys_giant, uint32_t* out) {
+                      const uint32_t* pts, const uint32_t* keys_baby, const uint32_t* keys_giant, int plain_giant,
+                      uint32_t* out) {
   if ((uint64_t)b * g * d > N / 2) return 1;
   const size_t cw = (size_t)4 * N, bw = (size_t)6 * N;   /* Q ct [2][2][N]; PQ ct [3][2][N] */
   const uint32_t P = m[2];
@@ -764,7 +778,40 @@ int or_slot_bsgs_lazy(uint32_t N, const uint32_t* m, uint32_t d, uint32_t b, uin
       memcpy(innerq + ((size_t)L * 2 + 1) * N, xb + (size_t)L * N, sizeof(uint32_t) * N);
     }
     const uint32_t* part = innerq;
-    if (j > 0) {
+    if (j > 0 && plain_giant) {
+      /* plain dnum-2 key (its noise lands at scale Delta q1): digits d_i of a, lifted into every modulus,
+       * then sigma on the lifted digits (as the device does in the NTT domain), MAC, ModDown */
+      uint64_t gal = 1;
+      for (uint64_t e = 0; e < ((uint64_t)j * b * d) % (N / 2); ++e) gal = gal * 5 % (2ull * N);
+      const uint32_t* ksk = keys_giant + (size_t)(j - 1) * 12 * N;
+      memset(U, 0, sizeof(uint32_t) * 3 * N);
+      memset(W, 0, sizeof(uint32_t) * 3 * N);
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t qi = m[i];
+        const uint64_t inv = powmod(m[1 - i] % qi, qi - 2, qi);
+        for (int jm = 0; jm < 3; ++jm) {
+          for (uint32_t k = 0; k < N; ++k)
+            t[k] = (uint32_t)(mulmod(innerq[((size_t)i * 2 + 0) * N + k], inv, qi) % m[jm]);
+          or_automorphism(t, N, (uint32_t)gal, m[jm], sd);
+          polymul(sd, ksk + ((size_t)(i * 2 + 0) * 3 + jm) * N, N, m[jm], t);
+          for (uint32_t k = 0; k < N; ++k) U[(size_t)jm * N + k] = (uint32_t)(((uint64_t)U[(size_t)jm * N + k] + t[k]) % m[jm]);
+          for (uint32_t k = 0; k < N; ++k)
+            t[k] = (uint32_t)(mulmod(innerq[((size_t)i * 2 + 0) * N + k], inv, qi) % m[jm]);
+          or_automorphism(t, N, (uint32_t)gal, m[jm], sd);
+          polymul(sd, ksk + ((size_t)(i * 2 + 1) * 3 + jm) * N, N, m[jm], t);
+          for (uint32_t k = 0; k < N; ++k) W[(size_t)jm * N + k] = (uint32_t)(((uint64_t)W[(size_t)jm * N + k] + t[k]) % m[jm]);
+        }
+      }
+      ks_moddown(U, W, N, m, xa, xb);
+      for (int L = 0; L < 2; ++L) {
+        or_automorphism(innerq + ((size_t)L * 2 + 1) * N, N, (uint32_t)gal, m[L], sd);
+        for (uint32_t k = 0; k < N; ++k) {
+          rot[((size_t)L * 2 + 0) * N + k] = xa[(size_t)L * N + k];
+          rot[((size_t)L * 2 + 1) * N + k] = (uint32_t)(((uint64_t)sd[k] + xb[(size_t)L * N + k]) % m[L]);
+        }
+      }
+      part = rot;
+    } else if (j > 0) {
       for (int L = 0; L < 2; ++L) memcpy(a_in + (size_t)L * N, innerq + ((size_t)L * 2 + 0) * N, sizeof(uint32_t) * N);
       ks_digits(a_in, N, m, D);
       rotate_with_digits(innerq, D, N, j * b * d, keys_giant + (size_t)(j - 1) * 24 * N, m, rot);

@@ -19,7 +19,7 @@ __all__ = [
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
     "decode_vector", "rhombus_pcmv", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
     "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe", "rotation_keys", "slot_pcmm",
-    "slot_bsgs",
+    "slot_bsgs", "rotation_keys_plain",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -576,7 +576,9 @@ def _sd_bind():
         L.or_slot_bsgs.restype = ctypes.c_int
         L.or_slot_bsgs.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
         L.or_slot_bsgs_lazy.restype = ctypes.c_int
-        L.or_slot_bsgs_lazy.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
+        L.or_slot_bsgs_lazy.argtypes = [u32, u32p, u32, u32, u32, u32p, u32p, u32p, u32p, ctypes.c_int, u32p]
+        L.or_rotation_ksk_plain.restype = None
+        L.or_rotation_ksk_plain.argtypes = [ctypes.c_uint64, u32, i32p, u32, u32p, u32p]
         L._sd_bound = True
     return L
 
@@ -608,19 +610,37 @@ def slot_pcmm(params, ct_in: np.ndarray, pts: np.ndarray, d: int, b: int, g: int
     return out
 
 
+def rotation_keys_plain(params, seed: int, s: np.ndarray, steps) -> np.ndarray:
+    """Plain dnum-2 keys sigma_{5^r}(s) -> s for each step r -> [len(steps), 2, 2, 3, N] (coefficient form)."""
+    N = params.N
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    out = np.zeros((len(steps), 2, 2, 3, N), np.uint32)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    for t, r in enumerate(steps):
+        g = np.zeros((2, 2, 3, N), np.uint32)
+        _sd_bind().or_rotation_ksk_plain(seed, int(r) % (N // 2), _i32(s), N, _u32(m), _u32(g))
+        out[t] = g
+    return out
+
+
 def slot_bsgs(params, ct_in: np.ndarray, pts: np.ndarray, stride: int, b: int, g: int, keys_baby,
               keys_giant, lazy: bool = False) -> np.ndarray:
     """or_slot_bsgs: the general BSGS slot map (baby steps i stride, giant steps j b stride) -- SlotToCoeffs
     with stride 1.  pts [b g, 2, N] residues (coefficient form) -> [2, N] level 0.  lazy: or_slot_bsgs_lazy
-    (baby rotations kept mod PQ, one ModDown per group), pts [b g, 3, N] (q0, q1, P)."""
+    (baby rotations kept mod PQ, one ModDown per group), pts [b g, 3, N] (q0, q1, P); giant keys of
+    rotation_keys_plain's shape [.., 2, 2, 3, N] select plain dnum-2 giant rotations."""
     N = params.N
     m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
     out = np.zeros((2, N), np.uint32)
     kb = np.ascontiguousarray(keys_baby if len(keys_baby) else np.zeros((1, 4, 2, 3, N), np.uint32), dtype=np.uint32)
     kg = np.ascontiguousarray(keys_giant if len(keys_giant) else np.zeros((1, 4, 2, 3, N), np.uint32), dtype=np.uint32)
-    fn = _sd_bind().or_slot_bsgs_lazy if lazy else _sd_bind().or_slot_bsgs
-    rc = fn(N, _u32(m), stride, b, g, _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
-                                 _u32(np.ascontiguousarray(pts, dtype=np.uint32)), _u32(kb), _u32(kg), _u32(out))
+    args = [N, _u32(m), stride, b, g, _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
+            _u32(np.ascontiguousarray(pts, dtype=np.uint32)), _u32(kb), _u32(kg)]
+    if lazy:
+        plain = kg.ndim == 5 and kg.shape[1] == 2 and len(keys_giant)
+        rc = _sd_bind().or_slot_bsgs_lazy(*args, 1 if plain else 0, _u32(out))
+    else:
+        rc = _sd_bind().or_slot_bsgs(*args, _u32(out))
     if rc:
         raise ValueError("slot_bsgs: split x stride exceeds the slots")
     return out

@@ -1227,20 +1227,35 @@ __global__ void k_sd_digits(const uint32_t* __restrict__ a, uint64_t as, uint64_
       }
   }
 }
+// plain dnum-2 digits: D^ [mod][z][i < 2][N] = d_i mod m_mod, d_i = [a_i (q/q_i)^-1]_{q_i}
+__global__ void k_sd_digits_plain(const uint32_t* __restrict__ a, uint64_t as, uint64_t ls, uint32_t N, uint32_t cnt,
+                                  Mods M, uint32_t qh0, uint32_t qh0p, uint32_t qh1, uint32_t qh1p,
+                                  uint32_t* __restrict__ D) {
+  const uint32_t z = blockIdx.z;
+  const uint32_t* src = a + z * as;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
+    const uint32_t dg[2] = {shoup_mul(src[x], qh0, qh0p, M.m[0]), shoup_mul(src[ls + x], qh1, qh1p, M.m[1])};
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int mod = 0; mod < 3; ++mod) D[(((size_t)mod * cnt + z) * 2 + i) * N + x] = dg[i] % M.m[mod];
+  }
+}
 // rotation z: UW [mod][z][part][N] = sum_t D^[mod][dz][t][perm_z c] K_z[t][part][mod][c]   (dz = hoist ? 0 : z)
-__global__ void k_sd_mac(const uint32_t* __restrict__ D, uint32_t dcnt, int hoist, const uint32_t* __restrict__ perms,
-                         const uint32_t* __restrict__ K, uint32_t N, uint32_t cnt, Mods M, uint32_t* __restrict__ UW) {
+template <int T>   // digits per key: kSdT (gadget keys) or 2 (plain dnum-2 keys, 12N words)
+__global__ void k_sd_mac_t(const uint32_t* __restrict__ D, uint32_t dcnt, int hoist, const uint32_t* __restrict__ perms,
+                           const uint32_t* __restrict__ K, uint32_t N, uint32_t cnt, Mods M, uint32_t* __restrict__ UW) {
   const uint32_t mod = blockIdx.y, z = blockIdx.z, dz = hoist ? 0 : z;
   const uint32_t q = mod == 0 ? M.m[0] : (mod == 1 ? M.m[1] : M.m[2]);
   const uint64_t mu = mod == 0 ? M.mu[0] : (mod == 1 ? M.mu[1] : M.mu[2]);
   const uint32_t* perm = perms + (size_t)z * N;
-  const uint32_t* Kz = K + (size_t)z * 24 * N;
-  const uint32_t* Dz = D + ((size_t)mod * dcnt + dz) * kSdT * N;
+  const uint32_t* Kz = K + (size_t)z * T * 6 * N;
+  const uint32_t* Dz = D + ((size_t)mod * dcnt + dz) * T * N;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
     const uint32_t pc = perm[c];
     uint64_t u = 0, w = 0;   // 4 products < 2^60 each
 #pragma unroll
-    for (int t = 0; t < kSdT; ++t) {
+    for (int t = 0; t < T; ++t) {
       const uint64_t dv = Dz[(size_t)t * N + pc];
       u += dv * Kz[(size_t)((t * 2 + 0) * 3 + mod) * N + c];
       w += dv * Kz[(size_t)((t * 2 + 1) * 3 + mod) * N + c];
@@ -1532,6 +1547,7 @@ struct he_slot_pcmm_plan {
   uint32_t shared;       // products through k_sd_inner_s
   uint32_t halves;       // baby range split (shared kernel runs once per half, accumulating)
   uint32_t lazy;         // lazy ModDown: baby rotations kept mod PQ, pts carry 3 moduli, one ModDown per group
+  uint32_t plain_giant;  // giant rotations with plain dnum-2 keys (lazy only: their noise lands at Delta q1)
 };
 
 // gadget key (layout [t][part][mod][deg], t = i kSdSub + h), NTT domain; streams use t as the digit index
@@ -1578,6 +1594,28 @@ extern "C" he_status he_slot_rotation_keygen(const he_context* c, uint64_t seed,
     const uint32_t g = (uint32_t)powmod_h(5, r, 2ull * N);
     k_secret_auto<<<grid_for(N), 256, 0, st>>>(s_dev, N, g, sk);
     s = make_ksk_gadget_dev(M, seed, 0x10000 + r, sk, s_dev, N, c->ntt, keys_dev + (size_t)t * 24 * N, st);
+  }
+  cudaFreeAsync(sk, st);
+  if (s) return s;
+  return cudaGetLastError() == cudaSuccess ? HE_OK : fail(HE_ECUDA, "rotation keygen launch failed");
+}
+
+// plain dnum-2 rotation keys sigma_{5^r}(s) -> s ([n][2][2][3][N], NTT), for the giant steps of lazy plans
+extern "C" he_status he_slot_rotation_keygen_plain(const he_context* c, uint64_t seed, const int32_t* s_dev,
+                                                   const int32_t* steps, uint32_t n_steps, uint32_t* keys_dev,
+                                                   void* stream) {
+  if (!c || !s_dev || !steps || (!keys_dev && n_steps)) return fail(HE_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->R.N;
+  const Mods M = make_mods(c->R);
+  int32_t* sk = nullptr;
+  HE_CUDA(cudaMallocAsync(&sk, N * sizeof(int32_t), st), "alloc");
+  he_status s = HE_OK;
+  for (uint32_t t = 0; t < n_steps && !s; ++t) {
+    const uint32_t r = (uint32_t)(((int64_t)steps[t] % (N / 2) + N / 2) % (N / 2));
+    const uint32_t g = (uint32_t)powmod_h(5, r, 2ull * N);
+    k_secret_auto<<<grid_for(N), 256, 0, st>>>(s_dev, N, g, sk);
+    s = make_ksk_dev(M, seed, 0x30000 + r, sk, s_dev, N, c->ntt, keys_dev + (size_t)t * 12 * N, st);
   }
   cudaFreeAsync(sk, st);
   if (s) return s;
@@ -1637,6 +1675,7 @@ static he_status slot_plan_make(const he_context* c, const uint32_t* pts_ntt_dev
   p->chunk = 1;
   p->shared = 0;
   p->lazy = 0;
+  p->plain_giant = 0;
   p->halves = 1;
   const bool shared_ok = b % 16 == 0 && N % kSdTile == 0 && p->M.m[0] < (1u << 30) && p->M.m[1] < (1u << 30);
   if (((uint64_t)b * g >= 4096 || getenv("HE_SD_SHARED")) && shared_ok && !getenv("HE_SD_PER_CT")) {
@@ -1721,6 +1760,7 @@ extern "C" he_status he_slot_bsgs_plan_create_ext(const he_context* c, const uin
   if (s) return s;
   (*out)->lazy = 1;
   (*out)->shared = 1;
+  (*out)->plain_giant = (flags & HE_SLOT_PLAIN_GIANT) ? 1u : 0u;
   return HE_OK;
 }
 
@@ -1824,9 +1864,22 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
   };
   // cnt rotations in one pass: rotation z uses perm table t0 + z, key z, digits dz (hoist: all z share D^ 0),
   // source b^ at bh + z * bs; result z at dst + z * 4N (NTT domain)
+  // plain digits (dnum-2 keys) of cnt sources -> D^ [mod][z][i < 2][N] (NTT)
+  auto digits_plain = [&](const uint32_t* a, uint64_t as, uint32_t cnt) -> he_status {
+    k_sd_digits_plain<<<grid3(1, cnt), 256, 0, st>>>(a, as, 2ull * N, N, cnt, p->M, p->qhinv[0], p->qhinvp[0],
+                                                     p->qhinv[1], p->qhinvp[1], w.D);
+    for (int mod = 0; mod < 3; ++mod)
+      HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * cnt * 2 * N, cnt * 2, N, st), "NTT(D plain)");
+    return HE_OK;
+  };
   auto rotate = [&](uint32_t cnt, int hoist, uint32_t dcnt, uint32_t t0, const uint32_t* keys, const uint32_t* bh,
-                    uint64_t bs, uint32_t* dst) -> he_status {
-    k_sd_mac<<<grid3(3, cnt), 256, 0, st>>>(w.D, dcnt, hoist, p->perms + (size_t)t0 * N, keys, N, cnt, p->M, w.UW);
+                    uint64_t bs, uint32_t* dst, bool plain = false) -> he_status {
+    if (plain)
+      k_sd_mac_t<2><<<grid3(3, cnt), 256, 0, st>>>(w.D, dcnt, hoist, p->perms + (size_t)t0 * N, keys, N, cnt, p->M,
+                                                   w.UW);
+    else
+      k_sd_mac_t<kSdT><<<grid3(3, cnt), 256, 0, st>>>(w.D, dcnt, hoist, p->perms + (size_t)t0 * N, keys, N, cnt,
+                                                      p->M, w.UW);
     uint32_t* UWP = w.UW + (size_t)2 * cnt * 2 * N;   // [z][part][N] of modulus P
     HE_CUDA(ntt_inverse(c->ntt[2], UWP, 2 * cnt, N, st), "INTT(U_P, W_P)");
     k_moddown_lift<<<grid_for(2ull * cnt * N), 256, 0, st>>>(UWP, (uint64_t)cnt * N, p->M, w.LB);
@@ -1903,9 +1956,9 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
         uint32_t* in1 = iz + 4ull * N;   // groups 1 .. g-1
         for (int L = 0; L < 2; ++L)
           HE_CUDA(ntt_inverse(c->ntt[L], in1 + (size_t)L * 2 * N, g - 1, 4ull * N, st), "INTT(inner a)");
-        he_status s = digits(in1, 4ull * N, g - 1);
+        he_status s = p->plain_giant ? digits_plain(in1, 4ull * N, g - 1) : digits(in1, 4ull * N, g - 1);
         if (s) return s;
-        s = rotate(g - 1, 0, g - 1, b - 1, keys_giant, in1 + N, 4ull * N, w.rot);
+        s = rotate(g - 1, 0, g - 1, b - 1, keys_giant, in1 + N, 4ull * N, w.rot, p->plain_giant != 0);
         if (s) return s;
       }
       k_sd_accumulate<<<grid3(2, 1), 256, 0, st>>>(iz, w.rot, g - 1, N, p->M, w.acc);

@@ -33,7 +33,7 @@ EXPORTS = (
     "he_ring_pack_workspace_bytes", "he_ring_pack_run", "he_rhombus_run_shard", "he_rhombus_combine",
     "he_encrypt_poly", "he_slot_rotation_keygen", "he_slot_pcmm_encode_pts", "he_slot_pcmm_plan_create",
     "he_slot_pcmm_plan_destroy", "he_slot_pcmm_workspace_bytes", "he_slot_pcmm_run", "he_slot_pcmm_run_batch", "he_mod_raise",
-    "he_slot_lt_plan_create", "he_slot_bsgs_plan_create", "he_slot_bsgs_plan_create_ext", "he_slot_pcmm_encode_pts_ext",
+    "he_slot_lt_plan_create", "he_slot_bsgs_plan_create", "he_slot_bsgs_plan_create_ext", "he_slot_pcmm_encode_pts_ext", "he_slot_rotation_keygen_plain",
 )
 
 
@@ -109,6 +109,7 @@ def lib():
             "he_mod_raise": (st, [vp, vp, u32, vp, u32, vp, vp]),
             "he_slot_lt_plan_create": (st, [vp, vp, u32, vp, ctypes.POINTER(vp)]),
             "he_slot_bsgs_plan_create": (st, [vp, vp, u32, u32, u32, ctypes.POINTER(vp)]),
+            "he_slot_rotation_keygen_plain": (st, [vp, u64, vp, vp, u32, vp, vp]),
             "he_slot_bsgs_plan_create_ext": (st, [vp, vp, u32, u32, u32, u32, ctypes.POINTER(vp)]),
             "he_slot_pcmm_encode_pts_ext": (st, [vp, vp, u32, u32, vp, vp]),
             "he_slot_rotation_keygen": (st, [vp, u64, vp, vp, u32, vp, vp]),

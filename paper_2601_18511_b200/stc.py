@@ -131,9 +131,12 @@ def make_slot_to_coeffs_plan(ctx: HeContext, split: BsgsSplit | None = None, bat
         native.call("he_slot_pcmm_encode_pts_ext", ctx.handle, pt.data_ptr(), cnt, nm, plan.pts[k0].data_ptr(),
                     ctx.stream())
     h = ctypes.c_void_p()
+    # lazy plans also switch the giant rotations with plain dnum-2 keys (HE_SLOT_PLAIN_GIANT): after the
+    # products their noise lands at scale Delta q1, so the gadget split buys nothing there
     native.call("he_slot_bsgs_plan_create_ext", ctx.handle, plan.pts.data_ptr(), split.baby, split.giant, 1,
-                1 if lazy else 0, ctypes.byref(h))
+                3 if lazy else 0, ctypes.byref(h))
     plan.lazy = lazy
+    plan.plain_giant = lazy
     plan._handle = h
     b, g = split.baby, split.giant
     plan.steps = tuple(range(1, b)) + tuple(j * b for j in range(1, g))
@@ -147,16 +150,16 @@ def slot_to_coeffs_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, see
     torch = _torch()
     N, b, g = ctx.params.N, plan.split.baby, plan.split.giant
 
-    def gen(steps):
-        keys = torch.empty((max(len(steps), 1), 4, 2, 3, N), dtype=torch.int32, device=ctx.device)
+    def gen(steps, plain=False):
+        keys = torch.empty((max(len(steps), 1), 2 if plain else 4, 2, 3, N), dtype=torch.int32, device=ctx.device)
         if steps:
             arr = (ctypes.c_int32 * len(steps))(*steps)
-            native.call("he_slot_rotation_keygen", ctx.handle, seed, sk.s.data_ptr(), arr, len(steps),
-                        keys.data_ptr(), ctx.stream())
+            native.call("he_slot_rotation_keygen_plain" if plain else "he_slot_rotation_keygen", ctx.handle, seed,
+                        sk.s.data_ptr(), arr, len(steps), keys.data_ptr(), ctx.stream())
         return keys
 
     baby, giant = list(range(1, b)), [j * b for j in range(1, g)]
-    return SlotPcmmKeys(gen(baby), gen(giant), tuple(baby + giant))
+    return SlotPcmmKeys(gen(baby), gen(giant, getattr(plan, "plain_giant", False)), tuple(baby + giant))
 
 
 def encrypt_slots(ctx: HeContext, sk: SecretKey, acts, seed: int, r0: int = 0, scale: float | None = None) -> SlotBlocks:

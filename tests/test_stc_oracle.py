@@ -52,9 +52,10 @@ def test_plaintexts_are_the_rotated_diagonals():
             assert np.abs(got - want).max() < 1e-3
 
 
-@pytest.mark.parametrize("lazy", [False, True])
-def test_oracle_stc_decrypts_to_app_a_coefficients(lazy):
-    """Both BSGS forms (per-rotation ModDown; lazy ModDown in the PQ basis, plaintexts also mod P)."""
+@pytest.mark.parametrize("lazy,plain", [(False, False), (True, False), (True, True)])
+def test_oracle_stc_decrypts_to_app_a_coefficients(lazy, plain):
+    """Both BSGS forms (per-rotation ModDown; lazy ModDown in the PQ basis, plaintexts also mod P), the lazy
+    one also with plain dnum-2 giant keys."""
     rng = np.random.default_rng(2)
     d, k = P.mlwe_degree, P.mlwe_rank
     N, n = P.N, P.N // 2
@@ -67,7 +68,7 @@ def test_oracle_stc_decrypts_to_app_a_coefficients(lazy):
     s = O.keygen(P, 7)
     ct = O.encrypt(P, 11, s, slots.encode(slot_vectors(P, A)[0], N, P.delta)[None])[0]
     kb = O.rotation_keys(P, 13, s, list(range(1, b)))
-    kg = O.rotation_keys(P, 13, s, [j * b for j in range(1, g)])
+    kg = (O.rotation_keys_plain if plain else O.rotation_keys)(P, 13, s, [j * b for j in range(1, g)])
     out = O.slot_bsgs(P, ct, pts, 1, b, g, kb, kg, lazy=lazy)
     ph = O.decrypt_under(P, out[0], out[1], s, P.moduli[0])
     want = O.encode_acts(P, A)[0]
