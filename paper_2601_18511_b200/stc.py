@@ -125,9 +125,12 @@ def make_slot_to_coeffs_plan(ctx: HeContext, split: BsgsSplit | None = None, bat
     plan = SlotPcmmPlan(n, 0, split, np.zeros((0, 0)))
     nm = 3 if lazy else 2
     plan.pts = torch.empty((n, nm, N), dtype=torch.int32, device=ctx.device)
+    # small rings build the plaintexts on the host (deterministic, and the same integers the oracle tests
+    # use: a device FFT can round a coefficient at .5 the other way); N = 2^16 needs the device's FFT
+    dev = "cpu" if N <= 8192 else ctx.device
     for k0 in range(0, n, batch):
         cnt = min(batch, n - k0)
-        pt = stc_plaintexts(ctx.params, split, k0, cnt, ctx.device, pt_shift).contiguous()
+        pt = stc_plaintexts(ctx.params, split, k0, cnt, dev, pt_shift).to(ctx.device).contiguous()
         native.call("he_slot_pcmm_encode_pts_ext", ctx.handle, pt.data_ptr(), cnt, nm, plan.pts[k0].data_ptr(),
                     ctx.stream())
     h = ctypes.c_void_p()
