@@ -1512,25 +1512,37 @@ __global__ void k_sd_lazy_baby0(const uint32_t* __restrict__ X, uint32_t N, Mods
     out[(size_t)mod * 2 * N + c] = mod < 2 ? mulmod_b(X[(size_t)mod * 2 * N + c], pm, mu, q) : 0u;
 }
 // ModDown of the g group sums [j][3][ab][N] (P part already inverse-NTT'd): LB [L][j][ab][N] = centred lift
+// (4 words per thread, Barrett lift)
 __global__ void k_sd_lazy_lift(const uint32_t* __restrict__ X, uint32_t g, uint32_t N, Mods M, uint32_t* __restrict__ LB) {
-  const uint32_t L = blockIdx.y, q = M.m[L], P = M.m[2];
-  const uint64_t tot = 2ull * g * N;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < tot; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t j = x / (2ull * N), r = x % (2ull * N);
-    const uint32_t v = X[j * 6 * N + 4ull * N + r];
-    const uint32_t vq = v % q;
-    LB[(uint64_t)L * tot + x] = v > P / 2 ? sub_mod(vq, P % q, q) : vq;   // v - P when v is "negative"
+  const uint32_t P = M.m[2];
+  const uint64_t tot4 = 2ull * g * N / 4, n4 = 2ull * N / 4;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < tot4; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = x / n4, r = x % n4;
+    const uint4 v = reinterpret_cast<const uint4*>(X + j * 6 * N + 4ull * N)[r];
+    const uint32_t vs[4] = {v.x, v.y, v.z, v.w};
+    uint32_t l0[4], l1[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t c = vs[e] > P / 2 ? (int64_t)vs[e] - P : (int64_t)vs[e];
+      l0[e] = lift_b(c, M.mu[0], M.m[0]);
+      l1[e] = lift_b(c, M.mu[1], M.m[1]);
+    }
+    reinterpret_cast<uint4*>(LB)[x] = make_uint4(l0[0], l0[1], l0[2], l0[3]);
+    reinterpret_cast<uint4*>(LB + 2ull * g * N)[x] = make_uint4(l1[0], l1[1], l1[2], l1[3]);
   }
 }
 // inner_j [L][ab][N] = (X_L - LB_L) P^-1 mod q_L  (NTT domain; Q layout [j][4N] for the giant step)
 __global__ void k_sd_lazy_down(const uint32_t* __restrict__ X, const uint32_t* __restrict__ LB, uint32_t g,
                                uint32_t N, Mods M, uint32_t pinv0, uint32_t pinv1, uint32_t* __restrict__ out) {
   const uint32_t L = blockIdx.y, q = M.m[L], pinv = L ? pinv1 : pinv0;
-  const uint64_t mu = M.mu[L], tot = 2ull * g * N;
-  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < tot; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t j = x / (2ull * N), r = x % (2ull * N);
-    out[j * 4 * N + (uint64_t)L * 2 * N + r] =
-        mulmod_b(sub_mod(X[j * 6 * N + (uint64_t)L * 2 * N + r], LB[(uint64_t)L * tot + x], q), pinv, mu, q);
+  const uint64_t mu = M.mu[L], tot4 = 2ull * g * N / 4, n4 = 2ull * N / 4;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < tot4; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = x / n4, r = x % n4;
+    const uint4 a = reinterpret_cast<const uint4*>(X + j * 6 * N + (uint64_t)L * 2 * N)[r];
+    const uint4 l = reinterpret_cast<const uint4*>(LB + (uint64_t)L * 2 * g * N)[x];
+    reinterpret_cast<uint4*>(out + j * 4 * N + (uint64_t)L * 2 * N)[r] =
+        make_uint4(mulmod_b(sub_mod(a.x, l.x, q), pinv, mu, q), mulmod_b(sub_mod(a.y, l.y, q), pinv, mu, q),
+                   mulmod_b(sub_mod(a.z, l.z, q), pinv, mu, q), mulmod_b(sub_mod(a.w, l.w, q), pinv, mu, q));
   }
 }
 
@@ -1944,9 +1956,9 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
         // one ModDown per group sum: INTT of the P parts, centred lift, NTT, (X - lift) P^-1 -> [j][4N]
         for (int ab = 0; ab < 2; ++ab)
           HE_CUDA(ntt_inverse(c->ntt[2], iz + (4ull + ab) * N, g, 6ull * N, st), "INTT(group sums, P)");
-        dim3 gl = grid_for(2ull * g * N);
-        gl.y = 2;
+        dim3 gl = grid_for(2ull * g * N / 4);
         k_sd_lazy_lift<<<gl, 256, 0, st>>>(iz, g, N, p->M, w.LB);
+        gl.y = 2;
         HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2 * g, N, st), "NTT(lift q0)");
         HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2ull * g * N, 2 * g, N, st), "NTT(lift q1)");
         k_sd_lazy_down<<<gl, 256, 0, st>>>(iz, w.LB, g, N, p->M, p->pinv[0], p->pinv[1], w.innerq);
