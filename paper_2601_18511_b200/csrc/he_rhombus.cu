@@ -1396,7 +1396,7 @@ __global__ void k_sd_inner_g(const uint32_t* __restrict__ baby, const uint32_t* 
 // Barrett reduction per group
 constexpr int kSdTile = 32;
 constexpr int kSdSharedThreads = 512;   // 16 warps; 256 threads with 32 terms ahead measured 7% slower
-template <int CT, int U>
+template <int CT, int U, int GW = 2>   // GW giant groups per warp
 __global__ void __launch_bounds__(kSdSharedThreads, 1)
     k_sd_inner_s(const uint32_t* __restrict__ baby, uint64_t baby_cs, const uint32_t* __restrict__ pts, uint32_t b,
                  uint32_t g, uint32_t N, uint32_t nl, Mods M, uint32_t* __restrict__ inner, uint64_t inner_cs,
@@ -1420,23 +1420,23 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
   __syncthreads();
   const size_t tstride = (size_t)nl * N;   // words between consecutive terms
   const uint2* sl = reinterpret_cast<const uint2*>(sbaby) + lane;
-  for (uint32_t j0 = warp * 2; j0 < g; j0 += 2 * (blockDim.x >> 5)) {
-    const bool two = j0 + 1 < g;
-    const uint32_t* P0 = pts + (((size_t)j0 * b + ib) * nl + L) * N + c0 + lane;
-    const uint32_t* P1 = two ? P0 + (size_t)b * tstride : P0;
-    uint64_t acc[2][CT][2];
+  for (uint32_t j0 = warp * GW; j0 < g; j0 += GW * (blockDim.x >> 5)) {
+    const uint32_t* Pg[GW];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < GW; ++h)   // groups past g re-read group j0 (their sums are not stored)
+      Pg[h] = pts + (((size_t)(j0 + h < g ? j0 + h : j0) * b + ib) * nl + L) * N + c0 + lane;
+    uint64_t acc[GW][CT][2];
+#pragma unroll
+    for (int h = 0; h < GW; ++h)
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct) acc[h][ct][0] = acc[h][ct][1] = 0;
     for (uint32_t i0 = 0; i0 < bn; i0 += U) {
-      uint32_t p0[U], p1[U];
-      const uint32_t* a0 = P0 + (size_t)i0 * tstride;
-      const uint32_t* a1 = P1 + (size_t)i0 * tstride;
+      uint32_t pv[GW][U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        p0[u] = __ldg(a0 + u * tstride);
-        p1[u] = __ldg(a1 + u * tstride);
+      for (int h = 0; h < GW; ++h) {
+        const uint32_t* a = Pg[h] + (size_t)i0 * tstride;
+#pragma unroll
+        for (int u = 0; u < U; ++u) pv[h][u] = __ldg(a + u * tstride);
       }
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct) {
@@ -1444,13 +1444,14 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint2 xy = sr[u * kSdTile];
-          acc[0][ct][0] += (uint64_t)p0[u] * xy.x;
-          acc[0][ct][1] += (uint64_t)p0[u] * xy.y;
-          acc[1][ct][0] += (uint64_t)p1[u] * xy.x;
-          acc[1][ct][1] += (uint64_t)p1[u] * xy.y;
+#pragma unroll
+          for (int h = 0; h < GW; ++h) {
+            acc[h][ct][0] += (uint64_t)pv[h][u] * xy.x;
+            acc[h][ct][1] += (uint64_t)pv[h][u] * xy.y;
+          }
           if ((u & 7) == 7) {   // fold: hi 2^32 + lo == hi (2^32 mod q) + lo  (< 2^62 + 2^32; 8 more fit)
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < GW; ++h)
 #pragma unroll
               for (int ab = 0; ab < 2; ++ab)
                 acc[h][ct][ab] = (uint64_t)(uint32_t)(acc[h][ct][ab] >> 32) * r32 + (uint32_t)acc[h][ct][ab];
@@ -1459,21 +1460,15 @@ __global__ void __launch_bounds__(kSdSharedThreads, 1)
       }
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int ct = 0; ct < CT; ++ct) {
-        acc[h][ct][0] = barrett64(acc[h][ct][0], mu, q);
-        acc[h][ct][1] = barrett64(acc[h][ct][1], mu, q);
-      }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (h == 1 && !two) break;
+    for (int h = 0; h < GW; ++h) {
+      if (j0 + h >= g) break;
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct)
 #pragma unroll
         for (int ab = 0; ab < 2; ++ab) {
+          const uint32_t v = barrett64(acc[h][ct][ab], mu, q);
           uint32_t* o = inner + ct * inner_cs + (((size_t)(j0 + h) * nl + L) * 2 + ab) * N + c0 + lane;
-          *o = accumulate ? add_mod((uint32_t)acc[h][ct][ab], *o, q) : (uint32_t)acc[h][ct][ab];
+          *o = accumulate ? add_mod(v, *o, q) : v;
         }
     }
   }
@@ -1815,17 +1810,18 @@ extern "C" he_status he_slot_pcmm_workspace_bytes(const he_slot_pcmm_plan* p, ui
   return HE_OK;
 }
 
-template <int CT, int U>
+template <int CT, int U, int GW = 2>
 static cudaError_t launch_sd_inner_s_cu(const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts, uint32_t b,
                                         uint32_t g, uint32_t N, uint32_t nl, const Mods& M, uint32_t* inner,
                                         uint64_t inner_cs, uint32_t halves, cudaStream_t st) {
   const uint32_t bn = b / halves;
   const int smem = CT * (int)bn * 2 * kSdTile * 4;
-  cudaError_t e = cudaFuncSetAttribute(k_sd_inner_s<CT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_sd_inner_s<CT, U, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   for (uint32_t h = 0; h < halves; ++h)
-    k_sd_inner_s<CT, U><<<dim3(N / kSdTile, nl), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, nl, M,
-                                                                               inner, inner_cs, h * bn, bn, h > 0);
+    k_sd_inner_s<CT, U, GW><<<dim3(N / kSdTile, nl), kSdSharedThreads, smem, st>>>(baby, baby_cs, pts, b, g, N, nl,
+                                                                                   M, inner, inner_cs, h * bn, bn,
+                                                                                   h > 0);
   return cudaGetLastError();
 }
 // U = plaintext terms loaded ahead per group (register budget: 2 U words + 4 CT sums); must divide the range
@@ -1836,6 +1832,7 @@ static cudaError_t launch_sd_inner_s_ct(const uint32_t* baby, uint64_t baby_cs, 
   const uint32_t bn = b / halves;
   if (CT <= 2 && bn % 16 == 0)   // 128-register cap at 512 threads: 16 ahead fits two ciphertexts' sums
     return launch_sd_inner_s_cu<CT, (CT <= 2 ? 16 : 8)>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
+  // (4 groups per warp: 288 B of spills at 3 cts under the 128-register cap -- not used)
   return launch_sd_inner_s_cu<CT, 8>(baby, baby_cs, pts, b, g, N, nl, M, inner, inner_cs, halves, st);
 }
 static cudaError_t launch_sd_inner_s(uint32_t cc, const uint32_t* baby, uint64_t baby_cs, const uint32_t* pts,
