@@ -83,3 +83,36 @@ def test_c_abi_status_codes(toy):
         native.call("he_mod_raise", ctx.handle, X.data.data_ptr(), 1, X.data.data_ptr(), 0, X.data.data_ptr(),
                     ctx.stream())
     torch.cuda.synchronize()
+
+
+def test_slot_bsgs_abi_status_codes(toy):
+    """The slot BSGS entry points added for SlotToCoeffs reject bad arguments with HE_EINVAL / ValueError."""
+    P, ctx, sk, W, X = toy
+    N = P.N
+    pts = torch.zeros((16 * 16, 3, N), dtype=torch.int32, device=ctx.device)
+    h = ctypes.c_void_p()
+    with pytest.raises(ValueError):   # lazy ModDown needs b % 8 == 0
+        native.call("he_slot_bsgs_plan_create_ext", ctx.handle, pts.data_ptr(), 4, 64, 1, 1, ctypes.byref(h))
+    with pytest.raises(ValueError):   # b g stride > N/2
+        native.call("he_slot_bsgs_plan_create_ext", ctx.handle, pts.data_ptr(), 16, 16, 2, 0, ctypes.byref(h))
+    pt = torch.zeros((2, N), dtype=torch.int64, device=ctx.device)
+    with pytest.raises(ValueError):   # n_mods must be 2 or 3
+        native.call("he_slot_pcmm_encode_pts_ext", ctx.handle, pt.data_ptr(), 2, 4, pts.data_ptr(), ctx.stream())
+    native.call("he_slot_bsgs_plan_create_ext", ctx.handle, pts.data_ptr(), 16, 16, 1, 3, ctypes.byref(h))
+    n = ctypes.c_uint64()
+    native.call("he_slot_pcmm_workspace_bytes", h, ctypes.byref(n))
+    ws = torch.empty(n.value // 4 + 1, dtype=torch.int32, device=ctx.device)
+    ct = torch.zeros((1, 2, 2, N), dtype=torch.int32, device=ctx.device)
+    out = torch.zeros((1, 2, N), dtype=torch.int32, device=ctx.device)
+    keys = torch.zeros((15, 4, 2, 3, N), dtype=torch.int32, device=ctx.device)
+    led = native.HeLedgerC()
+    with pytest.raises(ValueError):   # empty batch
+        native.call("he_slot_pcmm_run_batch", h, ct.data_ptr(), 0, 1, keys.data_ptr(), keys.data_ptr(), out.data_ptr(),
+                    ws.data_ptr(), ws.numel() * 4, ctx.stream(), ctypes.byref(led))
+    with pytest.raises(NeedsBootstrapError):
+        native.call("he_slot_pcmm_run_batch", h, ct.data_ptr(), 1, 0, keys.data_ptr(), keys.data_ptr(), out.data_ptr(),
+                    ws.data_ptr(), ws.numel() * 4, ctx.stream(), ctypes.byref(led))
+    with pytest.raises(ValueError):   # workspace too small
+        native.call("he_slot_pcmm_run_batch", h, ct.data_ptr(), 1, 1, keys.data_ptr(), keys.data_ptr(), out.data_ptr(),
+                    ws.data_ptr(), 64, ctx.stream(), ctypes.byref(led))
+    native.lib().he_slot_pcmm_plan_destroy(h)
