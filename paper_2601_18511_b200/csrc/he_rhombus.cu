@@ -1313,11 +1313,18 @@ __global__ void k_sd_combine(const uint32_t* __restrict__ UW, const uint32_t* __
   const uint32_t* lb = LB + (((size_t)L * cnt + z) * 2) * N;
   const uint32_t* b = bh + z * bs + L * bls;
   uint32_t* o = out + z * os + (size_t)L * 2 * N;
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
-    const uint32_t u = mulmod_b(sub_mod(U[c], lb[c], q), pinv, mu, q);
-    const uint32_t w = mulmod_b(sub_mod(U[N + c], lb[N + c], q), pinv, mu, q);
-    o[c] = u;
-    o[N + c] = add_mod(b[perm[c]], w, q);
+  for (uint32_t c4 = blockIdx.x * blockDim.x + threadIdx.x; c4 < N / 4; c4 += gridDim.x * blockDim.x) {
+    const uint4 uu = reinterpret_cast<const uint4*>(U)[c4], lu = reinterpret_cast<const uint4*>(lb)[c4];
+    const uint4 uw = reinterpret_cast<const uint4*>(U + N)[c4], lw = reinterpret_cast<const uint4*>(lb + N)[c4];
+    const uint4 pc = reinterpret_cast<const uint4*>(perm)[c4];
+    reinterpret_cast<uint4*>(o)[c4] =
+        make_uint4(mulmod_b(sub_mod(uu.x, lu.x, q), pinv, mu, q), mulmod_b(sub_mod(uu.y, lu.y, q), pinv, mu, q),
+                   mulmod_b(sub_mod(uu.z, lu.z, q), pinv, mu, q), mulmod_b(sub_mod(uu.w, lu.w, q), pinv, mu, q));
+    reinterpret_cast<uint4*>(o + N)[c4] =
+        make_uint4(add_mod(b[pc.x], mulmod_b(sub_mod(uw.x, lw.x, q), pinv, mu, q), q),
+                   add_mod(b[pc.y], mulmod_b(sub_mod(uw.y, lw.y, q), pinv, mu, q), q),
+                   add_mod(b[pc.z], mulmod_b(sub_mod(uw.z, lw.z, q), pinv, mu, q), q),
+                   add_mod(b[pc.w], mulmod_b(sub_mod(uw.w, lw.w, q), pinv, mu, q), q));
   }
 }
 // inner_z [L][ab][N] = sum_{i < b} pt[i + z b][L] * baby[i][L][ab]   (NTT domain), z = giant group
