@@ -1233,12 +1233,26 @@ __global__ void k_sd_digits_plain(const uint32_t* __restrict__ a, uint64_t as, u
                                   uint32_t* __restrict__ D) {
   const uint32_t z = blockIdx.z;
   const uint32_t* src = a + z * as;
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
-    const uint32_t dg[2] = {shoup_mul(src[x], qh0, qh0p, M.m[0]), shoup_mul(src[ls + x], qh1, qh1p, M.m[1])};
+  for (uint32_t x4 = blockIdx.x * blockDim.x + threadIdx.x; x4 < N / 4; x4 += gridDim.x * blockDim.x) {
+    const uint4 a0 = reinterpret_cast<const uint4*>(src)[x4], a1 = reinterpret_cast<const uint4*>(src + ls)[x4];
+    const uint32_t v0[4] = {a0.x, a0.y, a0.z, a0.w}, v1[4] = {a1.x, a1.y, a1.z, a1.w};
+    uint32_t dg[2][4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      dg[0][e] = shoup_mul(v0[e], qh0, qh0p, M.m[0]);
+      dg[1][e] = shoup_mul(v1[e], qh1, qh1p, M.m[1]);
+    }
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int mod = 0; mod < 3; ++mod) D[(((size_t)mod * cnt + z) * 2 + i) * N + x] = dg[i] % M.m[mod];
+      for (int mod = 0; mod < 3; ++mod) {
+        const uint32_t q = M.m[mod];
+        const uint64_t mu = M.mu[mod];
+        uint32_t r[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) r[e] = barrett64(dg[i][e], mu, q);
+        reinterpret_cast<uint4*>(D + (((size_t)mod * cnt + z) * 2 + i) * N)[x4] = make_uint4(r[0], r[1], r[2], r[3]);
+      }
   }
 }
 // rotation z: UW [mod][z][part][N] = sum_t D^[mod][dz][t][perm_z c] K_z[t][part][mod][c]   (dz = hoist ? 0 : z)
@@ -1251,17 +1265,26 @@ __global__ void k_sd_mac_t(const uint32_t* __restrict__ D, uint32_t dcnt, int ho
   const uint32_t* perm = perms + (size_t)z * N;
   const uint32_t* Kz = K + (size_t)z * T * 6 * N;
   const uint32_t* Dz = D + ((size_t)mod * dcnt + dz) * T * N;
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
-    const uint32_t pc = perm[c];
-    uint64_t u = 0, w = 0;   // 4 products < 2^60 each
+  for (uint32_t c4 = blockIdx.x * blockDim.x + threadIdx.x; c4 < N / 4; c4 += gridDim.x * blockDim.x) {
+    const uint4 pv = reinterpret_cast<const uint4*>(perm)[c4];   // 4 coefficients per thread, 16-byte I/O
+    const uint32_t pc[4] = {pv.x, pv.y, pv.z, pv.w};
+    uint64_t u[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};   // T products < 2^60 each
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      const uint64_t dv = Dz[(size_t)t * N + pc];
-      u += dv * Kz[(size_t)((t * 2 + 0) * 3 + mod) * N + c];
-      w += dv * Kz[(size_t)((t * 2 + 1) * 3 + mod) * N + c];
+      const uint4 ku = reinterpret_cast<const uint4*>(Kz + (size_t)((t * 2 + 0) * 3 + mod) * N)[c4];
+      const uint4 kw = reinterpret_cast<const uint4*>(Kz + (size_t)((t * 2 + 1) * 3 + mod) * N)[c4];
+      const uint32_t kus[4] = {ku.x, ku.y, ku.z, ku.w}, kws[4] = {kw.x, kw.y, kw.z, kw.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t dv = Dz[(size_t)t * N + pc[e]];
+        u[e] += dv * kus[e];
+        w[e] += dv * kws[e];
+      }
     }
-    UW[(((size_t)mod * cnt + z) * 2 + 0) * N + c] = barrett64(u, mu, q);
-    UW[(((size_t)mod * cnt + z) * 2 + 1) * N + c] = barrett64(w, mu, q);
+    reinterpret_cast<uint4*>(UW + (((size_t)mod * cnt + z) * 2 + 0) * N)[c4] =
+        make_uint4(barrett64(u[0], mu, q), barrett64(u[1], mu, q), barrett64(u[2], mu, q), barrett64(u[3], mu, q));
+    reinterpret_cast<uint4*>(UW + (((size_t)mod * cnt + z) * 2 + 1) * N)[c4] =
+        make_uint4(barrett64(w[0], mu, q), barrett64(w[1], mu, q), barrett64(w[2], mu, q), barrett64(w[3], mu, q));
   }
 }
 // lazy form of k_sd_mac for the baby steps of cc ciphertexts (one key read serves all; 6.3 MB per rotation):
