@@ -467,9 +467,13 @@ def side_measurements(P, dev):
             torch.cuda.synchronize()
             err = float(np.abs(decrypt_vector(ctx, keys.s_up_ntt, y) - clear_pcmv(W, v)).max())
             gms = graph_ms(lambda: pcmv_rhombus(ctx, plan, keys, x))
+            info = plan.info()
             rh[f"{n_out}x{n_in}"] = {"ms_per_op": round(e0.elapsed_time(e1) / 5, 3), "ms_per_op_cuda_graph": gms,
                                      "precision_bits": round(-math.log2(err), 1),
-                                     "key_switches": (P.rhombus_degree - 1) * -(-n_out // P.rhombus_degree) + 1}
+                                     "split_point": info[1], "window": info[0],
+                                     "key_switches": plan.key_switches() + 1,
+                                     "key_switches_split0": (P.rhombus_degree - 1) * -(-n_out // P.rhombus_degree) + 1,
+                                     "pt_ct_products": info[6] * info[4]}
             del plan
         out["rhombus_pcmv"] = {"workload": "BASELINE config 5: Rhombus PCMv at RLWE degree 4096 "
                                            "(decompose KS -> MVM + PackLWEs -> rescale/compose), 1 GPU", **rh}

@@ -164,45 +164,79 @@ he_status he_pcmm_profile(const he_pcmm_plan* plan, int enable);
 he_status he_pcmm_profile_read(const he_pcmm_plan* plan, double* ms, uint32_t* launches, uint32_t n);
 
 /* ---------------------------------------------------------------- Rhombus PCMv (K6), degree n = rhombus_degree */
-/* Vector layout (App. A + h): element e sits at degree-N coefficient
- * (e / n) + rho * h(e mod n), rho = N / n.  No hesim entry point exists for the PCMv
- * (SPEC.md:8); the calling convention follows pcmm_depth1 (matmul.py:152-162). */
+/* No hesim entry point exists for the PCMv; the calling convention follows pcmm_depth1
+ * (matmul.py:152-162).  Rhombus [rhombus] as the paper uses it:
+ *   decompose (key switch s -> s'(X^rho), free X^rho split, rho = N / n)  ->  products  ->  output
+ *   packing (PackLWEs with Galois key switches)  ->  rescale  ->  compose.
+ * Split point (Rhombus's input/output packing trade-off): window w = n >> split.  Input layout:
+ * element e at degree-N coefficient (e / w) + rho h_w(e mod w) (h_w fixes the top bit and reverses
+ * the others; w = n is the h layout of PAPER.md:674-680), so every input piece carries w values and
+ * one plaintext x ciphertext product yields n / w inner products.  Output packing then needs w - 1
+ * Galois key switches per output piece instead of n - 1.  Output layout (any window): element r at
+ * (r / n) + rho h_n(r mod n).  Oracle: or_rhombus_pcmv_w (oracle/he_oracle_pcmv.c). */
+he_status he_encrypt_vector_w(const he_context* ctx, const uint32_t* s_ntt_dev, const double* v_dev, uint32_t n_vals,
+                              uint32_t window, uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream);
+/* window = n (split point 0) */
 he_status he_encrypt_vector(const he_context* ctx, const uint32_t* s_ntt_dev, const double* v_dev, uint32_t n_vals,
                             uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream);
 /* keys: sparse secret s' (int32 [n]), s'(X^rho) (int32 [N]) and its NTT per limb (u32 [2][N]),
  * the decompose key s -> s'(X^rho) (u32 [2][2][3][N], NTT domain, moduli q0 q1 P) and the
- * Galois keys sigma_{2^l+1}(s') -> s' (u32 [log2 n][2][2][3][n], NTT domain) */
+ * Galois keys sigma_{2^l+1}(s') -> s' (u32 [log2 n][2][2][3][n], NTT domain; a window-w plan uses
+ * the top log2 w of them) */
 he_status he_rhombus_keygen(const he_context* ctx, uint64_t seed, const int32_t* s_dev, int32_t* s_small_dev,
                             int32_t* s_up_dev, uint32_t* s_up_ntt_dev, uint32_t* ksk_dec_dev, uint32_t* gal_dev,
                             void* stream);
-/* weights: W~ = round(q1 W) as NTT-domain plaintexts u32 [2][ceil(n_out/n) n][ceil(n_in/n)][n] */
+/* weights: W~ = round(q1 W) as NTT-domain plaintexts u32 [2][leaves][ceil(n_in/w)][n],
+ * leaves = ceil(n_out/n) * w / groups.  groups > 1: a leaf-interleaved multi-GPU shard holding the
+ * leaves j = group + groups * jl of every output piece (rows r = n o + h_n(u w + j)). */
+he_status he_rhombus_weight_bytes_w(const he_context* ctx, uint32_t n_out, uint32_t n_in, uint32_t window,
+                                    uint32_t groups, uint64_t* bytes);
+he_status he_rhombus_encode_weights_w(const he_context* ctx, const double* w_dev, uint32_t n_out, uint32_t n_in,
+                                      uint32_t window, uint32_t groups, uint32_t group, uint32_t* wpt_dev, void* stream);
+he_status he_rhombus_plan_create_w(const he_context* ctx, const uint32_t* wpt_dev, uint32_t n_out, uint32_t n_in,
+                                   uint32_t window, uint32_t groups, uint32_t group, he_rhombus_plan** out);
+/* the split-point-0, one-group forms of the three calls above */
 he_status he_rhombus_weight_bytes(const he_context* ctx, uint32_t n_out, uint32_t n_in, uint64_t* bytes);
 he_status he_rhombus_encode_weights(const he_context* ctx, const double* w_dev, uint32_t n_out, uint32_t n_in,
                                     uint32_t* wpt_dev, void* stream);
 he_status he_rhombus_plan_create(const he_context* ctx, const uint32_t* wpt_dev, uint32_t n_out, uint32_t n_in,
                                  he_rhombus_plan** out);
+/* info[0..6] = {window, split, groups, group, input pieces, output pieces, leaves} */
+he_status he_rhombus_plan_info(const he_rhombus_plan* plan, uint32_t* info);
 he_status he_rhombus_plan_destroy(he_rhombus_plan* plan);
 he_status he_rhombus_workspace_bytes(const he_rhombus_plan* plan, uint64_t* bytes);
 /* level-1 degree-N ct [2][2][N] under s -> level-0 degree-N ct [2 (a, b)][N] under s'(X^rho)
- * holding W v; ledger: pc_mults += n_out * ceil(n_in/n), ct_rotations += (n - 1) * ceil(n_out/n),
- * rescales += 1 */
+ * holding W v; ledger: pc_mults += plaintext x ciphertext products (leaves * input pieces),
+ * ct_rotations += (w - 1) * ceil(n_out/n) Galois key switches, rescales += 1.  groups must be 1. */
 he_status he_rhombus_run(const he_rhombus_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
                          const uint32_t* ksk_dec_dev, const uint32_t* gal_dev, uint32_t* out_dev, void* workspace_dev,
                          uint64_t workspace_bytes, void* stream, he_ledger* ledger);
-/* Multi-GPU shards: a plan over a column slice W[:, n piece0 ..] and/or a
- * row slice W[n opiece0 .., :] (piece = n = rhombus_degree elements) runs on the full input
- * ciphertext and writes its LEVEL-1 composed partial output out_l1 [2 limbs][2 (a, b)][N] (zeros
- * outside its output pieces; no rescale).  Row shards own disjoint output pieces (their words equal
- * the unsharded run's); column shards produce partial sums of the same pieces.  he_rhombus_combine
- * sums `count` such outputs mod q_i (parts [count][2][2][N], e.g. after an all-gather) and rescales
- * once -> level-0 ct [2][N].  ledger: the shard run counts pc_mults / ct_rotations, the combine
- * the one rescale. */
+/* Multi-GPU shards.
+ * Column shards ("the ciphertext is masked and each GPU is assigned 4096/8 values"): a plan over the
+ * columns [w piece0, ..) of W (groups 1) runs on input pieces piece0.. of the full input ciphertext
+ * (and/or on output pieces from opiece0) and writes its LEVEL-1 composed partial output out_l1
+ * [2 limbs][2 (a, b)][N] (zeros outside its output pieces; no rescale).  he_rhombus_combine sums `count`
+ * such outputs mod q_i (parts [count][2][2][N], e.g. after an all-gather) and rescales once ->
+ * level-0 ct [2][N] (the same plaintext as one GPU, different key-switching noise). */
 he_status he_rhombus_run_shard(const he_rhombus_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
                                const uint32_t* ksk_dec_dev, const uint32_t* gal_dev, uint32_t piece0, uint32_t opiece0,
                                uint32_t* out_l1_dev, void* workspace_dev, uint64_t workspace_bytes, void* stream,
                                he_ledger* ledger);
 he_status he_rhombus_combine(const he_context* ctx, const uint32_t* parts_dev, uint32_t count, uint32_t* out_dev,
                              void* stream, he_ledger* ledger);
+/* Row shards ("broadcast the ciphertext ... split the plaintext matrix"): a plan with groups = G
+ * ranks (group g) runs the products of its leaves and the packing levels below the top log2 G and
+ * writes its subtree roots roots_out [2 limbs][p_out][2][n] (NTT domain, level 1).  After an
+ * all-gather of the G roots ([G][2][p_out][2][n], rank order), he_rhombus_finish (any rank's plan)
+ * runs the top log2 G levels, the rescale and the compose: the output words equal the one-GPU
+ * run's.  ledger: the subtree run counts its products and key switches, the finish (G - 1) p_out key
+ * switches and the rescale. */
+he_status he_rhombus_run_subtree(const he_rhombus_plan* plan, const uint32_t* ct_in_dev, uint32_t level,
+                                 const uint32_t* ksk_dec_dev, const uint32_t* gal_dev, uint32_t* roots_out_dev,
+                                 void* workspace_dev, uint64_t workspace_bytes, void* stream, he_ledger* ledger);
+he_status he_rhombus_finish(const he_rhombus_plan* plan, const uint32_t* roots_dev, const uint32_t* gal_dev,
+                            uint32_t* out_dev, void* workspace_dev, uint64_t workspace_bytes, void* stream,
+                            he_ledger* ledger);
 
 /* ---------------------------------------------------------------- MLWE -> RLWE ring packing
  * The step after the PCMM toward Half-Bootstrap: each block of k MLWE output rows

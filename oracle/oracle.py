@@ -17,7 +17,7 @@ __all__ = [
     "negacyclic_mul", "negacyclic_mul_schoolbook", "sigma_table", "clear_pcmm", "mlwe_column",
     "py_mlwe_components", "py_pcmm_rows", "num_threads", "time_pcmm_sample", "rng",
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
-    "decode_vector", "rhombus_pcmv", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
+    "decode_vector", "rhombus_pcmv", "rhombus_pcmv_w", "rhombus_combine", "rhombus_window", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
     "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe", "rotation_keys", "slot_pcmm",
     "slot_bsgs", "rotation_keys_plain",
 ]
@@ -38,7 +38,7 @@ def stream_e(r: int) -> int:
 
 
 def build(force: bool = False) -> Path:
-    srcs = [_HERE / "he_oracle.c", _HERE / "he_oracle_rhombus.c"]
+    srcs = [_HERE / "he_oracle.c", _HERE / "he_oracle_rhombus.c", _HERE / "he_oracle_pcmv.c"]
     if force or not _SO.exists() or any(_SO.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
     return _SO
@@ -357,6 +357,11 @@ def _rh_lib():
             "or_rhombus_pcmv": (ctypes.c_int, [u32, u32, u32p, u32p, u32p, u32p, i64p, u32, u32, u32p, u32p]),
             "or_encode_vector": (None, [f64p, u32, u32, u32, ctypes.c_double, i64p]),
             "or_decode_vector": (None, [i64p, u32, u32, u32, ctypes.c_double, f64p]),
+            "or_encode_vector_w": (None, [f64p, u32, u32, u32, u32, ctypes.c_double, i64p]),
+            "or_window_reverse": (u32, [u32, u32]),
+            "or_rhombus_pcmv_w": (ctypes.c_int, [u32, u32, u32, u32p, u32p, u32p, u32p, i64p, u32, u32, u32,
+                                                 ctypes.c_int, u32p]),
+            "or_rhombus_combine": (None, [u32p, u32, u32, u32p, u32p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -398,10 +403,27 @@ def keyswitch(params, c: np.ndarray, ksk: np.ndarray, n: int):
     return u, w
 
 
-def encode_vector(params, v: np.ndarray) -> np.ndarray:
+def rhombus_window(params, n_in: int, split=None) -> int:
+    """Input window w = n >> split of the Rhombus PCMv (he_oracle_pcmv.c).  Default: the largest split
+    point whose pieces still hold n_in values (w = the smallest power of two >= n_in / rho)."""
+    n, rho = params.rhombus_degree, params.N // params.rhombus_degree
+    if split is None:
+        w = 1
+        while w * rho < n_in:
+            w *= 2
+        return min(w, n)
+    w = n >> int(split)
+    if w < 1 or w * rho < n_in:
+        raise ValueError(f"split {split}: window {w} x {rho} pieces cannot hold {n_in} values")
+    return w
+
+
+def encode_vector(params, v: np.ndarray, window=None) -> np.ndarray:
+    """Input layout: element e at (e / w) + rho h_w(e mod w); window None = the old h layout (w = n)."""
     v = np.ascontiguousarray(v, dtype=np.float64)
     pt = np.zeros((1, params.N), np.int64)
-    _rh_lib().or_encode_vector(_f64(v), len(v), params.N, params.rhombus_degree, params.delta, _i64(pt))
+    w = params.rhombus_degree if window is None else int(window)
+    _rh_lib().or_encode_vector_w(_f64(v), len(v), params.N, params.rhombus_degree, w, params.delta, _i64(pt))
     return pt
 
 
@@ -425,6 +447,32 @@ def rhombus_pcmv(params, ct_in: np.ndarray, ksk: np.ndarray, gal: np.ndarray, Wt
                               _u32(np.ascontiguousarray(ksk)), _u32(np.ascontiguousarray(gal)), _i64(Wt), n_out, n_in,
                               _u32(pieces), _u32(out))
     return pieces, out
+
+
+def rhombus_pcmv_w(params, ct_in: np.ndarray, ksk: np.ndarray, gal: np.ndarray, Wt: np.ndarray, n_in: int,
+                   window: int, piece0: int = 0, level1: bool = False) -> np.ndarray:
+    """Windowed (split-point) PCMv, he_oracle_pcmv.c or_rhombus_pcmv_w: level1=False -> [2 (a, b)][N]
+    level 0; level1=True -> the column shard's level-1 composed output [2 limbs][2][N]."""
+    N, n = params.N, params.rhombus_degree
+    Wt = np.ascontiguousarray(Wt, dtype=np.int64)
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    out = np.zeros((2, 2, N) if level1 else (2, N), np.uint32)
+    rc = _rh_lib().or_rhombus_pcmv_w(N, n, int(window), _u32(m), _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
+                                     _u32(np.ascontiguousarray(ksk, dtype=np.uint32)),
+                                     _u32(np.ascontiguousarray(gal, dtype=np.uint32)), _i64(Wt), Wt.shape[0], n_in,
+                                     int(piece0), int(level1), _u32(out))
+    if rc:
+        raise ValueError("or_rhombus_pcmv_w: bad shape / window")
+    return out
+
+
+def rhombus_combine(params, parts: np.ndarray) -> np.ndarray:
+    """Sum column-shard level-1 outputs [count][2][2][N] mod q_i, rescale by q1 -> [2][N]."""
+    parts = np.ascontiguousarray(parts, dtype=np.uint32)
+    m = np.ascontiguousarray(np.array(params.ks_moduli, dtype=np.uint32))
+    out = np.zeros((2, params.N), np.uint32)
+    _rh_lib().or_rhombus_combine(_u32(parts), parts.shape[0], params.N, _u32(m), _u32(out))
+    return out
 
 
 def rhombus_weights(params, W: np.ndarray) -> np.ndarray:

@@ -211,10 +211,15 @@ extern "C" he_status he_encrypt_acts(const he_context* c, const uint32_t* s_ntt_
   return HE_OK;
 }
 
-extern "C" he_status he_encrypt_vector(const he_context* c, const uint32_t* s_ntt_dev, const double* v_dev,
-                                       uint32_t n_vals, uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream) {
+extern "C" he_status he_encrypt_vector_w(const he_context* c, const uint32_t* s_ntt_dev, const double* v_dev,
+                                         uint32_t n_vals, uint32_t window, uint64_t seed, uint32_t r0, uint32_t* ct_dev,
+                                         void* stream) {
   if (!c || !s_ntt_dev || !v_dev || !ct_dev) return fail(HE_EINVAL, "null argument");
-  if (n_vals == 0 || n_vals > c->R.N) return fail(HE_EINVAL, "vector length %u outside [1, N]", n_vals);
+  const uint32_t n = c->R.n_rh, rho = c->R.N / n;
+  if (window == 0 || window > n || (window & (window - 1)))
+    return fail(HE_EINVAL, "window %u must be a power of two in [1, %u]", window, n);
+  if (n_vals == 0 || n_vals > (uint64_t)window * rho)
+    return fail(HE_EINVAL, "vector length %u outside [1, %u] (window %u x %u pieces)", n_vals, window * rho, window, rho);
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t N = c->R.N;
   HE_CUDA(launch_gen_a(c->R, seed, r0, 1, ct_dev, st), "sample a");
@@ -224,8 +229,14 @@ extern "C" he_status he_encrypt_vector(const he_context* c, const uint32_t* s_nt
     HE_CUDA(launch_pointwise_mul(bslot, N, s_ntt_dev + (size_t)L * N, N, 1, c->R.q[L], bslot, N, st), "a^ * s^");
     HE_CUDA(ntt_inverse(c->ntt[L], bslot, 1, N, st), "INTT(a s)");
   }
-  HE_CUDA(launch_finish_encrypt(c->R, v_dev, n_vals, seed, r0, 1, ct_dev, st, 1), "finish encrypt");
+  HE_CUDA(launch_finish_encrypt(c->R, v_dev, n_vals, seed, r0, 1, ct_dev, st, 1, window), "finish encrypt");
   return HE_OK;
+}
+
+extern "C" he_status he_encrypt_vector(const he_context* c, const uint32_t* s_ntt_dev, const double* v_dev,
+                                       uint32_t n_vals, uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream) {
+  if (!c) return fail(HE_EINVAL, "null argument");
+  return he_encrypt_vector_w(c, s_ntt_dev, v_dev, n_vals, c->R.n_rh, seed, r0, ct_dev, stream);
 }
 
 extern "C" he_status he_encrypt_poly(const he_context* c, const uint32_t* s_ntt_dev, const int64_t* pt_dev,

@@ -271,16 +271,17 @@ cudaError_t launch_pointwise_mul(const uint32_t* x, uint64_t x_stride, const uin
 }
 
 // b = -(a s) + Ecd_coeff(acts) + e; the b slot holds a*s on entry.
-// layout 0: App. A activation block (tokens x n_in); layout 1: Rhombus vector of n_in values,
-// element e at coefficient (e / n_rh) + rho h(e mod n_rh)
+// layout 0: App. A activation block (tokens x n_in); layout 1: Rhombus vector of n_in values with
+// window w (split point, oracle or_encode_vector_w): element e at coefficient (e / w) + rho h_w(e mod w),
+// rho = N / n_rh (w = n_rh: the plain h layout of PAPER.md:674-680)
 __global__ void finish_encrypt_kernel(const double* __restrict__ acts, uint32_t n_in, uint32_t d, uint32_t k,
                                       int logk, uint32_t N, double delta, uint64_t seed, uint32_t r0, uint32_t q0,
-                                      uint32_t q1, uint32_t* ct, int layout, uint32_t n_rh) {
+                                      uint32_t q1, uint32_t* ct, int layout, uint32_t n_rh, uint32_t win) {
   const uint32_t r = blockIdx.y;
   const uint64_t ekey = rng_key(seed, stream_e(r0 + r));
   const uint32_t half = d / 2;
   const int lh = ilog2_h(half);
-  const int lrh = ilog2_h(n_rh);
+  const int lw = ilog2_h(win);
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
     long long pt = 0;
     if (layout == 0) {
@@ -293,9 +294,11 @@ __global__ void finish_encrypt_kernel(const double* __restrict__ acts, uint32_t 
       pt = reinterpret_cast<const long long*>(acts)[(size_t)r * N + c];
     } else {
       const uint32_t rho = N / n_rh, p = c % rho, kk = c / rho;
-      const uint32_t hk = (kk & (n_rh >> 1)) | bitrev_h(kk & ((n_rh >> 1) - 1), lrh - 1);
-      const uint32_t e = n_rh * p + hk;
-      if (e < n_in) pt = __double2ll_rn(__dmul_rn(delta, acts[e]));
+      if (kk < win) {
+        const uint32_t hk = win < 2 ? 0u : (kk & (win >> 1)) | bitrev_h(kk & ((win >> 1) - 1), lw - 1);
+        const uint32_t e = win * p + hk;
+        if (e < n_in) pt = __double2ll_rn(__dmul_rn(delta, acts[e]));
+      }
     }
     const long long e = cbd21_d(rng_draw(ekey, c));
 #pragma unroll
@@ -309,10 +312,10 @@ __global__ void finish_encrypt_kernel(const double* __restrict__ acts, uint32_t 
   }
 }
 cudaError_t launch_finish_encrypt(const RingDims& R, const double* acts, uint32_t n_in, uint64_t seed, uint32_t r0,
-                                  uint32_t n_ct, uint32_t* ct, cudaStream_t st, int layout) {
+                                  uint32_t n_ct, uint32_t* ct, cudaStream_t st, int layout, uint32_t win) {
   dim3 g((R.N + 1023) / 1024, n_ct);
   finish_encrypt_kernel<<<g, 256, 0, st>>>(acts, n_in, R.d, R.k, (int)R.logk, R.N, (double)(1ull << R.log_delta),
-                                           seed, r0, R.q[0], R.q[1], ct, layout, R.n_rh);
+                                           seed, r0, R.q[0], R.q[1], ct, layout, R.n_rh, win ? win : R.n_rh);
   return cudaGetLastError();
 }
 

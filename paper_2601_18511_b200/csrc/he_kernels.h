@@ -127,7 +127,8 @@ cudaError_t launch_gen_a(const RingDims& R, uint64_t seed, uint32_t r0, uint32_t
 cudaError_t launch_pointwise_mul(const uint32_t* x, uint64_t x_stride, const uint32_t* y, uint32_t n,
                                  uint32_t count, uint32_t q, uint32_t* out, uint64_t out_stride, cudaStream_t st);
 cudaError_t launch_finish_encrypt(const RingDims& R, const double* acts, uint32_t n_in, uint64_t seed, uint32_t r0,
-                                  uint32_t n_ct, uint32_t* ct, cudaStream_t st, int layout = 0);
+                                  uint32_t n_ct, uint32_t* ct, cudaStream_t st, int layout = 0,
+                                  uint32_t win = 0);
 cudaError_t launch_phase(const uint32_t* b, uint64_t b_stride, const uint32_t* as, uint64_t as_stride, uint32_t n,
                          uint32_t count, uint32_t q, int64_t* phase, cudaStream_t st);
 cudaError_t launch_mlwe_rows_to_poly(const RingDims& R, const uint32_t* out_a, uint32_t row0, uint32_t rows, uint32_t* A,

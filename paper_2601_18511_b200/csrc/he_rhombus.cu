@@ -220,27 +220,45 @@ __global__ void k_decomp_split(const uint32_t* __restrict__ UW, const uint32_t* 
 }
 
 // ------------------------------------------------------------------ weights (plan)
-// Wpt [L][leaf][p][n] coefficient form before the NTT:  w(Z) = cpack * sum_k W~[r][n p + h(k)] Z^{-k}
+// Windowed (split-point) plaintexts, oracle or_rhombus_pcmv_w.  Window w = n / U, U = 2^s rows per product:
+//   pt_{o,j,p}(X) = w^-1 sum_{u<U} X^{u w} sum_{i<w} W~[r(o,j,u)][w p + i] X^{-h_w(i)},  r = n o + h_n(u w + j)
+// Coefficient pos of pt: pos = 0 -> (u 0, h 0); pos in [1, n - w] -> u = ceil(pos / w), h = u w - pos;
+// pos in (n - w, n) -> u = 0, h = n - pos, negated (X^-h = -X^{n-h}).  Leaf jl of output piece o in a
+// leaf-interleaved shard (G groups, this plan's group g) is global leaf j = g + G jl.
+// Wpt [L][leaf][p][n] coefficient form before the NTT.
 __global__ void k_rh_weights(const double* __restrict__ W, uint32_t n_out, uint32_t n_in, uint32_t n, int logn,
-                             uint32_t p_in, uint64_t leaves, uint32_t q0, uint32_t q1, uint32_t cp0, uint32_t cp1,
-                             double delta_w, uint32_t* __restrict__ out) {
+                             uint32_t win, int logw, uint32_t G, uint32_t g, uint32_t p_in, uint64_t leaves, uint32_t q0,
+                             uint32_t q1, uint32_t cp0, uint32_t cp1, double delta_w, uint32_t* __restrict__ out) {
   const uint64_t per_l = leaves * p_in * n;
+  const uint32_t lpp = win / G;  // leaves per output piece in this plan
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < per_l; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = (uint32_t)(x % n);
+    const uint32_t pos = (uint32_t)(x % n);
     const uint64_t lp = x / n;
     const uint32_t p = (uint32_t)(lp % p_in);
     const uint64_t leaf = lp / p_in;
-    const uint32_t o = (uint32_t)(leaf / n), j = (uint32_t)(leaf % n);
-    const uint32_t r = n * o + half_reverse(j, n, logn);
-    const uint32_t col = n * p + half_reverse(k, n, logn);
+    const uint32_t o = (uint32_t)(leaf / lpp), j = g + G * (uint32_t)(leaf % lpp);
+    uint32_t u, hw;
+    bool neg = false;
+    if (pos == 0) {
+      u = 0;
+      hw = 0;
+    } else if (pos <= n - win) {
+      u = (pos + win - 1) >> logw;
+      hw = u * win - pos;
+    } else {
+      u = 0;
+      hw = n - pos;
+      neg = true;
+    }
+    const uint32_t r = n * o + half_reverse(u * win + j, n, logn);
+    const uint32_t col = win * p + (win < 2 ? 0u : half_reverse(hw, win, logw));
     long long wv = 0;
     if (r < n_out && col < n_in) wv = __double2ll_rn(__dmul_rn(delta_w, W[(size_t)r * n_in + col]));
-    const uint32_t pos = k == 0 ? 0 : n - k;
 #pragma unroll
     for (int L = 0; L < 2; ++L) {
       const uint32_t q = L ? q1 : q0;
       uint32_t v = mul_mod(from_i64(wv, q), L ? cp1 : cp0, q);
-      if (k != 0 && v) v = q - v;
+      if (neg && v) v = q - v;
       out[(size_t)L * per_l + lp * n + pos] = v;
     }
   }
@@ -368,6 +386,20 @@ __global__ void k_rh_compose_l1(const uint32_t* __restrict__ A, uint32_t p_out, 
     out[((size_t)L * 2 + ab) * N + o0 + o + (size_t)rho * k] = A[x];
   }
 }
+// leaf-interleaved shards: roots [G][L][p_out][2][n] (each shard's packed subtree roots, NTT domain)
+// -> A [L][p_out G][2][n] with root (o, g) at o G + g, the order the top log2 G packing levels pair
+__global__ void k_rh_gather_roots(const uint32_t* __restrict__ roots, uint32_t G, uint32_t p_out, uint32_t n,
+                                  uint32_t* __restrict__ A) {
+  const uint64_t per = (uint64_t)2 * p_out * 2 * n;  // one shard's words
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < per * G; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = (uint32_t)(x / per);
+    const uint64_t r = x % per;
+    const uint32_t c = (uint32_t)(r % (2ull * n));
+    const uint64_t lo = r / (2ull * n);
+    const uint32_t o = (uint32_t)(lo % p_out), L = (uint32_t)(lo / p_out);
+    A[(((uint64_t)L * p_out * G + (uint64_t)o * G + g) * 2) * n + c] = roots[x];
+  }
+}
 // sum of shard outputs mod q_L, then rescale by q1:  parts [count][2 limbs][2][N] -> out [2][N]
 __global__ void k_rh_combine(const uint32_t* __restrict__ parts, uint32_t count, uint32_t N, uint32_t q0, uint32_t q1,
                              uint32_t q1inv, uint32_t q1invp, uint32_t* __restrict__ out) {
@@ -413,16 +445,20 @@ int ilog2_u(uint32_t x) { return ilog2_h(x); }
 }  // namespace
 
 // ======================================================================== plan / C ABI
+// A plan covers the window w (split point s = log2(n / w)) and, for leaf-interleaved multi-GPU shards,
+// the leaves j = g + G jl of every output piece (G = 1: all of them).
 struct he_rhombus_plan {
   const he_context* ctx;
   uint32_t n_out, n_in, p_in, p_out, n, N, logn;
-  const uint32_t* wpt;       // caller-owned [2][leaves][p_in][n] NTT domain
-  uint32_t* tables;          // owned: perm [logn][n], mono [logn][2][n]
+  uint32_t win, logw, split;  // window w = n >> split
+  uint32_t G, logG, g;        // leaf groups (shards) and this plan's group
+  const uint32_t* wpt;        // caller-owned [2][leaves][p_in][n] NTT domain
+  uint32_t* tables;           // owned: perm [logn][n], mono [logn][2][n]
   Mods M;
   uint32_t qhinv[2], pinv[2], q1inv, q1invp;
 };
 
-static uint64_t leaves_of(const he_rhombus_plan* p) { return (uint64_t)p->p_out * p->n; }
+static uint64_t leaves_of(const he_rhombus_plan* p) { return (uint64_t)p->p_out * (p->win / p->G); }
 
 // Hybrid key-switching key from s_old to s_new (degree deg; moduli q0, q1, P), NTT domain:
 //   ksk[i][0][j] = alpha (uniform),  ksk[i][1][j] = g_{i,j} s_old + e - alpha s_new   (oracle or_ksk_gen)
@@ -482,31 +518,54 @@ extern "C" he_status he_rhombus_keygen(const he_context* c, uint64_t seed, const
   return cudaGetLastError() == cudaSuccess ? HE_OK : fail(HE_ECUDA, "rhombus keygen launch failed");
 }
 
-extern "C" he_status he_rhombus_weight_bytes(const he_context* c, uint32_t n_out, uint32_t n_in, uint64_t* bytes) {
-  if (!c || !bytes) return fail(HE_EINVAL, "null argument");
+// shape checks shared by the weight / plan entry points
+static he_status rh_shape(const he_context* c, uint32_t n_out, uint32_t n_in, uint32_t win, uint32_t G, uint32_t g,
+                          uint32_t* p_in, uint32_t* p_out) {
+  if (!c) return fail(HE_EINVAL, "null argument");
   if (!n_out || !n_in) return fail(HE_EINVAL, "empty weight matrix");
   const uint32_t n = c->R.n_rh, rho = c->R.N / n;
-  const uint32_t p_in = (n_in + n - 1) / n, p_out = (n_out + n - 1) / n;
-  if (p_in > rho || p_out > rho)
-    return fail(HE_EINVAL, "dim mismatch: vector dims (%u, %u) exceed the %u x %u coefficients of one ciphertext",
-                n_out, n_in, rho, n);
-  *bytes = 2ull * p_out * n * p_in * n * sizeof(uint32_t);
+  if (win == 0 || win > n || (win & (win - 1)))
+    return fail(HE_EINVAL, "window %u must be a power of two in [1, %u]", win, n);
+  if (G == 0 || (G & (G - 1)) || G > win || g >= G)
+    return fail(HE_EINVAL, "leaf groups %u (group %u) must be a power of two <= the window %u", G, g, win);
+  *p_in = (n_in + win - 1) / win;
+  *p_out = (n_out + n - 1) / n;
+  if (*p_in > rho || *p_out > rho)
+    return fail(HE_EINVAL, "dim mismatch: vector dims (%u, %u) exceed %u pieces (input window %u, output %u)", n_out,
+                n_in, rho, win, n);
   return HE_OK;
 }
 
-extern "C" he_status he_rhombus_encode_weights(const he_context* c, const double* w_dev, uint32_t n_out, uint32_t n_in,
-                                               uint32_t* wpt_dev, void* stream) {
-  uint64_t bytes;
-  he_status s = he_rhombus_weight_bytes(c, n_out, n_in, &bytes);
+extern "C" he_status he_rhombus_weight_bytes_w(const he_context* c, uint32_t n_out, uint32_t n_in, uint32_t window,
+                                               uint32_t groups, uint64_t* bytes) {
+  uint32_t p_in, p_out;
+  he_status s = rh_shape(c, n_out, n_in, window, groups, 0, &p_in, &p_out);
+  if (s) return s;
+  if (!bytes) return fail(HE_EINVAL, "null argument");
+  *bytes = 2ull * p_out * (window / groups) * p_in * c->R.n_rh * sizeof(uint32_t);
+  return HE_OK;
+}
+
+extern "C" he_status he_rhombus_weight_bytes(const he_context* c, uint32_t n_out, uint32_t n_in, uint64_t* bytes) {
+  if (!c) return fail(HE_EINVAL, "null argument");
+  return he_rhombus_weight_bytes_w(c, n_out, n_in, c->R.n_rh, 1, bytes);
+}
+
+extern "C" he_status he_rhombus_encode_weights_w(const he_context* c, const double* w_dev, uint32_t n_out,
+                                                 uint32_t n_in, uint32_t window, uint32_t groups, uint32_t group,
+                                                 uint32_t* wpt_dev, void* stream) {
+  uint32_t p_in, p_out;
+  he_status s = rh_shape(c, n_out, n_in, window, groups, group, &p_in, &p_out);
   if (s) return s;
   if (!w_dev || !wpt_dev) return fail(HE_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t n = c->R.n_rh;
-  const uint32_t p_in = (n_in + n - 1) / n, p_out = (n_out + n - 1) / n;
-  const uint64_t leaves = (uint64_t)p_out * n;
+  const uint64_t leaves = (uint64_t)p_out * (window / groups);
   const Mods M = make_mods(c->R);
-  const uint32_t cp0 = (uint32_t)powmod_h(n, M.m[0] - 2, M.m[0]), cp1 = (uint32_t)powmod_h(n, M.m[1] - 2, M.m[1]);
-  k_rh_weights<<<grid_for(leaves * p_in * n), 256, 0, st>>>(w_dev, n_out, n_in, n, ilog2_u(n), p_in, leaves, M.m[0],
+  const uint32_t cp0 = (uint32_t)powmod_h(window, M.m[0] - 2, M.m[0]);
+  const uint32_t cp1 = (uint32_t)powmod_h(window, M.m[1] - 2, M.m[1]);
+  k_rh_weights<<<grid_for(leaves * p_in * n), 256, 0, st>>>(w_dev, n_out, n_in, n, ilog2_u(n), window,
+                                                            ilog2_u(window), groups, group, p_in, leaves, M.m[0],
                                                             M.m[1], cp0, cp1, (double)M.m[1], wpt_dev);
   for (int L = 0; L < 2; ++L)
     HE_CUDA(ntt_forward(c->ntt_rh[L], wpt_dev + (size_t)L * leaves * p_in * n, (uint32_t)(leaves * p_in), n, st),
@@ -514,10 +573,17 @@ extern "C" he_status he_rhombus_encode_weights(const he_context* c, const double
   return HE_OK;
 }
 
-extern "C" he_status he_rhombus_plan_create(const he_context* c, const uint32_t* wpt_dev, uint32_t n_out, uint32_t n_in,
-                                            he_rhombus_plan** out) {
-  uint64_t bytes;
-  he_status s = he_rhombus_weight_bytes(c, n_out, n_in, &bytes);
+extern "C" he_status he_rhombus_encode_weights(const he_context* c, const double* w_dev, uint32_t n_out, uint32_t n_in,
+                                               uint32_t* wpt_dev, void* stream) {
+  if (!c) return fail(HE_EINVAL, "null argument");
+  return he_rhombus_encode_weights_w(c, w_dev, n_out, n_in, c->R.n_rh, 1, 0, wpt_dev, stream);
+}
+
+extern "C" he_status he_rhombus_plan_create_w(const he_context* c, const uint32_t* wpt_dev, uint32_t n_out,
+                                              uint32_t n_in, uint32_t window, uint32_t groups, uint32_t group,
+                                              he_rhombus_plan** out) {
+  uint32_t p_in, p_out;
+  he_status s = rh_shape(c, n_out, n_in, window, groups, group, &p_in, &p_out);
   if (s) return s;
   if (!wpt_dev || !out) return fail(HE_EINVAL, "null argument");
   he_rhombus_plan* p = new (std::nothrow) he_rhombus_plan();
@@ -528,8 +594,14 @@ extern "C" he_status he_rhombus_plan_create(const he_context* c, const uint32_t*
   p->logn = (uint32_t)ilog2_u(p->n);
   p->n_out = n_out;
   p->n_in = n_in;
-  p->p_in = (n_in + p->n - 1) / p->n;
-  p->p_out = (n_out + p->n - 1) / p->n;
+  p->p_in = p_in;
+  p->p_out = p_out;
+  p->win = window;
+  p->logw = (uint32_t)ilog2_u(window);
+  p->split = p->logn - p->logw;
+  p->G = groups;
+  p->logG = (uint32_t)ilog2_u(groups);
+  p->g = group;
   p->wpt = wpt_dev;
   p->M = make_mods(c->R);
   for (int i = 0; i < 2; ++i) {
@@ -579,6 +651,24 @@ extern "C" he_status he_rhombus_plan_create(const he_context* c, const uint32_t*
   return HE_OK;
 }
 
+extern "C" he_status he_rhombus_plan_create(const he_context* c, const uint32_t* wpt_dev, uint32_t n_out, uint32_t n_in,
+                                            he_rhombus_plan** out) {
+  if (!c) return fail(HE_EINVAL, "null argument");
+  return he_rhombus_plan_create_w(c, wpt_dev, n_out, n_in, c->R.n_rh, 1, 0, out);
+}
+
+extern "C" he_status he_rhombus_plan_info(const he_rhombus_plan* p, uint32_t* info) {
+  if (!p || !info) return fail(HE_EINVAL, "null argument");
+  info[0] = p->win;
+  info[1] = p->split;
+  info[2] = p->G;
+  info[3] = p->g;
+  info[4] = p->p_in;
+  info[5] = p->p_out;
+  info[6] = (uint32_t)leaves_of(p);
+  return HE_OK;
+}
+
 extern "C" he_status he_rhombus_plan_destroy(he_rhombus_plan* p) {
   if (p) {
     if (p->tables) cudaFree(p->tables);
@@ -587,12 +677,15 @@ extern "C" he_status he_rhombus_plan_destroy(he_rhombus_plan* p) {
   return HE_OK;
 }
 
-// workspace carve-up (words)
+// workspace carve-up (words); the packing buffers hold max(leaves, p_out G) ciphertexts (the finish
+// of a leaf-interleaved shard packs p_out G roots)
 struct RhWs {
   uint32_t *pieces, *A0, *A1, *T, *C, *D, *UW, *LB, *dD, *dUW;
 };
 static uint64_t rh_ws_words(const he_rhombus_plan* p, RhWs* w, uint32_t* base) {
-  const uint64_t n = p->n, N = p->N, leaves = leaves_of(p), c1 = leaves / 2;
+  const uint64_t n = p->n, N = p->N;
+  const uint64_t cap = std::max<uint64_t>(leaves_of(p), (uint64_t)p->p_out * p->G);
+  const uint64_t c1 = std::max<uint64_t>(cap / 2, 1);
   uint64_t off = 0;
   auto take = [&](uint32_t*& ptr, uint64_t words) {
     if (w) ptr = base + off;
@@ -601,7 +694,7 @@ static uint64_t rh_ws_words(const he_rhombus_plan* p, RhWs* w, uint32_t* base) {
   RhWs dummy;
   RhWs& r = w ? *w : dummy;
   take(r.pieces, 2ull * p->p_in * 2 * n);
-  take(r.A0, 2ull * leaves * 2 * n);
+  take(r.A0, 2ull * cap * 2 * n);
   take(r.A1, 2ull * c1 * 2 * n);
   take(r.T, 2ull * c1 * 2 * n);
   take(r.C, 2ull * c1 * n);
@@ -619,49 +712,20 @@ extern "C" he_status he_rhombus_workspace_bytes(const he_rhombus_plan* p, uint64
   return HE_OK;
 }
 
-static he_status rhombus_run_impl(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level,
-                                  const uint32_t* ksk_dec, const uint32_t* gal, uint32_t* out, void* ws_dev,
-                                  uint64_t ws_bytes, void* stream, he_ledger* ledger, uint32_t piece0, int shard,
-                                  uint32_t opiece0) {
-  if (!p) return fail(HE_EINVAL, "null plan");
-  if (shard && (piece0 + p->p_in > p->N / p->n || opiece0 + p->p_out > p->N / p->n))
-    return fail(HE_EINVAL, "shard pieces [%u, %u) in / [%u, %u) out exceed the %u pieces of one ciphertext", piece0,
-                piece0 + p->p_in, opiece0, opiece0 + p->p_out, p->N / p->n);
-  if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmv needs one level");
-  if (level != 1) return fail(HE_EINVAL, "the Rhombus PCMv runs at level 1 (got %u)", level);
-  if (!ct_in || !ksk_dec || !gal || !out || !ws_dev) return fail(HE_EINVAL, "null argument");
-  uint64_t need = rh_ws_words(p, nullptr, nullptr) * sizeof(uint32_t);
-  if (ws_bytes < need) return fail(HE_EINVAL, "workspace too small (%llu < %llu)", (unsigned long long)ws_bytes,
-                                   (unsigned long long)need);
-  cudaStream_t st = (cudaStream_t)stream;
+// PackLWEs levels lv_first..lv_last over cnt ciphertexts (A in w.A0, NTT domain); level lv combines
+// E + X^{n/2^lv} O + sigma_{2^lv + 1}(E - X^{n/2^lv} O) with O the leaf n/2^lv further on -- which, in a
+// leaf-interleaved shard holding every G-th leaf, is (n/2^lv)/G positions further in A (stride = G).
+// Returns the buffer holding the result.
+static he_status rh_pack(const he_rhombus_plan* p, const RhWs& w, const uint32_t* gal, uint32_t cnt, uint32_t lv_first,
+                         uint32_t lv_last, uint32_t stride, uint32_t** result, cudaStream_t st) {
   const he_context* c = p->ctx;
-  const uint32_t n = p->n, N = p->N, q0 = p->M.m[0], q1 = p->M.m[1], P = p->M.m[2];
-  RhWs w;
-  rh_ws_words(p, &w, (uint32_t*)ws_dev);
-  // (D) decompose: key switch the a part at degree N, then split
-  k_decomp_modup<<<grid_for(N), 256, 0, st>>>(ct_in, N, q0, q1, P, p->qhinv[0], p->qhinv[1], w.dD);
-  for (int j = 0; j < 3; ++j) HE_CUDA(ntt_forward(c->ntt[j], w.dD + (size_t)j * 2 * N, 2, N, st), "NTT(digits)");
-  k_mac<<<grid_for(N), 256, 0, st>>>(w.dD, ksk_dec, N, N, p->M, w.dUW);
-  for (int j = 0; j < 3; ++j) HE_CUDA(ntt_inverse(c->ntt[j], w.dUW + (size_t)j * 2 * N, 2, N, st), "INTT(U,W)");
-  k_decomp_split<<<grid_for((uint64_t)p->p_in * n), 256, 0, st>>>(w.dUW, ct_in, N, n, p->p_in, piece0, q0, q1, P,
-                                                                   p->pinv[0], p->pinv[1], w.pieces);
-  for (int L = 0; L < 2; ++L)
-    HE_CUDA(ntt_forward(c->ntt_rh[L], w.pieces + (size_t)L * p->p_in * 2 * n, p->p_in * 2, n, st), "NTT(pieces)");
-  // (M) row ciphertexts
-  const uint64_t leaves = leaves_of(p);
-  {
-    dim3 g = grid_for(leaves * n / 4);
-    g.y = 2;
-    k_rh_mvm<<<g, 256, 0, st>>>(p->wpt, w.pieces, leaves, p->p_in, p->logn, p->M, w.A0);
-  }
-  // (P) PackLWEs, one batched level at a time
+  const uint32_t n = p->n;
   uint32_t* A = w.A0;
   uint32_t* An = w.A1;
-  uint32_t cnt = (uint32_t)leaves;
   const uint32_t* perm_base = p->tables;
   const uint32_t* mono_base = p->tables + (size_t)p->logn * n;
-  for (uint32_t lv = 1; lv <= p->logn; ++lv) {
-    const uint32_t cnt_out = cnt / 2, half = n >> lv;
+  for (uint32_t lv = lv_first; lv <= lv_last; ++lv) {
+    const uint32_t cnt_out = cnt / 2, half = (n >> lv) / stride;
     const uint64_t cn = (uint64_t)cnt_out * n;
     k_pack_comb1<<<dim3(cnt_out, 2, 2), 512, n * sizeof(uint32_t), st>>>(
         A, cnt, half, n, mono_base + (size_t)(lv - 1) * 2 * n, perm_base + (size_t)(lv - 1) * n, p->M, An, w.T, w.C);
@@ -680,14 +744,83 @@ static he_status rhombus_run_impl(const he_rhombus_plan* p, const uint32_t* ct_i
       g.y = 2;
       k_pack_comb2<<<g, 256, 0, st>>>(w.UW, w.LB, w.T, cnt_out, p->logn, p->M, p->pinv[0], p->pinv[1], An);
     }
+    // ping-pong: outputs alternate A1, A0, A1, ... (each level's output fits the other buffer)
     uint32_t* tmp = A;
     A = An;
-    An = (lv == 1) ? w.A0 : tmp;  // level 1 frees A0 for reuse as the next output
+    An = tmp;
     cnt = cnt_out;
   }
-  // (R) + (C)
+  *result = A;
+  return HE_OK;
+}
+
+static he_status rh_check_run(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level, const uint32_t* ksk_dec,
+                              const uint32_t* gal, const void* out, const void* ws_dev, uint64_t ws_bytes) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  if (level < 1) return fail(HE_ENEEDS_BOOTSTRAP, "pcmv needs one level");
+  if (level != 1) return fail(HE_EINVAL, "the Rhombus PCMv runs at level 1 (got %u)", level);
+  if (!ct_in || !ksk_dec || !gal || !out || !ws_dev) return fail(HE_EINVAL, "null argument");
+  const uint64_t need = rh_ws_words(p, nullptr, nullptr) * sizeof(uint32_t);
+  if (ws_bytes < need)
+    return fail(HE_EINVAL, "workspace too small (%llu < %llu)", (unsigned long long)ws_bytes, (unsigned long long)need);
+  return HE_OK;
+}
+
+// (D) decompose + (M) products + the packing levels this plan owns; the packed ciphertexts stay in
+// the workspace (NTT domain, [L][p_out][2][n]) at *packed.
+static he_status rh_front(const he_rhombus_plan* p, const uint32_t* ct_in, const uint32_t* ksk_dec, const uint32_t* gal,
+                          const RhWs& w, uint32_t piece0, uint32_t** packed, cudaStream_t st) {
+  const he_context* c = p->ctx;
+  const uint32_t n = p->n, N = p->N, q0 = p->M.m[0], q1 = p->M.m[1], P = p->M.m[2];
+  // (D) decompose: key switch the a part at degree N, then split
+  k_decomp_modup<<<grid_for(N), 256, 0, st>>>(ct_in, N, q0, q1, P, p->qhinv[0], p->qhinv[1], w.dD);
+  for (int j = 0; j < 3; ++j) HE_CUDA(ntt_forward(c->ntt[j], w.dD + (size_t)j * 2 * N, 2, N, st), "NTT(digits)");
+  k_mac<<<grid_for(N), 256, 0, st>>>(w.dD, ksk_dec, N, N, p->M, w.dUW);
+  for (int j = 0; j < 3; ++j) HE_CUDA(ntt_inverse(c->ntt[j], w.dUW + (size_t)j * 2 * N, 2, N, st), "INTT(U,W)");
+  k_decomp_split<<<grid_for((uint64_t)p->p_in * n), 256, 0, st>>>(w.dUW, ct_in, N, n, p->p_in, piece0, q0, q1, P,
+                                                                   p->pinv[0], p->pinv[1], w.pieces);
   for (int L = 0; L < 2; ++L)
-    HE_CUDA(ntt_inverse(c->ntt_rh[L], A + (size_t)L * cnt * 2 * n, cnt * 2, n, st), "INTT(packed)");
+    HE_CUDA(ntt_forward(c->ntt_rh[L], w.pieces + (size_t)L * p->p_in * 2 * n, p->p_in * 2, n, st), "NTT(pieces)");
+  // (M) leaf ciphertexts: U = n / w inner products each
+  const uint64_t leaves = leaves_of(p);
+  {
+    dim3 g = grid_for(leaves * n / 4);
+    g.y = 2;
+    k_rh_mvm<<<g, 256, 0, st>>>(p->wpt, w.pieces, leaves, p->p_in, p->logn, p->M, w.A0);
+  }
+  // (P) this plan's PackLWEs levels: s+1 .. log2 n - log2 G
+  return rh_pack(p, w, gal, (uint32_t)leaves, p->split + 1, p->logn - p->logG, p->G, packed, st);
+}
+
+static void rh_count(const he_rhombus_plan* p, he_ledger* ledger, int rescale) {
+  if (!ledger) return;
+  ledger->pc_mults += (int64_t)leaves_of(p) * p->p_in;
+  ledger->ct_rotations += (int64_t)(p->win / p->G - 1) * p->p_out;
+  ledger->rescales += rescale;
+}
+
+static he_status rhombus_run_impl(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level,
+                                  const uint32_t* ksk_dec, const uint32_t* gal, uint32_t* out, void* ws_dev,
+                                  uint64_t ws_bytes, void* stream, he_ledger* ledger, uint32_t piece0, int shard,
+                                  uint32_t opiece0) {
+  he_status s = rh_check_run(p, ct_in, level, ksk_dec, gal, out, ws_dev, ws_bytes);
+  if (s) return s;
+  if (p->G != 1)
+    return fail(HE_EINVAL, "a leaf-interleaved shard plan (%u groups) runs through he_rhombus_run_subtree", p->G);
+  if (shard && (piece0 + p->p_in > p->N / p->n || opiece0 + p->p_out > p->N / p->n))
+    return fail(HE_EINVAL, "shard pieces [%u, %u) in / [%u, %u) out exceed the %u pieces of one ciphertext", piece0,
+                piece0 + p->p_in, opiece0, opiece0 + p->p_out, p->N / p->n);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t n = p->n, N = p->N, q0 = p->M.m[0], q1 = p->M.m[1];
+  RhWs w;
+  rh_ws_words(p, &w, (uint32_t*)ws_dev);
+  uint32_t* A = nullptr;
+  s = rh_front(p, ct_in, ksk_dec, gal, w, piece0, &A, st);
+  if (s) return s;
+  // (R) + (C)
+  const uint32_t cnt = p->p_out;
+  for (int L = 0; L < 2; ++L)
+    HE_CUDA(ntt_inverse(p->ctx->ntt_rh[L], A + (size_t)L * cnt * 2 * n, cnt * 2, n, st), "INTT(packed)");
   if (shard) {
     HE_CUDA(cudaMemsetAsync(out, 0, 4ull * N * sizeof(uint32_t), st), "memset");
     k_rh_compose_l1<<<grid_for((uint64_t)cnt * 4 * n), 256, 0, st>>>(A, cnt, opiece0, n, N, out);
@@ -696,11 +829,7 @@ static he_status rhombus_run_impl(const he_rhombus_plan* p, const uint32_t* ct_i
     k_rh_rescale_compose<<<grid_for((uint64_t)cnt * 2 * n), 256, 0, st>>>(A, cnt, n, N, q0, q1, p->q1inv, p->q1invp, out);
   }
   HE_CUDA(cudaGetLastError(), "rhombus launch");
-  if (ledger) {
-    ledger->pc_mults += (int64_t)p->n_out * p->p_in;
-    ledger->ct_rotations += (int64_t)(n - 1) * p->p_out;
-    ledger->rescales += shard ? 0 : 1;
-  }
+  rh_count(p, ledger, shard ? 0 : 1);
   return HE_OK;
 }
 
@@ -715,6 +844,52 @@ extern "C" he_status he_rhombus_run_shard(const he_rhombus_plan* p, const uint32
                                           uint32_t opiece0, uint32_t* out_l1, void* ws_dev, uint64_t ws_bytes,
                                           void* stream, he_ledger* ledger) {
   return rhombus_run_impl(p, ct_in, level, ksk_dec, gal, out_l1, ws_dev, ws_bytes, stream, ledger, piece0, 1, opiece0);
+}
+
+extern "C" he_status he_rhombus_run_subtree(const he_rhombus_plan* p, const uint32_t* ct_in, uint32_t level,
+                                            const uint32_t* ksk_dec, const uint32_t* gal, uint32_t* roots_out,
+                                            void* ws_dev, uint64_t ws_bytes, void* stream, he_ledger* ledger) {
+  he_status s = rh_check_run(p, ct_in, level, ksk_dec, gal, roots_out, ws_dev, ws_bytes);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  RhWs w;
+  rh_ws_words(p, &w, (uint32_t*)ws_dev);
+  uint32_t* A = nullptr;
+  s = rh_front(p, ct_in, ksk_dec, gal, w, 0, &A, st);
+  if (s) return s;
+  HE_CUDA(cudaMemcpyAsync(roots_out, A, 2ull * p->p_out * 2 * p->n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st),
+          "roots");
+  rh_count(p, ledger, 0);
+  return HE_OK;
+}
+
+extern "C" he_status he_rhombus_finish(const he_rhombus_plan* p, const uint32_t* roots, const uint32_t* gal,
+                                       uint32_t* out, void* ws_dev, uint64_t ws_bytes, void* stream,
+                                       he_ledger* ledger) {
+  if (!p) return fail(HE_EINVAL, "null plan");
+  if (!roots || !gal || !out || !ws_dev) return fail(HE_EINVAL, "null argument");
+  const uint64_t need = rh_ws_words(p, nullptr, nullptr) * sizeof(uint32_t);
+  if (ws_bytes < need)
+    return fail(HE_EINVAL, "workspace too small (%llu < %llu)", (unsigned long long)ws_bytes, (unsigned long long)need);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t n = p->n, N = p->N, G = p->G, cnt = p->p_out;
+  RhWs w;
+  rh_ws_words(p, &w, (uint32_t*)ws_dev);
+  k_rh_gather_roots<<<grid_for(4ull * cnt * n * G), 256, 0, st>>>(roots, G, cnt, n, w.A0);
+  uint32_t* A = nullptr;
+  he_status s = rh_pack(p, w, gal, cnt * G, p->logn - p->logG + 1, p->logn, 1, &A, st);
+  if (s) return s;
+  for (int L = 0; L < 2; ++L)
+    HE_CUDA(ntt_inverse(p->ctx->ntt_rh[L], A + (size_t)L * cnt * 2 * n, cnt * 2, n, st), "INTT(packed)");
+  HE_CUDA(cudaMemsetAsync(out, 0, 2ull * N * sizeof(uint32_t), st), "memset");
+  k_rh_rescale_compose<<<grid_for((uint64_t)cnt * 2 * n), 256, 0, st>>>(A, cnt, n, N, p->M.m[0], p->M.m[1], p->q1inv,
+                                                                         p->q1invp, out);
+  HE_CUDA(cudaGetLastError(), "rhombus finish");
+  if (ledger) {
+    ledger->ct_rotations += (int64_t)(G - 1) * cnt;
+    ledger->rescales += 1;
+  }
+  return HE_OK;
 }
 
 extern "C" he_status he_rhombus_combine(const he_context* c, const uint32_t* parts, uint32_t count, uint32_t* out,

@@ -34,6 +34,8 @@ EXPORTS = (
     "he_encrypt_poly", "he_slot_rotation_keygen", "he_slot_pcmm_encode_pts", "he_slot_pcmm_plan_create",
     "he_slot_pcmm_plan_destroy", "he_slot_pcmm_workspace_bytes", "he_slot_pcmm_run", "he_slot_pcmm_run_batch", "he_mod_raise",
     "he_slot_lt_plan_create", "he_slot_bsgs_plan_create", "he_slot_bsgs_plan_create_ext", "he_slot_pcmm_encode_pts_ext", "he_slot_rotation_keygen_plain",
+    "he_encrypt_vector_w", "he_rhombus_weight_bytes_w", "he_rhombus_encode_weights_w", "he_rhombus_plan_create_w",
+    "he_rhombus_plan_info", "he_rhombus_run_subtree", "he_rhombus_finish",
 )
 
 
@@ -119,6 +121,13 @@ def lib():
             "he_slot_pcmm_workspace_bytes": (st, [vp, ctypes.POINTER(u64)]),
             "he_slot_pcmm_run": (st, [vp, vp, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_slot_pcmm_run_batch": (st, [vp, vp, u32, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
+            "he_encrypt_vector_w": (st, [vp, vp, vp, u32, u32, u64, u32, vp, vp]),
+            "he_rhombus_weight_bytes_w": (st, [vp, u32, u32, u32, u32, ctypes.POINTER(u64)]),
+            "he_rhombus_encode_weights_w": (st, [vp, vp, u32, u32, u32, u32, u32, vp, vp]),
+            "he_rhombus_plan_create_w": (st, [vp, vp, u32, u32, u32, u32, u32, ctypes.POINTER(vp)]),
+            "he_rhombus_plan_info": (st, [vp, ctypes.POINTER(u32)]),
+            "he_rhombus_run_subtree": (st, [vp, vp, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
+            "he_rhombus_finish": (st, [vp, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_ring_pack_key_bytes": (st, [vp, i32, ctypes.POINTER(u64)]),
             "he_ring_pack_keygen": (st, [vp, i32, u64, vp, vp, vp]),
             "he_ring_pack_plan_create": (st, [vp, u32, i32, ctypes.POINTER(vp)]),

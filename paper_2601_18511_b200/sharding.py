@@ -254,67 +254,99 @@ def pcmm_mlwe_sharded(ctx, plan, X, n_out: int, group=None, out_b=None, out_a=No
 
 
 # ---------------------------------------------------------------- Rhombus PCMv over several GPUs
-def rhombus_shards(n_out: int, n_in: int, n: int, world: int, strategy: str = "auto") -> list[dict]:
-    """Piece-aligned slices of W for the Rhombus PCMv.
+def rhombus_shards(n_out: int, n_in: int, n: int, world: int, strategy: str = "auto", window: int | None = None,
+                   rho: int | None = None) -> list[dict]:
+    """Per-rank work of the Rhombus PCMv the way PAPER.md:87 splits it.
 
-    A piece is n = rhombus_degree vector elements.  "rows": split the output pieces (each rank packs
-    whole output pieces -- no reduction, words identical to one GPU); "cols": split the input pieces
-    (every rank packs partial sums of all output pieces -- a ciphertext sum mod q, then one rescale);
-    "auto": whichever dimension has more pieces (rows on ties).  Returns per rank
-    {"rows": (r0, r1), "cols": (c0, c1), "opiece0": .., "piece0": ..}; a rank with nothing to do gets
-    an empty slice (r0 == r1 or c0 == c1) and contributes a zero partial."""
+    "cols" -- "the ciphertext is masked and each GPU is assigned 4096/8 values": the input pieces
+    (window w values each) are split over the ranks, each rank runs its columns against all rows and
+    the level-1 partial outputs are summed (one ciphertext sum mod q_i, then one rescale).  At
+    n_in = 4096 the default window is 256, i.e. 16 pieces: 2 pieces = 512 values per rank at 8 GPUs.
+    "rows" -- "broadcast the ciphertext ... split the plaintext matrix": every rank owns the leaves
+    j = g + G jl of every output piece (G = the largest power of two <= world, <= w): rows
+    n o + h(u w + j), n / G of each output piece, with its packing subtree; the G subtree roots are
+    gathered and the top log2 G levels finish the packing -- output words identical to one GPU.
+    "auto": cols when n_in fits one degree-n piece (4096x4096, 11008x4096, 14336x4096), rows
+    otherwise (4096x11008, 4096x14336) -- the paper's choice.
+    Returns per rank {"strategy", "cols": (c0, c1), "piece0", "groups", "group", "active"}."""
     if world < 1:
         raise ValueError("world must be >= 1")
-    p_out, p_in = -(-n_out // n), -(-n_in // n)
+    w = n if window is None else int(window)
+    p_in = -(-n_in // w)
     if strategy == "auto":
-        strategy = "rows" if p_out >= p_in else "cols"
+        strategy = "cols" if n_in <= n and p_in >= world else "rows"
     if strategy not in ("rows", "cols"):
         raise ValueError(f"unknown Rhombus shard strategy {strategy!r}")
-    pieces = p_out if strategy == "rows" else p_in
-    base, extra = divmod(pieces, world)
-    out, p0 = [], 0
+    out = []
+    if strategy == "cols":
+        base, extra = divmod(p_in, world)
+        p0 = 0
+        for r in range(world):
+            p1 = p0 + base + (1 if r < extra else 0)
+            c0, c1 = min(p0 * w, n_in), min(p1 * w, n_in)
+            out.append({"strategy": "cols", "cols": (c0, c1), "piece0": p0, "groups": 1, "group": 0,
+                        "active": c1 > c0})
+            p0 = p1
+        return out
+    G = 1
+    while G * 2 <= min(world, w):
+        G *= 2
     for r in range(world):
-        p1 = p0 + base + (1 if r < extra else 0)
-        if strategy == "rows":
-            out.append({"strategy": "rows", "rows": (min(p0 * n, n_out), min(p1 * n, n_out)), "cols": (0, n_in),
-                        "opiece0": p0, "piece0": 0})
-        else:
-            out.append({"strategy": "cols", "rows": (0, n_out), "cols": (min(p0 * n, n_in), min(p1 * n, n_in)),
-                        "opiece0": 0, "piece0": p0})
-        p0 = p1
+        out.append({"strategy": "rows", "cols": (0, n_in), "piece0": 0, "groups": G, "group": r if r < G else 0,
+                    "active": r < G})
     return out
 
 
 def pcmv_rhombus_sharded(ctx, W, keys, x, group=None, strategy: str = "auto"):
-    """Rhombus PCMv with W sliced over the ranks of `group`: each rank builds the plan of its slice,
-    runs it on the (broadcast) input to a level-1 partial output, the partials are all-gathered
-    (2 x 2 x N words each) and summed mod q_i with one rescale (he_rhombus_combine).  Returns the
-    same level-0 CtVector on every rank."""
+    """Rhombus PCMv split over the ranks of `group` (rhombus_shards).  Column shards: each rank's plan
+    covers its input pieces, the level-1 partial outputs (2 x 2 x N words each) are all-gathered and
+    summed mod q_i with one rescale (he_rhombus_combine).  Row shards: each rank runs its leaves'
+    products and packing subtree, the subtree roots (2 x p_out x 2 x n words each) are all-gathered and
+    every rank finishes the top packing levels (he_rhombus_finish).  Returns the same level-0 CtVector
+    on every rank."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    from .rhombus import combine_rhombus_parts, make_rhombus_plan, pcmv_rhombus_shard
+    from .rhombus import (combine_rhombus_parts, finish_rhombus_subtrees, make_rhombus_plan, pcmv_rhombus_shard,
+                          pcmv_rhombus_subtree)
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     W = np.asarray(W, dtype=np.float64) if not isinstance(W, torch.Tensor) else W
     broadcast_input(x.data, group)
     n_out, n_in = int(W.shape[0]), int(W.shape[1])
-    sl = rhombus_shards(n_out, n_in, ctx.params.rhombus_degree, world, strategy)[rank]
-    (r0, r1), (c0, c1) = sl["rows"], sl["cols"]
-    N = ctx.params.N
-    if r1 > r0 and c1 > c0:
-        plan = make_rhombus_plan(ctx, W[r0:r1, c0:c1])
-        part = pcmv_rhombus_shard(ctx, plan, keys, x, sl["piece0"], sl["opiece0"])
+    P = ctx.params
+    n, N = P.rhombus_degree, P.N
+    win = x.window or n
+    sl = rhombus_shards(n_out, n_in, n, world, strategy, window=win)[rank]
+    if sl["strategy"] == "cols":
+        c0, c1 = sl["cols"]
+        if sl["active"]:
+            plan = make_rhombus_plan(ctx, W[:, c0:c1], window=win)
+            part = pcmv_rhombus_shard(ctx, plan, keys, x, sl["piece0"], 0)
+        else:
+            part = torch.zeros((2, 2, N), dtype=torch.int32, device=ctx.device)
+        if world > 1:
+            parts = torch.empty((world, 2, 2, N), dtype=torch.int32, device=ctx.device)
+            all_gather_into(parts, part[None], group)
+        else:
+            parts = part[None]
+        return combine_rhombus_parts(ctx, parts, n_out)
+    G = sl["groups"]
+    plan = make_rhombus_plan(ctx, W, window=win, groups=G, group=sl["group"])
+    p_out = -(-n_out // n)
+    if sl["active"]:
+        roots = pcmv_rhombus_subtree(ctx, plan, keys, x)
     else:
-        part = torch.zeros((2, 2, N), dtype=torch.int32, device=ctx.device)
+        roots = torch.zeros((2, p_out, 2, n), dtype=torch.int32, device=ctx.device)
     if world > 1:
-        parts = torch.empty((world, 2, 2, N), dtype=torch.int32, device=ctx.device)
-        all_gather_into(parts, part[None], group)
+        allr = torch.empty((world, 2, p_out, 2, n), dtype=torch.int32, device=ctx.device)
+        all_gather_into(allr, roots[None], group)
+        allr = allr[:G]
     else:
-        parts = part[None]
-    return combine_rhombus_parts(ctx, parts, n_out)
+        allr = roots[None]
+    return finish_rhombus_subtrees(ctx, plan, keys, allr)
 
 
 def all_reduce_max(t, group=None):

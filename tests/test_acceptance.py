@@ -96,7 +96,7 @@ def test_a06_rhombus_toy_bit_exact():
     from test_gpu_rhombus import test_toy_pcmv_bit_exact
 
     t0 = time.perf_counter()
-    test_toy_pcmv_bit_exact(200, 300)
+    test_toy_pcmv_bit_exact(200, 300, None)
     check_budget(t0, 60)
 
 

@@ -86,24 +86,34 @@ def test_row_sharded_pcmm_gathers_exact_output(world, n_out):
     assert res == {r: "ok" for r in range(world)}
 
 
-def test_rhombus_shards_cover_the_matrix_once():
+def test_rhombus_shards_follow_the_paper():
+    """PAPER.md:87: n_in = 4096 -> column split, 4096/8 = 512 input values per rank at 8 GPUs;
+    n_in > 4096 -> row split (leaf groups), every rank busy."""
     from paper_2601_18511_b200.sharding import rhombus_shards
 
-    n = 4096
-    for n_out, n_in in ((4096, 11008), (14336, 4096), (8192, 4096), (4096, 4096)):
-        for world in (1, 2, 3, 4, 8):
-            sl = rhombus_shards(n_out, n_in, n, world)
-            assert len(sl) == world
+    n, rho = 4096, 16
+    for n_out, n_in in ((4096, 11008), (14336, 4096), (11008, 4096), (4096, 4096), (4096, 14336)):
+        w = 1
+        while w * rho < n_in:
+            w *= 2
+        for world in (1, 2, 4, 8):
+            sl = rhombus_shards(n_out, n_in, n, world, window=w)
+            assert len(sl) == world and all(s["active"] for s in sl)
             strat = sl[0]["strategy"]
-            assert strat == ("rows" if -(-n_out // n) >= -(-n_in // n) else "cols")
-            spans = [s["rows"] if strat == "rows" else s["cols"] for s in sl]
-            total = n_out if strat == "rows" else n_in
-            assert spans[0][0] == 0 and spans[-1][1] == total
-            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
-                assert a1 == b0 and a0 <= a1
-            for s in sl:   # piece-aligned offsets (idle ranks: empty slice at the end)
-                lo, hi = s["rows"] if strat == "rows" else s["cols"]
-                if hi > lo:
-                    assert lo % n == 0 and (s["opiece0"] if strat == "rows" else s["piece0"]) == lo // n
+            assert strat == ("cols" if n_in <= n else "rows")
+            if strat == "cols":
+                spans = [s["cols"] for s in sl]
+                assert spans[0][0] == 0 and spans[-1][1] == n_in
+                for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                    assert a1 == b0 and a0 < a1
+                for s in sl:
+                    assert s["cols"][0] == s["piece0"] * w
+                if world == 8 and n_in == 4096:
+                    assert all(s["cols"][1] - s["cols"][0] == 512 for s in sl)
+            else:
+                assert sorted(s["group"] for s in sl) == list(range(world))
+                assert all(s["groups"] == world for s in sl)
+    sl = rhombus_shards(4096, 11008, n, 3, window=1024)    # 3 ranks: 2 leaf groups, one idle rank
+    assert [s["active"] for s in sl] == [True, True, False] and sl[0]["groups"] == 2
     with pytest.raises(ValueError):
         rhombus_shards(4096, 4096, n, 2, strategy="diagonal")
