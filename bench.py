@@ -174,7 +174,7 @@ def run_ours(a, rank: int, world: int, local: int):
     b0, b1 = row_shards(n_out, k, world)[rank]         # balanced output row-blocks of this rank
     per = shard_slots(n_out, k, world)                 # padded slots per rank for the all-gather
     rows = (b1 - b0) * k
-    ctx = HeContext(P, device=dev)
+    ctx = HeContext(P, device=dev, rng="seeded")
 
     # synthetic data, identical on every rank (seeded device generator)
     g = torch.Generator(device=dev).manual_seed(20260117)
@@ -295,7 +295,8 @@ def run_ours(a, rank: int, world: int, local: int):
 
     cpu = None
     if rank == 0 and world == 1 and a.cpu_rows > 0:
-        cpu = cpu_baseline(P, A, plan, X, n_out, n_in, a.cpu_rows, W_seed_dev=dev, g_seed=20260117)
+        cpu = cpu_baseline(P, A, plan, X, n_out, n_in, a.cpu_rows, W_seed_dev=dev, g_seed=20260117, Y=Y, ctx=ctx,
+                           sk=sk)
 
     if rank == 0:
         d0, d1 = P.ct_digits(0), P.ct_digits(1)
@@ -324,6 +325,10 @@ def run_ours(a, rank: int, world: int, local: int):
             "clocks": clk.summary(),
             "kernels_ms": {n: round(v, 3) for n, v in stage_ms.items()},
         }
+        if cpu and cpu.get("parity"):
+            line["parity"] = cpu["parity"]
+        if cpu and cpu.get("gpu_precision"):
+            line["precision_bits"] = cpu["gpu_precision"]["precision_bits"]
         line.update(extras)
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -447,7 +452,7 @@ def side_measurements(P, dev):
 
     out = {}
     try:
-        ctx = HeContext(P, device=dev)
+        ctx = HeContext(P, device=dev, rng="seeded")
         sk = ctx.keygen(17)
         keys = rhombus_keygen(ctx, sk, 23)
         rh = {}
@@ -542,7 +547,7 @@ def slot_pcmm_side(P, dev, reps=5):
     from paper_2601_18511_b200 import (HeContext, clear_slot_pcmm, decrypt_packed, encrypt_packed,
                                        make_slot_pcmm_plan, pcmm_slot_bsgs, slot_pcmm_keygen)
 
-    ctx = HeContext(P, device=dev)
+    ctx = HeContext(P, device=dev, rng="seeded")
     sk = ctx.keygen(51)
     res = {}
     for d in (128, 64):
@@ -579,7 +584,7 @@ def stc_side(P, dev, reps=3):
     from paper_2601_18511_b200.stc import (encrypt_slots, make_slot_to_coeffs_plan, slot_to_coeffs,
                                            slot_to_coeffs_keygen)
 
-    ctx = HeContext(P, device=dev)
+    ctx = HeContext(P, device=dev, rng="seeded")
     sk = ctx.keygen(61)
     plan = make_slot_to_coeffs_plan(ctx)
     keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=63)
@@ -615,7 +620,7 @@ def ring_pack_side(P, dev, shape="4096x11008", reps=3):
                                        pcmm_packed, ring_pack, ring_pack_keygen)
 
     n_out, n_in = shape_of(shape)
-    ctx = HeContext(P, device=dev)
+    ctx = HeContext(P, device=dev, rng="seeded")
     g = torch.Generator(device=dev).manual_seed(31)
     W = (torch.rand((n_out, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1) / math.sqrt(n_in)
     A = torch.rand((P.tokens, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1
@@ -709,9 +714,11 @@ def load_traffic(shape: str, kernel: str):
 
 
 # ----------------------------------------------------------------- CPU baseline / reference arm
-def cpu_baseline(P, A, plan, X, n_out, n_in, n_rows, W_seed_dev=None, g_seed=None):
+def cpu_baseline(P, A, plan, X, n_out, n_in, n_rows, W_seed_dev=None, g_seed=None, Y=None, ctx=None, sk=None):
     """Time the oracle (C restatement, OpenMP over all host threads) on n_rows output rows x
-    all 65 792 columns x full K, both limbs + rescale; extrapolate to the full op."""
+    all 65 792 columns x full K, both limbs + rescale; extrapolate to the full op.  The sample's words
+    are then compared with the GPU output block of the same rows (every word), and the GPU rows are
+    decrypted against the float product (precision in bits)."""
     import torch
 
     import oracle as O
@@ -726,6 +733,25 @@ def cpu_baseline(P, A, plan, X, n_out, n_in, n_rows, W_seed_dev=None, g_seed=Non
     n_rows = min(n_rows, P.mlwe_rank)
     res = O.time_pcmm_sample(P, Wt, ct, n_rows)
     per_op = res["seconds"] * n_out / n_rows * 1e3
+    parity = precision = None
+    if Y is not None:
+        ref = res.pop("words")
+        k, d = P.mlwe_rank, P.mlwe_degree
+        ga = Y.out_a[:n_rows].cpu().numpy().view(np.uint32)
+        gb = Y.out_b[: -(-n_rows // k)].cpu().numpy().view(np.uint32)
+        eq_a = int((ga == ref[:, d:]).sum())
+        eq_b = sum(int((gb[y // k, y % k + k * np.arange(d)] == ref[y, :d]).sum()) for y in range(n_rows))
+        total = n_rows * P.width
+        parity = {"words_checked": total, "words_equal": eq_a + eq_b == total, "words_differing": total - eq_a - eq_b,
+                  "rows": [0, n_rows], "against": "oracle/he_oracle.c or_pcmm (direct BCHPS24 Alg. 2, exact)"}
+        if ctx is not None and sk is not None:
+            dec = ctx.decrypt_pcmm(sk, Y, rows=(0, n_rows))[:, :n_rows]
+            clear = A.cpu().numpy() @ W0[:n_rows].T
+            err = float(np.abs(dec - clear).max())
+            precision = {"precision_bits": round(-math.log2(err), 2), "max_abs_err": err,
+                         "max_abs_out": float(np.abs(clear).max()), "rows": [0, n_rows]}
+    else:
+        res.pop("words", None)
     # context: the unencrypted product on the same host, numpy float64 (BLAS threads)
     rng = np.random.default_rng(0)
     Wf, Af = rng.standard_normal((n_out, n_in)), rng.standard_normal((P.tokens, n_in))
@@ -737,6 +763,9 @@ def cpu_baseline(P, A, plan, X, n_out, n_in, n_rows, W_seed_dev=None, g_seed=Non
     return {"value": round(per_op, 1), "unit": "ms/op", "cores": res["threads"], "kind": "port",
             "sample": f"oracle/ C restatement: {n_rows} of {n_out} output rows x {P.width} cols x K={n_in}, "
                       f"both limbs + rescale, {res['seconds']:.2f} s, extrapolated x{n_out / n_rows:.0f}",
+            "extrapolated": True, "sample_rows": n_rows, "extrapolation_factor": round(n_out / n_rows, 3),
+            "sample_seconds": round(res["seconds"], 3), "algorithm": "direct (BCHPS24 Alg. 2 as a GEMM)",
+            "parity": parity, "gpu_precision": precision,
             "plaintext_floor_ms": round(floor_ms, 2),
             "plaintext_floor": f"numpy float64 acts @ W.T ({P.tokens} x {n_in} x {n_out}) on the host, unencrypted",
             "hesim_context": hesim_context()}
@@ -789,7 +818,10 @@ def run_reference(a, rank: int, world: int):
                    "mlwe": [P.mlwe_degree, P.mlwe_rank], "moduli": list(P.moduli)},
         "cpu_baseline": {"value": round(v, 1), "unit": "ms/op", "cores": O.num_threads(), "kind": "port",
                          "sample": f"per step {rows} of {n_out} output rows x {P.width} cols x K={n_in}, both "
-                                   f"limbs + rescale, extrapolated x{n_out / rows:.0f} (oracle/he_oracle.c, OpenMP)"},
+                                   f"limbs + rescale, extrapolated x{n_out / rows:.0f} (oracle/he_oracle.c, OpenMP)",
+                         "extrapolated": True, "sample_rows": rows, "extrapolation_factor": round(n_out / rows, 3),
+                         "algorithm": "direct (BCHPS24 Alg. 2 as a GEMM)"},
+        "extrapolated": True,
         "e2e": {"value": round(v, 1), "unit": "ms/op", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "hesim (the reference package) does not implement the MLWE PCMM (SPEC.md:8); the reference "
                 "arm times the CPU restatement of the path",

@@ -71,6 +71,13 @@ int he_version(void);
 /* replaces hesim.SlotContext(SimParams) construction (slotsim.py:171-176) */
 he_status he_context_create(const he_params* params, he_context** out);
 he_status he_context_destroy(he_context* ctx);
+/* Sampling key.  key = 32 secret bytes: secrets, masks a, errors and key-switching keys are drawn from
+ * ChaCha20 (RFC 8439) under that key, the per-call `seed` arguments acting as nonces (never reuse one
+ * for two encryptions).  key = NULL (the default of he_context_create): the seeded splitmix64 test
+ * path -- deterministic, reproduced word for word by the CPU oracle, and NOT secure (a 64-bit seed). */
+he_status he_context_set_rng_key(he_context* ctx, const uint8_t* key);
+/* one ChaCha20 block (host; the device sampler's block function, for known-answer tests) */
+he_status he_chacha20_block(const uint8_t* key, uint32_t counter, const uint8_t* nonce, uint8_t* out);
 
 /* ---------------------------------------------------------------- keys, encryption (test/bench plumbing) */
 /* ternary secret s (int32 [N]) and its NTT per limb (u32 [2][N]) */

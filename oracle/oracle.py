@@ -335,9 +335,9 @@ def time_pcmm_sample(params, Wt, ct, n_rows: int) -> dict:
     both limbs + rescale (the sample the cpu_baseline is extrapolated from)."""
     rows = list(range(n_rows))
     t0 = time.perf_counter()
-    pcmm(params, Wt, ct, rows=rows)
+    out = pcmm(params, Wt, ct, rows=rows)
     dt = time.perf_counter() - t0
-    return {"seconds": dt, "rows": n_rows, "threads": num_threads()}
+    return {"seconds": dt, "rows": n_rows, "threads": num_threads(), "words": out}
 
 
 # ---------------------------------------------------------------- Rhombus PCMv (he_oracle_rhombus.c)

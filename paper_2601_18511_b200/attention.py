@@ -34,9 +34,10 @@ def clear_pc_attention(q, k_pub, v_pub, positions):
     return np.asarray(v_pub, float) @ _softmax_columns(s)
 
 
-def pc_attention_hybrid(ctx, sk, q, k_pub, v_pub, positions=None, seed: int = 0) -> tuple[np.ndarray, dict]:
+def pc_attention_hybrid(ctx, sk, q, k_pub, v_pub, positions=None, seed: int | None = None) -> tuple[np.ndarray, dict]:
     """Private q (d x d, tokens as columns) against the public K/V cache blocks: two GPU slot-domain
-    PCMMs on ciphertexts, RoPE and the column softmax on the key holder's side.  Returns (out, report)."""
+    PCMMs on ciphertexts, RoPE and the column softmax on the key holder's side.  Returns (out, report).
+    seed None: fresh nonces for every key and encryption (secure contexts); a seed: seed + 1 .. seed + 4."""
     q = np.asarray(q, float)
     d = q.shape[0]
     k_pub, v_pub = np.asarray(k_pub, float), np.asarray(v_pub, float)
@@ -44,11 +45,12 @@ def pc_attention_hybrid(ctx, sk, q, k_pub, v_pub, positions=None, seed: int = 0)
         raise ValueError("q and the public cache blocks must be d x d")
     if positions is None:
         positions = k_pub.shape[1] + np.arange(d)
+    nonce = (lambda i: None) if seed is None else (lambda i: seed + i)
     before = ctx.ledger.snapshot()
     # scores: shear chain 2 -> 1 (client encrypts the rotary-encoded queries twice-sheared)
     s_plan = make_slot_pcmm_plan(ctx, k_pub.T / np.sqrt(d), shear_power=1)
-    s_keys = slot_pcmm_keygen(ctx, sk, s_plan, seed + 1)
-    q_ct = encrypt_packed(ctx, sk, rope_columns(q, positions), 2, seed=seed + 2)
+    s_keys = slot_pcmm_keygen(ctx, sk, s_plan, nonce(1))
+    q_ct = encrypt_packed(ctx, sk, rope_columns(q, positions), 2, seed=nonce(2))
     s_ct = pcmm_slot_bsgs(ctx, s_plan, s_keys, q_ct)
     # key holder: decrypt, undo the remaining shear, softmax over columns, re-encrypt once-sheared
     scores = decrypt_packed(ctx, sk, s_ct)
@@ -56,9 +58,9 @@ def pc_attention_hybrid(ctx, sk, q, k_pub, v_pub, positions=None, seed: int = 0)
     unsheared = np.empty_like(scores)
     unsheared[(i + j) % d, j] = scores        # s_ct holds col_shear(S, 1)[i, j] = S[(i + j) % d, j]
     probs = _softmax_columns(unsheared)
-    p_ct = encrypt_packed(ctx, sk, probs, 1, seed=seed + 3)
+    p_ct = encrypt_packed(ctx, sk, probs, 1, seed=nonce(3))
     # values: shear chain 1 -> 0
     v_plan = make_slot_pcmm_plan(ctx, v_pub, shear_power=0)
-    v_keys = slot_pcmm_keygen(ctx, sk, v_plan, seed + 4)
+    v_keys = slot_pcmm_keygen(ctx, sk, v_plan, nonce(4))
     out = decrypt_packed(ctx, sk, pcmm_slot_bsgs(ctx, v_plan, v_keys, p_ct))
     return out, {"ledger": ctx.ledger.diff(before), "scores": unsheared}

@@ -14,6 +14,8 @@ from __future__ import annotations
 
 import ctypes
 import json
+import os
+import secrets
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -86,7 +88,7 @@ def current_stream_handle(device=None) -> int:
 class _DeviceCtx:
     """Owns the he_context* of one CUDA device."""
 
-    def __init__(self, params: HeParams, device_index: int):
+    def __init__(self, params: HeParams, device_index: int, rng_key: bytes | None = None):
         torch = _torch()
         self.device_index = device_index
         p = native.HeParamsC()
@@ -100,6 +102,8 @@ class _DeviceCtx:
         with torch.cuda.device(device_index):
             native.call("he_context_create", ctypes.byref(p), ctypes.byref(h))
         self.handle = h
+        if rng_key is not None:
+            native.call("he_context_set_rng_key", h, rng_key)
 
     def __del__(self):
         try:
@@ -156,13 +160,30 @@ class MlweBlocks:
 
 
 class HeContext:
-    """Parameters + ledger + device context (hesim.SlotContext's role)."""
+    """Parameters + ledger + device context (hesim.SlotContext's role).
 
-    def __init__(self, params: HeParams | None = None, device=None):
+    rng="secure" (default): secrets, masks, errors and key-switching keys are sampled from ChaCha20
+    under a fresh 256-bit os.urandom key held by the device context; `seed` arguments are nonces and
+    default to fresh random ones (never pass the same seed to two encryptions).  rng="seeded": the
+    deterministic splitmix64 path the CPU oracle reproduces word for word -- tests and benchmarks
+    only, NOT secure (everything derives from 64-bit seeds)."""
+
+    def __init__(self, params: HeParams | None = None, device=None, rng: str = "secure"):
+        if rng not in ("secure", "seeded"):
+            raise ValueError(f"rng must be 'secure' or 'seeded', got {rng!r}")
         self.params = params or HeParams.llama()
         self.ledger = CostLedger(min_level_reached=self.params.top_level)
         self._device = device
         self._dev: _DeviceCtx | None = None
+        self.rng = rng
+
+    def nonce(self, seed=None) -> int:
+        """The seed a sampling call uses: the caller's, or (secure contexts) a fresh random nonce."""
+        if seed is not None:
+            return int(seed)
+        if self.rng == "seeded":
+            raise ValueError("a seeded (test) context needs explicit seeds")
+        return secrets.randbits(63)
 
     # -- device --------------------------------------------------------------
     @property
@@ -178,7 +199,8 @@ class HeContext:
     def handle(self):
         if self._dev is None:
             dev = self.device
-            self._dev = _DeviceCtx(self.params, dev.index if dev.index is not None else 0)
+            self._dev = _DeviceCtx(self.params, dev.index if dev.index is not None else 0,
+                                   os.urandom(32) if self.rng == "secure" else None)
         return self._dev.handle
 
     def stream(self) -> int:
@@ -191,24 +213,27 @@ class HeContext:
         child.ledger = CostLedger(min_level_reached=self.params.top_level)
         child._device = self._device
         child._dev = self._dev
+        child.rng = self.rng
         return child
 
     def merge(self, child: "HeContext") -> None:
         self.ledger.merge(child.ledger)
 
     # -- keys / encryption (test and bench plumbing, all on the device) -------
-    def keygen(self, seed: int) -> SecretKey:
+    def keygen(self, seed: int | None = None) -> SecretKey:
         torch = _torch()
+        seed = self.nonce(seed)
         N = self.params.N
         s = torch.empty(N, dtype=torch.int32, device=self.device)
         s_ntt = torch.empty((2, N), dtype=torch.int32, device=self.device)
         native.call("he_keygen", self.handle, seed, s.data_ptr(), s_ntt.data_ptr(), self.stream())
         return SecretKey(s, s_ntt, seed)
 
-    def encrypt_acts(self, sk: SecretKey, acts, seed: int, r0: int = 0, out=None) -> CtBlocks:
+    def encrypt_acts(self, sk: SecretKey, acts, seed: int | None = None, r0: int = 0, out=None) -> CtBlocks:
         """Coefficient-encode and encrypt a (d/2) x n_in activation matrix at level 1
         (hesim.pack_sheared / encrypt_matrix role, packing.py:81-91)."""
         torch = _torch()
+        seed = self.nonce(seed)
         acts_t = torch.as_tensor(acts, dtype=torch.float64, device=self.device).contiguous()
         tokens, n_in = acts_t.shape
         if tokens != self.params.tokens:

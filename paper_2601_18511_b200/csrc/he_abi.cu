@@ -170,6 +170,33 @@ extern "C" he_status he_context_create(const he_params* p, he_context** out) {
   return HE_OK;
 }
 
+extern "C" he_status he_context_set_rng_key(he_context* c, const uint8_t* key) {
+  if (!c) return fail(HE_EINVAL, "null argument");
+  if (!key) {
+    c->R.rng = he::RngCtx{};
+    return HE_OK;
+  }
+  for (int i = 0; i < 8; ++i)
+    c->R.rng.key[i] = (uint32_t)key[4 * i] | ((uint32_t)key[4 * i + 1] << 8) | ((uint32_t)key[4 * i + 2] << 16) |
+                      ((uint32_t)key[4 * i + 3] << 24);
+  c->R.rng.secure = 1;
+  return HE_OK;
+}
+
+extern "C" he_status he_chacha20_block(const uint8_t* key, uint32_t counter, const uint8_t* nonce, uint8_t* out) {
+  if (!key || !nonce || !out) return fail(HE_EINVAL, "null argument");
+  uint32_t k[8], n[3], b[16];
+  auto le = [](const uint8_t* p) {
+    return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+  };
+  for (int i = 0; i < 8; ++i) k[i] = le(key + 4 * i);
+  for (int i = 0; i < 3; ++i) n[i] = le(nonce + 4 * i);
+  he::chacha20_block(k, counter, n[0], n[1], n[2], b);
+  for (int i = 0; i < 16; ++i)
+    for (int j = 0; j < 4; ++j) out[4 * i + j] = (uint8_t)(b[i] >> (8 * j));
+  return HE_OK;
+}
+
 extern "C" he_status he_context_destroy(he_context* c) {
   if (!c) return HE_OK;
   for (int i = 0; i < 3; ++i) {

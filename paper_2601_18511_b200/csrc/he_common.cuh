@@ -22,6 +22,75 @@ HE_HD uint64_t rng_key(uint64_t seed, uint64_t stream) {
 }
 HE_HD uint64_t rng_draw(uint64_t key, uint64_t idx) { return mix64(key + (idx + 1) * 0x9E3779B97F4A7C15ULL); }
 
+// ---------------------------------------------------------------- secure sampling (ChaCha20, RFC 8439)
+// A context created with a 256-bit secret key (he_context_set_rng_key) samples secrets, masks a,
+// errors and key-switching keys from ChaCha20 instead: a per-seed subkey
+//   K_seed = ChaCha20_block(K, counter 0xFFFFFFFF, nonce (seed_lo, seed_hi, 0x5EED5EED))[0..8)
+// and draw idx of stream = the first 64 bits of ChaCha20_block(K_seed, (uint32)idx,
+// nonce (stream_lo, stream_hi, idx >> 32)).  Without a key (the seeded test path) the splitmix draws above
+// are used, which the oracle restates bit for bit.
+struct RngCtx {
+  uint32_t key[8];
+  uint32_t secure;
+};
+HE_HD uint32_t rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+HE_HD void chacha_qr(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+  a += b; d ^= a; d = rotl32(d, 16);
+  c += d; b ^= c; b = rotl32(b, 12);
+  a += b; d ^= a; d = rotl32(d, 8);
+  c += d; b ^= c; b = rotl32(b, 7);
+}
+HE_HD void chacha20_block(const uint32_t key[8], uint32_t counter, uint32_t n0, uint32_t n1, uint32_t n2,
+                          uint32_t out[16]) {
+  uint32_t x[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u, key[0], key[1], key[2], key[3],
+                    key[4],      key[5],      key[6],      key[7],      counter, n0, n1, n2};
+  uint32_t w[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w[i] = x[i];
+#pragma unroll 1
+  for (int r = 0; r < 10; ++r) {
+    chacha_qr(w[0], w[4], w[8], w[12]);
+    chacha_qr(w[1], w[5], w[9], w[13]);
+    chacha_qr(w[2], w[6], w[10], w[14]);
+    chacha_qr(w[3], w[7], w[11], w[15]);
+    chacha_qr(w[0], w[5], w[10], w[15]);
+    chacha_qr(w[1], w[6], w[11], w[12]);
+    chacha_qr(w[2], w[7], w[8], w[13]);
+    chacha_qr(w[3], w[4], w[9], w[14]);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) out[i] = w[i] + x[i];
+}
+struct Rng {
+  uint64_t det;
+  uint32_t k[8];
+  uint32_t s0, s1;
+  uint32_t secure;
+};
+HE_HD Rng rng_make(const RngCtx& rc, uint64_t seed, uint64_t stream) {
+  Rng r;
+  r.secure = rc.secure;
+  r.det = rng_key(seed, stream);
+  r.s0 = (uint32_t)stream;
+  r.s1 = (uint32_t)(stream >> 32);
+  if (rc.secure) {
+    uint32_t b[16];
+    chacha20_block(rc.key, 0xFFFFFFFFu, (uint32_t)seed, (uint32_t)(seed >> 32), 0x5EED5EEDu, b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.k[i] = b[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.k[i] = 0;
+  }
+  return r;
+}
+HE_HD uint64_t rng_next(const Rng& r, uint64_t idx) {
+  if (!r.secure) return rng_draw(r.det, idx);
+  uint32_t b[16];
+  chacha20_block(r.k, (uint32_t)idx, r.s0, r.s1, (uint32_t)(idx >> 32), b);
+  return (uint64_t)b[0] | ((uint64_t)b[1] << 32);
+}
+
 constexpr uint64_t kStreamSecret = 0x5EC0000000000000ULL;
 HE_HD uint64_t stream_a(uint32_t r, uint32_t limb) { return 0xA000000000000000ULL | ((uint64_t)r << 8) | limb; }
 HE_HD uint64_t stream_e(uint32_t r) { return 0xE000000000000000ULL | ((uint64_t)r << 8); }

@@ -217,13 +217,13 @@ cudaError_t launch_encode_weights(const RingDims& R, const double* W, uint32_t n
 }
 
 // ================================================================ keys / encryption / decryption
-__global__ void keygen_kernel(uint64_t seed, uint32_t N, int32_t* s) {
-  const uint64_t key = rng_key(seed, kStreamSecret);
+__global__ void keygen_kernel(RngCtx rc, uint64_t seed, uint32_t N, int32_t* s) {
+  const Rng key = rng_make(rc, seed, kStreamSecret);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
-    s[i] = ternary(rng_draw(key, i));
+    s[i] = ternary(rng_next(key, i));
 }
 cudaError_t launch_keygen(const RingDims& R, uint64_t seed, int32_t* s_dev, cudaStream_t st) {
-  keygen_kernel<<<(R.N + 255) / 256, 256, 0, st>>>(seed, R.N, s_dev);
+  keygen_kernel<<<(R.N + 255) / 256, 256, 0, st>>>(R.rng, seed, R.N, s_dev);
   return cudaGetLastError();
 }
 
@@ -240,20 +240,21 @@ cudaError_t launch_reduce_secret(const RingDims& R, const int32_t* s_dev, uint32
 }
 
 // a-part of every (ct, limb) and a copy in the b slot (NTT'd in place to form a*s)
-__global__ void gen_a_kernel(uint64_t seed, uint32_t r0, uint32_t N, uint32_t q0, uint32_t q1, uint32_t* ct) {
+__global__ void gen_a_kernel(RngCtx rc, uint64_t seed, uint32_t r0, uint32_t N, uint32_t q0, uint32_t q1,
+                             uint32_t* ct) {
   const uint32_t r = blockIdx.y, L = blockIdx.z;
   const uint32_t q = L ? q1 : q0;
-  const uint64_t key = rng_key(seed, stream_a(r0 + r, L));
+  const Rng key = rng_make(rc, seed, stream_a(r0 + r, L));
   uint32_t* a = ct + ((size_t)r * 2 + L) * 2 * N;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-    uint32_t v = (uint32_t)(rng_draw(key, i) % q);
+    uint32_t v = (uint32_t)(rng_next(key, i) % q);
     a[i] = v;
     a[N + i] = v;
   }
 }
 cudaError_t launch_gen_a(const RingDims& R, uint64_t seed, uint32_t r0, uint32_t n_ct, uint32_t* ct, cudaStream_t st) {
   dim3 g((R.N + 1023) / 1024, n_ct, 2);
-  gen_a_kernel<<<g, 256, 0, st>>>(seed, r0, R.N, R.q[0], R.q[1], ct);
+  gen_a_kernel<<<g, 256, 0, st>>>(R.rng, seed, r0, R.N, R.q[0], R.q[1], ct);
   return cudaGetLastError();
 }
 
@@ -276,9 +277,9 @@ cudaError_t launch_pointwise_mul(const uint32_t* x, uint64_t x_stride, const uin
 // rho = N / n_rh (w = n_rh: the plain h layout of PAPER.md:674-680)
 __global__ void finish_encrypt_kernel(const double* __restrict__ acts, uint32_t n_in, uint32_t d, uint32_t k,
                                       int logk, uint32_t N, double delta, uint64_t seed, uint32_t r0, uint32_t q0,
-                                      uint32_t q1, uint32_t* ct, int layout, uint32_t n_rh, uint32_t win) {
+                                      uint32_t q1, uint32_t* ct, int layout, uint32_t n_rh, uint32_t win, RngCtx rc) {
   const uint32_t r = blockIdx.y;
-  const uint64_t ekey = rng_key(seed, stream_e(r0 + r));
+  const Rng ekey = rng_make(rc, seed, stream_e(r0 + r));
   const uint32_t half = d / 2;
   const int lh = ilog2_h(half);
   const int lw = ilog2_h(win);
@@ -300,7 +301,7 @@ __global__ void finish_encrypt_kernel(const double* __restrict__ acts, uint32_t 
         if (e < n_in) pt = __double2ll_rn(__dmul_rn(delta, acts[e]));
       }
     }
-    const long long e = cbd21_d(rng_draw(ekey, c));
+    const long long e = cbd21_d(rng_next(ekey, c));
 #pragma unroll
     for (int L = 0; L < 2; ++L) {
       const uint32_t q = L ? q1 : q0;
@@ -315,7 +316,7 @@ cudaError_t launch_finish_encrypt(const RingDims& R, const double* acts, uint32_
                                   uint32_t n_ct, uint32_t* ct, cudaStream_t st, int layout, uint32_t win) {
   dim3 g((R.N + 1023) / 1024, n_ct);
   finish_encrypt_kernel<<<g, 256, 0, st>>>(acts, n_in, R.d, R.k, (int)R.logk, R.N, (double)(1ull << R.log_delta),
-                                           seed, r0, R.q[0], R.q[1], ct, layout, R.n_rh, win ? win : R.n_rh);
+                                           seed, r0, R.q[0], R.q[1], ct, layout, R.n_rh, win ? win : R.n_rh, R.rng);
   return cudaGetLastError();
 }
 

@@ -66,6 +66,7 @@ cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint6
 struct RingDims {
   uint32_t d, k, N, logk, q[2], log_delta;
   uint32_t n_rh, P;  // Rhombus degree and special prime
+  RngCtx rng{};      // sampling key (secure == 0: the seeded splitmix test path)
 };
 
 cudaError_t launch_decompose(const RingDims& R, const uint32_t* ct, uint32_t n_in, int d0, int d1, int8_t* planes,

@@ -44,6 +44,7 @@ HE_D uint32_t barrett64(uint64_t x, uint64_t mu, uint32_t q) {  // x mod q for a
 struct Mods {
   uint32_t m[3];
   uint64_t mu[3];
+  RngCtx rng;  // key material for the key generators (k_ksk_prep)
 };
 HE_D uint32_t mulmod_b(uint32_t a, uint32_t b, uint64_t mu, uint32_t q) { return barrett64((uint64_t)a * b, mu, q); }
 // centred c (|c| < q 2^32) -> c mod q
@@ -56,16 +57,17 @@ Mods make_mods(const RingDims& R) {
   M.m[1] = R.q[1];
   M.m[2] = R.P;
   for (int j = 0; j < 3; ++j) M.mu[j] = (uint64_t)(((unsigned __int128)1 << 64) / M.m[j]);
+  M.rng = R.rng;
   return M;
 }
 
 // ------------------------------------------------------------------ key generation
-__global__ void k_small_secret(uint64_t seed, uint32_t n, uint32_t N, int32_t* s_small, int32_t* s_up) {
-  const uint64_t key = rng_key(seed, kStreamSecretRh);
+__global__ void k_small_secret(RngCtx rc, uint64_t seed, uint32_t n, uint32_t N, int32_t* s_small, int32_t* s_up) {
+  const Rng key = rng_make(rc, seed, kStreamSecretRh);
   const uint32_t rho = N / n;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-    if (i < n) s_small[i] = ternary(rng_draw(key, i));
-    s_up[i] = (i % rho == 0) ? ternary(rng_draw(key, i / rho)) : 0;
+    if (i < n) s_small[i] = ternary(rng_next(key, i));
+    s_up[i] = (i % rho == 0) ? ternary(rng_next(key, i / rho)) : 0;
   }
 }
 // sigma_k(s) on a signed secret
@@ -83,12 +85,12 @@ __global__ void k_reduce_signed(const int32_t* s, uint32_t n, uint32_t q, uint32
   }
 }
 // alpha (uniform) and t = g * s_old + e  (coefficient form, modulus q)
-__global__ void k_ksk_prep(uint64_t seed, uint32_t id, uint32_t i, uint32_t j, uint32_t q, uint32_t g,
+__global__ void k_ksk_prep(RngCtx rc, uint64_t seed, uint32_t id, uint32_t i, uint32_t j, uint32_t q, uint32_t g,
                            const int32_t* s_old, uint32_t n, uint32_t* alpha, uint32_t* t) {
-  const uint64_t ka = rng_key(seed, stream_ksk_a(id, i, j)), ke = rng_key(seed, stream_ksk_e(id, i));
+  const Rng ka = rng_make(rc, seed, stream_ksk_a(id, i, j)), ke = rng_make(rc, seed, stream_ksk_e(id, i));
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    alpha[c] = (uint32_t)(rng_draw(ka, c) % q);
-    const int64_t e = cbd21_d(rng_draw(ke, c));
+    alpha[c] = (uint32_t)(rng_next(ka, c) % q);
+    const int64_t e = cbd21_d(rng_next(ke, c));
     const uint64_t gs = (uint64_t)g * from_i64(s_old[c], q) % q;
     t[c] = (uint32_t)((gs + from_i64(e, q)) % q);
   }
@@ -477,7 +479,7 @@ static he_status make_ksk_dev(const Mods& M, uint64_t seed, uint32_t id, const i
       const uint32_t g = (j == i) ? (uint32_t)((uint64_t)(M.m[2] % q) * (M.m[1 - i] % q) % q) : 0u;
       uint32_t* alpha = ksk + ((size_t)(i * 2 + 0) * 3 + j) * deg;
       uint32_t* beta = ksk + ((size_t)(i * 2 + 1) * 3 + j) * deg;
-      k_ksk_prep<<<grid_for(deg), 256, 0, st>>>(seed, id, i, j, q, g, s_old, deg, alpha, beta);
+      k_ksk_prep<<<grid_for(deg), 256, 0, st>>>(M.rng, seed, id, i, j, q, g, s_old, deg, alpha, beta);
       HE_CUDA(ntt_forward(tabs[j], alpha, 1, deg, st), "NTT(alpha)");
       HE_CUDA(ntt_forward(tabs[j], beta, 1, deg, st), "NTT(t)");
       k_ksk_beta<<<grid_for(deg), 256, 0, st>>>(alpha, snew + (size_t)j * deg, deg, q, beta);
@@ -495,7 +497,7 @@ extern "C" he_status he_rhombus_keygen(const he_context* c, uint64_t seed, const
   const uint32_t N = c->R.N, n = c->R.n_rh;
   const int logn = ilog2_u(n);
   const Mods M = make_mods(c->R);
-  k_small_secret<<<grid_for(N), 256, 0, st>>>(seed, n, N, s_small_dev, s_up_dev);
+  k_small_secret<<<grid_for(N), 256, 0, st>>>(c->R.rng, seed, n, N, s_small_dev, s_up_dev);
   for (int L = 0; L < 2; ++L) {
     uint32_t* dst = s_up_ntt_dev + (size_t)L * N;
     k_reduce_signed<<<grid_for(N), 256, 0, st>>>(s_up_dev, N, M.m[L], dst);
@@ -1781,7 +1783,7 @@ static he_status make_ksk_gadget_dev(const Mods& M, uint64_t seed, uint32_t id, 
         g = (uint32_t)((uint64_t)((uint64_t)(M.m[2] % q) * (M.m[1 - i] % q) % q) * powmod_h(2, (uint64_t)kSdBits * h, q) % q);
       uint32_t* alpha = ksk + ((size_t)(t * 2 + 0) * 3 + j) * deg;
       uint32_t* beta = ksk + ((size_t)(t * 2 + 1) * 3 + j) * deg;
-      k_ksk_prep<<<grid_for(deg), 256, 0, st>>>(seed, id, t, j, q, g, s_old, deg, alpha, beta);
+      k_ksk_prep<<<grid_for(deg), 256, 0, st>>>(M.rng, seed, id, t, j, q, g, s_old, deg, alpha, beta);
       HE_CUDA(ntt_forward(tabs[j], alpha, 1, deg, st), "NTT(alpha)");
       HE_CUDA(ntt_forward(tabs[j], beta, 1, deg, st), "NTT(t)");
       k_ksk_beta<<<grid_for(deg), 256, 0, st>>>(alpha, snew + (size_t)j * deg, deg, q, beta);
@@ -1962,6 +1964,9 @@ extern "C" he_status he_slot_bsgs_plan_create(const he_context* c, const uint32_
 
 extern "C" he_status he_slot_bsgs_plan_create_ext(const he_context* c, const uint32_t* pts_ntt_dev, uint32_t b,
                                                   uint32_t g, uint32_t stride, uint32_t flags, he_slot_pcmm_plan** out) {
+  if (flags & ~(HE_SLOT_LAZY_MODDOWN | HE_SLOT_PLAIN_GIANT)) return fail(HE_EINVAL, "unknown slot plan flags 0x%x", flags);
+  if ((flags & HE_SLOT_PLAIN_GIANT) && !(flags & HE_SLOT_LAZY_MODDOWN))
+    return fail(HE_EINVAL, "HE_SLOT_PLAIN_GIANT needs HE_SLOT_LAZY_MODDOWN (eager plans take gadget giant keys)");
   if (!(flags & HE_SLOT_LAZY_MODDOWN)) return he_slot_bsgs_plan_create(c, pts_ntt_dev, b, g, stride, out);
   if (!c || !out) return fail(HE_EINVAL, "null argument");
   const Mods M = make_mods(c->R);

@@ -35,7 +35,8 @@ EXPORTS = (
     "he_slot_pcmm_plan_destroy", "he_slot_pcmm_workspace_bytes", "he_slot_pcmm_run", "he_slot_pcmm_run_batch", "he_mod_raise",
     "he_slot_lt_plan_create", "he_slot_bsgs_plan_create", "he_slot_bsgs_plan_create_ext", "he_slot_pcmm_encode_pts_ext", "he_slot_rotation_keygen_plain",
     "he_encrypt_vector_w", "he_rhombus_weight_bytes_w", "he_rhombus_encode_weights_w", "he_rhombus_plan_create_w",
-    "he_rhombus_plan_info", "he_rhombus_run_subtree", "he_rhombus_finish",
+    "he_rhombus_plan_info", "he_rhombus_run_subtree", "he_rhombus_finish", "he_context_set_rng_key",
+    "he_chacha20_block",
 )
 
 
@@ -121,6 +122,8 @@ def lib():
             "he_slot_pcmm_workspace_bytes": (st, [vp, ctypes.POINTER(u64)]),
             "he_slot_pcmm_run": (st, [vp, vp, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_slot_pcmm_run_batch": (st, [vp, vp, u32, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
+            "he_context_set_rng_key": (st, [vp, ctypes.c_char_p]),
+            "he_chacha20_block": (st, [ctypes.c_char_p, u32, ctypes.c_char_p, ctypes.c_char_p]),
             "he_encrypt_vector_w": (st, [vp, vp, vp, u32, u32, u64, u32, vp, vp]),
             "he_rhombus_weight_bytes_w": (st, [vp, u32, u32, u32, u32, ctypes.POINTER(u64)]),
             "he_rhombus_encode_weights_w": (st, [vp, vp, u32, u32, u32, u32, u32, vp, vp]),

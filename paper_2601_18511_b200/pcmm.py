@@ -54,6 +54,7 @@ class MlwePcmmPlan:
     _workspace: object = field(default=None, repr=False)
     _stream_bufs: object = field(default=None, repr=False)
     _copy_stream: object = field(default=None, repr=False)
+    _ctx_keepalive: object = field(default=None, repr=False)   # the creating context's device state
 
     @property
     def shape(self) -> tuple[int, int]:
@@ -160,7 +161,7 @@ def _plan_from_digits(ctx: HeContext, digits, n_out: int, n_in: int, d_w: int, m
     torch = _torch()
     h = ctypes.c_void_p()
     native.call("he_pcmm_plan_create", ctx.handle, digits.data_ptr(), n_out, n_in, d_w, ctypes.byref(h))
-    plan = MlwePcmmPlan(n_out, n_in, d_w, max_abs, digits, algo=algo, _handle=h)
+    plan = MlwePcmmPlan(n_out, n_in, d_w, max_abs, digits, algo=algo, _handle=h, _ctx_keepalive=ctx._dev)
     if algo == "spectral":
         nb = ctypes.c_uint64()
         native.call("he_pcmm_spectral_weight_bytes", h, ctypes.byref(nb))
@@ -246,6 +247,8 @@ def _check_operand(ctx: HeContext, plan: MlwePcmmPlan, X) -> None:
     """Error contract of matmul.py:139-149, raised before any compute."""
     if not isinstance(X, CtBlocks):
         raise TypeError("pcmm consumes a ciphertext operand")
+    if plan._ctx_keepalive is not None and plan._ctx_keepalive is not ctx._dev:
+        raise ValueError("plan was built under another HeContext (its device tables); rebuild or load it here")
     if X.n_cols != plan.n_in:
         raise ValueError(f"dim mismatch: plan {plan.n_in}, operand {X.n_cols}")
     if X.layout != plan.layout:
@@ -256,6 +259,16 @@ def _check_operand(ctx: HeContext, plan: MlwePcmmPlan, X) -> None:
     shape = tuple(int(s) for s in X.data.shape)
     if shape != (plan.n_in // ctx.params.mlwe_rank, 2, 2, ctx.params.N):
         raise ValueError(f"ciphertext batch has shape {shape}")
+
+
+def _note_read(X, stream=None) -> None:
+    """Mark that every access to X.data so far is queued on `stream` (the current one by default):
+    pcmm_mlwe_to_host's input upload, on its own stream, waits for this event before overwriting
+    X.data (and for the whole current stream when X carries none)."""
+    torch = _torch()
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    X._read_done = ev
 
 
 def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks | None = None,
@@ -285,6 +298,7 @@ def pcmm_mlwe(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out: MlweBlocks |
         k = ctx.params.mlwe_rank
         led.pc_mults = (plan.n_out // k) * (plan.n_in // k)
         led.rescales = plan.n_out // k
+    _note_read(X)
     ctx.ledger.add_c(led)
     ctx.ledger.observe_level(X.level - 1)
     out.level = X.level - 1
@@ -308,6 +322,7 @@ def pcmm_mlwe_into_peers(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_
     pb = (ctypes.c_void_p * n)(*[int(v) for v in out_b_ptrs])
     pa = (ctypes.c_void_p * n)(*[int(v) for v in out_a_ptrs])
     native.call("he_pcmm_gemm_rows_peers", plan._handle, ws.data_ptr(), 0, plan.n_out, pb, pa, n, dst_row0, st)
+    _note_read(X)
     k = ctx.params.mlwe_rank
     ctx.ledger.pc_mults += (plan.n_out // k) * (plan.n_in // k)
     ctx.ledger.rescales += plan.n_out // k
@@ -335,14 +350,18 @@ def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_hos
         X.data.copy_(x_host, non_blocking=True)
         x_host = None
     if x_host is not None:
-        # the input goes up on its own stream: it only waits until the previous call's decompose has read
-        # X.data, so back-to-back calls overlap it with the previous call's device->host tail (the two
-        # directions use separate copy engines)
+        # the input goes up on its own stream: it only waits until the last queued access to X.data
+        # (e.g. the previous call's decompose, recorded on X itself, whichever plan ran it) -- so
+        # back-to-back calls overlap it with the previous call's device->host tail (the two directions
+        # use separate copy engines); an X with no recorded access waits for the whole current stream
         if getattr(plan, "_h2d_stream", None) is None:
             plan._h2d_stream = torch.cuda.Stream(dev)
         hs = plan._h2d_stream
-        if getattr(plan, "_x_consumed", None) is not None:
-            hs.wait_event(plan._x_consumed)
+        last = getattr(X, "_read_done", None)
+        if last is not None:
+            hs.wait_event(last)
+        else:
+            hs.wait_stream(st)
         with torch.cuda.stream(hs):
             X.data.copy_(x_host, non_blocking=True)
         up = torch.cuda.Event()
@@ -355,8 +374,7 @@ def pcmm_mlwe_to_host(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, out_b_hos
         plan._copy_stream = torch.cuda.Stream(dev)
     cs = plan._copy_stream
     native.call("he_pcmm_decompose", plan._handle, X.data.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
-    plan._x_consumed = torch.cuda.Event()
-    plan._x_consumed.record(st)
+    _note_read(X, st)
     copied = [None, None]
     # a short first chunk starts the device->host stream sooner (the copies, not the compute, set the pace)
     first = min(256, chunk_rows) if plan.n_out > chunk_rows else chunk_rows

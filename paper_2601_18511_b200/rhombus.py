@@ -122,8 +122,9 @@ class RhombusPlan:
             pass
 
 
-def rhombus_keygen(ctx: HeContext, sk: SecretKey, seed: int) -> RhombusKeys:
+def rhombus_keygen(ctx: HeContext, sk: SecretKey, seed: int | None = None) -> RhombusKeys:
     torch = _torch()
+    seed = ctx.nonce(seed)
     p = ctx.params
     N, n = p.N, p.rhombus_degree
     lg = n.bit_length() - 1
@@ -139,9 +140,11 @@ def rhombus_keygen(ctx: HeContext, sk: SecretKey, seed: int) -> RhombusKeys:
     return keys
 
 
-def encrypt_vector(ctx: HeContext, sk: SecretKey, v, seed: int, r0: int = 0, window=None, split=None) -> CtVector:
+def encrypt_vector(ctx: HeContext, sk: SecretKey, v, seed: int | None = None, r0: int = 0, window=None,
+                   split=None) -> CtVector:
     """Encrypt an n_in-vector in the PCMv input layout of window w (default rhombus_window(n_in))."""
     torch = _torch()
+    seed = ctx.nonce(seed)
     vt = torch.as_tensor(v, dtype=torch.float64, device=ctx.device).contiguous().reshape(-1)
     n_vals = int(vt.numel())
     w = int(window) if window is not None else rhombus_window(ctx.params, n_vals, split)

@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 
 from . import native
 from .context import CtBlocks, HeContext, SecretKey, _torch
-from .pcmm import MlwePcmmPlan, _check_operand
+from .pcmm import MlwePcmmPlan, _check_operand, _note_read
 
 
 METHODS = {"keyswitch": 0, "trace": 1}
@@ -56,6 +56,7 @@ class RingPackPlan:
     _handle: object = field(default=None, repr=False)
     _workspace: object = field(default=None, repr=False)
     _raw: tuple = field(default=None, repr=False)
+    _ctx_keepalive: object = field(default=None, repr=False)
 
     def workspace(self, device):
         torch = _torch()
@@ -82,8 +83,9 @@ class RingPackPlan:
             pass
 
 
-def ring_pack_keygen(ctx: HeContext, sk: SecretKey, seed: int, method: str = "keyswitch") -> RingPackKeys:
+def ring_pack_keygen(ctx: HeContext, sk: SecretKey, seed: int | None = None, method: str = "keyswitch") -> RingPackKeys:
     torch = _torch()
+    seed = ctx.nonce(seed)
     m = _method(method)
     nb = ctypes.c_uint64()
     native.call("he_ring_pack_key_bytes", ctx.handle, m, ctypes.byref(nb))
@@ -96,7 +98,7 @@ def ring_pack_keygen(ctx: HeContext, sk: SecretKey, seed: int, method: str = "ke
 def make_ring_pack_plan(ctx: HeContext, n_out: int, method: str = "keyswitch") -> RingPackPlan:
     h = ctypes.c_void_p()
     native.call("he_ring_pack_plan_create", ctx.handle, int(n_out), _method(method), ctypes.byref(h))
-    return RingPackPlan(int(n_out), method, _handle=h)
+    return RingPackPlan(int(n_out), method, _handle=h, _ctx_keepalive=ctx._dev)
 
 
 def pcmm_level1(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, raw_b=None, raw_a=None):
@@ -111,6 +113,7 @@ def pcmm_level1(ctx: HeContext, plan: MlwePcmmPlan, X: CtBlocks, raw_b=None, raw
     ws = plan.workspace(ctx.device)
     native.call("he_pcmm_run_level1", plan._handle, X.data.data_ptr(), X.level, raw_b.data_ptr(), raw_a.data_ptr(),
                 ws.data_ptr(), ws.numel(), ctx.stream())
+    _note_read(X)
     return raw_b, raw_a
 
 
@@ -119,6 +122,8 @@ def ring_pack(ctx: HeContext, rp: RingPackPlan, keys: RingPackKeys, raw_b, raw_a
     p = ctx.params
     if keys.method != rp.method:
         raise ValueError(f"key/plan mismatch: keys for {keys.method!r}, plan for {rp.method!r}")
+    if rp._ctx_keepalive is not None and rp._ctx_keepalive is not ctx._dev:
+        raise ValueError("ring-pack plan was built under another HeContext")
     if out is None:
         out = torch.empty((rp.n_out // p.mlwe_rank, 1, 2, p.N), dtype=torch.int32, device=ctx.device)
     ws = rp.workspace(ctx.device)

@@ -180,9 +180,10 @@ def make_slot_pcmm_plan(ctx: HeContext, weights, shear_power: int = 0, split: Bs
     return plan
 
 
-def slot_pcmm_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: int) -> SlotPcmmKeys:
+def slot_pcmm_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: int | None = None) -> SlotPcmmKeys:
     """Rotation keys the plan's BSGS schedule needs: baby steps i d, giant steps j b d."""
     torch = _torch()
+    seed = ctx.nonce(seed)
     d, b, g = plan.dim, plan.split.baby, plan.split.giant
     N = ctx.params.N
 
@@ -199,11 +200,12 @@ def slot_pcmm_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: in
     return SlotPcmmKeys(gen(baby), gen(giant), tuple(baby + giant))
 
 
-def encrypt_packed(ctx: HeContext, sk: SecretKey, mat, shear_power: int, seed: int, r0: int = 0,
+def encrypt_packed(ctx: HeContext, sk: SecretKey, mat, shear_power: int, seed: int | None = None, r0: int = 0,
                    scale: float | None = None) -> PackedCt:
     """Encrypt col_shear(mat, l) row-major in the slots at scale Delta (or a plan's input_scale), level 1
     (hesim pack_sheared)."""
     torch = _torch()
+    seed = ctx.nonce(seed)
     m = np.asarray(mat, dtype=float)
     d = m.shape[0]
     if m.shape != (d, d):
@@ -235,10 +237,31 @@ def _check_operand(plan: SlotPcmmPlan, B) -> None:
         raise ValueError(f"scale mismatch: plan expects operand scale {want}, got {B.scale}")
 
 
+def check_keys(ctx: HeContext, keys: SlotPcmmKeys, steps, giant_components: int = 4) -> None:
+    """The rotation keys must be the ones the plan's schedule reads: same steps, gadget baby keys
+    (4 components), giant keys with the plan's component count (2 for plain keys); raised before any
+    launch (a mismatched layout would make the kernels read past the key buffers)."""
+    if not isinstance(keys, SlotPcmmKeys):
+        raise TypeError("expected SlotPcmmKeys")
+    steps = tuple(int(s) for s in steps)
+    if tuple(int(s) for s in keys.steps) != steps:
+        raise ValueError(f"key/plan mismatch: keys for rotation steps {tuple(keys.steps)[:6]}..., plan needs "
+                         f"{steps[:6]}...")
+    N = ctx.params.N
+    if tuple(int(v) for v in keys.baby.shape[1:]) != (4, 2, 3, N):
+        raise ValueError(f"baby keys have shape {tuple(keys.baby.shape)}, expected [b-1, 4, 2, 3, {N}]")
+    if tuple(int(v) for v in keys.giant.shape[1:]) != (giant_components, 2, 3, N):
+        raise ValueError(f"giant keys have shape {tuple(keys.giant.shape)}, expected [g-1, {giant_components}, 2, 3, {N}]")
+
+
 def pcmm_slot_bsgs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, B: PackedCt) -> PackedCt:
     """hesim pcmm_bsgs on the GPU: B (shear power l + 1, level 1) -> A B (shear power l, level 0)."""
     torch = _torch()
     _check_operand(plan, B)
+    d, b, g = plan.dim, plan.split.baby, plan.split.giant
+    check_keys(ctx, keys, [i * d for i in range(1, b)] + [j * b * d for j in range(1, g)])
+    if tuple(int(v) for v in B.data.shape) != (2, 2, ctx.params.N):
+        raise ValueError(f"ciphertext has shape {tuple(B.data.shape)}, expected (2, 2, {ctx.params.N})")
     require_level(B.level)
     if B.level != 1:
         raise ValueError(f"the slot-domain PCMM runs at level 1, operand is at level {B.level}")
@@ -297,8 +320,9 @@ def make_slot_linear_plan(ctx: HeContext, masks, steps) -> SlotPcmmPlan:
     return plan
 
 
-def slot_linear_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: int) -> SlotPcmmKeys:
+def slot_linear_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: int | None = None) -> SlotPcmmKeys:
     torch = _torch()
+    seed = ctx.nonce(seed)
     N = ctx.params.N
     st = list(plan.steps[1:])
     keys = torch.empty((max(len(st), 1), 4, 2, 3, N), dtype=torch.int32, device=ctx.device)
@@ -313,6 +337,9 @@ def slot_linear(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, X: Packe
     torch = _torch()
     if not isinstance(X, PackedCt):
         raise TypeError("slot_linear consumes a ciphertext operand")
+    check_keys(ctx, keys, plan.steps[1:])
+    if tuple(int(v) for v in X.data.shape) != (2, 2, ctx.params.N):
+        raise ValueError(f"ciphertext has shape {tuple(X.data.shape)}, expected (2, 2, {ctx.params.N})")
     require_level(X.level)
     if X.level != 1:
         raise ValueError(f"slot linear maps run at level 1, operand is at level {X.level}")

@@ -33,7 +33,7 @@ from . import native, slots
 from .context import CtBlocks, HeContext, SecretKey, _torch, require_level
 from .errors import NeedsBootstrapError
 from .layout import bit_reverse_table, coeff_table
-from .slotpcmm import BsgsSplit, SlotPcmmKeys, SlotPcmmPlan
+from .slotpcmm import BsgsSplit, SlotPcmmKeys, SlotPcmmPlan, check_keys
 
 
 DEFAULT_PT_SHIFT = 1    # plaintexts at 2 q1, input slots at Delta / 2 (see make_slot_to_coeffs_plan)
@@ -148,9 +148,10 @@ def make_slot_to_coeffs_plan(ctx: HeContext, split: BsgsSplit | None = None, bat
     return plan
 
 
-def slot_to_coeffs_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: int) -> SlotPcmmKeys:
+def slot_to_coeffs_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, seed: int | None = None) -> SlotPcmmKeys:
     """Gadget rotation keys for baby steps 1 .. b-1 and giant steps j b."""
     torch = _torch()
+    seed = ctx.nonce(seed)
     N, b, g = ctx.params.N, plan.split.baby, plan.split.giant
 
     def gen(steps, plain=False):
@@ -165,11 +166,13 @@ def slot_to_coeffs_keygen(ctx: HeContext, sk: SecretKey, plan: SlotPcmmPlan, see
     return SlotPcmmKeys(gen(baby), gen(giant, getattr(plan, "plain_giant", False)), tuple(baby + giant))
 
 
-def encrypt_slots(ctx: HeContext, sk: SecretKey, acts, seed: int, r0: int = 0, scale: float | None = None) -> SlotBlocks:
+def encrypt_slots(ctx: HeContext, sk: SecretKey, acts, seed: int | None = None, r0: int = 0,
+                  scale: float | None = None) -> SlotBlocks:
     """Slot-encode and encrypt a (d/2) x n_in activation block at level 1, one ct per k columns -- the state
     the attention phase leaves behind.  scale: the plan's input_scale (Delta 2^-pt_shift,
     Delta / 2 by default) so that StC lands at Delta; None = the default plan's."""
     torch = _torch()
+    seed = ctx.nonce(seed)
     z = slot_vectors(ctx.params, acts)
     sc = ctx.params.delta / 2.0 ** DEFAULT_PT_SHIFT if scale is None else float(scale)
     pt = torch.from_numpy(np.stack([slots.encode(v, ctx.params.N, sc) for v in z])).to(ctx.device)
@@ -192,6 +195,11 @@ def slot_to_coeffs(ctx: HeContext, plan: SlotPcmmPlan, keys: SlotPcmmKeys, X: Sl
     if X.scale and X.scale != plan.input_scale:
         raise ValueError(f"scale mismatch: plan expects input scale {plan.input_scale}, operand has {X.scale}")
     N = ctx.params.N
+    b, g = plan.split.baby, plan.split.giant
+    check_keys(ctx, keys, list(range(1, b)) + [j * b for j in range(1, g)],
+               2 if getattr(plan, "plain_giant", False) else 4)
+    if tuple(int(v) for v in X.data.shape) != (X.n_ct, 2, 2, N):
+        raise ValueError(f"slot ciphertexts have shape {tuple(X.data.shape)}, expected ({X.n_ct}, 2, 2, {N})")
     out = torch.empty((X.n_ct, 1, 2, N), dtype=torch.int32, device=ctx.device)
     ws = plan.workspace(ctx.device)
     led = native.HeLedgerC()

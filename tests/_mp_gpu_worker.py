@@ -20,7 +20,7 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(0)
     P = HeParams.llama()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     k = P.mlwe_rank
     rng = np.random.default_rng(1)
     # MLWE PCMM, row-sharded

@@ -35,7 +35,7 @@ def test_a01_one_level_one_rescale_per_block():
 
     t0 = time.perf_counter()
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     rng = np.random.default_rng(0)
     sk = ctx.keygen(1)
     X = ctx.encrypt_acts(sk, rng.uniform(-1, 1, (P.tokens, 64)), seed=2)
@@ -138,7 +138,7 @@ def test_a10_slot_pcmm_rotation_counts_like_reference_c03():
 
     t0 = time.perf_counter()
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(1)
     rng = np.random.default_rng(3)
     d = 16
@@ -165,7 +165,7 @@ def test_a11_ring_packed_output_decrypts_in_input_layout():
 
     t0 = time.perf_counter()
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(1)
     rng = np.random.default_rng(4)
     A, W = rng.uniform(-1, 1, (P.tokens, 48)), rng.uniform(-1, 1, (64, 48)) / 8

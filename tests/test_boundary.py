@@ -82,7 +82,7 @@ def _plan(n_out=512, n_in=512):
 
 
 def test_operand_checks_follow_reference_order():
-    ctx = HeContext(HeParams.llama())
+    ctx = HeContext(HeParams.llama(), rng="seeded")
     plan = _plan()
     with pytest.raises(TypeError, match="ciphertext operand"):
         _check_operand(ctx, plan, np.zeros(3))
@@ -110,7 +110,7 @@ def test_ledger_semantics_match_hesim():
 
 
 def test_context_fork_merge_private_ledgers():
-    ctx = HeContext(HeParams.toy())
+    ctx = HeContext(HeParams.toy(), rng="seeded")
     kids = [ctx.fork() for _ in range(3)]
     for i, c in enumerate(kids):
         c.ledger.pc_mults += i + 1

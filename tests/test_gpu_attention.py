@@ -19,7 +19,7 @@ def test_pc_attention_hybrid_matches_hesim_oracle(d, params, tol):
     positions = d + np.arange(d)
     np.testing.assert_allclose(clear_pc_attention(q, k, v, positions), ref, atol=1e-12)   # restatement
     P = HeParams.toy() if params == "toy" else HeParams.llama()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(3)
     out, rep = pc_attention_hybrid(ctx, sk, q, k, v, positions, seed=10)
     assert rep["ledger"]["rescales"] == 2
@@ -36,7 +36,7 @@ def test_rope_packed_matches_hesim(d, params, tol):
     q, ref = G[f"d{d}_q"], G[f"d{d}_rope2"]
     positions = d + np.arange(d)
     P = HeParams.toy() if params == "toy" else HeParams.llama()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(3)
     plan = make_rope_plan(ctx, d, positions, shear_power=2)
     keys = slot_linear_keygen(ctx, sk, plan, seed=4)

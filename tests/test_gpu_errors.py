@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(scope="module")
 def toy():
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     rng = np.random.default_rng(0)
     W = rng.uniform(-1, 1, (32, 32)) / 8
@@ -116,3 +116,52 @@ def test_slot_bsgs_abi_status_codes(toy):
         native.call("he_slot_pcmm_run_batch", h, ct.data_ptr(), 1, 1, keys.data_ptr(), keys.data_ptr(), out.data_ptr(),
                     ws.data_ptr(), 64, ctx.stream(), ctypes.byref(led))
     native.lib().he_slot_pcmm_plan_destroy(h)
+    with pytest.raises(ValueError, match="unknown slot plan flags"):
+        native.call("he_slot_bsgs_plan_create_ext", ctx.handle, pts.data_ptr(), 16, 16, 1, 8, ctypes.byref(h))
+    with pytest.raises(ValueError, match="PLAIN_GIANT needs"):
+        native.call("he_slot_bsgs_plan_create_ext", ctx.handle, pts.data_ptr(), 16, 16, 1, 2, ctypes.byref(h))
+
+
+def test_slot_keys_must_match_the_plan(toy):
+    """keys from another plan (other steps, or plain instead of gadget giant keys) are rejected
+    before any launch -- the kernels would otherwise read past the key buffers."""
+    from paper_2601_18511_b200.slotpcmm import (BsgsSplit, SlotPcmmKeys, make_slot_pcmm_plan, pcmm_slot_bsgs,
+                                                slot_pcmm_keygen)
+    from paper_2601_18511_b200.stc import (encrypt_slots, make_slot_to_coeffs_plan, slot_to_coeffs,
+                                           slot_to_coeffs_keygen)
+
+    P, ctx, sk, W, X = toy
+    rng = np.random.default_rng(3)
+    p16 = make_slot_pcmm_plan(ctx, rng.uniform(-1, 1, (16, 16)) / 4, shear_power=0)
+    p16b = make_slot_pcmm_plan(ctx, rng.uniform(-1, 1, (16, 16)) / 4, shear_power=0, split=BsgsSplit(8, 2))
+    k16 = slot_pcmm_keygen(ctx, sk, p16, seed=3)
+    B = encrypt_packed(ctx, sk, rng.uniform(-1, 1, (16, 16)) / 4, 1, seed=4)
+    with pytest.raises(ValueError, match="key/plan mismatch"):
+        pcmm_slot_bsgs(ctx, p16b, k16, B)
+    assert pcmm_slot_bsgs(ctx, p16, k16, B).level == 0
+    sp = make_slot_to_coeffs_plan(ctx)
+    ks = slot_to_coeffs_keygen(ctx, sk, sp, seed=5)
+    Xs = encrypt_slots(ctx, sk, rng.uniform(-1, 1, (P.tokens, P.mlwe_rank)), seed=6, scale=sp.input_scale)
+    if getattr(sp, "plain_giant", False):   # gadget giant keys where the plan reads plain ones
+        bad = SlotPcmmKeys(ks.baby, torch.zeros((ks.giant.shape[0], 4, 2, 3, P.N), dtype=torch.int32,
+                                                device=ctx.device), ks.steps)
+        with pytest.raises(ValueError, match="giant keys have shape"):
+            slot_to_coeffs(ctx, sp, bad, Xs)
+    with pytest.raises(ValueError, match="key/plan mismatch"):
+        slot_to_coeffs(ctx, sp, k16, Xs)
+    assert slot_to_coeffs(ctx, sp, ks, Xs).level == 0
+
+
+def test_plans_keep_their_context(toy):
+    """a plan holds its creating context's device state alive and refuses another context."""
+    import gc
+
+    P, ctx, sk, W, X = toy
+    other = HeContext(P, rng="seeded")
+    plan = make_mlwe_pcmm_plan(other, W)
+    del other
+    gc.collect()
+    with pytest.raises(ValueError, match="another HeContext"):
+        from paper_2601_18511_b200 import pcmm_mlwe
+        pcmm_mlwe(ctx, plan, X)
+    assert plan._ctx_keepalive.handle   # the device context is still alive

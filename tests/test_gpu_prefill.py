@@ -19,7 +19,7 @@ def test_encrypted_projection_prefill_matches_hesim(name, algo):
     d_model, d_head, n_heads, d_ff, n_layers, seed, ptok = (int(v) for v in G[name + "_cfg"])
     cfg = ToyConfig(d_model, d_head, n_heads, d_ff, n_layers, seed)
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(5)
     layers, _ = make_weights(cfg)
     proj = make_projection_plans(ctx, layers, algo=algo)
@@ -44,7 +44,7 @@ def test_encrypted_decode_step_rhombus_matches_hesim(name):
     cfg = ToyConfig(d_model, d_head, n_heads, d_ff, n_layers, seed)
     _, cache = chunked_prefill(G[name + "_tokens"], ptok, cfg)
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(5)
     layers, _ = make_weights(cfg)
     proj = make_vector_projection_plans(ctx, sk, layers)

@@ -21,7 +21,7 @@ def u32(t):
 
 
 def _setup(P, n_out, n_in, seed=0, split=None):
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     rng = np.random.default_rng(seed)
     v = rng.uniform(-1, 1, n_in)
     W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
@@ -98,7 +98,7 @@ def test_pcmv_errors():
     with pytest.raises(NeedsBootstrapError):
         pcmv_rhombus(ctx, plan, keys, CtVector(x.data, 0, x.n_vals, window=x.window))
     with pytest.raises(ValueError, match="another HeContext"):
-        pcmv_rhombus(HeContext(P), plan, keys, x)
+        pcmv_rhombus(HeContext(P, rng="seeded"), plan, keys, x)
 
 
 @pytest.mark.parametrize("n_out,n_in,split", [(4096, 11008, None), (14336, 4096, None), (14336, 4096, 0)])

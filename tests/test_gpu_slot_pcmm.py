@@ -35,7 +35,7 @@ def test_toy_bit_exact_and_hesim_values(key):
     split = BsgsSplit(*(int(v) for v in g[key + "_split"]))
     d, b, gg = W.shape[0], split.baby, split.giant
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     plan = make_slot_pcmm_plan(ctx, W, shear_power=shear, split=split)
     keys = slot_pcmm_keygen(ctx, sk, plan, seed=13)
@@ -67,7 +67,7 @@ def test_toy_rotation_keys_match_oracle():
     from paper_2601_18511_b200 import native
 
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     plan = make_slot_pcmm_plan(ctx, np.eye(16) * 0.5)
     keys = slot_pcmm_keygen(ctx, sk, plan, seed=13)
@@ -84,7 +84,7 @@ def test_toy_rotation_keys_match_oracle():
 
 def test_error_contract():
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     W = np.eye(16) * 0.25
     plan = make_slot_pcmm_plan(ctx, W, shear_power=0)
@@ -111,7 +111,7 @@ def test_llama_ring_precision(d, shear):
     import torch
 
     P = HeParams.llama()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(3)
     rng = np.random.default_rng(d)
     W = rng.uniform(-1, 1, (d, d)) / np.sqrt(d)
@@ -142,7 +142,7 @@ def test_graph_replay_same_words():
     from paper_2601_18511_b200 import OpGraph
 
     P = HeParams.llama()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(3)
     rng = np.random.default_rng(1)
     d = 64
@@ -167,7 +167,7 @@ def test_depth1_schedule_matches_hesim_depth1(key):
     shear = int(key.split("_l")[1])
     d = W.shape[0]
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     plan = make_slot_pcmm_plan(ctx, W, shear_power=shear, split=BsgsSplit(d, 1))
     keys = slot_pcmm_keygen(ctx, sk, plan, seed=13)
@@ -186,7 +186,7 @@ def test_toy_lazy_and_scale_split_bit_exact():
     W, B, ref = g["d16_l0_W"], g["d16_l0_B"], g["d16_l0_hesim_bsgs"]
     d = W.shape[0]
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     split = BsgsSplit(8, 2)
     plan = make_slot_pcmm_plan(ctx, W, shear_power=0, split=split, pt_shift=2, lazy=True)

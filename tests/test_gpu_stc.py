@@ -24,7 +24,7 @@ def u32(t):
 @pytest.mark.parametrize("lazy", [False, True])
 def test_toy_bit_exact_and_layout(lazy):
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     d, k, N, n = P.mlwe_degree, P.mlwe_rank, P.N, P.N // 2
     A = np.random.default_rng(3).uniform(-1, 1, (d // 2, 2 * k))
@@ -62,7 +62,7 @@ def test_toy_batched_shared_path_bit_exact(n_ct, lazy, halves, monkeypatch):
     if halves:
         monkeypatch.setenv("HE_SD_HALVES", str(halves))
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     d, k, N, n = P.mlwe_degree, P.mlwe_rank, P.N, P.N // 2
     A = np.random.default_rng(5).uniform(-1, 1, (d // 2, n_ct * k))
@@ -87,7 +87,7 @@ def test_toy_batched_shared_path_bit_exact(n_ct, lazy, halves, monkeypatch):
 
 def test_error_contract():
     P = HeParams.toy()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     plan = make_slot_to_coeffs_plan(ctx)
     keys = slot_to_coeffs_keygen(ctx, sk, plan, seed=13)
@@ -112,7 +112,7 @@ def test_llama_ring():
     import torch
 
     P = HeParams()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     d, k = P.mlwe_degree, P.mlwe_rank
     t0 = time.perf_counter()
