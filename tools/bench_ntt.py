@@ -35,7 +35,7 @@ def run(ctx, n, limb, batch, iters=20):
 
 
 def main():
-    ctx = HeContext(HeParams.llama())
+    ctx = HeContext(HeParams.llama(), rng="seeded")
     res = {}
     for n, batch in ((65536, 256), (4096, 4096)):
         for limb in (0, 1):

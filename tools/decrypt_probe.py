@@ -12,7 +12,7 @@ from paper_2601_18511_b200 import HeContext, HeParams, make_mlwe_pcmm_plan, nati
 from paper_2601_18511_b200.context import decode_mlwe_rows
 
 P = HeParams.llama()
-ctx = HeContext(P)
+ctx = HeContext(P, rng="seeded")
 sk = ctx.keygen(1)
 g = torch.Generator(device="cuda").manual_seed(1)
 W = (torch.rand((4096, 4096), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) / 64

@@ -27,7 +27,7 @@ def stage(name):
 
 
 def run(P, n_out, n_in, seed=1, rows=None, cols=None, full=False):
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     rng = np.random.default_rng(seed)
     A = rng.uniform(-1, 1, (P.tokens, n_in))
     W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
@@ -119,7 +119,7 @@ def time_shape(n_out, n_in, iters=5):
     import ctypes
     from paper_2601_18511_b200 import native
     P = HeParams.llama()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     rng = np.random.default_rng(3)
     A = rng.uniform(-1, 1, (P.tokens, n_in))
     W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
@@ -158,7 +158,7 @@ def time_rhombus(shapes=((4096, 11008), (14336, 4096)), iters=3):
     from paper_2601_18511_b200.rhombus import (clear_pcmv, decrypt_vector, encrypt_vector, make_rhombus_plan,
                                                pcmv_rhombus, rhombus_keygen)
     P = HeParams.llama()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     t0 = time.time()
     keys = rhombus_keygen(ctx, sk, 99)

@@ -39,7 +39,7 @@ def graphed(fn):
 
 
 P = HeParams.llama()
-ctx = HeContext(P)
+ctx = HeContext(P, rng="seeded")
 sk = ctx.keygen(1)
 rng = np.random.default_rng(0)
 ops = {}

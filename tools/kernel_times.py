@@ -18,7 +18,7 @@ ap.add_argument("--ops", type=int, default=5)
 a = ap.parse_args()
 n_out, n_in = (int(v) for v in a.shape.split("x"))
 P = HeParams.llama()
-ctx = HeContext(P)
+ctx = HeContext(P, rng="seeded")
 g = torch.Generator(device="cuda").manual_seed(1)
 W = (torch.rand((n_out, n_in), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) / math.sqrt(n_in)
 A = torch.rand((P.tokens, n_in), generator=g, device="cuda", dtype=torch.float64) * 2 - 1

@@ -23,7 +23,7 @@ layers[0][6] *= 0.25
 x = rng.standard_normal((128, d))
 
 P = HeParams.llama()
-ctx = HeContext(P)
+ctx = HeContext(P, rng="seeded")
 sk = ctx.keygen(1)
 names = ("wq", "wk", "wv", "wo", "w_gate", "w_up", "w_down")
 t0 = time.perf_counter()

@@ -12,7 +12,7 @@ from paper_2601_18511_b200 import HeContext, HeParams, encrypt_vector, make_rhom
 for shape in (sys.argv[1:] or ["4096x11008", "14336x4096"]):
     n_out, n_in = (int(v) for v in shape.split("x"))
     P = HeParams.llama()
-    ctx = HeContext(P)
+    ctx = HeContext(P, rng="seeded")
     sk = ctx.keygen(7)
     keys = rhombus_keygen(ctx, sk, 99)
     rng = np.random.default_rng(1)

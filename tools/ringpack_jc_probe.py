@@ -11,7 +11,7 @@ from paper_2601_18511_b200 import (HeContext, HeParams, OpGraph, make_mlwe_pcmm_
                                    pcmm_level1, ring_pack, ring_pack_keygen)
 
 P = HeParams.llama()
-ctx = HeContext(P)
+ctx = HeContext(P, rng="seeded")
 sk = ctx.keygen(1)
 g = torch.Generator(device="cuda").manual_seed(1)
 W = (torch.rand((4096, 11008), generator=g, device="cuda", dtype=torch.float64) * 2 - 1) / math.sqrt(11008)

@@ -12,7 +12,7 @@ SHAPES = sys.argv[1].split(",") if len(sys.argv) > 1 else ["4096x4096", "4096x11
                                                             "4096x14336"]
 ALGOS = sys.argv[2].split(",") if len(sys.argv) > 2 else ["spectral", "direct"]
 P = HeParams.llama()
-ctx = HeContext(P)
+ctx = HeContext(P, rng="seeded")
 g = torch.Generator(device="cuda").manual_seed(1)
 for shp in SHAPES:
     n_out, n_in = (int(v) for v in shp.split("x"))

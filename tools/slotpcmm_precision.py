@@ -11,7 +11,7 @@ import torch
 from paper_2601_18511_b200 import (HeContext, HeParams, clear_slot_pcmm, decrypt_packed, encrypt_packed,
                                    make_slot_pcmm_plan, pcmm_slot_bsgs, slot_pcmm_keygen)
 
-ctx = HeContext(HeParams.llama())
+ctx = HeContext(HeParams.llama(), rng="seeded")
 sk = ctx.keygen(1)
 for d in (128, 64):
     rng = np.random.default_rng(d)

@@ -9,7 +9,7 @@ import torch
 from paper_2601_18511_b200 import (HeContext, HeParams, encrypt_packed, make_slot_pcmm_plan, pcmm_slot_bsgs,
                                    slot_pcmm_keygen)
 
-ctx = HeContext(HeParams.llama())
+ctx = HeContext(HeParams.llama(), rng="seeded")
 sk = ctx.keygen(1)
 d = 128
 rng = np.random.default_rng(0)

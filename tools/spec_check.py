@@ -26,7 +26,7 @@ def u32(t):
 
 # toy ring vs oracle
 P = HeParams.toy()
-ctx = HeContext(P)
+ctx = HeContext(P, rng="seeded")
 rng = np.random.default_rng(0)
 for n_out, n_in in [(16, 16), (64, 48), (256, 384)]:
     A = rng.uniform(-1, 1, (P.tokens, n_in))
@@ -49,7 +49,7 @@ for n_out, n_in in [(16, 16), (64, 48), (256, 384)]:
               flush=True)
 
 P = HeParams.llama()
-ctx = HeContext(P)
+ctx = HeContext(P, rng="seeded")
 g = torch.Generator(device="cuda").manual_seed(1)
 for shp in a.shapes.split(","):
     n_out, n_in = (int(v) for v in shp.split("x"))

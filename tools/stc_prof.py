@@ -9,7 +9,7 @@ import torch
 from paper_2601_18511_b200 import HeContext, HeParams
 from paper_2601_18511_b200.stc import encrypt_slots, make_slot_to_coeffs_plan, slot_to_coeffs, slot_to_coeffs_keygen
 
-ctx = HeContext(HeParams.llama())
+ctx = HeContext(HeParams.llama(), rng="seeded")
 sk = ctx.keygen(1)
 P = ctx.params
 plan = make_slot_to_coeffs_plan(ctx)
