@@ -515,7 +515,69 @@ def side_measurements(P, dev):
         out["slot_to_coeffs"] = stc_side(P, dev)
     except Exception as exc:
         out["slot_to_coeffs_error"] = repr(exc)
+    try:
+        out["chained_op"] = chain_side(dev)
+    except Exception as exc:
+        out["chained_op_error"] = repr(exc)
     return out
+
+
+def chain_side(dev, n_in: int = 11008, n_out: int = 4096, reps=3):
+    """§8f2 with the paper's pipeline: slot-encoded activations at level 5 -> lower to level 4
+    -> Cooley-Tukey-factorized SlotToCoeffs (three maps, levels 4 -> 1) -> the metric-shape MLWE PCMM -> ring
+    packing -> ModRaise: device ms per stage and the decrypted precision of each hand-off."""
+    import torch
+
+    from paper_2601_18511_b200 import (HeContext, HeParams, clear_pcmm, make_mlwe_pcmm_plan, make_ring_pack_plan,
+                                       mod_raise, pcmm_packed, ring_pack_keygen)
+    from paper_2601_18511_b200.chain import (encrypt_slots_at, factorized_stc_keygen, lower_level,
+                                             make_factorized_stc_plan, slot_to_coeffs_factorized)
+
+    P = HeParams.llama_chain(levels=4)
+    ctx = HeContext(P, device=dev, rng="seeded")
+    sk = ctx.keygen(71)
+    rng = np.random.default_rng(73)
+    A = rng.uniform(-1, 1, (P.tokens, n_in))
+    W = rng.uniform(-1, 1, (n_out, n_in)) / math.sqrt(n_in)
+    plan = make_factorized_stc_plan(ctx, input_level=4)
+    keys = factorized_stc_keygen(ctx, sk, plan, seed=75)
+    X5 = encrypt_slots_at(ctx, sk, A, level=5, seed=77, scale=plan.input_scale)
+    pp, rp, rk = make_mlwe_pcmm_plan(ctx, W), make_ring_pack_plan(ctx, n_out), ring_pack_keygen(ctx, sk, 79)
+    raise_to = list(P.moduli[2:])
+
+    def run():
+        Xc = slot_to_coeffs_factorized(ctx, plan, keys, lower_level(X5, 4))
+        Yp = pcmm_packed(ctx, pp, rp, rk, Xc)
+        return Xc, Yp, mod_raise(ctx, Yp, raise_to)
+
+    Xc, Yp, R = run()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    t = [0.0, 0.0, 0.0]
+    for _ in range(reps):
+        ev[0].record()
+        Xc = slot_to_coeffs_factorized(ctx, plan, keys, lower_level(X5, 4))
+        ev[1].record()
+        Yp = pcmm_packed(ctx, pp, rp, rk, Xc)
+        ev[2].record()
+        R = mod_raise(ctx, Yp, raise_to)
+        ev[3].record()
+        torch.cuda.synchronize()
+        for i in range(3):
+            t[i] += ev[i].elapsed_time(ev[i + 1]) / reps
+    e_stc = float(np.abs(ctx.decrypt_acts(sk, Xc) - A).max())
+    e_out = float(np.abs(ctx.decrypt_acts(sk, Yp) - clear_pcmm(W, A)).max())
+    n_ct = X5.n_ct
+    return {"workload": f"level-5 slot input ({n_ct} cts) -> lower to 4 -> factorized SlotToCoeffs (3 maps, "
+                        f"{plan.rotations} rotations / ct, {plan.plaintexts} plaintexts) -> PCMM {n_out}x{n_in}x128 -> "
+                        f"ring packing -> ModRaise to {len(raise_to)} primes, N = {P.N}, 1 GPU",
+            "ms_total": round(sum(t), 3), "ms_slot_to_coeffs": round(t[0], 3),
+            "ms_slot_to_coeffs_per_ct": round(t[0] / n_ct, 3), "ms_pcmm_packed": round(t[1], 3),
+            "ms_mod_raise": round(t[2], 3),
+            "precision_bits_slot_to_coeffs": round(-math.log2(e_stc), 1),
+            "precision_bits_output": round(-math.log2(e_out / float(np.abs(clear_pcmm(W, A)).max())), 1),
+            "levels": {"input": 5, "lowered": 4, "after_stc": Xc.level, "after_pcmm_pack": Yp.level,
+                       "raised_limbs": int(R.shape[1])}}
 
 
 def graph_ms(fn, reps=5):

@@ -339,6 +339,40 @@ he_status he_slot_pcmm_run_batch(const he_slot_pcmm_plan* plan, const uint32_t* 
                                  uint32_t* out_dev, void* workspace_dev, uint64_t workspace_bytes, void* stream,
                                  he_ledger* ledger);
 
+/* ---------------------------------------------------------------- the modulus chain above level 1
+ * ("lower the total level to 4; SlotToCoeffs to level 1").  A chain holds
+ * the primes q_0 .. q_L (q_0, q_1 = the context's) and the context's special prime P; a level-l ciphertext
+ * is [l + 1 limbs][2 (a, b)][N].  Lowering a level drops top limbs (no kernel: a view).  Slot linear maps
+ * consume one level each (BSGS, hybrid key switching with dnum = l + 1); the factorized SlotToCoeffs is three of
+ * them.  hesim has no counterpart; oracle: or_chain_* (oracle/he_oracle_chain.c). */
+typedef struct he_chain he_chain;
+typedef struct he_chain_map he_chain_map;
+he_status he_chain_create(const he_context* ctx, const uint32_t* primes, uint32_t count, he_chain** out);
+he_status he_chain_destroy(he_chain* chain);
+/* pt int64 [n_ct][N] -> ct [n_ct][level + 1][2][N] under s (the context's sampler; oracle or_encrypt) */
+he_status he_chain_encrypt(const he_chain* chain, const int32_t* s_dev, const int64_t* pt_dev, uint32_t n_ct,
+                           uint32_t level, uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream);
+/* key id of the rotation by `step` at `level` (the sampler's stream); words per rotation key at `level` */
+uint32_t he_chain_key_id(uint32_t level, uint32_t step);
+he_status he_chain_key_words(const he_chain* chain, uint32_t level, uint64_t* words);
+/* rotation keys sigma_{5^r}(s) -> s for `count` steps at `level`: u32 [count][l + 1][2][l + 2][N], NTT domain */
+he_status he_chain_rotation_keygen(const he_chain* chain, uint64_t seed, const int32_t* s_dev, uint32_t level,
+                                   const int32_t* steps, uint32_t count, uint32_t* keys_dev, void* stream);
+/* plaintexts int64 [count][N] -> NTT-domain residues [count][level + 1][N] */
+he_status he_chain_encode_pts(const he_chain* chain, const int64_t* pt_dev, uint32_t count, uint32_t level,
+                              uint32_t* pts_ntt_dev, void* stream);
+/* BSGS map at `level`: out = rescale(sum_j rot_{(j b - T) stride}(sum_i pt_{i + j b} rot_{i stride}(ct))), pts
+ * [b g][level + 1][N] (NTT domain, term i + j b pre-rotated by -(j b - T) stride).  Keys: baby [b - 1] for steps
+ * i stride, giant [g] for steps (j b - T) stride (the entry of a zero step is not read).  ledger: rotations,
+ * b g pc_mults and one rescale per ciphertext. */
+he_status he_chain_map_create(const he_chain* chain, const uint32_t* pts_ntt_dev, uint32_t level, uint32_t b,
+                              uint32_t g, uint32_t stride, uint32_t T, he_chain_map** out);
+he_status he_chain_map_destroy(he_chain_map* map);
+he_status he_chain_map_workspace_bytes(const he_chain_map* map, uint64_t* bytes);
+he_status he_chain_map_run(const he_chain_map* map, const uint32_t* ct_in_dev, uint32_t n_ct, uint32_t level,
+                           const uint32_t* keys_baby_dev, const uint32_t* keys_giant_dev, uint32_t* ct_out_dev,
+                           void* workspace_dev, uint64_t workspace_bytes, void* stream, he_ledger* ledger);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,7 @@ __all__ = [
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
     "decode_vector", "rhombus_pcmv", "rhombus_pcmv_w", "rhombus_combine", "rhombus_window", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
     "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe", "rotation_keys", "slot_pcmm",
-    "slot_bsgs", "rotation_keys_plain",
+    "slot_bsgs", "rotation_keys_plain", "chain_rotation_keys", "chain_bsgs", "chain_key_id",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -38,7 +38,7 @@ def stream_e(r: int) -> int:
 
 
 def build(force: bool = False) -> Path:
-    srcs = [_HERE / "he_oracle.c", _HERE / "he_oracle_rhombus.c", _HERE / "he_oracle_pcmv.c"]
+    srcs = [_HERE / "he_oracle.c", _HERE / "he_oracle_rhombus.c", _HERE / "he_oracle_pcmv.c", _HERE / "he_oracle_chain.c"]
     if force or not _SO.exists() or any(_SO.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
     return _SO
@@ -141,12 +141,12 @@ def decode_acts(params, phase: np.ndarray, n_cols: int) -> np.ndarray:
     return A
 
 
-def encrypt(params, seed: int, s: np.ndarray, pt: np.ndarray, r0: int = 0) -> np.ndarray:
-    """-> uint32 [n_ct, limbs=2, 2 (a, b), N]"""
+def encrypt(params, seed: int, s: np.ndarray, pt: np.ndarray, r0: int = 0, level: int = 1) -> np.ndarray:
+    """-> uint32 [n_ct, limbs = level + 1, 2 (a, b), N]"""
     pt = np.ascontiguousarray(pt, dtype=np.int64)
     n_ct = pt.shape[0]
-    ct = np.zeros((n_ct, 2, 2, params.N), dtype=np.uint32)
-    rc = lib().or_encrypt(seed, params.N, 2, _u32(_moduli(params)), _i32(np.ascontiguousarray(s)),
+    ct = np.zeros((n_ct, level + 1, 2, params.N), dtype=np.uint32)
+    rc = lib().or_encrypt(seed, params.N, level + 1, _u32(_moduli(params)), _i32(np.ascontiguousarray(s)),
                           _i64(pt), n_ct, r0, _u32(ct))
     if rc:
         raise RuntimeError("oracle encrypt failed")
@@ -297,7 +297,7 @@ def py_mlwe_components(params, a: list[int], q: int):
 def py_pcmm_rows(params, Wt, ct, rows):
     """Pure-Python MLWE PCMM for a few rows (toy sizes): returns rows x width words."""
     d, k, N = params.mlwe_degree, params.mlwe_rank, params.N
-    q0, q1 = params.moduli
+    q0, q1 = params.moduli[:2]
     n_ct = ct.shape[0]
     per_limb = []
     for limb, q in enumerate((q0, q1)):
@@ -691,4 +691,58 @@ def slot_bsgs(params, ct_in: np.ndarray, pts: np.ndarray, stride: int, b: int, g
         rc = _sd_bind().or_slot_bsgs(*args, _u32(out))
     if rc:
         raise ValueError("slot_bsgs: split x stride exceeds the slots")
+    return out
+
+
+# ---------------------------------------------------------------- modulus chain (he_oracle_chain.c)
+def _ch_bind():
+    L = lib()
+    if not getattr(L, "_ch_bound", False):
+        u32p, i32p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32)
+        u32, u64 = ctypes.c_uint32, ctypes.c_uint64
+        L.or_chain_key_id.restype = u32
+        L.or_chain_key_id.argtypes = [u32, u32]
+        L.or_chain_rotation_ksk.restype = None
+        L.or_chain_rotation_ksk.argtypes = [u64, u32, i32p, u32, u32p, u32, u32p]
+        L.or_chain_bsgs.restype = ctypes.c_int
+        L.or_chain_bsgs.argtypes = [u32, u32p, u32, u32, u32, u32, u32, u32p, u32p, u32p, u32p, u32p]
+        L._ch_bound = True
+    return L
+
+
+def _chain_mods(params, level: int) -> np.ndarray:
+    return np.ascontiguousarray(np.array(list(params.moduli[: level + 1]) + [params.special_prime], dtype=np.uint32))
+
+
+def chain_key_id(level: int, step: int) -> int:
+    return int(_ch_bind().or_chain_key_id(level, step))
+
+
+def chain_rotation_keys(params, seed: int, s: np.ndarray, steps, level: int) -> np.ndarray:
+    """[len(steps), l+1, 2, l+2, N] coefficient-form rotation keys at `level` (he_oracle_chain.c)."""
+    L = _ch_bind()
+    N, nq = params.N, level + 1
+    m = _chain_mods(params, level)
+    out = np.zeros((max(len(steps), 1), nq, 2, nq + 1, N), np.uint32)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    for t, r in enumerate(steps):
+        k = np.zeros((nq, 2, nq + 1, N), np.uint32)
+        L.or_chain_rotation_ksk(seed, int(r) % (N // 2), _i32(s), N, _u32(m), nq, _u32(k))
+        out[t] = k
+    return out
+
+
+def chain_bsgs(params, ct_in: np.ndarray, pts: np.ndarray, level: int, b: int, g: int, stride: int, T: int,
+               keys_baby: np.ndarray, keys_giant: np.ndarray) -> np.ndarray:
+    """One BSGS map at `level` (he_oracle_chain.c or_chain_bsgs): ct [l+1, 2, N] -> [l, 2, N]."""
+    L = _ch_bind()
+    N, nq = params.N, level + 1
+    m = _chain_mods(params, level)
+    out = np.zeros((nq - 1, 2, N), np.uint32)
+    rc = L.or_chain_bsgs(N, _u32(m), nq, b, g, stride, T, _u32(np.ascontiguousarray(ct_in, dtype=np.uint32)),
+                         _u32(np.ascontiguousarray(pts, dtype=np.uint32)),
+                         _u32(np.ascontiguousarray(keys_baby, dtype=np.uint32)),
+                         _u32(np.ascontiguousarray(keys_giant, dtype=np.uint32)), _u32(out))
+    if rc:
+        raise ValueError("or_chain_bsgs: bad level")
     return out

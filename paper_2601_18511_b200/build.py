@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libhe_b200.so"
-SOURCES = ["he_abi.cu", "he_modgemm.cu", "he_ntt.cu", "he_crypto.cu", "he_rhombus.cu", "he_spectral.cu"]
+SOURCES = ["he_abi.cu", "he_modgemm.cu", "he_ntt.cu", "he_crypto.cu", "he_rhombus.cu", "he_spectral.cu", "he_chain.cu"]
 HEADERS = ["he_common.cuh", "he_tc.cuh", "he_kernels.h", "he_internal.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -94,7 +94,7 @@ class _DeviceCtx:
         p = native.HeParamsC()
         p.mlwe_degree = params.mlwe_degree
         p.mlwe_rank = params.mlwe_rank
-        p.moduli[0], p.moduli[1] = params.moduli
+        p.moduli[0], p.moduli[1] = params.moduli[:2]
         p.log_delta = params.log_delta
         p.rhombus_degree = params.rhombus_degree
         p.special_prime = params.special_prime

@@ -36,7 +36,9 @@ EXPORTS = (
     "he_slot_lt_plan_create", "he_slot_bsgs_plan_create", "he_slot_bsgs_plan_create_ext", "he_slot_pcmm_encode_pts_ext", "he_slot_rotation_keygen_plain",
     "he_encrypt_vector_w", "he_rhombus_weight_bytes_w", "he_rhombus_encode_weights_w", "he_rhombus_plan_create_w",
     "he_rhombus_plan_info", "he_rhombus_run_subtree", "he_rhombus_finish", "he_context_set_rng_key",
-    "he_chacha20_block",
+    "he_chacha20_block", "he_chain_create", "he_chain_destroy", "he_chain_encrypt", "he_chain_key_id",
+    "he_chain_key_words", "he_chain_rotation_keygen", "he_chain_encode_pts", "he_chain_map_create",
+    "he_chain_map_destroy", "he_chain_map_workspace_bytes", "he_chain_map_run",
 )
 
 
@@ -124,6 +126,17 @@ def lib():
             "he_slot_pcmm_run_batch": (st, [vp, vp, u32, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_context_set_rng_key": (st, [vp, ctypes.c_char_p]),
             "he_chacha20_block": (st, [ctypes.c_char_p, u32, ctypes.c_char_p, ctypes.c_char_p]),
+            "he_chain_create": (st, [vp, vp, u32, ctypes.POINTER(vp)]),
+            "he_chain_destroy": (st, [vp]),
+            "he_chain_encrypt": (st, [vp, vp, vp, u32, u32, u64, u32, vp, vp]),
+            "he_chain_key_id": (u32, [u32, u32]),
+            "he_chain_key_words": (st, [vp, u32, ctypes.POINTER(u64)]),
+            "he_chain_rotation_keygen": (st, [vp, u64, vp, u32, vp, u32, vp, vp]),
+            "he_chain_encode_pts": (st, [vp, vp, u32, u32, vp, vp]),
+            "he_chain_map_create": (st, [vp, vp, u32, u32, u32, u32, u32, ctypes.POINTER(vp)]),
+            "he_chain_map_destroy": (st, [vp]),
+            "he_chain_map_workspace_bytes": (st, [vp, ctypes.POINTER(u64)]),
+            "he_chain_map_run": (st, [vp, vp, u32, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(HeLedgerC)]),
             "he_encrypt_vector_w": (st, [vp, vp, vp, u32, u32, u64, u32, vp, vp]),
             "he_rhombus_weight_bytes_w": (st, [vp, u32, u32, u32, u32, ctypes.POINTER(u64)]),
             "he_rhombus_encode_weights_w": (st, [vp, vp, u32, u32, u32, u32, u32, vp, vp]),

@@ -17,6 +17,11 @@ Prime choice (the paper does not pin it; SURVEY.md §7 "Choosing Delta_w"):
        bits of weight precision for Llama-scale weights (|W| < 2^-6), above the
        paper's 12-bit target, and needs 3 ciphertext digits.
 Both are NTT-friendly: q = 1 mod 2N.
+
+Chain: moduli[2:] are the primes of the levels above the PCMM's
+level 1 -- "lower the total level to 4; SlotToCoeffs to level 1": the factorized SlotToCoeffs consumes
+q_4, q_3, q_2 (three slot linear maps, one level each) and hands the PCMM its (q_0, q_1) input.  The
+kernels of the PCMM / PCMv / ring packing use q_0, q_1 and P only; he_chain.cu runs the levels above.
 """
 
 from __future__ import annotations
@@ -95,8 +100,8 @@ class HeParams:
             if v < 2 or v & (v - 1):
                 raise ValueError(f"{what} must be a power of two >= 2, got {v}")
         object.__setattr__(self, "moduli", tuple(int(q) for q in self.moduli))
-        if len(self.moduli) != 2:
-            raise ValueError("the PCMM path runs at level 1: exactly two moduli (q0, q1)")
+        if not 2 <= len(self.moduli) <= 7:
+            raise ValueError("moduli: (q0, q1) for the PCMM's level 1, plus up to 5 chain primes above it")
         for q in self.moduli:
             if not is_prime(q):
                 raise ValueError(f"modulus {q} is not prime")
@@ -193,6 +198,27 @@ class HeParams:
         kw.setdefault("moduli", tuple(pr[:2]))
         kw.setdefault("special_prime", pr[2])
         kw.setdefault("name", "wide")
+        return cls(**kw)
+
+    @classmethod
+    def llama_chain(cls, levels: int = 3, **kw) -> "HeParams":
+        """The llama preset plus `levels` ~30-bit primes above q1 (default 3: input at level 4, the factorized
+        SlotToCoeffs consumes three levels and outputs the PCMM's level-1 input)."""
+        base = cls.llama()
+        extra = [p for p in ntt_primes(2 * base.N, 1 << 30, levels + 4) if p not in (*base.moduli, base.special_prime)]
+        kw.setdefault("moduli", tuple(base.moduli) + tuple(extra[:levels]))
+        kw.setdefault("name", "llama_chain")
+        return cls(**kw)
+
+    @classmethod
+    def toy_chain(cls, levels: int = 3, **kw) -> "HeParams":
+        """The toy ring (N = 512) with `levels` chain primes above q1."""
+        base = cls.toy()
+        extra = [p for p in ntt_primes(2 * base.N, 1 << 30, levels + 4) if p not in (*base.moduli, base.special_prime)]
+        kw.setdefault("moduli", tuple(base.moduli) + tuple(extra[:levels]))
+        for k in ("mlwe_degree", "mlwe_rank", "special_prime", "rhombus_degree"):
+            kw.setdefault(k, getattr(base, k))
+        kw.setdefault("name", "toy_chain")
         return cls(**kw)
 
     @classmethod
