@@ -484,12 +484,12 @@ def side_measurements(P, dev):
                                            "(decompose KS -> MVM + PackLWEs -> rescale/compose), 1 GPU", **rh}
         hbm = measured_hbm()
         ntt = {}
-        for n, batch in ((65536, 256), (4096, 4096)):
+        for n, batch in ((65536, 1024), (4096, 16384)):   # 268 MB per batch: larger than L2, streamed from HBM
             q = P.moduli[0]
             xt = torch.randint(0, q, (batch, n), dtype=torch.int64, device=dev).to(torch.int32)
             st = ctx.stream()
             for name in ("he_ntt_forward", "he_ntt_inverse"):
-                for _ in range(3):
+                for _ in range(50):
                     native.call(name, ctx.handle, xt.data_ptr(), n, 0, batch, n, st)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()

@@ -251,8 +251,8 @@ HE_D constexpr uint32_t poff(int e) {
 
 // forward: rounds of 4 stages, T = N2/16, N2/256, ..., 1; first round straight from global.  NP transforms
 // (polys blockIdx.y * NP .. + NP - 1 of the batch, block b of each) per CTA share every twiddle load.
-template <int N2, int NP>
-__global__ void __launch_bounds__(N2 / 16) ntt_fwd_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
+template <int N2, int NP, int MINB = 1>
+__global__ void __launch_bounds__(N2 / 16, MINB) ntt_fwd_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
                                                         const uint2* __restrict__ tw, uint32_t q, int final_reduce) {
   __shared__ uint32_t s[NP][N2 + N2 / 32];
   const uint32_t b = blockIdx.x;
@@ -298,12 +298,13 @@ __global__ void __launch_bounds__(N2 / 16) ntt_fwd_rows(uint32_t* __restrict__ d
 #pragma unroll
         for (int e = 0; e < 16; ++e) x[p][e] = s[p][pad(j0) + poff<T>(e)];
       ct_round16<NP>(x, tw, n / (16 * T), b * (N2 / (16 * T)) + tau / T, q2, q);
-      __syncthreads();
+      // rounds 2 -> 3 exchange within the 256-word sub-block of this half-warp: no CTA barrier
+      __syncwarp();
 #pragma unroll
       for (int p = 0; p < NP; ++p)
 #pragma unroll
         for (int e = 0; e < 16; ++e) s[p][pad(j0) + poff<T>(e)] = x[p][e];
-      __syncthreads();
+      __syncwarp();
     }
     {
 #pragma unroll
@@ -327,8 +328,8 @@ __global__ void __launch_bounds__(N2 / 16) ntt_fwd_rows(uint32_t* __restrict__ d
 
 // inverse: rounds of 4 stages, T = 1, 16, 256, ...; first round straight from global (16 contiguous words),
 // last round straight to global (coalesced), optional n^-1 scaling
-template <int N2, int NP>
-__global__ void __launch_bounds__(N2 / 16) ntt_inv_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
+template <int N2, int NP, int MINB = 1>
+__global__ void __launch_bounds__(N2 / 16, MINB) ntt_inv_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
                                                         const uint2* __restrict__ tw, uint32_t q, uint32_t ninv,
                                                         uint32_t ninvp, int do_scale) {
   __shared__ uint32_t s[NP][N2 + N2 / 32];
@@ -358,7 +359,8 @@ __global__ void __launch_bounds__(N2 / 16) ntt_inv_rows(uint32_t* __restrict__ d
       for (int p = 0; p < NP; ++p)
 #pragma unroll
         for (int e = 0; e < 16; ++e) s[p][pad(16 * tau) + e] = x[p][e];
-      __syncthreads();
+      if constexpr (N2 == 4096) __syncwarp();   // rounds 1 -> 2 stay inside the half-warp's 256-word sub-block
+      else __syncthreads();
     }
     if constexpr (N2 == 4096) {
       constexpr int T = 16;
@@ -442,8 +444,11 @@ cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint6
   return with_n2(n2, [&](auto N2) {
     constexpr int K = decltype(N2)::value;
     if (count / 2) {
+      // 4096-point blocks: compiled for 4 resident CTAs per SM (<= 64 registers, 32 warps); measured against
+      // 3 / 5 CTAs and one poly per CTA at 6 / 7
       dim3 g(n1, count / 2);
-      ntt_fwd_rows<K, 2><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, 1);
+      if constexpr (K == 4096) ntt_fwd_rows<K, 2, 4><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, 1);
+      else ntt_fwd_rows<K, 2><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, 1);
     }
     if (count & 1) {
       dim3 g(n1, 1);
@@ -461,8 +466,11 @@ cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint6
   cudaError_t e = with_n2(n2, [&](auto N2) {
     constexpr int K = decltype(N2)::value;
     if (count / 2) {
+      // 4096-point blocks: compiled for 4 resident CTAs per SM (<= 64 registers, 32 warps); measured against
+      // 3 / 5 CTAs and one poly per CTA at 6 / 7
       dim3 g(n1, count / 2);
-      ntt_inv_rows<K, 2><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv, t.ninvp, n1 == 1);
+      if constexpr (K == 4096) ntt_inv_rows<K, 2, 4><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv, t.ninvp, n1 == 1);
+      else ntt_inv_rows<K, 2><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv, t.ninvp, n1 == 1);
     }
     if (count & 1) {
       dim3 g(n1, 1);
