@@ -513,11 +513,24 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
 //   round 1: lane l holds positions 32 l + e: DIT stages len = 1 .. 16 in registers (lane-uniform twiddles);
 //   round 2: lane l holds l + 32 e: stages len = 32 .. 512 in registers (per-stage lane tables); the last
 //            stage forms only the outputs u < 768.
-// 8 blocks per CTA, both limbs in smem (pitch 1060 = 4 mod 8, pad(p) = p + p/32: conflict-free transposing
-// stores and round accesses); a' rows of 3 x 8 positions are written as 96-byte segments.
+// 8 blocks per CTA, both limbs in smem (pitch 1148 = 4 mod 8, position p at pin36(p): conflict-free transposing
+// stores, 16-byte round-1 loads/stores); a' rows of 3 x 8 positions are written as 96-byte segments.
 constexpr int kInv1kBlocks = 8;
-constexpr int kInv1kLd = 1060;
-HE_D uint32_t pad32(uint32_t p) { return p + (p >> 5); }
+constexpr int kInv1kLd = 1148;   // pin36(1023) + 1, = 4 mod 8
+// position p at p + 4 (p / 32): rows of 32 positions at pitch 36 words, so a lane's 32 round-1 positions are
+// 16-byte aligned (8 x LDS/STS.128, conflict-free per quarter-warp) and the round-2 reads p = l + 32 e hit 32 banks
+HE_D uint32_t pin36(uint32_t p) { return p + 4 * (p >> 5); }
+HE_D void ld_row32(const uint32_t* c, uint32_t (&x)[32]) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const uint4 w = reinterpret_cast<const uint4*>(c)[v];
+    x[4 * v] = w.x, x[4 * v + 1] = w.y, x[4 * v + 2] = w.z, x[4 * v + 3] = w.w;
+  }
+}
+HE_D void st_row32(uint32_t* c, const uint32_t (&x)[32]) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) reinterpret_cast<uint4*>(c)[v] = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+}
 // -> x[l][e] = INTT value u = lane + 32 e of limb l for e < 24, reduced to [0, q); both limbs in lockstep
 struct Inv1kLimb {
   uint32_t* col;
@@ -526,9 +539,7 @@ struct Inv1kLimb {
 };
 HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_t lane, uint32_t (&x)[2][32]) {
 #pragma unroll
-  for (int l = 0; l < 2; ++l)
-#pragma unroll
-    for (int e = 0; e < 32; ++e) x[l][e] = L[l].col[33 * lane + e];
+  for (int l = 0; l < 2; ++l) ld_row32(L[l].col + 36 * lane, x[l]);
 #pragma unroll
   for (int e = 0; e < 32; e += 2)
 #pragma unroll
@@ -548,14 +559,12 @@ HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_
     }
   }
 #pragma unroll
-  for (int l = 0; l < 2; ++l)
-#pragma unroll
-    for (int e = 0; e < 32; ++e) L[l].col[33 * lane + e] = x[l][e];
+  for (int l = 0; l < 2; ++l) st_row32(L[l].col + 36 * lane, x[l]);
   __syncwarp();
 #pragma unroll
   for (int l = 0; l < 2; ++l)
 #pragma unroll
-    for (int e = 0; e < 32; ++e) x[l][e] = L[l].col[lane + 33 * e];
+    for (int e = 0; e < 32; ++e) x[l][e] = L[l].col[lane + 36 * e];
   __syncwarp();
 #pragma unroll
   for (int s = 5; s < 9; ++s) {
@@ -623,7 +632,7 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
     }
 #pragma unroll
     for (uint32_t it = 0; it < 8; ++it) {
-      const uint32_t o = 4 * bq * kInv1kLd + pad32(warp * 16 + ps + 128 * it);
+      const uint32_t o = 4 * bq * kInv1kLd + pin36(warp * 16 + ps + 128 * it);
       xs0[o] = v0[it].x; xs0[o + kInv1kLd] = v0[it].y; xs0[o + 2 * kInv1kLd] = v0[it].z; xs0[o + 3 * kInv1kLd] = v0[it].w;
       xs1[o] = v1[it].x; xs1[o + kInv1kLd] = v1[it].y; xs1[o + 2 * kInv1kLd] = v1[it].z; xs1[o + 3 * kInv1kLd] = v1[it].w;
     }
