@@ -71,6 +71,23 @@ def test_fixture_parity_baseline_config1():
 ALGOS = ["spectral", "direct"]
 
 
+def test_llama_ring_keygen_and_encryption_every_word():
+    """N = 2^16: the device secret and every word of a fresh 4-ciphertext encryption (both limbs, a and b)
+    equal the oracle's keygen / Ecd_coeff / or_encrypt on the same seeds (the words every Llama-shape PCMM
+    check starts from)."""
+    P = HeParams.llama()
+    ctx = HeContext(P, rng="seeded")
+    rng = np.random.default_rng(5)
+    A = rng.uniform(-1, 1, (P.tokens, 4 * P.mlwe_rank))
+    sk = ctx.keygen(7)
+    s = O.keygen(P, 7)
+    assert np.array_equal(sk.s.cpu().numpy(), s)
+    X = ctx.encrypt_acts(sk, A, seed=11)
+    ct = O.encrypt(P, 11, s, O.encode_acts(P, A))
+    assert ct.shape == tuple(X.data.shape)
+    assert np.array_equal(u32(X.data), ct)
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("n_out,n_in", [(16, 16), (48, 32), (256, 384), (128, 1024)])
 def test_toy_all_words_bit_exact(n_out, n_in, algo):
