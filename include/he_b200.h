@@ -352,6 +352,10 @@ he_status he_chain_destroy(he_chain* chain);
 /* pt int64 [n_ct][N] -> ct [n_ct][level + 1][2][N] under s (the context's sampler; oracle or_encrypt) */
 he_status he_chain_encrypt(const he_chain* chain, const int32_t* s_dev, const int64_t* pt_dev, uint32_t n_ct,
                            uint32_t level, uint64_t seed, uint32_t r0, uint32_t* ct_dev, void* stream);
+/* phase of ct [n_ct][level + 1][2][N] in limb `limb`, centred int64 [n_ct][N] (CRT over the limbs = the integer
+ * phase, e.g. m + q0 I(X) after he_mod_raise into the chain; test/inspection entry point, oracle or_decrypt_rlwe) */
+he_status he_chain_decrypt(const he_chain* chain, const int32_t* s_dev, const uint32_t* ct_dev, uint32_t n_ct,
+                           uint32_t level, uint32_t limb, int64_t* phase_dev, void* stream);
 /* key id of the rotation by `step` at `level` (the sampler's stream); words per rotation key at `level` */
 uint32_t he_chain_key_id(uint32_t level, uint32_t step);
 he_status he_chain_key_words(const he_chain* chain, uint32_t level, uint64_t* words);

@@ -84,6 +84,45 @@ def encrypt_slots_at(ctx: HeContext, sk: SecretKey, acts, level: int | None = No
     return SlotBlocks(out, level=level, n_cols=int(np.asarray(acts).shape[1]), scale=sc)
 
 
+def encrypt_coeffs_at(ctx: HeContext, sk: SecretKey, pt, level: int | None = None, seed: int | None = None,
+                      r0: int = 0) -> CtBlocks:
+    """Encrypt int64 coefficient plaintexts [n_ct, N] (e.g. or_encode_acts of an activation block) at `level`."""
+    torch = _torch()
+    p = ctx.params
+    level = p.top_level if level is None else int(level)
+    if not 0 <= level <= p.top_level:
+        raise ValueError(f"level {level} outside [0, {p.top_level}]")
+    pt = torch.as_tensor(np.asarray(pt, dtype=np.int64)).reshape(-1, p.N).to(ctx.device)
+    out = torch.empty((pt.shape[0], level + 1, 2, p.N), dtype=torch.int32, device=ctx.device)
+    native.call("he_chain_encrypt", chain_of(ctx).handle, sk.s.data_ptr(), pt.data_ptr(), pt.shape[0], level,
+                ctx.nonce(seed), r0, out.data_ptr(), ctx.stream())
+    return CtBlocks(out, level=level, n_cols=0)
+
+
+def decrypt_exact(ctx: HeContext, sk: SecretKey, data) -> np.ndarray:
+    """The integer phase b + a s of chain ciphertexts [n_ct, level + 1, 2, N] by CRT over all their limbs
+    (object array of Python ints, centred mod Q_level): e.g. m + q0 I(X) after ModRaise."""
+    torch = _torch()
+    p = ctx.params
+    n_ct, nl = int(data.shape[0]), int(data.shape[1])
+    ch = chain_of(ctx)
+    res = []
+    for j in range(nl):
+        ph = torch.empty((n_ct, p.N), dtype=torch.int64, device=ctx.device)
+        native.call("he_chain_decrypt", ch.handle, sk.s.data_ptr(), data.data_ptr(), n_ct, nl - 1, j, ph.data_ptr(),
+                    ctx.stream())
+        res.append(ph.cpu().numpy().astype(object))
+    Q = 1
+    for q in p.moduli[:nl]:
+        Q *= q
+    acc = np.zeros_like(res[0])
+    for j, q in enumerate(p.moduli[:nl]):
+        Qj = Q // q
+        acc = acc + res[j] % q * Qj * pow(Qj, -1, q)
+    acc = acc % Q
+    return np.where(acc > Q // 2, acc - Q, acc)
+
+
 def lower_level(X, level: int):
     """Drop the limbs above `level` (a ciphertext mod Q_L is one mod every divisor Q_l: no noise, no kernel)."""
     if not getattr(X, "is_ct", False):
@@ -111,6 +150,28 @@ def special_fft_layers(N: int) -> list[dict]:
         _merge(D, 0, np.where(first, 1.0, -w), n)
         _merge(D, h, np.where(first, w, 0.0), n)
         _merge(D, -h, np.where(first, 0.0, 1.0), n)
+        out.append(D)
+        ln *= 2
+    return out
+
+
+def special_ifft_layers(N: int) -> list[dict]:
+    """The inverses of special_fft_layers' L_1 .. L_log n (same index): (x, y) at (p, p + len/2) ->
+    ((x + y) / 2, (x - y) / (2 w_p)) -- three diagonals again, entries of modulus 1/2."""
+    n = N // 2
+    e = slots.slot_exponents(N)
+    x = np.arange(n)
+    out = []
+    ln = 2
+    while ln <= n:
+        h = ln // 2
+        jj = x % ln
+        first = jj < h
+        w = np.exp(1j * np.pi * (e[jj % h] % (4 * ln)) / (2 * ln))
+        D: dict = {}
+        _merge(D, 0, np.where(first, 0.5, -0.5 / w), n)
+        _merge(D, h, np.where(first, 0.5, 0.0), n)
+        _merge(D, -h, np.where(first, 0.0, 0.5 / w), n)
         out.append(D)
         ln *= 2
     return out
@@ -158,6 +219,31 @@ def stc_factors(N: int, levels: int = 3) -> list[dict]:
             count = 2 * T + 1
         out.append({"diags": G, "stride": stride, "T": T, "count": count})
         k += sz
+    return out
+
+
+def cts_factors(N: int, levels: int = 3) -> list[dict]:
+    """CoeffToSlots = M^-1 = L_1^-1 ... L_log n^-1 as `levels` maps in application order: the layer groups of
+    stc_factors taken last group first, each G_g^-1 = L_k^-1 ... L_(k + sz - 1)^-1 (same offsets, stride, T)."""
+    n = N // 2
+    Li = special_ifft_layers(N)
+    groups, k = [], 0
+    for sz in layer_groups(n.bit_length() - 1, levels):
+        groups.append((k, sz))
+        k += sz
+    out = []
+    for k, sz in reversed(groups):
+        G = Li[k + sz - 1]
+        for lay in reversed(Li[k:k + sz - 1]):
+            G = compose(lay, G, n)
+        stride = 1 << k
+        span = n // stride
+        T = (1 << sz) - 1
+        if 2 * T + 1 > span:
+            T, count = 0, span
+        else:
+            count = 2 * T + 1
+        out.append({"diags": G, "stride": stride, "T": T, "count": count})
     return out
 
 
@@ -231,6 +317,7 @@ class FactorizedStcPlan:
     input_scale: float
     shifts: tuple
     _chain: object = field(default=None, repr=False)
+    pre_log2: int = 0                    # CoeffToSlots: the input is multiplied by 2^pre_log2 first
 
     @property
     def rotations(self) -> int:
@@ -255,18 +342,55 @@ def make_factorized_stc_plan(ctx: HeContext, levels: int = 3, shifts=None,
     """The `levels` maps of the factorized SlotToCoeffs as chain BSGS plans (default: three, input at level 4 ->
     output at level 1, the PCMM's input level); map k's plaintexts at q_k / 2^shifts[k] (default 6 each),
     input slots at plan.input_scale = Delta 2^sum(shifts)."""
+    return _factorized_plan(ctx, stc_factors, levels, (6,) * levels if shifts is None else shifts, input_level)
+
+
+def make_factorized_cts_plan(ctx: HeContext, levels: int = 3, shifts=None, input_level: int | None = None,
+                             pre_log2: int = 0) -> FactorizedStcPlan:
+    """CoeffToSlots, the linear first half of the Half-Bootstrap after ModRaise: the inverse of the
+    factorized SlotToCoeffs, M^-1 as `levels` chain maps (default: input at the top level).  A ciphertext whose
+    phase has coefficients p_c comes out with slot s = (p_(bitReverse(s)) + i p_(N/2 + bitReverse(s))) times
+    2^(pre_log2 - sum(shifts)) (SlotBlocks.scale): the input is multiplied by the integer 2^pre_log2 (no level) and
+    map k's plaintexts are encoded at q_k 2^-shifts[k].
+
+    Precision (measured at N = 2^16 on a ModRaised ciphertext, tools/cts_precision.py): the plaintext rounding of
+    every map, ~2^-23.7 of an entry at scale q_k ~ 2^30 acting on slot values up to sqrt(N/2) |p| wide, dominates
+    the key-switching noise until the shifts reach ~-10 each; past that the key-switching noise (absolute, ~2^20 in
+    the slots) is what is left and the integer pre-multiplication lifts the signal over it.  The output -- |p| ~
+    q0 |I| ~ 2^38 after ModRaise, times the total scale-up T -- has to stay inside the output modulus (output
+    coefficients measured at 2^(30.3 + T)).  Default: T = log2 Q_out - 33.5; below 40 all of it as shifts (output
+    level 1, q0 q1 ~ 2^50: T = 16, shifts (-6, -5, -5), 2^-16.4 q0), else pre_log2 8 and shifts of -12 (output
+    level 2 on llama_chain(4): 2^-22.9 q0)."""
+    p = ctx.params
+    input_level = p.top_level if input_level is None else int(input_level)
+    if shifts is None:
+        out_level = input_level - levels
+        qlog = sum(np.log2(float(q)) for q in p.moduli[:max(out_level, 0) + 1])
+        T = max(int(np.floor(qlog - 33.5)), 0)
+        if T >= 40 and pre_log2 == 0:
+            pre_log2, T = 8, T - 8
+        T = min(T, 12 * levels)
+        shifts = tuple(-(T // levels + (1 if i < T % levels else 0)) for i in range(levels))
+    plan = _factorized_plan(ctx, cts_factors, levels, shifts, input_level)
+    if not 0 <= int(pre_log2) <= 31:
+        raise ValueError("pre_log2 must be in [0, 31]")
+    plan.pre_log2 = int(pre_log2)
+    return plan
+
+
+def _factorized_plan(ctx, factors, levels, shifts, input_level) -> FactorizedStcPlan:
     torch = _torch()
     p = ctx.params
-    shifts = tuple(int(v) for v in (shifts if shifts is not None else (6,) * levels))
-    if len(shifts) != levels or min(shifts) < 0 or max(shifts) > 20:
-        raise ValueError(f"need {levels} shifts in [0, 20], got {shifts}")
+    shifts = tuple(int(v) for v in shifts)
+    if len(shifts) != levels or min(shifts) < -20 or max(shifts) > 20:
+        raise ValueError(f"need {levels} shifts in [-20, 20], got {shifts}")
     input_level = levels + 1 if input_level is None else int(input_level)
     if input_level > p.top_level or input_level - levels < 0:
         raise ValueError(f"{levels} maps from level {input_level} do not fit the chain (top level {p.top_level})")
     ch = chain_of(ctx)
     N, n = p.N, p.N // 2
     maps = []
-    for k, f in enumerate(stc_factors(N, levels)):
+    for k, f in enumerate(factors(N, levels)):
         level = input_level - k
         scale = float(p.moduli[level]) / 2.0 ** shifts[k]
         b, g = bsgs_shape(f["count"])
@@ -333,6 +457,40 @@ def chain_map(ctx: HeContext, m: ChainMap, keys: ChainMapKeys, data, level: int)
     ctx.ledger.add_c(led)
     ctx.ledger.observe_level(level - 1)
     return out
+
+
+def coeffs_to_slots_factorized(ctx: HeContext, plan: FactorizedStcPlan, keys: list, X) -> SlotBlocks:
+    """Coefficient-encoded ciphertexts at plan.input_level (CtBlocks, or the raw [n_ct, level + 1, 2, N] tensor
+    mod_raise returns) -> SlotBlocks at plan.output_level holding the coefficient pairs in the slots."""
+    data = getattr(X, "data", X)
+    level = getattr(X, "level", None)
+    if level is None:
+        if not hasattr(data, "shape") or len(data.shape) != 4:
+            raise TypeError("coeffs_to_slots takes CtBlocks or a [n_ct, level + 1, 2, N] ciphertext tensor")
+        level = int(data.shape[1]) - 1
+    if isinstance(X, SlotBlocks):
+        raise TypeError("coeffs_to_slots consumes coefficient-encoded ciphertexts, not SlotBlocks")
+    if level < len(plan.maps):
+        raise NeedsBootstrapError(f"the factorized CoeffToSlots needs {len(plan.maps)} levels, operand has {level}")
+    if level != plan.input_level:
+        raise ValueError(f"plan expects level {plan.input_level}, operand is at level {level}: lower it first")
+    if len(keys) != len(plan.maps):
+        raise ValueError("one key set per map")
+    if plan.pre_log2:
+        data = mul_pow2(ctx, data, plan.pre_log2)
+    for m, k in zip(plan.maps, keys):
+        data = chain_map(ctx, m, k, data, level)
+        level -= 1
+    return SlotBlocks(data, level=level, n_cols=getattr(X, "n_cols", 0),
+                      scale=2.0 ** (plan.pre_log2 - sum(plan.shifts)), layout="coeff_pairs")
+
+
+def mul_pow2(ctx: HeContext, data, e: int):
+    """Chain ciphertexts [n_ct, l + 1, 2, N] times the integer 2^e, limb by limb (no level consumed)."""
+    torch = _torch()
+    nl = int(data.shape[1])
+    q = torch.tensor(ctx.params.moduli[:nl], dtype=torch.int64, device=data.device).view(1, nl, 1, 1)
+    return (((data.to(torch.int64) & 0xFFFFFFFF) << e) % q).to(torch.int32)
 
 
 def slot_to_coeffs_factorized(ctx: HeContext, plan: FactorizedStcPlan, keys: list, X: SlotBlocks) -> CtBlocks:

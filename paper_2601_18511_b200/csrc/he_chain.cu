@@ -280,6 +280,21 @@ __global__ void k_ch_reduce_pts(const int64_t* __restrict__ pt, uint64_t count, 
   }
 }
 
+// decryption of one limb: a [ct][N] (copied out of the ct) -> a * s (NTT domain, in place)
+__global__ void k_ch_dec_mul(uint32_t* a, uint32_t n_ct, uint32_t N, const uint32_t* s_ntt, uint64_t mu, uint32_t q) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < (uint64_t)n_ct * N; x += (uint64_t)gridDim.x * blockDim.x)
+    a[x] = ch_mulmod(a[x], s_ntt[x % N], mu, q);
+}
+// phase [ct][N] = [b + a s]_q centred
+__global__ void k_ch_dec_phase(const uint32_t* __restrict__ ct, uint64_t cstride, const uint32_t* __restrict__ as,
+                               uint32_t n_ct, uint32_t N, uint32_t q, int64_t* __restrict__ phase) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < (uint64_t)n_ct * N; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = x / N, c = x % N;
+    const uint32_t v = add_mod(ct[r * cstride + N + c], as[x], q);
+    phase[x] = v > q / 2 ? (int64_t)v - q : (int64_t)v;
+  }
+}
+
 }  // namespace
 
 // ======================================================================== chain object / C ABI
@@ -383,6 +398,43 @@ extern "C" he_status he_chain_encrypt(const he_chain* c, const int32_t* s_dev, c
   k_ch_finish<<<dim3((N + 1023) / 1024, n_ct), 256, 0, st>>>(c->ctx->R.rng, pt_dev, seed, r0, N, M, ct_dev);
   cudaFreeAsync(s_ntt, st);
   HE_CUDA(cudaGetLastError(), "chain encrypt");
+  return HE_OK;
+}
+
+// phase of chain ciphertexts [n_ct][level + 1][2][N] in one limb, centred mod that prime (CRT over the limbs
+// gives the integer phase, e.g. m + q0 I(X) after ModRaise)
+extern "C" he_status he_chain_decrypt(const he_chain* c, const int32_t* s_dev, const uint32_t* ct_dev, uint32_t n_ct,
+                                      uint32_t level, uint32_t limb, int64_t* phase_dev, void* stream) {
+  if (!c || !s_dev || !ct_dev || !phase_dev) return fail(HE_EINVAL, "null argument");
+  if (level >= c->count || limb > level) return fail(HE_EINVAL, "limb %u / level %u outside the chain", limb, level);
+  if (n_ct == 0) return fail(HE_EINVAL, "empty batch");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t N = c->N, q = c->primes[limb];
+  const uint64_t cstride = (uint64_t)(level + 1) * 2 * N;
+  ChMods M{};
+  M.nq = 1;
+  M.m[0] = q;
+  M.mu[0] = (uint64_t)(((unsigned __int128)1 << 64) / q);
+  uint32_t *sj = nullptr, *tmp = nullptr;
+  HE_CUDA(cudaMallocAsync(&sj, (size_t)N * sizeof(uint32_t), st), "alloc");
+  HE_CUDA(cudaMallocAsync(&tmp, (size_t)n_ct * N * sizeof(uint32_t), st), "alloc");
+  k_ch_reduce_secret<<<ch_grid(N), 256, 0, st>>>(s_dev, N, M, 1, sj);
+  cudaError_t e = ntt_forward(c->ntt[limb], sj, 1, N, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(tmp, N * sizeof(uint32_t), ct_dev + (size_t)limb * 2 * N, cstride * sizeof(uint32_t),
+                          N * sizeof(uint32_t), n_ct, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = ntt_forward(c->ntt[limb], tmp, n_ct, N, st);
+  if (e == cudaSuccess) {
+    k_ch_dec_mul<<<ch_grid((uint64_t)n_ct * N), 256, 0, st>>>(tmp, n_ct, N, sj, M.mu[0], q);
+    e = ntt_inverse(c->ntt[limb], tmp, n_ct, N, st);
+  }
+  if (e == cudaSuccess)
+    k_ch_dec_phase<<<ch_grid((uint64_t)n_ct * N), 256, 0, st>>>(ct_dev + (size_t)limb * 2 * N, cstride, tmp, n_ct, N, q,
+                                                                 phase_dev);
+  cudaFreeAsync(sj, st);
+  cudaFreeAsync(tmp, st);
+  if (e != cudaSuccess) return cuda_fail(e, "chain decrypt");
+  HE_CUDA(cudaGetLastError(), "chain decrypt");
   return HE_OK;
 }
 

@@ -38,7 +38,7 @@ EXPORTS = (
     "he_rhombus_plan_info", "he_rhombus_run_subtree", "he_rhombus_finish", "he_context_set_rng_key",
     "he_chacha20_block", "he_chain_create", "he_chain_destroy", "he_chain_encrypt", "he_chain_key_id",
     "he_chain_key_words", "he_chain_rotation_keygen", "he_chain_encode_pts", "he_chain_map_create",
-    "he_chain_map_destroy", "he_chain_map_workspace_bytes", "he_chain_map_run",
+    "he_chain_map_destroy", "he_chain_map_workspace_bytes", "he_chain_map_run", "he_chain_decrypt",
 )
 
 
@@ -129,6 +129,7 @@ def lib():
             "he_chain_create": (st, [vp, vp, u32, ctypes.POINTER(vp)]),
             "he_chain_destroy": (st, [vp]),
             "he_chain_encrypt": (st, [vp, vp, vp, u32, u32, u64, u32, vp, vp]),
+            "he_chain_decrypt": (st, [vp, vp, vp, u32, u32, u32, vp, vp]),
             "he_chain_key_id": (u32, [u32, u32]),
             "he_chain_key_words": (st, [vp, u32, ctypes.POINTER(u64)]),
             "he_chain_rotation_keygen": (st, [vp, u64, vp, u32, vp, u32, vp, vp]),

@@ -88,3 +88,24 @@ def test_oracle_factorized_stc_toy():
     want = O.encode_acts(P, A)[0]
     err = np.abs(ph - want).max() / P.delta
     assert err < 2 ** -14, err
+
+
+@pytest.mark.parametrize("N,levels", [(512, 3), (4096, 3), (65536, 3), (4096, 2)])
+def test_cts_maps_invert_the_stc_maps(N, levels):
+    """CoeffToSlots (cts_factors) = M^-1: applied to the slots of a real polynomial m it returns the coefficient
+    pairs z_s = m_(c(s)) + i m_(N/2 + c(s)), c = bitReverse -- the first half of the Half-Bootstrap."""
+    from paper_2601_18511_b200.chain import cts_factors
+
+    n = N // 2
+    m = np.random.default_rng(3).standard_normal(N)
+    w = slots.decode(m, N, 1.0, real=False)
+    fs = cts_factors(N, levels)
+    assert [(f["stride"], f["T"], f["count"]) for f in fs] == [(f["stride"], f["T"], f["count"])
+                                                            for f in stc_factors(N, levels)][::-1]
+    v = w.copy()
+    for f in fs:
+        assert max(np.abs(d).max() for d in f["diags"].values()) <= 1 + 1e-12
+        v = apply_diagonals(f["diags"], v)
+    c = np.argsort(slot_of_coeff(N))           # c[s] = bitReverse(s)
+    want = m[c] + 1j * m[n + c]
+    assert np.abs(v - want).max() < 1e-9 * np.sqrt(N)

@@ -152,3 +152,120 @@ def test_llama_chain_precision_sweep():
         X = encrypt_slots_at(ctx, sk, A, seed=3, scale=plan.input_scale)
         err = np.abs(ctx.decrypt_acts(sk, slot_to_coeffs_factorized(ctx, plan, keys, X)) - A).max()
         print(f"shifts {shifts}: max err {err:.3e} = 2^{np.log2(err):.1f}")
+
+
+# ---------------------------------------------------------------- CoeffToSlots (the linear half of the Half-Bootstrap)
+def _pairs(P, ph):
+    """slot s <- (p_(c(s)) + i p_(N/2 + c(s))) of integer phases [n_ct][N] (c = bitReverse)."""
+    from paper_2601_18511_b200.stc import slot_of_coeff
+
+    c = np.argsort(slot_of_coeff(P.N))
+    ph = np.asarray(ph, dtype=np.float64)
+    return ph[:, c] + 1j * ph[:, P.N // 2 + c]
+
+
+def _mul_pow2_np(P, ct, e):
+    q = np.array(P.moduli[:ct.shape[1]], dtype=np.uint64).reshape(1, -1, 1, 1)
+    return ((ct.astype(np.uint64) << np.uint64(e)) % q).astype(np.uint32)
+
+
+def _slots_of(P, ph, shifts=0):
+    return np.stack([slots.decode(np.asarray(v, dtype=np.float64), P.N, 2.0 ** -shifts, real=False) for v in ph])
+
+
+def test_factorized_cts_bit_exact_and_decrypts_to_coefficient_pairs():
+    from paper_2601_18511_b200.chain import (coeffs_to_slots_factorized, decrypt_exact, encrypt_coeffs_at,
+                                             make_factorized_cts_plan, mul_pow2)
+
+    P, ctx, sk, A = _toy()
+    s = O.keygen(P, 7)
+    plan = make_factorized_cts_plan(ctx)
+    assert [m.level for m in plan.maps] == [4, 3, 2] and plan.output_level == 1
+    pt = O.encode_acts(P, A)
+    X = encrypt_coeffs_at(ctx, sk, pt, level=4, seed=13)
+    assert np.array_equal(u32(X.data), O.encrypt(P, 13, s, pt, level=4))
+    keys = factorized_stc_keygen(ctx, sk, plan, seed=23)
+    ref = _mul_pow2_np(P, u32(X.data), plan.pre_log2)
+    data, level = mul_pow2(ctx, X.data, plan.pre_log2), 4
+    assert np.array_equal(u32(data), ref)
+    for k, (m, kk) in enumerate(zip(plan.maps, keys)):
+        data = chain_map(ctx, m, kk, data, level)
+        kb, kg = _oracle_keys(P, m, 23 + 7919 * k, s)
+        pts = np.stack([np.stack([(m.pts_int[t] % q).astype(np.uint32) for q in P.moduli[:level + 1]])
+                        for t in range(m.b * m.g)])
+        ref = np.stack([O.chain_bsgs(P, ref[r], pts, level, m.b, m.g, m.stride, m.T, kb, kg) for r in range(len(ref))])
+        assert np.array_equal(u32(data), ref), f"CtS map {k} (level {level}) differs from the oracle"
+        level -= 1
+    Z = coeffs_to_slots_factorized(ctx, plan, keys, X)
+    assert Z.level == 1 and np.array_equal(u32(Z.data), ref) and Z.layout == "coeff_pairs"
+    got = _slots_of(P, decrypt_exact(ctx, sk, Z.data), sum(plan.shifts) - plan.pre_log2)
+    err = np.abs(got - _pairs(P, pt)).max() / P.delta
+    assert err < 2 ** -12, err
+
+
+def test_modraise_then_cts_toy():
+    """ModRaise of a level-0 ciphertext into the whole chain (phase m + q0 I(X), |I| small) -> CoeffToSlots: the
+    slots carry the raised phase's coefficient pairs -- EvalMod's input -- every map word bit-exact."""
+    from paper_2601_18511_b200.chain import (coeffs_to_slots_factorized, decrypt_exact, encrypt_coeffs_at,
+                                             make_factorized_cts_plan, mul_pow2)
+
+    P, ctx, sk, A = _toy()
+    s = O.keygen(P, 7)
+    X0 = encrypt_coeffs_at(ctx, sk, O.encode_acts(P, A), level=0, seed=29)
+    from paper_2601_18511_b200.context import CtBlocks
+    raised = mod_raise(ctx, CtBlocks(X0.data, level=0, n_cols=0), list(P.moduli))
+    ph = decrypt_exact(ctx, sk, raised)
+    m0 = ctx.decrypt_phase(sk, CtBlocks(X0.data, level=0, n_cols=0)).cpu().numpy()
+    I = (ph - m0.astype(object)) // P.moduli[0]
+    assert np.array_equal((ph - m0.astype(object)) % P.moduli[0], np.zeros_like(ph)) and np.abs(I).max() > 0
+    plan = make_factorized_cts_plan(ctx)
+    keys = factorized_stc_keygen(ctx, sk, plan, seed=31)
+    Z = coeffs_to_slots_factorized(ctx, plan, keys, raised)
+    ref = _mul_pow2_np(P, u32(raised), plan.pre_log2)
+    level = 4
+    for k, m in enumerate(plan.maps):
+        kb, kg = _oracle_keys(P, m, 31 + 7919 * k, s)
+        pts = np.stack([np.stack([(m.pts_int[t] % q).astype(np.uint32) for q in P.moduli[:level + 1]])
+                        for t in range(m.b * m.g)])
+        ref = np.stack([O.chain_bsgs(P, ref[r], pts, level, m.b, m.g, m.stride, m.T, kb, kg) for r in range(len(ref))])
+        level -= 1
+    assert np.array_equal(u32(Z.data), ref)
+    got = _slots_of(P, decrypt_exact(ctx, sk, Z.data), sum(plan.shifts) - plan.pre_log2)
+    err = np.abs(got - _pairs(P, ph)).max() / P.moduli[0]
+    assert err < 2 ** -20, err
+
+
+@pytest.mark.parametrize("chain_levels,bound", [(3, 2 ** -15), (4, 2 ** -21)])
+def test_llama_modraise_cts_precision(chain_levels, bound):
+    """N = 2^16: a level-0 coefficient ciphertext -> ModRaise into the whole chain -> CoeffToSlots (3 maps, 54
+    rotations, output at level 1 / 2): the slot values agree with the exact raised phase m + q0 I to the stated
+    fraction of q0 (what EvalMod would consume; EvalMod itself is out of reach of this prime chain)."""
+    import time
+
+    from paper_2601_18511_b200.chain import (coeffs_to_slots_factorized, decrypt_exact, encrypt_coeffs_at,
+                                             make_factorized_cts_plan, mul_pow2)
+    from paper_2601_18511_b200.context import CtBlocks
+
+    P = HeParams.llama_chain(chain_levels)
+    ctx = HeContext(P, rng="seeded")
+    sk = ctx.keygen(7)
+    A = np.random.default_rng(5).uniform(-1, 1, (P.tokens, 2 * P.mlwe_rank))
+    X0 = encrypt_coeffs_at(ctx, sk, O.encode_acts(P, A), level=0, seed=3)
+    raised = mod_raise(ctx, CtBlocks(X0.data, level=0, n_cols=0), list(P.moduli))
+    ph = decrypt_exact(ctx, sk, raised)
+    plan = make_factorized_cts_plan(ctx)
+    assert plan.rotations == 54
+    keys = factorized_stc_keygen(ctx, sk, plan, seed=9)
+    coeffs_to_slots_factorized(ctx, plan, keys, raised)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    Z = coeffs_to_slots_factorized(ctx, plan, keys, raised)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    got = _slots_of(P, decrypt_exact(ctx, sk, Z.data), sum(plan.shifts) - plan.pre_log2)
+    want = _pairs(P, ph)
+    err = np.abs(got - want).max()
+    Imax = float(np.abs(want).max()) / P.moduli[0]
+    print(f"ModRaise + CtS at N = 2^16: {ms:.2f} ms for {raised.shape[0]} cts, |I| <= {Imax:.1f}, "
+          f"max err {err:.3g} = 2^{np.log2(err / P.moduli[0]):.1f} q0 = 2^{np.log2(err / P.delta):.1f} Delta")
+    assert err / P.moduli[0] < bound, err
