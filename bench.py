@@ -562,15 +562,18 @@ def side_measurements(P, dev):
 
 
 def chain_side(dev, n_in: int = 11008, n_out: int = 4096, reps=3):
-    """§8f2 with the paper's pipeline: slot-encoded activations at level 5 -> lower to level 4
-    -> Cooley-Tukey-factorized SlotToCoeffs (three maps, levels 4 -> 1) -> the metric-shape MLWE PCMM -> ring
-    packing -> ModRaise: device ms per stage and the decrypted precision of each hand-off."""
+    """§8f2 / §8f4 with the paper's pipeline: slot-encoded activations at level 5 -> lower to
+    level 4 -> Cooley-Tukey-factorized SlotToCoeffs (three maps, levels 4 -> 1) -> the metric-shape MLWE PCMM ->
+    ring packing -> ModRaise into the whole chain -> CoeffToSlots (three maps, levels 5 -> 2; the linear half of
+    the Half-Bootstrap): device ms per stage and the precision of each hand-off."""
     import torch
 
     from paper_2601_18511_b200 import (HeContext, HeParams, clear_pcmm, make_mlwe_pcmm_plan, make_ring_pack_plan,
-                                       mod_raise, pcmm_packed, ring_pack_keygen)
-    from paper_2601_18511_b200.chain import (encrypt_slots_at, factorized_stc_keygen, lower_level,
+                                       mod_raise, pcmm_packed, ring_pack_keygen, slots)
+    from paper_2601_18511_b200.chain import (coeffs_to_slots_factorized, decrypt_exact, encrypt_slots_at,
+                                             factorized_stc_keygen, lower_level, make_factorized_cts_plan,
                                              make_factorized_stc_plan, slot_to_coeffs_factorized)
+    from paper_2601_18511_b200.stc import slot_of_coeff
 
     P = HeParams.llama_chain(levels=4)
     ctx = HeContext(P, device=dev, rng="seeded")
@@ -580,19 +583,22 @@ def chain_side(dev, n_in: int = 11008, n_out: int = 4096, reps=3):
     W = rng.uniform(-1, 1, (n_out, n_in)) / math.sqrt(n_in)
     plan = make_factorized_stc_plan(ctx, input_level=4)
     keys = factorized_stc_keygen(ctx, sk, plan, seed=75)
+    cts = make_factorized_cts_plan(ctx)
+    ckeys = factorized_stc_keygen(ctx, sk, cts, seed=81)
     X5 = encrypt_slots_at(ctx, sk, A, level=5, seed=77, scale=plan.input_scale)
     pp, rp, rk = make_mlwe_pcmm_plan(ctx, W), make_ring_pack_plan(ctx, n_out), ring_pack_keygen(ctx, sk, 79)
-    raise_to = list(P.moduli[2:])
+    raise_to = list(P.moduli)
 
     def run():
         Xc = slot_to_coeffs_factorized(ctx, plan, keys, lower_level(X5, 4))
         Yp = pcmm_packed(ctx, pp, rp, rk, Xc)
-        return Xc, Yp, mod_raise(ctx, Yp, raise_to)
+        R = mod_raise(ctx, Yp, raise_to)
+        return Xc, Yp, R, coeffs_to_slots_factorized(ctx, cts, ckeys, R)
 
-    Xc, Yp, R = run()
+    Xc, Yp, R, Z = run()
     torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    t = [0.0, 0.0, 0.0]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    t = [0.0] * 4
     for _ in range(reps):
         ev[0].record()
         Xc = slot_to_coeffs_factorized(ctx, plan, keys, lower_level(X5, 4))
@@ -601,22 +607,37 @@ def chain_side(dev, n_in: int = 11008, n_out: int = 4096, reps=3):
         ev[2].record()
         R = mod_raise(ctx, Yp, raise_to)
         ev[3].record()
+        Z = coeffs_to_slots_factorized(ctx, cts, ckeys, R)
+        ev[4].record()
         torch.cuda.synchronize()
-        for i in range(3):
+        for i in range(4):
             t[i] += ev[i].elapsed_time(ev[i + 1]) / reps
     e_stc = float(np.abs(ctx.decrypt_acts(sk, Xc) - A).max())
     e_out = float(np.abs(ctx.decrypt_acts(sk, Yp) - clear_pcmm(W, A)).max())
+    # CoeffToSlots: the slots of two output blocks vs the exact raised phase m + q0 I (CRT over all limbs)
+    ph = np.asarray(decrypt_exact(ctx, sk, R[:2]), dtype=np.float64)
+    c = np.argsort(slot_of_coeff(P.N))
+    want = ph[:, c] + 1j * ph[:, P.N // 2 + c]
+    zo = np.asarray(decrypt_exact(ctx, sk, Z.data[:2]), dtype=np.float64)
+    got = np.stack([slots.decode(v, P.N, Z.scale, real=False) for v in zo])
+    e_cts = float(np.abs(got - want).max())
     n_ct = X5.n_ct
     return {"workload": f"level-5 slot input ({n_ct} cts) -> lower to 4 -> factorized SlotToCoeffs (3 maps, "
                         f"{plan.rotations} rotations / ct, {plan.plaintexts} plaintexts) -> PCMM {n_out}x{n_in}x128 -> "
-                        f"ring packing -> ModRaise to {len(raise_to)} primes, N = {P.N}, 1 GPU",
+                        f"ring packing -> ModRaise into the {len(raise_to)}-prime chain -> factorized CoeffToSlots "
+                        f"(3 maps, {cts.rotations} rotations / ct), N = {P.N}, 1 GPU",
             "ms_total": round(sum(t), 3), "ms_slot_to_coeffs": round(t[0], 3),
             "ms_slot_to_coeffs_per_ct": round(t[0] / n_ct, 3), "ms_pcmm_packed": round(t[1], 3),
-            "ms_mod_raise": round(t[2], 3),
+            "ms_mod_raise": round(t[2], 3), "ms_coeffs_to_slots": round(t[3], 3),
+            "ms_coeffs_to_slots_per_ct": round(t[3] / int(R.shape[0]), 3),
             "precision_bits_slot_to_coeffs": round(-math.log2(e_stc), 1),
             "precision_bits_output": round(-math.log2(e_out / float(np.abs(clear_pcmm(W, A)).max())), 1),
+            "coeffs_to_slots_err_log2_q0": round(math.log2(e_cts / P.moduli[0]), 1),
+            "coeffs_to_slots_err_log2_delta": round(math.log2(e_cts / P.delta), 1),
+            "coeffs_to_slots_shifts": list(cts.shifts), "coeffs_to_slots_pre_log2": cts.pre_log2,
+            "half_bootstrap": "ModRaise + CoeffToSlots built; EvalMod not built (DESIGN.md §7e)",
             "levels": {"input": 5, "lowered": 4, "after_stc": Xc.level, "after_pcmm_pack": Yp.level,
-                       "raised_limbs": int(R.shape[1])}}
+                       "raised": int(R.shape[1]) - 1, "after_cts": Z.level}}
 
 
 def graph_ms(fn, reps=5):
