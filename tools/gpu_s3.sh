@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+export PYTHONUNBUFFERED=1
+timeout 900 python -m pytest tests/test_gpu_pcmm.py -x -q > gpurun_out/pytest_s3.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_s3.log
+for v in 0 1 0 1; do echo "GPAD64=$v"; if [ $v = 1 ]; then export HE_SPEC_GPAD64=1; else unset HE_SPEC_GPAD64; fi; timeout 300 python bench.py --no-direct --no-e2e --no-extras --cpu-rows 0 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['kernels_ms'])"; done > gpurun_out/bench_s3.txt 2>&1
+unset HE_SPEC_GPAD64
+timeout 600 python tools/shapes_times.py > gpurun_out/shapes.txt 2>&1
