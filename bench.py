@@ -780,7 +780,8 @@ def ring_pack_side(P, dev, shape="4096x11008", reps=3):
             ts.append(e0.elapsed_time(e1))
         res[name] = round(float(np.median(ts)), 3)
     return {"workload": f"{shape} PCMM + MLWE->RLWE key-switch packing (k = {P.mlwe_rank} hybrid key switches "
-                        f"per block, dnum 2) -> {n_out // P.mlwe_rank} level-0 RLWE ciphertexts, 1 GPU",
+                        f"per block, one digit, special modulus P1 P2; method {rp.method}) -> "
+                        f"{n_out // P.mlwe_rank} level-0 RLWE ciphertexts, 1 GPU",
             **res, "precision_bits": round(-math.log2(err / float(np.abs(ref).max())), 1),
             "output_bytes": int(Y.data.numel() * 4), "h2d_bytes": int(x_host.numel() * 4)}
 

@@ -264,9 +264,16 @@ he_status he_pcmm_run_level1(const he_pcmm_plan* plan, const uint32_t* ct_in_dev
  *   HE_RING_PACK_TRACE: PackLWEs over the subring Z[X^k] (CDKS21): log2 k levels of
  *     E + X^{k/2^l} O + sigma_g(E - X^{k/2^l} O), g = 1 + 2^l d, one Galois key switch per combine.
  *     Keys sigma_g(s) -> s: u32 [log2 k][2][2][3][N] (ids 0x100 + l).
- * Keys are NTT domain, moduli q0 q1 P; both methods give identical plaintexts (different noise). */
+ *   HE_RING_PACK_KEYSWITCH1: the same key switching with ONE digit (alpha_j mod Q = q0 q1 itself) and two
+ *     special primes P1 = P, P2 = he_ring_pack_special2 (the largest NTT prime < 2^30 that is not q0, q1, P):
+ *     4 NTT'd planes per (block, j) instead of 6.  Keys: u32 [k][2 (alpha, beta)][4 (q0, q1, P1, P2)][N]
+ *     encrypting P1 P2 s_j(X^k) (ids 0x300 + j); ModDown by P1 P2 with a CRT-centred [x]_{P1 P2}.
+ * Keys are NTT domain (moduli q0 q1 P, plus P2 for KEYSWITCH1); all methods give identical plaintexts
+ * (different noise). */
 #define HE_RING_PACK_KEYSWITCH 0
 #define HE_RING_PACK_TRACE 1
+#define HE_RING_PACK_KEYSWITCH1 2
+he_status he_ring_pack_special2(const he_context* ctx, uint32_t* p2);
 he_status he_ring_pack_key_bytes(const he_context* ctx, int method, uint64_t* bytes);
 he_status he_ring_pack_keygen(const he_context* ctx, int method, uint64_t seed, const int32_t* s_dev,
                               uint32_t* keys_dev, void* stream);

@@ -518,6 +518,101 @@ int or_mlwe_to_rlwe(uint32_t d, uint32_t k, const uint32_t* m, const uint32_t* r
   return 0;
 }
 
+/* ------------------------------------------------------------------ one-digit variant (he_ring_pack KEYSWITCH1)
+ * The same packed phase, key-switched with ONE digit -- alpha_j itself, centred mod Q = q0 q1 -- and the special
+ * modulus P1 P2 (m4 = {q0, q1, P1 = P, P2}): keys (alpha, beta = -alpha s + e + P1 P2 s^_j) mod q0, q1, P1, P2
+ * (beta's gadget term vanishes mod P1, P2), U = sum_j [alpha_j]_Q K_j[0], W = sum_j [alpha_j]_Q K_j[1] mod each
+ * modulus, ModDown x_q = (X_q - [X]_{P1 P2}) (P1 P2)^-1 mod q with [X]_{P1 P2} centred by CRT.
+ */
+/* key from s^_j = s_j(X^k) to s (key id 0x300 + j, digit i = 0): ksk [2 (alpha, beta)][4][N], coefficient form */
+void or_mlwe_ksk1(uint64_t seed, uint32_t j, const int32_t* s, uint32_t N, uint32_t k, const uint32_t* m4,
+                  uint32_t* ksk) {
+  int32_t* sj = (int32_t*)calloc(N, sizeof(int32_t));
+  int32_t* e = (int32_t*)malloc(sizeof(int32_t) * N);
+  uint32_t* as = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  for (uint32_t c = 0; c < N; c += k) sj[c] = s[j + c];
+  const uint32_t id = 0x300 + j;
+  or_sample_cbd(seed, STREAM_KSK_E(id, 0), e, N);
+  for (uint32_t mi = 0; mi < 4; ++mi) {
+    const uint32_t q = m4[mi];
+    uint32_t* alpha = ksk + ((size_t)0 * 4 + mi) * N;
+    uint32_t* beta = ksk + ((size_t)1 * 4 + mi) * N;
+    or_sample_uniform(seed, STREAM_KSK_A(id, 0, mi), q, alpha, N);
+    or_negacyclic_mul(alpha, s, N, q, as);
+    const uint64_t g = mi < 2 ? mulmod(m4[2] % q, m4[3] % q, q) : 0;
+    for (uint32_t c = 0; c < N; ++c) {
+      uint64_t v = (uint64_t)(q - as[c]) + modq_i64(e[c], q) + mulmod(g, modq_i64(sj[c], q), q);
+      beta[c] = (uint32_t)(v % q);
+    }
+  }
+  free(sj);
+  free(e);
+  free(as);
+}
+/* raw_b, raw_a as or_mlwe_to_rlwe; ksk [k][2][4][N] (or_mlwe_ksk1) -> out [n_out/k][2 (a, b)][N] level 0 */
+int or_mlwe_to_rlwe1(uint32_t d, uint32_t k, const uint32_t* m4, const uint32_t* raw_b, const uint32_t* raw_a,
+                     uint32_t n_out, const uint32_t* ksk, uint32_t* out) {
+  const uint32_t N = d * k;
+  if (n_out % k) return 1;
+  const uint32_t blocks = n_out / k;
+  const uint32_t q0 = m4[0], q1 = m4[1], P1 = m4[2], P2 = m4[3];
+  const uint64_t q1inv = powmod(q1 % q0, q0 - 2, q0);
+  const uint64_t q0inv1 = powmod(q0 % q1, q1 - 2, q1), p1inv2 = powmod(P1 % P2, P2 - 2, P2);
+  const uint64_t Q = (uint64_t)q0 * q1, PP = (uint64_t)P1 * P2;
+#pragma omp parallel for schedule(dynamic)
+  for (uint32_t Y = 0; Y < blocks; ++Y) {
+    uint32_t* U = (uint32_t*)calloc((size_t)4 * N, sizeof(uint32_t));
+    uint32_t* W = (uint32_t*)calloc((size_t)4 * N, sizeof(uint32_t));
+    int64_t* al = (int64_t*)malloc(sizeof(int64_t) * N);
+    uint32_t* dl = (uint32_t*)malloc(sizeof(uint32_t) * N);
+    uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * N);
+    for (uint32_t j = 0; j < k; ++j) {
+      for (uint32_t tt = 0; tt < k; ++tt)
+        for (uint32_t mm = 0; mm < d; ++mm) {
+          const size_t src = ((size_t)Y * k + tt) * N + (size_t)d * j + mm;
+          const uint64_t a0 = raw_a[src], a1 = raw_a[(size_t)n_out * N + src];
+          const uint64_t x = a0 + (uint64_t)q0 * mulmod((a1 + q1 - a0 % q1) % q1, q0inv1, q1);   /* CRT, [0, Q) */
+          al[tt + (size_t)k * mm] = x > Q / 2 ? (int64_t)x - (int64_t)Q : (int64_t)x;
+        }
+      const uint32_t* K = ksk + (size_t)j * 8 * N;
+      for (uint32_t mi = 0; mi < 4; ++mi) {
+        const uint32_t q = m4[mi];
+        for (uint32_t c = 0; c < N; ++c) dl[c] = modq_i64(al[c], q);
+        polymul(dl, K + ((size_t)0 * 4 + mi) * N, N, q, t);
+        for (uint32_t c = 0; c < N; ++c) U[(size_t)mi * N + c] = (uint32_t)(((uint64_t)U[(size_t)mi * N + c] + t[c]) % q);
+        polymul(dl, K + ((size_t)1 * 4 + mi) * N, N, q, t);
+        for (uint32_t c = 0; c < N; ++c) W[(size_t)mi * N + c] = (uint32_t)(((uint64_t)W[(size_t)mi * N + c] + t[c]) % q);
+      }
+    }
+    for (uint32_t c = 0; c < N; ++c) {
+      uint32_t x[2][2];
+      for (int part = 0; part < 2; ++part) {
+        const uint32_t* V = part ? W : U;
+        const uint64_t v1 = V[2 * (size_t)N + c], v2 = V[3 * (size_t)N + c];
+        const uint64_t xp = v1 + (uint64_t)P1 * mulmod((v2 + P2 - v1 % P2) % P2, p1inv2, P2);   /* [0, P1 P2) */
+        const int64_t xc = xp > PP / 2 ? (int64_t)xp - (int64_t)PP : (int64_t)xp;   /* |xc| <= P1 P2 / 2 < 2^60 */
+        for (int L = 0; L < 2; ++L) {
+          const uint32_t q = m4[L];
+          const uint64_t ppinv = powmod(mulmod(P1 % q, P2 % q, q), q - 2, q);
+          uint32_t v = (uint32_t)mulmod(modq_i64((int64_t)V[(size_t)L * N + c] - xc, q), ppinv, q);
+          if (part) v = (uint32_t)(((uint64_t)v + raw_b[((size_t)L * blocks + Y) * N + c]) % q);
+          x[L][part] = v;
+        }
+      }
+      for (int ab = 0; ab < 2; ++ab) {
+        const int64_t x1c = x[1][ab] > q1 / 2 ? (int64_t)x[1][ab] - q1 : (int64_t)x[1][ab];
+        out[((size_t)Y * 2 + ab) * N + c] = (uint32_t)mulmod(modq_i64((int64_t)x[0][ab] - x1c, q0), q1inv, q0);
+      }
+    }
+    free(U);
+    free(W);
+    free(al);
+    free(dl);
+    free(t);
+  }
+  return 0;
+}
+
 /* ================================================================== slot-domain BSGS PCMM
  * hesim pcmm_bsgs (matmul.py:165-176) on real CKKS ciphertexts: the input matrix sits row-major in the
  * slots (tiled), a left slot rotation by r is the automorphism X -> X^(5^r) followed by a hybrid key

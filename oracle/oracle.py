@@ -18,7 +18,8 @@ __all__ = [
     "py_mlwe_components", "py_pcmm_rows", "num_threads", "time_pcmm_sample", "rng",
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
     "decode_vector", "rhombus_pcmv", "rhombus_pcmv_w", "rhombus_combine", "rhombus_window", "rhombus_weights", "decrypt_under", "ring_pack_keys", "ring_pack_leaves",
-    "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe", "rotation_keys", "slot_pcmm",
+    "ring_pack", "pcmm_ring_pack", "mlwe_ks_keys", "raw_device_layout", "mlwe_to_rlwe", "mlwe_ks_keys1",
+    "mlwe_to_rlwe1", "ring_pack_special2", "rotation_keys", "slot_pcmm",
     "slot_bsgs", "rotation_keys_plain", "chain_rotation_keys", "chain_bsgs", "chain_key_id",
 ]
 
@@ -580,6 +581,61 @@ def mlwe_ks_keys(params, seed: int, s: np.ndarray) -> np.ndarray:
         g = np.zeros((2, 2, 3, N), np.uint32)
         _ms_bind().or_mlwe_ksk(seed, j, _i32(s), N, k, _u32(m), _u32(g))
         out[j] = g
+    return out
+
+
+def ring_pack_special2(params) -> int:
+    """The second special prime of ring packing KEYSWITCH1 (he_ring_pack_special2): the largest prime < 2^30,
+    1 mod 2N, other than q0, q1 and P."""
+    from paper_2601_18511_b200.params import ntt_primes
+
+    for p in ntt_primes(2 * params.N, 1 << 30, 8):
+        if p not in (params.moduli[0], params.moduli[1], params.special_prime):
+            return p
+    raise ValueError("no second special prime")
+
+
+def _ms1_bind():
+    L = _rp_lib()
+    if not getattr(L, "_ms1_bound", False):
+        u32p, i32p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32)
+        u32, u64 = ctypes.c_uint32, ctypes.c_uint64
+        L.or_mlwe_ksk1.restype = None
+        L.or_mlwe_ksk1.argtypes = [u64, u32, i32p, u32, u32, u32p, u32p]
+        L.or_mlwe_to_rlwe1.restype = ctypes.c_int
+        L.or_mlwe_to_rlwe1.argtypes = [u32, u32, u32p, u32p, u32p, u32, u32p, u32p]
+        L._ms1_bound = True
+    return L
+
+
+def _m4(params):
+    return np.ascontiguousarray(np.array([params.moduli[0], params.moduli[1], params.special_prime,
+                                          ring_pack_special2(params)], dtype=np.uint32))
+
+
+def mlwe_ks_keys1(params, seed: int, s: np.ndarray) -> np.ndarray:
+    """One-digit MLWE -> RLWE keys s_j(X^k) -> s mod (q0, q1, P1, P2): [k, 2, 4, N] (coefficient form)."""
+    N, k = params.N, params.mlwe_rank
+    m = _m4(params)
+    out = np.zeros((k, 2, 4, N), np.uint32)
+    s = np.ascontiguousarray(s, dtype=np.int32)
+    for j in range(k):
+        g = np.zeros((2, 4, N), np.uint32)
+        _ms1_bind().or_mlwe_ksk1(seed, j, _i32(s), N, k, _u32(m), _u32(g))
+        out[j] = g
+    return out
+
+
+def mlwe_to_rlwe1(params, raw_b: np.ndarray, raw_a: np.ndarray, ksk: np.ndarray) -> np.ndarray:
+    """One-digit MLWE -> RLWE key-switch packing (or_mlwe_to_rlwe1) -> [n_out/k, 2, N] level 0."""
+    d, k, N = params.mlwe_degree, params.mlwe_rank, params.N
+    n_out = raw_a.shape[1]
+    out = np.zeros((n_out // k, 2, N), np.uint32)
+    rc = _ms1_bind().or_mlwe_to_rlwe1(d, k, _u32(_m4(params)), _u32(np.ascontiguousarray(raw_b, dtype=np.uint32)),
+                                      _u32(np.ascontiguousarray(raw_a, dtype=np.uint32)), n_out,
+                                      _u32(np.ascontiguousarray(ksk, dtype=np.uint32)), _u32(out))
+    if rc:
+        raise ValueError("mlwe_to_rlwe1: bad shape")
     return out
 
 

@@ -1095,6 +1095,154 @@ __global__ void k_ms_component(const int32_t* s, uint32_t N, uint32_t k, uint32_
     out[c] = (c % k == 0) ? s[j + c] : 0;
 }
 
+// ---- one-digit MLWE -> RLWE key switching with two special primes (method HE_RING_PACK_KEYSWITCH1; oracle
+// or_mlwe_to_rlwe1): the digit of alpha_j is alpha_j itself (mod Q = q0 q1), its centred value lifted to
+// P1 = P and P2, and the keys encrypt P1 P2 s_j(X^k) modulo Q P1 P2 -- 4 NTT'd planes per (block, j) instead of
+// 2 digits x 3 moduli, 8 key planes per component instead of 12.
+struct Mods4 {
+  uint32_t m[4];   // q0, q1, P1, P2
+  uint64_t mu[4];
+};
+// D [mod 4][cnt][N]: alpha mod q0, alpha mod q1 (the residues themselves) and [alpha]_Q mod P1, P2.  One CTA per
+// (16 positions m, pair): both limbs' [t][m] tiles through smem (pitch 17), 4 consecutive t per thread -> 16-byte
+// stores of every plane.
+constexpr int kMs1M = 16;
+__global__ void __launch_bounds__(256) k_ms1_digits(const uint32_t* __restrict__ raw_a, uint32_t n_out, uint32_t Y0,
+                                                    uint32_t j0, uint32_t Yc, uint32_t cnt, uint32_t d, uint32_t k,
+                                                    uint32_t N, Mods4 M, uint32_t q0inv_q1, uint32_t* __restrict__ D) {
+  __shared__ uint32_t tile[2][256 * (kMs1M + 1)];  // [limb][t][m], k <= 256
+  const uint32_t m0 = blockIdx.x * kMs1M, idx = blockIdx.y, jj = idx / Yc, Y = idx % Yc, j = j0 + jj;
+  const size_t plane = (size_t)cnt * N;
+  for (uint32_t L = 0; L < 2; ++L) {
+    const uint32_t* src = raw_a + ((size_t)L * n_out + (size_t)(Y0 + Y) * k) * N + (size_t)d * j + m0;
+    for (uint32_t i = threadIdx.x; i < kMs1M * k; i += blockDim.x)
+      tile[L][(i / kMs1M) * (kMs1M + 1) + (i % kMs1M)] = src[(size_t)(i / kMs1M) * N + (i % kMs1M)];
+  }
+  __syncthreads();
+  const uint32_t q0 = M.m[0], q1 = M.m[1];
+  const uint64_t Q = (uint64_t)q0 * q1;
+  const uint32_t k4 = k / 4;
+  for (uint32_t i = threadIdx.x; i < kMs1M * k4; i += blockDim.x) {
+    const uint32_t mm = i / k4, t0 = 4 * (i % k4);
+    uint32_t o[4][4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t a0 = tile[0][(t0 + e) * (kMs1M + 1) + mm], a1 = tile[1][(t0 + e) * (kMs1M + 1) + mm];
+      // CRT: alpha = a0 + q0 ((a1 - a0) q0^-1 mod q1) in [0, Q), centred
+      const uint32_t tq = mulmod_b(sub_mod(a1, barrett64(a0, M.mu[1], q1), q1), q0inv_q1, M.mu[1], q1);
+      const uint64_t al = (uint64_t)a0 + (uint64_t)q0 * tq;
+      const int64_t ac = al > Q / 2 ? (int64_t)al - (int64_t)Q : (int64_t)al;
+      o[0][e] = a0;
+      o[1][e] = a1;
+      o[2][e] = lift_b(ac, M.mu[2], M.m[2]);
+      o[3][e] = lift_b(ac, M.mu[3], M.m[3]);
+    }
+    const size_t c = (size_t)idx * N + t0 + (size_t)k * (m0 + mm);
+#pragma unroll
+    for (int mod = 0; mod < 4; ++mod)
+      *reinterpret_cast<uint4*>(D + mod * plane + c) = make_uint4(o[mod][0], o[mod][1], o[mod][2], o[mod][3]);
+  }
+}
+// UW [mod][part][Yc][N] += sum_jj D^[mod][jj Yc + Y] * K_{j0+jj}[part][mod]   (NTT domain; 4 frequencies per thread)
+__global__ void __launch_bounds__(256) k_ms1_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict__ K,
+                                                 uint32_t jc, uint32_t Yc, uint32_t logN, Mods4 M,
+                                                 uint32_t* __restrict__ UW) {
+  const uint32_t N = 1u << logN, mod = blockIdx.y;
+  const uint64_t x4 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (x4 >= ((uint64_t)Yc << logN) / 4) return;
+  const uint32_t f4 = (uint32_t)((x4 * 4) & (N - 1)) / 4;
+  const uint32_t q = M.m[mod];
+  const uint64_t mu = M.mu[mod];
+  const size_t plane4 = (size_t)jc * Yc * N / 4, yn4 = (size_t)Yc * N / 4, n4 = N / 4;
+  const uint4* d0 = reinterpret_cast<const uint4*>(D) + (size_t)mod * plane4 + x4;
+  uint64_t au[4] = {0, 0, 0, 0}, aw[4] = {0, 0, 0, 0};
+  for (uint32_t jj = 0; jj < jc; ++jj) {
+    const uint4* Kj = reinterpret_cast<const uint4*>(K + (size_t)jj * 8 * N) + f4;
+    const uint4 x = __ldcs(d0 + jj * yn4);
+    const uint4 ku = __ldg(Kj + (0 * 4 + mod) * n4), kw = __ldg(Kj + (1 * 4 + mod) * n4);
+    const uint32_t a[4] = {x.x, x.y, x.z, x.w}, u[4] = {ku.x, ku.y, ku.z, ku.w}, w[4] = {kw.x, kw.y, kw.z, kw.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      au[e] += (uint64_t)a[e] * u[e];
+      aw[e] += (uint64_t)a[e] * w[e];
+    }
+    if ((jj & 7) == 7) {  // products < 2^60: reduce every 8 steps (< 2^63)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        au[e] = barrett64(au[e], mu, q);
+        aw[e] = barrett64(aw[e], mu, q);
+      }
+    }
+  }
+  uint4* U = reinterpret_cast<uint4*>(UW) + (size_t)(mod * 2 + 0) * yn4 + x4;
+  uint4* W = reinterpret_cast<uint4*>(UW) + (size_t)(mod * 2 + 1) * yn4 + x4;
+  const uint4 uo = *U, wo = *W;
+  *U = make_uint4(add_mod(uo.x, barrett64(au[0], mu, q), q), add_mod(uo.y, barrett64(au[1], mu, q), q),
+                  add_mod(uo.z, barrett64(au[2], mu, q), q), add_mod(uo.w, barrett64(au[3], mu, q), q));
+  *W = make_uint4(add_mod(wo.x, barrett64(aw[0], mu, q), q), add_mod(wo.y, barrett64(aw[1], mu, q), q),
+                  add_mod(wo.z, barrett64(aw[2], mu, q), q), add_mod(wo.w, barrett64(aw[3], mu, q), q));
+}
+// ModDown by P1 P2 of the summed (U, W) (coefficient form; [x]_P centred by CRT), b += composed b', rescale by q1
+__global__ void k_ms1_finish(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ raw_b, uint32_t blocks,
+                             uint32_t Y0, uint32_t Yc, uint32_t logN, Mods4 M, uint32_t p1inv_p2, uint32_t pinv0,
+                             uint32_t pinv1, uint32_t q1inv, uint32_t q1invp, uint32_t* __restrict__ out) {
+  const uint32_t N = 1u << logN, q0 = M.m[0], q1 = M.m[1], P1 = M.m[2], P2 = M.m[3];
+  const uint64_t per = (uint64_t)Yc << logN, PP = (uint64_t)P1 * P2;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < per; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t Y = (uint32_t)(x >> logN), c = (uint32_t)(x & (N - 1));
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const uint32_t v1 = UW[(size_t)(2 * 2 + part) * per + x], v2 = UW[(size_t)(3 * 2 + part) * per + x];
+      const uint32_t tq = mulmod_b(sub_mod(v2, barrett64(v1, M.mu[3], P2), P2), p1inv_p2, M.mu[3], P2);
+      const uint64_t xp = (uint64_t)v1 + (uint64_t)P1 * tq;   // [x]_{P1 P2} in [0, P1 P2)
+      const bool neg = xp > PP / 2;
+      const uint64_t mag = neg ? PP - xp : xp;
+      uint32_t v[2];
+#pragma unroll
+      for (int L = 0; L < 2; ++L) {
+        const uint32_t q = M.m[L];
+        uint32_t r = barrett64(mag, M.mu[L], q);
+        if (neg && r) r = q - r;                                   // [x]_P mod q
+        v[L] = mulmod_b(sub_mod(UW[(size_t)(L * 2 + part) * per + x], r, q), L ? pinv1 : pinv0, M.mu[L], q);
+        if (part) v[L] = add_mod(v[L], raw_b[((size_t)L * blocks + Y0 + Y) * N + c], q);
+      }
+      uint32_t t;
+      if (v[1] > (q1 >> 1)) t = csub(v[0] + (q1 - v[1]), q0);
+      else t = sub_mod(v[0], v[1], q0);
+      out[((size_t)(Y0 + Y) * 2 + part) * N + c] = shoup_mul(t, q1inv, q1invp, q0);
+    }
+  }
+}
+// the second special prime of method KEYSWITCH1: the largest prime < 2^30, 1 mod 2N, not q0, q1 or P
+static bool is_prime_h(uint64_t n) {
+  if (n < 2) return false;
+  for (uint64_t p : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull})
+    if (n % p == 0) return n == p;
+  uint64_t dd = n - 1;
+  int sh = 0;
+  while (!(dd & 1)) dd >>= 1, ++sh;
+  for (uint64_t a : {2ull, 3ull, 5ull, 7ull, 11ull}) {
+    uint64_t x = powmod_h(a, dd, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int r = 1; r < sh && comp; ++r) {
+      x = (unsigned __int128)x * x % n;
+      if (x == n - 1) comp = false;
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+uint32_t ring_pack_p2(const RingDims& R) {
+  const uint64_t two_n = 2ull * R.N;
+  for (uint64_t cc = ((1ull << 30) - 1) / two_n; cc > 0; --cc) {
+    const uint64_t p = cc * two_n + 1;
+    if (p >= (1ull << 30) || p == R.q[0] || p == R.q[1] || p == R.P) continue;
+    if (is_prime_h(p)) return (uint32_t)p;
+  }
+  return 0;
+}
+
 uint64_t find_psi(uint32_t q, uint32_t n) {  // the root ntt_table_init uses
   for (uint64_t g = 2; g < q; ++g) {
     const uint64_t cand = powmod_h(g, (q - 1) / (2ull * n), q);
@@ -1107,7 +1255,10 @@ uint64_t find_psi(uint32_t q, uint32_t n) {  // the root ntt_table_init uses
 
 struct he_ring_pack_plan {
   const he_context* ctx;
-  int method;        // HE_RING_PACK_KEYSWITCH (0) or HE_RING_PACK_TRACE (1)
+  int method;        // HE_RING_PACK_KEYSWITCH (0), HE_RING_PACK_TRACE (1) or HE_RING_PACK_KEYSWITCH1 (2)
+  NttTable ntt_p2{};  // KEYSWITCH1: degree-N tables of the second special prime
+  Mods4 M4{};
+  uint32_t q0inv_q1 = 0, p1inv_p2 = 0, ppinv[2] = {0, 0};
   uint32_t jc;       // keyswitch: components j per pass
   uint32_t n_out, blocks, chunk, d, k, N, logN, logk;
   uint32_t* tables;  // owned: perm [logk][N], mono [logk][2][N]
@@ -1116,12 +1267,30 @@ struct he_ring_pack_plan {
 };
 
 static uint64_t ring_pack_key_words(const he_context* c, int method) {
+  if (method == HE_RING_PACK_KEYSWITCH1) return (uint64_t)c->R.k * 8ull * c->R.N;   // [k][2][4][N]
   const uint64_t n_keys = method == HE_RING_PACK_TRACE ? (uint64_t)ilog2_u(c->R.k) : (uint64_t)c->R.k;
   return n_keys * 12ull * c->R.N;
 }
+static bool rp_method_ok(int m) {
+  return m == HE_RING_PACK_KEYSWITCH || m == HE_RING_PACK_TRACE || m == HE_RING_PACK_KEYSWITCH1;
+}
+static Mods4 make_mods4(const RingDims& R, uint32_t P2) {
+  Mods4 M;
+  M.m[0] = R.q[0];
+  M.m[1] = R.q[1];
+  M.m[2] = R.P;
+  M.m[3] = P2;
+  for (int j = 0; j < 4; ++j) M.mu[j] = (uint64_t)(((unsigned __int128)1 << 64) / M.m[j]);
+  return M;
+}
+extern "C" he_status he_ring_pack_special2(const he_context* c, uint32_t* p2) {
+  if (!c || !p2) return fail(HE_EINVAL, "null argument");
+  *p2 = ring_pack_p2(c->R);
+  return *p2 ? HE_OK : fail(HE_EINVAL, "no second special prime below 2^30 for N = %u", c->R.N);
+}
 extern "C" he_status he_ring_pack_key_bytes(const he_context* c, int method, uint64_t* bytes) {
   if (!c || !bytes) return fail(HE_EINVAL, "null argument");
-  if (method != HE_RING_PACK_KEYSWITCH && method != HE_RING_PACK_TRACE) return fail(HE_EINVAL, "unknown method %d", method);
+  if (!rp_method_ok(method)) return fail(HE_EINVAL, "unknown method %d", method);
   *bytes = ring_pack_key_words(c, method) * sizeof(uint32_t);
   return HE_OK;
 }
@@ -1129,7 +1298,7 @@ extern "C" he_status he_ring_pack_key_bytes(const he_context* c, int method, uin
 extern "C" he_status he_ring_pack_keygen(const he_context* c, int method, uint64_t seed, const int32_t* s_dev,
                                          uint32_t* keys_dev, void* stream) {
   if (!c || !s_dev || !keys_dev) return fail(HE_EINVAL, "null argument");
-  if (method != HE_RING_PACK_KEYSWITCH && method != HE_RING_PACK_TRACE) return fail(HE_EINVAL, "unknown method %d", method);
+  if (!rp_method_ok(method)) return fail(HE_EINVAL, "unknown method %d", method);
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t N = c->R.N, d = c->R.d, k = c->R.k;
   const int logk = ilog2_u(k);
@@ -1137,7 +1306,38 @@ extern "C" he_status he_ring_pack_keygen(const he_context* c, int method, uint64
   int32_t* sk = nullptr;
   HE_CUDA(cudaMallocAsync(&sk, N * sizeof(int32_t), st), "alloc");
   he_status s = HE_OK;
-  if (method == HE_RING_PACK_TRACE) {
+  if (method == HE_RING_PACK_KEYSWITCH1) {
+    // keys [j][part (alpha, beta)][mod (q0, q1, P1, P2)][N], NTT domain: beta = -alpha s + e + P1 P2 s_j(X^k)
+    // mod q0, q1 (0 mod P1, P2); key id 0x300 + j, one digit (i = 0)
+    const uint32_t P2 = ring_pack_p2(c->R);
+    if (!P2) s = fail(HE_EINVAL, "no second special prime");
+    NttTable t2{};
+    uint32_t* snew = nullptr;
+    if (!s && ntt_table_init(t2, N, P2) != cudaSuccess) s = fail(HE_ECUDA, "P2 tables");
+    if (!s && cudaMallocAsync(&snew, 4ull * N * sizeof(uint32_t), st) != cudaSuccess) s = fail(HE_ENOMEM, "alloc");
+    const Mods4 M4 = make_mods4(c->R, P2);
+    const NttTable* tab[4] = {&c->ntt[0], &c->ntt[1], &c->ntt[2], &t2};
+    for (int mi = 0; mi < 4 && !s; ++mi) {
+      k_reduce_signed<<<grid_for(N), 256, 0, st>>>(s_dev, N, M4.m[mi], snew + (size_t)mi * N);
+      if (ntt_forward(*tab[mi], snew + (size_t)mi * N, 1, N, st) != cudaSuccess) s = fail(HE_ECUDA, "NTT(s)");
+    }
+    for (uint32_t j = 0; j < k && !s; ++j) {
+      k_ms_component<<<grid_for(N), 256, 0, st>>>(s_dev, N, k, j, sk);
+      for (int mi = 0; mi < 4 && !s; ++mi) {
+        const uint32_t q = M4.m[mi];
+        const uint32_t g = mi < 2 ? (uint32_t)((uint64_t)(c->R.P % q) * (P2 % q) % q) : 0u;
+        uint32_t* alpha = keys_dev + ((size_t)j * 8 + 0 * 4 + mi) * N;
+        uint32_t* beta = keys_dev + ((size_t)j * 8 + 1 * 4 + mi) * N;
+        k_ksk_prep<<<grid_for(N), 256, 0, st>>>(M.rng, seed, 0x300 + j, 0, (uint32_t)mi, q, g, sk, N, alpha, beta);
+        if (ntt_forward(*tab[mi], alpha, 1, N, st) != cudaSuccess || ntt_forward(*tab[mi], beta, 1, N, st) != cudaSuccess)
+          s = fail(HE_ECUDA, "NTT(key)");
+        k_ksk_beta<<<grid_for(N), 256, 0, st>>>(alpha, snew + (size_t)mi * N, N, q, beta);
+      }
+    }
+    if (snew) cudaFreeAsync(snew, st);
+    cudaStreamSynchronize(st);
+    ntt_table_free(t2);
+  } else if (method == HE_RING_PACK_TRACE) {
     for (int lv = 1; lv <= logk && !s; ++lv) {  // sigma_g(s) -> s, g = 1 + 2^l d
       k_secret_auto<<<grid_for(N), 256, 0, st>>>(s_dev, N, (d << lv) + 1, sk);
       s = make_ksk_dev(M, seed, 0x100 + lv, sk, s_dev, N, c->ntt, keys_dev + (size_t)(lv - 1) * 12 * N, st);
@@ -1156,10 +1356,11 @@ extern "C" he_status he_ring_pack_keygen(const he_context* c, int method, uint64
 extern "C" he_status he_ring_pack_plan_create(const he_context* c, uint32_t n_out, int method,
                                               he_ring_pack_plan** out) {
   if (!c || !out) return fail(HE_EINVAL, "null argument");
-  if (method != HE_RING_PACK_KEYSWITCH && method != HE_RING_PACK_TRACE) return fail(HE_EINVAL, "unknown method %d", method);
+  if (!rp_method_ok(method)) return fail(HE_EINVAL, "unknown method %d", method);
   const uint32_t k = c->R.k;
   if (n_out == 0 || n_out % k) return fail(HE_EINVAL, "n_out (%u) must be a positive multiple of k = %u", n_out, k);
   if (k > 256 || c->R.d % 32) return fail(HE_EINVAL, "ring packing needs k <= 256 and d a multiple of 32");
+  if (method == HE_RING_PACK_KEYSWITCH1 && k % 4) return fail(HE_EINVAL, "keyswitch1 packing needs k %% 4 == 0");
   he_ring_pack_plan* p = new (std::nothrow) he_ring_pack_plan();
   if (!p) return fail(HE_ENOMEM, "out of host memory");
   p->ctx = c;
@@ -1175,7 +1376,7 @@ extern "C" he_status he_ring_pack_plan_create(const he_context* c, uint32_t n_ou
   static const int env_jc = getenv("HE_MS_JC") ? atoi(getenv("HE_MS_JC")) : 0;       // components per pass
   if (method == HE_RING_PACK_TRACE) {
     p->chunk = env_chunk > 0 ? (uint32_t)env_chunk : 8;
-  } else {
+  } else {   // both key-switch methods
     p->chunk = env_chunk > 0 && env_chunk <= kMsMaxYc ? (uint32_t)env_chunk : kMsMaxYc;
     p->jc = env_jc > 0 ? (uint32_t)env_jc : 32;  // measured: 4 -> 14.6, 16 -> 11.8, 32 -> 11.0, 64 -> 10.8 ms
     if (p->jc > k) p->jc = k;
@@ -1192,6 +1393,21 @@ extern "C" he_status he_ring_pack_plan_create(const he_context* c, uint32_t n_ou
   }
   p->q1inv = (uint32_t)powmod_h(p->M.m[1] % p->M.m[0], p->M.m[0] - 2, p->M.m[0]);
   p->q1invp = shoup_pre(p->q1inv, p->M.m[0]);
+  if (method == HE_RING_PACK_KEYSWITCH1) {
+    const uint32_t P2 = ring_pack_p2(c->R);
+    if (!P2 || ntt_table_init(p->ntt_p2, c->R.N, P2) != cudaSuccess) {
+      delete p;
+      return fail(HE_EINVAL, "no NTT-friendly second special prime for N = %u", c->R.N);
+    }
+    p->M4 = make_mods4(c->R, P2);
+    const uint32_t q0 = p->M4.m[0], q1 = p->M4.m[1], P1 = p->M4.m[2];
+    p->q0inv_q1 = (uint32_t)powmod_h(q0 % q1, q1 - 2, q1);
+    p->p1inv_p2 = (uint32_t)powmod_h(P1 % P2, P2 - 2, P2);
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t qi = p->M4.m[i];
+      p->ppinv[i] = (uint32_t)powmod_h((uint64_t)(P1 % qi) * (P2 % qi) % qi, qi - 2, qi);
+    }
+  }
   // NTT-domain tables at degree N: output c of the forward transform holds p(psi^{2 brv(c) + 1})
   const uint32_t N = p->N, logN = p->logN, logk = p->logk;
   std::vector<uint32_t> h((size_t)logk * N * 3);
@@ -1235,6 +1451,7 @@ extern "C" he_status he_ring_pack_plan_create(const he_context* c, uint32_t n_ou
 extern "C" he_status he_ring_pack_plan_destroy(he_ring_pack_plan* p) {
   if (p) {
     if (p->tables) cudaFree(p->tables);
+    ntt_table_free(p->ntt_p2);
     delete p;
   }
   return HE_OK;
@@ -1255,6 +1472,11 @@ static uint64_t rp_ws_words(const he_ring_pack_plan* p, RpWs* w, uint32_t* base)
   if (p->method == HE_RING_PACK_KEYSWITCH) {  // D [3][2][jc * Yc][N], UW [3][2][Yc][N]
     take(r.D, 6ull * p->jc * p->chunk * N);
     take(r.UW, 6ull * p->chunk * N);
+    return off;
+  }
+  if (p->method == HE_RING_PACK_KEYSWITCH1) {  // D [4][jc * Yc][N], UW [4][2][Yc][N]
+    take(r.D, 4ull * p->jc * p->chunk * N);
+    take(r.UW, 8ull * p->chunk * N);
     return off;
   }
   take(r.A0, 2ull * cnt * 2 * N);
@@ -1307,6 +1529,30 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
     }
     HE_CUDA(cudaGetLastError(), "ring pack launch");
     if (ledger) ledger->rescales += p->blocks;  // k key switches per block, no rotations
+    return HE_OK;
+  }
+  if (p->method == HE_RING_PACK_KEYSWITCH1) {
+    const NttTable* tab[4] = {&c->ntt[0], &c->ntt[1], &c->ntt[2], &p->ntt_p2};
+    for (uint32_t Y0 = 0; Y0 < p->blocks; Y0 += p->chunk) {
+      const uint32_t Yc = (p->blocks - Y0 < p->chunk) ? p->blocks - Y0 : p->chunk;
+      const uint32_t cnt = p->jc * Yc;
+      HE_CUDA(cudaMemsetAsync(w.UW, 0, 8ull * Yc * N * sizeof(uint32_t), st), "memset");
+      for (uint32_t j0 = 0; j0 < k; j0 += p->jc) {
+        k_ms1_digits<<<dim3(d / kMs1M, cnt), 256, 0, st>>>(raw_a, p->n_out, Y0, j0, Yc, cnt, d, k, N, p->M4,
+                                                           p->q0inv_q1, w.D);
+        for (int mod = 0; mod < 4; ++mod)
+          HE_CUDA(ntt_forward(*tab[mod], w.D + (size_t)mod * cnt * N, cnt, N, st), "NTT(digits)");
+        k_ms1_mac<<<dim3((unsigned)(((uint64_t)Yc * N / 4 + 255) / 256), 4), 256, 0, st>>>(
+            w.D, gal + (size_t)j0 * 8 * N, p->jc, Yc, p->logN, p->M4, w.UW);
+      }
+      for (int mod = 0; mod < 4; ++mod)
+        HE_CUDA(ntt_inverse(*tab[mod], w.UW + (size_t)mod * 2 * Yc * N, 2 * Yc, N, st), "INTT(U, W)");
+      k_ms1_finish<<<grid_for((uint64_t)Yc * N), 256, 0, st>>>(w.UW, raw_b, p->blocks, Y0, Yc, p->logN, p->M4,
+                                                                p->p1inv_p2, p->ppinv[0], p->ppinv[1], p->q1inv,
+                                                                p->q1invp, out);
+    }
+    HE_CUDA(cudaGetLastError(), "ring pack launch");
+    if (ledger) ledger->rescales += p->blocks;
     return HE_OK;
   }
   const uint32_t* perm_base = p->tables;

@@ -39,6 +39,7 @@ EXPORTS = (
     "he_chacha20_block", "he_chain_create", "he_chain_destroy", "he_chain_encrypt", "he_chain_key_id",
     "he_chain_key_words", "he_chain_rotation_keygen", "he_chain_encode_pts", "he_chain_map_create",
     "he_chain_map_destroy", "he_chain_map_workspace_bytes", "he_chain_map_run", "he_chain_decrypt",
+    "he_ring_pack_special2",
 )
 
 
@@ -130,6 +131,7 @@ def lib():
             "he_chain_destroy": (st, [vp]),
             "he_chain_encrypt": (st, [vp, vp, vp, u32, u32, u64, u32, vp, vp]),
             "he_chain_decrypt": (st, [vp, vp, vp, u32, u32, u32, vp, vp]),
+            "he_ring_pack_special2": (st, [vp, ctypes.POINTER(u32)]),
             "he_chain_key_id": (u32, [u32, u32]),
             "he_chain_key_words": (st, [vp, u32, ctypes.POINTER(u64)]),
             "he_chain_rotation_keygen": (st, [vp, u64, vp, u32, vp, u32, vp, vp]),

@@ -9,10 +9,12 @@ in the activation coefficient layout of ``HeContext.encrypt_acts`` (so the resul
 Pipeline (all on the device, include/he_b200.h he_pcmm_run_level1 / he_ring_pack_*;
 restated in oracle/he_oracle_rhombus.c): the PCMM at level 1 without the rescale (both limbs'
 words), then one of two packings, then the rescale by q1 -> level 0:
-  "keyswitch" (default, or_mlwe_to_rlwe): MLWE -> RLWE key switching -- block Y's packed phase is
+  "keyswitch" (or_mlwe_to_rlwe): MLWE -> RLWE key switching -- block Y's packed phase is
       b'_Y + sum_j alpha_j(X) s_j(X^k), alpha_j[t + k m] = a'_{kY+t}[j][m]; one hybrid key switch
       (dnum 2, special prime P) per component j from s_j(X^k) to s, summed before one ModDown.
       k keys (~805 MB at Llama parameters), 6 NTTs per (block, j), no automorphisms.
+  "keyswitch1" (default, or_mlwe_to_rlwe1): the same with ONE digit (alpha_j mod q0 q1 itself) and two special primes
+      P1 = P, P2 (he_ring_pack_special2): 4 NTTs per (block, j) instead of 6, 8 key planes instead of 12.
   "trace" (or_ring_pack): PackLWEs over the subring Z[X^k] on leaves C_y with A_y[k m - j] =
       a'_y[j][m], B_y[k m] = b'_y[m] scaled by k^-1: log2 k levels of E + X^{k/2^l} O +
       sigma_g(E - X^{k/2^l} O), g = 1 + 2^l d, each automorphism followed by a Galois key switch.
@@ -33,7 +35,7 @@ from .context import CtBlocks, HeContext, SecretKey, _torch
 from .pcmm import MlwePcmmPlan, _check_operand, _note_read
 
 
-METHODS = {"keyswitch": 0, "trace": 1}
+METHODS = {"keyswitch": 0, "trace": 1, "keyswitch1": 2}
 
 
 def _method(method: str) -> int:
@@ -45,14 +47,15 @@ def _method(method: str) -> int:
 @dataclass
 class RingPackKeys:
     gal: object          # keyswitch: u32 [k, 2, 2, 3, N] keys s_j(X^k) -> s; trace: u32 [log2 k, 2, 2, 3, N]
-                         # Galois keys sigma_{1 + 2^l d}(s) -> s; NTT domain
-    method: str = "keyswitch"
+                         # Galois keys sigma_{1 + 2^l d}(s) -> s; keyswitch1: u32 [k, 2, 4, N] one-digit keys
+                         # modulo q0 q1 P1 P2; NTT domain
+    method: str = "keyswitch1"
 
 
 @dataclass
 class RingPackPlan:
     n_out: int
-    method: str = "keyswitch"
+    method: str = "keyswitch1"
     _handle: object = field(default=None, repr=False)
     _workspace: object = field(default=None, repr=False)
     _raw: tuple = field(default=None, repr=False)
@@ -83,19 +86,20 @@ class RingPackPlan:
             pass
 
 
-def ring_pack_keygen(ctx: HeContext, sk: SecretKey, seed: int | None = None, method: str = "keyswitch") -> RingPackKeys:
+def ring_pack_keygen(ctx: HeContext, sk: SecretKey, seed: int | None = None, method: str = "keyswitch1") -> RingPackKeys:
     torch = _torch()
     seed = ctx.nonce(seed)
     m = _method(method)
     nb = ctypes.c_uint64()
     native.call("he_ring_pack_key_bytes", ctx.handle, m, ctypes.byref(nb))
-    gal = torch.empty((nb.value // (4 * 12 * ctx.params.N), 2, 2, 3, ctx.params.N), dtype=torch.int32,
-                      device=ctx.device)
+    N = ctx.params.N
+    shape = (nb.value // (4 * 8 * N), 2, 4, N) if m == 2 else (nb.value // (4 * 12 * N), 2, 2, 3, N)
+    gal = torch.empty(shape, dtype=torch.int32, device=ctx.device)
     native.call("he_ring_pack_keygen", ctx.handle, m, seed, sk.s.data_ptr(), gal.data_ptr(), ctx.stream())
     return RingPackKeys(gal, method)
 
 
-def make_ring_pack_plan(ctx: HeContext, n_out: int, method: str = "keyswitch") -> RingPackPlan:
+def make_ring_pack_plan(ctx: HeContext, n_out: int, method: str = "keyswitch1") -> RingPackPlan:
     h = ctypes.c_void_p()
     native.call("he_ring_pack_plan_create", ctx.handle, int(n_out), _method(method), ctypes.byref(h))
     return RingPackPlan(int(n_out), method, _handle=h, _ctx_keepalive=ctx._dev)

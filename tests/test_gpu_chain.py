@@ -96,7 +96,7 @@ def test_lower_stc_pcmm_ringpack_modraise_chain_toy():
     rk = ring_pack_keygen(ctx, sk, 5)
     Yp = pcmm_packed(ctx, pplan, make_ring_pack_plan(ctx, W.shape[0]), rk, Xc)
     raw = [O.pcmm_limb(P, O.encode_weights(P, W), ct, L) for L in range(2)]
-    ref_rp = O.mlwe_to_rlwe(P, *O.raw_device_layout(P, raw), O.mlwe_ks_keys(P, 5, s))
+    ref_rp = O.mlwe_to_rlwe1(P, *O.raw_device_layout(P, raw), O.mlwe_ks_keys1(P, 5, s))
     assert np.array_equal(u32(Yp.data)[:, 0], ref_rp)
     assert np.abs(ctx.decrypt_acts(sk, Yp) - clear_pcmm(W, A)).max() < 2 ** -12
     raised = mod_raise(ctx, Yp, list(P.moduli[2:]))

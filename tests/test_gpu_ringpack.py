@@ -19,7 +19,7 @@ from test_gpu_pcmm import setup, u32
 
 pytestmark = pytest.mark.gpu
 ALGOS = ["spectral", "direct"]
-METHODS = ["keyswitch", "trace"]
+METHODS = ["keyswitch", "trace", "keyswitch1"]
 
 
 def _raw_oracle(P, W, A):
@@ -48,10 +48,20 @@ def test_toy_keys_match_oracle(method):
     P = HeParams.toy()
     ctx, sk, A, W, X = setup(P, 16, 16)
     keys = ring_pack_keygen(ctx, sk, seed=5, method=method)
-    ref = (O.ring_pack_keys if method == "trace" else O.mlwe_ks_keys)(P, 5, O.keygen(P, 7))
-    # device keys are NTT-domain: compare after the inverse transform per modulus
     import torch
 
+    if method == "keyswitch1":   # [k, 2, 4, N]: q0, q1, P1 through the context's inverse NTTs (P2 via the output)
+        ref = O.mlwe_ks_keys1(P, 5, O.keygen(P, 7))
+        g = keys.gal.clone()
+        for j in range(3):
+            blk = g[:, :, j, :].contiguous().reshape(-1, P.N)
+            ctx_ntt_inverse(ctx, blk, j)
+            g[:, :, j, :] = blk.reshape(g.shape[0], 2, P.N)
+        torch.cuda.synchronize()
+        assert np.array_equal(u32(g)[:, :, :3], ref[:, :, :3])
+        return
+    ref = (O.ring_pack_keys if method == "trace" else O.mlwe_ks_keys)(P, 5, O.keygen(P, 7))
+    # device keys are NTT-domain: compare after the inverse transform per modulus
     g = keys.gal.clone()
     lg, N = g.shape[0], P.N
     for j in range(3):
@@ -79,6 +89,8 @@ def test_toy_packed_ciphertexts_bit_exact_and_decrypt(n_out, n_in, algo, method)
     s = O.keygen(P, 7)
     if method == "trace":
         ref = O.ring_pack(P, O.ring_pack_leaves(P, raw), O.ring_pack_keys(P, 5, s))[1]
+    elif method == "keyswitch1":
+        ref = O.mlwe_to_rlwe1(P, *O.raw_device_layout(P, raw), O.mlwe_ks_keys1(P, 5, s))
     else:
         ref = O.mlwe_to_rlwe(P, *O.raw_device_layout(P, raw), O.mlwe_ks_keys(P, 5, s))
     keys = ring_pack_keygen(ctx, sk, seed=5, method=method)

@@ -186,3 +186,21 @@ def test_mlwe_keyswitch_packing_matches_trace_packing_plaintext():
     assert np.abs(ph_ks - ph_tr).max() < 64
     ref = A @ W.T
     assert np.abs(O.decode_acts(P, ph_ks, n_out) - ref).max() < np.abs(ref).max() * 2.0 ** -14
+
+
+def test_oracle_one_digit_ring_packing_decrypts():
+    """or_mlwe_to_rlwe1 (one digit, special modulus P1 P2) packs the toy PCMM output to the same plaintext as the
+    two-digit or_mlwe_to_rlwe (both decrypt to A W^T within 2^-16)."""
+    P = HeParams.toy()
+    rng = np.random.default_rng(1)
+    n_out, n_in = 32, 48
+    A = rng.uniform(-1, 1, (P.tokens, n_in))
+    W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
+    s = O.keygen(P, 7)
+    ct = O.encrypt(P, 11, s, O.encode_acts(P, A))
+    raw = [O.pcmm_limb(P, O.encode_weights(P, W), ct, L) for L in range(2)]
+    rb, ra = O.raw_device_layout(P, raw)
+    assert O.ring_pack_special2(P) not in (*P.moduli, P.special_prime)
+    for out in (O.mlwe_to_rlwe1(P, rb, ra, O.mlwe_ks_keys1(P, 5, s)), O.mlwe_to_rlwe(P, rb, ra, O.mlwe_ks_keys(P, 5, s))):
+        dec = O.decode_acts(P, O.decrypt_rlwe(P, out[:, None], s), n_out)
+        assert np.abs(dec - A @ W.T).max() < 2 ** -16
