@@ -160,6 +160,27 @@ def test_llama_sampled_words_bit_exact_and_precision(n_out, n_in, algo):
 
 
 @pytest.mark.parametrize("n_out,n_in", LLAMA_SHAPES)
+def test_llama_last_row_block_every_word(n_out, n_in):
+    """Every word of the LAST 256-row output block (all 65 792 columns, b' and a') of each Llama-2-7B /
+    Llama-3-8B projection shape on the default (spectral) path equals the oracle's exact BCHPS24 Alg. 2 on the
+    same ciphertexts (the bench checks the FIRST block of the metric shape the same way)."""
+    import torch
+
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, n_out, n_in, seed=7)
+    Y = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W), X)
+    torch.cuda.synchronize()
+    k, d = P.mlwe_rank, P.mlwe_degree
+    y0 = n_out - k
+    ref = O.pcmm(P, O.encode_weights(P, W), u32(X.data), rows=list(range(y0, n_out)))
+    got_a = u32(Y.out_a[y0:n_out])
+    got_b = u32(Y.out_b[y0 // k])
+    assert np.array_equal(got_a, ref[:, d:]), f"{int((got_a != ref[:, d:]).sum())} a' words differ"
+    for t in range(k):
+        assert np.array_equal(got_b[t + k * np.arange(d)], ref[t, :d]), f"b' row {y0 + t}"
+
+
+@pytest.mark.parametrize("n_out,n_in", LLAMA_SHAPES)
 def test_spectral_equals_direct_every_word(n_out, n_in):
     """The two a'-column algorithms agree on ALL n_out x 65 792 output words (random weights);
     the direct K1 words are themselves oracle-pinned on samples and by the selection identity."""
