@@ -103,6 +103,7 @@ struct SpecInvConst {
   uint32_t linv[2], linvp[2];
   uint32_t q1inv, q1invp;
   uint32_t* out1 = nullptr;  // level-1 mode: no rescale; limb-0 words -> out_a, limb-1 words -> out1 (same layout)
+  uint32_t q1bar = 0;        // floor(2^32 / q[1]) (set by launch_spec_inverse for the lazy q1 limb of S4 v2)
 };
 cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out, uint32_t n_in, uint32_t k,
                                 const SpecTable& t, int D, uint32_t r_pad, int8_t* out, cudaStream_t s);

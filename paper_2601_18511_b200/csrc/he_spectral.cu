@@ -537,15 +537,21 @@ struct Inv1kLimb {
   const uint2* r2;
   uint32_t q;
 };
+// Lazy q1 limb (LAZY1, when 42 q1 < 2^32 -- the 21-bit q1): no correction of x in its butterflies (values grow
+// by at most 2 q per twiddled stage and double per twiddle-1 stage: < 42 q after the 10 stages), one Barrett
+// reduction at the end.  Outputs: limb 0 in [0, 2 q0), limb 1 in [0, q1).
+HE_D void bfl(uint32_t& x, uint32_t& y, uint2 w, uint32_t q2, uint32_t q) {  // DIT, x not corrected
+  const uint32_t t = y * w.x - __umulhi(y, w.y) * q;
+  const uint32_t a = x;
+  x = a + t;
+  y = a + q2 - t;
+}
+template <bool LAZY1>
 HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_t lane, uint32_t (&x)[2][32]) {
 #pragma unroll
   for (int l = 0; l < 2; ++l) ld_row32(L[l].col + 36 * lane, x[l]);
 #pragma unroll
-  for (int e = 0; e < 32; e += 2)
-#pragma unroll
-    for (int l = 0; l < 2; ++l) dit_bf1(x[l][e], x[l][e + 1], 2 * L[l].q);
-#pragma unroll
-  for (int s = 1; s < 5; ++s) {
+  for (int s = 0; s < 5; ++s) {
     const int len = 1 << s;
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
@@ -553,8 +559,20 @@ HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_
       const int off = e & (len - 1);
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
-        if (off == 0) dit_bf1(x[l][e], x[l][e + len], 2 * L[l].q);
-        else dit_bf(x[l][e], x[l][e + len], cst.r1[l][(1 << s) - s - 1 + off - 1], 2 * L[l].q, L[l].q);
+        const bool lazy = LAZY1 && l == 1;
+        if (off == 0) {
+          if (lazy) {  // inputs < 2^s q: K = 2^s q keeps x + K - y >= 0
+            const uint32_t u = x[l][e], v = x[l][e + len];
+            x[l][e] = u + v;
+            x[l][e + len] = u + (L[l].q << s) - v;
+          } else {
+            dit_bf1(x[l][e], x[l][e + len], 2 * L[l].q);
+          }
+        } else {
+          const uint2 w = cst.r1[l][(1 << s) - s - 1 + off - 1];
+          if (lazy) bfl(x[l][e], x[l][e + len], w, 2 * L[l].q, L[l].q);
+          else dit_bf(x[l][e], x[l][e + len], w, 2 * L[l].q, L[l].q);
+        }
       }
     }
   }
@@ -574,8 +592,11 @@ HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_
     for (int e = 0; e < 32; ++e) {
       if (e & len) continue;
 #pragma unroll
-      for (int l = 0; l < 2; ++l)
-        dit_bf(x[l][e], x[l][e + len], L[l].r2[base + 32 * (e & (len - 1)) + lane], 2 * L[l].q, L[l].q);
+      for (int l = 0; l < 2; ++l) {
+        const uint2 w = L[l].r2[base + 32 * (e & (len - 1)) + lane];
+        if (LAZY1 && l == 1) bfl(x[l][e], x[l][e + len], w, 2 * L[l].q, L[l].q);
+        else dit_bf(x[l][e], x[l][e + len], w, 2 * L[l].q, L[l].q);
+      }
     }
   }
   // len = 512: pairs (e, e + 16); the upper output u = lane + 32 e + 512 is needed only for e < 8
@@ -583,25 +604,29 @@ HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_
   for (int e = 0; e < 16; ++e) {
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
+      const bool lazy = LAZY1 && l == 1;
       const uint32_t q = L[l].q, q2 = 2 * q;
       const uint2 w = L[l].r2[480 + 32 * e + lane];
       if (e < 8) {
-        dit_bf(x[l][e], x[l][e + 16], w, q2, q);
+        if (lazy) bfl(x[l][e], x[l][e + 16], w, q2, q);
+        else dit_bf(x[l][e], x[l][e + 16], w, q2, q);
       } else {
         const uint32_t t = x[l][e + 16] * w.x - __umulhi(x[l][e + 16], w.y) * q;
-        x[l][e] = min(x[l][e], x[l][e] - q2) + t;
+        x[l][e] = (lazy ? x[l][e] : min(x[l][e], x[l][e] - q2)) + t;
       }
     }
   }
 #pragma unroll
-  for (int l = 0; l < 2; ++l)
-#pragma unroll
-    for (int e = 0; e < 24; ++e) {
-      const uint32_t v = min(x[l][e], x[l][e] - 2 * L[l].q);
-      x[l][e] = min(v, v - L[l].q);
-    }
+  for (int e = 0; e < 24; ++e) {
+    x[0][e] = min(x[0][e], x[0][e] - 2 * L[0].q);   // [0, 2 q0)
+    uint32_t v = x[1][e];
+    if (LAZY1) v -= __umulhi(v, cst.q1bar) * L[1].q;   // v < 42 q1 < 2^32: quotient off by at most one
+    else v = min(v, v - 2 * L[1].q);
+    x[1][e] = min(v, v - L[1].q);                       // [0, q1)
+  }
 }
 
+template <bool LAZY1>
 __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t* __restrict__ c0,
                                                                   const uint32_t* __restrict__ c1, uint32_t n_out,
                                                                   uint32_t row0, uint32_t nbp, uint32_t nblk,
@@ -643,21 +668,23 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
     const uint32_t q0 = cst.q[0], q1 = cst.q[1];
     const Inv1kLimb L[2] = {{xs0 + b * kInv1kLd, tws, q0}, {xs1 + b * kInv1kLd, tws + 992, q1}};
     uint32_t x[2][32];
-    inv1024_pair(L, cst, lane, x);
+    inv1024_pair<LAZY1>(L, cst, lane, x);
     if (cst.out1) {  // level-1 mode: both limbs, no rescale
 #pragma unroll
       for (int e = 0; e < 24; ++e) {
-        xs0[b * kInv1kLd + lane + 32 * e + (e >> 3)] = x[0][e];
+        xs0[b * kInv1kLd + lane + 32 * e + (e >> 3)] = min(x[0][e], x[0][e] - q0);
         xs1[b * kInv1kLd + lane + 32 * e + (e >> 3)] = x[1][e];
       }
     } else
 #pragma unroll
     for (int e = 0; e < 24; ++e) {
-      uint32_t t;
-      if (x[1][e] > (q1 >> 1)) t = csub(x[0][e] + (q1 - x[1][e]), q0);
-      else t = sub_mod(x[0][e], x[1][e], q0);
+      // (x0 - [x1]_centred) q1^-1 mod q0, branch-free: t = x0 + q0 - x1 (+ q1 when x1 > q1 / 2) < 3 q0 + q1,
+      // one Shoup product (any 32-bit input) -> [0, 2 q0), one correction
+      const uint32_t x0 = x[0][e], x1 = x[1][e];
+      const uint32_t t = x0 + q0 - x1 + (x1 > (q1 >> 1) ? q1 : 0u);
+      const uint32_t v = t * cst.q1inv - __umulhi(t, cst.q1invp) * q0;
       // u = lane + 32 e stored at u + u / 256 (the three thirds of a block one bank apart for phase C)
-      xs1[b * kInv1kLd + lane + 32 * e + (e >> 3)] = shoup_mul(t, cst.q1inv, cst.q1invp, q0);
+      xs1[b * kInv1kLd + lane + 32 * e + (e >> 3)] = min(v, v - q0);
     }
   }
   __syncthreads();
@@ -1015,9 +1042,14 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
     if (Rg.k != 256) return cudaErrorInvalidValue;
     dim3 grid((nblk + kInv1kBlocks - 1) / kInv1kBlocks, rows);
     const size_t smem = (size_t)2 * kInv1kBlocks * kInv1kLd * sizeof(uint32_t) + 2 * 992 * sizeof(uint2);
-    cudaError_t e = cudaFuncSetAttribute(spec_inverse1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    SpecInvConst c2 = cst;
+    c2.q1bar = (uint32_t)(0x100000000ull / cst.q[1]);
+    static const bool strict = getenv("HE_S4_STRICT") != nullptr;  // A/B switch: corrected q1 butterflies
+    const bool lazy = !strict && 42ull * cst.q[1] < 0x100000000ull;
+    auto kern = lazy ? spec_inverse1024_kernel<true> : spec_inverse1024_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    spec_inverse1024_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, nbp, nblk, Rg.d, cst, out_a, peers);
+    kern<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, nbp, nblk, Rg.d, c2, out_a, peers);
     return cudaGetLastError();
   }
   static const bool generic = getenv("HE_SPEC_INV_GENERIC") != nullptr;  // debug: the simple S4
