@@ -97,6 +97,23 @@ static he_status make_map_u32(CUtensorMap* m, const void* base, uint64_t inner, 
   return HE_OK;
 }
 
+// u32 [planes][rows][inner] tensor boxed as {box_inner, 1 row, box_planes}: the box takes one row of each of
+// box_planes consecutive planes (S3's C^ store: 8 blocks of one frequency for 32 output rows)
+static he_status make_map_u32_rows(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t planes,
+                                   uint32_t box_inner, uint32_t box_planes, uint64_t extent) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {extent, rows, planes};
+  cuuint64_t strides[2] = {inner * 4, inner * rows * 4};
+  cuuint32_t box[3] = {box_inner, 1, box_planes};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled (u32 rows) failed (%d)", (int)r);
+  return HE_OK;
+}
+
 // 4-D int8 tensor with explicit strides (bytes), box {128, box_rows, 1, 1}, 128-B swizzle
 static he_status make_map4(CUtensorMap* m, const void* base, const uint64_t dims_in[4], const uint64_t strides_in[3],
                            uint32_t box_rows) {
@@ -592,6 +609,17 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     a.off64 = p->spec_off[L];
     for (int i = 0; i < 8; ++i) a.pw[i] = (int32_t)powmod_h(2, 16ull * i + 32, q);
     a.out = C[L];
+    // S3 L2 policy (tiles run y-tile-major, SpecGemmArgs): G^ normal, A^ evict-last, C^ stores evict-first (measured
+    // 1.02 ms for both limbs at 4096x11008 vs 1.10 with G^ evict-last, 1.39 with G^ evict-first);
+    // HE_S3_HINTS=<g><a><c> (digits 0 first / 1 normal / 2 last) overrides for measurements
+    if (const char* h = getenv("HE_S3_HINTS")) {
+      static const uint64_t pol[3] = {0x12F0000000000000ULL, 0x1000000000000000ULL, 0x14F0000000000000ULL};
+      if (strlen(h) == 3) {
+        a.hint_g = pol[(h[0] - '0') % 3];
+        a.hint_a = pol[(h[1] - '0') % 3];
+        a.hint_c = pol[(h[2] - '0') % 3];
+      }
+    }
     const int8_t* A = base + (L ? w.a1 : w.a0);
     if (simple) {
       const int8_t* G = p->spec_w + (L ? (uint64_t)p->L * p->dsp[0] * p->n_out * p->r_pad : 0);
@@ -601,8 +629,8 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     CUtensorMap tmB;
     he_status s = make_map_sw64(&tmB, A, p->r_pad, p->nbp, (uint64_t)p->L * p->dsp[L], 16);
     if (s) return s;
-    CUtensorMap tmC;  // C^ limb L: u32 {d, n_out, 2k}, box {8, 32, 1} (one epilogue warp's TMA store)
-    s = make_map_u32(&tmC, C[L], p->nbp, p->n_out, p->L, 8, 32, p->nblk);  // padding blocks are never stored
+    CUtensorMap tmC;  // C^ limb L: u32 [n_out][L][nbp], box {8 blocks, 1 f, 32 rows} (one epilogue warp's TMA store)
+    s = make_map_u32_rows(&tmC, C[L], p->nbp, p->L, p->n_out, 8, 32, p->nblk);  // padding blocks are never stored
     if (s) return s;
     p->prof_begin(3 + L, st);
     HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, tmC, a, p->ctx->sm_count, st), "spectral gemm");

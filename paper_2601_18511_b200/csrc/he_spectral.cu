@@ -308,10 +308,11 @@ __global__ void __launch_bounds__(512) spec_data1024_kernel(const uint32_t* __re
 }
 
 // ---------------------------------------------------------------- S4: inverse transform + rescale + store
-// One CTA per (row y, group of 32 blocks m).  C^ limb i: [L][n_out][d] u32.
+// One CTA per (row y, group of 32 blocks m).  C^ limb i: [n_out][L][nbp] u32 (row-major in y: S3 writes and S4
+// reads each row's L x nbp words as one contiguous region).
 constexpr int kSpecMGroup = 32;
 __global__ void __launch_bounds__(256) spec_inverse_kernel(const uint32_t* __restrict__ c0, const uint32_t* __restrict__ c1,
-                                                           uint32_t n_out, uint32_t row0, uint32_t d, uint32_t k,
+                                                           uint32_t nbp, uint32_t row0, uint32_t d, uint32_t k,
                                                            uint32_t L, SpecInvConst cst, uint32_t* __restrict__ out_a) {
   extern __shared__ uint32_t sm[];
   const uint32_t ld = L + 1;
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(256) spec_inverse_kernel(const uint32_t* __res
   for (int limb = 1; limb >= 0; --limb) {
     const uint32_t* src = limb ? c1 : c0;
     const uint32_t q = cst.q[limb];
-    for (uint32_t f = warp; f < L; f += nw) xs[lane * ld + f] = src[((size_t)f * n_out + y) * d + m0 + lane];
+    for (uint32_t f = warp; f < L; f += nw) xs[lane * ld + f] = src[((size_t)y * L + f) * nbp + m0 + lane];
     __syncthreads();
     cyc_inv_smem(xs, kSpecMGroup, (int)ld, (int)L, cst.iv[limb], q);
     if (limb) {
@@ -450,7 +451,7 @@ HE_D void inv512_pair(const Inv512Limb (&L)[2], const SpecInvConst& cst, uint32_
 }
 
 __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t* __restrict__ c0,
-                                                                 const uint32_t* __restrict__ c1, uint32_t n_out,
+                                                                 const uint32_t* __restrict__ c1, uint32_t nbp,
                                                                  uint32_t row0, uint32_t d, SpecInvConst cst,
                                                                  uint32_t* __restrict__ out_a) {
   extern __shared__ uint32_t sm[];
@@ -462,9 +463,9 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
   // (16-byte loads; pitch 546 = 2 mod 32 makes the 4 scattered stores per load conflict-free)
   {
     const uint32_t mq = lane & 3;
-    const size_t stride = (size_t)64 * n_out * d;    // 64 rows p
+    const size_t stride = (size_t)64 * nbp;          // 64 rows p
     const uint32_t p_first = warp * 8 + (lane >> 2);
-    const size_t g = ((size_t)p_first * n_out + y) * d + m0 + 4 * mq;
+    const size_t g = ((size_t)y * 512 + p_first) * nbp + m0 + 4 * mq;
     const uint4* g0 = reinterpret_cast<const uint4*>(c0 + g);
     const uint4* g1 = reinterpret_cast<const uint4*>(c1 + g);
 #pragma unroll 4
@@ -642,11 +643,11 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
     reinterpret_cast<uint4*>(tws)[i] = __ldg(reinterpret_cast<const uint4*>(cst.r2[0]) + i);
     reinterpret_cast<uint4*>(tws + 992)[i] = __ldg(reinterpret_cast<const uint4*>(cst.r2[1]) + i);
   }
-  // phase A: C^[p][y][b0 .. b0 + 7] of both limbs -> xs[b][pad(p)]; one warp access = 16 rows p x 32 B
+  // phase A: C^[y][p][b0 .. b0 + 7] of both limbs -> xs[b][pad(p)]; one warp access = 16 rows p x 32 B
   {
     const uint32_t bq = lane & 1, ps = lane >> 1;
-    const size_t g = ((size_t)(warp * 16 + ps) * n_out + y) * nbp + b0 + 4 * bq;
-    const size_t stride = (size_t)128 * n_out * nbp / 4;   // 128 rows p, in uint4
+    const size_t g = ((size_t)y * 1024 + warp * 16 + ps) * nbp + b0 + 4 * bq;
+    const size_t stride = (size_t)128 * nbp / 4;   // 128 rows p, in uint4
     const uint4* g0 = reinterpret_cast<const uint4*>(c0 + g);
     const uint4* g1 = reinterpret_cast<const uint4*>(c1 + g);
     uint4 v0[8], v1[8];   // all 16 loads in flight before the first store
@@ -726,6 +727,12 @@ HE_D void tma_store_3d(const void* map, const void* src, int x, int y, int z) {
                "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
                : "memory");
 }
+HE_D void tma_store_3d_hint(const void* map, const void* src, int x, int y, int z, uint64_t hint) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;"
+               ::"l"(map), "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z), "l"(hint)
+               : "memory");
+}
+
 HE_D void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 HE_D void bulk_wait_read() {
@@ -813,14 +820,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // tile -> (f, y tile, m tile), m fastest; divisions by 32-bit reciprocals (exact for operands < 2^16)
+  // tile -> (y tile, f, m tile), m fastest, y tile slowest: the pairs working at one time cover a run of
+  // frequencies of the same 256 rows, so their C^ stores ([y][f][blk]) fill contiguous per-row regions and
+  // each row's C^ is complete early for S4; divisions by 32-bit reciprocals (exact for operands < 2^16)
   const uint32_t m_magic = (uint32_t)((0xFFFFFFFFull + m_tiles) / m_tiles);
-  const uint32_t y_magic = (uint32_t)((0xFFFFFFFFull + y_tiles) / y_tiles);
+  const uint32_t lg_l = 31 - __clz(args.L);   // L is a power of two
   auto tile_coords = [&](int tile, int& f, int& y0, int& m0) {
     const uint32_t rest = m_tiles == 1 ? (uint32_t)tile : __umulhi((uint32_t)tile, m_magic);
-    const uint32_t fq = y_tiles == 1 ? rest : __umulhi(rest, y_magic);
-    f = (int)fq;
-    y0 = args.row0 + (int)(rest - fq * (uint32_t)y_tiles) * 256;
+    f = (int)(rest & (uint32_t)(args.L - 1));
+    y0 = args.row0 + (int)(rest >> lg_l) * 256;
     m0 = (int)((uint32_t)tile - rest * (uint32_t)m_tiles) * kSpecBN;
   };
 
@@ -842,13 +850,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
 #pragma unroll
           for (int a = 0; a < D; ++a)
             tma_load_3d_2sm(a_dst + a * 128 * kSpecBK, &tmA, &full[stage], kb * kSpecBK, y0 + (int)rank * 128,
-                            f * D + a, kEvictLast);
+                            f * D + a, args.hint_g);
           // stacked operand [P0 | P1 | .. | P(D-1)] x 32 rows: this CTA holds chunks [rank*D, rank*D + D)
 #pragma unroll
           for (int c = 0; c < D; ++c) {
             const int g = (int)rank * D + c;
             tma_load_3d_2sm(b_dst + c * C::kChunk * kSpecBK, &tmB, &full[stage], kb * kSpecBK,
-                            m0 + (g & 1) * C::kChunk, f * D + (g >> 1), kEvictLast);
+                            m0 + (g & 1) * C::kChunk, f * D + (g >> 1), args.hint_a);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -955,7 +963,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        tma_store_3d(&tmC, so, m0 + (int)part * kSpecEpiCols, y0 + (int)rank * 128 + (int)quarter * 32, f);
+        tma_store_3d_hint(&tmC, so, m0 + (int)part * kSpecEpiCols, f, y0 + (int)rank * 128 + (int)quarter * 32,
+                          args.hint_c);
         bulk_commit();
       }
     }
@@ -991,7 +1000,7 @@ __global__ void spec_gemm_simple_kernel(const int8_t* __restrict__ G, const int8
     if (am < 0) am += q;
     accq = (accq + (uint64_t)gm * (uint64_t)am) % q;
   }
-  args.out[((size_t)f * args.n_out + y) * args.nb + m] = (uint32_t)accq;
+  args.out[((size_t)y * args.L + f) * args.nb + m] = (uint32_t)accq;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -1040,7 +1049,6 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
   if (peers.n > 0 && cst.out1) return cudaErrorNotSupported;
   if (L == 1024) {
     if (Rg.k != 256) return cudaErrorInvalidValue;
-    dim3 grid((nblk + kInv1kBlocks - 1) / kInv1kBlocks, rows);
     const size_t smem = (size_t)2 * kInv1kBlocks * kInv1kLd * sizeof(uint32_t) + 2 * 992 * sizeof(uint2);
     SpecInvConst c2 = cst;
     c2.q1bar = (uint32_t)(0x100000000ull / cst.q[1]);
@@ -1049,6 +1057,7 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
     auto kern = lazy ? spec_inverse1024_kernel<true> : spec_inverse1024_kernel<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    dim3 grid((nblk + kInv1kBlocks - 1) / kInv1kBlocks, rows);
     kern<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, nbp, nblk, Rg.d, c2, out_a, peers);
     return cudaGetLastError();
   }
@@ -1058,7 +1067,7 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
     const size_t smem = (size_t)2 * kInv512Cols * kInv512Ld * sizeof(uint32_t);
     cudaError_t e = cudaFuncSetAttribute(spec_inverse512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    spec_inverse512_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, Rg.d, cst, out_a);
+    spec_inverse512_kernel<<<grid, 256, smem, s>>>(c0, c1, nbp, row0, Rg.d, cst, out_a);
     return cudaGetLastError();
   }
   if (Rg.d % kSpecMGroup) return cudaErrorInvalidValue;
@@ -1068,7 +1077,7 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
     cudaError_t e = cudaFuncSetAttribute(spec_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  spec_inverse_kernel<<<grid, 256, smem, s>>>(c0, c1, n_out, row0, Rg.d, Rg.k, L, cst, out_a);
+  spec_inverse_kernel<<<grid, 256, smem, s>>>(c0, c1, nbp, row0, Rg.d, Rg.k, L, cst, out_a);
   return cudaGetLastError();
 }
 
