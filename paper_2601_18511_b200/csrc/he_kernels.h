@@ -60,7 +60,9 @@ struct NttTable {
 };
 cudaError_t ntt_table_init(NttTable& t, uint32_t n, uint32_t q);
 void ntt_table_free(NttTable& t);
-cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s);
+// rows_only: the caller already ran the outer (cols) stages, e.g. fused into the kernel producing the data
+cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s,
+                        bool rows_only = false);
 cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s);
 
 struct RingDims {

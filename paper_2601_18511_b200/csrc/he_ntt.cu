@@ -427,13 +427,14 @@ static bool split(uint32_t n, uint32_t& n1, uint32_t& n2) {
   return false;
 }
 
-cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t st) {
+cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t st,
+                        bool rows_only) {
   uint32_t n1, n2;
   if (!split(t.n, n1, n2)) return cudaErrorInvalidValue;
   if (count == 0) return cudaSuccess;
   const uint2* tw = reinterpret_cast<const uint2*>(t.fw);
   cudaError_t e = cudaSuccess;
-  if (n1 > 1) {
+  if (n1 > 1 && !rows_only) {
     e = with_n1(n1, [&](auto N1) {
       dim3 g((n2 + 255) / 256, count);
       ntt_fwd_cols<decltype(N1)::value><<<g, 256, 0, st>>>(data, stride, n2, tw, t.q);

@@ -1143,6 +1143,81 @@ __global__ void __launch_bounds__(256) k_ms1_digits(const uint32_t* __restrict__
       *reinterpret_cast<uint4*>(D + mod * plane + c) = make_uint4(o[mod][0], o[mod][1], o[mod][2], o[mod][3]);
   }
 }
+// The same digits with the outer (cols) stages of K2's forward NTT fused in, for N = 16 x 4096 and k = 256: the
+// 16-point column c of plane alpha_j holds coefficients c + 4096 v = t + 256 (m0 + 16 v) (t = c % 256,
+// m0 = c / 256), i.e. the positions m = m0 mod 16 of ONE a' row segment -- so a CTA that stages 32 whole row
+// segments a'[t][j][0 .. 255] (both limbs, 1 KB each, coalesced) owns 512 complete columns. Per column: CRT
+// lift to P1, P2, then the 16-point merged-twiddle CT transform of each modulus exactly as ntt_fwd_cols<16>
+// does it (same butterflies, same lazy [0, 4q) outputs), 128-byte stores per (modulus, v). The rows pass then
+// runs as usual (ntt_forward(..., rows_only)). Saves the digit planes' HBM round trip between the two kernels.
+constexpr int kMs1T = 32;                 // rows t per CTA
+constexpr int kMs1Pitch = 257;            // smem words per staged row segment (conflict-free column gathers)
+HE_D void ct_bf_rp(uint32_t& x, uint32_t& y, uint2 w, uint32_t q2, uint32_t q) {  // = he_ntt.cu ct_bf
+  const uint32_t a = min(x, x - q2);
+  const uint32_t t = y * w.x - __umulhi(y, w.y) * q;
+  x = a + t;
+  y = a + q2 - t;
+}
+HE_D void cols16_store(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t q, uint32_t* dst) {
+  const uint32_t q2 = 2 * q;
+#pragma unroll
+  for (int m = 1, t = 8; m < 16; m <<= 1, t >>= 1) {
+#pragma unroll
+    for (int i = 0; i < m; ++i) {
+      const uint2 w = __ldg(tw + m + i);
+#pragma unroll
+      for (int u = 0; u < t; ++u) ct_bf_rp(x[2 * i * t + u], x[2 * i * t + u + t], w, q2, q);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 16; ++v) dst[(size_t)4096 * v] = x[v];
+}
+struct Ms1Tw {
+  const uint2* tw[4];   // forward twiddle tables (W, Shoup) of q0, q1, P1, P2 at N = 2^16
+};
+__global__ void __launch_bounds__(256, 2) k_ms1_digits_cols(const uint32_t* __restrict__ raw_a, uint32_t n_out,
+                                                            uint32_t Y0, uint32_t j0, uint32_t Yc, uint32_t cnt,
+                                                            Mods4 M, uint32_t q0inv_q1, Ms1Tw T,
+                                                            uint32_t* __restrict__ D) {
+  extern __shared__ uint32_t seg[];   // [limb][kMs1T rows t][kMs1Pitch]
+  constexpr uint32_t k = 256, d = 256, N = 65536;
+  const uint32_t t0 = blockIdx.x * kMs1T, idx = blockIdx.y, jj = idx / Yc, Y = idx % Yc, j = j0 + jj;
+  for (uint32_t L = 0; L < 2; ++L) {
+    const uint32_t* src = raw_a + ((size_t)L * n_out + (size_t)(Y0 + Y) * k + t0) * N + (size_t)d * j;
+    for (uint32_t i = threadIdx.x; i < kMs1T * d / 4; i += blockDim.x) {
+      // a warp access = 4 rows x 128 B; stores hit banks r + 4 m4 (+ e): all 32 distinct
+      const uint32_t w = i >> 5, ln = i & 31, r = (w & 7) * 4 + (ln >> 3), m4 = (w >> 3) * 8 + (ln & 7);
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + (size_t)r * N) + m4);
+      uint32_t* o = seg + (L * kMs1T + r) * kMs1Pitch + 4 * m4;
+      o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+    }
+  }
+  __syncthreads();
+  const uint32_t q0 = M.m[0], q1 = M.m[1];
+  const uint64_t Q = (uint64_t)q0 * q1;
+  const size_t plane = (size_t)cnt * N;
+  // thread -> (t = lane, m0 = warp + 8 i): the 32 lanes of a warp gather 32 rows (banks t * 257 = t mod 32)
+  const uint32_t t = threadIdx.x & 31;
+  for (uint32_t m0 = threadIdx.x >> 5; m0 < 16; m0 += blockDim.x >> 5) {
+    uint32_t a0[16], a1[16], x2[16], x3[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      a0[v] = seg[t * kMs1Pitch + m0 + 16 * v];
+      a1[v] = seg[(kMs1T + t) * kMs1Pitch + m0 + 16 * v];
+      // CRT: alpha = a0 + q0 ((a1 - a0) q0^-1 mod q1) in [0, Q), centred (as k_ms1_digits)
+      const uint32_t tq = mulmod_b(sub_mod(a1[v], barrett64(a0[v], M.mu[1], q1), q1), q0inv_q1, M.mu[1], q1);
+      const uint64_t al = (uint64_t)a0[v] + (uint64_t)q0 * tq;
+      const int64_t ac = al > Q / 2 ? (int64_t)al - (int64_t)Q : (int64_t)al;
+      x2[v] = lift_b(ac, M.mu[2], M.m[2]);
+      x3[v] = lift_b(ac, M.mu[3], M.m[3]);
+    }
+    const size_t c = (size_t)idx * N + t0 + t + (size_t)k * m0;
+    cols16_store(a0, T.tw[0], q0, D + c);
+    cols16_store(a1, T.tw[1], q1, D + plane + c);
+    cols16_store(x2, T.tw[2], M.m[2], D + 2 * plane + c);
+    cols16_store(x3, T.tw[3], M.m[3], D + 3 * plane + c);
+  }
+}
 // UW [mod][part][Yc][N] += sum_jj D^[mod][jj Yc + Y] * K_{j0+jj}[part][mod]   (NTT domain; 4 frequencies per thread)
 __global__ void __launch_bounds__(256) k_ms1_mac(const uint32_t* __restrict__ D, const uint32_t* __restrict__ K,
                                                  uint32_t jc, uint32_t Yc, uint32_t logN, Mods4 M,
@@ -1533,15 +1608,29 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
   }
   if (p->method == HE_RING_PACK_KEYSWITCH1) {
     const NttTable* tab[4] = {&c->ntt[0], &c->ntt[1], &c->ntt[2], &p->ntt_p2};
+    // Llama ring (N = 2^16, k = d = 256): digits fused with the NTT's cols pass; HE_RP_UNFUSED=1 keeps the
+    // separate kernels (the path every other ring size takes) for A/B checks
+    const bool fused = getenv("HE_RP_UNFUSED") == nullptr && N == 65536 && k == 256 && d == 256;
+    const size_t fused_smem = (size_t)2 * kMs1T * kMs1Pitch * sizeof(uint32_t);
+    Ms1Tw tw4;
+    for (int mod = 0; mod < 4; ++mod) tw4.tw[mod] = reinterpret_cast<const uint2*>(tab[mod]->fw);
+    if (fused)
+      HE_CUDA(cudaFuncSetAttribute(k_ms1_digits_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem),
+              "smem attribute");
     for (uint32_t Y0 = 0; Y0 < p->blocks; Y0 += p->chunk) {
       const uint32_t Yc = (p->blocks - Y0 < p->chunk) ? p->blocks - Y0 : p->chunk;
       const uint32_t cnt = p->jc * Yc;
       HE_CUDA(cudaMemsetAsync(w.UW, 0, 8ull * Yc * N * sizeof(uint32_t), st), "memset");
       for (uint32_t j0 = 0; j0 < k; j0 += p->jc) {
-        k_ms1_digits<<<dim3(d / kMs1M, cnt), 256, 0, st>>>(raw_a, p->n_out, Y0, j0, Yc, cnt, d, k, N, p->M4,
-                                                           p->q0inv_q1, w.D);
+        if (fused) {   // digits + the NTT's outer stages in one pass over a' (k_ms1_digits_cols)
+          k_ms1_digits_cols<<<dim3(k / kMs1T, cnt), 256, fused_smem, st>>>(raw_a, p->n_out, Y0, j0, Yc, cnt, p->M4,
+                                                                          p->q0inv_q1, tw4, w.D);
+        } else {
+          k_ms1_digits<<<dim3(d / kMs1M, cnt), 256, 0, st>>>(raw_a, p->n_out, Y0, j0, Yc, cnt, d, k, N, p->M4,
+                                                             p->q0inv_q1, w.D);
+        }
         for (int mod = 0; mod < 4; ++mod)
-          HE_CUDA(ntt_forward(*tab[mod], w.D + (size_t)mod * cnt * N, cnt, N, st), "NTT(digits)");
+          HE_CUDA(ntt_forward(*tab[mod], w.D + (size_t)mod * cnt * N, cnt, N, st, fused), "NTT(digits)");
         k_ms1_mac<<<dim3((unsigned)(((uint64_t)Yc * N / 4 + 255) / 256), 4), 256, 0, st>>>(
             w.D, gal + (size_t)j0 * 8 * N, p->jc, Yc, p->logN, p->M4, w.UW);
       }

@@ -190,3 +190,23 @@ def test_mod_raise_of_packed_output():
         assert all(v % q0 == 0 for v in diff)
         I = np.array([v // q0 for v in diff], dtype=np.int64)
         assert np.abs(I).max() <= P.N
+
+
+@pytest.mark.gpu
+def test_llama_fused_digits_cols_equal_unfused(monkeypatch):
+    """KEYSWITCH1 at the Llama ring fuses the digit formation with the NTT's cols pass (k_ms1_digits_cols);
+    HE_RP_UNFUSED=1 runs the separate kernels every other ring size uses (bit-exact vs the oracle at the toy
+    ring).  Both must give the same packed words."""
+    import torch
+
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, 512, 1024, seed=6)
+    keys = ring_pack_keygen(ctx, sk, seed=9, method="keyswitch1")
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    rp = make_ring_pack_plan(ctx, 512, method="keyswitch1")
+    monkeypatch.delenv("HE_RP_UNFUSED", raising=False)
+    fused = pcmm_packed(ctx, plan, rp, keys, X).data.clone()
+    monkeypatch.setenv("HE_RP_UNFUSED", "1")
+    unfused = pcmm_packed(ctx, plan, rp, keys, X).data.clone()
+    torch.cuda.synchronize()
+    assert torch.equal(fused, unfused)
