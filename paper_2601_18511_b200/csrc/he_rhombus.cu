@@ -1175,7 +1175,7 @@ HE_D void cols16_store(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t
 struct Ms1Tw {
   const uint2* tw[4];   // forward twiddle tables (W, Shoup) of q0, q1, P1, P2 at N = 2^16
 };
-__global__ void __launch_bounds__(256, 2) k_ms1_digits_cols(const uint32_t* __restrict__ raw_a, uint32_t n_out,
+__global__ void __launch_bounds__(256, 3) k_ms1_digits_cols(const uint32_t* __restrict__ raw_a, uint32_t n_out,
                                                             uint32_t Y0, uint32_t j0, uint32_t Yc, uint32_t cnt,
                                                             Mods4 M, uint32_t q0inv_q1, Ms1Tw T,
                                                             uint32_t* __restrict__ D) {
@@ -1196,25 +1196,32 @@ __global__ void __launch_bounds__(256, 2) k_ms1_digits_cols(const uint32_t* __re
   const uint32_t q0 = M.m[0], q1 = M.m[1];
   const uint64_t Q = (uint64_t)q0 * q1;
   const size_t plane = (size_t)cnt * N;
-  // thread -> (t = lane, m0 = warp + 8 i): the 32 lanes of a warp gather 32 rows (banks t * 257 = t mod 32)
+  // thread -> (t = lane, m0 = warp + 8 i): the 32 lanes of a warp gather 32 rows (banks t * 257 = t mod 32).
+  // Moduli in sequence (q0, q1 straight from the staged words, then P1, P2 via the CRT lift) to stay at 3 CTAs/SM
   const uint32_t t = threadIdx.x & 31;
   for (uint32_t m0 = threadIdx.x >> 5; m0 < 16; m0 += blockDim.x >> 5) {
-    uint32_t a0[16], a1[16], x2[16], x3[16];
+    const uint32_t* s0 = seg + t * kMs1Pitch + m0;
+    const uint32_t* s1 = seg + (kMs1T + t) * kMs1Pitch + m0;
+    const size_t c = (size_t)idx * N + t0 + t + (size_t)k * m0;
+    uint32_t x[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = s0[16 * v];
+    cols16_store(x, T.tw[0], q0, D + c);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = s1[16 * v];
+    cols16_store(x, T.tw[1], q1, D + plane + c);
+    uint32_t x3[16];
 #pragma unroll
     for (int v = 0; v < 16; ++v) {
-      a0[v] = seg[t * kMs1Pitch + m0 + 16 * v];
-      a1[v] = seg[(kMs1T + t) * kMs1Pitch + m0 + 16 * v];
       // CRT: alpha = a0 + q0 ((a1 - a0) q0^-1 mod q1) in [0, Q), centred (as k_ms1_digits)
-      const uint32_t tq = mulmod_b(sub_mod(a1[v], barrett64(a0[v], M.mu[1], q1), q1), q0inv_q1, M.mu[1], q1);
-      const uint64_t al = (uint64_t)a0[v] + (uint64_t)q0 * tq;
+      const uint32_t a0 = s0[16 * v], a1 = s1[16 * v];
+      const uint32_t tq = mulmod_b(sub_mod(a1, barrett64(a0, M.mu[1], q1), q1), q0inv_q1, M.mu[1], q1);
+      const uint64_t al = (uint64_t)a0 + (uint64_t)q0 * tq;
       const int64_t ac = al > Q / 2 ? (int64_t)al - (int64_t)Q : (int64_t)al;
-      x2[v] = lift_b(ac, M.mu[2], M.m[2]);
+      x[v] = lift_b(ac, M.mu[2], M.m[2]);
       x3[v] = lift_b(ac, M.mu[3], M.m[3]);
     }
-    const size_t c = (size_t)idx * N + t0 + t + (size_t)k * m0;
-    cols16_store(a0, T.tw[0], q0, D + c);
-    cols16_store(a1, T.tw[1], q1, D + plane + c);
-    cols16_store(x2, T.tw[2], M.m[2], D + 2 * plane + c);
+    cols16_store(x, T.tw[2], M.m[2], D + 2 * plane + c);
     cols16_store(x3, T.tw[3], M.m[3], D + 3 * plane + c);
   }
 }
@@ -1231,6 +1238,7 @@ __global__ void __launch_bounds__(256) k_ms1_mac(const uint32_t* __restrict__ D,
   const size_t plane4 = (size_t)jc * Yc * N / 4, yn4 = (size_t)Yc * N / 4, n4 = N / 4;
   const uint4* d0 = reinterpret_cast<const uint4*>(D) + (size_t)mod * plane4 + x4;
   uint64_t au[4] = {0, 0, 0, 0}, aw[4] = {0, 0, 0, 0};
+#pragma unroll 8
   for (uint32_t jj = 0; jj < jc; ++jj) {
     const uint4* Kj = reinterpret_cast<const uint4*>(K + (size_t)jj * 8 * N) + f4;
     const uint4 x = __ldcs(d0 + jj * yn4);
@@ -1256,6 +1264,53 @@ __global__ void __launch_bounds__(256) k_ms1_mac(const uint32_t* __restrict__ D,
                   add_mod(uo.z, barrett64(au[2], mu, q), q), add_mod(uo.w, barrett64(au[3], mu, q), q));
   *W = make_uint4(add_mod(wo.x, barrett64(aw[0], mu, q), q), add_mod(wo.y, barrett64(aw[1], mu, q), q),
                   add_mod(wo.z, barrett64(aw[2], mu, q), q), add_mod(wo.w, barrett64(aw[3], mu, q), q));
+}
+// The same MAC with each thread owning 2 frequencies of kMacY output blocks: every key pair is loaded once per
+// (component, frequency) and used for kMacY blocks (k_ms1_mac re-reads the keys once per block from L2).
+constexpr uint32_t kMacY = 8;
+__global__ void __launch_bounds__(256) k_ms1_mac_y(const uint32_t* __restrict__ D, const uint32_t* __restrict__ K,
+                                                   uint32_t jc, uint32_t Yc, uint32_t logN, Mods4 M,
+                                                   uint32_t* __restrict__ UW) {
+  const uint32_t N = 1u << logN, mod = blockIdx.z, y0 = blockIdx.y * kMacY;
+  const uint32_t f2 = blockIdx.x * blockDim.x + threadIdx.x;   // frequencies 2 f2, 2 f2 + 1
+  const uint32_t q = M.m[mod];
+  const uint64_t mu = M.mu[mod];
+  const size_t plane2 = (size_t)jc * Yc * N / 2, n2 = N / 2;
+  const uint2* d0 = reinterpret_cast<const uint2*>(D) + (size_t)mod * plane2 + (size_t)y0 * n2 + f2;
+  uint64_t au[kMacY][2], aw[kMacY][2];
+#pragma unroll
+  for (uint32_t y = 0; y < kMacY; ++y) au[y][0] = au[y][1] = aw[y][0] = aw[y][1] = 0;
+#pragma unroll 2
+  for (uint32_t jj = 0; jj < jc; ++jj) {
+    const uint2* Kj = reinterpret_cast<const uint2*>(K + (size_t)jj * 8 * N) + f2;
+    const uint2 ku = __ldg(Kj + (0 * 4 + mod) * n2), kw = __ldg(Kj + (1 * 4 + mod) * n2);
+#pragma unroll
+    for (uint32_t y = 0; y < kMacY; ++y) {
+      const uint2 x = __ldcs(d0 + ((size_t)jj * Yc + y) * n2);
+      au[y][0] += (uint64_t)x.x * ku.x;
+      au[y][1] += (uint64_t)x.y * ku.y;
+      aw[y][0] += (uint64_t)x.x * kw.x;
+      aw[y][1] += (uint64_t)x.y * kw.y;
+    }
+    if ((jj & 7) == 7) {  // products < 2^60: reduce every 8 steps (< 2^63)
+#pragma unroll
+      for (uint32_t y = 0; y < kMacY; ++y)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          au[y][e] = barrett64(au[y][e], mu, q);
+          aw[y][e] = barrett64(aw[y][e], mu, q);
+        }
+    }
+  }
+  const size_t yn2 = (size_t)Yc * n2;
+#pragma unroll
+  for (uint32_t y = 0; y < kMacY; ++y) {
+    uint2* U = reinterpret_cast<uint2*>(UW) + (size_t)(mod * 2 + 0) * yn2 + (size_t)(y0 + y) * n2 + f2;
+    uint2* W = reinterpret_cast<uint2*>(UW) + (size_t)(mod * 2 + 1) * yn2 + (size_t)(y0 + y) * n2 + f2;
+    const uint2 uo = *U, wo = *W;
+    *U = make_uint2(add_mod(uo.x, barrett64(au[y][0], mu, q), q), add_mod(uo.y, barrett64(au[y][1], mu, q), q));
+    *W = make_uint2(add_mod(wo.x, barrett64(aw[y][0], mu, q), q), add_mod(wo.y, barrett64(aw[y][1], mu, q), q));
+  }
 }
 // ModDown by P1 P2 of the summed (U, W) (coefficient form; [x]_P centred by CRT), b += composed b', rescale by q1
 __global__ void k_ms1_finish(const uint32_t* __restrict__ UW, const uint32_t* __restrict__ raw_b, uint32_t blocks,
@@ -1631,8 +1686,13 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
         }
         for (int mod = 0; mod < 4; ++mod)
           HE_CUDA(ntt_forward(*tab[mod], w.D + (size_t)mod * cnt * N, cnt, N, st, fused), "NTT(digits)");
-        k_ms1_mac<<<dim3((unsigned)(((uint64_t)Yc * N / 4 + 255) / 256), 4), 256, 0, st>>>(
-            w.D, gal + (size_t)j0 * 8 * N, p->jc, Yc, p->logN, p->M4, w.UW);
+        if (Yc % kMacY == 0 && getenv("HE_RP_MAC4") == nullptr) {
+          k_ms1_mac_y<<<dim3((unsigned)(N / 2 / 256), Yc / kMacY, 4), 256, 0, st>>>(w.D, gal + (size_t)j0 * 8 * N,
+                                                                                 p->jc, Yc, p->logN, p->M4, w.UW);
+        } else {
+          k_ms1_mac<<<dim3((unsigned)(((uint64_t)Yc * N / 4 + 255) / 256), 4), 256, 0, st>>>(
+              w.D, gal + (size_t)j0 * 8 * N, p->jc, Yc, p->logN, p->M4, w.UW);
+        }
       }
       for (int mod = 0; mod < 4; ++mod)
         HE_CUDA(ntt_inverse(*tab[mod], w.UW + (size_t)mod * 2 * Yc * N, 2 * Yc, N, st), "INTT(U, W)");
