@@ -97,20 +97,20 @@ static he_status make_map_u32(CUtensorMap* m, const void* base, uint64_t inner, 
   return HE_OK;
 }
 
-// u32 [planes][rows][inner] tensor boxed as {box_inner, 1 row, box_planes}: the box takes one row of each of
-// box_planes consecutive planes (S3's C^ store: 8 blocks of one frequency for 32 output rows)
-static he_status make_map_u32_rows(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t planes,
-                                   uint32_t box_inner, uint32_t box_planes, uint64_t extent) {
+// S3's C^ store map: u32 [n_out][groups][L][8] (he_spectral.cu cidx), box {8, 1 f, 1 group, 32 rows}: one
+// epilogue warp's 32 rows x 8 blocks of one frequency; groups past group_ext (all padding) are never stored
+static he_status make_map_c4(CUtensorMap* m, const void* base, uint64_t groups, uint64_t L, uint64_t rows,
+                             uint64_t group_ext) {
   PFN_encodeTiled_t fn = encode_fn();
   if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {extent, rows, planes};
-  cuuint64_t strides[2] = {inner * 4, inner * rows * 4};
-  cuuint32_t box[3] = {box_inner, 1, box_planes};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
+  cuuint64_t dims[4] = {8, L, group_ext, rows};
+  cuuint64_t strides[3] = {8 * 4, L * 8 * 4, groups * L * 8 * 4};
+  cuuint32_t box[4] = {8, 1, 1, 32};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled (u32 rows) failed (%d)", (int)r);
+  if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled (C^) failed (%d)", (int)r);
   return HE_OK;
 }
 
@@ -629,8 +629,8 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     CUtensorMap tmB;
     he_status s = make_map_sw64(&tmB, A, p->r_pad, p->nbp, (uint64_t)p->L * p->dsp[L], 16);
     if (s) return s;
-    CUtensorMap tmC;  // C^ limb L: u32 [n_out][L][nbp], box {8 blocks, 1 f, 32 rows} (one epilogue warp's TMA store)
-    s = make_map_u32_rows(&tmC, C[L], p->nbp, p->L, p->n_out, 8, 32, p->nblk);  // padding blocks are never stored
+    CUtensorMap tmC;  // C^ limb L: u32 [n_out][nbp / 8][L][8] (cidx), box {8 blocks, 1 f, 1 group, 32 rows}
+    s = make_map_c4(&tmC, C[L], p->nbp / 8, p->L, p->n_out, (p->nblk + 7) / 8);  // all-padding groups never stored
     if (s) return s;
     p->prof_begin(3 + L, st);
     HE_CUDA(launch_spec_gemm((int)p->dsp[L], p->tmSA[L], tmB, tmC, a, p->ctx->sm_count, st), "spectral gemm");

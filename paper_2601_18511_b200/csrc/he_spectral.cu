@@ -32,6 +32,12 @@
 
 namespace he {
 
+// C^ (S3 -> S4) layout: [y][group of 8 blocks][f][8], so the 8 blocks x L frequencies of one (row, group) -- the
+// unit of the fast S4 -- are one contiguous L x 32-byte region per limb
+HE_HD size_t cidx(uint32_t y, uint32_t f, uint32_t blk, uint32_t L, uint32_t nbp) {
+  return (((size_t)y * (nbp >> 3) + (blk >> 3)) * L + f) * 8 + (blk & 7);
+}
+
 // ---------------------------------------------------------------- host tables
 cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
   t.L = L;
@@ -308,8 +314,7 @@ __global__ void __launch_bounds__(512) spec_data1024_kernel(const uint32_t* __re
 }
 
 // ---------------------------------------------------------------- S4: inverse transform + rescale + store
-// One CTA per (row y, group of 32 blocks m).  C^ limb i: [n_out][L][nbp] u32 (row-major in y: S3 writes and S4
-// reads each row's L x nbp words as one contiguous region).
+// One CTA per (row y, group of 32 blocks m).  C^ limb i: cidx layout (row-major in y).
 constexpr int kSpecMGroup = 32;
 __global__ void __launch_bounds__(256) spec_inverse_kernel(const uint32_t* __restrict__ c0, const uint32_t* __restrict__ c1,
                                                            uint32_t nbp, uint32_t row0, uint32_t d, uint32_t k,
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(256) spec_inverse_kernel(const uint32_t* __res
   for (int limb = 1; limb >= 0; --limb) {
     const uint32_t* src = limb ? c1 : c0;
     const uint32_t q = cst.q[limb];
-    for (uint32_t f = warp; f < L; f += nw) xs[lane * ld + f] = src[((size_t)y * L + f) * nbp + m0 + lane];
+    for (uint32_t f = warp; f < L; f += nw) xs[lane * ld + f] = src[cidx(y, f, m0 + lane, L, nbp)];
     __syncthreads();
     cyc_inv_smem(xs, kSpecMGroup, (int)ld, (int)L, cst.iv[limb], q);
     if (limb) {
@@ -463,9 +468,9 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
   // (16-byte loads; pitch 546 = 2 mod 32 makes the 4 scattered stores per load conflict-free)
   {
     const uint32_t mq = lane & 3;
-    const size_t stride = (size_t)64 * nbp;          // 64 rows p
+    const size_t stride = (size_t)64 * 8;            // 64 rows p
     const uint32_t p_first = warp * 8 + (lane >> 2);
-    const size_t g = ((size_t)y * 512 + p_first) * nbp + m0 + 4 * mq;
+    const size_t g = cidx(y, p_first, m0 + 4 * mq, 512, nbp);
     const uint4* g0 = reinterpret_cast<const uint4*>(c0 + g);
     const uint4* g1 = reinterpret_cast<const uint4*>(c1 + g);
 #pragma unroll 4
@@ -643,11 +648,11 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
     reinterpret_cast<uint4*>(tws)[i] = __ldg(reinterpret_cast<const uint4*>(cst.r2[0]) + i);
     reinterpret_cast<uint4*>(tws + 992)[i] = __ldg(reinterpret_cast<const uint4*>(cst.r2[1]) + i);
   }
-  // phase A: C^[y][p][b0 .. b0 + 7] of both limbs -> xs[b][pad(p)]; one warp access = 16 rows p x 32 B
+  // phase A: C^[y][b0 / 8][p][0 .. 7] of both limbs -> xs[b][pin36(p)]; one warp access = 512 contiguous bytes
   {
     const uint32_t bq = lane & 1, ps = lane >> 1;
-    const size_t g = ((size_t)y * 1024 + warp * 16 + ps) * nbp + b0 + 4 * bq;
-    const size_t stride = (size_t)128 * nbp / 4;   // 128 rows p, in uint4
+    const size_t g = cidx(y, warp * 16 + ps, b0 + 4 * bq, 1024, nbp);   // the unit is one contiguous 32 KB run
+    const size_t stride = (size_t)128 * 8 / 4;   // 128 rows p, in uint4
     const uint4* g0 = reinterpret_cast<const uint4*>(c0 + g);
     const uint4* g1 = reinterpret_cast<const uint4*>(c1 + g);
     uint4 v0[8], v1[8];   // all 16 loads in flight before the first store
@@ -727,9 +732,9 @@ HE_D void tma_store_3d(const void* map, const void* src, int x, int y, int z) {
                "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
                : "memory");
 }
-HE_D void tma_store_3d_hint(const void* map, const void* src, int x, int y, int z, uint64_t hint) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;"
-               ::"l"(map), "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z), "l"(hint)
+HE_D void tma_store_4d_hint(const void* map, const void* src, int x, int y, int z, int w, uint64_t hint) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;"
+               ::"l"(map), "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z), "r"(w), "l"(hint)
                : "memory");
 }
 
@@ -820,16 +825,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // tile -> (y tile, f, m tile), m fastest, y tile slowest: the pairs working at one time cover a run of
-  // frequencies of the same 256 rows, so their C^ stores ([y][f][blk]) fill contiguous per-row regions and
-  // each row's C^ is complete early for S4; divisions by 32-bit reciprocals (exact for operands < 2^16)
+  // tile -> (y tile, f / 4, m tile, f % 4): each CTA pair takes runs of 4 consecutive tiles (4 consecutive
+  // frequencies of one (y tile, m tile)), so an epilogue warp writes the 4 x 32-byte pieces of each row's
+  // C^ group run ([y][group][f][8]) back to back -- full 128-byte lines -- while the pairs working at one time
+  // still cover the 3 m tiles of a run of frequencies of the same 256 rows (G^_f read once from DRAM);
+  // divisions by 32-bit reciprocals (exact for operands < 2^16)
   const uint32_t m_magic = (uint32_t)((0xFFFFFFFFull + m_tiles) / m_tiles);
-  const uint32_t lg_l = 31 - __clz(args.L);   // L is a power of two
+  const uint32_t lg_l4 = 29 - __clz(args.L);   // log2(L / 4), L a power of two >= 4
+  auto pair_tile = [&](int it) { return ((pair + (it >> 2) * npairs) << 2) + (it & 3); };
   auto tile_coords = [&](int tile, int& f, int& y0, int& m0) {
-    const uint32_t rest = m_tiles == 1 ? (uint32_t)tile : __umulhi((uint32_t)tile, m_magic);
-    f = (int)(rest & (uint32_t)(args.L - 1));
-    y0 = args.row0 + (int)(rest >> lg_l) * 256;
-    m0 = (int)((uint32_t)tile - rest * (uint32_t)m_tiles) * kSpecBN;
+    const uint32_t rest = (uint32_t)tile >> 2;
+    const uint32_t r2 = m_tiles == 1 ? rest : __umulhi(rest, m_magic);
+    m0 = (int)(rest - r2 * (uint32_t)m_tiles) * kSpecBN;
+    f = (int)(((r2 & ((uint32_t)(args.L >> 2) - 1)) << 2) | ((uint32_t)tile & 3));
+    y0 = args.row0 + (int)(r2 >> lg_l4) * 256;
   };
 
   if (warp == 0) {
@@ -838,7 +847,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t full0_remote = mapa_rank(&full[0], 0);
-      for (int tile = pair; tile < num_tiles; tile += npairs) {
+      for (int it = 0, tile; (tile = pair_tile(it)) < num_tiles; ++it) {
         int f, y0, m0;
         tile_coords(tile, f, y0, m0);
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -874,7 +883,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs, ++iter) {
+      for (int tile; (tile = pair_tile(iter)) < num_tiles; ++iter) {
         const int buf = iter & 1;
         const uint32_t acc = tmem_base + buf * C::kBuf;
         if (iter >= 2) mbar_wait(&tmem_empty[buf], ((iter >> 1) - 1) & 1);
@@ -915,7 +924,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
     const uint32_t tmem_empty_remote = mapa_rank(&tmem_empty[0], 0);
     const uint32_t q = args.q;
     int iter = 0;
-    for (int tile = pair; tile < num_tiles; tile += npairs, ++iter) {
+    for (int tile; (tile = pair_tile(iter)) < num_tiles; ++iter) {
       const int buf = iter & 1;
       int f, y0, m0;
       tile_coords(tile, f, y0, m0);
@@ -963,7 +972,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        tma_store_3d_hint(&tmC, so, m0 + (int)part * kSpecEpiCols, f, y0 + (int)rank * 128 + (int)quarter * 32,
+        tma_store_4d_hint(&tmC, so, 0, f, (m0 + (int)part * kSpecEpiCols) >> 3, y0 + (int)rank * 128 + (int)quarter * 32,
                           args.hint_c);
         bulk_commit();
       }
@@ -1000,7 +1009,7 @@ __global__ void spec_gemm_simple_kernel(const int8_t* __restrict__ G, const int8
     if (am < 0) am += q;
     accq = (accq + (uint64_t)gm * (uint64_t)am) % q;
   }
-  args.out[((size_t)y * args.L + f) * args.nb + m] = (uint32_t)accq;
+  args.out[cidx(y, f, m, args.L, args.nb)] = (uint32_t)accq;
 }
 
 // ---------------------------------------------------------------- launchers
