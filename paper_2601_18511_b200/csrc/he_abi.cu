@@ -97,6 +97,23 @@ static he_status make_map_u32(CUtensorMap* m, const void* base, uint64_t inner, 
   return HE_OK;
 }
 
+// S3's G^ map over the gidx layout: int8 [planes * row tiles][kg / 2 lines][256], box {256, kg / 2, 1}: one
+// (digit plane, 128-row tile) = kg / 16 chunks of 128 rows x 16 B (no-swizzle core matrices) copied as is
+static he_status make_map_g16(CUtensorMap* m, const void* base, uint64_t kg, uint64_t rows, uint64_t planes) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return fail(HE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t tiles = planes * ((rows + 127) / 128);
+  cuuint64_t dims[3] = {256, kg / 2, tiles};
+  cuuint64_t strides[2] = {256, kg * 128};
+  cuuint32_t box[3] = {256, (cuuint32_t)(kg < 64 ? kg / 2 : 32), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HE_ECUDA, "cuTensorMapEncodeTiled (G^) failed (%d)", (int)r);
+  return HE_OK;
+}
+
 // S3's C^ store map: u32 [n_out][groups][L][8] (he_spectral.cu cidx), box {8, 1 f, 1 group, 32 rows}: one
 // epilogue warp's 32 rows x 8 blocks of one frequency; groups past group_ext (all padding) are never stored
 static he_status make_map_c4(CUtensorMap* m, const void* base, uint64_t groups, uint64_t L, uint64_t rows,
@@ -601,6 +618,7 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     a.L = (int)p->L;
     a.nb = (int)p->nbp;
     a.r_pad = (int)p->r_pad;
+    a.kg = (int)p->kg;
     const uint32_t q = p->epi.q[L];
     a.q = q;
     uint32_t inv = 1;  // q^-1 mod 2^32 by Newton iteration
@@ -622,7 +640,7 @@ static he_status spec_rows(const he_pcmm_plan* p, const void* ws, uint32_t row0,
     }
     const int8_t* A = base + (L ? w.a1 : w.a0);
     if (simple) {
-      const int8_t* G = p->spec_w + (L ? (uint64_t)p->L * p->dsp[0] * p->n_out * p->r_pad : 0);
+      const int8_t* G = p->spec_w + (L ? (uint64_t)p->L * p->dsp[0] * ((p->n_out + 127) / 128 * 128) * p->kg : 0);
       HE_CUDA(launch_spec_gemm_simple((int)p->dsp[L], G, A, a, st), "spectral gemm (simple)");
       continue;
     }
@@ -811,18 +829,23 @@ static uint32_t spec_len(const he_context* c) {
   if (c->R.k == 256 && env != 512) return 1024;
   return 2 * c->R.k;
 }
-static void spec_dims(const he_pcmm_plan* p, uint32_t& L, uint32_t& r_pad, uint32_t dsp[2]) {
+static void spec_dims(const he_pcmm_plan* p, uint32_t& L, uint32_t& r_pad, uint32_t dsp[2], uint32_t* kg = nullptr) {
   L = spec_len(p->ctx);
   r_pad = ((p->n_in / p->ctx->R.k) + 63) / 64 * 64;
+  // G^ rows are stored at 16-byte granularity (S3 stages them as no-swizzle core matrices; the MMA's reads past
+  // kg meet A^'s zero padding), A^ rows stay padded to the 64-byte swizzle atom
+  // (R > 64: whole 64-byte K blocks, so every S3 TMA box is full)
+  const uint32_t R = p->n_in / p->ctx->R.k;
+  if (kg) *kg = (getenv("HE_SPEC_G64") || R > 64) ? r_pad : (R + 15) / 16 * 16;
   dsp[0] = (uint32_t)digits_for(p->ctx->R.q[0]);
   dsp[1] = (uint32_t)digits_for(p->ctx->R.q[1]);
 }
 
 extern "C" he_status he_pcmm_spectral_weight_bytes(const he_pcmm_plan* p, uint64_t* bytes) {
   if (!p || !bytes) return fail(HE_EINVAL, "null argument");
-  uint32_t L, r_pad, dsp[2];
-  spec_dims(p, L, r_pad, dsp);
-  *bytes = (uint64_t)L * (dsp[0] + dsp[1]) * p->n_out * r_pad;
+  uint32_t L, r_pad, dsp[2], kg;
+  spec_dims(p, L, r_pad, dsp, &kg);
+  *bytes = (uint64_t)L * (dsp[0] + dsp[1]) * ((p->n_out + 127) / 128 * 128) * kg;
   return HE_OK;
 }
 
@@ -830,8 +853,8 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
   if (!p || !wspec) return fail(HE_EINVAL, "null argument");
   const he_context* c = p->ctx;
   if (c->R.d % 32) return fail(HE_EINVAL, "spectral path needs mlwe_degree %% 32 == 0");
-  uint32_t L, r_pad, dsp[2];
-  spec_dims(p, L, r_pad, dsp);
+  uint32_t L, r_pad, dsp[2], kg;
+  spec_dims(p, L, r_pad, dsp, &kg);
   // exactness of S3 (|digit product| <= 2^14, K = R = n_in / k terms):
   //   int32 shift accumulators      R * D * 2^14 < 2^31
   //   int32 paired shifts           |t_j| = |acc_2j + 256 acc_2j+1| <= R 2^14 (pairs(2j) + 256 pairs(2j+1)) < 2^31
@@ -856,15 +879,16 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
     spec_table_free(p->st[i]);
     HE_CUDA(spec_table_init(p->st[i], L, c->R.q[i]), "spectral table");
   }
-  const uint64_t sz0 = (uint64_t)L * dsp[0] * p->n_out * r_pad;
-  const uint64_t total = sz0 + (uint64_t)L * dsp[1] * p->n_out * r_pad;
+  const uint64_t rows128 = (p->n_out + 127) / 128 * 128;   // G^ is stored in 128-row tiles (gidx)
+  const uint64_t sz0 = (uint64_t)L * dsp[0] * rows128 * kg;
+  const uint64_t total = sz0 + (uint64_t)L * dsp[1] * rows128 * kg;
   HE_CUDA(cudaMemsetAsync(wspec, 0, total, st), "memset");
   for (int i = 0; i < 2; ++i)
-    HE_CUDA(launch_spec_weights(p->digits, p->d_w, p->n_out, p->n_in, c->R.k, p->st[i], (int)dsp[i], r_pad,
+    HE_CUDA(launch_spec_weights(p->digits, p->d_w, p->n_out, p->n_in, c->R.k, p->st[i], (int)dsp[i], kg,
                                 wspec + (i ? sz0 : 0), st),
             "spectral weights");
   for (int i = 0; i < 2; ++i) {
-    he_status s = make_map_sw64(&p->tmSA[i], wspec + (i ? sz0 : 0), r_pad, p->n_out, (uint64_t)L * dsp[i], 128);
+    he_status s = make_map_g16(&p->tmSA[i], wspec + (i ? sz0 : 0), kg, p->n_out, (uint64_t)L * dsp[i]);
     if (s) return s;
   }
   p->L = L;
@@ -872,6 +896,7 @@ extern "C" he_status he_pcmm_spectral_prepare(he_pcmm_plan* p, int8_t* wspec, vo
   p->nblk = (c->R.N + p->ob - 1) / p->ob;
   p->nbp = (p->nblk + 31) / 32 * 32;
   p->r_pad = r_pad;
+  p->kg = kg;
   p->dsp[0] = dsp[0];
   p->dsp[1] = dsp[1];
   p->spec_w = wspec;

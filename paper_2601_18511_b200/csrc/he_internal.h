@@ -25,10 +25,10 @@ struct he_pcmm_plan {
   he::GemmEpiConst epi;
   // K7 spectral a-part (he_pcmm_spectral_prepare); algo 0 = K1 over every GEMM column
   int algo = 0;
-  uint32_t L = 0, r_pad = 0, dsp[2] = {0, 0};
+  uint32_t L = 0, r_pad = 0, kg = 0, dsp[2] = {0, 0};   // kg: G^ row bytes (16 ceil(R / 16)), r_pad: A^ row bytes
   uint32_t ob = 0, nblk = 0, nbp = 0;  // outputs per block (L - k), blocks, blocks padded to 32
   uint64_t spec_off[2] = {0, 0};       // S3 recombination offsets (multiples of q_i)
-  const int8_t* spec_w = nullptr;  // caller-owned: G^ limb 0 [L][D0][n_out][r_pad], then limb 1
+  const int8_t* spec_w = nullptr;  // caller-owned: G^ limb 0 [L][D0][n_out][kg], then limb 1
   CUtensorMap tmSA[2];
   he::SpecTable st[2];
   // he_pcmm_profile: per-stage CUDA events recorded on the launching stream (profiling state only)

@@ -90,7 +90,8 @@ void spec_table_free(SpecTable& t);
 
 struct SpecGemmArgs {
   int n_rows, row0, n_out;  // row range [row0, row0 + n_rows) of n_out
-  int L, nb, r_pad;         // transform length, blocks (padded to 32), K bytes
+  int L, nb, r_pad;         // transform length, blocks (padded to 32), K bytes of A^ (multiple of 64)
+  int kg;                   // K bytes of G^ rows (multiple of 16, <= r_pad): the A operand's 16-byte chunks
   uint32_t q;
   uint32_t qninv;           // -q^-1 mod 2^32 (Montgomery)
   uint64_t off64;           // multiple of q above the recombination bound: makes the sum non-negative

@@ -148,8 +148,14 @@ HE_D void write_digits(uint32_t v, uint32_t q, int D, int8_t* dst, uint64_t plan
 }
 
 // ---------------------------------------------------------------- S1: spectral weights (plan time)
-// G^[f][a][y][r_pad] int8 (balanced digit a of the transformed filter g'_{y,r}).
+// G^ int8 (balanced digit a of the transformed filter g'_{y,r}), stored as S3's A-operand tiles: plane f D + a,
+// 128-row tile yt, then kg / 16 chunks of 128 rows x 16 bytes (no-swizzle UMMA core matrices, K-major), so one
+// TMA box of 256-byte lines copies a whole (plane, row tile) into shared memory as is (gidx).
 // One CTA per (row y, chunk of kSpecRChunk input cts).
+HE_HD size_t gidx(uint32_t plane, uint32_t y, uint32_t r, uint32_t n_out, uint32_t kg) {
+  const uint32_t yt = (n_out + 127) / 128;
+  return (((size_t)plane * yt + (y >> 7)) * (kg >> 4) + (r >> 4)) * 2048 + (y & 127) * 16 + (r & 15);
+}
 constexpr int kSpecRChunk = 16;
 __global__ void __launch_bounds__(256) spec_weights_kernel(const int8_t* __restrict__ wdig, uint32_t d_w, uint32_t n_out,
                                                            uint32_t n_in, uint32_t k, uint32_t L, uint32_t q, int D,
@@ -172,10 +178,10 @@ __global__ void __launch_bounds__(256) spec_weights_kernel(const int8_t* __restr
   }
   __syncthreads();
   cyc_fwd_smem(xs, cnt, (int)L, (int)L, tw, q);
-  const uint64_t plane = (uint64_t)n_out * r_pad;
+  const uint64_t plane = gidx(1, 0, 0, n_out, r_pad);   // bytes per digit plane (r_pad = kg here)
   for (int i = threadIdx.x; i < cnt * (int)L; i += blockDim.x) {
     const int f = i / cnt, b = i % cnt;  // consecutive threads: consecutive r (bytes)
-    int8_t* dst = out + ((size_t)f * D * n_out + y) * r_pad + r0 + b;
+    int8_t* dst = out + gidx((uint32_t)f * D, y, r0 + b, n_out, r_pad);
     write_digits(shoup_mul(xs[b * L + f], linv, linvp, q), q, D, dst, plane);  // L^-1 of the INTT folded in
   }
 }
@@ -799,6 +805,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
   const int y_tiles = (args.n_rows + 255) / 256;
   const int num_tiles = m_tiles * y_tiles * args.L;
   const int num_kb = args.r_pad / kSpecBK;
+  // G^ bytes of K block kb (kg <= r_pad; the last block may be partial)
+  auto kg_kb = [&](int kb) { const int r = args.kg - kb * kSpecBK; return r < kSpecBK ? (r > 0 ? r : 0) : kSpecBK; };
 
   for (int i = threadIdx.x; i < C::kZeroBytes / 16; i += kSpecThreads)
     reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
@@ -852,14 +860,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
         tile_coords(tile, f, y0, m0);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (uint32_t)(D * 128 * kg_kb(kb) + C::kBBytes));
           else mbar_arrive_cluster(full0_remote + stage * 8);
           uint8_t* a_dst = sA + stage * C::kABytes;
           uint8_t* b_dst = sB + stage * C::kBBytes;
+          // A: this CTA's 128-row tile of each digit plane, kg_kb(kb) / 16 chunks of 2 KB stored contiguously
+          // (gidx): one box of kg_kb / 2 lines of 256 bytes
 #pragma unroll
           for (int a = 0; a < D; ++a)
-            tma_load_3d_2sm(a_dst + a * 128 * kSpecBK, &tmA, &full[stage], kb * kSpecBK, y0 + (int)rank * 128,
-                            f * D + a, args.hint_g);
+            tma_load_3d_2sm(a_dst + a * 128 * kSpecBK, &tmA, &full[stage], 0, kb * (kSpecBK / 2),
+                            (f * D + a) * ((args.n_out + 127) / 128) + (y0 + (int)rank * 128) / 128, args.hint_g);
           // stacked operand [P0 | P1 | .. | P(D-1)] x 32 rows: this CTA holds chunks [rank*D, rank*D + D)
 #pragma unroll
           for (int c = 0; c < D; ++c) {
@@ -896,12 +906,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpecThreads, 1)
           if (elect_one()) {
             const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
             const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
-#pragma unroll
-            for (int kk = 0; kk < kSpecBK / 32; ++kk) {
+            // K steps of 32 bytes = A chunks (2 kk, 2 kk + 1): LBO 2 KB between K chunks, SBO 128 B between
+            // 8-row groups. A chunk past kg is stale smem (the next digit's / stage's bytes) whose products meet
+            // A^'s zero padding (rows r >= R are zero), so it adds nothing; K steps wholly past kg are skipped.
+            for (int kk = 0; kk < (kg_kb(kb) + 31) / 32; ++kk) {
               const uint64_t bd = desc_sw64(b_base + kk * 32);
 #pragma unroll
               for (int a = 0; a < D; ++a)
-                mma_i8_2sm(acc + a * kSpecBN, desc_sw64(a_base + a * 128 * kSpecBK + kk * 32), bd, kIdesc, 1);
+                mma_i8_2sm(acc + a * kSpecBN, desc_noswz(a_base + a * 128 * kSpecBK + kk * 4096, 2048, 128), bd,
+                           kIdesc, 1);
             }
             tc_commit_2sm_mc(&empty[stage], 0x3);
           }
@@ -1001,7 +1014,7 @@ __global__ void spec_gemm_simple_kernel(const int8_t* __restrict__ G, const int8
   for (int r = 0; r < args.r_pad; ++r) {
     int64_t gv = 0, av = 0;
     for (int a = D - 1; a >= 0; --a) {
-      gv = gv * 256 + G[(((size_t)f * D + a) * args.n_out + y) * args.r_pad + r];
+      gv = gv * 256 + (r < args.kg ? G[gidx(f * D + a, y, r, args.n_out, args.kg)] : 0);
       av = av * 256 + A[(((size_t)f * D + a) * args.nb + m) * args.r_pad + r];
     }
     int64_t gm = gv % (int64_t)q, am = av % (int64_t)q;
