@@ -527,6 +527,11 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
 //            stage forms only the outputs u < 768.
 // 8 blocks per CTA, both limbs in smem (pitch 1148 = 4 mod 8, position p at pin36(p): conflict-free transposing
 // stores, 16-byte round-1 loads/stores); a' rows of 3 x 8 positions are written as 96-byte segments.
+HE_D void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+HE_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+HE_D void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 constexpr int kInv1kBlocks = 8;
 constexpr int kInv1kLd = 1148;   // pin36(1023) + 1, = 4 mod 8
 // position p at p + 4 (p / 32): rows of 32 positions at pitch 36 words, so a lane's 32 round-1 positions are
@@ -650,11 +655,9 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
   uint2* tws = reinterpret_cast<uint2*>(xs1 + kInv1kBlocks * kInv1kLd);   // round-2 lane tables [2][992]
   const uint32_t y = row0 + blockIdx.y, b0 = blockIdx.x * kInv1kBlocks;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t i = threadIdx.x; i < 496; i += 256) {   // 992 uint2 = 496 uint4 per limb
-    reinterpret_cast<uint4*>(tws)[i] = __ldg(reinterpret_cast<const uint4*>(cst.r2[0]) + i);
-    reinterpret_cast<uint4*>(tws + 992)[i] = __ldg(reinterpret_cast<const uint4*>(cst.r2[1]) + i);
-  }
-  // phase A: C^[y][b0 / 8][p][0 .. 7] of both limbs -> xs[b][pin36(p)]; one warp access = 512 contiguous bytes
+  // phase A: C^[y][b0 / 8][p][0 .. 7] of both limbs -> xs[b][pin36(p)]; one warp access = 512 contiguous bytes.
+  // The round-2 lane tables are copied with cp.async after the unit's loads are issued (no register staging,
+  // no wait in front of the loads)
   {
     const uint32_t bq = lane & 1, ps = lane >> 1;
     const size_t g = cidx(y, warp * 16 + ps, b0 + 4 * bq, 1024, nbp);   // the unit is one contiguous 32 KB run
@@ -667,6 +670,11 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
       v0[it] = __ldg(g0 + it * stride);
       v1[it] = __ldg(g1 + it * stride);
     }
+    for (uint32_t i = threadIdx.x; i < 496; i += 256) {   // 992 uint2 = 496 uint4 per limb
+      cp_async16(reinterpret_cast<uint4*>(tws) + i, reinterpret_cast<const uint4*>(cst.r2[0]) + i);
+      cp_async16(reinterpret_cast<uint4*>(tws + 992) + i, reinterpret_cast<const uint4*>(cst.r2[1]) + i);
+    }
+    cp_async_commit();
 #pragma unroll
     for (uint32_t it = 0; it < 8; ++it) {
       const uint32_t o = 4 * bq * kInv1kLd + pin36(warp * 16 + ps + 128 * it);
@@ -674,6 +682,7 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
       xs1[o] = v1[it].x; xs1[o + kInv1kLd] = v1[it].y; xs1[o + 2 * kInv1kLd] = v1[it].z; xs1[o + 3 * kInv1kLd] = v1[it].w;
     }
   }
+  cp_async_wait_all();
   __syncthreads();
   const uint32_t b = warp;
   if (b0 + b < nblk) {
