@@ -458,3 +458,24 @@ def test_mlwe_decryption_matches_oracle_and_direct_kernel(params):
         full[i, d:] = oa[y]
     ref = O.decrypt_mlwe(P, sk.s.cpu().numpy(), full)
     assert np.array_equal(got[rows], ref)
+
+
+@pytest.mark.parametrize("n_out,n_in", [(4096, 4096), (4096, 11008)])
+def test_llama_headroom_log_delta_24(n_out, n_in):
+    """Dynamic-range option: at the default Delta = 2^26 a level-0 output must stay below q0 / (2 Delta) = 8 in
+    magnitude; HeParams.llama(log_delta=24) raises that bound to 32 (activations / outputs with outliers) at
+    2 bits less precision.  Outputs up to |y| ~ 20 here: sampled words bit-exact vs the oracle and the decrypted
+    product within 2^-10 relative to its range."""
+    P = HeParams.llama(log_delta=24)
+    ctx, sk, A, W, X = setup(P, n_out, n_in, scale=np.sqrt(n_in) / 10.0)   # 10x the default weights: |y| up to ~14
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    Y = pcmm_mlwe(ctx, plan, X)
+    rows, cols = _llama_sample(P, n_out)
+    ref = O.pcmm(P, O.encode_weights(P, W), u32(X.data), rows=rows, cols=cols)
+    assert np.array_equal(gather(P, Y, rows, cols), ref)
+    dec = ctx.decrypt_pcmm(sk, Y, rows=(0, 256))
+    exact = A @ W.T
+    top = np.abs(exact[:, :256]).max()
+    assert 8 < top < 32, top                         # beyond the default preset's range, inside this one's
+    err = np.nanmax(np.abs(dec - exact))
+    assert err / top < 2 ** -10, (err, top)
