@@ -582,10 +582,10 @@ extern "C" he_status he_pcmm_decompose(const he_pcmm_plan* p, const uint32_t* ct
     p->prof_begin(1, st);
     HE_CUDA(cudaMemsetAsync(base + w.a0, 0, w.c0 - w.a0, st), "memset");
     const uint32_t n_ct = p->n_in / p->ctx->R.k;
-    for (uint32_t L = 0; L < 2; ++L)
-      HE_CUDA(launch_spec_data(p->ctx->R, ct_in, n_ct, L, p->st[L], (int)p->dsp[L], p->r_pad, p->ob, p->nblk, p->nbp,
-                               base + (L ? w.a1 : w.a0), st),
-              "spectral data transform");
+    const int D[2] = {(int)p->dsp[0], (int)p->dsp[1]};
+    int8_t* const outs[2] = {base + w.a0, base + w.a1};
+    HE_CUDA(launch_spec_data2(p->ctx->R, ct_in, n_ct, p->st, D, p->r_pad, p->ob, p->nblk, p->nbp, outs, st),
+            "spectral data transform");
     p->prof_end(1, st);
     return HE_OK;
   }

@@ -109,13 +109,17 @@ struct SpecInvConst {
   uint32_t linv[2], linvp[2];
   uint32_t q1inv, q1invp;
   uint32_t* out1 = nullptr;  // level-1 mode: no rescale; limb-0 words -> out_a, limb-1 words -> out1 (same layout)
-  uint32_t q1bar = 0;        // floor(2^32 / q[1]) (set by launch_spec_inverse for the lazy q1 limb of S4 v2)
+  uint32_t q1bar = 0;        // floor(2^32 / q[1]) (set by launch_spec_inverse: the lazy q1 limb's final Barrett step)
 };
 cudaError_t launch_spec_weights(const int8_t* wdig, uint32_t d_w, uint32_t n_out, uint32_t n_in, uint32_t k,
                                 const SpecTable& t, int D, uint32_t r_pad, int8_t* out, cudaStream_t s);
 cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, uint32_t limb, const SpecTable& t,
                              int D, uint32_t r_pad, uint32_t ob, uint32_t nblk, uint32_t nbp, int8_t* out,
                              cudaStream_t s);
+// both limbs of S2 in one launch where the fast L = 1024 kernel applies (else two launch_spec_data calls)
+cudaError_t launch_spec_data2(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, const SpecTable (&t)[2],
+                              const int (&D)[2], uint32_t r_pad, uint32_t ob, uint32_t nblk, uint32_t nbp,
+                              int8_t* const (&out)[2], cudaStream_t s);
 cudaError_t launch_spec_gemm(int D, const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                              const SpecGemmArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_spec_gemm_simple(int D, const int8_t* G, const int8_t* A, const SpecGemmArgs& a, cudaStream_t s);

@@ -239,11 +239,21 @@ struct SpecFwdConst {
   uint2 f1[26];
 };
 constexpr int kS2Ld = 1057;   // per-warp region pitch: 1024 + 32 + 1 (odd: conflict-free digit read-out)
+struct SpecData2 {   // both limbs of S2 in one launch (blockIdx.z = limb)
+  SpecFwdConst cf[2];
+  uint32_t q[2];
+  int D[2];
+  int8_t* out[2];
+};
 __global__ void __launch_bounds__(512) spec_data1024_kernel(const uint32_t* __restrict__ ct, uint32_t n_ct,
-                                                            uint32_t limb, uint32_t k, uint32_t ob, uint32_t nbp,
-                                                            uint32_t N, uint32_t q, int D, uint32_t r_pad,
-                                                            SpecFwdConst cf, int8_t* __restrict__ out) {
+                                                            uint32_t k, uint32_t ob, uint32_t nbp, uint32_t N,
+                                                            uint32_t r_pad, const __grid_constant__ SpecData2 sd) {
   extern __shared__ uint32_t xs[];                      // [16 windows][1057]
+  const uint32_t limb = blockIdx.z;
+  const SpecFwdConst& cf = sd.cf[limb];
+  const uint32_t q = sd.q[limb];
+  const int D = sd.D[limb];
+  int8_t* __restrict__ out = sd.out[limb];
   const uint32_t m = blockIdx.x, r0 = blockIdx.y * 16;
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t q2 = 2 * q;
@@ -1053,14 +1063,18 @@ cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_
                              int D, uint32_t r_pad, uint32_t ob, uint32_t nblk, uint32_t nbp, int8_t* out,
                              cudaStream_t s) {
   if (t.L == 1024 && t.f2) {
-    dim3 grid(nblk, (n_ct + 15) / 16);
+    dim3 grid(nblk, (n_ct + 15) / 16, 1);
     const size_t smem = (size_t)16 * kS2Ld * sizeof(uint32_t);
     cudaError_t e = cudaFuncSetAttribute(spec_data1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    SpecFwdConst cf;
-    cf.f2 = t.f2;
-    for (int i = 0; i < 26; ++i) cf.f1[i] = t.f1[i];
-    spec_data1024_kernel<<<grid, 512, smem, s>>>(ct, n_ct, limb, Rg.k, ob, nbp, Rg.N, t.q, D, r_pad, cf, out);
+    SpecData2 sd{};
+    sd.cf[0].f2 = t.f2;
+    for (int i = 0; i < 26; ++i) sd.cf[0].f1[i] = t.f1[i];
+    sd.q[0] = t.q;
+    sd.D[0] = D;
+    // one limb per call: the kernel reads limb blockIdx.z of the ciphertexts, so shift the base to this limb
+    sd.out[0] = out;
+    spec_data1024_kernel<<<grid, 512, smem, s>>>(ct + (size_t)limb * 2 * Rg.N, n_ct, Rg.k, ob, nbp, Rg.N, r_pad, sd);
     return cudaGetLastError();
   }
   dim3 grid(nblk, (n_ct + kSpecRChunk - 1) / kSpecRChunk);
@@ -1070,6 +1084,32 @@ cudaError_t launch_spec_data(const RingDims& Rg, const uint32_t* ct, uint32_t n_
     if (e != cudaSuccess) return e;
   }
   spec_data_kernel<<<grid, 256, smem, s>>>(ct, n_ct, limb, Rg.k, ob, nbp, Rg.N, t.L, t.q, D, r_pad, t.fw, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spec_data2(const RingDims& Rg, const uint32_t* ct, uint32_t n_ct, const SpecTable (&t)[2],
+                              const int (&D)[2], uint32_t r_pad, uint32_t ob, uint32_t nblk, uint32_t nbp,
+                              int8_t* const (&out)[2], cudaStream_t s) {
+  if (t[0].L != 1024 || !t[0].f2 || !t[1].f2) {
+    for (uint32_t L = 0; L < 2; ++L) {
+      cudaError_t e = launch_spec_data(Rg, ct, n_ct, L, t[L], D[L], r_pad, ob, nblk, nbp, out[L], s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  dim3 grid(nblk, (n_ct + 15) / 16, 2);
+  const size_t smem = (size_t)16 * kS2Ld * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(spec_data1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  SpecData2 sd{};
+  for (int L = 0; L < 2; ++L) {
+    sd.cf[L].f2 = t[L].f2;
+    for (int i = 0; i < 26; ++i) sd.cf[L].f1[i] = t[L].f1[i];
+    sd.q[L] = t[L].q;
+    sd.D[L] = D[L];
+    sd.out[L] = out[L];
+  }
+  spec_data1024_kernel<<<grid, 512, smem, s>>>(ct, n_ct, Rg.k, ob, nbp, Rg.N, r_pad, sd);
   return cudaGetLastError();
 }
 
