@@ -141,29 +141,38 @@ __global__ void k_ch_digits(const uint32_t* __restrict__ a, uint64_t as, uint64_
 }
 // UW [j][z][part][N] = sum_i D[j][src(z)][i][perm_rot(z) c] K_rot(z)[i][part][j][c] for the C ciphertexts of the
 // chunk: grid z = the rotation slot r < per, each thread loads its key words once and loops z = ct per + r
+// NQ: the number of data primes (compile time, so the digit loop unrolls and every gather of a ct is in flight
+// at once -- the runtime-nq loop sat on long-scoreboard stalls, ~21 per issue)
+template <uint32_t NQ>
 __global__ void k_ch_mac(const uint32_t* __restrict__ D, uint32_t dcnt, RotMap rm, uint32_t C,
                          const uint32_t* __restrict__ perms, const uint32_t* __restrict__ K, uint64_t kstride,
                          uint32_t N, uint32_t cnt, ChMods M, uint32_t* __restrict__ UW) {
-  const uint32_t j = blockIdx.y, r0 = blockIdx.z, nq = M.nq, nm = nq + 1, r = rm_rot(rm, r0);
+  constexpr uint32_t nq = NQ, nm = NQ + 1;
+  const uint32_t j = blockIdx.y, r0 = blockIdx.z, r = rm_rot(rm, r0);
   const uint32_t q = M.m[j];
   const uint64_t mu = M.mu[j];
   const uint32_t* perm = perms + (size_t)r * N;
   const uint32_t* Kz = K + (size_t)r * kstride;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
     const uint32_t pc = perm[c];
-    uint32_t ku[kChMaxQ - 1], kw[kChMaxQ - 1];
+    uint32_t ku[NQ], kw[NQ];
+#pragma unroll
     for (uint32_t i = 0; i < nq; ++i) {
       ku[i] = Kz[((size_t)(i * 2 + 0) * nm + j) * N + c];
       kw[i] = Kz[((size_t)(i * 2 + 1) * nm + j) * N + c];
     }
+#pragma unroll 2
     for (uint32_t ct = 0; ct < C; ++ct) {
       const uint32_t z = ct * rm.per + r0;
       const uint32_t* Dz = D + ((size_t)j * dcnt + rm_src(rm, z)) * nq * N + pc;
+      uint32_t dv[NQ];
+#pragma unroll
+      for (uint32_t i = 0; i < nq; ++i) dv[i] = Dz[(size_t)i * N];
       uint64_t u = 0, w = 0;   // nq <= 7 products < 2^60 each: no overflow
+#pragma unroll
       for (uint32_t i = 0; i < nq; ++i) {
-        const uint64_t dv = Dz[(size_t)i * N];
-        u += dv * ku[i];
-        w += dv * kw[i];
+        u += (uint64_t)dv[i] * ku[i];
+        w += (uint64_t)dv[i] * kw[i];
       }
       UW[(((size_t)j * cnt + z) * 2 + 0) * N + c] = ch_barrett(u, mu, q);
       UW[(((size_t)j * cnt + z) * 2 + 1) * N + c] = ch_barrett(w, mu, q);
@@ -605,8 +614,17 @@ static he_status ch_keyswitch(const he_chain_map* p, const ChWs& w, const ChMods
   const he_chain* c = p->chain;
   const uint32_t N = p->N, nq = M.nq, level = p->level;
   const uint64_t kstride = (uint64_t)nq * 2 * (nq + 1) * N;
-  k_ch_mac<<<dim3((N + 511) / 512, nq + 1, rm.per), 256, 0, st>>>(w.D, dcnt, rm, cnt / rm.per, perms, keys, kstride, N,
-                                                                 cnt, M, w.UW);
+  {
+    const dim3 grid((N + 511) / 512, nq + 1, rm.per);
+    const uint32_t C = cnt / rm.per;
+    switch (nq) {
+#define HE_CH_MAC(Q) \
+      case Q: k_ch_mac<Q><<<grid, 256, 0, st>>>(w.D, dcnt, rm, C, perms, keys, kstride, N, cnt, M, w.UW); break;
+      HE_CH_MAC(1) HE_CH_MAC(2) HE_CH_MAC(3) HE_CH_MAC(4) HE_CH_MAC(5) HE_CH_MAC(6) HE_CH_MAC(7)
+#undef HE_CH_MAC
+      default: return fail(HE_EINVAL, "chain level %u out of range", level);
+    }
+  }
   // ModDown: P parts to coefficient form, centred lift to every data prime, back to the NTT domain
   uint32_t* UWP = w.UW + (size_t)nq * cnt * 2 * N;
   HE_CUDA(ntt_inverse(ch_tab(c, nq, nq), UWP, 2 * cnt, N, st), "INTT(U_P, W_P)");
