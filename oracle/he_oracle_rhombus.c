@@ -559,30 +559,51 @@ int or_mlwe_to_rlwe1(uint32_t d, uint32_t k, const uint32_t* m4, const uint32_t*
   const uint64_t q1inv = powmod(q1 % q0, q0 - 2, q0);
   const uint64_t q0inv1 = powmod(q0 % q1, q1 - 2, q1), p1inv2 = powmod(P1 % P2, P2 - 2, P2);
   const uint64_t Q = (uint64_t)q0 * q1, PP = (uint64_t)P1 * P2;
-#pragma omp parallel for schedule(dynamic)
+  uint32_t* U = (uint32_t*)malloc(sizeof(uint32_t) * 4 * N);
+  uint32_t* W = (uint32_t*)malloc(sizeof(uint32_t) * 4 * N);
   for (uint32_t Y = 0; Y < blocks; ++Y) {
-    uint32_t* U = (uint32_t*)calloc((size_t)4 * N, sizeof(uint32_t));
-    uint32_t* W = (uint32_t*)calloc((size_t)4 * N, sizeof(uint32_t));
-    int64_t* al = (int64_t*)malloc(sizeof(int64_t) * N);
-    uint32_t* dl = (uint32_t*)malloc(sizeof(uint32_t) * N);
-    uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * N);
-    for (uint32_t j = 0; j < k; ++j) {
-      for (uint32_t tt = 0; tt < k; ++tt)
-        for (uint32_t mm = 0; mm < d; ++mm) {
-          const size_t src = ((size_t)Y * k + tt) * N + (size_t)d * j + mm;
-          const uint64_t a0 = raw_a[src], a1 = raw_a[(size_t)n_out * N + src];
-          const uint64_t x = a0 + (uint64_t)q0 * mulmod((a1 + q1 - a0 % q1) % q1, q0inv1, q1);   /* CRT, [0, Q) */
-          al[tt + (size_t)k * mm] = x > Q / 2 ? (int64_t)x - (int64_t)Q : (int64_t)x;
+    memset(U, 0, sizeof(uint32_t) * 4 * N);
+    memset(W, 0, sizeof(uint32_t) * 4 * N);
+    /* the k components of one block in parallel (thread-private sums, added mod q at the end: the same
+       residues in any order) */
+#pragma omp parallel
+    {
+      uint32_t* Ut = (uint32_t*)calloc((size_t)4 * N, sizeof(uint32_t));
+      uint32_t* Wt = (uint32_t*)calloc((size_t)4 * N, sizeof(uint32_t));
+      int64_t* al = (int64_t*)malloc(sizeof(int64_t) * N);
+      uint32_t* dl = (uint32_t*)malloc(sizeof(uint32_t) * N);
+      uint32_t* t = (uint32_t*)malloc(sizeof(uint32_t) * N);
+#pragma omp for schedule(dynamic)
+      for (uint32_t j = 0; j < k; ++j) {
+        for (uint32_t tt = 0; tt < k; ++tt)
+          for (uint32_t mm = 0; mm < d; ++mm) {
+            const size_t src = ((size_t)Y * k + tt) * N + (size_t)d * j + mm;
+            const uint64_t a0 = raw_a[src], a1 = raw_a[(size_t)n_out * N + src];
+            const uint64_t x = a0 + (uint64_t)q0 * mulmod((a1 + q1 - a0 % q1) % q1, q0inv1, q1);   /* CRT, [0, Q) */
+            al[tt + (size_t)k * mm] = x > Q / 2 ? (int64_t)x - (int64_t)Q : (int64_t)x;
+          }
+        const uint32_t* K = ksk + (size_t)j * 8 * N;
+        for (uint32_t mi = 0; mi < 4; ++mi) {
+          const uint32_t q = m4[mi];
+          for (uint32_t c = 0; c < N; ++c) dl[c] = modq_i64(al[c], q);
+          polymul(dl, K + ((size_t)0 * 4 + mi) * N, N, q, t);
+          for (uint32_t c = 0; c < N; ++c) Ut[(size_t)mi * N + c] = (uint32_t)(((uint64_t)Ut[(size_t)mi * N + c] + t[c]) % q);
+          polymul(dl, K + ((size_t)1 * 4 + mi) * N, N, q, t);
+          for (uint32_t c = 0; c < N; ++c) Wt[(size_t)mi * N + c] = (uint32_t)(((uint64_t)Wt[(size_t)mi * N + c] + t[c]) % q);
         }
-      const uint32_t* K = ksk + (size_t)j * 8 * N;
-      for (uint32_t mi = 0; mi < 4; ++mi) {
-        const uint32_t q = m4[mi];
-        for (uint32_t c = 0; c < N; ++c) dl[c] = modq_i64(al[c], q);
-        polymul(dl, K + ((size_t)0 * 4 + mi) * N, N, q, t);
-        for (uint32_t c = 0; c < N; ++c) U[(size_t)mi * N + c] = (uint32_t)(((uint64_t)U[(size_t)mi * N + c] + t[c]) % q);
-        polymul(dl, K + ((size_t)1 * 4 + mi) * N, N, q, t);
-        for (uint32_t c = 0; c < N; ++c) W[(size_t)mi * N + c] = (uint32_t)(((uint64_t)W[(size_t)mi * N + c] + t[c]) % q);
       }
+#pragma omp critical
+      for (uint32_t mi = 0; mi < 4; ++mi)
+        for (uint32_t c = 0; c < N; ++c) {
+          const size_t i = (size_t)mi * N + c;
+          U[i] = (uint32_t)(((uint64_t)U[i] + Ut[i]) % m4[mi]);
+          W[i] = (uint32_t)(((uint64_t)W[i] + Wt[i]) % m4[mi]);
+        }
+      free(Ut);
+      free(Wt);
+      free(al);
+      free(dl);
+      free(t);
     }
     for (uint32_t c = 0; c < N; ++c) {
       uint32_t x[2][2];
@@ -604,13 +625,15 @@ int or_mlwe_to_rlwe1(uint32_t d, uint32_t k, const uint32_t* m4, const uint32_t*
         out[((size_t)Y * 2 + ab) * N + c] = (uint32_t)mulmod(modq_i64((int64_t)x[0][ab] - x1c, q0), q1inv, q0);
       }
     }
-    free(U);
-    free(W);
-    free(al);
-    free(dl);
-    free(t);
   }
+  free(U);
+  free(W);
   return 0;
+}
+/* all k keys of or_mlwe_ksk1 (components in parallel): ksk [k][2][4][N] */
+void or_mlwe_ksk1_all(uint64_t seed, const int32_t* s, uint32_t N, uint32_t k, const uint32_t* m4, uint32_t* ksk) {
+#pragma omp parallel for schedule(dynamic)
+  for (uint32_t j = 0; j < k; ++j) or_mlwe_ksk1(seed, j, s, N, k, m4, ksk + (size_t)j * 8 * N);
 }
 
 /* ================================================================== slot-domain BSGS PCMM

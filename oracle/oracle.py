@@ -602,6 +602,8 @@ def _ms1_bind():
         u32, u64 = ctypes.c_uint32, ctypes.c_uint64
         L.or_mlwe_ksk1.restype = None
         L.or_mlwe_ksk1.argtypes = [u64, u32, i32p, u32, u32, u32p, u32p]
+        L.or_mlwe_ksk1_all.restype = None
+        L.or_mlwe_ksk1_all.argtypes = [u64, i32p, u32, u32, u32p, u32p]
         L.or_mlwe_to_rlwe1.restype = ctypes.c_int
         L.or_mlwe_to_rlwe1.argtypes = [u32, u32, u32p, u32p, u32p, u32, u32p, u32p]
         L._ms1_bound = True
@@ -619,10 +621,7 @@ def mlwe_ks_keys1(params, seed: int, s: np.ndarray) -> np.ndarray:
     m = _m4(params)
     out = np.zeros((k, 2, 4, N), np.uint32)
     s = np.ascontiguousarray(s, dtype=np.int32)
-    for j in range(k):
-        g = np.zeros((2, 4, N), np.uint32)
-        _ms1_bind().or_mlwe_ksk1(seed, j, _i32(s), N, k, _u32(m), _u32(g))
-        out[j] = g
+    _ms1_bind().or_mlwe_ksk1_all(seed, _i32(s), N, k, _u32(m), _u32(out))
     return out
 
 

@@ -13,7 +13,7 @@ import pytest
 
 import oracle as O
 from paper_2601_18511_b200 import (HeParams, make_mlwe_pcmm_plan, make_ring_pack_plan, pcmm_level1, pcmm_mlwe,
-                                   pcmm_packed, ring_pack_keygen)
+                                   pcmm_packed, ring_pack, ring_pack_keygen)
 
 from test_gpu_pcmm import setup, u32
 
@@ -210,3 +210,22 @@ def test_llama_fused_digits_cols_equal_unfused(monkeypatch):
     unfused = pcmm_packed(ctx, plan, rp, keys, X).data.clone()
     torch.cuda.synchronize()
     assert torch.equal(fused, unfused)
+
+
+def test_llama_keyswitch1_block_bit_exact_vs_oracle():
+    """Ring packing at the Llama ring (N = 2^16, k = d = 256) word for word against the oracle: one output block
+    (256 rows) packed by the GPU (the fused digits + cols path, the rows NTT, the MAC, ModDown + rescale) equals
+    oracle.mlwe_to_rlwe1 on the same level-1 words with the oracle's own keys (or_mlwe_ksk1 from the same seed and
+    secret; the device keygen equals them at the toy ring)."""
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, 256, 1024, seed=8)
+    keys = ring_pack_keygen(ctx, sk, seed=9, method="keyswitch1")
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    rp = make_ring_pack_plan(ctx, 256, method="keyswitch1")
+    raw_b, raw_a = pcmm_level1(ctx, plan, X, *rp.raw(ctx))
+    Y = ring_pack(ctx, rp, keys, raw_b, raw_a)
+    got = u32(Y.data)[:, 0]
+    s = O.keygen(P, 7)
+    assert np.array_equal(s, sk.s.cpu().numpy())
+    ref = O.mlwe_to_rlwe1(P, u32(raw_b), u32(raw_a), O.mlwe_ks_keys1(P, 9, s))
+    assert np.array_equal(got, ref), f"{int((got != ref).sum())} words differ"
