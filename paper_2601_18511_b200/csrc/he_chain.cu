@@ -327,6 +327,20 @@ static ChMods ch_mods(const he_chain* c, uint32_t level) {
 static const NttTable& ch_tab(const he_chain* c, uint32_t j, uint32_t nq) {
   return j == nq ? c->ntt[kChMaxQ - 1] : c->ntt[j];
 }
+// the per-limb (and per-component) transforms of a batch as one launch per NTT pass (ntt_*_multi):
+// job (j, ab) for j < nj, ab < nab at base + j js + ab abs, table ch_tab(c, j, nq)
+static cudaError_t ch_ntt(const he_chain* c, bool inverse, uint32_t nj, uint32_t nab, uint32_t nq, uint32_t* base,
+                          uint64_t js, uint64_t abs, uint32_t count, uint64_t stride, cudaStream_t st) {
+  const NttTable* t[16];
+  uint32_t* d[16];
+  int n = 0;
+  for (uint32_t j = 0; j < nj; ++j)
+    for (uint32_t ab = 0; ab < nab; ++ab) {
+      t[n] = &ch_tab(c, j, nq);
+      d[n++] = base + (size_t)j * js + (size_t)ab * abs;
+    }
+  return inverse ? ntt_inverse_multi(t, d, n, count, stride, st) : ntt_forward_multi(t, d, n, count, stride, st);
+}
 static const uint32_t* ch_qhinv(const he_chain* c, uint32_t level) { return c->consts + (size_t)level * 3 * kChMaxQ; }
 static const uint32_t* ch_pinv(const he_chain* c, uint32_t level) { return ch_qhinv(c, level) + kChMaxQ; }
 static const uint32_t* ch_topinv(const he_chain* c, uint32_t level) { return ch_qhinv(c, level) + 2 * kChMaxQ; }
@@ -629,8 +643,7 @@ static he_status ch_keyswitch(const he_chain_map* p, const ChWs& w, const ChMods
   uint32_t* UWP = w.UW + (size_t)nq * cnt * 2 * N;
   HE_CUDA(ntt_inverse(ch_tab(c, nq, nq), UWP, 2 * cnt, N, st), "INTT(U_P, W_P)");
   k_ch_lift<<<ch_grid((uint64_t)cnt * 2 * N), 256, 0, st>>>(UWP, (uint64_t)cnt * 2 * N, M, w.LB);
-  for (uint32_t j = 0; j < nq; ++j)
-    HE_CUDA(ntt_forward(c->ntt[j], w.LB + (size_t)j * cnt * 2 * N, 2 * cnt, N, st), "NTT(lift)");
+  HE_CUDA(ch_ntt(c, false, nq, 1, nq, w.LB, (uint64_t)cnt * 2 * N, 0, 2 * cnt, N, st), "NTT(lift)");
   k_ch_combine<<<dim3((N + 4095) / 4096, nq, cnt), 256, 0, st>>>(w.UW, w.LB, bh, bs, rm, perms, N, cnt, M,
                                                                    ch_pinv(c, level), out, os);
   return HE_OK;
@@ -649,12 +662,9 @@ static he_status ch_map_chunk(const he_chain_map* p, const uint32_t* ct_in, uint
   baby.g = g;
   // baby digits from the coefficient-form inputs, then the inputs to the NTT domain (baby 0)
   k_ch_digits<<<dim3((N + 255) / 256, C), 256, 0, st>>>(ct_in, cw, 2ull * N, N, C, M, ch_qhinv(c, level), baby, 0, w.D);
-  for (uint32_t j = 0; j <= nq; ++j)
-    HE_CUDA(ntt_forward(ch_tab(c, j, nq), w.D + (size_t)j * C * nq * N, C * nq, N, st), "NTT(D)");
+  HE_CUDA(ch_ntt(c, false, nq + 1, 1, nq, w.D, (uint64_t)C * nq * N, 0, C * nq, N, st), "NTT(D)");
   HE_CUDA(cudaMemcpyAsync(w.X, ct_in, C * cw * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
-  for (uint32_t j = 0; j < nq; ++j)
-    for (uint32_t ab = 0; ab < 2; ++ab)
-      HE_CUDA(ntt_forward(c->ntt[j], w.X + ((size_t)j * 2 + ab) * N, C, cw, st), "NTT(ct)");
+  HE_CUDA(ch_ntt(c, false, nq, 2, nq, w.X, 2ull * N, N, C, cw, st), "NTT(ct)");
   // baby rotations 1 .. b-1 of every ct (hoisted digits): rot [ct][i - 1]
   if (b > 1) {
     he_status s = ch_keyswitch(p, w, M, C * (b - 1), C, baby, p->perms, keys_baby, w.X + N, cw, w.rot, cw, st);
@@ -674,21 +684,17 @@ static he_status ch_map_chunk(const he_chain_map* p, const uint32_t* ct_in, uint
   if (p->gskip < g)
     k_ch_sum<<<ch_grid(C * cw), 256, 0, st>>>(w.rot2, 0, w.inner + (size_t)p->gskip * cw, (uint64_t)g * cw, C, N, M, w.acc);
   if (nrot) {
-    for (uint32_t j = 0; j < nq; ++j)
-      HE_CUDA(ntt_inverse(c->ntt[j], w.inner + (size_t)j * 2 * N, C * g, cw, st), "INTT(inner a)");
+    HE_CUDA(ch_ntt(c, true, nq, 1, nq, w.inner, 2ull * N, 0, C * g, cw, st), "INTT(inner a)");
     k_ch_digits<<<dim3((N + 255) / 256, C * nrot), 256, 0, st>>>(w.inner, cw, 2ull * N, N, C * nrot, M,
                                                                   ch_qhinv(c, level), giant, 1, w.D);
-    for (uint32_t j = 0; j <= nq; ++j)
-      HE_CUDA(ntt_forward(ch_tab(c, j, nq), w.D + (size_t)j * C * nrot * nq * N, C * nrot * nq, N, st), "NTT(D)");
+    HE_CUDA(ch_ntt(c, false, nq + 1, 1, nq, w.D, (uint64_t)C * nrot * nq * N, 0, C * nrot * nq, N, st), "NTT(D)");
     he_status s = ch_keyswitch(p, w, M, C * nrot, C * nrot, giant, p->perms + (size_t)(b - 1) * N, keys_giant,
                                w.inner + N, cw, w.rot2, cw, st);
     if (s) return s;
   }
   // acc = the zero-step group + every rotated group
   k_ch_sum<<<ch_grid(C * cw), 256, 0, st>>>(w.rot2, nrot, p->gskip < g ? w.acc : nullptr, cw, C, N, M, w.acc);
-  for (uint32_t j = 0; j < nq; ++j)
-    for (uint32_t ab = 0; ab < 2; ++ab)
-      HE_CUDA(ntt_inverse(c->ntt[j], w.acc + ((size_t)j * 2 + ab) * N, C, cw, st), "INTT(acc)");
+  HE_CUDA(ch_ntt(c, true, nq, 2, nq, w.acc, 2ull * N, N, C, cw, st), "INTT(acc)");
   k_ch_rescale<<<ch_grid((uint64_t)C * (nq - 1) * 2 * N), 256, 0, st>>>(w.acc, C, N, M, ch_topinv(c, level), ct_out);
   return HE_OK;
 }

@@ -64,6 +64,11 @@ void ntt_table_free(NttTable& t);
 cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s,
                         bool rows_only = false);
 cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s);
+// njobs (<= 16) batches of the same degree, count and stride in one launch per pass (job i: table t[i], data[i])
+cudaError_t ntt_forward_multi(const NttTable* const* t, uint32_t* const* data, int njobs, uint32_t count,
+                              uint64_t stride, cudaStream_t s, bool rows_only = false);
+cudaError_t ntt_inverse_multi(const NttTable* const* t, uint32_t* const* data, int njobs, uint32_t count,
+                              uint64_t stride, cudaStream_t s);
 
 struct RingDims {
   uint32_t d, k, N, logk, q[2], log_delta;

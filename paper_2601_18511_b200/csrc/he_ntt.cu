@@ -93,10 +93,50 @@ HE_D uint32_t reduce4(uint32_t x, uint32_t q) {  // [0, 4q) -> [0, q)
 }
 HE_D uint2 ldtw(const uint2* tw, uint32_t i) { return __ldg(tw + i); }
 
+// ---------------------------------------------------------------- job tables
+// One launch transforms up to kNttMaxJobs batches that share the degree, batch count and stride but may differ in
+// modulus and base pointer (blockIdx.z = job): the RNS limbs / components of a ciphertext batch in one launch.
+constexpr int kNttMaxJobs = 16;
+struct NttJobs {
+  uint32_t* data[kNttMaxJobs];
+  const uint2* tw[kNttMaxJobs];
+  uint32_t q[kNttMaxJobs], ninv[kNttMaxJobs], ninvp[kNttMaxJobs];
+};
+
 // ---------------------------------------------------------------- cols pass (outer stages)
 template <int N1>
-__global__ void __launch_bounds__(256) ntt_fwd_cols(uint32_t* __restrict__ data, uint64_t stride, uint32_t n2,
-                                                    const uint2* __restrict__ tw, uint32_t q) {
+__global__ void __launch_bounds__(256) ntt_fwd_cols(const __grid_constant__ NttJobs J, uint64_t stride, uint32_t n2) {
+  uint32_t* __restrict__ data = J.data[blockIdx.z];
+  const uint2* __restrict__ tw = J.tw[blockIdx.z];
+  const uint32_t q = J.q[blockIdx.z];
+  const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n2) return;
+  uint32_t* a = data + blockIdx.y * stride + col;
+  // the N1 - 1 warp-uniform twiddles first (L1/L2 hits), then the strided column loads from HBM
+  uint2 w[N1];
+#pragma unroll
+  for (int i = 1; i < N1; ++i) w[i] = ldtw(tw, i);
+  uint32_t x[N1];
+#pragma unroll
+  for (int v = 0; v < N1; ++v) x[v] = a[(size_t)n2 * v];
+  const uint32_t q2 = 2 * q;
+#pragma unroll
+  for (int m = 1, t = N1 / 2; m < N1; m <<= 1, t >>= 1) {
+#pragma unroll
+    for (int i = 0; i < m; ++i) {
+#pragma unroll
+      for (int u = 0; u < t; ++u) ct_bf(x[2 * i * t + u], x[2 * i * t + u + t], w[m + i], q2, q);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < N1; ++v) a[(size_t)n2 * v] = x[v];
+}
+
+// single-batch form with plain parameters (the multi-job form's indexed parameter loads cost the standalone
+// 2^16 forward ~8%: 0.254 -> 0.277 ms for 1024 polys)
+template <int N1>
+__global__ void __launch_bounds__(256) ntt_fwd_cols1(uint32_t* __restrict__ data, uint64_t stride, uint32_t n2,
+                                                     const uint2* __restrict__ tw, uint32_t q) {
   const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= n2) return;
   uint32_t* a = data + blockIdx.y * stride + col;
@@ -118,9 +158,10 @@ __global__ void __launch_bounds__(256) ntt_fwd_cols(uint32_t* __restrict__ data,
 }
 
 template <int N1>
-__global__ void __launch_bounds__(256) ntt_inv_cols(uint32_t* __restrict__ data, uint64_t stride, uint32_t n2,
-                                                    const uint2* __restrict__ tw, uint32_t q, uint32_t ninv,
-                                                    uint32_t ninvp) {
+__global__ void __launch_bounds__(256) ntt_inv_cols(const __grid_constant__ NttJobs J, uint64_t stride, uint32_t n2) {
+  uint32_t* __restrict__ data = J.data[blockIdx.z];
+  const uint2* __restrict__ tw = J.tw[blockIdx.z];
+  const uint32_t q = J.q[blockIdx.z], ninv = J.ninv[blockIdx.z], ninvp = J.ninvp[blockIdx.z];
   const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= n2) return;
   uint32_t* a = data + blockIdx.y * stride + col;
@@ -252,8 +293,11 @@ HE_D constexpr uint32_t poff(int e) {
 // forward: rounds of 4 stages, T = N2/16, N2/256, ..., 1; first round straight from global.  NP transforms
 // (polys blockIdx.y * NP .. + NP - 1 of the batch, block b of each) per CTA share every twiddle load.
 template <int N2, int NP, int MINB = 1>
-__global__ void __launch_bounds__(N2 / 16, MINB) ntt_fwd_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
-                                                        const uint2* __restrict__ tw, uint32_t q, int final_reduce) {
+__global__ void __launch_bounds__(N2 / 16, MINB) ntt_fwd_rows(const __grid_constant__ NttJobs J, uint64_t stride,
+                                                        uint32_t n, int final_reduce) {
+  uint32_t* __restrict__ data = J.data[blockIdx.z];
+  const uint2* __restrict__ tw = J.tw[blockIdx.z];
+  const uint32_t q = J.q[blockIdx.z];
   __shared__ uint32_t s[NP][N2 + N2 / 32];
   const uint32_t b = blockIdx.x;
   uint32_t* a[NP];
@@ -329,9 +373,11 @@ __global__ void __launch_bounds__(N2 / 16, MINB) ntt_fwd_rows(uint32_t* __restri
 // inverse: rounds of 4 stages, T = 1, 16, 256, ...; first round straight from global (16 contiguous words),
 // last round straight to global (coalesced), optional n^-1 scaling
 template <int N2, int NP, int MINB = 1>
-__global__ void __launch_bounds__(N2 / 16, MINB) ntt_inv_rows(uint32_t* __restrict__ data, uint64_t stride, uint32_t n,
-                                                        const uint2* __restrict__ tw, uint32_t q, uint32_t ninv,
-                                                        uint32_t ninvp, int do_scale) {
+__global__ void __launch_bounds__(N2 / 16, MINB) ntt_inv_rows(const __grid_constant__ NttJobs J, uint64_t stride,
+                                                        uint32_t n, int do_scale) {
+  uint32_t* __restrict__ data = J.data[blockIdx.z];
+  const uint2* __restrict__ tw = J.tw[blockIdx.z];
+  const uint32_t q = J.q[blockIdx.z], ninv = J.ninv[blockIdx.z], ninvp = J.ninvp[blockIdx.z];
   __shared__ uint32_t s[NP][N2 + N2 / 32];
   const uint32_t b = blockIdx.x;
   uint32_t* a[NP];
@@ -427,17 +473,38 @@ static bool split(uint32_t n, uint32_t& n1, uint32_t& n2) {
   return false;
 }
 
-cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t st,
-                        bool rows_only) {
+static NttJobs make_jobs(const NttTable* const* t, uint32_t* const* data, int njobs, bool inverse) {
+  NttJobs J{};
+  for (int i = 0; i < njobs; ++i) {
+    J.data[i] = data[i];
+    J.tw[i] = reinterpret_cast<const uint2*>(inverse ? t[i]->iv : t[i]->fw);
+    J.q[i] = t[i]->q;
+    J.ninv[i] = t[i]->ninv;
+    J.ninvp[i] = t[i]->ninvp;
+  }
+  return J;
+}
+static NttJobs shift_jobs(NttJobs J, int njobs, uint64_t off) {
+  for (int i = 0; i < njobs; ++i) J.data[i] += off;
+  return J;
+}
+
+cudaError_t ntt_forward_multi(const NttTable* const* t, uint32_t* const* data, int njobs, uint32_t count,
+                              uint64_t stride, cudaStream_t st, bool rows_only) {
+  if (njobs < 1 || njobs > kNttMaxJobs) return cudaErrorInvalidValue;
+  const uint32_t n = t[0]->n;
+  for (int i = 1; i < njobs; ++i)
+    if (t[i]->n != n) return cudaErrorInvalidValue;
   uint32_t n1, n2;
-  if (!split(t.n, n1, n2)) return cudaErrorInvalidValue;
+  if (!split(n, n1, n2)) return cudaErrorInvalidValue;
   if (count == 0) return cudaSuccess;
-  const uint2* tw = reinterpret_cast<const uint2*>(t.fw);
+  const NttJobs J = make_jobs(t, data, njobs, false);
   cudaError_t e = cudaSuccess;
   if (n1 > 1 && !rows_only) {
     e = with_n1(n1, [&](auto N1) {
-      dim3 g((n2 + 255) / 256, count);
-      ntt_fwd_cols<decltype(N1)::value><<<g, 256, 0, st>>>(data, stride, n2, tw, t.q);
+      dim3 g((n2 + 255) / 256, count, njobs);
+      if (njobs == 1) ntt_fwd_cols1<decltype(N1)::value><<<g, 256, 0, st>>>(J.data[0], stride, n2, J.tw[0], J.q[0]);
+      else ntt_fwd_cols<decltype(N1)::value><<<g, 256, 0, st>>>(J, stride, n2);
       return cudaGetLastError();
     });
     if (e != cudaSuccess) return e;
@@ -447,45 +514,58 @@ cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint6
     if (count / 2) {
       // 4096-point blocks: compiled for 4 resident CTAs per SM (<= 64 registers, 32 warps); measured against
       // 3 / 5 CTAs and one poly per CTA at 6 / 7
-      dim3 g(n1, count / 2);
-      if constexpr (K == 4096) ntt_fwd_rows<K, 2, 4><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, 1);
-      else ntt_fwd_rows<K, 2><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, 1);
+      dim3 g(n1, count / 2, njobs);
+      if constexpr (K == 4096) ntt_fwd_rows<K, 2, 4><<<g, K / 16, 0, st>>>(J, stride, n, 1);
+      else ntt_fwd_rows<K, 2><<<g, K / 16, 0, st>>>(J, stride, n, 1);
     }
     if (count & 1) {
-      dim3 g(n1, 1);
-      ntt_fwd_rows<K, 1><<<g, K / 16, 0, st>>>(data + (size_t)(count - 1) * stride, stride, t.n, tw, t.q, 1);
+      dim3 g(n1, 1, njobs);
+      ntt_fwd_rows<K, 1><<<g, K / 16, 0, st>>>(shift_jobs(J, njobs, (uint64_t)(count - 1) * stride), stride, n, 1);
     }
     return cudaGetLastError();
   });
 }
 
-cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t st) {
+cudaError_t ntt_inverse_multi(const NttTable* const* t, uint32_t* const* data, int njobs, uint32_t count,
+                              uint64_t stride, cudaStream_t st) {
+  if (njobs < 1 || njobs > kNttMaxJobs) return cudaErrorInvalidValue;
+  const uint32_t n = t[0]->n;
+  for (int i = 1; i < njobs; ++i)
+    if (t[i]->n != n) return cudaErrorInvalidValue;
   uint32_t n1, n2;
-  if (!split(t.n, n1, n2)) return cudaErrorInvalidValue;
+  if (!split(n, n1, n2)) return cudaErrorInvalidValue;
   if (count == 0) return cudaSuccess;
-  const uint2* tw = reinterpret_cast<const uint2*>(t.iv);
+  const NttJobs J = make_jobs(t, data, njobs, true);
   cudaError_t e = with_n2(n2, [&](auto N2) {
     constexpr int K = decltype(N2)::value;
     if (count / 2) {
-      // 4096-point blocks: compiled for 4 resident CTAs per SM (<= 64 registers, 32 warps); measured against
-      // 3 / 5 CTAs and one poly per CTA at 6 / 7
-      dim3 g(n1, count / 2);
-      if constexpr (K == 4096) ntt_inv_rows<K, 2, 4><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv, t.ninvp, n1 == 1);
-      else ntt_inv_rows<K, 2><<<g, K / 16, 0, st>>>(data, stride, t.n, tw, t.q, t.ninv, t.ninvp, n1 == 1);
+      dim3 g(n1, count / 2, njobs);
+      if constexpr (K == 4096) ntt_inv_rows<K, 2, 4><<<g, K / 16, 0, st>>>(J, stride, n, n1 == 1);
+      else ntt_inv_rows<K, 2><<<g, K / 16, 0, st>>>(J, stride, n, n1 == 1);
     }
     if (count & 1) {
-      dim3 g(n1, 1);
-      ntt_inv_rows<K, 1><<<g, K / 16, 0, st>>>(data + (size_t)(count - 1) * stride, stride, t.n, tw, t.q, t.ninv,
-                                               t.ninvp, n1 == 1);
+      dim3 g(n1, 1, njobs);
+      ntt_inv_rows<K, 1><<<g, K / 16, 0, st>>>(shift_jobs(J, njobs, (uint64_t)(count - 1) * stride), stride, n, n1 == 1);
     }
     return cudaGetLastError();
   });
   if (e != cudaSuccess || n1 == 1) return e;
   return with_n1(n1, [&](auto N1) {
-    dim3 g((n2 + 255) / 256, count);
-    ntt_inv_cols<decltype(N1)::value><<<g, 256, 0, st>>>(data, stride, n2, tw, t.q, t.ninv, t.ninvp);
+    dim3 g((n2 + 255) / 256, count, njobs);
+    ntt_inv_cols<decltype(N1)::value><<<g, 256, 0, st>>>(J, stride, n2);
     return cudaGetLastError();
   });
+}
+
+cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t st,
+                        bool rows_only) {
+  const NttTable* tp = &t;
+  return ntt_forward_multi(&tp, &data, 1, count, stride, st, rows_only);
+}
+
+cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t st) {
+  const NttTable* tp = &t;
+  return ntt_inverse_multi(&tp, &data, 1, count, stride, st);
 }
 
 }  // namespace he
