@@ -16,6 +16,7 @@
 //   - multi-GPU shards of the PCMv (he_rhombus_run_shard / he_rhombus_combine).
 // Each is restated in oracle/he_oracle_rhombus.c and bit-exact with it.
 #include <algorithm>
+#include <initializer_list>
 #include <vector>
 
 #include "he_common.cuh"
@@ -39,6 +40,18 @@ HE_HD uint32_t half_reverse(uint32_t x, uint32_t n, int logn) {
 HE_D uint32_t barrett64(uint64_t x, uint64_t mu, uint32_t q) {  // x mod q for any x < 2^64
   const uint64_t qh = __umul64hi(x, mu);
   return csub((uint32_t)(x - qh * q), q);
+}
+
+// several same-shape NTT batches (table t[i], base d[i]) as one launch per pass (ntt_*_multi)
+static cudaError_t ntt_jobs(bool inverse, std::initializer_list<const NttTable*> t, std::initializer_list<uint32_t*> d,
+                            uint32_t count, uint64_t stride, cudaStream_t st) {
+  const NttTable* tt[16];
+  uint32_t* dd[16];
+  int n = 0;
+  for (const NttTable* x : t) tt[n++] = x;
+  n = 0;
+  for (uint32_t* x : d) dd[n++] = x;
+  return inverse ? ntt_inverse_multi(tt, dd, n, count, stride, st) : ntt_forward_multi(tt, dd, n, count, stride, st);
 }
 
 struct Mods {
@@ -731,16 +744,15 @@ static he_status rh_pack(const he_rhombus_plan* p, const RhWs& w, const uint32_t
     const uint64_t cn = (uint64_t)cnt_out * n;
     k_pack_comb1<<<dim3(cnt_out, 2, 2), 512, n * sizeof(uint32_t), st>>>(
         A, cnt, half, n, mono_base + (size_t)(lv - 1) * 2 * n, perm_base + (size_t)(lv - 1) * n, p->M, An, w.T, w.C);
-    for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt_rh[L], w.C + (size_t)L * cn, cnt_out, n, st), "INTT(T_a)");
+    const NttTable *t0 = &c->ntt_rh[0], *t1 = &c->ntt_rh[1], *t2 = &c->ntt_rh[2];
+    HE_CUDA(ntt_jobs(true, {t0, t1}, {w.C, w.C + cn}, cnt_out, n, st), "INTT(T_a)");
     k_modup<<<grid_for(cn), 256, 0, st>>>(w.C, w.T, p->logn, cn, p->M, p->qhinv[0], p->qhinv[1], w.D);
-    HE_CUDA(ntt_forward(c->ntt_rh[0], w.D + (0 * 2 + 1) * cn, cnt_out, n, st), "NTT(d1 mod q0)");
-    HE_CUDA(ntt_forward(c->ntt_rh[1], w.D + (1 * 2 + 0) * cn, cnt_out, n, st), "NTT(d0 mod q1)");
-    HE_CUDA(ntt_forward(c->ntt_rh[2], w.D + (2 * 2 + 0) * cn, 2 * cnt_out, n, st), "NTT(d mod P)");
+    HE_CUDA(ntt_jobs(false, {t0, t1, t2, t2}, {w.D + (0 * 2 + 1) * cn, w.D + (1 * 2 + 0) * cn, w.D + 4 * cn, w.D + 5 * cn},
+                     cnt_out, n, st), "NTT(digits)");
     k_mac<<<grid_for(cn), 256, 0, st>>>(w.D, gal + (size_t)(lv - 1) * 12 * n, n, cn, p->M, w.UW);
     HE_CUDA(ntt_inverse(c->ntt_rh[2], w.UW + 2 * 2 * cn, 2 * cnt_out, n, st), "INTT(U_P, W_P)");
     k_moddown_lift<<<grid_for(2 * cn), 256, 0, st>>>(w.UW + 2 * 2 * cn, cn, p->M, w.LB);
-    HE_CUDA(ntt_forward(c->ntt_rh[0], w.LB, 2 * cnt_out, n, st), "NTT(lift q0)");
-    HE_CUDA(ntt_forward(c->ntt_rh[1], w.LB + 2 * cn, 2 * cnt_out, n, st), "NTT(lift q1)");
+    HE_CUDA(ntt_jobs(false, {t0, t1}, {w.LB, w.LB + 2 * cn}, 2 * cnt_out, n, st), "NTT(lift)");
     {
       dim3 g = grid_for(cn / 4);
       g.y = 2;
@@ -776,13 +788,15 @@ static he_status rh_front(const he_rhombus_plan* p, const uint32_t* ct_in, const
   const uint32_t n = p->n, N = p->N, q0 = p->M.m[0], q1 = p->M.m[1], P = p->M.m[2];
   // (D) decompose: key switch the a part at degree N, then split
   k_decomp_modup<<<grid_for(N), 256, 0, st>>>(ct_in, N, q0, q1, P, p->qhinv[0], p->qhinv[1], w.dD);
-  for (int j = 0; j < 3; ++j) HE_CUDA(ntt_forward(c->ntt[j], w.dD + (size_t)j * 2 * N, 2, N, st), "NTT(digits)");
+  HE_CUDA(ntt_jobs(false, {&c->ntt[0], &c->ntt[1], &c->ntt[2]}, {w.dD, w.dD + 2ull * N, w.dD + 4ull * N}, 2, N, st),
+          "NTT(digits)");
   k_mac<<<grid_for(N), 256, 0, st>>>(w.dD, ksk_dec, N, N, p->M, w.dUW);
-  for (int j = 0; j < 3; ++j) HE_CUDA(ntt_inverse(c->ntt[j], w.dUW + (size_t)j * 2 * N, 2, N, st), "INTT(U,W)");
+  HE_CUDA(ntt_jobs(true, {&c->ntt[0], &c->ntt[1], &c->ntt[2]}, {w.dUW, w.dUW + 2ull * N, w.dUW + 4ull * N}, 2, N, st),
+          "INTT(U,W)");
   k_decomp_split<<<grid_for((uint64_t)p->p_in * n), 256, 0, st>>>(w.dUW, ct_in, N, n, p->p_in, piece0, q0, q1, P,
                                                                    p->pinv[0], p->pinv[1], w.pieces);
-  for (int L = 0; L < 2; ++L)
-    HE_CUDA(ntt_forward(c->ntt_rh[L], w.pieces + (size_t)L * p->p_in * 2 * n, p->p_in * 2, n, st), "NTT(pieces)");
+  HE_CUDA(ntt_jobs(false, {&c->ntt_rh[0], &c->ntt_rh[1]}, {w.pieces, w.pieces + (size_t)p->p_in * 2 * n}, p->p_in * 2, n,
+                   st), "NTT(pieces)");
   // (M) leaf ciphertexts: U = n / w inner products each
   const uint64_t leaves = leaves_of(p);
   {
@@ -821,8 +835,8 @@ static he_status rhombus_run_impl(const he_rhombus_plan* p, const uint32_t* ct_i
   if (s) return s;
   // (R) + (C)
   const uint32_t cnt = p->p_out;
-  for (int L = 0; L < 2; ++L)
-    HE_CUDA(ntt_inverse(p->ctx->ntt_rh[L], A + (size_t)L * cnt * 2 * n, cnt * 2, n, st), "INTT(packed)");
+  HE_CUDA(ntt_jobs(true, {&p->ctx->ntt_rh[0], &p->ctx->ntt_rh[1]}, {A, A + (size_t)cnt * 2 * n}, cnt * 2, n, st),
+          "INTT(packed)");
   if (shard) {
     HE_CUDA(cudaMemsetAsync(out, 0, 4ull * N * sizeof(uint32_t), st), "memset");
     k_rh_compose_l1<<<grid_for((uint64_t)cnt * 4 * n), 256, 0, st>>>(A, cnt, opiece0, n, N, out);
@@ -881,8 +895,8 @@ extern "C" he_status he_rhombus_finish(const he_rhombus_plan* p, const uint32_t*
   uint32_t* A = nullptr;
   he_status s = rh_pack(p, w, gal, cnt * G, p->logn - p->logG + 1, p->logn, 1, &A, st);
   if (s) return s;
-  for (int L = 0; L < 2; ++L)
-    HE_CUDA(ntt_inverse(p->ctx->ntt_rh[L], A + (size_t)L * cnt * 2 * n, cnt * 2, n, st), "INTT(packed)");
+  HE_CUDA(ntt_jobs(true, {&p->ctx->ntt_rh[0], &p->ctx->ntt_rh[1]}, {A, A + (size_t)cnt * 2 * n}, cnt * 2, n, st),
+          "INTT(packed)");
   HE_CUDA(cudaMemsetAsync(out, 0, 2ull * N * sizeof(uint32_t), st), "memset");
   k_rh_rescale_compose<<<grid_for((uint64_t)cnt * 2 * n), 256, 0, st>>>(A, cnt, n, N, p->M.m[0], p->M.m[1], p->q1inv,
                                                                          p->q1invp, out);
