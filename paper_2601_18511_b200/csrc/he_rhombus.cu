@@ -1661,13 +1661,13 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
       for (uint32_t j0 = 0; j0 < k; j0 += p->jc) {
         k_ms_digits<<<dim3(d / 32, cnt), 256, 0, st>>>(raw_a, p->n_out, Y0, j0, Yc, cnt, d, k, N, p->M, p->qhinv[0],
                                                       qh0p, p->qhinv[1], qh1p, w.D);
-        for (int mod = 0; mod < 3; ++mod)
-          HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * 2 * cnt * N, 2 * cnt, N, st), "NTT(digits)");
+        HE_CUDA(ntt_jobs(false, {&c->ntt[0], &c->ntt[1], &c->ntt[2]},
+                         {w.D, w.D + 2ull * cnt * N, w.D + 4ull * cnt * N}, 2 * cnt, N, st), "NTT(digits)");
         k_ms_mac<<<dim3((unsigned)(((uint64_t)Yc * N / 4 + 255) / 256), 3), 256, 0, st>>>(w.D, gal + (size_t)j0 * 12 * N, p->jc,
                                                                                    Yc, p->logN, p->M, w.UW);
       }
-      for (int mod = 0; mod < 3; ++mod)
-        HE_CUDA(ntt_inverse(c->ntt[mod], w.UW + (size_t)mod * 2 * Yc * N, 2 * Yc, N, st), "INTT(U, W)");
+      HE_CUDA(ntt_jobs(true, {&c->ntt[0], &c->ntt[1], &c->ntt[2]}, {w.UW, w.UW + 2ull * Yc * N, w.UW + 4ull * Yc * N},
+                       2 * Yc, N, st), "INTT(U, W)");
       k_ms_finish<<<grid_for((uint64_t)Yc * N), 256, 0, st>>>(w.UW, raw_b, p->blocks, Y0, Yc, p->logN, p->M, p->pinv[0],
                                                                p->pinv[1], p->q1inv, p->q1invp, out);
     }
@@ -1698,8 +1698,10 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
           k_ms1_digits<<<dim3(d / kMs1M, cnt), 256, 0, st>>>(raw_a, p->n_out, Y0, j0, Yc, cnt, d, k, N, p->M4,
                                                              p->q0inv_q1, w.D);
         }
-        for (int mod = 0; mod < 4; ++mod)
-          HE_CUDA(ntt_forward(*tab[mod], w.D + (size_t)mod * cnt * N, cnt, N, st, fused), "NTT(digits)");
+        {
+          uint32_t* dd[4] = {w.D, w.D + (size_t)cnt * N, w.D + 2ull * cnt * N, w.D + 3ull * cnt * N};
+          HE_CUDA(ntt_forward_multi(tab, dd, 4, cnt, N, st, fused), "NTT(digits)");
+        }
         if (Yc % kMacY == 0 && getenv("HE_RP_MAC4") == nullptr) {
           k_ms1_mac_y<<<dim3((unsigned)(N / 2 / 256), Yc / kMacY, 4), 256, 0, st>>>(w.D, gal + (size_t)j0 * 8 * N,
                                                                                  p->jc, Yc, p->logN, p->M4, w.UW);
@@ -1708,8 +1710,10 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
               w.D, gal + (size_t)j0 * 8 * N, p->jc, Yc, p->logN, p->M4, w.UW);
         }
       }
-      for (int mod = 0; mod < 4; ++mod)
-        HE_CUDA(ntt_inverse(*tab[mod], w.UW + (size_t)mod * 2 * Yc * N, 2 * Yc, N, st), "INTT(U, W)");
+      {
+        uint32_t* dd[4] = {w.UW, w.UW + 2ull * Yc * N, w.UW + 4ull * Yc * N, w.UW + 6ull * Yc * N};
+        HE_CUDA(ntt_inverse_multi(tab, dd, 4, 2 * Yc, N, st), "INTT(U, W)");
+      }
       k_ms1_finish<<<grid_for((uint64_t)Yc * N), 256, 0, st>>>(w.UW, raw_b, p->blocks, Y0, Yc, p->logN, p->M4,
                                                                 p->p1inv_p2, p->ppinv[0], p->ppinv[1], p->q1inv,
                                                                 p->q1invp, out);
@@ -2486,8 +2490,8 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
   auto digits = [&](const uint32_t* a, uint64_t as, uint32_t cnt) -> he_status {
     k_sd_digits<<<grid3(1, cnt), 256, 0, st>>>(a, as, 2ull * N, N, cnt, p->M, p->qhinv[0], p->qhinvp[0], p->qhinv[1],
                                                p->qhinvp[1], w.D);
-    for (int mod = 0; mod < 3; ++mod)
-      HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * cnt * kSdT * N, cnt * kSdT, N, st), "NTT(D)");
+    const uint64_t ms = (uint64_t)cnt * kSdT * N;
+    HE_CUDA(ntt_jobs(false, {&c->ntt[0], &c->ntt[1], &c->ntt[2]}, {w.D, w.D + ms, w.D + 2 * ms}, cnt * kSdT, N, st), "NTT(D)");
     return HE_OK;
   };
   // cnt rotations in one pass: rotation z uses perm table t0 + z, key z, digits dz (hoist: all z share D^ 0),
@@ -2496,8 +2500,8 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
   auto digits_plain = [&](const uint32_t* a, uint64_t as, uint32_t cnt) -> he_status {
     k_sd_digits_plain<<<grid3(1, cnt), 256, 0, st>>>(a, as, 2ull * N, N, cnt, p->M, p->qhinv[0], p->qhinvp[0],
                                                      p->qhinv[1], p->qhinvp[1], w.D);
-    for (int mod = 0; mod < 3; ++mod)
-      HE_CUDA(ntt_forward(c->ntt[mod], w.D + (size_t)mod * cnt * 2 * N, cnt * 2, N, st), "NTT(D plain)");
+    const uint64_t ms = (uint64_t)cnt * 2 * N;
+    HE_CUDA(ntt_jobs(false, {&c->ntt[0], &c->ntt[1], &c->ntt[2]}, {w.D, w.D + ms, w.D + 2 * ms}, cnt * 2, N, st), "NTT(D plain)");
     return HE_OK;
   };
   auto rotate = [&](uint32_t cnt, int hoist, uint32_t dcnt, uint32_t t0, const uint32_t* keys, const uint32_t* bh,
@@ -2511,8 +2515,7 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
     uint32_t* UWP = w.UW + (size_t)2 * cnt * 2 * N;   // [z][part][N] of modulus P
     HE_CUDA(ntt_inverse(c->ntt[2], UWP, 2 * cnt, N, st), "INTT(U_P, W_P)");
     k_moddown_lift<<<grid_for(2ull * cnt * N), 256, 0, st>>>(UWP, (uint64_t)cnt * N, p->M, w.LB);
-    HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2 * cnt, N, st), "NTT(lift q0)");
-    HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2ull * cnt * N, 2 * cnt, N, st), "NTT(lift q1)");
+    HE_CUDA(ntt_jobs(false, {&c->ntt[0], &c->ntt[1]}, {w.LB, w.LB + 2ull * cnt * N}, 2 * cnt, N, st), "NTT(lift)");
     k_sd_combine<<<grid3(2, cnt), 256, 0, st>>>(w.UW, w.LB, bh, bs, 2ull * N, p->perms + (size_t)t0 * N, N, cnt, p->M,
                                                p->pinv[0], p->pinv[1], dst, 4ull * N);
     return HE_OK;
@@ -2530,8 +2533,8 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
       HE_CUDA(cudaMemcpyAsync(w.X, ct_in + (size_t)c0 * 4 * N, 4ull * N * cc * sizeof(uint32_t),
                               cudaMemcpyDeviceToDevice, st), "copy");
       for (uint32_t z = 0; z < cc; ++z) {
-        for (int L = 0; L < 2; ++L)
-          HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)z * 4 * N + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
+        HE_CUDA(ntt_jobs(false, {&c->ntt[0], &c->ntt[1]}, {w.X + (size_t)z * 4 * N, w.X + (size_t)z * 4 * N + 2ull * N}, 2,
+                         N, st), "NTT(ct)");
         k_sd_lazy_baby0<<<grid3(3, 1), 256, 0, st>>>(w.X + (size_t)z * 4 * N, N, p->M, w.baby + z * baby_cs);
       }
       if (b > 1)
@@ -2545,7 +2548,7 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
       he_status s = digits(ct, 0, 1);
       if (s) return s;
       HE_CUDA(cudaMemcpyAsync(w.X, ct, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
-      for (int L = 0; L < 2; ++L) HE_CUDA(ntt_forward(c->ntt[L], w.X + (size_t)L * 2 * N, 2, N, st), "NTT(ct)");
+      HE_CUDA(ntt_jobs(false, {&c->ntt[0], &c->ntt[1]}, {w.X, w.X + 2ull * N}, 2, N, st), "NTT(ct)");
       HE_CUDA(cudaMemcpyAsync(bz, w.X, 4ull * N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
       if (b > 1) {
         s = rotate(b - 1, 1, 1, 0, keys_baby, w.X + N, 0, bz + 4ull * N);
@@ -2570,27 +2573,25 @@ static he_status sd_run(const he_slot_pcmm_plan* p, const uint32_t* ct_in, uint3
       uint32_t* iz = w.inner + z * inner_cs;
       if (p->lazy) {
         // one ModDown per group sum: INTT of the P parts, centred lift, NTT, (X - lift) P^-1 -> [j][4N]
-        for (int ab = 0; ab < 2; ++ab)
-          HE_CUDA(ntt_inverse(c->ntt[2], iz + (4ull + ab) * N, g, 6ull * N, st), "INTT(group sums, P)");
+        HE_CUDA(ntt_jobs(true, {&c->ntt[2], &c->ntt[2]}, {iz + 4ull * N, iz + 5ull * N}, g, 6ull * N, st),
+                "INTT(group sums, P)");
         dim3 gl = grid_for(2ull * g * N / 4);
         k_sd_lazy_lift<<<gl, 256, 0, st>>>(iz, g, N, p->M, w.LB);
         gl.y = 2;
-        HE_CUDA(ntt_forward(c->ntt[0], w.LB, 2 * g, N, st), "NTT(lift q0)");
-        HE_CUDA(ntt_forward(c->ntt[1], w.LB + 2ull * g * N, 2 * g, N, st), "NTT(lift q1)");
+        HE_CUDA(ntt_jobs(false, {&c->ntt[0], &c->ntt[1]}, {w.LB, w.LB + 2ull * g * N}, 2 * g, N, st), "NTT(lift)");
         k_sd_lazy_down<<<gl, 256, 0, st>>>(iz, w.LB, g, N, p->M, p->pinv[0], p->pinv[1], w.innerq);
         iz = w.innerq;
       }
       if (g > 1) {
         uint32_t* in1 = iz + 4ull * N;   // groups 1 .. g-1
-        for (int L = 0; L < 2; ++L)
-          HE_CUDA(ntt_inverse(c->ntt[L], in1 + (size_t)L * 2 * N, g - 1, 4ull * N, st), "INTT(inner a)");
+        HE_CUDA(ntt_jobs(true, {&c->ntt[0], &c->ntt[1]}, {in1, in1 + 2ull * N}, g - 1, 4ull * N, st), "INTT(inner a)");
         he_status s = p->plain_giant ? digits_plain(in1, 4ull * N, g - 1) : digits(in1, 4ull * N, g - 1);
         if (s) return s;
         s = rotate(g - 1, 0, g - 1, b - 1, keys_giant, in1 + N, 4ull * N, w.rot, p->plain_giant != 0);
         if (s) return s;
       }
       k_sd_accumulate<<<grid3(2, 1), 256, 0, st>>>(iz, w.rot, g - 1, N, p->M, w.acc);
-      for (int L = 0; L < 2; ++L) HE_CUDA(ntt_inverse(c->ntt[L], w.acc + (size_t)L * 2 * N, 2, N, st), "INTT(acc)");
+      HE_CUDA(ntt_jobs(true, {&c->ntt[0], &c->ntt[1]}, {w.acc, w.acc + 2ull * N}, 2, N, st), "INTT(acc)");
       k_rh_combine<<<grid_for(2ull * N), 256, 0, st>>>(w.acc, 1, N, p->M.m[0], p->M.m[1], p->q1inv, p->q1invp,
                                                        out + (size_t)(c0 + z) * 2 * N);
     }
