@@ -1188,6 +1188,9 @@ HE_D void cols16_store(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t
 }
 struct Ms1Tw {
   const uint2* tw[4];   // forward twiddle tables (W, Shoup) of q0, q1, P1, P2 at N = 2^16
+  // 32-bit CRT constants: floor(2^32 / q1); q0^-1 mod q1 (Shoup); per special prime i: q0 mod P_i (Shoup), Q mod P_i
+  uint32_t m1, w01, w01p, c[2], cp[2], qp[2];
+  uint64_t Q;
 };
 __global__ void __launch_bounds__(256, 3) k_ms1_digits_cols(const uint32_t* __restrict__ raw_a, uint32_t n_out,
                                                             uint32_t Y0, uint32_t j0, uint32_t Yc, uint32_t cnt,
@@ -1227,13 +1230,25 @@ __global__ void __launch_bounds__(256, 3) k_ms1_digits_cols(const uint32_t* __re
     uint32_t x3[16];
 #pragma unroll
     for (int v = 0; v < 16; ++v) {
-      // CRT: alpha = a0 + q0 ((a1 - a0) q0^-1 mod q1) in [0, Q), centred (as k_ms1_digits)
+      // CRT: alpha = a0 + q0 tq, tq = (a1 - a0) q0^-1 mod q1, in [0, Q), centred (= k_ms1_digits) -- in 32-bit
+      // pieces: [alpha]_Q mod P = (a0 mod P) + (q0 mod P) tq - (Q mod P if alpha > Q/2), all mod P
       const uint32_t a0 = s0[16 * v], a1 = s1[16 * v];
-      const uint32_t tq = mulmod_b(sub_mod(a1, barrett64(a0, M.mu[1], q1), q1), q0inv_q1, M.mu[1], q1);
-      const uint64_t al = (uint64_t)a0 + (uint64_t)q0 * tq;
-      const int64_t ac = al > Q / 2 ? (int64_t)al - (int64_t)Q : (int64_t)al;
-      x[v] = lift_b(ac, M.mu[2], M.m[2]);
-      x3[v] = lift_b(ac, M.mu[3], M.m[3]);
+      uint32_t r = a0 - __umulhi(a0, T.m1) * q1;   // a0 < 2^30: Barrett remainder in [0, 2 q1)
+      r = min(r, r - q1);
+      const uint32_t dd = a1 >= r ? a1 - r : a1 + q1 - r;
+      uint32_t tq = dd * T.w01 - __umulhi(dd, T.w01p) * q1;
+      tq = min(tq, tq - q1);
+      const bool neg = (uint64_t)a0 + (uint64_t)q0 * tq > T.Q / 2;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t P = M.m[2 + i];
+        uint32_t u = min(a0, a0 - P) + (tq * T.c[i] - __umulhi(tq, T.cp[i]) * P);   // [0, 3P)
+        u = min(u, u - 2 * P);
+        u = min(u, u - P);
+        if (neg) u = u >= T.qp[i] ? u - T.qp[i] : u + P - T.qp[i];
+        if (i == 0) x[v] = u;
+        else x3[v] = u;
+      }
     }
     cols16_store(x, T.tw[2], M.m[2], D + 2 * plane + c);
     cols16_store(x3, T.tw[3], M.m[3], D + 3 * plane + c);
@@ -1683,6 +1698,19 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
     const size_t fused_smem = (size_t)2 * kMs1T * kMs1Pitch * sizeof(uint32_t);
     Ms1Tw tw4;
     for (int mod = 0; mod < 4; ++mod) tw4.tw[mod] = reinterpret_cast<const uint2*>(tab[mod]->fw);
+    {
+      const uint32_t q0m = p->M4.m[0], q1m = p->M4.m[1];
+      tw4.m1 = (uint32_t)(0x100000000ull / q1m);
+      tw4.w01 = p->q0inv_q1;
+      tw4.w01p = shoup_pre(p->q0inv_q1, q1m);
+      tw4.Q = (uint64_t)q0m * q1m;
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t P = p->M4.m[2 + i];
+        tw4.c[i] = q0m % P;
+        tw4.cp[i] = shoup_pre(tw4.c[i], P);
+        tw4.qp[i] = (uint32_t)(tw4.Q % P);
+      }
+    }
     if (fused)
       HE_CUDA(cudaFuncSetAttribute(k_ms1_digits_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem),
               "smem attribute");
