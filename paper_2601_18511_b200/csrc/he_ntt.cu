@@ -299,10 +299,12 @@ __global__ void __launch_bounds__(N2 / 16, MINB) ntt_fwd_rows(const __grid_const
   const uint2* __restrict__ tw = J.tw[blockIdx.z];
   const uint32_t q = J.q[blockIdx.z];
   __shared__ uint32_t s[NP][N2 + N2 / 32];
-  const uint32_t b = blockIdx.x;
+  // block b of each poly = blockIdx.y: consecutive CTAs share b, so the CTAs resident on an SM read the same
+  // twiddle slice (L1 hits even when the table is the 512 KB of a 2^16 transform)
+  const uint32_t b = blockIdx.y;
   uint32_t* a[NP];
 #pragma unroll
-  for (int p = 0; p < NP; ++p) a[p] = data + ((size_t)blockIdx.y * NP + p) * stride + (size_t)b * N2;
+  for (int p = 0; p < NP; ++p) a[p] = data + ((size_t)blockIdx.x * NP + p) * stride + (size_t)b * N2;
   const uint32_t tau = threadIdx.x;
   const uint32_t q2 = 2 * q;
   uint32_t x[NP][16];
@@ -379,10 +381,12 @@ __global__ void __launch_bounds__(N2 / 16, MINB) ntt_inv_rows(const __grid_const
   const uint2* __restrict__ tw = J.tw[blockIdx.z];
   const uint32_t q = J.q[blockIdx.z], ninv = J.ninv[blockIdx.z], ninvp = J.ninvp[blockIdx.z];
   __shared__ uint32_t s[NP][N2 + N2 / 32];
-  const uint32_t b = blockIdx.x;
+  // block b of each poly = blockIdx.y: consecutive CTAs share b, so the CTAs resident on an SM read the same
+  // twiddle slice (L1 hits even when the table is the 512 KB of a 2^16 transform)
+  const uint32_t b = blockIdx.y;
   uint32_t* a[NP];
 #pragma unroll
-  for (int p = 0; p < NP; ++p) a[p] = data + ((size_t)blockIdx.y * NP + p) * stride + (size_t)b * N2;
+  for (int p = 0; p < NP; ++p) a[p] = data + ((size_t)blockIdx.x * NP + p) * stride + (size_t)b * N2;
   const uint32_t tau = threadIdx.x;
   const uint32_t q2 = 2 * q;
   uint32_t x[NP][16];
@@ -514,12 +518,12 @@ cudaError_t ntt_forward_multi(const NttTable* const* t, uint32_t* const* data, i
     if (count / 2) {
       // 4096-point blocks: compiled for 4 resident CTAs per SM (<= 64 registers, 32 warps); measured against
       // 3 / 5 CTAs and one poly per CTA at 6 / 7
-      dim3 g(n1, count / 2, njobs);
+      dim3 g(count / 2, n1, njobs);
       if constexpr (K == 4096) ntt_fwd_rows<K, 2, 4><<<g, K / 16, 0, st>>>(J, stride, n, 1);
       else ntt_fwd_rows<K, 2><<<g, K / 16, 0, st>>>(J, stride, n, 1);
     }
     if (count & 1) {
-      dim3 g(n1, 1, njobs);
+      dim3 g(1, n1, njobs);
       ntt_fwd_rows<K, 1><<<g, K / 16, 0, st>>>(shift_jobs(J, njobs, (uint64_t)(count - 1) * stride), stride, n, 1);
     }
     return cudaGetLastError();
@@ -539,12 +543,12 @@ cudaError_t ntt_inverse_multi(const NttTable* const* t, uint32_t* const* data, i
   cudaError_t e = with_n2(n2, [&](auto N2) {
     constexpr int K = decltype(N2)::value;
     if (count / 2) {
-      dim3 g(n1, count / 2, njobs);
+      dim3 g(count / 2, n1, njobs);
       if constexpr (K == 4096) ntt_inv_rows<K, 2, 4><<<g, K / 16, 0, st>>>(J, stride, n, n1 == 1);
       else ntt_inv_rows<K, 2><<<g, K / 16, 0, st>>>(J, stride, n, n1 == 1);
     }
     if (count & 1) {
-      dim3 g(n1, 1, njobs);
+      dim3 g(1, n1, njobs);
       ntt_inv_rows<K, 1><<<g, K / 16, 0, st>>>(shift_jobs(J, njobs, (uint64_t)(count - 1) * stride), stride, n, n1 == 1);
     }
     return cudaGetLastError();
