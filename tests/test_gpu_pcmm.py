@@ -134,7 +134,7 @@ def test_wide_params_four_digit_limbs(algo):
 
 def _llama_sample(P, n_out):
     rng = np.random.default_rng(5)
-    rows = sorted(set([0, 1, 127, 128, 255, 256, n_out - 1] + list(rng.integers(0, n_out, 5))))
+    rows = sorted(r for r in set([0, 1, 127, 128, 255, 256, n_out - 1] + list(rng.integers(0, n_out, 5))) if r < n_out)
     cols = sorted(set([0, 1, 255, 256, 257, 511, 512, 4095, P.width - 1] + list(rng.integers(0, P.width, 32))))
     return rows, cols
 
@@ -479,3 +479,17 @@ def test_llama_headroom_log_delta_24(n_out, n_in):
     assert 8 < top < 32, top                         # beyond the default preset's range, inside this one's
     err = np.nanmax(np.abs(dec - exact))
     assert err / top < 2 ** -10, (err, top)
+
+
+def test_llama_wide_input_two_k_blocks():
+    """n_in = 72 x 256 (R = 72 > 64 input cts): the spectral GEMM's K spans two 64-byte blocks (G^ rows at the full
+    128-byte padding, two TMA boxes per digit), sampled words bit-exact vs the oracle, spectral == direct."""
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, 512, 72 * 256, seed=9)
+    plan = make_mlwe_pcmm_plan(ctx, W)
+    Y = pcmm_mlwe(ctx, plan, X)
+    rows, cols = _llama_sample(P, 512)
+    ref = O.pcmm(P, O.encode_weights(P, W), u32(X.data), rows=rows, cols=cols)
+    assert np.array_equal(gather(P, Y, rows, cols), ref)
+    Yd = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W, algo="direct"), X)
+    assert np.array_equal(u32(Y.out_a), u32(Yd.out_a)) and np.array_equal(u32(Y.out_b), u32(Yd.out_b))
