@@ -298,6 +298,7 @@ def run_ours(a, rank: int, world: int, local: int):
                                           dev=dev, cublas=cublas, ref=Y)
     if rank == 0 and world == 1 and not a.no_extras:
         extras.update(side_measurements(P, dev))
+        extras["llama_shapes"] = llama_shapes_side(P, dev)
 
     cpu = None
     if rank == 0 and world == 1 and a.cpu_rows > 0:
@@ -660,6 +661,41 @@ def graph_ms(fn, reps=5):
         return round(e0.elapsed_time(e1) / reps, 3)
     except Exception:
         return None
+
+
+def llama_shapes_side(P, dev, reps=5):
+    """The spectral MLWE PCMM at every Llama-2-7B / Llama-3-8B projection shape (BASELINE configs 2-4; x 128
+    tokens, N = 2^16): device ms/op (CUDA events, inputs resident), synthetic seeded weights and activations."""
+    import torch
+
+    from paper_2601_18511_b200 import HeContext, make_mlwe_pcmm_plan, pcmm_mlwe
+
+    out = {"workload": "spectral MLWE PCMM (K7) at the Llama projection shapes x 128 tokens, N = 2^16, 1 GPU"}
+    try:
+        ctx = HeContext(P, device=dev, rng="seeded")
+        sk = ctx.keygen(3)
+        g = torch.Generator(device=dev).manual_seed(7)
+        for n_out, n_in in ((4096, 4096), (4096, 11008), (11008, 4096), (14336, 4096), (4096, 14336)):
+            W = (torch.rand((n_out, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1) / math.sqrt(n_in)
+            A = torch.rand((P.tokens, n_in), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+            X = ctx.encrypt_acts(sk, A, seed=2)
+            plan = make_mlwe_pcmm_plan(ctx, W)
+            Y = pcmm_mlwe(ctx, plan, X)
+            for _ in range(2):
+                pcmm_mlwe(ctx, plan, X, out=Y)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                pcmm_mlwe(ctx, plan, X, out=Y)
+            e1.record()
+            torch.cuda.synchronize()
+            out[f"{n_out}x{n_in}"] = {"ms_per_op": round(e0.elapsed_time(e1) / reps, 3)}
+            del W, A, X, plan, Y
+            torch.cuda.empty_cache()
+    except Exception as exc:   # a side line must not take the headline down
+        out["error"] = repr(exc)
+    return out
 
 
 def slot_pcmm_side(P, dev, reps=5):
