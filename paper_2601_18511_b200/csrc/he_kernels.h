@@ -101,7 +101,7 @@ struct SpecGemmArgs {
   uint32_t qninv;           // -q^-1 mod 2^32 (Montgomery)
   uint64_t off64;           // multiple of q above the recombination bound: makes the sum non-negative
   int32_t pw[8];            // 2^(16 i + 32) mod q (paired shifts)
-  uint32_t* out;            // C^ [n_out][L][nb]
+  uint32_t* out;            // C^ [n_out][nb / 8][L][8] (he_spectral.cu cidx)
   uint64_t hint_g = 0x1000000000000000ULL;  // L2 policy of the G^ loads (normal: read by the 3 block tiles of one (y tile, f))
   uint64_t hint_a = 0x14F0000000000000ULL;  // of the A^ loads (evict-last: re-read by every y tile)
   uint64_t hint_c = 0x12F0000000000000ULL;  // of the C^ stores (evict-first: S4 reads them back much later)

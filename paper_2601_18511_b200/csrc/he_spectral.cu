@@ -21,9 +21,12 @@
 // int8 digit planes (D = 4 for q0 < 2^30, 3 for q1 ~ 2^20), one MMA per weight digit against
 // the D stacked data planes writing at TMEM column offset 32 a, so digit pair (a, b) lands in
 // the int32 accumulator of shift s = a + b (2D-1 accumulators per word); the epilogue sums
-// acc_s * (2^(8 s) mod q) in int64 and Barrett-reduces.  CTA pairs (cta_group::2), tiles of
+// acc_s * (2^(8 s) mod q) in int64 and Montgomery-reduces.  CTA pairs (cta_group::2), tiles of
 // 256 rows x 32 columns, two TMEM accumulator buffers so the epilogue of one tile overlaps
-// the MMAs of the next; K = R padded to 64 bytes, 64-byte swizzle.
+// the MMAs of the next.  A operand (G^): 16-byte K chunks stored as no-swizzle core-matrix tiles
+// (gidx); B operand (A^): K = R padded to 64 bytes, 64-byte swizzle.  Tiles run y-tile-major in
+// runs of 4 consecutive frequencies per CTA pair; C^ lands in [row][group of 8 blocks][f][8]
+// (cidx), one contiguous run per S4 unit.
 #include <cuda.h>
 #include <cstdlib>
 #include "he_common.cuh"
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(256, 3) spec_inverse512_kernel(const uint32_t*
   uint32_t* xs1 = sm + kInv512Cols * kInv512Ld;      // [16 m][546]
   const uint32_t y = row0 + blockIdx.y, m0 = blockIdx.x * kInv512Cols;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // phase A: C^[p][y][m0 .. m0 + 15] of both limbs -> xs[m][pad(p)]; one warp access = 8 rows of 64 B
+  // phase A: C^ (cidx layout) positions p of blocks m0 .. m0 + 15 of both limbs -> xs[m][pad(p)]
   // (16-byte loads; pitch 546 = 2 mod 32 makes the 4 scattered stores per load conflict-free)
   {
     const uint32_t mq = lane & 3;
