@@ -546,6 +546,7 @@ HE_D void cp_async16(void* dst, const void* src) {
 HE_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 HE_D void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 constexpr int kInv1kBlocks = 8;
+constexpr uint32_t kLlamaQ0 = 1073479681u, kLlamaQ1 = 1179649u;   // HeParams.llama() (S4 specialisation)
 constexpr int kInv1kLd = 1148;   // pin36(1023) + 1, = 4 mod 8
 // position p at p + 4 (p / 32): rows of 32 positions at pitch 36 words, so a lane's 32 round-1 positions are
 // 16-byte aligned (8 x LDS/STS.128, conflict-free per quarter-warp) and the round-2 reads p = l + 32 e hit 32 banks
@@ -576,8 +577,10 @@ HE_D void bfl(uint32_t& x, uint32_t& y, uint2 w, uint32_t q2, uint32_t q) {  // 
   x = a + t;
   y = a + q2 - t;
 }
-template <bool LAZY1>
-HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_t lane, uint32_t (&x)[2][32]) {
+template <bool LAZY1, uint32_t KQ0 = 0, uint32_t KQ1 = 0>
+HE_D void inv1024_pair(const Inv1kLimb (&L_)[2], const SpecInvConst& cst, uint32_t lane, uint32_t (&x)[2][32]) {
+  // KQ0 / KQ1 != 0: the moduli as compile-time constants (immediate operands of the q products)
+  const Inv1kLimb L[2] = {{L_[0].col, L_[0].r2, KQ0 ? KQ0 : L_[0].q}, {L_[1].col, L_[1].r2, KQ1 ? KQ1 : L_[1].q}};
 #pragma unroll
   for (int l = 0; l < 2; ++l) ld_row32(L[l].col + 36 * lane, x[l]);
 #pragma unroll
@@ -656,7 +659,7 @@ HE_D void inv1024_pair(const Inv1kLimb (&L)[2], const SpecInvConst& cst, uint32_
   }
 }
 
-template <bool LAZY1>
+template <bool LAZY1, uint32_t KQ0 = 0, uint32_t KQ1 = 0>
 __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t* __restrict__ c0,
                                                                   const uint32_t* __restrict__ c1, uint32_t n_out,
                                                                   uint32_t row0, uint32_t nbp, uint32_t nblk,
@@ -699,10 +702,10 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
   __syncthreads();
   const uint32_t b = warp;
   if (b0 + b < nblk) {
-    const uint32_t q0 = cst.q[0], q1 = cst.q[1];
+    const uint32_t q0 = KQ0 ? KQ0 : cst.q[0], q1 = KQ1 ? KQ1 : cst.q[1];
     const Inv1kLimb L[2] = {{xs0 + b * kInv1kLd, tws, q0}, {xs1 + b * kInv1kLd, tws + 992, q1}};
     uint32_t x[2][32];
-    inv1024_pair<LAZY1>(L, cst, lane, x);
+    inv1024_pair<LAZY1, KQ0, KQ1>(L, cst, lane, x);
     if (cst.out1) {  // level-1 mode: both limbs, no rescale
 #pragma unroll
       for (int e = 0; e < 24; ++e) {
@@ -1128,7 +1131,10 @@ cudaError_t launch_spec_inverse(const RingDims& Rg, const uint32_t* c0, const ui
     c2.q1bar = (uint32_t)(0x100000000ull / cst.q[1]);
     static const bool strict = getenv("HE_S4_STRICT") != nullptr;  // A/B switch: corrected q1 butterflies
     const bool lazy = !strict && 42ull * cst.q[1] < 0x100000000ull;
+    static const bool kq_off = getenv("HE_S4_RUNTIME_Q") != nullptr;  // A/B switch: moduli as kernel parameters
     auto kern = lazy ? spec_inverse1024_kernel<true> : spec_inverse1024_kernel<false>;
+    if (lazy && !kq_off && cst.q[0] == kLlamaQ0 && cst.q[1] == kLlamaQ1)
+      kern = spec_inverse1024_kernel<true, kLlamaQ0, kLlamaQ1>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((nblk + kInv1kBlocks - 1) / kInv1kBlocks, rows);
