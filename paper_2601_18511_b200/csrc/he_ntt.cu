@@ -290,6 +290,23 @@ HE_D constexpr uint32_t poff(int e) {
   return T >= 32 ? (uint32_t)(e * T + e * T / 32) : (T == 16 ? (uint32_t)(16 * e + e / 2) : (uint32_t)e);
 }
 
+// 4096-point exchange layout (no padding): word i at i ^ 4 sx(i / 32), sx(X) = (X mod 4) | 4 (bit 3 of X) -- an
+// XOR of the 16-byte granule inside each 128-byte row.  The three access patterns of the rounds are then all
+// conflict-free: (A) tau + 256 e (32 consecutive words per warp), (B) j0 + 16 e with j0 = 256 (tau / 16) + tau % 16
+// (the two half-warps land in opposite 64-byte halves of the row; with the additive pad they shared 8 banks), and
+// (C) the 16 consecutive words of thread tau as 4 x 16-byte accesses (8 lanes per quarter-warp on 8 granules).
+HE_D uint32_t swz_a(uint32_t tau, int e) { return (tau ^ (((tau >> 5) & 3) << 2) ^ ((e & 1) << 4)) + 256 * e; }
+HE_D uint32_t swz_b(uint32_t tau, int e) {
+  return 256 * (tau >> 4) + ((tau & 15) ^ (4 * ((e >> 1) & 3))) + 32 * (e >> 1) + 16 * ((e & 1) ^ ((tau >> 4) & 1));
+}
+HE_D uint32_t swz_c(uint32_t tau, int v) {   // granule v (words 4 v .. 4 v + 3) of thread tau's 16
+  const uint32_t sx = ((tau >> 1) & 3) | (((tau >> 4) & 1) << 2);
+  return 32 * (tau >> 1) + 4 * ((4 * (tau & 1) + v) ^ sx);
+}
+constexpr int kNttSwz = 4096;                 // the rows size that uses the swizzled exchange layout
+template <int N2>
+constexpr int rows_smem_words() { return N2 == kNttSwz ? N2 : N2 + N2 / 32; }
+
 // forward: rounds of 4 stages, T = N2/16, N2/256, ..., 1; first round straight from global.  NP transforms
 // (polys blockIdx.y * NP .. + NP - 1 of the batch, block b of each) per CTA share every twiddle load.
 template <int N2, int NP, int MINB = 1>
@@ -298,7 +315,7 @@ __global__ void __launch_bounds__(N2 / 16, MINB) ntt_fwd_rows(const __grid_const
   uint32_t* __restrict__ data = J.data[blockIdx.z];
   const uint2* __restrict__ tw = J.tw[blockIdx.z];
   const uint32_t q = J.q[blockIdx.z];
-  __shared__ uint32_t s[NP][N2 + N2 / 32];
+  __shared__ __align__(16) uint32_t s[NP][rows_smem_words<N2>()];
   // block b of each poly = blockIdx.y: consecutive CTAs share b, so the CTAs resident on an SM read the same
   // twiddle slice (L1 hits even when the table is the 512 KB of a 2^16 transform)
   const uint32_t b = blockIdx.y;
@@ -313,7 +330,44 @@ __global__ void __launch_bounds__(N2 / 16, MINB) ntt_fwd_rows(const __grid_const
 #pragma unroll
     for (int e = 0; e < 16; ++e) x[p][e] = a[p][tau + e * (N2 / 16)];  // coalesced across the warp
   ct_round16<NP>(x, tw, n / N2, b, q2, q);
-  if constexpr (N2 == 16) {
+  if constexpr (N2 == kNttSwz) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) s[p][swz_a(tau, e)] = x[p][e];
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[p][e] = s[p][swz_b(tau, e)];
+    ct_round16<NP>(x, tw, n / 256, b * 16 + tau / 16, q2, q);
+    // each thread writes back exactly the words it read; rounds 2 -> 3 stay inside the half-warp's 256-word
+    // sub-block, so one __syncwarp orders the store before the round-3 loads
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) s[p][swz_b(tau, e)] = x[p][e];
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint4 w = *reinterpret_cast<const uint4*>(&s[p][swz_c(tau, v)]);
+        x[p][4 * v] = w.x, x[p][4 * v + 1] = w.y, x[p][4 * v + 2] = w.z, x[p][4 * v + 3] = w.w;
+      }
+    ct_round16<NP>(x, tw, n / 16, b * (N2 / 16) + tau, q2, q);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      if (final_reduce) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[p][e] = reduce4(x[p][e], q);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(a[p] + 16 * tau);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dst[v] = make_uint4(x[p][4 * v], x[p][4 * v + 1], x[p][4 * v + 2], x[p][4 * v + 3]);
+    }
+    return;
+  } else if constexpr (N2 == 16) {
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       if (final_reduce) {
@@ -380,7 +434,7 @@ __global__ void __launch_bounds__(N2 / 16, MINB) ntt_inv_rows(const __grid_const
   uint32_t* __restrict__ data = J.data[blockIdx.z];
   const uint2* __restrict__ tw = J.tw[blockIdx.z];
   const uint32_t q = J.q[blockIdx.z], ninv = J.ninv[blockIdx.z], ninvp = J.ninvp[blockIdx.z];
-  __shared__ uint32_t s[NP][N2 + N2 / 32];
+  __shared__ __align__(16) uint32_t s[NP][rows_smem_words<N2>()];
   // block b of each poly = blockIdx.y: consecutive CTAs share b, so the CTAs resident on an SM read the same
   // twiddle slice (L1 hits even when the table is the 512 KB of a 2^16 transform)
   const uint32_t b = blockIdx.y;
@@ -403,7 +457,30 @@ __global__ void __launch_bounds__(N2 / 16, MINB) ntt_inv_rows(const __grid_const
     }
   }
   gs_round16<NP>(x, tw, n / 2, b * (N2 / 16) + tau, q2, q);
-  if constexpr (N2 > 16) {
+  if constexpr (N2 == kNttSwz) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        *reinterpret_cast<uint4*>(&s[p][swz_c(tau, v)]) = make_uint4(x[p][4 * v], x[p][4 * v + 1], x[p][4 * v + 2], x[p][4 * v + 3]);
+    __syncwarp();   // rounds 1 -> 2 stay inside the half-warp's 256-word sub-block
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[p][e] = s[p][swz_b(tau, e)];
+    gs_round16<NP>(x, tw, n / 32, b * 16 + tau / 16, q2, q);
+    // each thread writes back exactly the words it read: no barrier before the store
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) s[p][swz_b(tau, e)] = x[p][e];
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[p][e] = s[p][swz_a(tau, e)];
+    gs_round16<NP>(x, tw, n / 512, b, q2, q);
+  } else if constexpr (N2 > 16) {
     {
 #pragma unroll
       for (int p = 0; p < NP; ++p)
