@@ -64,9 +64,10 @@ void ntt_table_free(NttTable& t);
 cudaError_t ntt_forward(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s,
                         bool rows_only = false);
 cudaError_t ntt_inverse(const NttTable& t, uint32_t* data, uint32_t count, uint64_t stride, cudaStream_t s);
-// njobs (<= 16) batches of the same degree, count and stride in one launch per pass (job i: table t[i], data[i])
+// njobs (<= 16) batches of the same degree, count and stride in one launch per pass (job i: table t[i], data[i]);
+// reduce = false leaves the outputs lazy in [0, 4 q) for a consumer that reduces them itself
 cudaError_t ntt_forward_multi(const NttTable* const* t, uint32_t* const* data, int njobs, uint32_t count,
-                              uint64_t stride, cudaStream_t s, bool rows_only = false);
+                              uint64_t stride, cudaStream_t s, bool rows_only = false, bool reduce = true);
 cudaError_t ntt_inverse_multi(const NttTable* const* t, uint32_t* const* data, int njobs, uint32_t count,
                               uint64_t stride, cudaStream_t s);
 

@@ -571,7 +571,7 @@ static NttJobs shift_jobs(NttJobs J, int njobs, uint64_t off) {
 }
 
 cudaError_t ntt_forward_multi(const NttTable* const* t, uint32_t* const* data, int njobs, uint32_t count,
-                              uint64_t stride, cudaStream_t st, bool rows_only) {
+                              uint64_t stride, cudaStream_t st, bool rows_only, bool reduce) {
   if (njobs < 1 || njobs > kNttMaxJobs) return cudaErrorInvalidValue;
   const uint32_t n = t[0]->n;
   for (int i = 1; i < njobs; ++i)
@@ -596,12 +596,13 @@ cudaError_t ntt_forward_multi(const NttTable* const* t, uint32_t* const* data, i
       // 4096-point blocks: compiled for 4 resident CTAs per SM (<= 64 registers, 32 warps); measured against
       // 3 / 5 CTAs and one poly per CTA at 6 / 7
       dim3 g(count / 2, n1, njobs);
-      if constexpr (K == 4096) ntt_fwd_rows<K, 2, 4><<<g, K / 16, 0, st>>>(J, stride, n, 1);
-      else ntt_fwd_rows<K, 2><<<g, K / 16, 0, st>>>(J, stride, n, 1);
+      if constexpr (K == 4096) ntt_fwd_rows<K, 2, 4><<<g, K / 16, 0, st>>>(J, stride, n, reduce);
+      else ntt_fwd_rows<K, 2><<<g, K / 16, 0, st>>>(J, stride, n, reduce);
     }
     if (count & 1) {
       dim3 g(1, n1, njobs);
-      ntt_fwd_rows<K, 1><<<g, K / 16, 0, st>>>(shift_jobs(J, njobs, (uint64_t)(count - 1) * stride), stride, n, 1);
+      ntt_fwd_rows<K, 1><<<g, K / 16, 0, st>>>(shift_jobs(J, njobs, (uint64_t)(count - 1) * stride), stride, n,
+                                               reduce);
     }
     return cudaGetLastError();
   });

@@ -1297,6 +1297,7 @@ __global__ void __launch_bounds__(256) k_ms1_mac(const uint32_t* __restrict__ D,
 // The same MAC with each thread owning 2 frequencies of kMacY output blocks: every key pair is loaded once per
 // (component, frequency) and used for kMacY blocks (k_ms1_mac re-reads the keys once per block from L2).
 constexpr uint32_t kMacY = 8;
+template <bool LAZY_IN>
 __global__ void __launch_bounds__(256) k_ms1_mac_y(const uint32_t* __restrict__ D, const uint32_t* __restrict__ K,
                                                    uint32_t jc, uint32_t Yc, uint32_t logN, Mods4 M,
                                                    uint32_t* __restrict__ UW) {
@@ -1315,7 +1316,11 @@ __global__ void __launch_bounds__(256) k_ms1_mac_y(const uint32_t* __restrict__ 
     const uint2 ku = __ldg(Kj + (0 * 4 + mod) * n2), kw = __ldg(Kj + (1 * 4 + mod) * n2);
 #pragma unroll
     for (uint32_t y = 0; y < kMacY; ++y) {
-      const uint2 x = __ldcs(d0 + ((size_t)jj * Yc + y) * n2);
+      uint2 x = __ldcs(d0 + ((size_t)jj * Yc + y) * n2);
+      if (LAZY_IN) {   // digit NTT outputs left in [0, 4 q) by the rows pass
+        x.x = min(x.x, x.x - 2 * q), x.y = min(x.y, x.y - 2 * q);
+        x.x = min(x.x, x.x - q), x.y = min(x.y, x.y - q);
+      }
       au[y][0] += (uint64_t)x.x * ku.x;
       au[y][1] += (uint64_t)x.y * ku.y;
       aw[y][0] += (uint64_t)x.x * kw.x;
@@ -1726,13 +1731,19 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
           k_ms1_digits<<<dim3(d / kMs1M, cnt), 256, 0, st>>>(raw_a, p->n_out, Y0, j0, Yc, cnt, d, k, N, p->M4,
                                                              p->q0inv_q1, w.D);
         }
+        // the MAC over 8 blocks reduces its inputs itself (free in a memory-bound kernel), so the rows pass
+        // skips its final reduction; HE_RP_NTT_REDUCE=1 keeps it there (A/B)
+        static const bool ntt_reduce = getenv("HE_RP_NTT_REDUCE") != nullptr;
+        const bool mac_y = Yc % kMacY == 0 && getenv("HE_RP_MAC4") == nullptr;
+        const bool lazy = mac_y && !ntt_reduce;
         {
           uint32_t* dd[4] = {w.D, w.D + (size_t)cnt * N, w.D + 2ull * cnt * N, w.D + 3ull * cnt * N};
-          HE_CUDA(ntt_forward_multi(tab, dd, 4, cnt, N, st, fused), "NTT(digits)");
+          HE_CUDA(ntt_forward_multi(tab, dd, 4, cnt, N, st, fused, !lazy), "NTT(digits)");
         }
-        if (Yc % kMacY == 0 && getenv("HE_RP_MAC4") == nullptr) {
-          k_ms1_mac_y<<<dim3((unsigned)(N / 2 / 256), Yc / kMacY, 4), 256, 0, st>>>(w.D, gal + (size_t)j0 * 8 * N,
-                                                                                 p->jc, Yc, p->logN, p->M4, w.UW);
+        if (mac_y) {
+          auto mac = lazy ? k_ms1_mac_y<true> : k_ms1_mac_y<false>;
+          mac<<<dim3((unsigned)(N / 2 / 256), Yc / kMacY, 4), 256, 0, st>>>(w.D, gal + (size_t)j0 * 8 * N, p->jc, Yc,
+                                                                         p->logN, p->M4, w.UW);
         } else {
           k_ms1_mac<<<dim3((unsigned)(((uint64_t)Yc * N / 4 + 255) / 256), 4), 256, 0, st>>>(
               w.D, gal + (size_t)j0 * 8 * N, p->jc, Yc, p->logN, p->M4, w.UW);
