@@ -51,6 +51,7 @@ cudaError_t ntt_table_init(NttTable& t, uint32_t n, uint32_t q) {
     h[2 * i + 1] = shoup_pre(f, q);
     h[2 * (size_t)n + 2 * i] = v;
     h[2 * (size_t)n + 2 * i + 1] = shoup_pre(v, q);
+    if (i < 16) t.fw16[i] = make_uint2(h[2 * i], h[2 * i + 1]);
   }
   delete[] pw;
   delete[] pwi;

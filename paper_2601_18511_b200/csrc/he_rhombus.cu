@@ -1172,22 +1172,30 @@ HE_D void ct_bf_rp(uint32_t& x, uint32_t& y, uint2 w, uint32_t q2, uint32_t q) {
   x = a + t;
   y = a + q2 - t;
 }
-HE_D void cols16_store(uint32_t (&x)[16], const uint2* __restrict__ tw, uint32_t q, uint32_t* dst) {
+// the 16-point cols transform of canonical inputs (< q): twiddles are kernel parameters (constant-bank operands,
+// no loads), and the first stage skips the x correction (x < q already)
+HE_D void cols16_store(uint32_t (&x)[16], const uint2 (&tw)[16], uint32_t q, uint32_t* dst) {
   const uint32_t q2 = 2 * q;
 #pragma unroll
-  for (int m = 1, t = 8; m < 16; m <<= 1, t >>= 1) {
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t a = x[u], y = x[u + 8];
+    const uint32_t t = y * tw[1].x - __umulhi(y, tw[1].y) * q;
+    x[u] = a + t;
+    x[u + 8] = a + q2 - t;
+  }
+#pragma unroll
+  for (int m = 2, t = 4; m < 16; m <<= 1, t >>= 1) {
 #pragma unroll
     for (int i = 0; i < m; ++i) {
-      const uint2 w = __ldg(tw + m + i);
 #pragma unroll
-      for (int u = 0; u < t; ++u) ct_bf_rp(x[2 * i * t + u], x[2 * i * t + u + t], w, q2, q);
+      for (int u = 0; u < t; ++u) ct_bf_rp(x[2 * i * t + u], x[2 * i * t + u + t], tw[m + i], q2, q);
     }
   }
 #pragma unroll
   for (int v = 0; v < 16; ++v) dst[(size_t)4096 * v] = x[v];
 }
 struct Ms1Tw {
-  const uint2* tw[4];   // forward twiddle tables (W, Shoup) of q0, q1, P1, P2 at N = 2^16
+  uint2 tw[4][16];      // forward twiddles (W, Shoup) 0 .. 15 of q0, q1, P1, P2 at N = 2^16 (NttTable::fw16)
   // 32-bit CRT constants: floor(2^32 / q1); q0^-1 mod q1 (Shoup); per special prime i: q0 mod P_i (Shoup), Q mod P_i
   uint32_t m1, w01, w01p, c[2], cp[2], qp[2];
   uint64_t Q;
@@ -1702,7 +1710,8 @@ extern "C" he_status he_ring_pack_run(const he_ring_pack_plan* p, const uint32_t
     const bool fused = getenv("HE_RP_UNFUSED") == nullptr && N == 65536 && k == 256 && d == 256;
     const size_t fused_smem = (size_t)2 * kMs1T * kMs1Pitch * sizeof(uint32_t);
     Ms1Tw tw4;
-    for (int mod = 0; mod < 4; ++mod) tw4.tw[mod] = reinterpret_cast<const uint2*>(tab[mod]->fw);
+    for (int mod = 0; mod < 4; ++mod)
+      for (int i = 0; i < 16; ++i) tw4.tw[mod][i] = tab[mod]->fw16[i];
     {
       const uint32_t q0m = p->M4.m[0], q1m = p->M4.m[1];
       tw4.m1 = (uint32_t)(0x100000000ull / q1m);
