@@ -1241,19 +1241,20 @@ __global__ void __launch_bounds__(256, 3) k_ms1_digits_cols(const uint32_t* __re
       // CRT: alpha = a0 + q0 tq, tq = (a1 - a0) q0^-1 mod q1, in [0, Q), centred (= k_ms1_digits) -- in 32-bit
       // pieces: [alpha]_Q mod P = (a0 mod P) + (q0 mod P) tq - (Q mod P if alpha > Q/2), all mod P
       const uint32_t a0 = s0[16 * v], a1 = s1[16 * v];
-      uint32_t r = a0 - __umulhi(a0, T.m1) * q1;   // a0 < 2^30: Barrett remainder in [0, 2 q1)
-      r = min(r, r - q1);
-      const uint32_t dd = a1 >= r ? a1 - r : a1 + q1 - r;
+      const uint32_t r = a0 - __umulhi(a0, T.m1) * q1;   // a0 < 2^30: Barrett remainder in [0, 2 q1)
+      const uint32_t dd = a1 + 2 * q1 - r;               // = a1 - a0 mod q1, in (0, 3 q1): Shoup takes any u32
       uint32_t tq = dd * T.w01 - __umulhi(dd, T.w01p) * q1;
-      tq = min(tq, tq - q1);
-      const bool neg = (uint64_t)a0 + (uint64_t)q0 * tq > T.Q / 2;
+      tq = min(tq, tq - q1);                              // [0, q1)
+      // alpha = a0 + q0 tq > Q / 2 (Q, q0, q1 odd)  <=>  tq > (q1 - 1) / 2, or tq == (q1 - 1) / 2 and a0 > q0 / 2
+      const uint32_t h1 = q1 >> 1;
+      const bool neg = tq > h1 || (tq == h1 && a0 > (q0 >> 1));
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const uint32_t P = M.m[2 + i];
-        uint32_t u = min(a0, a0 - P) + (tq * T.c[i] - __umulhi(tq, T.cp[i]) * P);   // [0, 3P)
+        // (a0 mod P) + (q0 mod P) tq + (P - (Q mod P) if negative): [0, P) + [0, 2P) + [0, P) < 4P < 2^32
+        uint32_t u = min(a0, a0 - P) + (tq * T.c[i] - __umulhi(tq, T.cp[i]) * P) + (neg ? P - T.qp[i] : 0u);
         u = min(u, u - 2 * P);
         u = min(u, u - P);
-        if (neg) u = u >= T.qp[i] ? u - T.qp[i] : u + P - T.qp[i];
         if (i == 0) x[v] = u;
         else x3[v] = u;
       }
