@@ -318,17 +318,29 @@ __global__ void __launch_bounds__(512) spec_data1024_kernel(const uint32_t* __re
     for (int e = 0; e < 32; ++e) col[32 * lane + e] = min(x[e], x[e] - q);   // position p, [0, q)
   }
   __syncthreads();
-  // digits: for each position p the 16 windows' words are 16 consecutive bytes of every digit plane
+  // digits: for each position p the 16 windows' words are 16 consecutive bytes of every digit plane -- one
+  // thread per p builds them in registers and stores each digit's 16 bytes at once (windows r >= n_ct: zeros)
   const uint32_t cnt = min(16u, n_ct - r0);
   const uint64_t plane = (uint64_t)nbp * r_pad;
-  for (uint32_t i = threadIdx.x; i < 1024 * 16; i += 512) {
-    const uint32_t p = i >> 4, rl = i & 15;
-    if (rl >= cnt) continue;
-    int8_t* dst = out + ((size_t)p * D * nbp + m) * r_pad + r0 + rl;
-    const uint32_t v = xs[rl * kS2Ld + p];
-    const uint32_t c = v > (q >> 1) ? v - q : v;
-    const uint32_t wv = (c + 0x80808080u) ^ 0x80808080u;
-    for (int d = 0; d < D; ++d) dst[(size_t)d * plane] = (int8_t)(wv >> (8 * d));
+  for (uint32_t p = threadIdx.x; p < 1024; p += 512) {
+    uint32_t wv[16];
+#pragma unroll
+    for (int rl = 0; rl < 16; ++rl) {
+      const uint32_t v = (uint32_t)rl < cnt ? xs[rl * kS2Ld + p] : 0u;   // lanes: consecutive p, distinct banks
+      const uint32_t c = v > (q >> 1) ? v - q : v;
+      wv[rl] = (c + 0x80808080u) ^ 0x80808080u;                          // balanced base-256 digits as bytes
+    }
+    int8_t* dst = out + ((size_t)p * D * nbp + m) * r_pad + r0;
+    for (int d = 0; d < D; ++d) {
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {   // byte d of windows 4 j .. 4 j + 3
+        const uint32_t sh = 8 * d;
+        o[j] = ((wv[4 * j] >> sh) & 0xFF) | (((wv[4 * j + 1] >> sh) & 0xFF) << 8) |
+               (((wv[4 * j + 2] >> sh) & 0xFF) << 16) | (((wv[4 * j + 3] >> sh) & 0xFF) << 24);
+      }
+      *reinterpret_cast<uint4*>(dst + (size_t)d * plane) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
   }
 }
 
