@@ -57,7 +57,8 @@ struct NttTable {
   uint32_t n = 0, q = 0;
   uint32_t *fw = nullptr, *fwp = nullptr, *iv = nullptr, *ivp = nullptr;  // device, n entries each
   uint32_t ninv = 0, ninvp = 0;
-  uint2 fw16[16] = {};   // host copy of fw pairs 0 .. 15 (the cols-pass twiddles of n = 16 n2, as kernel parameters)
+  uint2 fw16[16] = {};   // host copies of fw / iv pairs 0 .. 15 (the cols-pass twiddles of n = 16 n2, as kernel
+  uint2 iv16[16] = {};   // parameters)
 };
 cudaError_t ntt_table_init(NttTable& t, uint32_t n, uint32_t q);
 void ntt_table_free(NttTable& t);

@@ -51,7 +51,10 @@ cudaError_t ntt_table_init(NttTable& t, uint32_t n, uint32_t q) {
     h[2 * i + 1] = shoup_pre(f, q);
     h[2 * (size_t)n + 2 * i] = v;
     h[2 * (size_t)n + 2 * i + 1] = shoup_pre(v, q);
-    if (i < 16) t.fw16[i] = make_uint2(h[2 * i], h[2 * i + 1]);
+    if (i < 16) {
+      t.fw16[i] = make_uint2(h[2 * i], h[2 * i + 1]);
+      t.iv16[i] = make_uint2(h[2 * (size_t)n + 2 * i], h[2 * (size_t)n + 2 * i + 1]);
+    }
   }
   delete[] pw;
   delete[] pwi;
@@ -133,11 +136,15 @@ __global__ void __launch_bounds__(256) ntt_fwd_cols(const __grid_constant__ NttJ
   for (int v = 0; v < N1; ++v) a[(size_t)n2 * v] = x[v];
 }
 
-// single-batch form with plain parameters (the multi-job form's indexed parameter loads cost the standalone
-// 2^16 forward ~8%: 0.254 -> 0.277 ms for 1024 polys)
+// single-batch forms with plain parameters (the multi-job form's indexed parameter loads cost the standalone
+// 2^16 forward ~8%: 0.254 -> 0.277 ms for 1024 polys); the N1 - 1 twiddles are kernel parameters
+// (NttTable::fw16 / iv16: constant-bank operands, no loads)
+struct Tw16 {
+  uint2 w[16];
+};
 template <int N1>
 __global__ void __launch_bounds__(256) ntt_fwd_cols1(uint32_t* __restrict__ data, uint64_t stride, uint32_t n2,
-                                                     const uint2* __restrict__ tw, uint32_t q) {
+                                                     const Tw16 tw, uint32_t q) {
   const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= n2) return;
   uint32_t* a = data + blockIdx.y * stride + col;
@@ -149,13 +156,34 @@ __global__ void __launch_bounds__(256) ntt_fwd_cols1(uint32_t* __restrict__ data
   for (int m = 1, t = N1 / 2; m < N1; m <<= 1, t >>= 1) {
 #pragma unroll
     for (int i = 0; i < m; ++i) {
-      const uint2 w = ldtw(tw, m + i);
 #pragma unroll
-      for (int u = 0; u < t; ++u) ct_bf(x[2 * i * t + u], x[2 * i * t + u + t], w, q2, q);
+      for (int u = 0; u < t; ++u) ct_bf(x[2 * i * t + u], x[2 * i * t + u + t], tw.w[m + i], q2, q);
     }
   }
 #pragma unroll
   for (int v = 0; v < N1; ++v) a[(size_t)n2 * v] = x[v];
+}
+template <int N1>
+__global__ void __launch_bounds__(256) ntt_inv_cols1(uint32_t* __restrict__ data, uint64_t stride, uint32_t n2,
+                                                     const Tw16 tw, uint32_t q, uint32_t ninv, uint32_t ninvp) {
+  const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n2) return;
+  uint32_t* a = data + blockIdx.y * stride + col;
+  uint32_t x[N1];
+#pragma unroll
+  for (int v = 0; v < N1; ++v) x[v] = a[(size_t)n2 * v];
+  const uint32_t q2 = 2 * q;
+#pragma unroll
+  for (int t = 1; t < N1; t <<= 1) {
+    const int h = N1 / (2 * t);
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+#pragma unroll
+      for (int u = 0; u < t; ++u) gs_bf(x[2 * i * t + u], x[2 * i * t + u + t], tw.w[h + i], q2, q);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < N1; ++v) a[(size_t)n2 * v] = shoup_mul(x[v], ninv, ninvp, q);
 }
 
 template <int N1>
@@ -585,7 +613,11 @@ cudaError_t ntt_forward_multi(const NttTable* const* t, uint32_t* const* data, i
   if (n1 > 1 && !rows_only) {
     e = with_n1(n1, [&](auto N1) {
       dim3 g((n2 + 255) / 256, count, njobs);
-      if (njobs == 1) ntt_fwd_cols1<decltype(N1)::value><<<g, 256, 0, st>>>(J.data[0], stride, n2, J.tw[0], J.q[0]);
+      if (njobs == 1) {
+        Tw16 tw;
+        for (int i = 0; i < 16; ++i) tw.w[i] = t[0]->fw16[i];
+        ntt_fwd_cols1<decltype(N1)::value><<<g, 256, 0, st>>>(J.data[0], stride, n2, tw, J.q[0]);
+      }
       else ntt_fwd_cols<decltype(N1)::value><<<g, 256, 0, st>>>(J, stride, n2);
       return cudaGetLastError();
     });
@@ -635,7 +667,13 @@ cudaError_t ntt_inverse_multi(const NttTable* const* t, uint32_t* const* data, i
   if (e != cudaSuccess || n1 == 1) return e;
   return with_n1(n1, [&](auto N1) {
     dim3 g((n2 + 255) / 256, count, njobs);
-    ntt_inv_cols<decltype(N1)::value><<<g, 256, 0, st>>>(J, stride, n2);
+    if (njobs == 1) {
+      Tw16 tw;
+      for (int i = 0; i < 16; ++i) tw.w[i] = t[0]->iv16[i];
+      ntt_inv_cols1<decltype(N1)::value><<<g, 256, 0, st>>>(J.data[0], stride, n2, tw, J.q[0], J.ninv[0], J.ninvp[0]);
+    } else {
+      ntt_inv_cols<decltype(N1)::value><<<g, 256, 0, st>>>(J, stride, n2);
+    }
     return cudaGetLastError();
   });
 }
