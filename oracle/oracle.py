@@ -13,7 +13,7 @@ import numpy as np
 
 __all__ = [
     "lib", "build", "keygen", "encode_acts", "decode_acts", "encrypt", "decrypt_rlwe",
-    "encode_weights", "pcmm", "pcmm_limb", "decrypt_mlwe", "decode_mlwe_rows", "rescale",
+    "encode_weights", "pcmm", "pcmm_spectral", "pcmm_limb", "decrypt_mlwe", "decode_mlwe_rows", "rescale",
     "negacyclic_mul", "negacyclic_mul_schoolbook", "sigma_table", "clear_pcmm", "mlwe_column",
     "py_mlwe_components", "py_pcmm_rows", "num_threads", "time_pcmm_sample", "rng",
     "stream_a", "stream_e", "STREAM_SECRET", "half_reverse", "rhombus_keys", "keyswitch", "encode_vector",
@@ -39,7 +39,8 @@ def stream_e(r: int) -> int:
 
 
 def build(force: bool = False) -> Path:
-    srcs = [_HERE / "he_oracle.c", _HERE / "he_oracle_rhombus.c", _HERE / "he_oracle_pcmv.c", _HERE / "he_oracle_chain.c"]
+    srcs = [_HERE / "he_oracle.c", _HERE / "he_oracle_rhombus.c", _HERE / "he_oracle_pcmv.c", _HERE / "he_oracle_chain.c",
+            _HERE / "he_oracle_spectral.c"]
     if force or not _SO.exists() or any(_SO.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
     return _SO
@@ -195,6 +196,30 @@ def pcmm(params, Wt: np.ndarray, ct: np.ndarray, rows=None, cols=None) -> np.nda
     lib().or_pcmm(params.mlwe_degree, params.mlwe_rank, _u32(_moduli(params)), _i64(Wt), n_out, n_in,
                   _u32(ct), _i32(r) if r is not None else None, nr, _i32(c) if c is not None else None, nc,
                   _u32(out))
+    return out
+
+
+def pcmm_spectral(params, Wt: np.ndarray, ct: np.ndarray, row0: int = 0, n_rows=None, L=None) -> np.ndarray:
+    """Rescaled level-0 output rows [row0, row0 + n_rows) x all columns (the `pcmm` layout), computed by the
+    spectral restatement (he_oracle_spectral.c: overlap-save correlations, L = 4k by default) -- the same words
+    as `pcmm`, fast enough for every row of a Llama shape."""
+    Wt = np.ascontiguousarray(Wt, dtype=np.int64)
+    ct = np.ascontiguousarray(ct, dtype=np.uint32)
+    n_out, n_in = Wt.shape
+    n_rows = n_out - row0 if n_rows is None else n_rows
+    L = 4 * params.mlwe_rank if L is None else L
+    out = np.zeros((n_rows, params.width), dtype=np.uint32)
+    L_ = lib()
+    if not getattr(L_, "_sp_bound", False):
+        u32p, i64p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int64)
+        u32 = ctypes.c_uint32
+        L_.or_pcmm_spectral.restype = ctypes.c_int
+        L_.or_pcmm_spectral.argtypes = [u32, u32, u32p, i64p, u32, u32, u32p, u32, u32, u32, u32p]
+        L_._sp_bound = True
+    rc = L_.or_pcmm_spectral(params.mlwe_degree, params.mlwe_rank, _u32(_moduli(params)), _i64(Wt), n_out, n_in,
+                             _u32(ct), row0, n_rows, L, _u32(out))
+    if rc != 0:
+        raise ValueError("or_pcmm_spectral: unsupported parameters")
     return out
 
 

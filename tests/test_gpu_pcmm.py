@@ -181,6 +181,26 @@ def test_llama_last_row_block_every_word(n_out, n_in):
 
 
 @pytest.mark.parametrize("n_out,n_in", LLAMA_SHAPES)
+def test_llama_full_output_every_word_vs_cpu_spectral_oracle(n_out, n_in):
+    """EVERY word of the full output (all n_out rows x 65 792 columns, b' and a') of each Llama-2-7B / Llama-3-8B
+    projection shape equals the CPU restatement oracle/he_oracle_spectral.c on the same ciphertexts -- itself
+    pinned word for word to the direct BCHPS24 Alg. 2 oracle (tests/test_oracle.py, toy and Llama ring)."""
+    import torch
+
+    P = HeParams.llama()
+    ctx, sk, A, W, X = setup(P, n_out, n_in, seed=5)
+    Y = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W), X)
+    torch.cuda.synchronize()
+    k, d = P.mlwe_rank, P.mlwe_degree
+    ref = O.pcmm_spectral(P, O.encode_weights(P, W), u32(X.data))
+    got_a = u32(Y.out_a)
+    assert np.array_equal(got_a, ref[:, d:]), f"{int((got_a != ref[:, d:]).sum())} a' words differ"
+    got_b = u32(Y.out_b).reshape(-1, P.N)
+    ref_b = ref[:, :d].reshape(-1, k, d).transpose(0, 2, 1).reshape(-1, P.N)   # b'_(Y k + t)[m] at t + k m
+    assert np.array_equal(got_b, ref_b), f"{int((got_b != ref_b).sum())} b' words differ"
+
+
+@pytest.mark.parametrize("n_out,n_in", LLAMA_SHAPES)
 def test_spectral_equals_direct_every_word(n_out, n_in):
     """The two a'-column algorithms agree on ALL n_out x 65 792 output words (random weights);
     the direct K1 words are themselves oracle-pinned on samples and by the selection identity."""

@@ -204,3 +204,30 @@ def test_oracle_one_digit_ring_packing_decrypts():
     for out in (O.mlwe_to_rlwe1(P, rb, ra, O.mlwe_ks_keys1(P, 5, s)), O.mlwe_to_rlwe(P, rb, ra, O.mlwe_ks_keys(P, 5, s))):
         dec = O.decode_acts(P, O.decrypt_rlwe(P, out[:, None], s), n_out)
         assert np.abs(dec - A @ W.T).max() < 2 ** -16
+
+
+@pytest.mark.parametrize("L", [32, 64, 128])
+def test_spectral_restatement_equals_direct_every_word(toy, L):
+    """he_oracle_spectral.c (overlap-save correlations, any L > k) == or_pcmm (BCHPS24 Alg. 2) on every word,
+    including row slices, and both equal the seeded golden output."""
+    A, W, s, ct, Wt = toy
+    ref = O.pcmm(P, Wt, ct)
+    assert np.array_equal(O.pcmm_spectral(P, Wt, ct, L=L), ref)
+    assert np.array_equal(O.pcmm_spectral(P, Wt, ct, row0=5, n_rows=17, L=L), ref[5:22])
+    g = np.load(GOLD / "oracle_toy_int.npz")
+    gt = np.load(GOLD / "pcmm_toy_golden.npz")
+    ct2 = O.encrypt(P, 11, O.keygen(P, 7), O.encode_acts(P, gt["M"].T.copy()))
+    assert np.array_equal(O.pcmm_spectral(P, O.encode_weights(P, gt["W"]), ct2, L=L), g["out"])
+
+
+def test_spectral_restatement_equals_direct_llama_ring():
+    """At the Llama ring (N = 2^16, MLWE (256, 256), L = 1024): 6 output rows x all 65 792 columns, 2 input
+    ciphertexts, every word equal to the direct oracle."""
+    PL = HeParams.llama()
+    rng = np.random.default_rng(3)
+    n_in, n_out = 2 * PL.mlwe_rank, 6
+    A = rng.uniform(-1, 1, (PL.tokens, n_in))
+    W = rng.uniform(-1, 1, (n_out, n_in)) / np.sqrt(n_in)
+    ct = O.encrypt(PL, 11, O.keygen(PL, 7), O.encode_acts(PL, A))
+    Wt = O.encode_weights(PL, W)
+    assert np.array_equal(O.pcmm_spectral(PL, Wt, ct), O.pcmm(PL, Wt, ct))
