@@ -1003,6 +1003,15 @@ def run_reference(a, rank: int, world: int):
         res = O.time_pcmm_sample(P, Wt, ct, rows)
         vals.append(res["seconds"] * n_out / rows * 1e3)
     v = float(np.median(vals))
+    # context: the GPU path's own algorithm on the same host cores, full workload (one run, no extrapolation)
+    Wf = rng.uniform(-1, 1, (n_out, n_in)) / math.sqrt(n_in)
+    Wtf = O.encode_weights(P, Wf)
+    del Wf
+    O.pcmm_spectral(P, Wtf[:8], ct)
+    t0 = time.perf_counter()
+    O.pcmm_spectral(P, Wtf, ct)
+    sp_ms = (time.perf_counter() - t0) * 1e3
+    del Wtf
     line = {
         "metric": METRIC, "value": round(v, 1), "unit": "ms/op", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(v, 1), "higher_is_better": False, "scaling": "strong",
@@ -1017,8 +1026,11 @@ def run_reference(a, rank: int, world: int):
                          "algorithm": "direct (BCHPS24 Alg. 2 as a GEMM)"},
         "extrapolated": True,
         "e2e": {"value": round(v, 1), "unit": "ms/op", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "same_algorithm_cpu": {"value": round(sp_ms, 1), "unit": "ms/op", "cores": O.num_threads(),
+                               "algorithm": "spectral (oracle/he_oracle_spectral.c), the full op, not extrapolated"},
         "note": "hesim (the reference package) does not implement the MLWE PCMM (SPEC.md:8); the reference "
-                "arm times the CPU restatement of the path",
+                "arm times the CPU restatement of the path (BCHPS24 Alg. 2); same_algorithm_cpu is the GPU "
+                "path's algorithm on the same cores",
     }
     print(json.dumps(line), flush=True)
 
