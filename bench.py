@@ -285,6 +285,11 @@ def run_ours(a, rank: int, world: int, local: int):
             "ms": round(g_ms, 3), "int8_ops": gops, "TOPS": round(gops / (g_ms * 1e-3) / 1e12, 1),
             "frac_int8_peak": round(gops / (g_ms * 1e-3) / 1e12 / INT8_PEAK_TOPS, 4),
             "traffic": load_traffic(a.shape, "spectral_gemm")}
+        tr = roof["spectral_gemm"]["traffic"]
+        if isinstance(tr, dict) and g_ms > 0:   # S3 is bound by its DRAM traffic (G^ reads + C^ writes), not the MMAs
+            s3_gbs = (tr["q0"] + tr["q1"]) / (g_ms * 1e-3) / 1e9
+            roof["spectral_gemm"]["dram_GBs"] = round(s3_gbs, 1)
+            roof["spectral_gemm"]["frac_hbm"] = round(s3_gbs / hbm, 4)
 
     extras = {}
     if world > 1 and not a.no_extras:
@@ -388,6 +393,7 @@ def k1_roofline(P, rows, n_in, d_w, gemm_ms, shape, cublas):
             "int8_ops_per_launch": ops,
             "peak_note": "NVIDIA dense INT8 spec (4.5 POPS); MEASURED_PEAKS.json has no int8 entry",
             "cublas_int8_tops_measured": cublas,
+            "frac_of_cublas_int8_measured": round(achieved / cublas, 4) if cublas else None,
             "frac_of_2x_measured_bf16": round(achieved / (2 * measured_bf16()), 4) if measured_bf16() else None}
 
 
