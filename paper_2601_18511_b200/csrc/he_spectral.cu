@@ -559,6 +559,12 @@ HE_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"
 HE_D void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 constexpr int kInv1kBlocks = 8;
 constexpr uint32_t kLlamaQ0 = 1073479681u, kLlamaQ1 = 1179649u;   // HeParams.llama() (S4 specialisation)
+constexpr uint64_t cx_powmod(uint64_t a, uint64_t e, uint64_t q) {
+  uint64_t r = 1;
+  for (a %= q; e; e >>= 1, a = a * a % q)
+    if (e & 1) r = r * a % q;
+  return r;
+}
 constexpr int kInv1kLd = 1148;   // pin36(1023) + 1, = 4 mod 8
 // position p at p + 4 (p / 32): rows of 32 positions at pitch 36 words, so a lane's 32 round-1 positions are
 // 16-byte aligned (8 x LDS/STS.128, conflict-free per quarter-warp) and the round-2 reads p = l + 32 e hit 32 banks
@@ -661,13 +667,20 @@ HE_D void inv1024_pair(const Inv1kLimb (&L_)[2], const SpecInvConst& cst, uint32
       }
     }
   }
+  // limb 1 leaves as r = (x1 + h) mod q1, h = (q1 - 1) / 2: r - h is the centred representative the rescale needs
+  const uint32_t q1 = L[1].q, h = q1 >> 1;
+  const uint32_t q1bar = KQ1 ? (uint32_t)(0x100000000ull / KQ1) : cst.q1bar;
 #pragma unroll
   for (int e = 0; e < 24; ++e) {
     x[0][e] = min(x[0][e], x[0][e] - 2 * L[0].q);   // [0, 2 q0)
-    uint32_t v = x[1][e];
-    if (LAZY1) v -= __umulhi(v, cst.q1bar) * L[1].q;   // v < 42 q1 < 2^32: quotient off by at most one
-    else v = min(v, v - 2 * L[1].q);
-    x[1][e] = min(v, v - L[1].q);                       // [0, q1)
+    uint32_t v = x[1][e] + h;
+    if (LAZY1) {
+      v -= __umulhi(v, q1bar) * q1;                   // v < 43 q1 < 2^32: quotient off by at most one -> [0, 2 q1)
+    } else {
+      v = min(v, v - 2 * q1);
+      v = min(v, v - 2 * q1);                         // x1 < 4 q1: [0, 2 q1)
+    }
+    x[1][e] = min(v, v - q1);                         // [0, q1)
   }
 }
 
@@ -718,20 +731,24 @@ __global__ void __launch_bounds__(256, 2) spec_inverse1024_kernel(const uint32_t
     const Inv1kLimb L[2] = {{xs0 + b * kInv1kLd, tws, q0}, {xs1 + b * kInv1kLd, tws + 992, q1}};
     uint32_t x[2][32];
     inv1024_pair<LAZY1, KQ0, KQ1>(L, cst, lane, x);
+    const uint32_t h = q1 >> 1;
     if (cst.out1) {  // level-1 mode: both limbs, no rescale
 #pragma unroll
       for (int e = 0; e < 24; ++e) {
         xs0[b * kInv1kLd + lane + 32 * e + (e >> 3)] = min(x[0][e], x[0][e] - q0);
-        xs1[b * kInv1kLd + lane + 32 * e + (e >> 3)] = x[1][e];
+        const uint32_t r = x[1][e];   // (x1 + h) mod q1
+        xs1[b * kInv1kLd + lane + 32 * e + (e >> 3)] = min(r - h, r + q1 - h);
       }
     } else
 #pragma unroll
     for (int e = 0; e < 24; ++e) {
-      // (x0 - [x1]_centred) q1^-1 mod q0, branch-free: t = x0 + q0 - x1 (+ q1 when x1 > q1 / 2) < 3 q0 + q1,
+      // (x0 - [x1]_centred) q1^-1 mod q0 with [x1]_centred = r - h: t = x0 + (q0 + h) - r in (0, 3 q0 + h),
       // one Shoup product (any 32-bit input) -> [0, 2 q0), one correction
-      const uint32_t x0 = x[0][e], x1 = x[1][e];
-      const uint32_t t = x0 + q0 - x1 + (x1 > (q1 >> 1) ? q1 : 0u);
-      const uint32_t v = t * cst.q1inv - __umulhi(t, cst.q1invp) * q0;
+      constexpr uint32_t kInv = KQ0 ? (uint32_t)cx_powmod(KQ1, KQ0 - 2, KQ0) : 0u;
+      const uint32_t qi = KQ0 ? kInv : cst.q1inv;
+      const uint32_t qip = KQ0 ? (uint32_t)(((uint64_t)kInv << 32) / KQ0) : cst.q1invp;
+      const uint32_t t = x[0][e] + (q0 + h) - x[1][e];
+      const uint32_t v = t * qi - __umulhi(t, qip) * q0;
       // u = lane + 32 e stored at u + u / 256 (the three thirds of a block one bank apart for phase C)
       xs1[b * kInv1kLd + lane + 32 * e + (e >> 3)] = min(v, v - q0);
     }
