@@ -75,8 +75,12 @@ cudaError_t spec_table_init(SpecTable& t, uint32_t L, uint32_t q) {
     for (int i = 0; i < len; ++i)
       for (int lo = 0; lo < lanes; ++lo) {
         const uint32_t j = (uint32_t)(lo + lanes * i) << (lg - st);
-        h[2 * (size_t)L + 2 * (base + lanes * i + lo)] = h[L + 2 * j];
-        h[2 * (size_t)L + 2 * (base + lanes * i + lo) + 1] = h[L + 2 * j + 1];
+        // L = 1024 inverse tables: entries i, i + 1 (i even) of a lane adjacent, so S4 reads them as one 16-byte
+        // load: [base + 2 lanes (i / 2) + 2 lo + i % 2]; the single-entry first stage and L = 512 stay [i][lane]
+        const size_t ri = (L == 1024 && len >= 2) ? base + 2 * lanes * (i >> 1) + 2 * lo + (i & 1)
+                                                  : base + lanes * i + lo;
+        h[2 * (size_t)L + 2 * ri] = h[L + 2 * j];
+        h[2 * (size_t)L + 2 * ri + 1] = h[L + 2 * j + 1];
         h[2 * (size_t)L + 2 * nr2 + 2 * (base + lanes * i + lo)] = h[2 * j];        // forward (f2)
         h[2 * (size_t)L + 2 * nr2 + 2 * (base + lanes * i + lo) + 1] = h[2 * j + 1];
       }
@@ -616,6 +620,12 @@ HE_D void inv1024_pair(const Inv1kLimb (&L_)[2], const SpecInvConst& cst, uint32
             const uint32_t u = x[l][e], v = x[l][e + len];
             x[l][e] = u + v;
             x[l][e + len] = u + (L[l].q << s) - v;
+          } else if (s == 0 || (s == 1 && (e & 1) == 0)) {
+            // no corrections needed: S3 stores C^ reduced to [0, q), and the even positions after the first stage
+            // hold x + y < 2 q (only the odd ones, x - y + 2 q, reach 3 q)
+            const uint32_t u = x[l][e], v = x[l][e + len];
+            x[l][e] = u + v;
+            x[l][e + len] = u + 2 * L[l].q - v;
           } else {
             dit_bf1(x[l][e], x[l][e + len], 2 * L[l].q);
           }
@@ -639,12 +649,27 @@ HE_D void inv1024_pair(const Inv1kLimb (&L_)[2], const SpecInvConst& cst, uint32
   for (int s = 5; s < 9; ++s) {
     const int len = 1 << (s - 5);
     const int base = 32 * (len - 1);
+    // this stage's len twiddles of the lane, entries (2 i, 2 i + 1) as one 16-byte load (spec_table_init layout)
+    uint2 tw[2][8];
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      if (len == 1) {
+        tw[l][0] = L[l].r2[lane];
+      } else {
+#pragma unroll
+        for (int i = 0; i < len / 2; ++i) {
+          const uint4 v = *reinterpret_cast<const uint4*>(L[l].r2 + base + 64 * i + 2 * lane);
+          tw[l][2 * i] = make_uint2(v.x, v.y);
+          tw[l][2 * i + 1] = make_uint2(v.z, v.w);
+        }
+      }
+    }
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       if (e & len) continue;
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
-        const uint2 w = L[l].r2[base + 32 * (e & (len - 1)) + lane];
+        const uint2 w = tw[l][e & (len - 1)];
         if (LAZY1 && l == 1) bfl(x[l][e], x[l][e + len], w, 2 * L[l].q, L[l].q);
         else dit_bf(x[l][e], x[l][e + len], w, 2 * L[l].q, L[l].q);
       }
@@ -657,7 +682,8 @@ HE_D void inv1024_pair(const Inv1kLimb (&L_)[2], const SpecInvConst& cst, uint32
     for (int l = 0; l < 2; ++l) {
       const bool lazy = LAZY1 && l == 1;
       const uint32_t q = L[l].q, q2 = 2 * q;
-      const uint2 w = L[l].r2[480 + 32 * e + lane];
+      const uint4 wv = *reinterpret_cast<const uint4*>(L[l].r2 + 480 + 64 * (e >> 1) + 2 * lane);
+      const uint2 w = (e & 1) ? make_uint2(wv.z, wv.w) : make_uint2(wv.x, wv.y);
       if (e < 8) {
         if (lazy) bfl(x[l][e], x[l][e + 16], w, q2, q);
         else dit_bf(x[l][e], x[l][e + 16], w, q2, q);
