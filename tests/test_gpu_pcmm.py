@@ -374,6 +374,33 @@ def test_spectral_transform_length_512_subprocess():
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("env", [{"HE_S4_RUNTIME_Q": "1"}, {"HE_S4_STRICT": "1"}])
+def test_s4_variants_subprocess(env):
+    """The S4 instantiations the Llama parameters do not select by default -- moduli as kernel parameters
+    (HE_S4_RUNTIME_Q) and corrected q1 butterflies (HE_S4_STRICT) -- produce the default path's words, in both
+    the rescaled and the level-1 output modes (read once per process: child process)."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, torch, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import test_gpu_pcmm as G; from paper_2601_18511_b200 import HeParams, make_mlwe_pcmm_plan, pcmm_mlwe;"
+        "P = HeParams.llama(); ctx, sk, A, W, X = G.setup(P, 512, 2048, seed=6);"
+        "Y1 = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W), X);"
+        "Y2 = pcmm_mlwe(ctx, make_mlwe_pcmm_plan(ctx, W, algo='direct'), X);"
+        "assert torch.equal(Y1.out_a, Y2.out_a) and torch.equal(Y1.out_b, Y2.out_b);"
+        "from paper_2601_18511_b200 import pcmm_level1;"
+        "rb, ra = pcmm_level1(ctx, make_mlwe_pcmm_plan(ctx, W), X);"
+        "rb2, ra2 = pcmm_level1(ctx, make_mlwe_pcmm_plan(ctx, W, algo='direct'), X);"
+        "assert torch.equal(ra, ra2) and torch.equal(rb, rb2); print('ok')"
+    )
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 def test_fused_peer_output_writes_every_destination(algo):
     """he_pcmm_gemm_rows_peers (the fused output all-gather): the shard's words land, identical to
