@@ -1326,9 +1326,9 @@ __global__ void __launch_bounds__(256) k_ms1_mac_y(const uint32_t* __restrict__ 
 #pragma unroll
     for (uint32_t y = 0; y < kMacY; ++y) {
       uint2 x = __ldcs(d0 + ((size_t)jj * Yc + y) * n2);
-      if (LAZY_IN) {   // digit NTT outputs left in [0, 4 q) by the rows pass
+      if (LAZY_IN) {   // digit NTT outputs left in [0, 4 q) by the rows pass -> [0, 2 q): with the keys < q and
+        // the reduction every 8 steps, 8 (2 q) q + q < 2^64 for q < 2^30
         x.x = min(x.x, x.x - 2 * q), x.y = min(x.y, x.y - 2 * q);
-        x.x = min(x.x, x.x - q), x.y = min(x.y, x.y - q);
       }
       au[y][0] += (uint64_t)x.x * ku.x;
       au[y][1] += (uint64_t)x.y * ku.y;
